@@ -1,0 +1,292 @@
+/*
+ * mtk_cuda.h -- the C-ABI kernel seam of the B200 backend (libmtkcuda.so).
+ *
+ * The reference (mtk, /root/reference/proj) funnels every piece of training
+ * arithmetic through "kernels writing into preallocated outputs"
+ * (include/mtk/tensor.h:116-145) plus the fused-op bodies inside
+ * src/graph.cpp, the Adam/EMA loops in src/train.cpp and the worker-ordered
+ * gradient combine (train.cpp:254-269).  This header is that seam re-cut for
+ * sm_100a: one extern "C" entry per reference kernel, plain device pointers,
+ * sizes, strides and flags, a stream handle (a cudaStream_t passed as void*),
+ * no C++ or torch types.  Each entry cites the reference interface it
+ * replaces.
+ *
+ * Conventions
+ *   - All tensors are dense fp32 unless stated; ids are int32.
+ *   - "accumulate" flags: 1 = out += result (the reference's backward
+ *     convention, tensor.cpp:589-596), 0 = out = result.
+ *   - Functions never allocate device memory; workspaces come from the
+ *     caller (the graph arena, tensor.cpp:30-59 semantics).
+ *   - Return value: MTKC_OK or an error code; mtkc_last_error() gives the
+ *     thread-local message.  Codes mirror the reference's error taxonomy
+ *     (common.h:18-35) so the C++ host rethrows the same exception types.
+ *   - Data-dependent errors that the reference raises mid-kernel (division
+ *     by zero, tensor.cpp:161-165; fully-masked softmax row, :424-425;
+ *     out-of-vocabulary ids, graph.cpp:602-606; non-finite gradients,
+ *     train.cpp:51-53) set bits in a caller-provided device flag word
+ *     instead of stopping the stream; the host checks the word at its next
+ *     synchronisation point.
+ */
+#ifndef MTK_CUDA_H
+#define MTK_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (common.h:18-35) ------------------------------------- */
+enum {
+  MTKC_OK = 0,
+  MTKC_DIMENSION = 1, /* DimensionError */
+  MTKC_NUMERIC = 2,   /* NumericError   */
+  MTKC_CONTRACT = 3,  /* ContractError  */
+  MTKC_DATA = 4,      /* DataError      */
+  MTKC_CUDA = 7       /* CUDA runtime / launch failure */
+};
+
+/* ---- device flag bits (checked by the host at sync points) ------------- */
+enum {
+  MTKC_FLAG_DIV_ZERO = 1,     /* ewiseBinaryInto Div, tensor.cpp:161-165 */
+  MTKC_FLAG_MASKED_ROW = 2,   /* softmaxInto fully-masked row, :424-425  */
+  MTKC_FLAG_BAD_ID = 4,       /* embed/gather id range, graph.cpp:602-606 */
+  MTKC_FLAG_NONFINITE = 8     /* allFinite, tensor.cpp:95-100            */
+};
+
+/* ---- elementwise op ids (tensor.h:100, EwiseOp) ------------------------ */
+enum {
+  MTKC_ADD = 0, MTKC_SUB = 1, MTKC_MUL = 2, MTKC_DIV = 3,
+  MTKC_TANH = 4, MTKC_SIGMOID = 5, MTKC_RELU = 6, MTKC_EXP = 7,
+  MTKC_LOG = 8, MTKC_NEG = 9
+};
+/* ---- reduce op ids (tensor.h:101, ReduceOp) ---------------------------- */
+enum { MTKC_RSUM = 0, MTKC_RMAX = 1, MTKC_RMEAN = 2, MTKC_RARGMAX = 3 };
+
+/* ======================================================================== */
+/* runtime: device, memory, streams (replaces the host Arena backing store, */
+/* tensor.cpp:30-59, and the implicit "everything is host memory" model)    */
+/* ======================================================================== */
+const char* mtkc_last_error(void);
+int mtkc_init(int device);
+int mtkc_device_count(int* count);
+int mtkc_sm_count(int* count);
+int mtkc_malloc(void** ptr, size_t bytes);
+int mtkc_free(void* ptr);
+int mtkc_host_alloc_pinned(void** ptr, size_t bytes);
+int mtkc_host_free_pinned(void* ptr);
+int mtkc_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int mtkc_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int mtkc_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+int mtkc_memset(void* dst, int value, size_t bytes, void* stream);
+int mtkc_stream_create(void** stream);
+int mtkc_stream_destroy(void* stream);
+int mtkc_stream_sync(void* stream);
+int mtkc_event_create(void** ev);
+int mtkc_event_destroy(void* ev);
+int mtkc_event_record(void* ev, void* stream);
+int mtkc_stream_wait_event(void* stream, void* ev);
+int mtkc_event_elapsed_ms(void* start, void* stop, float* ms);
+int mtkc_device_sync(void);
+/* Kernel-launch counter (every mtkc_* kernel launch increments it). */
+uint64_t mtkc_launch_count(void);
+
+/* ======================================================================== */
+/* GEMM: matmulInto (tensor.cpp:258-306), matmulAccumInto (graph.cpp:273-   */
+/* 291), affine (graph.cpp:334-336) and the GRU pre-activations (gruPre,    */
+/* graph.cpp:633-645), with epilogues the reference runs as separate nodes. */
+/* ======================================================================== */
+enum { MTKC_GEMM_FP32 = 0, /* CUDA-core FP32, reference summation order   */
+       MTKC_GEMM_TF32 = 1  /* tcgen05.mma kind::tf32, fp32 accumulate (TMEM) */ };
+enum { MTKC_EPI_NONE = 0, MTKC_EPI_RELU = 1 };
+
+typedef struct mtkc_gemm_args {
+  int64_t M, N, K;      /* op(A) is M x K, op(B) is K x N, C is M x N        */
+  int64_t batch;        /* >= 1; batch count of the product                  */
+  const float* A;       /* row-major storage of A (or A^T when transA)       */
+  int64_t lda;          /* row stride of the stored A                        */
+  int64_t strideA;      /* batch stride of A, 0 = broadcast (tensor.cpp:246-256) */
+  int transA;
+  const float* B;
+  int64_t ldb;
+  int64_t strideB;
+  int transB;
+  float* C;
+  int64_t ldc;
+  int64_t strideC;      /* 0 with batch > 1 = sum the batch into one C (graph.cpp:281-290) */
+  float alpha;          /* C = alpha*op(A)op(B) + beta*C                     */
+  float beta;
+  const float* bias;    /* optional [N] row-broadcast add (affine)           */
+  int epilogue;         /* MTKC_EPI_NONE | MTKC_EPI_RELU                     */
+  const float* gate;    /* optional [M x N], ldc-strided: out *= (gate > 0)  */
+  int precision;        /* MTKC_GEMM_FP32 | MTKC_GEMM_TF32                   */
+  float* workspace;     /* split-K scratch (may be NULL)                     */
+  size_t workspace_bytes;
+} mtkc_gemm_args;
+
+int mtkc_gemm(const mtkc_gemm_args* args, void* stream);
+/* which path the last mtkc_gemm on this thread used: 0 simt, 1 tcgen05 */
+int mtkc_gemm_last_path(void);
+
+/* ======================================================================== */
+/* elementwise / broadcast (tensor.cpp:111-237, graph.cpp:139-268)          */
+/* Shapes are passed right-aligned in 4 dims (tensor.cpp:102-108).          */
+/* ======================================================================== */
+/* out[od] = op(a, b), a/b broadcast to od (ewiseBinaryInto tensor.cpp:160-183) */
+int mtkc_ewise_binary(int op, float* out, const int64_t od[4], const float* a,
+                      const int64_t ad[4], const float* b, const int64_t bd[4], int* flags,
+                      void* stream);
+/* out = op(a) (ewiseUnaryInto tensor.cpp:185-190) */
+int mtkc_ewise_unary(int op, float* out, const float* a, int64_t n, void* stream);
+/* gx += dOp(go, y, x) (graph.cpp:193-221) */
+int mtkc_unary_backward(int op, float* gx, const float* go, const float* y, const float* x,
+                        int64_t n, void* stream);
+/* binary backward for one operand: g_a += reduce_to(ad, f(go, other, y)) --
+ * Add/Sub/Mul/Div rules of graph.cpp:149-180.  which = 0 for a, 1 for b. */
+int mtkc_binary_backward(int op, int which, float* gtarget, const int64_t td[4],
+                         const float* go, const int64_t od[4], const float* a,
+                         const int64_t ad[4], const float* b, const int64_t bd[4],
+                         const float* y, void* stream);
+/* out = s*a + c (scale graph.cpp:236-252, addScalar :254-268) */
+int mtkc_scale_shift(float* out, const float* a, float s, float c, int64_t n, void* stream);
+/* out += alpha * a (axpy tensor.cpp:225-237) */
+int mtkc_axpy(float* out, const float* a, float alpha, int64_t n, void* stream);
+/* out[od] += sum of src[sd] down to od (accumulateReduced tensor.cpp:204-223) */
+int mtkc_accumulate_reduced(float* out, const int64_t od[4], const float* src,
+                            const int64_t sd[4], void* stream);
+int mtkc_fill(float* out, float v, int64_t n, void* stream);
+/* out = a*m + b*(1-m), m broadcast over cols: RNN padding blend
+ * (models.cpp:170-172, 360-364) fused */
+int mtkc_mask_blend(float* out, const float* a, const float* b, const float* m, int64_t rows,
+                    int64_t cols, void* stream);
+int mtkc_mask_blend_backward(float* ga, float* gb, const float* go, const float* m,
+                             int64_t rows, int64_t cols, int accumulate_a, int accumulate_b,
+                             void* stream);
+
+/* ======================================================================== */
+/* reductions (reduceInto tensor.cpp:322-368, graph.cpp:463-524)            */
+/* ======================================================================== */
+int mtkc_reduce(int op, float* out, const float* in, int64_t outer, int64_t n, int64_t inner,
+                void* stream);
+int mtkc_reduce_backward(int op, float* gin, const float* gout, const float* in,
+                         int64_t outer, int64_t n, int64_t inner, void* stream);
+/* out[c] (+)= sum_r in[r*cols + c]; deterministic two-level (bias grads) */
+int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int accumulate,
+                float* workspace, size_t workspace_bytes, void* stream);
+/* flags |= MTKC_FLAG_NONFINITE if any in[i] is not finite (allFinite) */
+int mtkc_check_finite(const float* in, int64_t n, int* flags, void* stream);
+
+/* ======================================================================== */
+/* softmax (softmaxInto tensor.cpp:393-440; graph softmax :526-555)          */
+/* ======================================================================== */
+/* x viewed as rows x cols (last axis).  mask (optional) broadcast against x
+ * with right-aligned dims md[4]; xd[4] are x's dims. */
+int mtkc_softmax(float* out, const float* x, const int64_t xd[4], const float* mask,
+                 const int64_t md[4], int log_mode, int* flags, void* stream);
+int mtkc_softmax_backward(float* gx, const float* y, const float* go, int64_t rows,
+                          int64_t cols, void* stream);
+
+/* ======================================================================== */
+/* layout (transposeInto/concatInto/sliceInto tensor.cpp:480-541,           */
+/* gatherRowsInto/scatterAddRows :456-476)                                  */
+/* ======================================================================== */
+int mtkc_transpose(float* out, const float* src, const int64_t sd[4], const int perm[4],
+                   int accumulate, void* stream);
+/* strided block copy: for o < outer: dst[o*dst_stride + dst_off .. +len] (+)=
+ * src[o*src_stride + src_off .. +len]  (concat/slice and their backwards) */
+int mtkc_copy_blocks(float* dst, int64_t dst_stride, int64_t dst_off, const float* src,
+                     int64_t src_stride, int64_t src_off, int64_t outer, int64_t len,
+                     int accumulate, void* stream);
+int mtkc_gather_rows(float* out, const float* src, const int32_t* rows, int64_t n,
+                     int64_t cols, int64_t src_rows, int* flags, void* stream);
+/* Deterministic scatter-add: out[ids[perm[k]]] += src[perm[k]] in segment
+ * order.  perm sorts positions by id (stable), seg_start[u]..seg_start[u+1]
+ * delimit the positions of unique id uniq[u]; each segment is summed in
+ * original position order, matching the reference's sequential loop
+ * (tensor.cpp:468-476) up to the rounding of one fp32 sum per row. */
+int mtkc_scatter_add_rows(float* out, const float* src, const int32_t* perm,
+                          const int32_t* seg_start, const int32_t* uniq, int64_t n_uniq,
+                          int64_t cols, float scale, void* stream);
+
+/* ======================================================================== */
+/* layer norm (layerNormInto / layerNormBackward tensor.cpp:545-599)        */
+/* ======================================================================== */
+int mtkc_layernorm(float* out, const float* x, const float* gain, const float* bias,
+                   float eps, float* inv_std, float* xhat, int64_t rows, int64_t d,
+                   void* stream);
+/* dx (+)= ..., dgain += ..., dbias += ... ; accumulate_dx selects dx mode.
+ * dgain/dbias use a deterministic row-block partial sum (workspace). */
+int mtkc_layernorm_backward(const float* dy, const float* gain, const float* inv_std,
+                            const float* xhat, float* dx, float* dgain, float* dbias,
+                            int64_t rows, int64_t d, int accumulate_dx, int accumulate_params,
+                            float* workspace, size_t workspace_bytes, void* stream);
+
+/* ======================================================================== */
+/* embedding (embed graph.cpp:595-622) fused with positional encoding       */
+/* (addPositionalEncoding layers.cpp:175-179): out = E[id]*s + pe[pos]       */
+/* pe may be NULL (plain gather); t = positions per sequence for pe lookup. */
+/* ======================================================================== */
+int mtkc_embed(float* out, const float* table, const int32_t* ids, int64_t n, int64_t e,
+               int64_t vocab, float s, const float* pe, int64_t t, int* flags, void* stream);
+
+/* ======================================================================== */
+/* scaled dot-product multi-head attention core (MultiHeadAttention::apply,  */
+/* layers.cpp:89-126: splitHeads, dot(q,k^T), scale, masked softmax, dot(w,v),*/
+/* merge) fused.  q [b,tq,ldq], k/v [b,tk,ldk]; head h occupies columns      */
+/* [h*dk, (h+1)*dk).  key_mask [b,tk] (NULL = all keys real); causal masks   */
+/* j > tk - tq + i (layers.cpp:115-116).  probs [b,heads,tq,tk] is saved for */
+/* the backward pass. out [b,tq,ldo].                                        */
+/* ======================================================================== */
+int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_t ldq,
+                   const float* k, const float* v, int64_t ldk, const float* key_mask,
+                   int64_t b, int64_t tq, int64_t tk, int heads, int64_t dk, float scale,
+                   int causal, int* flags, void* stream);
+/* gq/gk/gv (+)= ...; dsbuf is a [b,heads,tq,tk] workspace */
+int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
+                            const float* q, int64_t ldq, const float* k, const float* v,
+                            int64_t ldk, float* gq, float* gk, float* gv, float* dsbuf,
+                            int64_t b, int64_t tq, int64_t tk, int heads, int64_t dk,
+                            float scale, int accumulate_q, int accumulate_k, int accumulate_v,
+                            void* stream);
+
+/* ======================================================================== */
+/* cross-entropy over the vocabulary (crossEntropy graph.cpp:859-924)       */
+/* fwd: per row lse = max + log(sum exp(x - max)); row_loss = m*(lse - x_y); */
+/* loss = sum(row_loss)/count (deterministic single-block sum).              */
+/* bwd: g (+)= (softmax(x) - onehot(y)) * m * go / count, go read on device. */
+/* ======================================================================== */
+int mtkc_xent_forward(const float* logits, const int32_t* targets, const float* mask,
+                      int64_t rows, int64_t vocab, float* lse, float* row_loss, float* loss,
+                      float count, void* stream);
+int mtkc_xent_backward(float* glogits, const float* logits, const float* lse,
+                       const int32_t* targets, const float* mask, const float* gloss,
+                       int64_t rows, int64_t vocab, float count, int accumulate,
+                       void* stream);
+
+/* ======================================================================== */
+/* optimizer (Adam::updateTensor train.cpp:30-47, Adam::update :49-59,      */
+/* AveragedParameters::update :69-79) fused: one pass over the flat         */
+/* parameter/gradient/moment/average buffers.  Skipped entirely (device-side)*/
+/* when *flags has MTKC_FLAG_NONFINITE (all-or-nothing, train.cpp:51-53).    */
+/* corr1/corr2 are the host's (Real)(1 - pow((double)beta, step)).           */
+/* zero_grad: grad = 0 afterwards (train.cpp:57).                            */
+/* ======================================================================== */
+int mtkc_adam_ema(float* theta, float* grad, float* m, float* v, float* avg, int64_t n,
+                  float lr, float beta1, float beta2, float eps, float corr1, float corr2,
+                  float avg_beta, int do_avg, int zero_grad, const int* flags, void* stream);
+
+/* ======================================================================== */
+/* data-parallel gradient exchange (trainSync train.cpp:254-269): NCCL       */
+/* all-reduce(sum) of grads pre-scaled by tokens_r/total.                    */
+/* ======================================================================== */
+int mtkc_nccl_unique_id(void* id_out_128);
+int mtkc_nccl_comm_init(void** comm, int nranks, int rank, const void* id_128);
+int mtkc_nccl_comm_destroy(void* comm);
+int mtkc_allreduce_sum(void* comm, float* buf, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MTK_CUDA_H */

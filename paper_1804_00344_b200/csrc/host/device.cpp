@@ -1,0 +1,84 @@
+// Device context and error mapping for the host framework.
+#include "mtk/device.h"
+
+#include <cstdlib>
+#include <mutex>
+
+namespace mtk {
+
+namespace {
+int g_selected = -1;
+}
+
+void mtkcCheck(int rc, const char* what) {
+  if(rc == MTKC_OK)
+    return;
+  std::string msg = std::string(mtkc_last_error()) + " [" + what + "]";
+  switch(rc) {
+    case MTKC_DIMENSION: throw DimensionError(msg);
+    case MTKC_NUMERIC: throw NumericError(msg);
+    case MTKC_CONTRACT: throw ContractError(msg);
+    case MTKC_DATA: throw DataError(msg);
+    default: throw Error("device error: " + msg);
+  }
+}
+
+void Device::selectDevice(int index) { g_selected = index; }
+
+Device::Device() {
+  index_ = g_selected;
+  if(index_ < 0) {
+    const char* e = std::getenv("LOCAL_RANK");
+    index_ = e ? std::atoi(e) : 0;
+    int n = 0;
+    if(mtkc_device_count(&n) == MTKC_OK && n > 0)
+      index_ %= n;
+  }
+  MTKC(mtkc_init(index_));
+  MTKC(mtkc_stream_create(&stream_));
+  MTKC(mtkc_stream_create(&comm_));
+  void* f = nullptr;
+  MTKC(mtkc_malloc(&f, 256));
+  flags_ = (int*)f;
+  MTKC(mtkc_memset(flags_, 0, 256, stream_));
+  MTKC(mtkc_sm_count(&sms_));
+  const char* p = std::getenv("MTK_PRECISION");
+  if(p && (std::string(p) == "fp32" || std::string(p) == "FP32"))
+    precision_ = Precision::FP32;
+}
+
+Device& Device::get() {
+  static Device* d = new Device();  // intentionally leaked: lives for the process
+  return *d;
+}
+
+float* Device::scratch(size_t bytes) {
+  if(bytes <= scratchBytes_ && scratch_)
+    return scratch_->ptr;
+  size_t want = std::max(bytes, (size_t)256 << 20);
+  sync();
+  scratch_ = std::make_shared<DeviceBuffer>(want / sizeof(float));
+  scratchBytes_ = want;
+  return scratch_->ptr;
+}
+
+void Device::sync() { MTKC(mtkc_stream_sync(stream_)); }
+
+void Device::checkFlags(const std::string& where) {
+  int host = 0;
+  MTKC(mtkc_memcpy_d2h(&host, flags_, sizeof(int), stream_));
+  sync();
+  if(!host)
+    return;
+  MTKC(mtkc_memset(flags_, 0, sizeof(int), stream_));
+  if(host & MTKC_FLAG_MASKED_ROW)
+    throw NumericError("softmax over a fully-masked row (" + where + ")");
+  if(host & MTKC_FLAG_DIV_ZERO)
+    throw NumericError("division by zero in elementwise div (" + where + ")");
+  if(host & MTKC_FLAG_BAD_ID)
+    throw DataError("row/token id out of range (" + where + ")");
+  if(host & MTKC_FLAG_NONFINITE)
+    throw NumericError("non-finite value (" + where + ")");
+}
+
+}  // namespace mtk

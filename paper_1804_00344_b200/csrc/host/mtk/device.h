@@ -1,0 +1,55 @@
+// Per-process device context: the compute stream every kernel is issued on,
+// the communication stream, the device error-flag word and a shared
+// stream-ordered scratch buffer (split-K partials, column-sum partials).
+#pragma once
+
+#include <cstddef>
+#include <memory>
+#include <string>
+
+#include "mtk/tensor.h"
+#include "mtk_cuda.h"
+
+namespace mtk {
+
+// GEMM arithmetic.  FP32 = CUDA-core kernel with the reference's exact
+// summation order (parity mode); TF32 = tcgen05 tensor cores (default).
+enum class Precision { FP32 = 0, TF32 = 1 };
+
+class Device {
+public:
+  static Device& get();  // initialises the device on first use
+
+  void* stream() const { return stream_; }
+  void* commStream() const { return comm_; }
+  int* flags() const { return flags_; }
+  int sms() const { return sms_; }
+  int index() const { return index_; }
+  Precision precision() const { return precision_; }
+  void setPrecision(Precision p) { precision_ = p; }
+
+  float* scratch(size_t bytes);  // stream-ordered scratch, grows on demand
+  size_t scratchBytes() const { return scratchBytes_; }
+
+  void sync();        // synchronise the compute stream
+  // synchronise, read and clear the flag word, throw the mapped error
+  void checkFlags(const std::string& where);
+  static void selectDevice(int index);  // before first get()
+
+private:
+  Device();
+  void* stream_ = nullptr;
+  void* comm_ = nullptr;
+  int* flags_ = nullptr;
+  int sms_ = 148;
+  int index_ = 0;
+  Precision precision_ = Precision::TF32;
+  std::shared_ptr<DeviceBuffer> scratch_;
+  size_t scratchBytes_ = 0;
+};
+
+// Map an mtkc status code to the reference's exception types.
+void mtkcCheck(int rc, const char* what);
+#define MTKC(call) ::mtk::mtkcCheck((call), #call)
+
+}  // namespace mtk

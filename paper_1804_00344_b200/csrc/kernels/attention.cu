@@ -1,0 +1,413 @@
+// Fused scaled dot-product multi-head attention core.
+//
+// Replaces the reference's node chain in MultiHeadAttention::apply
+// (layers.cpp:89-126): splitHeads (reshape/transpose/reshape copies),
+// dot(q, k^T), scale(1/sqrt(dk)), softmax with a host-built dense
+// [b*h, tq, tk] mask (:108-118), dot(weights, v) and the merge transpose.
+// Here heads are column slices of the projection outputs (no transposes),
+// the mask is the [b, tk] key mask plus a causal flag, and probabilities are
+// saved once for the backward pass.  Products are summed over the head dim
+// and over keys in ascending order with separately rounded multiply/add
+// (the reference's GEMM order, tensor.cpp:289-303), so scores and context
+// match the unfused reference up to the softmax's exp/sum rounding.
+#include "common.cuh"
+
+using namespace mtkc;
+
+namespace {
+
+constexpr int QB = 32;      // query rows per CTA
+constexpr int KC = 64;      // keys per staged chunk
+constexpr int ATT_T = 128;  // threads
+constexpr int MAX_TK = 512;
+constexpr int MAX_DK = 128;
+
+struct AttP {
+  float* out;
+  int64_t ldo;
+  float* probs;
+  const float* q;
+  int64_t ldq;
+  const float* k;
+  const float* v;
+  int64_t ldk;
+  const float* mask;
+  int64_t b, tq, tk;
+  int heads;
+  int64_t dk;
+  float scale;
+  int causal;
+  int* flags;
+};
+
+__device__ __forceinline__ bool key_ok(const AttP& p, int64_t bi, int64_t i, int64_t j) {
+  if(p.mask && p.mask[bi * p.tk + j] == 0.f)
+    return false;
+  if(p.causal && j > p.tk - p.tq + i)  // layers.cpp:115-116
+    return false;
+  return true;
+}
+
+__global__ void __launch_bounds__(ATT_T) attn_fwd_kernel(AttP p) {
+  extern __shared__ float sm[];
+  const int64_t dk = p.dk, ldS = p.tk + 1;
+  float* Qs = sm;                       // [QB][dk+1]
+  float* KVs = Qs + QB * (dk + 1);      // [KC][dk+1]
+  float* Ss = KVs + KC * (dk + 1);      // [QB][tk+1]
+  const int64_t q0 = (int64_t)blockIdx.x * QB;
+  const int h = blockIdx.y;
+  const int64_t bi = blockIdx.z;
+  const int nq = (int)min((int64_t)QB, p.tq - q0);
+  const int tid = threadIdx.x;
+  const int64_t hoff = (int64_t)h * dk;
+
+  for(int e = tid; e < QB * dk; e += ATT_T) {
+    int i = e / (int)dk, c = e % (int)dk;
+    Qs[i * (dk + 1) + c] = i < nq ? p.q[(bi * p.tq + q0 + i) * p.ldq + hoff + c] : 0.f;
+  }
+  // scores
+  for(int64_t k0 = 0; k0 < p.tk; k0 += KC) {
+    int nk = (int)min((int64_t)KC, p.tk - k0);
+    __syncthreads();
+    for(int e = tid; e < KC * dk; e += ATT_T) {
+      int j = e / (int)dk, c = e % (int)dk;
+      KVs[j * (dk + 1) + c] = j < nk ? p.k[(bi * p.tk + k0 + j) * p.ldk + hoff + c] : 0.f;
+    }
+    __syncthreads();
+    for(int e = tid; e < QB * KC; e += ATT_T) {
+      int i = e / KC, j = e % KC;
+      if(i >= nq || j >= nk)
+        continue;
+      const float* qr = Qs + i * (dk + 1);
+      const float* kr = KVs + j * (dk + 1);
+      float acc = 0.f;
+      for(int c = 0; c < dk; ++c)
+        if(qr[c] != 0.f)
+          acc = __fadd_rn(acc, __fmul_rn(qr[c], kr[c]));
+      Ss[i * ldS + k0 + j] = __fmul_rn(p.scale, acc);
+    }
+  }
+  __syncthreads();
+  // masked softmax, one warp per row
+  const int w = tid >> 5, lane = tid & 31;
+  for(int i = w; i < nq; i += ATT_T / 32) {
+    int64_t gi = q0 + i;
+    float* sr = Ss + i * ldS;
+    float mx = -INFINITY;
+    int any = 0;
+    for(int64_t j = lane; j < p.tk; j += 32)
+      if(key_ok(p, bi, gi, j)) {
+        any = 1;
+        mx = fmaxf(mx, sr[j]);
+      }
+    mx = warp_max(mx);
+    any = __any_sync(0xffffffffu, any);
+    if(!any && lane == 0 && p.flags)
+      atomicOr(p.flags, MTKC_FLAG_MASKED_ROW);
+    float s = 0.f;
+    for(int64_t j = lane; j < p.tk; j += 32)
+      if(key_ok(p, bi, gi, j))
+        s += expf(sr[j] - mx);
+    s = warp_sum(s);
+    float* pr = p.probs + (((bi * p.heads + h) * p.tq) + gi) * p.tk;
+    for(int64_t j = lane; j < p.tk; j += 32) {
+      float y = (any && key_ok(p, bi, gi, j)) ? expf(sr[j] - mx) / s : 0.f;
+      sr[j] = y;
+      pr[j] = y;
+    }
+  }
+  // context = P V
+  const int CPT = (int)((QB * dk + ATT_T - 1) / ATT_T);  // outputs per thread (<= 32)
+  float acc[32];
+#pragma unroll
+  for(int u = 0; u < 32; ++u)
+    acc[u] = 0.f;
+  for(int64_t k0 = 0; k0 < p.tk; k0 += KC) {
+    int nk = (int)min((int64_t)KC, p.tk - k0);
+    __syncthreads();
+    for(int e = tid; e < KC * dk; e += ATT_T) {
+      int j = e / (int)dk, c = e % (int)dk;
+      KVs[j * (dk + 1) + c] = j < nk ? p.v[(bi * p.tk + k0 + j) * p.ldk + hoff + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for(int u = 0; u < 32; ++u) {
+      if(u >= CPT)
+        break;
+      int e = tid + u * ATT_T;
+      int i = e / (int)dk, c = e % (int)dk;
+      if(i >= nq)
+        continue;
+      const float* pr = Ss + i * ldS + k0;
+      float a = acc[u];
+      for(int j = 0; j < nk; ++j) {
+        float pv = pr[j];
+        if(pv != 0.f)
+          a = __fadd_rn(a, __fmul_rn(pv, KVs[j * (dk + 1) + c]));
+      }
+      acc[u] = a;
+    }
+  }
+#pragma unroll
+  for(int u = 0; u < 32; ++u) {
+    if(u >= CPT)
+      break;
+    int e = tid + u * ATT_T;
+    int i = e / (int)dk, c = e % (int)dk;
+    if(i < nq)
+      p.out[(bi * p.tq + q0 + i) * p.ldo + hoff + c] = acc[u];
+  }
+}
+
+struct AttBP {
+  const float* gout;
+  int64_t ldo;
+  const float* probs;
+  const float* q;
+  int64_t ldq;
+  const float* k;
+  const float* v;
+  int64_t ldk;
+  float* gq;
+  float* gk;
+  float* gv;
+  float* ds;
+  int64_t b, tq, tk;
+  int heads;
+  int64_t dk;
+  float scale;
+  int accQ, accK, accV;
+};
+
+// Pass A, per (query block, head, batch row):
+//   dP = dO V^T ; D = rowsum(dP*P) ; G = scale * P*(dP - D) -> ds ; dQ (+)= G K
+__global__ void __launch_bounds__(ATT_T) attn_bwd_q_kernel(AttBP p) {
+  extern __shared__ float sm[];
+  const int64_t dk = p.dk, ldS = p.tk + 1;
+  float* Os = sm;                   // dO block [QB][dk+1]
+  float* KVs = Os + QB * (dk + 1);  // [KC][dk+1]
+  float* Ss = KVs + KC * (dk + 1);  // dP then G [QB][tk+1]
+  const int64_t q0 = (int64_t)blockIdx.x * QB;
+  const int h = blockIdx.y;
+  const int64_t bi = blockIdx.z;
+  const int nq = (int)min((int64_t)QB, p.tq - q0);
+  const int tid = threadIdx.x;
+  const int64_t hoff = (int64_t)h * dk;
+  const float* P = p.probs + ((bi * p.heads + h) * p.tq) * p.tk;
+
+  for(int e = tid; e < QB * dk; e += ATT_T) {
+    int i = e / (int)dk, c = e % (int)dk;
+    Os[i * (dk + 1) + c] = i < nq ? p.gout[(bi * p.tq + q0 + i) * p.ldo + hoff + c] : 0.f;
+  }
+  for(int64_t k0 = 0; k0 < p.tk; k0 += KC) {
+    int nk = (int)min((int64_t)KC, p.tk - k0);
+    __syncthreads();
+    for(int e = tid; e < KC * dk; e += ATT_T) {
+      int j = e / (int)dk, c = e % (int)dk;
+      KVs[j * (dk + 1) + c] = j < nk ? p.v[(bi * p.tk + k0 + j) * p.ldk + hoff + c] : 0.f;
+    }
+    __syncthreads();
+    for(int e = tid; e < QB * KC; e += ATT_T) {
+      int i = e / KC, j = e % KC;
+      if(i >= nq || j >= nk)
+        continue;
+      const float* orow = Os + i * (dk + 1);
+      const float* vr = KVs + j * (dk + 1);
+      float acc = 0.f;
+      for(int c = 0; c < dk; ++c)
+        acc = __fadd_rn(acc, __fmul_rn(orow[c], vr[c]));
+      Ss[i * ldS + k0 + j] = acc;
+    }
+  }
+  __syncthreads();
+  const int w = tid >> 5, lane = tid & 31;
+  for(int i = w; i < nq; i += ATT_T / 32) {
+    const float* pr = P + (q0 + i) * p.tk;
+    float* sr = Ss + i * ldS;
+    float d = 0.f;
+    for(int64_t j = lane; j < p.tk; j += 32)
+      d += sr[j] * pr[j];
+    d = warp_sum(d);
+    float* dsr = p.ds + ((bi * p.heads + h) * p.tq + q0 + i) * p.tk;
+    for(int64_t j = lane; j < p.tk; j += 32) {
+      float gval = p.scale * (pr[j] * (sr[j] - d));
+      sr[j] = gval;
+      dsr[j] = gval;
+    }
+  }
+  // dQ = G K
+  const int CPT = (int)((QB * dk + ATT_T - 1) / ATT_T);
+  float acc[32];
+#pragma unroll
+  for(int u = 0; u < 32; ++u)
+    acc[u] = 0.f;
+  for(int64_t k0 = 0; k0 < p.tk; k0 += KC) {
+    int nk = (int)min((int64_t)KC, p.tk - k0);
+    __syncthreads();
+    for(int e = tid; e < KC * dk; e += ATT_T) {
+      int j = e / (int)dk, c = e % (int)dk;
+      KVs[j * (dk + 1) + c] = j < nk ? p.k[(bi * p.tk + k0 + j) * p.ldk + hoff + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for(int u = 0; u < 32; ++u) {
+      if(u >= CPT)
+        break;
+      int e = tid + u * ATT_T;
+      int i = e / (int)dk, c = e % (int)dk;
+      if(i >= nq)
+        continue;
+      const float* gr = Ss + i * ldS + k0;
+      float a = acc[u];
+      for(int j = 0; j < nk; ++j)
+        a = __fadd_rn(a, __fmul_rn(gr[j], KVs[j * (dk + 1) + c]));
+      acc[u] = a;
+    }
+  }
+#pragma unroll
+  for(int u = 0; u < 32; ++u) {
+    if(u >= CPT)
+      break;
+    int e = tid + u * ATT_T;
+    int i = e / (int)dk, c = e % (int)dk;
+    if(i < nq) {
+      float* dst = p.gq + (bi * p.tq + q0 + i) * p.ldq + hoff + c;
+      *dst = p.accQ ? *dst + acc[u] : acc[u];
+    }
+  }
+}
+
+// Pass B, per (key chunk, head, batch row): dK (+)= G^T Q, dV (+)= P^T dO,
+// summing over queries in ascending order.
+__global__ void __launch_bounds__(ATT_T) attn_bwd_kv_kernel(AttBP p) {
+  extern __shared__ float sm[];
+  const int64_t dk = p.dk;
+  float* Qs = sm;                     // [QB][dk+1] query chunk (Q then dO)
+  float* Gs = Qs + QB * (dk + 1);     // [QB][KC+1] G chunk
+  float* Ps = Gs + QB * (KC + 1);     // [QB][KC+1] P chunk
+  float* Os = Ps + QB * (KC + 1);     // [QB][dk+1] dO chunk
+  const int64_t k0 = (int64_t)blockIdx.x * KC;
+  const int h = blockIdx.y;
+  const int64_t bi = blockIdx.z;
+  const int nk = (int)min((int64_t)KC, p.tk - k0);
+  const int tid = threadIdx.x;
+  const int64_t hoff = (int64_t)h * dk;
+  const float* P = p.probs + ((bi * p.heads + h) * p.tq) * p.tk;
+  const float* G = p.ds + ((bi * p.heads + h) * p.tq) * p.tk;
+  const int CPT = (int)((KC * dk + ATT_T - 1) / ATT_T);  // <= 64
+  float ak[64], av[64];
+#pragma unroll
+  for(int u = 0; u < 64; ++u) {
+    ak[u] = 0.f;
+    av[u] = 0.f;
+  }
+  for(int64_t i0 = 0; i0 < p.tq; i0 += QB) {
+    int nq = (int)min((int64_t)QB, p.tq - i0);
+    __syncthreads();
+    for(int e = tid; e < QB * dk; e += ATT_T) {
+      int i = e / (int)dk, c = e % (int)dk;
+      bool ok = i < nq;
+      Qs[i * (dk + 1) + c] = ok ? p.q[(bi * p.tq + i0 + i) * p.ldq + hoff + c] : 0.f;
+      Os[i * (dk + 1) + c] = ok ? p.gout[(bi * p.tq + i0 + i) * p.ldo + hoff + c] : 0.f;
+    }
+    for(int e = tid; e < QB * KC; e += ATT_T) {
+      int i = e / KC, j = e % KC;
+      bool ok = i < nq && j < nk;
+      Gs[i * (KC + 1) + j] = ok ? G[(i0 + i) * p.tk + k0 + j] : 0.f;
+      Ps[i * (KC + 1) + j] = ok ? P[(i0 + i) * p.tk + k0 + j] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for(int u = 0; u < 64; ++u) {
+      if(u >= CPT)
+        break;
+      int e = tid + u * ATT_T;
+      int j = e / (int)dk, c = e % (int)dk;
+      if(j >= nk)
+        continue;
+      float a1 = ak[u], a2 = av[u];
+      for(int i = 0; i < nq; ++i) {
+        a1 = __fadd_rn(a1, __fmul_rn(Gs[i * (KC + 1) + j], Qs[i * (dk + 1) + c]));
+        a2 = __fadd_rn(a2, __fmul_rn(Ps[i * (KC + 1) + j], Os[i * (dk + 1) + c]));
+      }
+      ak[u] = a1;
+      av[u] = a2;
+    }
+  }
+#pragma unroll
+  for(int u = 0; u < 64; ++u) {
+    if(u >= CPT)
+      break;
+    int e = tid + u * ATT_T;
+    int j = e / (int)dk, c = e % (int)dk;
+    if(j >= nk)
+      continue;
+    int64_t off = (bi * p.tk + k0 + j) * p.ldk + hoff + c;
+    p.gk[off] = p.accK ? p.gk[off] + ak[u] : ak[u];
+    p.gv[off] = p.accV ? p.gv[off] + av[u] : av[u];
+  }
+}
+
+int set_smem(const void* fn, size_t bytes) {
+  if(bytes <= 48 * 1024)
+    return MTKC_OK;
+  return cuda_status(
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+      "attention smem attribute");
+}
+
+}  // namespace
+
+extern "C" {
+
+int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_t ldq,
+                   const float* k, const float* v, int64_t ldk, const float* key_mask,
+                   int64_t b, int64_t tq, int64_t tk, int heads, int64_t dk, float scale,
+                   int causal, int* flags, void* stream) {
+  if(b <= 0 || tq <= 0 || tk <= 0)
+    return MTKC_OK;
+  if(tk > MAX_TK || dk > MAX_DK || dk <= 0)
+    return fail(MTKC_DIMENSION, "fused attention supports tk <= 512 and head dim <= 128");
+  AttP p{out, ldo, probs, q, ldq, k, v, ldk, key_mask, b, tq, tk, heads, dk, scale, causal, flags};
+  size_t smem = sizeof(float) * ((size_t)QB * (dk + 1) + (size_t)KC * (dk + 1) +
+                                 (size_t)QB * (tk + 1));
+  int rc = set_smem((const void*)attn_fwd_kernel, smem);
+  if(rc)
+    return rc;
+  dim3 grid((unsigned)cdiv(tq, QB), (unsigned)heads, (unsigned)b);
+  attn_fwd_kernel<<<grid, ATT_T, smem, S(stream)>>>(p);
+  MTKC_POST_LAUNCH("attn_fwd_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
+                            const float* q, int64_t ldq, const float* k, const float* v,
+                            int64_t ldk, float* gq, float* gk, float* gv, float* dsbuf,
+                            int64_t b, int64_t tq, int64_t tk, int heads, int64_t dk,
+                            float scale, int accumulate_q, int accumulate_k, int accumulate_v,
+                            void* stream) {
+  if(b <= 0 || tq <= 0 || tk <= 0)
+    return MTKC_OK;
+  if(tk > MAX_TK || dk > MAX_DK || dk <= 0)
+    return fail(MTKC_DIMENSION, "fused attention supports tk <= 512 and head dim <= 128");
+  AttBP p{gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, dsbuf, b, tq, tk, heads, dk, scale,
+          accumulate_q, accumulate_k, accumulate_v};
+  size_t smemA = sizeof(float) * ((size_t)QB * (dk + 1) + (size_t)KC * (dk + 1) +
+                                  (size_t)QB * (tk + 1));
+  int rc = set_smem((const void*)attn_bwd_q_kernel, smemA);
+  if(rc)
+    return rc;
+  dim3 gA((unsigned)cdiv(tq, QB), (unsigned)heads, (unsigned)b);
+  attn_bwd_q_kernel<<<gA, ATT_T, smemA, S(stream)>>>(p);
+  MTKC_POST_LAUNCH("attn_bwd_q_kernel");
+  size_t smemB = sizeof(float) * (2 * (size_t)QB * (dk + 1) + 2 * (size_t)QB * (KC + 1));
+  rc = set_smem((const void*)attn_bwd_kv_kernel, smemB);
+  if(rc)
+    return rc;
+  dim3 gB((unsigned)cdiv(tk, KC), (unsigned)heads, (unsigned)b);
+  attn_bwd_kv_kernel<<<gB, ATT_T, smemB, S(stream)>>>(p);
+  MTKC_POST_LAUNCH("attn_bwd_kv_kernel");
+  return MTKC_OK;
+}
+
+}  // extern "C"

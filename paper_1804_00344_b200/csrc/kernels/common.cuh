@@ -1,0 +1,131 @@
+// Shared helpers for the libmtkcuda.so kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "mtk_cuda.h"
+
+namespace mtkc {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_status(cudaError_t e, const char* where);
+void count_launch(int n = 1);
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Launch check used after every <<<>>>: counts the launch and converts a
+// launch failure into MTKC_CUDA with the kernel name.
+#define MTKC_POST_LAUNCH(name)                                  \
+  do {                                                          \
+    ::mtkc::count_launch();                                     \
+    cudaError_t _e = cudaGetLastError();                        \
+    if(_e != cudaSuccess) return ::mtkc::cuda_status(_e, name); \
+  } while(0)
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline unsigned grid1d(int64_t n, int threads, int64_t cap = 148 * 32) {
+  int64_t g = cdiv(n, threads);
+  if(g > cap)
+    g = cap;
+  if(g < 1)
+    g = 1;
+  return (unsigned)g;
+}
+
+// Right-aligned 4-d strides of a broadcast operand (tensor.cpp:120-130).
+struct Bcast4 {
+  int64_t s[4];
+};
+
+inline Bcast4 bcast_strides(const int64_t d[4]) {
+  Bcast4 b;
+  int64_t run = 1;
+  for(int i = 3; i >= 0; --i) {
+    b.s[i] = d[i] == 1 ? 0 : run;
+    run *= d[i];
+  }
+  return b;
+}
+
+struct Dims4 {
+  int64_t d[4];
+};
+
+inline Dims4 dims4(const int64_t d[4]) {
+  Dims4 r;
+  for(int i = 0; i < 4; ++i)
+    r.d[i] = d[i];
+  return r;
+}
+
+}  // namespace mtkc
+
+// ---------------------------------------------------------------- device
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for(int o = 16; o > 0; o >>= 1)
+    v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for(int o = 16; o > 0; o >>= 1)
+    v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum; `red` must hold >= 32 floats. All threads get the result.
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if(lane == 0)
+    red[w] = v;
+  __syncthreads();
+  float t = lane < nw ? red[lane] : 0.f;
+  t = warp_sum(t);
+  return t;
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if(lane == 0)
+    red[w] = v;
+  __syncthreads();
+  float t = lane < nw ? red[lane] : -INFINITY;
+  t = warp_max(t);
+  return t;
+}
+
+// Reference elementwise semantics (tensor.cpp:140-158).
+__device__ __forceinline__ float apply_unary(int op, float x) {
+  switch(op) {
+    case MTKC_TANH: return tanhf(x);
+    case MTKC_SIGMOID: return 1.f / (1.f + expf(-x));
+    case MTKC_RELU: return x > 0.f ? x : 0.f;
+    case MTKC_EXP: return expf(x);
+    case MTKC_LOG: return logf(x);
+    case MTKC_NEG: return -x;
+    default: return x;
+  }
+}
+
+__device__ __forceinline__ float apply_binary(int op, float x, float y) {
+  switch(op) {
+    case MTKC_ADD: return x + y;
+    case MTKC_SUB: return x - y;
+    case MTKC_MUL: return x * y;
+    case MTKC_DIV: return x / y;
+    default: return x;
+  }
+}

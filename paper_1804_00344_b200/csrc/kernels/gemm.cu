@@ -1,0 +1,179 @@
+// GEMM entry point (matmulInto tensor.cpp:258-306, matmulAccumInto
+// graph.cpp:273-291, affine graph.cpp:334-336) and its CUDA-core FP32 path.
+//
+// The FP32 path reproduces the reference's arithmetic exactly: every output
+// element starts from beta*C (or 0), then adds round(round(alpha*a)*b) for
+// k = 0..K-1 in ascending order, skipping alpha*a == 0 (tensor.cpp:282-303),
+// with separately rounded multiplies and adds (the reference is compiled
+// without FMA contraction).  It is the parity-mode GEMM and the fallback for
+// shapes the tensor-core path does not take (unaligned strides, tiny or
+// batched-broadcast products).  The tensor-core path lives in gemm_tc.cu.
+#include "common.cuh"
+
+namespace mtkc {
+bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc);  // gemm_tc.cu
+}
+
+using namespace mtkc;
+
+namespace {
+
+thread_local int t_last_path = 0;
+
+constexpr int TM = 64, TN = 64, TK = 16;
+
+struct GemmP {
+  int64_t M, N, K, batch;
+  const float* A;
+  int64_t lda, sA;
+  int tA;
+  const float* B;
+  int64_t ldb, sB;
+  int tB;
+  float* C;
+  int64_t ldc, sC;
+  float alpha, beta;
+  const float* bias;
+  int epi;
+  const float* gate;
+  int foldBatch;  // sum over batch into one C
+};
+
+__global__ void __launch_bounds__(256) gemm_fp32_kernel(GemmP p) {
+  __shared__ float As[TK][TM + 1];
+  __shared__ float Bs[TK][TN + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t row0 = (int64_t)blockIdx.y * TM, col0 = (int64_t)blockIdx.x * TN;
+  const int64_t zb = p.foldBatch ? 0 : blockIdx.z;
+  float* C = p.C + zb * p.sC;
+  float acc[4][4];
+  const bool gated = p.gate != nullptr;
+#pragma unroll
+  for(int i = 0; i < 4; ++i)
+#pragma unroll
+    for(int j = 0; j < 4; ++j) {
+      int64_t r = row0 + ty * 4 + i, c = col0 + tx * 4 + j;
+      float v = 0.f;
+      if(!gated && p.beta != 0.f && r < p.M && c < p.N) {
+        v = C[r * p.ldc + c];
+        if(p.beta != 1.f)
+          v = __fmul_rn(v, p.beta);
+      }
+      acc[i][j] = v;
+    }
+  const int64_t nb = p.foldBatch ? p.batch : 1;
+  for(int64_t bb = 0; bb < nb; ++bb) {
+    const int64_t b = p.foldBatch ? bb : zb;
+    const float* A = p.A + b * p.sA;
+    const float* B = p.B + b * p.sB;
+    for(int64_t k0 = 0; k0 < p.K; k0 += TK) {
+      // cooperative tile loads (4 elements per thread per operand)
+      for(int e = threadIdx.x; e < TK * TM; e += 256) {
+        int kk = e / TM, mm = e % TM;
+        int64_t gi = row0 + mm, gk = k0 + kk;
+        float v = 0.f;
+        if(gi < p.M && gk < p.K)
+          v = p.tA ? A[gk * p.lda + gi] : A[gi * p.lda + gk];
+        As[kk][mm] = p.alpha == 1.f ? v : __fmul_rn(p.alpha, v);
+      }
+      for(int e = threadIdx.x; e < TK * TN; e += 256) {
+        int kk = e / TN, nn = e % TN;
+        int64_t gj = col0 + nn, gk = k0 + kk;
+        float v = 0.f;
+        if(gj < p.N && gk < p.K)
+          v = p.tB ? B[gj * p.ldb + gk] : B[gk * p.ldb + gj];
+        Bs[kk][nn] = v;
+      }
+      __syncthreads();
+      const int kmax = (int)min((int64_t)TK, p.K - k0);
+      for(int kk = 0; kk < kmax; ++kk) {
+        float av[4], bv[4];
+#pragma unroll
+        for(int i = 0; i < 4; ++i)
+          av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+        for(int j = 0; j < 4; ++j)
+          bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+        for(int i = 0; i < 4; ++i) {
+          if(av[i] == 0.f)
+            continue;  // tensor.cpp:293-294
+#pragma unroll
+          for(int j = 0; j < 4; ++j)
+            acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+        }
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for(int i = 0; i < 4; ++i)
+#pragma unroll
+    for(int j = 0; j < 4; ++j) {
+      int64_t r = row0 + ty * 4 + i, c = col0 + tx * 4 + j;
+      if(r >= p.M || c >= p.N)
+        continue;
+      float v = acc[i][j];
+      if(p.bias)
+        v = __fadd_rn(v, p.bias[c]);
+      if(p.epi == MTKC_EPI_RELU)
+        v = v > 0.f ? v : 0.f;
+      float* dst = C + r * p.ldc + c;
+      if(gated) {
+        v = p.gate[zb * p.sC + r * p.ldc + c] > 0.f ? v : 0.f;
+        if(p.beta != 0.f)
+          v = __fadd_rn(p.beta == 1.f ? *dst : __fmul_rn(p.beta, *dst), v);
+      }
+      *dst = v;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int mtkc_gemm_last_path(void) { return t_last_path; }
+
+int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
+  if(!a)
+    return fail(MTKC_CONTRACT, "mtkc_gemm: null args");
+  if(a->M <= 0 || a->N <= 0 || a->K <= 0 || a->batch <= 0)
+    return fail(MTKC_DIMENSION, "mtkc_gemm: non-positive extent");
+  if(!a->A || !a->B || !a->C)
+    return fail(MTKC_CONTRACT, "mtkc_gemm: null operand");
+  int rc = MTKC_OK;
+  if(a->precision == MTKC_GEMM_TF32 && tc_gemm(*a, S(stream), &rc)) {
+    t_last_path = 1;
+    return rc;
+  }
+  t_last_path = 0;
+  GemmP p;
+  p.M = a->M;
+  p.N = a->N;
+  p.K = a->K;
+  p.batch = a->batch;
+  p.A = a->A;
+  p.lda = a->lda;
+  p.sA = a->strideA;
+  p.tA = a->transA;
+  p.B = a->B;
+  p.ldb = a->ldb;
+  p.sB = a->strideB;
+  p.tB = a->transB;
+  p.C = a->C;
+  p.ldc = a->ldc;
+  p.sC = a->strideC;
+  p.alpha = a->alpha;
+  p.beta = a->beta;
+  p.bias = a->bias;
+  p.epi = a->epilogue;
+  p.gate = a->gate;
+  p.foldBatch = (a->batch > 1 && a->strideC == 0) ? 1 : 0;
+  dim3 grid((unsigned)cdiv(a->N, TN), (unsigned)cdiv(a->M, TM),
+            p.foldBatch ? 1u : (unsigned)a->batch);
+  gemm_fp32_kernel<<<grid, 256, 0, S(stream)>>>(p);
+  MTKC_POST_LAUNCH("gemm_fp32_kernel");
+  return MTKC_OK;
+}
+
+}  // extern "C"

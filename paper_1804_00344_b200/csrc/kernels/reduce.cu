@@ -1,0 +1,183 @@
+// Reductions: reduceInto (tensor.cpp:322-368) and its graph backward
+// (graph.cpp:488-521); deterministic column sums for bias/gain gradients;
+// the allFinite scan (tensor.cpp:95-100) as a device flag.
+#include "common.cuh"
+
+using namespace mtkc;
+
+namespace {
+
+__global__ void reduce_kernel(int op, float* out, const float* in, int64_t outer, int64_t n,
+                              int64_t inner) {
+  int64_t total = outer * inner;
+  for(int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+      t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = t / inner, c = t % inner;
+    const float* base = in + a * n * inner + c;
+    float acc;
+    if(op == MTKC_RSUM || op == MTKC_RMEAN) {
+      acc = 0.f;
+      for(int64_t i = 0; i < n; ++i)
+        acc += base[i * inner];
+      if(op == MTKC_RMEAN)
+        acc /= (float)n;
+    } else if(op == MTKC_RMAX) {
+      acc = base[0];
+      for(int64_t i = 1; i < n; ++i)
+        acc = fmaxf(acc, base[i * inner]);
+    } else {
+      float best = base[0];
+      int64_t arg = 0;
+      for(int64_t i = 1; i < n; ++i)
+        if(base[i * inner] > best) {  // strict: ties keep the lowest index (:357)
+          best = base[i * inner];
+          arg = i;
+        }
+      acc = (float)arg;
+    }
+    out[t] = acc;
+  }
+}
+
+__global__ void reduce_bwd_kernel(int op, float* gin, const float* gout, const float* in,
+                                  int64_t outer, int64_t n, int64_t inner) {
+  int64_t total = outer * inner;
+  for(int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+      t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = t / inner, c = t % inner;
+    float go = gout[t];
+    float* base = gin + a * n * inner + c;
+    const float* xv = in + a * n * inner + c;
+    if(op == MTKC_RSUM) {
+      for(int64_t i = 0; i < n; ++i)
+        base[i * inner] += go;
+    } else if(op == MTKC_RMEAN) {
+      float v = go / (float)n;
+      for(int64_t i = 0; i < n; ++i)
+        base[i * inner] += v;
+    } else if(op == MTKC_RMAX) {
+      int64_t best = 0;
+      for(int64_t i = 1; i < n; ++i)
+        if(xv[i * inner] > xv[best * inner])
+          best = i;
+      base[best * inner] += go;
+    }
+  }
+}
+
+constexpr int CS_ROWS = 128;  // rows per partial
+constexpr int CS_COLS = 128;  // columns per CTA (one per thread)
+
+// partial[rb][c] = sum_{r in block rb} in[r][c]
+__global__ void colsum_partial_kernel(float* part, const float* in, int64_t rows, int64_t cols) {
+  int64_t c = (int64_t)blockIdx.x * CS_COLS + threadIdx.x;
+  int64_t r0 = (int64_t)blockIdx.y * CS_ROWS;
+  if(c >= cols)
+    return;
+  int64_t r1 = min(rows, r0 + CS_ROWS);
+  float acc = 0.f;
+  for(int64_t r = r0; r < r1; ++r)
+    acc += in[r * cols + c];
+  part[(int64_t)blockIdx.y * cols + c] = acc;
+}
+
+__global__ void colsum_final_kernel(float* out, const float* part, int64_t nparts, int64_t cols,
+                                    int accumulate) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if(c >= cols)
+    return;
+  float acc = accumulate ? out[c] : 0.f;
+  float s = 0.f;
+  for(int64_t p = 0; p < nparts; ++p)
+    s += part[p * cols + c];
+  out[c] = acc + s;
+}
+
+// single-level variant (no workspace): one thread per column walks all rows
+__global__ void colsum_direct_kernel(float* out, const float* in, int64_t rows, int64_t cols,
+                                     int accumulate) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if(c >= cols)
+    return;
+  float s = 0.f;
+  for(int64_t r = 0; r < rows; ++r)
+    s += in[r * cols + c];
+  out[c] = (accumulate ? out[c] : 0.f) + s;
+}
+
+__global__ void finite_kernel(const float* in, int64_t n, int* flags) {
+  bool bad = false;
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+      i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(in[i]);
+  if(__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    atomicOr(flags, MTKC_FLAG_NONFINITE);
+}
+
+__global__ void finite4_kernel(const float4* in, int64_t n4, int* flags) {
+  bool bad = false;
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = in[i];
+    bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+  }
+  if(__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    atomicOr(flags, MTKC_FLAG_NONFINITE);
+}
+
+}  // namespace
+
+extern "C" {
+
+int mtkc_reduce(int op, float* out, const float* in, int64_t outer, int64_t n, int64_t inner,
+                void* stream) {
+  if(outer * inner <= 0 || n <= 0)
+    return MTKC_OK;
+  reduce_kernel<<<grid1d(outer * inner, 128), 128, 0, S(stream)>>>(op, out, in, outer, n, inner);
+  MTKC_POST_LAUNCH("reduce_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_reduce_backward(int op, float* gin, const float* gout, const float* in,
+                         int64_t outer, int64_t n, int64_t inner, void* stream) {
+  if(op == MTKC_RARGMAX || outer * inner <= 0)
+    return MTKC_OK;
+  reduce_bwd_kernel<<<grid1d(outer * inner, 128), 128, 0, S(stream)>>>(op, gin, gout, in, outer,
+                                                                       n, inner);
+  MTKC_POST_LAUNCH("reduce_bwd_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int accumulate,
+                float* workspace, size_t workspace_bytes, void* stream) {
+  if(rows <= 0 || cols <= 0)
+    return MTKC_OK;
+  int64_t nparts = cdiv(rows, CS_ROWS);
+  if(nparts <= 1 || !workspace || workspace_bytes < (size_t)(nparts * cols) * sizeof(float)) {
+    colsum_direct_kernel<<<(unsigned)cdiv(cols, 128), 128, 0, S(stream)>>>(out, in, rows, cols,
+                                                                          accumulate);
+    MTKC_POST_LAUNCH("colsum_direct_kernel");
+    return MTKC_OK;
+  }
+  dim3 g((unsigned)cdiv(cols, CS_COLS), (unsigned)nparts);
+  colsum_partial_kernel<<<g, CS_COLS, 0, S(stream)>>>(workspace, in, rows, cols);
+  MTKC_POST_LAUNCH("colsum_partial_kernel");
+  colsum_final_kernel<<<(unsigned)cdiv(cols, 128), 128, 0, S(stream)>>>(out, workspace, nparts,
+                                                                      cols, accumulate);
+  MTKC_POST_LAUNCH("colsum_final_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_check_finite(const float* in, int64_t n, int* flags, void* stream) {
+  if(n <= 0)
+    return MTKC_OK;
+  if(n % 4 == 0 && (uintptr_t)in % 16 == 0)
+    finite4_kernel<<<grid1d(n / 4, 256, 148 * 8), 256, 0, S(stream)>>>((const float4*)in, n / 4,
+                                                                      flags);
+  else
+    finite_kernel<<<grid1d(n, 256, 148 * 8), 256, 0, S(stream)>>>(in, n, flags);
+  MTKC_POST_LAUNCH("finite_kernel");
+  return MTKC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,333 @@
+// Masked softmax (softmaxInto tensor.cpp:393-440, graph.cpp:526-555) and the
+// layout kernels: transposeInto / concatInto / sliceInto (tensor.cpp:480-541),
+// gatherRowsInto / scatterAddRows (:456-476) and the embedding lookup fused
+// with the positional encoding (graph.cpp:595-622 + layers.cpp:164-179).
+#include "common.cuh"
+
+using namespace mtkc;
+
+namespace {
+
+struct SmP {
+  float* out;
+  const float* x;
+  const float* mask;
+  int64_t rows, cols;
+  int64_t xd[4];
+  int64_t ms[4];
+  int logMode;
+  int* flags;
+};
+
+// One warp per row.  Two passes over the row like the reference: max over
+// unmasked entries, then sum of exp(x - max) over unmasked entries.
+__global__ void softmax_kernel(SmP p) {
+  int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  int lane = threadIdx.x & 31;
+  if(row >= p.rows)
+    return;
+  const float* xr = p.x + row * p.cols;
+  float* orow = p.out + row * p.cols;
+  int64_t moff = 0;
+  if(p.mask) {
+    int64_t i2 = row % p.xd[2], rest = row / p.xd[2];
+    int64_t i1 = rest % p.xd[1], i0 = rest / p.xd[1];
+    moff = i0 * p.ms[0] + i1 * p.ms[1] + i2 * p.ms[2];
+  }
+  auto m = [&](int64_t j) -> bool { return !p.mask || p.mask[moff + j * p.ms[3]] != 0.f; };
+  float mx = -INFINITY;
+  int any = 0;
+  for(int64_t j = lane; j < p.cols; j += 32)
+    if(m(j)) {
+      any = 1;
+      mx = fmaxf(mx, xr[j]);
+    }
+  mx = warp_max(mx);
+  any = __any_sync(0xffffffffu, any);
+  if(!any) {
+    if(lane == 0 && p.flags)
+      atomicOr(p.flags, MTKC_FLAG_MASKED_ROW);
+    for(int64_t j = lane; j < p.cols; j += 32)
+      orow[j] = p.logMode ? -INFINITY : 0.f;
+    return;
+  }
+  float s = 0.f;
+  for(int64_t j = lane; j < p.cols; j += 32)
+    if(m(j))
+      s += expf(xr[j] - mx);
+  s = warp_sum(s);
+  if(p.logMode) {
+    float lz = mx + logf(s);
+    for(int64_t j = lane; j < p.cols; j += 32)
+      orow[j] = m(j) ? xr[j] - lz : -INFINITY;
+  } else {
+    for(int64_t j = lane; j < p.cols; j += 32)
+      orow[j] = m(j) ? expf(xr[j] - mx) / s : 0.f;
+  }
+}
+
+// dx += y * (g - sum(g*y))  (graph.cpp:539-552)
+__global__ void softmax_bwd_kernel(float* gx, const float* y, const float* go, int64_t rows,
+                                   int64_t cols) {
+  int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  int lane = threadIdx.x & 31;
+  if(row >= rows)
+    return;
+  const float* yr = y + row * cols;
+  const float* gr = go + row * cols;
+  float* xr = gx + row * cols;
+  float d = 0.f;
+  for(int64_t j = lane; j < cols; j += 32)
+    d += gr[j] * yr[j];
+  d = warp_sum(d);
+  for(int64_t j = lane; j < cols; j += 32)
+    xr[j] += yr[j] * (gr[j] - d);
+}
+
+struct TrP {
+  float* out;
+  const float* src;
+  int64_t od[4];
+  int64_t ss[4];  // source stride for each output dim
+  int64_t n;
+  int acc;
+};
+
+__global__ void transpose_kernel(TrP p) {
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i;
+    int64_t i3 = r % p.od[3];
+    r /= p.od[3];
+    int64_t i2 = r % p.od[2];
+    r /= p.od[2];
+    int64_t i1 = r % p.od[1];
+    int64_t i0 = r / p.od[1];
+    float v = p.src[i0 * p.ss[0] + i1 * p.ss[1] + i2 * p.ss[2] + i3 * p.ss[3]];
+    p.out[i] = p.acc ? p.out[i] + v : v;
+  }
+}
+
+__global__ void copy_blocks_kernel(float* dst, int64_t dstStride, int64_t dstOff,
+                                   const float* src, int64_t srcStride, int64_t srcOff,
+                                   int64_t outer, int64_t len, int acc) {
+  int64_t n = outer * len;
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = i / len, j = i % len;
+    float v = src[o * srcStride + srcOff + j];
+    float* d = dst + o * dstStride + dstOff + j;
+    *d = acc ? *d + v : v;
+  }
+}
+
+__global__ void gather_rows_kernel(float* out, const float* src, const int32_t* rows, int64_t n,
+                                   int64_t cols, int64_t srcRows, int* flags) {
+  int64_t total = n * cols;
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / cols, c = i % cols;
+    int32_t id = rows[r];
+    if(id < 0 || id >= srcRows) {
+      if(flags && c == 0)
+        atomicOr(flags, MTKC_FLAG_BAD_ID);
+      out[i] = 0.f;
+      continue;
+    }
+    out[i] = src[(int64_t)id * cols + c];
+  }
+}
+
+// One CTA per unique row id; threads stride over columns; the segment is
+// summed in original position order (stable sort), starting from out[id].
+__global__ void scatter_add_kernel(float* out, const float* src, const int32_t* perm,
+                                   const int32_t* seg, const int32_t* uniq, int64_t cols,
+                                   float scale) {
+  int64_t u = blockIdx.x;
+  int64_t id = uniq[u];
+  int32_t s0 = seg[u], s1 = seg[u + 1];
+  float* dst = out + id * cols;
+  for(int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    float acc = dst[c];
+    for(int32_t k = s0; k < s1; ++k) {
+      float v = src[(int64_t)perm[k] * cols + c];
+      acc += scale == 1.f ? v : scale * v;
+    }
+    dst[c] = acc;
+  }
+}
+
+// out[n,:] = table[id,:]*s + pe[n % t,:]; exact gather when s == 1, pe == 0.
+__global__ void embed_kernel(float* out, const float* table, const int32_t* ids, int64_t n,
+                             int64_t e, int64_t vocab, float s, const float* pe, int64_t t,
+                             int* flags) {
+  int64_t total = n * e;
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / e, c = i % e;
+    int32_t id = ids[r];
+    if(id < 0 || id >= vocab) {
+      if(flags && c == 0)
+        atomicOr(flags, MTKC_FLAG_BAD_ID);
+      out[i] = 0.f;
+      continue;
+    }
+    float v = table[(int64_t)id * e + c];
+    if(s != 1.f)
+      v = s * v;
+    if(pe)
+      v = v + pe[(r % t) * e + c];
+    out[i] = v;
+  }
+}
+
+__global__ void embed4_kernel(float4* out, const float4* table, const int32_t* ids, int64_t n,
+                              int64_t e4, int64_t vocab, float s, const float4* pe, int64_t t,
+                              int* flags) {
+  int64_t total = n * e4;
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / e4, c = i % e4;
+    int32_t id = ids[r];
+    if(id < 0 || id >= vocab) {
+      if(flags && c == 0)
+        atomicOr(flags, MTKC_FLAG_BAD_ID);
+      out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    float4 v = table[(int64_t)id * e4 + c];
+    if(s != 1.f) {
+      v.x = s * v.x;
+      v.y = s * v.y;
+      v.z = s * v.z;
+      v.w = s * v.w;
+    }
+    if(pe) {
+      float4 q = pe[(r % t) * e4 + c];
+      v.x = v.x + q.x;
+      v.y = v.y + q.y;
+      v.z = v.z + q.z;
+      v.w = v.w + q.w;
+    }
+    out[i] = v;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int mtkc_softmax(float* out, const float* x, const int64_t xd[4], const float* mask,
+                 const int64_t md[4], int log_mode, int* flags, void* stream) {
+  SmP p;
+  p.out = out;
+  p.x = x;
+  p.mask = mask;
+  p.cols = xd[3];
+  p.rows = xd[0] * xd[1] * xd[2];
+  for(int i = 0; i < 4; ++i)
+    p.xd[i] = xd[i];
+  if(mask) {
+    Bcast4 ms = bcast_strides(md);
+    for(int i = 0; i < 4; ++i) {
+      if(md[i] != 1 && md[i] != xd[i])
+        return fail(MTKC_DIMENSION, "softmax: mask not broadcastable to input");
+      p.ms[i] = ms.s[i];
+    }
+  } else {
+    for(int i = 0; i < 4; ++i)
+      p.ms[i] = 0;
+  }
+  p.logMode = log_mode;
+  p.flags = flags;
+  if(p.rows <= 0)
+    return MTKC_OK;
+  softmax_kernel<<<(unsigned)cdiv(p.rows, 8), 256, 0, S(stream)>>>(p);
+  MTKC_POST_LAUNCH("softmax_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_softmax_backward(float* gx, const float* y, const float* go, int64_t rows,
+                          int64_t cols, void* stream) {
+  if(rows <= 0)
+    return MTKC_OK;
+  softmax_bwd_kernel<<<(unsigned)cdiv(rows, 8), 256, 0, S(stream)>>>(gx, y, go, rows, cols);
+  MTKC_POST_LAUNCH("softmax_bwd_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_transpose(float* out, const float* src, const int64_t sd[4], const int perm[4],
+                   int accumulate, void* stream) {
+  TrP p;
+  int64_t ss[4], run = 1;
+  for(int i = 3; i >= 0; --i) {
+    ss[i] = run;
+    run *= sd[i];
+  }
+  p.n = run;
+  for(int i = 0; i < 4; ++i) {
+    p.od[i] = sd[perm[i]];
+    p.ss[i] = ss[perm[i]];
+  }
+  p.out = out;
+  p.src = src;
+  p.acc = accumulate;
+  if(p.n <= 0)
+    return MTKC_OK;
+  transpose_kernel<<<grid1d(p.n, 256), 256, 0, S(stream)>>>(p);
+  MTKC_POST_LAUNCH("transpose_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_copy_blocks(float* dst, int64_t dst_stride, int64_t dst_off, const float* src,
+                     int64_t src_stride, int64_t src_off, int64_t outer, int64_t len,
+                     int accumulate, void* stream) {
+  if(outer * len <= 0)
+    return MTKC_OK;
+  copy_blocks_kernel<<<grid1d(outer * len, 256), 256, 0, S(stream)>>>(
+      dst, dst_stride, dst_off, src, src_stride, src_off, outer, len, accumulate);
+  MTKC_POST_LAUNCH("copy_blocks_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_gather_rows(float* out, const float* src, const int32_t* rows, int64_t n,
+                     int64_t cols, int64_t src_rows, int* flags, void* stream) {
+  if(n * cols <= 0)
+    return MTKC_OK;
+  gather_rows_kernel<<<grid1d(n * cols, 256), 256, 0, S(stream)>>>(out, src, rows, n, cols,
+                                                                  src_rows, flags);
+  MTKC_POST_LAUNCH("gather_rows_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_scatter_add_rows(float* out, const float* src, const int32_t* perm,
+                          const int32_t* seg_start, const int32_t* uniq, int64_t n_uniq,
+                          int64_t cols, float scale, void* stream) {
+  if(n_uniq <= 0 || cols <= 0)
+    return MTKC_OK;
+  int threads = cols >= 256 ? 256 : (int)((cols + 31) / 32 * 32);
+  scatter_add_kernel<<<(unsigned)n_uniq, threads, 0, S(stream)>>>(out, src, perm, seg_start,
+                                                                  uniq, cols, scale);
+  MTKC_POST_LAUNCH("scatter_add_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_embed(float* out, const float* table, const int32_t* ids, int64_t n, int64_t e,
+               int64_t vocab, float s, const float* pe, int64_t t, int* flags, void* stream) {
+  if(n * e <= 0)
+    return MTKC_OK;
+  if(t <= 0)
+    t = 1;
+  bool vec = e % 4 == 0 && (uintptr_t)out % 16 == 0 && (uintptr_t)table % 16 == 0 &&
+             (!pe || (uintptr_t)pe % 16 == 0);
+  if(vec)
+    embed4_kernel<<<grid1d(n * e / 4, 256), 256, 0, S(stream)>>>(
+        (float4*)out, (const float4*)table, ids, n, e / 4, vocab, s, (const float4*)pe, t, flags);
+  else
+    embed_kernel<<<grid1d(n * e, 256), 256, 0, S(stream)>>>(out, table, ids, n, e, vocab, s, pe,
+                                                           t, flags);
+  MTKC_POST_LAUNCH("embed_kernel");
+  return MTKC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+// Fused softmax + cross-entropy over the vocabulary (crossEntropy
+// graph.cpp:859-924) and the fused Adam + EMA + grad-zero update
+// (Adam::updateTensor train.cpp:30-47, Adam::update :49-59,
+// AveragedParameters::update :69-79).
+//
+// Cross-entropy never materialises probabilities: the forward keeps only the
+// per-row max and sum of exp(x - max) (8 bytes per row instead of the
+// reference's [N x V] probs cache, graph.cpp:882-897); the backward
+// recomputes p = exp(x - max)/sum in the same order as the reference and
+// writes the logits gradient in one pass: 2*4*N*V bytes of HBM per step.
+#include "common.cuh"
+
+using namespace mtkc;
+
+namespace {
+
+constexpr int XT = 512;
+
+// stats[r] = {max, sum}; row_loss[r] = m*(max + log(sum) - x[y]) or 0
+__global__ void __launch_bounds__(XT) xent_fwd_kernel(const float* logits, const int32_t* tg,
+                                                      const float* mask, int64_t V,
+                                                      float* stats, float* rowLoss) {
+  __shared__ float red[32];
+  int64_t r = blockIdx.x;
+  const float* x = logits + r * V;
+  float mx = -INFINITY;
+  if(V % 4 == 0 && ((uintptr_t)x % 16 == 0)) {
+    const float4* x4 = (const float4*)x;
+    for(int64_t j = threadIdx.x; j < V / 4; j += XT) {
+      float4 v = x4[j];
+      mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    }
+  } else {
+    for(int64_t j = threadIdx.x; j < V; j += XT)
+      mx = fmaxf(mx, x[j]);
+  }
+  mx = block_max(mx, red);
+  float s = 0.f;
+  if(V % 4 == 0 && ((uintptr_t)x % 16 == 0)) {
+    const float4* x4 = (const float4*)x;
+    for(int64_t j = threadIdx.x; j < V / 4; j += XT) {
+      float4 v = x4[j];
+      s += expf(v.x - mx) + expf(v.y - mx) + expf(v.z - mx) + expf(v.w - mx);
+    }
+  } else {
+    for(int64_t j = threadIdx.x; j < V; j += XT)
+      s += expf(x[j] - mx);
+  }
+  s = block_sum(s, red);
+  if(threadIdx.x == 0) {
+    stats[2 * r] = mx;
+    stats[2 * r + 1] = s;
+    float m = mask ? mask[r] : 1.f;
+    float l = 0.f;
+    if(m != 0.f) {
+      float lse = mx + logf(s);
+      l = m * (lse - x[tg[r]]);
+    }
+    rowLoss[r] = l;
+  }
+}
+
+// loss = sum(row_loss)/count, fixed-order block reduction
+__global__ void __launch_bounds__(1024) loss_sum_kernel(const float* rowLoss, int64_t rows,
+                                                        float count, float* loss) {
+  __shared__ float red[32];
+  float s = 0.f;
+  for(int64_t r = threadIdx.x; r < rows; r += blockDim.x)
+    s += rowLoss[r];
+  s = block_sum(s, red);
+  if(threadIdx.x == 0)
+    loss[0] = s / count;
+}
+
+// g[r,j] (+)= (go*m)*p_j, then g[r,y] -= go*m  (graph.cpp:909-922)
+__global__ void __launch_bounds__(256) xent_bwd_kernel(float* g, const float* logits,
+                                                       const float* stats, const int32_t* tg,
+                                                       const float* mask, const float* gloss,
+                                                       int64_t rows, int64_t V, float count,
+                                                       int acc) {
+  int64_t r = blockIdx.y;
+  float go = gloss[0] / count;
+  float m = mask ? mask[r] : 1.f;
+  float gm = go * m;
+  float mx = stats[2 * r], sum = stats[2 * r + 1];
+  int32_t y = tg[r];
+  const float* x = logits + r * V;
+  float* gr = g + r * V;
+  int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  bool vec = V % 4 == 0 && ((uintptr_t)x % 16 == 0) && ((uintptr_t)gr % 16 == 0);
+  for(int64_t j = j0; j < V; j += stride) {
+    if(vec) {
+      float4 xv = *(const float4*)(x + j);
+      float4 o = acc ? *(float4*)(gr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+      float os[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for(int u = 0; u < 4; ++u) {
+        if(m != 0.f) {
+          float p = expf(xs[u] - mx) / sum;
+          float t = os[u] + gm * p;
+          if(j + u == y)
+            t = t - gm;
+          os[u] = t;
+        }
+      }
+      *(float4*)(gr + j) = make_float4(os[0], os[1], os[2], os[3]);
+    } else {
+      for(int u = 0; u < 4 && j + u < V; ++u) {
+        float t = acc ? gr[j + u] : 0.f;
+        if(m != 0.f) {
+          float p = expf(x[j + u] - mx) / sum;
+          t = t + gm * p;
+          if(j + u == y)
+            t = t - gm;
+        }
+        gr[j + u] = t;
+      }
+    }
+  }
+}
+
+// One element of the reference's Adam + EMA, with separately rounded ops
+// (kernels are compiled with -fmad=false) in the reference's order.
+__device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v, float& a,
+                                         float lr, float b1, float b2, float eps, float c1,
+                                         float c2, float ab, int doAvg, int zg) {
+  float gv = g;
+  m = b1 * m + (1.f - b1) * gv;
+  v = b2 * v + (1.f - b2) * gv * gv;
+  float mh = m / c1;
+  float vh = v / c2;
+  th = th - lr * mh / (sqrtf(vh) + eps);
+  if(doAvg)
+    a = ab * a + (1.f - ab) * th;
+  if(zg)
+    g = 0.f;
+}
+
+__global__ void adam_ema_kernel(float* th, float* g, float* m, float* v, float* a, int64_t n,
+                                float lr, float b1, float b2, float eps, float c1, float c2,
+                                float ab, int doAvg, int zg, const int* flags) {
+  if(flags && (*flags & MTKC_FLAG_NONFINITE))
+    return;  // all-or-nothing (train.cpp:51-53)
+  int64_t n4 = n / 4;
+  float4* th4 = (float4*)th;
+  float4* g4 = (float4*)g;
+  float4* m4 = (float4*)m;
+  float4* v4 = (float4*)v;
+  float4* a4 = (float4*)a;
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    float4 T = th4[i], G = g4[i], M = m4[i], Vv = v4[i];
+    float4 A = doAvg ? a4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    adam_one(T.x, G.x, M.x, Vv.x, A.x, lr, b1, b2, eps, c1, c2, ab, doAvg, zg);
+    adam_one(T.y, G.y, M.y, Vv.y, A.y, lr, b1, b2, eps, c1, c2, ab, doAvg, zg);
+    adam_one(T.z, G.z, M.z, Vv.z, A.z, lr, b1, b2, eps, c1, c2, ab, doAvg, zg);
+    adam_one(T.w, G.w, M.w, Vv.w, A.w, lr, b1, b2, eps, c1, c2, ab, doAvg, zg);
+    th4[i] = T;
+    m4[i] = M;
+    v4[i] = Vv;
+    if(zg)
+      g4[i] = G;
+    if(doAvg)
+      a4[i] = A;
+  }
+  for(int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    float dummy = 0.f;
+    adam_one(th[i], g[i], m[i], v[i], doAvg ? a[i] : dummy, lr, b1, b2, eps, c1, c2, ab, doAvg,
+             zg);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int mtkc_xent_forward(const float* logits, const int32_t* targets, const float* mask,
+                      int64_t rows, int64_t vocab, float* lse, float* row_loss, float* loss,
+                      float count, void* stream) {
+  if(rows <= 0)
+    return MTKC_OK;
+  xent_fwd_kernel<<<(unsigned)rows, XT, 0, S(stream)>>>(logits, targets, mask, vocab, lse,
+                                                       row_loss);
+  MTKC_POST_LAUNCH("xent_fwd_kernel");
+  loss_sum_kernel<<<1, 1024, 0, S(stream)>>>(row_loss, rows, count, loss);
+  MTKC_POST_LAUNCH("loss_sum_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_xent_backward(float* glogits, const float* logits, const float* lse,
+                       const int32_t* targets, const float* mask, const float* gloss,
+                       int64_t rows, int64_t vocab, float count, int accumulate,
+                       void* stream) {
+  if(rows <= 0)
+    return MTKC_OK;
+  int64_t per = cdiv(vocab, 4);
+  unsigned gx = (unsigned)std::min<int64_t>(cdiv(per, 256), 8);
+  dim3 grid(gx, (unsigned)rows);
+  xent_bwd_kernel<<<grid, 256, 0, S(stream)>>>(glogits, logits, lse, targets, mask, gloss, rows,
+                                              vocab, count, accumulate);
+  MTKC_POST_LAUNCH("xent_bwd_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_adam_ema(float* theta, float* grad, float* m, float* v, float* avg, int64_t n,
+                  float lr, float beta1, float beta2, float eps, float corr1, float corr2,
+                  float avg_beta, int do_avg, int zero_grad, const int* flags, void* stream) {
+  if(n <= 0)
+    return MTKC_OK;
+  if(((uintptr_t)theta | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v |
+      (do_avg ? (uintptr_t)avg : 0)) % 16)
+    return fail(MTKC_CONTRACT, "adam: buffers must be 16-byte aligned");
+  adam_ema_kernel<<<grid1d(cdiv(n, 4), 256, 148 * 16), 256, 0, S(stream)>>>(
+      theta, grad, m, v, avg, n, lr, beta1, beta2, eps, corr1, corr2, avg_beta, do_avg,
+      zero_grad, flags);
+  MTKC_POST_LAUNCH("adam_ema_kernel");
+  return MTKC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+"""GEMM parity: the C-ABI mtkc_gemm against the reference's matmulInto
+(tensor.cpp:258-306) run from oracle/_ref, for every transpose case.
+
+* FP32 (CUDA-core) path: bit-exact with the reference (same summation order,
+  separately rounded multiply/add).
+* TF32 tcgen05 path: |C - C64| <= 4e-3 * (|A||B|)_ij  (tf32 has a 10-bit
+  mantissa; the bound is on the absolute-value product, so it holds for any
+  cancellation pattern).
+"""
+import numpy as np
+import pytest
+
+from oracle import refbind as R
+from paper_1804_00344_b200 import cabi
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def _run(torch, a, b, ta, tb, alpha=1.0, beta=0.0, c0=None, precision=0, bias=None, relu=False):
+    M = a.shape[1] if ta else a.shape[0]
+    K = a.shape[0] if ta else a.shape[1]
+    N = b.shape[0] if tb else b.shape[1]
+    A, B = _dev(torch, a), _dev(torch, b)
+    Cd = _dev(torch, c0 if c0 is not None else np.zeros((M, N), np.float32))
+    bd = _dev(torch, bias) if bias is not None else None
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    path = cabi.gemm(M, N, K, A.data_ptr(), a.shape[1], B.data_ptr(), b.shape[1], Cd.data_ptr(), N,
+                     trans_a=ta, trans_b=tb, alpha=alpha, beta=beta,
+                     bias=bd.data_ptr() if bd is not None else None, relu=relu,
+                     precision=precision, workspace=ws.data_ptr(), workspace_bytes=ws.numel())
+    torch.cuda.synchronize()
+    return Cd.cpu().numpy(), path
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("shape", [(7, 5, 3), (64, 48, 80), (130, 70, 33)])
+def test_fp32_gemm_bitexact_vs_reference(cuda, ta, tb, shape):
+    import torch
+    rng = np.random.default_rng(1)
+    M, K, N = shape
+    a = rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+    c0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    for alpha, beta in [(1.0, 0.0), (1.0, 1.0), (0.5, 2.0)]:
+        ref = R.matmul(a, b, bool(ta), bool(tb), alpha, beta, c0)
+        got, path = _run(torch, a, b, ta, tb, alpha, beta, c0, precision=0)
+        assert path == 0
+        assert np.array_equal(got, ref), f"max diff {np.abs(got - ref).max()}"
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("shape", [(128, 64, 128), (256, 512, 384), (300, 520, 200),
+                                   (1024, 4096, 512), (512, 8192, 512)])
+def test_tf32_tcgen05_gemm(cuda, ta, tb, shape):
+    import torch
+    rng = np.random.default_rng(2)
+    M, K, N = shape
+    a = rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+    opa = a.T if ta else a
+    opb = b.T if tb else b
+    exact = opa.astype(np.float64) @ opb.astype(np.float64)
+    bound = np.abs(opa).astype(np.float64) @ np.abs(opb).astype(np.float64)
+    got, path = _run(torch, a, b, ta, tb, precision=1)
+    assert path == 1, "tensor-core path not taken"
+    err = np.abs(got - exact)
+    assert np.all(err <= 4e-3 * bound + 1e-6), f"max rel {np.max(err / (bound + 1e-9))}"
+
+
+def test_tf32_epilogues(cuda):
+    import torch
+    rng = np.random.default_rng(3)
+    M, K, N = 256, 256, 384
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    c0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    exact = a.astype(np.float64) @ b.astype(np.float64)
+    bound = np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64) + 1
+    got, _ = _run(torch, a, b, 0, 0, precision=1, bias=bias, relu=True)
+    want = np.maximum(exact + bias, 0)
+    assert np.all(np.abs(got - want) <= 4e-3 * bound)
+    got, _ = _run(torch, a, b, 0, 0, alpha=0.5, beta=1.0, c0=c0, precision=1)
+    want = 0.5 * exact + c0
+    assert np.all(np.abs(got - want) <= 4e-3 * bound)
