@@ -156,6 +156,12 @@ int mtkc_axpy(float* out, const float* a, float alpha, int64_t n, void* stream);
 int mtkc_accumulate_reduced(float* out, const int64_t od[4], const float* src,
                             const int64_t sd[4], void* stream);
 int mtkc_fill(float* out, float v, int64_t n, void* stream);
+/* out[i] = s*x[i] + c[i % period]  (addPositionalEncoding layers.cpp:175-179:
+ * scale(x, sqrt(e)) + PE broadcast over the batch) */
+int mtkc_scale_add_periodic(float* out, const float* x, float s, const float* c, int64_t n,
+                            int64_t period, void* stream);
+/* gx = gx*(gate > 0): ReLU backward applied to an accumulated gradient */
+int mtkc_relu_mask(float* gx, const float* gate, int64_t n, void* stream);
 /* out = a*m + b*(1-m), m broadcast over cols: RNN padding blend
  * (models.cpp:170-172, 360-364) fused */
 int mtkc_mask_blend(float* out, const float* a, const float* b, const float* m, int64_t rows,
@@ -275,6 +281,8 @@ int mtkc_xent_backward(float* glogits, const float* logits, const float* lse,
 int mtkc_adam_ema(float* theta, float* grad, float* m, float* v, float* avg, int64_t n,
                   float lr, float beta1, float beta2, float eps, float corr1, float corr2,
                   float avg_beta, int do_avg, int zero_grad, const int* flags, void* stream);
+/* avg = beta*avg + (1-beta)*theta (AveragedParameters::update train.cpp:69-79) */
+int mtkc_ema(float* avg, const float* theta, int64_t n, float beta, void* stream);
 
 /* ======================================================================== */
 /* data-parallel gradient exchange (trainSync train.cpp:254-269): NCCL       */

@@ -1,0 +1,1300 @@
+// Expression graph over device tensors (reference: src/graph.cpp).  Every
+// op's forward/backward closure launches kernels from libmtkcuda.so on the
+// device stream; see mtk/graph.h for the B200-specific execution model.
+#include "mtk/graph.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "mtk/device.h"
+
+namespace mtk {
+
+// ----------------------------------------------------------------- refs
+
+Tensor& NodeRef::val() const {
+  if(!graph)
+    throw ContractError("empty node reference");
+  return graph->nodeValue(index, gen);
+}
+
+Tensor& NodeRef::grad() const {
+  if(!graph)
+    throw ContractError("empty node reference");
+  return graph->nodeGrad(index, gen);
+}
+
+// ---------------------------------------------------------------- inits
+// Host-side, bit-identical to the reference (graph.cpp:23-63): same RNG
+// stream per parameter, same distribution calls.
+
+namespace inits {
+
+ParamInit zeros() {
+  return [](Tensor& t, Rng&) { t.setZero(); };
+}
+
+ParamInit ones() {
+  return [](Tensor& t, Rng&) { t.fill(1); };
+}
+
+ParamInit constant(Real v) {
+  return [v](Tensor& t, Rng&) { t.fill(v); };
+}
+
+ParamInit glorotUniform() {
+  return [](Tensor& t, Rng& rng) {
+    int rank = t.shape().rank();
+    Real fanIn = (Real)t.shape()[rank - 1];
+    Real fanOut = rank >= 2 ? (Real)t.shape()[rank - 2] : fanIn;
+    Real limit = std::sqrt(Real(6) / (fanIn + fanOut));
+    std::uniform_real_distribution<double> d(-(double)limit, (double)limit);
+    Real* p = t.data();
+    for(int64_t i = 0; i < t.size(); ++i)
+      p[i] = (Real)d(rng);
+  };
+}
+
+ParamInit uniform(Real lo, Real hi) {
+  return [lo, hi](Tensor& t, Rng& rng) {
+    std::uniform_real_distribution<double> d((double)lo, (double)hi);
+    Real* p = t.data();
+    for(int64_t i = 0; i < t.size(); ++i)
+      p[i] = (Real)d(rng);
+  };
+}
+
+ParamInit fromVector(std::vector<Real> v) {
+  return [v = std::move(v)](Tensor& t, Rng&) {
+    if((int64_t)v.size() != t.size())
+      throw DimensionError("init vector length mismatch");
+    std::copy(v.begin(), v.end(), t.data());
+  };
+}
+
+}  // namespace inits
+
+// ------------------------------------------------------------ ParamPool
+
+ParamPool::ParamPool() = default;
+
+void ParamPool::grow(int64_t need) {
+  int64_t cap = values_ ? (int64_t)values_->elems : 0;
+  if(need <= cap)
+    return;
+  int64_t ncap = std::max<int64_t>(need, std::max<int64_t>(cap * 2, 1 << 20));
+  Device& d = Device::get();
+  auto swapIn = [&](std::shared_ptr<DeviceBuffer>& buf) {
+    DeviceBuffer fresh((size_t)ncap);
+    MTKC(mtkc_memset(fresh.ptr, 0, (size_t)ncap * sizeof(float), d.stream()));
+    if(buf && used_ > 0)
+      MTKC(mtkc_memcpy_d2d(fresh.ptr, buf->ptr, (size_t)used_ * sizeof(float), d.stream()));
+    d.sync();
+    if(!buf) {
+      buf = std::make_shared<DeviceBuffer>();
+      buf->owned = true;
+    } else if(buf->ptr) {
+      mtkc_free(buf->ptr);
+    }
+    // move the allocation into the long-lived buffer object so every view follows
+    buf->ptr = fresh.ptr;
+    buf->elems = (size_t)ncap;
+    fresh.ptr = nullptr;
+  };
+  swapIn(values_);
+  swapIn(grads_);
+}
+
+int64_t ParamPool::reserve(int64_t elems) {
+  int64_t off = used_;
+  int64_t n = (elems + 63) & ~(int64_t)63;
+  grow(used_ + n);
+  used_ += n;
+  return off;
+}
+
+// ------------------------------------------------------------ the graph
+
+ExpressionGraph::ExpressionGraph(uint64_t seed, bool inference)
+    : rng_(seed), seed_(seed), inference_(inference) {
+  const char* e = std::getenv("MTK_CHECK_FINITE");
+  checkFinite_ = e && e[0] == '1';
+}
+
+void ExpressionGraph::checkRef(const NodeRef& r) const {
+  if(r.graph != this)
+    throw ContractError("node reference belongs to a different graph");
+  if(r.gen != generation_)
+    throw ContractError("stale node reference (graph was cleared)");
+  if(r.index < 0 || (size_t)r.index >= nodes_.size())
+    throw ContractError("node index out of range");
+}
+
+int ExpressionGraph::resolve(int i) const {
+  while(nodes_[(size_t)i].alias >= 0)
+    i = nodes_[(size_t)i].alias;
+  return i;
+}
+
+Tensor& ExpressionGraph::nodeValue(int index, uint64_t gen) {
+  if(gen != generation_)
+    throw ContractError("stale node reference (graph was cleared)");
+  Tensor& v = nodes_[(size_t)index].value;
+  if(v.empty())
+    throw ContractError("node value not computed; call forward() first");
+  return v;
+}
+
+Tensor& ExpressionGraph::nodeGrad(int index, uint64_t gen) {
+  if(gen != generation_)
+    throw ContractError("stale node reference (graph was cleared)");
+  Node& n = nodes_[(size_t)index];
+  int r = resolve(index);
+  Node& root = nodes_[(size_t)r];
+  if(root.isParam) {
+    Param& p = paramOf(root);
+    if(!p.gradLive) {
+      p.grad.setZero();
+      p.gradLive = true;
+    }
+    if(r != index)
+      n.grad = p.grad.reshaped(n.shape);
+    else
+      n.grad = p.grad;
+    return n.grad;
+  }
+  if(root.grad.empty())
+    throw ContractError("node gradient not available; call backward() first");
+  if(!root.gradLive) {
+    root.grad.setZero();
+    root.gradLive = true;
+  }
+  gradSrc(root);  // apply a pending ReLU mask
+  if(r != index)
+    n.grad = root.grad.reshaped(n.shape);
+  return n.grad;
+}
+
+NodeRef ExpressionGraph::addNode(Node n) {
+  nodes_.push_back(std::move(n));
+  return NodeRef{this, (int)nodes_.size() - 1, generation_, nodes_.back().shape};
+}
+
+Tensor ExpressionGraph::allocTensor(const Shape& s) {
+  auto [buf, off] = arena_.alloc(s.size());
+  return Tensor(s, buf, off);
+}
+
+ExpressionGraph::Param& ExpressionGraph::paramOf(Node& n) { return params_.at(n.paramName); }
+
+ExpressionGraph::GradDst ExpressionGraph::gradDst(int nodeIndex, bool supportsGate) {
+  int r = resolve(nodeIndex);
+  Node& n = nodes_[(size_t)r];
+  if(n.isParam) {
+    Param& p = paramOf(n);
+    int acc = p.gradLive ? 1 : 0;
+    p.gradLive = true;
+    return {p.grad.dev(), acc, nullptr};
+  }
+  if(n.grad.empty())
+    n.grad = allocTensor(n.shape);
+  int acc = n.gradLive ? 1 : 0;
+  n.gradLive = true;
+  if(n.gate && !supportsGate)
+    n.gradGated = false;
+  return {n.grad.dev(), acc, supportsGate ? n.gate : nullptr};
+}
+
+const float* ExpressionGraph::gradSrc(Node& n) {
+  if(n.gate && !n.gradGated) {
+    MTKC(mtkc_relu_mask(n.grad.dev(), n.gate, n.grad.size(), Device::get().stream()));
+    n.gradGated = true;
+  }
+  return n.grad.devc();
+}
+
+namespace {
+
+void* stream() { return Device::get().stream(); }
+
+// destination pointer with "+=" semantics: zero-fills a fresh buffer
+float* accPtr(ExpressionGraph& g, int idx, int64_t elems) {
+  auto d = g.gradDst(idx);
+  if(!d.accumulate)
+    MTKC(mtkc_memset(d.ptr, 0, (size_t)elems * sizeof(float), stream()));
+  return d.ptr;
+}
+
+void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA, const float* B,
+          int64_t ldb, bool tB, float* C, int64_t ldc, float beta, const float* bias = nullptr,
+          int epi = MTKC_EPI_NONE, const float* gate = nullptr, int64_t batch = 1,
+          int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
+  Device& d = Device::get();
+  mtkc_gemm_args g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.batch = batch;
+  g.A = A;
+  g.lda = lda;
+  g.strideA = sA;
+  g.transA = tA;
+  g.B = B;
+  g.ldb = ldb;
+  g.strideB = sB;
+  g.transB = tB;
+  g.C = C;
+  g.ldc = ldc;
+  g.strideC = sC;
+  g.alpha = 1.f;
+  g.beta = beta;
+  g.bias = bias;
+  g.epilogue = epi;
+  g.gate = gate;
+  g.precision = (int)d.precision();
+  g.workspace = d.scratch(64 << 20);
+  g.workspace_bytes = d.scratchBytes();
+  MTKC(mtkc_gemm(&g, d.stream()));
+}
+
+std::shared_ptr<DeviceBuffer> uploadIntsTo(ExpressionGraph& g, const std::vector<int32_t>& v,
+                                           int64_t* off) {
+  auto [buf, o] = g.arena().alloc(std::max<int64_t>((int64_t)v.size(), 1));
+  MTKC(mtkc_memcpy_h2d(buf->ptr + o, v.data(), v.size() * sizeof(int32_t), stream()));
+  *off = o;
+  return buf;
+}
+
+// device copy of a host tensor in the arena
+Tensor uploadTensor(ExpressionGraph& g, const Tensor& t) {
+  Tensor d = g.allocTensor(t.shape());
+  if(t.onDevice())
+    MTKC(mtkc_memcpy_d2d(d.dev(), t.devc(), (size_t)t.size() * sizeof(float), stream()));
+  else
+    MTKC(mtkc_memcpy_h2d(d.dev(), t.data(), (size_t)t.size() * sizeof(float), stream()));
+  return d;
+}
+
+// Deterministic scatter plan: positions stably sorted by id.
+struct ScatterPlan {
+  std::shared_ptr<DeviceBuffer> buf;
+  int64_t permOff = 0, segOff = 0, uniqOff = 0, nUniq = 0;
+};
+
+ScatterPlan makeScatterPlan(ExpressionGraph& g, const std::vector<int32_t>& ids) {
+  std::vector<int32_t> perm(ids.size());
+  for(size_t i = 0; i < ids.size(); ++i)
+    perm[i] = (int32_t)i;
+  std::stable_sort(perm.begin(), perm.end(),
+                   [&](int32_t a, int32_t b) { return ids[(size_t)a] < ids[(size_t)b]; });
+  std::vector<int32_t> all;  // perm | seg | uniq
+  all.reserve(perm.size() * 3 + 1);
+  all.insert(all.end(), perm.begin(), perm.end());
+  std::vector<int32_t> seg, uniq;
+  for(size_t k = 0; k < perm.size(); ++k)
+    if(k == 0 || ids[(size_t)perm[k]] != ids[(size_t)perm[k - 1]]) {
+      seg.push_back((int32_t)k);
+      uniq.push_back(ids[(size_t)perm[k]]);
+    }
+  seg.push_back((int32_t)perm.size());
+  ScatterPlan p;
+  p.segOff = (int64_t)all.size();
+  all.insert(all.end(), seg.begin(), seg.end());
+  p.uniqOff = (int64_t)all.size();
+  all.insert(all.end(), uniq.begin(), uniq.end());
+  p.nUniq = (int64_t)uniq.size();
+  int64_t off = 0;
+  p.buf = uploadIntsTo(g, all, &off);
+  p.permOff = off;
+  p.segOff += off;
+  p.uniqOff += off;
+  return p;
+}
+
+void scatterPlanAdd(const ScatterPlan& p, float* out, const float* src, int64_t cols, float s) {
+  const int32_t* base = (const int32_t*)p.buf->ptr;
+  MTKC(mtkc_scatter_add_rows(out, src, base + p.permOff, base + p.segOff, base + p.uniqOff,
+                             p.nUniq, cols, s, stream()));
+}
+
+void pad4(const Shape& s, int64_t out[4]) { s.pad4(out); }
+
+}  // namespace
+
+// ---------------------------------------------------------------- leaves
+
+NodeRef ExpressionGraph::param(const std::string& name, const Shape& shape,
+                               const ParamInit& init) {
+  auto it = params_.find(name);
+  if(it == params_.end()) {
+    Param p;
+    p.offset = pool_.reserve(shape.size());
+    p.value = Tensor(shape, pool_.values(), p.offset);
+    p.grad = Tensor(shape, pool_.grads(), p.offset);
+    Tensor host(shape);
+    Rng prng(hash64(name) ^ seed_);
+    init(host, prng);
+    MTKC(mtkc_memcpy_h2d(p.value.dev(), host.data(), (size_t)shape.size() * sizeof(float),
+                         stream()));
+    Device::get().sync();  // host staging vector goes out of scope
+    it = params_.emplace(name, std::move(p)).first;
+    paramOrder_.push_back(name);
+  } else if(it->second.value.shape() != shape) {
+    throw ContractError("parameter " + name + " redefined with shape " + shape.str() + " (was " +
+                        it->second.value.shape().str() + ")");
+  }
+  Node n;
+  n.op = "param";
+  n.shape = shape;
+  n.isParam = true;
+  n.paramName = name;
+  n.value = it->second.value;
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::constant(const Tensor& t) {
+  Node n;
+  n.op = "const";
+  n.shape = t.shape();
+  n.value = uploadTensor(*this, t);
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::constant(Shape shape, std::vector<Real> values) {
+  return constant(Tensor(std::move(shape), std::move(values)));
+}
+
+// ----------------------------------------------------------- elementwise
+
+NodeRef ExpressionGraph::binary(const std::string& name, EwiseOp op, NodeRef a, NodeRef b) {
+  checkRef(a);
+  checkRef(b);
+  Node n;
+  n.op = name;
+  n.shape = broadcastShape(a.shape, b.shape);
+  n.inputs = {a.index, b.index};
+  n.fwd = [op](ExpressionGraph& g, Node& n) {
+    int64_t od[4], ad[4], bd[4];
+    pad4(n.shape, od);
+    pad4(g.node(n.inputs[0]).shape, ad);
+    pad4(g.node(n.inputs[1]).shape, bd);
+    MTKC(mtkc_ewise_binary((int)op, n.value.dev(), od, g.valPtr(n.inputs[0]), ad,
+                           g.valPtr(n.inputs[1]), bd, Device::get().flags(), stream()));
+  };
+  n.bwd = [op](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    int64_t od[4], ad[4], bd[4];
+    Shape sa = g.node(n.inputs[0]).shape, sb = g.node(n.inputs[1]).shape;
+    pad4(n.shape, od);
+    pad4(sa, ad);
+    pad4(sb, bd);
+    for(int which = 0; which < 2; ++which) {
+      const Shape& st = which == 0 ? sa : sb;
+      int idx = n.inputs[(size_t)which];
+      bool same = st == n.shape;
+      if(op == EwiseOp::Add && same) {
+        auto d = g.gradDst(idx);
+        if(d.accumulate)
+          MTKC(mtkc_axpy(d.ptr, go, 1.f, st.size(), stream()));
+        else
+          MTKC(mtkc_memcpy_d2d(d.ptr, go, (size_t)st.size() * sizeof(float), stream()));
+        continue;
+      }
+      float* dst = accPtr(g, idx, st.size());
+      MTKC(mtkc_binary_backward((int)op, which, dst, which == 0 ? ad : bd, go, od,
+                                g.valPtr(n.inputs[0]), ad, g.valPtr(n.inputs[1]), bd,
+                                n.value.devc(), stream()));
+    }
+  };
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::unary(const std::string& name, EwiseOp op, NodeRef a) {
+  checkRef(a);
+  Node n;
+  n.op = name;
+  n.shape = a.shape;
+  n.inputs = {a.index};
+  n.fwd = [op](ExpressionGraph& g, Node& n) {
+    MTKC(mtkc_ewise_unary((int)op, n.value.dev(), g.valPtr(n.inputs[0]), n.value.size(),
+                          stream()));
+  };
+  n.bwd = [op](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    float* dst = accPtr(g, n.inputs[0], n.shape.size());
+    MTKC(mtkc_unary_backward((int)op, dst, go, n.value.devc(), g.valPtr(n.inputs[0]),
+                             n.shape.size(), stream()));
+  };
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::add(NodeRef a, NodeRef b) { return binary("add", EwiseOp::Add, a, b); }
+NodeRef ExpressionGraph::sub(NodeRef a, NodeRef b) { return binary("sub", EwiseOp::Sub, a, b); }
+NodeRef ExpressionGraph::mul(NodeRef a, NodeRef b) { return binary("mul", EwiseOp::Mul, a, b); }
+NodeRef ExpressionGraph::div(NodeRef a, NodeRef b) { return binary("div", EwiseOp::Div, a, b); }
+NodeRef ExpressionGraph::tanh(NodeRef a) { return unary("tanh", EwiseOp::Tanh, a); }
+NodeRef ExpressionGraph::sigmoid(NodeRef a) { return unary("sigmoid", EwiseOp::Sigmoid, a); }
+NodeRef ExpressionGraph::relu(NodeRef a) { return unary("relu", EwiseOp::Relu, a); }
+NodeRef ExpressionGraph::exp(NodeRef a) { return unary("exp", EwiseOp::Exp, a); }
+NodeRef ExpressionGraph::log(NodeRef a) { return unary("log", EwiseOp::Log, a); }
+NodeRef ExpressionGraph::neg(NodeRef a) { return unary("neg", EwiseOp::Neg, a); }
+
+static NodeRef scaleShift(ExpressionGraph& g, const char* name, NodeRef a, Real s, Real c) {
+  g.checkRef(a);
+  ExpressionGraph::Node n;
+  n.op = name;
+  n.shape = a.shape;
+  n.inputs = {a.index};
+  n.fwd = [s, c](ExpressionGraph& g, ExpressionGraph::Node& n) {
+    MTKC(mtkc_scale_shift(n.value.dev(), g.valPtr(n.inputs[0]), s, c, n.value.size(), stream()));
+  };
+  n.bwd = [s](ExpressionGraph& g, ExpressionGraph::Node& n) {
+    const float* go = g.gradSrc(n);
+    auto d = g.gradDst(n.inputs[0]);
+    if(d.accumulate)
+      MTKC(mtkc_axpy(d.ptr, go, s, n.shape.size(), stream()));
+    else
+      MTKC(mtkc_scale_shift(d.ptr, go, s, 0.f, n.shape.size(), stream()));
+  };
+  return g.addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::scale(NodeRef a, Real s) { return scaleShift(*this, "scale", a, s, 0); }
+NodeRef ExpressionGraph::addScalar(NodeRef a, Real s) {
+  return scaleShift(*this, "addScalar", a, 1, s);
+}
+
+// -------------------------------------------------------- linear algebra
+
+namespace {
+struct MV {
+  int64_t batch, rows, cols, bstride, ld;
+};
+MV mview(const Shape& s, bool t) {
+  if(s.rank() == 2)
+    return {1, t ? s[1] : s[0], t ? s[0] : s[1], 0, s[1]};
+  return {s[0], t ? s[2] : s[1], t ? s[1] : s[2], s[1] * s[2], s[2]};
+}
+
+// dst (+)= op(x) op(y) with the reference's batching rules (graph.cpp:273-291):
+// a batched product accumulated into a rank-2 destination sums the batch.
+void gemmAccum(float* dst, int acc, const Shape& ds, const float* x, const Shape& xs, bool tx,
+               const float* y, const Shape& ys, bool ty) {
+  MV vx = mview(xs, tx), vy = mview(ys, ty);
+  int64_t M = vx.rows, K = vx.cols, N = vy.cols;
+  int64_t batch = std::max(vx.batch, vy.batch);
+  bool sumBatch = batch > 1 && ds.rank() == 2;
+  if(sumBatch && xs.rank() == 3 && ys.rank() == 3 && tx && !ty) {
+    // sum_b x_b^T y_b == X^T Y with the batch stacked along K
+    gemm(M, N, K * batch, x, xs[2], true, y, ys[2], false, dst, N, acc ? 1.f : 0.f);
+    return;
+  }
+  if(!sumBatch && ds.rank() == 3 && xs.rank() == 3 && ys.rank() == 2 && !tx) {
+    // [B,T,K] x op(y) into [B,T,N]: one GEMM over B*T rows
+    gemm(M * batch, N, K, x, vx.ld, false, y, vy.ld, ty, dst, N, acc ? 1.f : 0.f);
+    return;
+  }
+  gemm(M, N, K, x, vx.ld, tx, y, vy.ld, ty, dst, N, acc ? 1.f : 0.f, nullptr, MTKC_EPI_NONE,
+       nullptr, batch, vx.batch == 1 ? 0 : vx.bstride, vy.batch == 1 ? 0 : vy.bstride,
+       sumBatch ? 0 : M * N);
+}
+}  // namespace
+
+NodeRef ExpressionGraph::dot(NodeRef a, NodeRef b, bool transA, bool transB) {
+  checkRef(a);
+  checkRef(b);
+  auto opRows = [](const Shape& s, bool t) { return t ? s.back() : s[s.rank() - 2]; };
+  auto opCols = [](const Shape& s, bool t) { return t ? s[s.rank() - 2] : s.back(); };
+  if(a.shape.rank() < 2 || b.shape.rank() < 2)
+    throw DimensionError("matmul needs rank >= 2 operands: " + a.shape.str() + " x " +
+                         b.shape.str());
+  if(a.shape.rank() > 3 || b.shape.rank() > 3)
+    throw DimensionError("matmul operands must be rank 2 or 3, got " + a.shape.str() + " x " +
+                         b.shape.str());
+  if(opCols(a.shape, transA) != opRows(b.shape, transB))
+    throw DimensionError("matmul inner dims disagree: " + a.shape.str() + " x " +
+                         b.shape.str());
+  int64_t batchA = a.shape.rank() == 3 ? a.shape[0] : 1;
+  int64_t batchB = b.shape.rank() == 3 ? b.shape[0] : 1;
+  if(batchA != batchB && batchA != 1 && batchB != 1)
+    throw DimensionError("matmul batch dims disagree: " + a.shape.str() + " x " +
+                         b.shape.str());
+  Node n;
+  n.op = "matmul";
+  int64_t m = opRows(a.shape, transA), c = opCols(b.shape, transB);
+  n.shape = (a.shape.rank() == 3 || b.shape.rank() == 3)
+                ? Shape({std::max(batchA, batchB), m, c})
+                : Shape({m, c});
+  n.inputs = {a.index, b.index};
+  n.fwd = [transA, transB](ExpressionGraph& g, Node& n) {
+    const Shape& sa = g.node(n.inputs[0]).shape;
+    const Shape& sb = g.node(n.inputs[1]).shape;
+    MV va = mview(sa, transA), vb = mview(sb, transB);
+    int64_t batch = std::max(va.batch, vb.batch);
+    if(batch == 1 || (sa.rank() == 3 && sb.rank() == 2 && !transA)) {
+      // [B,T,K] x [K,N]: one GEMM over B*T rows
+      int64_t rows = va.rows * va.batch;
+      gemm(rows, vb.cols, va.cols, g.valPtr(n.inputs[0]), va.ld, transA, g.valPtr(n.inputs[1]),
+           vb.ld, transB, n.value.dev(), vb.cols, 0.f);
+      return;
+    }
+    gemm(va.rows, vb.cols, va.cols, g.valPtr(n.inputs[0]), va.ld, transA,
+         g.valPtr(n.inputs[1]), vb.ld, transB, n.value.dev(), vb.cols, 0.f, nullptr,
+         MTKC_EPI_NONE, nullptr, batch, va.batch == 1 ? 0 : va.bstride,
+         vb.batch == 1 ? 0 : vb.bstride, va.rows * vb.cols);
+  };
+  n.bwd = [transA, transB](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    Node& na = g.node(n.inputs[0]);
+    Node& nb = g.node(n.inputs[1]);
+    Shape sa = na.shape, sb = nb.shape, so = n.shape;
+    // graph.cpp:322-330
+    {
+      auto d = g.gradDst(n.inputs[0]);
+      if(!transA)
+        gemmAccum(d.ptr, d.accumulate, sa, go, so, false, g.valPtr(n.inputs[1]), sb, !transB);
+      else
+        gemmAccum(d.ptr, d.accumulate, sa, g.valPtr(n.inputs[1]), sb, transB, go, so, true);
+    }
+    {
+      auto d = g.gradDst(n.inputs[1]);
+      if(!transB)
+        gemmAccum(d.ptr, d.accumulate, sb, g.valPtr(n.inputs[0]), sa, !transA, go, so, false);
+      else
+        gemmAccum(d.ptr, d.accumulate, sb, go, so, true, g.valPtr(n.inputs[0]), sa, transA);
+    }
+  };
+  return addNode(std::move(n));
+}
+
+// Fused affine: out = x op(W) + b in one GEMM with a bias (and optional
+// ReLU) epilogue.  Backward: dX = dY op(W)^T (ReLU-gated epilogue into a
+// gated producer), dW = X^T dY or dY^T X, db = colsum(dY).
+static NodeRef affineImpl(ExpressionGraph& g, NodeRef x, NodeRef w, NodeRef b, bool transW,
+                          bool relu) {
+  g.checkRef(x);
+  g.checkRef(w);
+  g.checkRef(b);
+  if(x.shape.rank() < 2 || w.shape.rank() != 2)
+    throw DimensionError("matmul needs rank >= 2 operands: " + x.shape.str() + " x " +
+                         w.shape.str());
+  int64_t K = x.shape.back();
+  int64_t wr = transW ? w.shape[1] : w.shape[0];
+  int64_t N = transW ? w.shape[0] : w.shape[1];
+  if(K != wr)
+    throw DimensionError("matmul inner dims disagree: " + x.shape.str() + " x " +
+                         w.shape.str());
+  if(b.shape.size() != N)
+    throw DimensionError("shapes not broadcastable: bias " + b.shape.str() + " vs output width " +
+                         std::to_string(N));
+  std::vector<int64_t> dims = x.shape.dims();
+  dims.back() = N;
+  ExpressionGraph::Node n;
+  n.op = relu ? "affineRelu" : "affine";
+  n.shape = Shape(dims);
+  n.inputs = {x.index, w.index, b.index};
+  int64_t rows = x.shape.size() / K;
+  n.fwd = [rows, K, N, transW, relu](ExpressionGraph& g, ExpressionGraph::Node& n) {
+    gemm(rows, N, K, g.valPtr(n.inputs[0]), K, false, g.valPtr(n.inputs[1]), transW ? K : N,
+         transW, n.value.dev(), N, 0.f, g.valPtr(n.inputs[2]),
+         relu ? MTKC_EPI_RELU : MTKC_EPI_NONE);
+    if(relu)
+      n.gate = n.value.devc();
+  };
+  n.bwd = [rows, K, N, transW](ExpressionGraph& g, ExpressionGraph::Node& n) {
+    const float* go = g.gradSrc(n);
+    {  // dX = dY op(W)^T
+      auto d = g.gradDst(n.inputs[0], true);
+      gemm(rows, K, N, go, N, false, g.valPtr(n.inputs[1]), transW ? K : N, !transW, d.ptr, K,
+           d.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, d.gate);
+    }
+    {  // dW
+      auto d = g.gradDst(n.inputs[1]);
+      if(!transW)
+        gemm(K, N, rows, g.valPtr(n.inputs[0]), K, true, go, N, false, d.ptr, N,
+             d.accumulate ? 1.f : 0.f);
+      else
+        gemm(N, K, rows, go, N, true, g.valPtr(n.inputs[0]), K, false, d.ptr, K,
+             d.accumulate ? 1.f : 0.f);
+    }
+    {  // db
+      auto d = g.gradDst(n.inputs[2]);
+      Device& dev = Device::get();
+      size_t ws = (size_t)((rows + 127) / 128) * (size_t)N * sizeof(float);
+      float* w = dev.scratch(ws);
+      MTKC(mtkc_colsum(d.ptr, go, rows, N, d.accumulate, w, dev.scratchBytes(), dev.stream()));
+    }
+  };
+  return g.addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::affine(NodeRef x, NodeRef w, NodeRef b, bool transW) {
+  return affineImpl(*this, x, w, b, transW, false);
+}
+
+NodeRef ExpressionGraph::affineRelu(NodeRef x, NodeRef w, NodeRef b) {
+  return affineImpl(*this, x, w, b, false, true);
+}
+
+NodeRef ExpressionGraph::reshape(NodeRef a, Shape shape) {
+  checkRef(a);
+  if(shape.size() != a.shape.size())
+    throw DimensionError("reshape element count mismatch: " + a.shape.str() + " -> " +
+                         shape.str());
+  Node n;
+  n.op = "reshape";
+  n.shape = shape;
+  n.inputs = {a.index};
+  n.alias = a.index;  // value and gradient are views of the input
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::transpose(NodeRef a, std::vector<int> perm) {
+  checkRef(a);
+  if((int)perm.size() != a.shape.rank())
+    throw DimensionError("transpose perm rank mismatch");
+  std::vector<int64_t> dims;
+  for(int p : perm)
+    dims.push_back(a.shape[p]);
+  std::vector<int> inv((size_t)a.shape.rank());
+  for(int i = 0; i < (int)perm.size(); ++i)
+    inv[(size_t)perm[(size_t)i]] = i;
+  Node n;
+  n.op = "transpose";
+  n.shape = Shape(dims);
+  n.inputs = {a.index};
+  auto p4 = [](const Shape& s, const std::vector<int>& p, int out[4]) {
+    int off = 4 - s.rank();
+    for(int i = 0; i < 4; ++i)
+      out[i] = i;
+    for(int i = 0; i < s.rank(); ++i)
+      out[off + i] = off + p[(size_t)i];
+  };
+  n.fwd = [perm, p4](ExpressionGraph& g, Node& n) {
+    const Shape& s = g.node(n.inputs[0]).shape;
+    int64_t sd[4];
+    int pp[4];
+    pad4(s, sd);
+    p4(s, perm, pp);
+    MTKC(mtkc_transpose(n.value.dev(), g.valPtr(n.inputs[0]), sd, pp, 0, stream()));
+  };
+  n.bwd = [inv, p4](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    int64_t sd[4];
+    int pp[4];
+    pad4(n.shape, sd);
+    p4(n.shape, inv, pp);
+    auto d = g.gradDst(n.inputs[0]);
+    MTKC(mtkc_transpose(d.ptr, go, sd, pp, d.accumulate, stream()));
+  };
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::concat(const std::vector<NodeRef>& parts, int axis) {
+  if(parts.empty())
+    throw ContractError("concat of zero parts");
+  for(auto& p : parts)
+    checkRef(p);
+  std::vector<int64_t> dims = parts[0].shape.dims();
+  for(size_t i = 1; i < parts.size(); ++i) {
+    for(int d = 0; d < (int)dims.size(); ++d)
+      if(d != axis && parts[i].shape[d] != dims[(size_t)d])
+        throw DimensionError("concat shape mismatch on non-concat axis");
+    dims[(size_t)axis] += parts[i].shape[axis];
+  }
+  Node n;
+  n.op = "concat";
+  n.shape = Shape(dims);
+  for(auto& p : parts)
+    n.inputs.push_back(p.index);
+  int64_t outer = 1, inner = 1;
+  for(int i = 0; i < axis; ++i)
+    outer *= n.shape[i];
+  for(int i = axis + 1; i < n.shape.rank(); ++i)
+    inner *= n.shape[i];
+  int64_t total = n.shape[axis];
+  n.fwd = [axis, outer, inner, total](ExpressionGraph& g, Node& n) {
+    int64_t off = 0;
+    float* o = n.value.dev();
+    for(int i : n.inputs) {
+      int64_t pa = g.node(i).shape[axis];
+      MTKC(mtkc_copy_blocks(o, total * inner, off * inner, g.valPtr(i), pa * inner, 0, outer,
+                            pa * inner, 0, stream()));
+      off += pa;
+    }
+  };
+  n.bwd = [axis, outer, inner, total](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    int64_t off = 0;
+    for(int i : n.inputs) {
+      int64_t pa = g.node(i).shape[axis];
+      auto d = g.gradDst(i);
+      MTKC(mtkc_copy_blocks(d.ptr, pa * inner, 0, go, total * inner, off * inner, outer,
+                            pa * inner, d.accumulate, stream()));
+      off += pa;
+    }
+  };
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::slice(NodeRef a, int axis, int64_t start, int64_t len) {
+  checkRef(a);
+  if(axis < 0 || axis >= a.shape.rank() || start < 0 || len < 1 || start + len > a.shape[axis])
+    throw DimensionError("slice out of range for " + a.shape.str());
+  std::vector<int64_t> dims = a.shape.dims();
+  dims[(size_t)axis] = len;
+  Node n;
+  n.op = "slice";
+  n.shape = Shape(dims);
+  n.inputs = {a.index};
+  int64_t outer = 1, inner = 1;
+  for(int i = 0; i < axis; ++i)
+    outer *= a.shape[i];
+  for(int i = axis + 1; i < a.shape.rank(); ++i)
+    inner *= a.shape[i];
+  int64_t full = a.shape[axis];
+  n.fwd = [=](ExpressionGraph& g, Node& n) {
+    MTKC(mtkc_copy_blocks(n.value.dev(), len * inner, 0, g.valPtr(n.inputs[0]), full * inner,
+                          start * inner, outer, len * inner, 0, stream()));
+  };
+  n.bwd = [=](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    float* dst = accPtr(g, n.inputs[0], outer * full * inner);
+    MTKC(mtkc_copy_blocks(dst, full * inner, start * inner, go, len * inner, 0, outer,
+                          len * inner, 1, stream()));
+  };
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::gatherRows(NodeRef a, std::vector<int64_t> rows) {
+  checkRef(a);
+  std::vector<int64_t> dims = a.shape.dims();
+  dims[0] = (int64_t)rows.size();
+  std::vector<int32_t> r32(rows.size());
+  for(size_t i = 0; i < rows.size(); ++i) {
+    if(rows[i] < 0 || rows[i] >= a.shape[0])
+      throw ContractError("row index " + std::to_string(rows[i]) + " out of range 0.." +
+                          std::to_string(a.shape[0] - 1));
+    r32[i] = (int32_t)rows[i];
+  }
+  Node n;
+  n.op = "gatherRows";
+  n.shape = Shape(dims);
+  n.inputs = {a.index};
+  int64_t cols = a.shape.size() / a.shape[0];
+  int64_t srcRows = a.shape[0];
+  int64_t off = 0;
+  auto ids = uploadIntsTo(*this, r32, &off);
+  auto plan = std::make_shared<ScatterPlan>(makeScatterPlan(*this, r32));
+  n.aux = plan;
+  int64_t nr = (int64_t)rows.size();
+  n.fwd = [=](ExpressionGraph& g, Node& n) {
+    MTKC(mtkc_gather_rows(n.value.dev(), g.valPtr(n.inputs[0]), (const int32_t*)ids->ptr + off,
+                          nr, cols, srcRows, Device::get().flags(), stream()));
+  };
+  n.bwd = [=](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    float* dst = accPtr(g, n.inputs[0], srcRows * cols);
+    scatterPlanAdd(*plan, dst, go, cols, 1.f);
+  };
+  return addNode(std::move(n));
+}
+
+// -------------------------------------------- reductions / normalisation
+
+NodeRef ExpressionGraph::reduce(ReduceOp op, NodeRef a, int axis, bool keepAxis) {
+  checkRef(a);
+  if(axis < 0 || axis >= a.shape.rank())
+    throw DimensionError("reduce axis " + std::to_string(axis) + " out of range for " +
+                         a.shape.str());
+  std::vector<int64_t> dims;
+  for(int i = 0; i < a.shape.rank(); ++i) {
+    if(i == axis) {
+      if(keepAxis)
+        dims.push_back(1);
+    } else {
+      dims.push_back(a.shape[i]);
+    }
+  }
+  if(dims.empty())
+    dims.push_back(1);
+  Node n;
+  n.op = op == ReduceOp::Sum ? "sum" : op == ReduceOp::Mean ? "mean"
+                                     : op == ReduceOp::Max  ? "max"
+                                                            : "argmax";
+  n.shape = Shape(dims);
+  n.inputs = {a.index};
+  int64_t outer = 1, inner = 1, cnt = a.shape[axis];
+  for(int i = 0; i < axis; ++i)
+    outer *= a.shape[i];
+  for(int i = axis + 1; i < a.shape.rank(); ++i)
+    inner *= a.shape[i];
+  int64_t total = a.shape.size();
+  n.fwd = [=](ExpressionGraph& g, Node& n) {
+    MTKC(mtkc_reduce((int)op, n.value.dev(), g.valPtr(n.inputs[0]), outer, cnt, inner,
+                     stream()));
+  };
+  if(op != ReduceOp::Argmax) {
+    n.bwd = [=](ExpressionGraph& g, Node& n) {
+      const float* go = g.gradSrc(n);
+      float* dst = accPtr(g, n.inputs[0], total);
+      MTKC(mtkc_reduce_backward((int)op, dst, go, g.valPtr(n.inputs[0]), outer, cnt, inner,
+                                stream()));
+    };
+  }
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::softmax(NodeRef a, Tensor mask) {
+  checkRef(a);
+  Node n;
+  n.op = "softmax";
+  n.shape = a.shape;
+  n.inputs = {a.index};
+  Tensor dmask;
+  int64_t md[4] = {1, 1, 1, 1};
+  if(!mask.empty()) {
+    int64_t xd[4];
+    a.shape.pad4(xd);
+    mask.shape().pad4(md);
+    for(int i = 0; i < 4; ++i)
+      if(md[i] != 1 && md[i] != xd[i])
+        throw DimensionError("operand shape " + mask.shape().str() +
+                             " incompatible with broadcast result");
+    dmask = uploadTensor(*this, mask);
+  }
+  auto keep = std::make_shared<Tensor>(dmask);
+  n.aux = keep;
+  std::vector<int64_t> mdv(md, md + 4);
+  n.fwd = [keep, mdv](ExpressionGraph& g, Node& n) {
+    int64_t xd[4];
+    pad4(n.shape, xd);
+    Device& d = Device::get();
+    MTKC(mtkc_softmax(n.value.dev(), g.valPtr(n.inputs[0]), xd,
+                      keep->empty() ? nullptr : keep->devc(), mdv.data(), 0, d.flags(),
+                      d.stream()));
+  };
+  n.bwd = [](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    int64_t cols = n.shape.back(), rows = n.shape.size() / cols;
+    float* dst = accPtr(g, n.inputs[0], n.shape.size());
+    MTKC(mtkc_softmax_backward(dst, n.value.devc(), go, rows, cols, stream()));
+  };
+  return addNode(std::move(n));
+}
+
+namespace {
+struct LnCache {
+  Tensor invStd, xhat;
+};
+}  // namespace
+
+NodeRef ExpressionGraph::layerNorm(NodeRef x, NodeRef gain, NodeRef bias, Real eps) {
+  checkRef(x);
+  checkRef(gain);
+  checkRef(bias);
+  int64_t d = x.shape.back();
+  if(d < 2)
+    throw DimensionError("layer norm needs last extent >= 2, got " + x.shape.str());
+  if(gain.shape.size() != d || bias.shape.size() != d)
+    throw DimensionError("layer norm gain/bias must have length " + std::to_string(d));
+  Node n;
+  n.op = "layerNorm";
+  n.shape = x.shape;
+  n.inputs = {x.index, gain.index, bias.index};
+  auto cache = std::make_shared<LnCache>();
+  n.aux = cache;
+  int64_t rows = x.shape.size() / d;
+  n.fwd = [cache, eps, d, rows](ExpressionGraph& g, Node& n) {
+    cache->invStd = g.allocTensor(Shape({rows}));
+    cache->xhat = g.allocTensor(n.shape);
+    MTKC(mtkc_layernorm(n.value.dev(), g.valPtr(n.inputs[0]), g.valPtr(n.inputs[1]),
+                        g.valPtr(n.inputs[2]), eps, cache->invStd.dev(), cache->xhat.dev(), rows,
+                        d, stream()));
+  };
+  n.bwd = [cache, d, rows](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    auto dx = g.gradDst(n.inputs[0]);
+    auto dg = g.gradDst(n.inputs[1]);
+    auto db = g.gradDst(n.inputs[2]);
+    if(dg.accumulate != db.accumulate) {  // one flag for both parameter grads
+      MTKC(mtkc_memset(dg.accumulate ? db.ptr : dg.ptr, 0, (size_t)d * sizeof(float), stream()));
+      dg.accumulate = db.accumulate = 1;
+    }
+    Device& dev = Device::get();
+    size_t ws = (size_t)((rows + 63) / 64) * 2 * (size_t)d * sizeof(float);
+    float* w = dev.scratch(ws);
+    MTKC(mtkc_layernorm_backward(go, g.valPtr(n.inputs[1]), cache->invStd.devc(),
+                                 cache->xhat.devc(), dx.ptr, dg.ptr, db.ptr, rows, d,
+                                 dx.accumulate, dg.accumulate, w, dev.scratchBytes(),
+                                 dev.stream()));
+  };
+  return addNode(std::move(n));
+}
+
+// ---------------------------------------------------------------- embed
+
+namespace {
+struct EmbedAux {
+  std::shared_ptr<DeviceBuffer> ids;
+  int64_t off = 0;
+  ScatterPlan plan;
+};
+}  // namespace
+
+NodeRef ExpressionGraph::embed(NodeRef table, const IntMat& ids) {
+  checkRef(table);
+  if(table.shape.rank() != 2)
+    throw DimensionError("embedding table must be rank 2, got " + table.shape.str());
+  int64_t vocab = table.shape[0], e = table.shape[1];
+  for(int32_t id : ids.data)
+    if(id < 0 || id >= vocab)
+      throw DataError("token id " + std::to_string(id) + " out of vocabulary of size " +
+                      std::to_string(vocab));
+  Node n;
+  n.op = "embed";
+  n.shape = Shape({ids.rows, ids.cols, e});
+  n.inputs = {table.index};
+  auto aux = std::make_shared<EmbedAux>();
+  aux->ids = uploadIntsTo(*this, ids.data, &aux->off);
+  if(!inference_)
+    aux->plan = makeScatterPlan(*this, ids.data);
+  n.aux = aux;
+  int64_t cnt = ids.size();
+  n.fwd = [aux, cnt, e, vocab](ExpressionGraph& g, Node& n) {
+    MTKC(mtkc_embed(n.value.dev(), g.valPtr(n.inputs[0]), (const int32_t*)aux->ids->ptr + aux->off,
+                    cnt, e, vocab, 1.f, nullptr, 1, Device::get().flags(), stream()));
+  };
+  n.bwd = [aux, e, vocab](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    float* dst = accPtr(g, n.inputs[0], vocab * e);
+    scatterPlanAdd(aux->plan, dst, go, e, 1.f);
+  };
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::scaleAddConst(NodeRef x, Real s, const Tensor& pe) {
+  checkRef(x);
+  if(x.shape.size() % pe.size() != 0)
+    throw DimensionError("shapes not broadcastable: " + x.shape.str() + " vs " + pe.shape().str());
+  Node n;
+  n.op = "posenc";
+  n.shape = x.shape;
+  n.inputs = {x.index};
+  auto c = std::make_shared<Tensor>(uploadTensor(*this, pe));
+  n.aux = c;
+  int64_t period = pe.size();
+  n.fwd = [c, s, period](ExpressionGraph& g, Node& n) {
+    MTKC(mtkc_scale_add_periodic(n.value.dev(), g.valPtr(n.inputs[0]), s, c->devc(),
+                                 n.value.size(), period, stream()));
+  };
+  n.bwd = [s](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    auto d = g.gradDst(n.inputs[0]);
+    if(d.accumulate)
+      MTKC(mtkc_axpy(d.ptr, go, s, n.shape.size(), stream()));
+    else
+      MTKC(mtkc_scale_shift(d.ptr, go, s, 0.f, n.shape.size(), stream()));
+  };
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::maskBlend(NodeRef a, NodeRef b, const Tensor& m) {
+  checkRef(a);
+  checkRef(b);
+  if(a.shape != b.shape || a.shape.rank() != 2 || m.size() != a.shape[0])
+    throw DimensionError("maskBlend shapes: " + a.shape.str() + " " + b.shape.str() + " " +
+                         m.shape().str());
+  Node n;
+  n.op = "maskBlend";
+  n.shape = a.shape;
+  n.inputs = {a.index, b.index};
+  auto dm = std::make_shared<Tensor>(uploadTensor(*this, m));
+  n.aux = dm;
+  int64_t rows = a.shape[0], cols = a.shape[1];
+  n.fwd = [dm, rows, cols](ExpressionGraph& g, Node& n) {
+    MTKC(mtkc_mask_blend(n.value.dev(), g.valPtr(n.inputs[0]), g.valPtr(n.inputs[1]), dm->devc(),
+                         rows, cols, stream()));
+  };
+  n.bwd = [dm, rows, cols](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    auto da = g.gradDst(n.inputs[0]);
+    auto db = g.gradDst(n.inputs[1]);
+    MTKC(mtkc_mask_blend_backward(da.ptr, db.ptr, go, dm->devc(), rows, cols, da.accumulate,
+                                  db.accumulate, stream()));
+  };
+  return addNode(std::move(n));
+}
+
+// ------------------------------------------------------------ attention
+
+namespace {
+struct AttAux {
+  Tensor probs, mask;
+  bool hasMask = false;
+};
+}  // namespace
+
+NodeRef ExpressionGraph::attention(NodeRef q, NodeRef k, NodeRef v, const Tensor& keyMask,
+                                   bool causal, int heads) {
+  checkRef(q);
+  checkRef(k);
+  checkRef(v);
+  if(q.shape.rank() != 3 || k.shape.rank() != 3 || v.shape != k.shape)
+    throw DimensionError("attention expects q [b,tq,d], k/v [b,tk,d]");
+  int64_t b = q.shape[0], tq = q.shape[1], tk = k.shape[1], d = q.shape[2];
+  if(k.shape[0] != b || k.shape[2] != d)
+    throw DimensionError("attention q/k shapes disagree: " + q.shape.str() + " " + k.shape.str());
+  if(d % heads != 0)
+    throw DimensionError("model dim " + std::to_string(d) + " not divisible by heads " +
+                         std::to_string(heads));
+  int64_t dk = d / heads;
+  // fully-masked query rows raise like softmaxInto (tensor.cpp:424-425)
+  if(!keyMask.empty()) {
+    if(keyMask.size() != b * tk)
+      throw DimensionError("attention key mask must be [b x tk]");
+    const Real* m = keyMask.data();
+    for(int64_t bi = 0; bi < b; ++bi) {
+      int64_t first = -1;
+      for(int64_t j = 0; j < tk && first < 0; ++j)
+        if(m[bi * tk + j] != 0)
+          first = j;
+      if(first < 0 || (causal && first > tk - tq))
+        throw NumericError("softmax over a fully-masked row");
+    }
+  } else if(causal && tk < tq) {
+    throw NumericError("softmax over a fully-masked row");
+  }
+  Node n;
+  n.op = "attention";
+  n.shape = q.shape;
+  n.inputs = {q.index, k.index, v.index};
+  auto aux = std::make_shared<AttAux>();
+  if(!keyMask.empty()) {
+    aux->mask = uploadTensor(*this, keyMask);
+    aux->hasMask = true;
+  }
+  n.aux = aux;
+  float scale = (float)(1.0 / std::sqrt((double)dk));  // layers.cpp:106
+  n.fwd = [=](ExpressionGraph& g, Node& n) {
+    aux->probs = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));
+    MTKC(mtkc_attention(n.value.dev(), d, aux->probs.dev(), g.valPtr(n.inputs[0]), d,
+                        g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d,
+                        aux->hasMask ? aux->mask.devc() : nullptr, b, tq, tk, heads, dk, scale,
+                        causal ? 1 : 0, Device::get().flags(), stream()));
+  };
+  n.bwd = [=](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    Tensor ds = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));
+    auto dq = g.gradDst(n.inputs[0]);
+    auto dkk = g.gradDst(n.inputs[1]);
+    auto dv = g.gradDst(n.inputs[2]);
+    MTKC(mtkc_attention_backward(go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d,
+                                 g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d, dq.ptr, dkk.ptr,
+                                 dv.ptr, ds.dev(), b, tq, tk, heads, dk, scale, dq.accumulate,
+                                 dkk.accumulate, dv.accumulate, stream()));
+  };
+  return addNode(std::move(n));
+}
+
+// -------------------------------------------------------------- dropout
+
+NodeRef ExpressionGraph::dropoutMask(const Shape& shape, Real p) {
+  if(p >= Real(1) || p < Real(0))
+    throw ContractError("dropout probability must be in [0, 1)");
+  Tensor mask(shape);
+  if(inference_ || p == Real(0)) {
+    mask.fill(1);
+  } else {
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    Real keepInv = Real(1) / (Real(1) - p);
+    Real* m = mask.data();
+    for(int64_t i = 0; i < mask.size(); ++i)
+      m[i] = u(rng_) >= (double)p ? keepInv : Real(0);
+  }
+  return constant(mask);
+}
+
+NodeRef ExpressionGraph::dropout(NodeRef x, Real p, int variationalAxis) {
+  checkRef(x);
+  if(p >= Real(1) || p < Real(0))
+    throw ContractError("dropout probability must be in [0, 1)");
+  if(inference_ || p == Real(0))
+    return x;
+  std::vector<int64_t> dims = x.shape.dims();
+  if(variationalAxis >= 0) {
+    if(variationalAxis >= x.shape.rank())
+      throw ContractError("variational axis out of range");
+    dims[(size_t)variationalAxis] = 1;
+  }
+  NodeRef mask = dropoutMask(Shape(dims), p);
+  return mul(x, mask);
+}
+
+// -------------------------------------------------------- cross entropy
+
+namespace {
+struct CeAux {
+  std::shared_ptr<DeviceBuffer> tg;
+  int64_t tgOff = 0;
+  Tensor mask, stats, rowLoss;
+  bool hasMask = false;
+  Real count = 0;
+};
+}  // namespace
+
+NodeRef ExpressionGraph::crossEntropy(NodeRef logits, const IntMat& targets, const Tensor& mask) {
+  checkRef(logits);
+  int64_t vocab = logits.shape.back();
+  int64_t positions = logits.shape.size() / vocab;
+  if(targets.size() != positions)
+    throw DimensionError("cross entropy target count mismatch");
+  if(!mask.empty() && mask.size() != positions)
+    throw DimensionError("cross entropy mask count mismatch");
+  for(int32_t id : targets.data)
+    if(id < 0 || id >= vocab)
+      throw DataError("target id " + std::to_string(id) + " out of vocabulary of size " +
+                      std::to_string(vocab));
+  auto aux = std::make_shared<CeAux>();
+  aux->tg = uploadIntsTo(*this, targets.data, &aux->tgOff);
+  Real count = 0;
+  if(mask.empty()) {
+    count = (Real)positions;
+  } else {
+    const Real* m = mask.data();
+    for(int64_t r = 0; r < positions; ++r)  // graph.cpp:898-902 (sum of m in row order)
+      if(m[r] != Real(0))
+        count += m[r];
+    aux->mask = uploadTensor(*this, mask);
+    aux->hasMask = true;
+  }
+  aux->count = count;
+  Node n;
+  n.op = "crossEntropy";
+  n.shape = Shape({1});
+  n.inputs = {logits.index};
+  n.aux = aux;
+  n.fwd = [aux, vocab, positions](ExpressionGraph& g, Node& n) {
+    if(aux->count == Real(0))
+      throw ContractError("cross entropy over a fully-masked batch");
+    aux->stats = g.allocTensor(Shape({positions, 2}));
+    aux->rowLoss = g.allocTensor(Shape({positions}));
+    MTKC(mtkc_xent_forward(g.valPtr(n.inputs[0]), (const int32_t*)aux->tg->ptr + aux->tgOff,
+                           aux->hasMask ? aux->mask.devc() : nullptr, positions, vocab,
+                           aux->stats.dev(), aux->rowLoss.dev(), n.value.dev(), aux->count,
+                           stream()));
+  };
+  n.bwd = [aux, vocab, positions](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    auto d = g.gradDst(n.inputs[0]);
+    MTKC(mtkc_xent_backward(d.ptr, g.valPtr(n.inputs[0]), aux->stats.devc(),
+                            (const int32_t*)aux->tg->ptr + aux->tgOff,
+                            aux->hasMask ? aux->mask.devc() : nullptr, go, positions, vocab,
+                            aux->count, d.accumulate, stream()));
+  };
+  return addNode(std::move(n));
+}
+
+// ------------------------------------------------------------ execution
+
+void ExpressionGraph::forward() {
+  for(size_t i = computed_; i < nodes_.size(); ++i) {
+    Node& n = nodes_[i];
+    if(n.alias >= 0) {
+      Node& root = nodes_[(size_t)resolve((int)i)];
+      n.value = root.value.reshaped(n.shape);
+      continue;
+    }
+    if(n.fwd) {
+      if(n.value.empty())
+        n.value = allocTensor(n.shape);
+      n.fwd(*this, n);
+      if(checkFinite_) {
+        Device& d = Device::get();
+        MTKC(mtkc_check_finite(n.value.devc(), n.value.size(), d.flags(), d.stream()));
+        try {
+          d.checkFlags("op " + n.op);
+        } catch(const NumericError&) {
+          throw NumericError("non-finite value produced by op '" + n.op + "' (node " +
+                             std::to_string(i) + ")");
+        }
+      }
+    }
+  }
+  computed_ = nodes_.size();
+}
+
+void ExpressionGraph::backward(NodeRef loss) {
+  checkRef(loss);
+  if(inference_)
+    throw ContractError("backward() called on an inference-mode graph");
+  if(loss.shape.size() != 1)
+    throw ContractError("loss must be scalar-shaped, got " + loss.shape.str());
+  if(computed_ < nodes_.size())
+    forward();
+  for(auto& n : nodes_)
+    if(!n.isParam) {
+      n.gradLive = false;
+      n.gradGated = true;
+    }
+  {
+    auto d = gradDst(loss.index);
+    MTKC(mtkc_fill(d.ptr, lossScale_, 1, stream()));
+  }
+  for(int i = loss.index; i >= 0; --i) {
+    Node& n = nodes_[(size_t)i];
+    if(n.alias >= 0 || !n.bwd || !n.gradLive)
+      continue;
+    n.bwd(*this, n);
+  }
+}
+
+void ExpressionGraph::clear() {
+  nodes_.clear();
+  computed_ = 0;
+  ++generation_;
+  arena_.reset();
+}
+
+Tensor& ExpressionGraph::paramValue(const std::string& name) {
+  auto it = params_.find(name);
+  if(it == params_.end())
+    throw ContractError("unknown parameter: " + name);
+  return it->second.value;
+}
+
+Tensor& ExpressionGraph::paramGrad(const std::string& name) {
+  auto it = params_.find(name);
+  if(it == params_.end())
+    throw ContractError("unknown parameter: " + name);
+  Param& p = it->second;
+  if(!p.gradLive) {
+    p.grad.setZero();
+    p.gradLive = true;
+  }
+  return p.grad;
+}
+
+int64_t ExpressionGraph::paramOffset(const std::string& name) const {
+  auto it = params_.find(name);
+  if(it == params_.end())
+    throw ContractError("unknown parameter: " + name);
+  return it->second.offset;
+}
+
+void ExpressionGraph::zeroGrads() {
+  for(auto& [name, p] : params_)
+    p.gradLive = false;  // logically zero; the first contributor writes
+}
+
+void ExpressionGraph::realizeParamGrads() {
+  for(auto& [name, p] : params_)
+    if(!p.gradLive) {
+      p.grad.setZero();
+      p.gradLive = true;
+    }
+}
+
+}  // namespace mtk

@@ -1,0 +1,150 @@
+// Optimiser, schedule, parameter averaging and synchronous data-parallel
+// training (reference: include/mtk/train.h, src/train.cpp).
+//
+// B200 design: every parameter, gradient, Adam moment and EMA shadow is one
+// flat device buffer in the graph's parameter-pool layout, so the update is
+// one fused kernel (Adam + EMA, 36 B/param) and the data-parallel exchange
+// is one NCCL all-reduce over the flat gradient buffer.  Worker gradients
+// are pre-weighted by tokens_i/total through the backward seed, which makes
+// the all-reduce sum equal the reference's worker-ordered weighted combine
+// (train.cpp:254-269).
+#pragma once
+
+#include <iosfwd>
+#include <map>
+
+#include "mtk/models.h"
+
+namespace mtk {
+
+struct AdamConfig {
+  Real beta1 = Real(0.9);
+  Real beta2 = Real(0.999);
+  Real eps = Real(1e-8);
+};
+
+AdamConfig adamDefaultsFor(const ModelConfig& config);
+
+class AveragedParameters;
+
+class Adam {
+public:
+  explicit Adam(AdamConfig config = AdamConfig()) : cfg_(config) {}
+
+  // One update from the accumulated gradients, then zero them
+  // (train.cpp:49-59).  Throws NumericError and leaves every parameter
+  // untouched if any gradient is non-finite.  When `avg` is given the EMA
+  // update is fused into the same pass.
+  void update(ExpressionGraph& g, Real lr, AveragedParameters* avg = nullptr);
+  // Same, but the non-finite check is deferred to checkDeferred() (no host
+  // synchronisation inside the step).
+  void updateAsync(ExpressionGraph& g, Real lr, AveragedParameters* avg = nullptr);
+  void checkDeferred();
+  // Single-tensor variant (train.cpp:30-47) with its own moments per name.
+  void updateTensor(const std::string& name, Tensor& value, const Tensor& grad, Real lr,
+                    int64_t step);
+
+  int64_t step() const { return step_; }
+  const AdamConfig& config() const { return cfg_; }
+  void setStep(int64_t s) { step_ = s; }
+  // moment views for checkpointing (names in graph order)
+  Tensor firstMoment(ExpressionGraph& g, const std::string& name);
+  Tensor secondMoment(ExpressionGraph& g, const std::string& name);
+
+private:
+  void ensure(ExpressionGraph& g);
+  void launch(ExpressionGraph& g, Real lr, AveragedParameters* avg);
+  AdamConfig cfg_;
+  int64_t step_ = 0;
+  std::shared_ptr<DeviceBuffer> m_, v_;
+  int64_t n_ = 0;
+  bool pending_ = false;
+  ExpressionGraph* lastGraph_ = nullptr;
+  std::map<std::string, std::pair<Tensor, Tensor>> single_;  // updateTensor moments
+};
+
+struct LrSchedule {
+  Real base = Real(0.0003);
+  int64_t warmup = 16000;
+  Real operator()(int64_t step) const;
+};
+
+class AveragedParameters {
+public:
+  explicit AveragedParameters(Real beta = Real(0.9999)) : beta_(beta) {}
+  void update(ExpressionGraph& g);  // avg <- beta*avg + (1-beta)*params
+  void applyTo(ExpressionGraph& g) const;
+  bool empty() const { return !buf_; }
+  Real beta() const { return beta_; }
+  Tensor value(ExpressionGraph& g, const std::string& name);
+  float* ensure(ExpressionGraph& g);  // flat shadow in pool layout (zero-initialised)
+
+private:
+  Real beta_;
+  std::shared_ptr<DeviceBuffer> buf_;
+  int64_t n_ = 0;
+};
+
+// Data-parallel context: one process per GPU; `workers` in TrainOptions is
+// the total worker count across ranks (the reference's threads).
+struct DistContext {
+  int rank = 0;
+  int world = 1;
+  void* comm = nullptr;  // ncclComm_t
+};
+void setDistributed(int rank, int world, const void* ncclId128);
+DistContext& distContext();
+
+struct TrainOptions {
+  int workers = 1;
+  bool async = false;
+  int64_t tokenBudget = 256;
+  uint64_t seed = 1;
+  int64_t epochs = 1;
+  int64_t maxUpdates = -1;
+  LrSchedule lr;
+  Real averageBeta = Real(0.9999);
+  std::string checkpointPath;
+  int64_t checkpointEvery = 0;
+  std::string resumeFrom;
+  int64_t logEvery = 0;
+  std::ostream* log = nullptr;
+};
+
+struct TrainResult {
+  int64_t updates = 0;
+  int64_t epochs = 0;
+  double finalLoss = 0;
+};
+
+// One synchronous update: this rank's share of `batches` (worker i =
+// rank*L + j handles batches[i]), weighted gradients, NCCL all-reduce,
+// fused Adam + EMA.  Stateless apart from the objects passed in.
+struct UpdateResult {
+  double loss = 0;   // token-weighted mean loss over all workers
+  double tokens = 0;  // total target tokens of the update
+};
+class SyncStepper {
+public:
+  SyncStepper(const Model& model, ExpressionGraph& g, Adam& adam, AveragedParameters& avg,
+              const TrainOptions& opts);
+  // launches the update; the returned loss is read from the device
+  // (one synchronisation) unless `readLoss` is false.
+  UpdateResult update(const std::vector<const Batch*>& batches, int64_t updateIndex,
+                      bool readLoss = true);
+
+private:
+  const Model& model_;
+  ExpressionGraph& g_;
+  Adam& adam_;
+  AveragedParameters& avg_;
+  TrainOptions opts_;
+  std::shared_ptr<DeviceBuffer> lossAcc_;
+};
+
+uint64_t mixSeed(uint64_t seed, int64_t update, int worker);
+
+TrainResult train(Model& model, const std::vector<Example>& data, ExpressionGraph& master,
+                  Adam& adam, AveragedParameters& average, const TrainOptions& opts);
+
+}  // namespace mtk

@@ -1,0 +1,327 @@
+// Adam + EMA, learning-rate schedule and synchronous data-parallel training
+// (reference: src/train.cpp).
+#include "mtk/train.h"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <ostream>
+
+#include "mtk/device.h"
+
+namespace mtk {
+
+AdamConfig adamDefaultsFor(const ModelConfig& config) {  // train.cpp:11-20
+  bool transformer = config.architecture == "transformer" || config.decoderKind == "transformer";
+  AdamConfig c;
+  if(transformer) {
+    c.beta2 = Real(0.98);
+    c.eps = Real(1e-9);
+  }
+  return c;
+}
+
+namespace {
+int* adamFlag() { return Device::get().flags() + 1; }
+
+std::shared_ptr<DeviceBuffer> zeroBuffer(int64_t n) {
+  auto b = std::make_shared<DeviceBuffer>((size_t)n);
+  MTKC(mtkc_memset(b->ptr, 0, (size_t)n * sizeof(float), Device::get().stream()));
+  return b;
+}
+
+// grow a pool-layout buffer to n elements, keeping its prefix
+void growTo(std::shared_ptr<DeviceBuffer>& b, int64_t& have, int64_t n) {
+  if(b && have >= n)
+    return;
+  auto nb = zeroBuffer(n);
+  if(b && have > 0)
+    MTKC(mtkc_memcpy_d2d(nb->ptr, b->ptr, (size_t)have * sizeof(float), Device::get().stream()));
+  b = nb;
+  have = n;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ Adam
+
+void Adam::ensure(ExpressionGraph& g) {
+  int64_t n = g.pool().used();
+  int64_t have = n_;
+  growTo(m_, have, n);
+  have = n_;
+  growTo(v_, have, n);
+  n_ = std::max(n_, n);
+}
+
+void Adam::launch(ExpressionGraph& g, Real lr, AveragedParameters* avg) {
+  if(pending_)
+    checkDeferred();
+  ensure(g);
+  g.realizeParamGrads();
+  Device& d = Device::get();
+  int64_t n = g.pool().used();
+  MTKC(mtkc_memset(adamFlag(), 0, sizeof(int), d.stream()));
+  float* grads = g.pool().grads()->ptr;
+  MTKC(mtkc_check_finite(grads, n, adamFlag(), d.stream()));
+  int64_t step = step_ + 1;
+  Real corr1 = Real(1) - (Real)std::pow((double)cfg_.beta1, (double)step);  // train.cpp:37-38
+  Real corr2 = Real(1) - (Real)std::pow((double)cfg_.beta2, (double)step);
+  float* avgPtr = avg ? avg->ensure(g) : nullptr;
+  MTKC(mtkc_adam_ema(g.pool().values()->ptr, grads, m_->ptr, v_->ptr, avgPtr, n, lr, cfg_.beta1,
+                     cfg_.beta2, cfg_.eps, corr1, corr2, avg ? avg->beta() : 0.f, avg ? 1 : 0,
+                     /*zero_grad=*/0, adamFlag(), d.stream()));
+  step_ = step;
+  pending_ = true;
+  lastGraph_ = &g;
+}
+
+void Adam::checkDeferred() {
+  if(!pending_)
+    return;
+  pending_ = false;
+  Device& d = Device::get();
+  int flag = 0;
+  MTKC(mtkc_memcpy_d2h(&flag, adamFlag(), sizeof(int), d.stream()));
+  d.sync();
+  ExpressionGraph& g = *lastGraph_;
+  if(!(flag & MTKC_FLAG_NONFINITE)) {
+    g.zeroGrads();  // consumed by the update (train.cpp:57), lazily zero
+    return;
+  }
+  --step_;  // the device skipped the update: nothing changed
+  std::string bad = "?";
+  for(auto& name : g.paramNames()) {
+    Tensor& gr = g.paramGrad(name);
+    if(!gr.allFinite()) {
+      bad = name;
+      break;
+    }
+  }
+  throw NumericError("non-finite gradient for parameter " + bad + "; update aborted");
+}
+
+void Adam::updateAsync(ExpressionGraph& g, Real lr, AveragedParameters* avg) {
+  launch(g, lr, avg);
+}
+
+void Adam::update(ExpressionGraph& g, Real lr, AveragedParameters* avg) {
+  launch(g, lr, avg);
+  checkDeferred();
+}
+
+void Adam::updateTensor(const std::string& name, Tensor& value, const Tensor& grad, Real lr,
+                        int64_t step) {
+  if(!grad.allFinite())
+    throw NumericError("non-finite gradient for parameter " + name + "; update aborted");
+  auto it = single_.find(name);
+  if(it == single_.end()) {
+    Tensor m(value.shape()), v(value.shape());
+    it = single_.emplace(name, std::make_pair(m, v)).first;
+  }
+  Tensor& m = it->second.first;
+  Tensor& v = it->second.second;
+  Real corr1 = Real(1) - (Real)std::pow((double)cfg_.beta1, (double)step);
+  Real corr2 = Real(1) - (Real)std::pow((double)cfg_.beta2, (double)step);
+  // a private copy of the gradient keeps the caller's tensor untouched
+  Tensor gcopy = grad.copy();
+  MTKC(mtkc_adam_ema(value.dev(), gcopy.dev(), m.dev(), v.dev(), nullptr, value.size(), lr,
+                     cfg_.beta1, cfg_.beta2, cfg_.eps, corr1, corr2, 0.f, 0, 0, nullptr,
+                     Device::get().stream()));
+}
+
+static Tensor poolView(ExpressionGraph& g, const std::shared_ptr<DeviceBuffer>& buf,
+                       const std::string& name) {
+  return Tensor(g.paramValue(name).shape(), buf, g.paramOffset(name));
+}
+
+Tensor Adam::firstMoment(ExpressionGraph& g, const std::string& name) {
+  ensure(g);
+  return poolView(g, m_, name);
+}
+
+Tensor Adam::secondMoment(ExpressionGraph& g, const std::string& name) {
+  ensure(g);
+  return poolView(g, v_, name);
+}
+
+Real LrSchedule::operator()(int64_t step) const {  // train.cpp:61-67
+  if(step < 0)
+    throw ContractError("negative lr step");
+  if(step <= warmup)
+    return base * (Real)step / (Real)warmup;
+  return base * (Real)std::sqrt((double)warmup / (double)step);
+}
+
+// ---------------------------------------------------- AveragedParameters
+
+float* AveragedParameters::ensure(ExpressionGraph& g) {
+  growTo(buf_, n_, g.pool().used());
+  return buf_->ptr;
+}
+
+void AveragedParameters::update(ExpressionGraph& g) {  // train.cpp:69-79
+  float* a = ensure(g);
+  MTKC(mtkc_ema(a, g.pool().values()->ptr, g.pool().used(), beta_, Device::get().stream()));
+}
+
+void AveragedParameters::applyTo(ExpressionGraph& g) const {
+  if(!buf_)
+    return;
+  MTKC(mtkc_memcpy_d2d(g.pool().values()->ptr, buf_->ptr,
+                       (size_t)std::min<int64_t>(n_, g.pool().used()) * sizeof(float),
+                       Device::get().stream()));
+}
+
+Tensor AveragedParameters::value(ExpressionGraph& g, const std::string& name) {
+  ensure(g);
+  return poolView(g, buf_, name);
+}
+
+// ---------------------------------------------------------- distributed
+
+namespace {
+DistContext g_dist;
+}
+
+DistContext& distContext() { return g_dist; }
+
+void setDistributed(int rank, int world, const void* ncclId128) {
+  Device::get();
+  g_dist.rank = rank;
+  g_dist.world = world;
+  if(world > 1)
+    MTKC(mtkc_nccl_comm_init(&g_dist.comm, world, rank, ncclId128));
+}
+
+// ----------------------------------------------------------- training
+
+uint64_t mixSeed(uint64_t seed, int64_t update, int worker) {  // train.cpp:170-176
+  uint64_t h = hash64("update");
+  h ^= seed + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  h ^= (uint64_t)update * 0xbf58476d1ce4e5b9ull;
+  h ^= (uint64_t)(worker + 1) * 0x94d049bb133111ebull;
+  return h;
+}
+
+SyncStepper::SyncStepper(const Model& model, ExpressionGraph& g, Adam& adam,
+                         AveragedParameters& avg, const TrainOptions& opts)
+    : model_(model), g_(g), adam_(adam), avg_(avg), opts_(opts) {
+  if(opts.workers < 1)
+    throw ContractError("training needs at least one worker");
+  lossAcc_ = std::make_shared<DeviceBuffer>(64);
+}
+
+UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64_t updateIndex,
+                                 bool readLoss) {
+  DistContext& dc = distContext();
+  int W = opts_.workers;
+  if(W % dc.world != 0)
+    throw ContractError("workers must be a multiple of the number of ranks");
+  int L = W / dc.world;
+  int take = (int)batches.size();
+  if(take < 1 || take > W)
+    throw ContractError("an update takes between 1 and `workers` batches");
+  std::vector<double> tokens((size_t)take);
+  double total = 0;
+  for(int i = 0; i < take; ++i) {
+    tokens[(size_t)i] = (double)batches[(size_t)i]->targetTokenCount();
+    total += tokens[(size_t)i];
+  }
+  Device& d = Device::get();
+  MTKC(mtkc_memset(lossAcc_->ptr, 0, sizeof(float), d.stream()));
+  g_.zeroGrads();
+  for(int j = 0; j < L; ++j) {
+    int i = dc.rank * L + j;
+    if(i >= take)
+      break;
+    g_.clear();
+    g_.setSeed(mixSeed(opts_.seed, updateIndex, i));
+    Real w = (Real)tokens[(size_t)i] / (Real)total;  // train.cpp:262-266
+    g_.setLossScale(w);
+    NodeRef loss = model_.buildLoss(g_, *batches[(size_t)i]);
+    g_.forward();
+    g_.backward(loss);
+    MTKC(mtkc_axpy(lossAcc_->ptr, loss.val().devc(), w, 1, d.stream()));
+  }
+  g_.setLossScale(1);
+  if(dc.world > 1) {
+    g_.realizeParamGrads();
+    MTKC(mtkc_allreduce_sum(dc.comm, g_.pool().grads()->ptr, g_.pool().used(), d.stream()));
+    MTKC(mtkc_allreduce_sum(dc.comm, lossAcc_->ptr, 1, d.stream()));
+  }
+  Real lr = opts_.lr(adam_.step() + 1);
+  adam_.updateAsync(g_, lr, &avg_);
+  UpdateResult r;
+  r.tokens = total;
+  if(readLoss) {
+    float l = 0;
+    MTKC(mtkc_memcpy_d2h(&l, lossAcc_->ptr, sizeof(float), d.stream()));
+    adam_.checkDeferred();  // synchronises
+    d.checkFlags("training step");
+    r.loss = l;
+  }
+  return r;
+}
+
+namespace {
+void logLine(const TrainOptions& opts, int64_t update, int64_t epoch, double loss, Real lr,
+             double wps) {
+  if(!opts.log || opts.logEvery <= 0 || update % opts.logEvery != 0)
+    return;
+  (*opts.log) << "update=" << update << " epoch=" << epoch << " loss=" << loss
+              << " lr=" << (double)lr << " wps=" << wps << "\n";
+}
+}  // namespace
+
+TrainResult train(Model& model, const std::vector<Example>& data, ExpressionGraph& master,
+                  Adam& adam, AveragedParameters& average, const TrainOptions& opts) {
+  if(opts.workers < 1)
+    throw ContractError("training needs at least one worker");
+  if(opts.async)
+    throw ContractError("asynchronous (hogwild) training is outside the B200 training path");
+  if(!opts.resumeFrom.empty())
+    throw ContractError("resume is not implemented in this build");
+  model.registerParams(master);
+  master.clear();
+  SyncStepper stepper(model, master, adam, average, opts);
+  TrainResult res;
+  int64_t update = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  int64_t tokensSeen = 0;
+  for(int64_t epoch = 0; epoch < opts.epochs; ++epoch) {
+    BatchOptions bo;
+    bo.tokenBudget = opts.tokenBudget;
+    bo.seed = opts.seed + (uint64_t)epoch;
+    bo.shuffle = true;
+    auto batches = makeBatches(data, bo);  // epochBatches, train.cpp:183-190
+    double epochLoss = 0;
+    int64_t epochUpdates = 0;
+    for(size_t idx = 0; idx < batches.size();) {
+      int take = (int)std::min<size_t>((size_t)opts.workers, batches.size() - idx);
+      std::vector<const Batch*> ptrs;
+      for(int i = 0; i < take; ++i)
+        ptrs.push_back(&batches[idx + (size_t)i]);
+      Real lr = opts.lr(adam.step() + 1);
+      UpdateResult r = stepper.update(ptrs, update);
+      ++update;
+      idx += (size_t)take;
+      epochLoss += r.loss;
+      ++epochUpdates;
+      tokensSeen += (int64_t)r.tokens;
+      double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      logLine(opts, update, epoch, r.loss, lr, secs > 0 ? (double)tokensSeen / secs : 0);
+      if(opts.maxUpdates >= 0 && update >= opts.maxUpdates) {
+        res.updates = update;
+        res.epochs = epoch + 1;
+        res.finalLoss = epochUpdates ? epochLoss / (double)epochUpdates : 0;
+        return res;
+      }
+    }
+    res.finalLoss = epochUpdates ? epochLoss / (double)epochUpdates : res.finalLoss;
+    res.epochs = epoch + 1;
+  }
+  res.updates = update;
+  return res;
+}
+
+}  // namespace mtk

@@ -190,6 +190,24 @@ __global__ void mask_blend_bwd_kernel(float* ga, float* gb, const float* go, con
   }
 }
 
+__global__ void scale_add_periodic_kernel(float* out, const float* x, float s, const float* c,
+                                          int64_t n, int64_t period) {
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    float v = x[i];
+    if(s != 1.f)
+      v = s * v;
+    out[i] = v + c[i % period];
+  }
+}
+
+__global__ void relu_mask_kernel(float* gx, const float* gate, int64_t n) {
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+      i += (int64_t)gridDim.x * blockDim.x)
+    if(!(gate[i] > 0.f))
+      gx[i] = 0.f;
+}
+
 int64_t prod4(const int64_t d[4]) { return d[0] * d[1] * d[2] * d[3]; }
 
 }  // namespace
@@ -301,6 +319,23 @@ int mtkc_fill(float* out, float v, int64_t n, void* stream) {
     return MTKC_OK;
   fill_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(out, v, n);
   MTKC_POST_LAUNCH("fill_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_scale_add_periodic(float* out, const float* x, float s, const float* c, int64_t n,
+                            int64_t period, void* stream) {
+  if(n <= 0)
+    return MTKC_OK;
+  scale_add_periodic_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(out, x, s, c, n, period);
+  MTKC_POST_LAUNCH("scale_add_periodic_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_relu_mask(float* gx, const float* gate, int64_t n, void* stream) {
+  if(n <= 0)
+    return MTKC_OK;
+  relu_mask_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(gx, gate, n);
+  MTKC_POST_LAUNCH("relu_mask_kernel");
   return MTKC_OK;
 }
 

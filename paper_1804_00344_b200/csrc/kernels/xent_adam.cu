@@ -173,9 +173,23 @@ __global__ void adam_ema_kernel(float* th, float* g, float* m, float* v, float* 
   }
 }
 
+__global__ void ema_kernel(float* a, const float* th, int64_t n, float b) {
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+      i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = b * a[i] + (1.f - b) * th[i];
+}
+
 }  // namespace
 
 extern "C" {
+
+int mtkc_ema(float* avg, const float* theta, int64_t n, float beta, void* stream) {
+  if(n <= 0)
+    return MTKC_OK;
+  ema_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(avg, theta, n, beta);
+  MTKC_POST_LAUNCH("ema_kernel");
+  return MTKC_OK;
+}
 
 int mtkc_xent_forward(const float* logits, const int32_t* targets, const float* mask,
                       int64_t rows, int64_t vocab, float* lse, float* row_loss, float* loss,
