@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: target words/sec of the synchronous data-parallel training step
+(BASELINE.json metric), Transformer-base by default.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config base|tiny|big|shallow|deep]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+  python bench.py --impl reference      # the reference's own CPU step (oracle/_ref)
+
+One "step" is one synchronous update (train.cpp:221-272): every rank builds
+the loss of one token-budget batch, runs forward/backward, the gradients are
+all-reduced (NCCL) and Adam+EMA is applied.  Batches come from the
+reference's own batching of the SURVEY 8(d) synthetic corpus, so the units
+are the reference's target words (incl. </s>).
+
+value   = sum of target words of all ranks' timed updates / max-over-ranks
+          device time (CUDA events on the compute stream, no host syncs
+          inside the timed region; token ids/masks uploaded per step).
+e2e     = same through the public update call with the loss read back to
+          the host every step, wall clock, H2D/D2H bytes counted.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "target words/sec, Transformer-base training step at 1/2/4/8 B200"
+DATA = "synthetic: SURVEY.md 8(d) splitmix64 corpus, lengths 16..32+</s>, ids uniform in [2,V)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="base")
+    p.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=20.0)
+    return p.parse_args()
+
+
+def dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as td
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        td.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world, local
+
+
+def all_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as td
+    t = torch.tensor([x], dtype=torch.float64)
+    td.all_reduce(t, op=td.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as td
+        td.barrier()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return j["hbm_gbs"], j.get("bf16_tflops_sustained", j["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------ CPU reference
+
+def cpu_reference(cfg_text, vocab, seconds_budget, threads=None, steps=1):
+    """The UNMODIFIED reference trainSync (oracle/_ref, train.cpp:200-300) on a
+    bounded sample: `threads` workers, one single-sentence batch each (token
+    budget 66 slots), `steps` updates.  Returns (words/s, words, seconds)."""
+    from oracle import refbind as R
+    from paper_1804_00344_b200 import synth
+    threads = threads or os.cpu_count() or 1
+    n = threads * steps * 2 + 16
+    src, tgt = synth.corpus(n, vocab)
+    ex = R.Examples(src, tgt)
+    budget = 66
+    bl = R.make_batches(ex, budget, 1)
+    words = sum(float(b["tgt_mask"].sum()) for b in bl[: threads * steps])
+    model = R.RefModel(cfg_text, 1)
+    t0 = time.perf_counter()
+    model.train(ex, workers=threads, budget=budget, seed=1, epochs=1, max_updates=steps)
+    dt = time.perf_counter() - t0
+    return words / dt, words, dt, threads
+
+
+# ------------------------------------------------------------ B200 arm
+
+def run_b200(a):
+    rank, world, local = dist()
+    from paper_1804_00344_b200 import CONFIGS, TOKEN_BUDGET, config_text, mtk as M
+    M.select_device(local)
+    M.set_precision(a.precision)
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        buf = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = torch.tensor(list(M.nccl_unique_id()), dtype=torch.uint8)
+        td.broadcast(buf, 0)
+        M.set_distributed(rank, world, bytes(buf.tolist()))
+    spec = CONFIGS[a.config]
+    cfg = config_text(**spec)
+    budget = TOKEN_BUDGET[a.config]
+    vocab = spec["vocab"]
+
+    model = M.Model(cfg)
+    g = M.ExpressionGraph(1)
+    model.register_params(g)
+    g.clear()
+    adam = M.Adam(M.adam_defaults_for(cfg))
+    avg = M.AveragedParameters(0.9999)
+    opts = M.TrainOptions()
+    opts.workers = world
+    opts.token_budget = budget
+    opts.seed = 1
+    stepper = M.SyncStepper(model, g, adam, avg, opts)
+
+    prof_steps, e2e_steps = 2, max(3, min(a.steps, 10))
+    updates = a.warmup + a.steps + e2e_steps + prof_steps
+    per_batch = max(1, budget // 70)
+    n_pairs = int(updates * world * per_batch * 1.15) + 64
+    ex = M.synth_examples(n_pairs, vocab)
+    batches = M.make_batches(ex, budget, 1, True)  # epoch 0 (train.cpp:183-190)
+    while len(batches) < updates * world:
+        n_pairs = int(n_pairs * 1.3)
+        ex = M.synth_examples(n_pairs, vocab)
+        batches = M.make_batches(ex, budget, 1, True)
+
+    def group(u):
+        return batches[u * world:(u + 1) * world]
+
+    u = 0
+    for _ in range(a.warmup):
+        stepper.update(group(u), u, True)
+        u += 1
+
+    # ---- value: device-timed, inputs uploaded per step, no host sync inside
+    clocks = Clocks(local)
+    barrier(world)
+    M.sync()
+    clocks.start()
+    l0 = M.launch_count()
+    e0 = M.event_record()
+    words = 0.0
+    for _ in range(a.steps):
+        grp = group(u)
+        words += sum(b.target_tokens() for b in grp)
+        stepper.update(grp, u, False)
+        u += 1
+    e1 = M.event_record()
+    ms = M.event_elapsed_ms(e0, e1)
+    launches = M.launch_count() - l0
+    clk = clocks.stop()
+    ms_max = all_max(ms, world)
+    value = words / (ms_max / 1e3)
+
+    # ---- e2e: public update call, host batches, loss read back every step
+    barrier(world)
+    M.sync()
+    h0, d0 = M.h2d_bytes(), M.d2h_bytes()
+    t0 = time.perf_counter()
+    ewords = 0.0
+    losses = []
+    for _ in range(e2e_steps):
+        grp = group(u)
+        ewords += sum(b.target_tokens() for b in grp)
+        r = stepper.update(grp, u, True)
+        losses.append(r.loss)
+        u += 1
+    M.sync()
+    et = all_max(time.perf_counter() - t0, world)
+    h2d = (M.h2d_bytes() - h0) / e2e_steps
+    d2h = (M.d2h_bytes() - d0) / e2e_steps
+
+    # ---- per-kernel-class device time (events around each C-ABI call)
+    M.sync()
+    M.prof_enable(True)
+    pe0 = M.event_record()
+    for _ in range(prof_steps):
+        stepper.update(group(u), u, True)
+        u += 1
+    pe1 = M.event_record()
+    step_ms = M.event_elapsed_ms(pe0, pe1) / prof_steps
+    rep = M.prof_report()
+    M.prof_enable(False)
+    classes = {}
+    for line in rep.strip().splitlines():
+        name, n, tms, work = line.split()
+        classes[name] = dict(launches=int(n) / prof_steps, ms=float(tms) / prof_steps,
+                             work=float(work) / prof_steps)
+    hbm, tflops, src = peaks()
+    dom = max(classes, key=lambda k: classes[k]["ms"]) if classes else None
+    roof = None
+    if dom:
+        c = classes[dom]
+        tensor = dom.startswith("gemm") or dom == "attention"
+        per_launch_work = c["work"] / max(c["launches"], 1)
+        per_launch_s = c["ms"] / max(c["launches"], 1) / 1e3
+        achieved = per_launch_work / per_launch_s / (1e12 if tensor else 1e9)
+        peak = tflops if tensor else hbm
+        roof = {"bound": "tensor" if tensor else "hbm", "kernel": dom,
+                "achieved": round(achieved, 2), "peak": peak,
+                "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": None, "peak_source": f"{src} (bf16 dense, sustained)",
+                "share_of_step": round(c["ms"] / step_ms, 4),
+                "note": "GEMMs run tcgen05 kind::tf32 on fp32 storage; tf32 dense peak is half the bf16 denominator"}
+    breakdown = {k: {"ms_per_step": round(v["ms"], 3), "share": round(v["ms"] / step_ms, 4),
+                     "launches_per_step": v["launches"]} for k, v in classes.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            v, w, dt, th = cpu_reference(cfg, vocab, a.cpu_seconds)
+            cpu = {"value": round(v, 3), "unit": "target words/sec", "cores": th,
+                   "kind": "reference",
+                   "sample": f"oracle/_ref trainSync (unmodified reference, -O3), {th} workers x "
+                             f"one single-sentence batch, 1 update, {int(w)} target words in {dt:.1f}s"}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC if a.config == "base" else f"target words/sec, {a.config} training step",
+            "value": round(value, 1), "unit": "target words/sec", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max / a.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": a.precision, "data": DATA,
+            "config": {"workload": f"{a.config}: {cfg.strip().replace(chr(10), '; ')}; "
+                                   f"tokenBudget {budget}/GPU",
+                       "global_batch": f"{world} x tokenBudget {budget} (~{words / a.steps:.0f} target words/update)",
+                       "seq_len": "16..32 + </s> (padded per batch)", "parallelism": f"dp{world}",
+                       "l2": "working set (activations, logits) far exceeds the 126 MB L2"},
+            "e2e": {"value": round(ewords / et, 1), "unit": "target words/sec",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "loss_last": losses[-1] if losses else None},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "kernel_breakdown": breakdown,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1804_00344_b200 import CONFIGS, config_text
+    spec = CONFIGS[a.config]
+    cfg = config_text(**spec)
+    threads = os.cpu_count() or 1
+    # time steps until ~180 s are used (each step = one reference update)
+    v, w, dt, th = cpu_reference(cfg, spec["vocab"], 0, threads=threads, steps=1)
+    steps = max(1, min(a.steps, int(180 / max(dt, 1e-3))))
+    if steps > 1:
+        v, w, dt, th = cpu_reference(cfg, spec["vocab"], 0, threads=threads, steps=steps)
+    out = {"metric": METRIC if a.config == "base" else f"target words/sec, {a.config} training step",
+           "impl": "reference", "value": round(v, 3), "unit": "target words/sec",
+           "n_gpus": a.gpus, "steps": steps, "steps_requested": a.steps, "warmup": 1,
+           "ms_per_step": round(dt / steps * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "fp32", "data": DATA,
+           "config": {"workload": f"{a.config}: {cfg.strip().replace(chr(10), '; ')}",
+                      "global_batch": f"{th} workers x 1 sentence", "parallelism": f"{th} CPU threads"},
+           "cpu_baseline": {"value": round(v, 3), "unit": "target words/sec", "cores": th,
+                            "kind": "reference",
+                            "sample": f"{th} workers x single-sentence batches, {steps} update(s), "
+                                      f"{int(w)} target words in {dt:.1f}s (first update was warm-up)"},
+           "e2e": {"value": round(v, 3), "unit": "target words/sec", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)

@@ -91,6 +91,17 @@ int mtkc_event_elapsed_ms(void* start, void* stop, float* ms);
 int mtkc_device_sync(void);
 /* Kernel-launch counter (every mtkc_* kernel launch increments it). */
 uint64_t mtkc_launch_count(void);
+/* Host<->device byte counters of mtkc_memcpy_h2d / mtkc_memcpy_d2h. */
+uint64_t mtkc_h2d_bytes(void);
+uint64_t mtkc_d2h_bytes(void);
+/* Per-kernel-class profiling with CUDA events on the launching stream.
+ * While enabled, the GEMM, attention, layer-norm, cross-entropy, embedding
+ * and Adam entry points bracket their launches with events and record the
+ * algorithmic work (FLOPs for GEMM/attention, HBM bytes otherwise).
+ * mtkc_prof_report synchronises and writes one line per class:
+ *   "<class> <launches> <total_ms> <total_work>\n"  (then resets). */
+int mtkc_prof_enable(int on);
+int mtkc_prof_report(char* buf, size_t len);
 
 /* ======================================================================== */
 /* GEMM: matmulInto (tensor.cpp:258-306), matmulAccumInto (graph.cpp:273-   */

@@ -210,6 +210,13 @@ int ref_grad_get(void* h, const char* name, float* out) {
   return guard([&] { copyOut(static_cast<RefModel*>(h)->g->paramGrad(name), out); });
 }
 
+int ref_grad_set(void* h, const char* name, const float* in) {
+  return guard([&] {
+    Tensor& t = static_cast<RefModel*>(h)->g->paramGrad(name);
+    std::memcpy(t.data(), in, sizeof(float) * (size_t)t.size());
+  });
+}
+
 // which: 0 = Adam m, 1 = Adam v, 2 = EMA average
 int ref_state_get(void* h, int which, const char* name, float* out) {
   return guard([&] {
@@ -398,6 +405,38 @@ int ref_op_embed(int64_t V, int64_t e, const float* table, int64_t rows, int64_t
     g.backward(loss);
     copyOut(o.val(), out);
     copyOut(g.paramGrad("E"), gtable);
+  });
+}
+
+// MultiHeadAttention::apply (layers.cpp:89-126) with identity q/k/v/o
+// projections and zero biases, so out == the attention core; returns the
+// gradients of the q/k/v inputs for d(out) = G.
+int ref_op_mha(int64_t b, int64_t tq, int64_t tk, int64_t d, int heads, const float* q,
+               const float* k, const float* v, const float* keyMask, int causal,
+               const float* G, float* out, float* gq, float* gk, float* gv) {
+  return guard([&] {
+    ExpressionGraph g(1);
+    std::vector<Real> eye((size_t)(d * d), Real(0));
+    for(int64_t i = 0; i < d; ++i)
+      eye[(size_t)(i * d + i)] = 1;
+    for(const char* n : {"q", "k", "v", "o"}) {
+      g.param(std::string("mha.") + n + "W", Shape({d, d}), inits::fromVector(eye));
+      g.param(std::string("mha.") + n + "B", Shape({d}), inits::zeros());
+    }
+    NodeRef nq = g.param("xq", Shape({b, tq, d}), inits::fromVector(std::vector<Real>(q, q + b * tq * d)));
+    NodeRef nk = g.param("xk", Shape({b, tk, d}), inits::fromVector(std::vector<Real>(k, k + b * tk * d)));
+    NodeRef nv = g.param("xv", Shape({b, tk, d}), inits::fromVector(std::vector<Real>(v, v + b * tk * d)));
+    MultiHeadAttention mha{"mha", d, heads};
+    Tensor km = keyMask ? Tensor(Shape({b, tk}), std::vector<Real>(keyMask, keyMask + b * tk)) : Tensor();
+    NodeRef o = mha.apply(g, nq, nk, nv, km, causal != 0);
+    NodeRef loss = seededLoss(g, o, G);
+    g.forward();
+    g.zeroGrads();
+    g.backward(loss);
+    copyOut(o.val(), out);
+    copyOut(g.paramGrad("xq"), gq);
+    copyOut(g.paramGrad("xk"), gk);
+    copyOut(g.paramGrad("xv"), gv);
   });
 }
 

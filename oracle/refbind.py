@@ -60,6 +60,7 @@ def lib():
             "ref_param_get": (I, [P, C.c_char_p, fp]),
             "ref_param_set": (I, [P, C.c_char_p, fp]),
             "ref_grad_get": (I, [P, C.c_char_p, fp]),
+            "ref_grad_set": (I, [P, C.c_char_p, fp]),
             "ref_state_get": (I, [P, I, C.c_char_p, fp]),
             "ref_adam_step": (I64, [P]),
             "ref_loss_grads": (I, [P, P, I64, U64, dp, fp]),
@@ -74,6 +75,7 @@ def lib():
             "ref_op_xent": (I, [I64, I64, I64, fp, ip, fp, dp, fp]),
             "ref_op_embed": (I, [I64, I64, fp, I64, I64, ip, fp, fp, fp]),
             "ref_op_gru": (I, [I64, I64, I64, I, fp, fp, fp, fp, fp, fp, fp, fp]),
+            "ref_op_mha": (I, [I64, I64, I64, I64, I, fp, fp, fp, fp, I, fp, fp, fp, fp, fp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -209,6 +211,10 @@ class RefModel:
         _check(lib().ref_grad_get(self.h, name.encode(), _f(out)))
         return out
 
+    def set_grad(self, name, value):
+        v = f32(value).reshape(self.shape(name))
+        _check(lib().ref_grad_set(self.h, name.encode(), _f(v)))
+
     def state(self, which: str, name):
         out = np.zeros(self.shape(name), np.float32)
         _check(lib().ref_state_get(self.h, {"m": 0, "v": 1, "avg": 2}[which], name.encode(), _f(out)))
@@ -311,6 +317,19 @@ def op_embed(table, ids, G):
     gt = np.zeros_like(table)
     _check(lib().ref_op_embed(V, e, _f(table), rows, cols, _i(ids), _f(G), _f(out), _f(gt)))
     return out, gt
+
+
+def op_mha(q, k, v, key_mask, causal, heads, G):
+    """MultiHeadAttention with identity projections: the attention core."""
+    q, k, v, G = f32(q), f32(k), f32(v), f32(G)
+    b, tq, d = q.shape
+    tk = k.shape[1]
+    out = np.zeros_like(q)
+    gq, gk, gv = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
+    km = None if key_mask is None else f32(key_mask)
+    _check(lib().ref_op_mha(b, tq, tk, d, heads, _f(q), _f(k), _f(v), _f(km), int(causal),
+                            _f(G), _f(out), _f(gq), _f(gk), _f(gv)))
+    return out, gq, gk, gv
 
 
 def op_gru(h, x, packed_w, ln, G, e, d):

@@ -118,9 +118,18 @@ int64_t ParamPool::reserve(int64_t elems) {
 // ------------------------------------------------------------ the graph
 
 ExpressionGraph::ExpressionGraph(uint64_t seed, bool inference)
-    : rng_(seed), seed_(seed), inference_(inference) {
+    : arena_(defaultArenaBytes()), rng_(seed), seed_(seed), inference_(inference) {
   const char* e = std::getenv("MTK_CHECK_FINITE");
   checkFinite_ = e && e[0] == '1';
+}
+
+// The reference's 8 GiB host default (tensor.h:45) is far below one
+// Transformer-base step's working set on a GPU with 180 GB of HBM3e; the
+// device arena defaults to 96 GiB (MTK_ARENA_GB overrides).
+size_t ExpressionGraph::defaultArenaBytes() {
+  const char* e = std::getenv("MTK_ARENA_GB");
+  double gb = e ? std::atof(e) : 96.0;
+  return (size_t)(gb * (double)(1ull << 30));
 }
 
 void ExpressionGraph::checkRef(const NodeRef& r) const {

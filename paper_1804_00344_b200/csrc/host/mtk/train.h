@@ -59,6 +59,7 @@ private:
   std::shared_ptr<DeviceBuffer> m_, v_;
   int64_t n_ = 0;
   bool pending_ = false;
+  int64_t pendingSteps_ = 0;
   ExpressionGraph* lastGraph_ = nullptr;
   std::map<std::string, std::pair<Tensor, Tensor>> single_;  // updateTensor moments
 };

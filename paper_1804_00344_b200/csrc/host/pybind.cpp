@@ -115,6 +115,29 @@ PYBIND11_MODULE(_mtk, m) {
   m.def("sync", [] { Device::get().sync(); });
   m.def("check_flags", [] { Device::get().checkFlags("explicit check"); });
   m.def("launch_count", [] { return (uint64_t)mtkc_launch_count(); });
+  m.def("h2d_bytes", [] { return (uint64_t)mtkc_h2d_bytes(); });
+  m.def("d2h_bytes", [] { return (uint64_t)mtkc_d2h_bytes(); });
+  m.def("prof_enable", [](bool on) { MTKC(mtkc_prof_enable(on ? 1 : 0)); });
+  // CUDA events on the compute stream (the stream every kernel runs on)
+  m.def("event_record", [] {
+    void* e = nullptr;
+    MTKC(mtkc_event_create(&e));
+    MTKC(mtkc_event_record(e, Device::get().stream()));
+    return (uintptr_t)e;
+  });
+  m.def("event_elapsed_ms", [](uintptr_t a, uintptr_t b) {
+    Device::get().sync();
+    float ms = 0;
+    MTKC(mtkc_event_elapsed_ms((void*)a, (void*)b, &ms));
+    mtkc_event_destroy((void*)a);
+    mtkc_event_destroy((void*)b);
+    return ms;
+  });
+  m.def("prof_report", [] {
+    std::vector<char> buf(1 << 16);
+    MTKC(mtkc_prof_report(buf.data(), buf.size()));
+    return std::string(buf.data());
+  });
   m.def("sm_count", [] { return Device::get().sms(); });
   m.def("stream_handle", [] { return (uintptr_t)Device::get().stream(); });
   m.def("nccl_unique_id", [] {
@@ -265,6 +288,33 @@ PYBIND11_MODULE(_mtk, m) {
              return e;
            }))
       .def("__len__", [](const Examples& e) { return e.ex.size(); });
+
+  // SURVEY.md 8(d) synthetic generator (same formula as synth.py)
+  m.def("synth_examples", [](int64_t n, int64_t vocab, int64_t start) {
+    auto sm = [](uint64_t x) {
+      uint64_t z = x + 0x9e3779b97f4a7c15ull;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      return z ^ (z >> 31);
+    };
+    Examples e;
+    e.ex.resize((size_t)n);
+    for(int64_t k = 0; k < n; ++k) {
+      uint64_t i = (uint64_t)(start + k);
+      int64_t ls = 16 + (int64_t)(sm(1234ull * 1000003ull + i) % 17);
+      int64_t lt = 16 + (int64_t)(sm(5678ull * 1000003ull + i) % 17);
+      std::vector<int32_t> s((size_t)ls), t((size_t)lt);
+      for(int64_t j = 0; j < ls; ++j)
+        s[(size_t)j] = (int32_t)(2 + sm((i << 20) ^ (uint64_t)j ^ 0xabcull) % (uint64_t)(vocab - 2));
+      for(int64_t j = 0; j < lt; ++j)
+        t[(size_t)j] = (int32_t)(2 + sm((i << 20) ^ (uint64_t)j ^ 0xdefull) % (uint64_t)(vocab - 2));
+      e.ex[(size_t)k].sources = {s};
+      e.ex[(size_t)k].target = t;
+      e.ex[(size_t)k].hasTarget = true;
+      e.ex[(size_t)k].id = (size_t)k;
+    }
+    return e;
+  }, py::arg("n"), py::arg("vocab"), py::arg("start") = 0);
 
   py::class_<Batch>(m, "Batch")
       .def(py::init([](IArr srcIds, FArr srcMask, IArr tgtIds, FArr tgtMask) {

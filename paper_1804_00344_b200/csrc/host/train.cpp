@@ -54,13 +54,14 @@ void Adam::ensure(ExpressionGraph& g) {
 }
 
 void Adam::launch(ExpressionGraph& g, Real lr, AveragedParameters* avg) {
-  if(pending_)
-    checkDeferred();
   ensure(g);
   g.realizeParamGrads();
   Device& d = Device::get();
   int64_t n = g.pool().used();
-  MTKC(mtkc_memset(adamFlag(), 0, sizeof(int), d.stream()));
+  // While earlier updates are unchecked the flag stays sticky: once a
+  // non-finite gradient is seen every later update is skipped on the device.
+  if(!pending_)
+    MTKC(mtkc_memset(adamFlag(), 0, sizeof(int), d.stream()));
   float* grads = g.pool().grads()->ptr;
   MTKC(mtkc_check_finite(grads, n, adamFlag(), d.stream()));
   int64_t step = step_ + 1;
@@ -72,27 +73,36 @@ void Adam::launch(ExpressionGraph& g, Real lr, AveragedParameters* avg) {
                      /*zero_grad=*/0, adamFlag(), d.stream()));
   step_ = step;
   pending_ = true;
+  ++pendingSteps_;
   lastGraph_ = &g;
+  g.zeroGrads();  // consumed by the update (train.cpp:57); lazily zero, memory kept
 }
 
 void Adam::checkDeferred() {
   if(!pending_)
     return;
   pending_ = false;
+  int64_t steps = pendingSteps_;
+  pendingSteps_ = 0;
   Device& d = Device::get();
   int flag = 0;
   MTKC(mtkc_memcpy_d2h(&flag, adamFlag(), sizeof(int), d.stream()));
   d.sync();
-  ExpressionGraph& g = *lastGraph_;
-  if(!(flag & MTKC_FLAG_NONFINITE)) {
-    g.zeroGrads();  // consumed by the update (train.cpp:57), lazily zero
+  if(!(flag & MTKC_FLAG_NONFINITE))
     return;
-  }
-  --step_;  // the device skipped the update: nothing changed
+  step_ -= steps;  // the device skipped the update(s): parameters unchanged
+  ExpressionGraph& g = *lastGraph_;
+  std::vector<float> host((size_t)g.pool().used());
+  MTKC(mtkc_memcpy_d2h(host.data(), g.pool().grads()->ptr, host.size() * sizeof(float),
+                       d.stream()));
+  d.sync();
   std::string bad = "?";
   for(auto& name : g.paramNames()) {
-    Tensor& gr = g.paramGrad(name);
-    if(!gr.allFinite()) {
+    int64_t off = g.paramOffset(name), sz = g.paramValue(name).size();
+    bool finite = true;
+    for(int64_t i = 0; i < sz && finite; ++i)
+      finite = std::isfinite(host[(size_t)(off + i)]);
+    if(!finite) {
       bad = name;
       break;
     }

@@ -368,6 +368,7 @@ int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_
     return MTKC_OK;
   if(tk > MAX_TK || dk > MAX_DK || dk <= 0)
     return fail(MTKC_DIMENSION, "fused attention supports tk <= 512 and head dim <= 128");
+  ProfScope prof(S(stream), "attention", 4.0 * b * heads * tq * tk * dk);
   AttP p{out, ldo, probs, q, ldq, k, v, ldk, key_mask, b, tq, tk, heads, dk, scale, causal, flags};
   size_t smem = sizeof(float) * ((size_t)QB * (dk + 1) + (size_t)KC * (dk + 1) +
                                  (size_t)QB * (tk + 1));
@@ -390,6 +391,7 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
     return MTKC_OK;
   if(tk > MAX_TK || dk > MAX_DK || dk <= 0)
     return fail(MTKC_DIMENSION, "fused attention supports tk <= 512 and head dim <= 128");
+  ProfScope prof(S(stream), "attention", 8.0 * b * heads * tq * tk * dk);
   AttBP p{gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, dsbuf, b, tq, tk, heads, dk, scale,
           accumulate_q, accumulate_k, accumulate_v};
   size_t smemA = sizeof(float) * ((size_t)QB * (dk + 1) + (size_t)KC * (dk + 1) +

@@ -18,6 +18,25 @@ void count_launch(int n = 1);
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Event-bracketed profiling of one C-ABI call (mtkc_prof_enable).
+bool prof_on();
+void prof_begin(cudaStream_t st, void** token);
+void prof_end(cudaStream_t st, void* token, const char* cls, double work);
+struct ProfScope {
+  cudaStream_t st;
+  void* tok = nullptr;
+  const char* cls;
+  double work;
+  ProfScope(cudaStream_t s, const char* c, double w) : st(s), cls(c), work(w) {
+    if(prof_on())
+      prof_begin(st, &tok);
+  }
+  ~ProfScope() {
+    if(tok)
+      prof_end(st, tok, cls, work);
+  }
+};
+
 // Launch check used after every <<<>>>: counts the launch and converts a
 // launch failure into MTKC_CUDA with the kernel name.
 #define MTKC_POST_LAUNCH(name)                                  \

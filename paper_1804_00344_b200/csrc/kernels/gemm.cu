@@ -142,10 +142,12 @@ int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
   if(!a->A || !a->B || !a->C)
     return fail(MTKC_CONTRACT, "mtkc_gemm: null operand");
   int rc = MTKC_OK;
+  ProfScope prof(S(stream), "gemm_tc", 2.0 * a->M * a->N * a->K * a->batch);
   if(a->precision == MTKC_GEMM_TF32 && tc_gemm(*a, S(stream), &rc)) {
     t_last_path = 1;
     return rc;
   }
+  prof.cls = "gemm_simt";
   t_last_path = 0;
   GemmP p;
   p.M = a->M;

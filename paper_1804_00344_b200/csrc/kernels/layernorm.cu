@@ -177,6 +177,7 @@ int mtkc_layernorm(float* out, const float* x, const float* gain, const float* b
     return fail(MTKC_DIMENSION, "layer norm needs last extent >= 2");
   unsigned grid = (unsigned)cdiv(rows, LN_WARPS);
   cudaStream_t st = S(stream);
+  ProfScope prof(st, "layernorm", 8.0 * rows * d);  // read x, write y
   int v = (int)cdiv(d, 32);
   if(v <= 1)
     ln_fwd_kernel<1><<<grid, LN_WARPS * 32, 0, st>>>(out, x, gain, bias, eps, inv_std, xhat, rows, d);
@@ -203,6 +204,7 @@ int mtkc_layernorm_backward(const float* dy, const float* gain, const float* inv
   if(rows <= 0)
     return MTKC_OK;
   cudaStream_t st = S(stream);
+  ProfScope prof(st, "layernorm", 12.0 * rows * d);  // read dy, xhat; write dx
   int64_t nparts = cdiv(rows, LN_ROWS_PER_CTA);
   size_t smem = (size_t)LN_WARPS * 2 * (size_t)d * sizeof(float);
   bool usePart = dgain && workspace &&

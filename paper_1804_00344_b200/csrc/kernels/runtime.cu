@@ -4,7 +4,10 @@
 // mtkc_malloc'd slab.
 #include "common.cuh"
 
+#include <algorithm>
 #include <cstdio>
+#include <cstring>
+#include <vector>
 
 namespace mtkc {
 
@@ -27,6 +30,45 @@ int cuda_status(cudaError_t e, const char* where) {
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+static std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+
+// ------------------------------------------------------------ profiling
+namespace {
+struct ProfRec {
+  cudaEvent_t a, b;
+  const char* cls;
+  double work;
+};
+bool g_prof = false;
+std::vector<ProfRec> g_recs;
+std::vector<cudaEvent_t> g_evpool;
+
+cudaEvent_t take_event() {
+  if(g_evpool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = g_evpool.back();
+  g_evpool.pop_back();
+  return e;
+}
+}  // namespace
+
+bool prof_on() { return g_prof; }
+
+void prof_begin(cudaStream_t st, void** token) {
+  cudaEvent_t e = take_event();
+  cudaEventRecord(e, st);
+  *token = (void*)e;
+}
+
+void prof_end(cudaStream_t st, void* token, const char* cls, double work) {
+  cudaEvent_t e = take_event();
+  cudaEventRecord(e, st);
+  g_recs.push_back(ProfRec{(cudaEvent_t)token, e, cls, work});
+}
+
 }  // namespace mtkc
 
 using namespace mtkc;
@@ -36,6 +78,51 @@ extern "C" {
 const char* mtkc_last_error(void) { return t_err.c_str(); }
 
 uint64_t mtkc_launch_count(void) { return g_launches.load(); }
+uint64_t mtkc_h2d_bytes(void) { return g_h2d.load(); }
+uint64_t mtkc_d2h_bytes(void) { return g_d2h.load(); }
+
+int mtkc_prof_enable(int on) {
+  g_prof = on != 0;
+  return MTKC_OK;
+}
+
+int mtkc_prof_report(char* buf, size_t len) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if(e != cudaSuccess)
+    return cuda_status(e, "mtkc_prof_report");
+  struct Acc {
+    int64_t n = 0;
+    double ms = 0, work = 0;
+  };
+  std::vector<std::pair<std::string, Acc>> acc;
+  for(auto& r : g_recs) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto it = std::find_if(acc.begin(), acc.end(), [&](auto& p) { return p.first == r.cls; });
+    if(it == acc.end()) {
+      acc.push_back({r.cls, Acc{}});
+      it = acc.end() - 1;
+    }
+    it->second.n += 1;
+    it->second.ms += ms;
+    it->second.work += r.work;
+    g_evpool.push_back(r.a);
+    g_evpool.push_back(r.b);
+  }
+  g_recs.clear();
+  std::string out;
+  char line[256];
+  for(auto& [k, a] : acc) {
+    snprintf(line, sizeof(line), "%s %lld %.6f %.6e\n", k.c_str(), (long long)a.n, a.ms, a.work);
+    out += line;
+  }
+  if(buf && len) {
+    size_t n = std::min(len - 1, out.size());
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return MTKC_OK;
+}
 
 int mtkc_init(int device) { return cuda_status(cudaSetDevice(device), "cudaSetDevice"); }
 
@@ -67,6 +154,7 @@ int mtkc_host_free_pinned(void* ptr) { return cuda_status(cudaFreeHost(ptr), "cu
 int mtkc_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
   if(!bytes)
     return MTKC_OK;
+  g_h2d.fetch_add(bytes, std::memory_order_relaxed);
   return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S(stream)),
                      "cudaMemcpyAsync(H2D)");
 }
@@ -74,6 +162,7 @@ int mtkc_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
 int mtkc_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
   if(!bytes)
     return MTKC_OK;
+  g_d2h.fetch_add(bytes, std::memory_order_relaxed);
   return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(stream)),
                      "cudaMemcpyAsync(D2H)");
 }

@@ -196,6 +196,7 @@ int mtkc_xent_forward(const float* logits, const int32_t* targets, const float* 
                       float count, void* stream) {
   if(rows <= 0)
     return MTKC_OK;
+  ProfScope prof(S(stream), "xent", 4.0 * rows * vocab);  // read logits
   xent_fwd_kernel<<<(unsigned)rows, XT, 0, S(stream)>>>(logits, targets, mask, vocab, lse,
                                                        row_loss);
   MTKC_POST_LAUNCH("xent_fwd_kernel");
@@ -210,6 +211,7 @@ int mtkc_xent_backward(float* glogits, const float* logits, const float* lse,
                        void* stream) {
   if(rows <= 0)
     return MTKC_OK;
+  ProfScope prof(S(stream), "xent", (accumulate ? 12.0 : 8.0) * rows * vocab);
   int64_t per = cdiv(vocab, 4);
   unsigned gx = (unsigned)std::min<int64_t>(cdiv(per, 256), 8);
   dim3 grid(gx, (unsigned)rows);
@@ -227,6 +229,7 @@ int mtkc_adam_ema(float* theta, float* grad, float* m, float* v, float* avg, int
   if(((uintptr_t)theta | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v |
       (do_avg ? (uintptr_t)avg : 0)) % 16)
     return fail(MTKC_CONTRACT, "adam: buffers must be 16-byte aligned");
+  ProfScope prof(S(stream), "adam_ema", (do_avg ? 36.0 : 28.0) * n);
   adam_ema_kernel<<<grid1d(cdiv(n, 4), 256, 148 * 16), 256, 0, S(stream)>>>(
       theta, grad, m, v, avg, n, lr, beta1, beta2, eps, corr1, corr2, avg_beta, do_avg,
       zero_grad, flags);
