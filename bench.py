@@ -220,11 +220,13 @@ def run_b200(a):
     l0 = M.launch_count()
     e0 = M.event_record()
     words = 0.0
+    th0 = time.perf_counter()
     for _ in range(a.steps):
         grp = group(u)
         words += sum(b.target_tokens() for b in grp)
         stepper.update(grp, u, False)
         u += 1
+    host_ms = (time.perf_counter() - th0) * 1e3 / a.steps
     e1 = M.event_record()
     ms = M.event_elapsed_ms(e0, e1)
     launches = M.launch_count() - l0
@@ -252,6 +254,9 @@ def run_b200(a):
 
     # ---- per-kernel-class device time (events around each C-ABI call)
     M.sync()
+    # The GPU sleeps while the host queues the profiled steps, so the
+    # per-class event timings below measure device time, not host gaps.
+    M.gpu_sleep(int(max(200.0, 3 * host_ms * prof_steps) * 1e3))
     M.prof_enable(True)
     pe0 = M.event_record()
     for _ in range(prof_steps):
@@ -312,6 +317,7 @@ def run_b200(a):
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "loss_last": losses[-1] if losses else None},
             "gpu_launches": int(launches),
+            "host_submit_ms_per_step": round(host_ms, 3),
             "roofline": roof,
             "kernel_breakdown": breakdown,
             "cpu_baseline": cpu,

@@ -87,6 +87,7 @@ int mtkc_event_create(void** ev);
 int mtkc_event_destroy(void* ev);
 int mtkc_event_record(void* ev, void* stream);
 int mtkc_stream_wait_event(void* stream, void* ev);
+int mtkc_event_sync(void* ev);
 int mtkc_event_elapsed_ms(void* start, void* stop, float* ms);
 int mtkc_device_sync(void);
 /* Kernel-launch counter (every mtkc_* kernel launch increments it). */
@@ -101,6 +102,9 @@ uint64_t mtkc_d2h_bytes(void);
  * mtkc_prof_report synchronises and writes one line per class:
  *   "<class> <launches> <total_ms> <total_work>\n"  (then resets). */
 int mtkc_prof_enable(int on);
+/* Keep the stream busy for `us` microseconds (profiling aid: lets the host
+ * queue a whole step ahead so event timings measure device time only). */
+int mtkc_gpu_sleep(int64_t us, void* stream);
 int mtkc_prof_report(char* buf, size_t len);
 
 /* ======================================================================== */
@@ -225,6 +229,19 @@ int mtkc_gather_rows(float* out, const float* src, const int32_t* rows, int64_t 
 int mtkc_scatter_add_rows(float* out, const float* src, const int32_t* perm,
                           const int32_t* seg_start, const int32_t* uniq, int64_t n_uniq,
                           int64_t cols, float scale, void* stream);
+/* Same contract with long segments split into chunks of consecutive sorted
+ * positions so one frequent id (e.g. </s> padding) does not serialise the
+ * kernel.  chunk_start[c]..chunk_start[c+1] are chunk c's positions in perm,
+ * chunk_row[c] its table row, chunk_slot[c] = -1 for a segment that is a
+ * single chunk (added to out directly, in position order) or the partial
+ * slot it writes.  Multi-chunk segment m owns slots multi_first[m] ..
+ * multi_first[m+1]-1 and is added to row multi_row[m] in chunk order. */
+int mtkc_scatter_add_rows_chunked(float* out, const float* src, const int32_t* perm,
+                                  const int32_t* chunk_start, const int32_t* chunk_row,
+                                  const int32_t* chunk_slot, int64_t n_chunks,
+                                  const int32_t* multi_first, const int32_t* multi_row,
+                                  int64_t n_multi, float* partial, int64_t cols, float scale,
+                                  void* stream);
 
 /* ======================================================================== */
 /* layer norm (layerNormInto / layerNormBackward tensor.cpp:545-599)        */

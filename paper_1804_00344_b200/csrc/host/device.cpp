@@ -2,6 +2,7 @@
 #include "mtk/device.h"
 
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 namespace mtk {
@@ -63,6 +64,48 @@ float* Device::scratch(size_t bytes) {
 }
 
 void Device::sync() { MTKC(mtkc_stream_sync(stream_)); }
+
+void Device::upload(void* dst, const void* src, size_t bytes) {
+  if(!bytes)
+    return;
+  size_t need = (bytes + 255) & ~(size_t)255;
+  if(need > pinnedBytes_ / 2) {  // oversized: plain (possibly blocking) copy
+    MTKC(mtkc_memcpy_h2d(dst, src, bytes, stream_));
+    return;
+  }
+  if(!pinned_) {
+    pinnedBytes_ = (size_t)64 << 20;
+    void* p = nullptr;
+    MTKC(mtkc_host_alloc_pinned(&p, pinnedBytes_));
+    pinned_ = (char*)p;
+  }
+  if(head_ + need > pinnedBytes_)
+    head_ = 0;
+  size_t b = head_, e = head_ + need;
+  // wait for earlier copies still reading the region we are about to reuse
+  for(size_t i = 0; i < inflight_.size();) {
+    Pending& q = inflight_[i];
+    if(q.begin < e && b < q.end) {
+      MTKC(mtkc_event_sync(q.event));  // host waits for that copy only
+      eventPool_.push_back(q.event);
+      inflight_.erase(inflight_.begin() + (long)i);
+    } else {
+      ++i;
+    }
+  }
+  std::memcpy(pinned_ + b, src, bytes);
+  MTKC(mtkc_memcpy_h2d(dst, pinned_ + b, bytes, stream_));
+  void* ev = nullptr;
+  if(!eventPool_.empty()) {
+    ev = eventPool_.back();
+    eventPool_.pop_back();
+  } else {
+    MTKC(mtkc_event_create(&ev));
+  }
+  MTKC(mtkc_event_record(ev, stream_));
+  inflight_.push_back(Pending{b, e, ev});
+  head_ = e;
+}
 
 void Device::checkFlags(const std::string& where) {
   int host = 0;

@@ -271,7 +271,7 @@ void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
 std::shared_ptr<DeviceBuffer> uploadIntsTo(ExpressionGraph& g, const std::vector<int32_t>& v,
                                            int64_t* off) {
   auto [buf, o] = g.arena().alloc(std::max<int64_t>((int64_t)v.size(), 1));
-  MTKC(mtkc_memcpy_h2d(buf->ptr + o, v.data(), v.size() * sizeof(int32_t), stream()));
+  Device::get().upload(buf->ptr + o, v.data(), v.size() * sizeof(int32_t));
   *off = o;
   return buf;
 }
@@ -282,50 +282,98 @@ Tensor uploadTensor(ExpressionGraph& g, const Tensor& t) {
   if(t.onDevice())
     MTKC(mtkc_memcpy_d2d(d.dev(), t.devc(), (size_t)t.size() * sizeof(float), stream()));
   else
-    MTKC(mtkc_memcpy_h2d(d.dev(), t.data(), (size_t)t.size() * sizeof(float), stream()));
+    Device::get().upload(d.dev(), t.data(), (size_t)t.size() * sizeof(float));
   return d;
 }
 
-// Deterministic scatter plan: positions stably sorted by id.
+// A read-only device view of a host constant (mask, position table): the
+// tensor's own device copy, shared by every node and every copy of it, so a
+// batch mask used by 18 attention nodes is uploaded once.
+std::shared_ptr<Tensor> sharedConst(const Tensor& t) { return std::make_shared<Tensor>(t); }
+
+// Deterministic scatter plan: positions stably sorted by id (counting
+// sort), each id's segment split into chunks of at most kChunk positions.
 struct ScatterPlan {
   std::shared_ptr<DeviceBuffer> buf;
-  int64_t permOff = 0, segOff = 0, uniqOff = 0, nUniq = 0;
+  int64_t permOff = 0, cstartOff = 0, crowOff = 0, cslotOff = 0, mfirstOff = 0, mrowOff = 0;
+  int64_t nChunks = 0, nMulti = 0, nSlots = 0;
 };
 
+constexpr int32_t kChunk = 32;
+
 ScatterPlan makeScatterPlan(ExpressionGraph& g, const std::vector<int32_t>& ids) {
+  int32_t maxId = 0;
+  for(int32_t v : ids)
+    maxId = std::max(maxId, v);
+  std::vector<int32_t> cnt((size_t)maxId + 2, 0);
+  for(int32_t v : ids)
+    ++cnt[(size_t)v + 1];
+  for(size_t i = 1; i < cnt.size(); ++i)
+    cnt[i] += cnt[i - 1];
   std::vector<int32_t> perm(ids.size());
-  for(size_t i = 0; i < ids.size(); ++i)
-    perm[i] = (int32_t)i;
-  std::stable_sort(perm.begin(), perm.end(),
-                   [&](int32_t a, int32_t b) { return ids[(size_t)a] < ids[(size_t)b]; });
-  std::vector<int32_t> all;  // perm | seg | uniq
-  all.reserve(perm.size() * 3 + 1);
-  all.insert(all.end(), perm.begin(), perm.end());
-  std::vector<int32_t> seg, uniq;
-  for(size_t k = 0; k < perm.size(); ++k)
-    if(k == 0 || ids[(size_t)perm[k]] != ids[(size_t)perm[k - 1]]) {
-      seg.push_back((int32_t)k);
-      uniq.push_back(ids[(size_t)perm[k]]);
+  {
+    std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+    for(size_t i = 0; i < ids.size(); ++i)
+      perm[(size_t)pos[(size_t)ids[i]]++] = (int32_t)i;
+  }
+  std::vector<int32_t> cstart, crow, cslot, mfirst, mrow;
+  int32_t slots = 0;
+  for(int32_t id = 0; id <= maxId; ++id) {
+    int32_t s0 = cnt[(size_t)id], s1 = cnt[(size_t)id + 1];
+    if(s0 == s1)
+      continue;
+    int32_t len = s1 - s0;
+    if(len <= kChunk) {
+      cstart.push_back(s0);
+      crow.push_back(id);
+      cslot.push_back(-1);
+      continue;
     }
-  seg.push_back((int32_t)perm.size());
+    mfirst.push_back(slots);
+    mrow.push_back(id);
+    for(int32_t k = s0; k < s1; k += kChunk) {
+      cstart.push_back(k);
+      crow.push_back(id);
+      cslot.push_back(slots++);
+    }
+  }
   ScatterPlan p;
-  p.segOff = (int64_t)all.size();
-  all.insert(all.end(), seg.begin(), seg.end());
-  p.uniqOff = (int64_t)all.size();
-  all.insert(all.end(), uniq.begin(), uniq.end());
-  p.nUniq = (int64_t)uniq.size();
+  p.nChunks = (int64_t)crow.size();
+  p.nMulti = (int64_t)mrow.size();
+  p.nSlots = slots;
+  cstart.push_back((int32_t)perm.size());
+  mfirst.push_back(slots);
+  std::vector<int32_t> all;
+  auto put = [&](const std::vector<int32_t>& v) {
+    int64_t o = (int64_t)all.size();
+    all.insert(all.end(), v.begin(), v.end());
+    return o;
+  };
+  p.permOff = put(perm);
+  p.cstartOff = put(cstart);
+  p.crowOff = put(crow);
+  p.cslotOff = put(cslot);
+  p.mfirstOff = put(mfirst);
+  p.mrowOff = put(mrow);
   int64_t off = 0;
   p.buf = uploadIntsTo(g, all, &off);
-  p.permOff = off;
-  p.segOff += off;
-  p.uniqOff += off;
+  for(int64_t* o : {&p.permOff, &p.cstartOff, &p.crowOff, &p.cslotOff, &p.mfirstOff, &p.mrowOff})
+    *o += off;
   return p;
 }
 
-void scatterPlanAdd(const ScatterPlan& p, float* out, const float* src, int64_t cols, float s) {
+void scatterPlanAdd(ExpressionGraph& g, const ScatterPlan& p, float* out, const float* src,
+                    int64_t cols, float s) {
   const int32_t* base = (const int32_t*)p.buf->ptr;
-  MTKC(mtkc_scatter_add_rows(out, src, base + p.permOff, base + p.segOff, base + p.uniqOff,
-                             p.nUniq, cols, s, stream()));
+  float* partial = nullptr;
+  if(p.nSlots > 0) {
+    auto [buf, off] = g.arena().alloc(p.nSlots * cols);
+    partial = buf->ptr + off;
+  }
+  MTKC(mtkc_scatter_add_rows_chunked(out, src, base + p.permOff, base + p.cstartOff,
+                                     base + p.crowOff, base + p.cslotOff, p.nChunks,
+                                     base + p.mfirstOff, base + p.mrowOff, p.nMulti, partial,
+                                     cols, s, stream()));
 }
 
 void pad4(const Shape& s, int64_t out[4]) { s.pad4(out); }
@@ -806,7 +854,7 @@ NodeRef ExpressionGraph::gatherRows(NodeRef a, std::vector<int64_t> rows) {
   n.bwd = [=](ExpressionGraph& g, Node& n) {
     const float* go = g.gradSrc(n);
     float* dst = accPtr(g, n.inputs[0], srcRows * cols);
-    scatterPlanAdd(*plan, dst, go, cols, 1.f);
+    scatterPlanAdd(g, *plan, dst, go, cols, 1.f);
   };
   return addNode(std::move(n));
 }
@@ -872,7 +920,7 @@ NodeRef ExpressionGraph::softmax(NodeRef a, Tensor mask) {
       if(md[i] != 1 && md[i] != xd[i])
         throw DimensionError("operand shape " + mask.shape().str() +
                              " incompatible with broadcast result");
-    dmask = uploadTensor(*this, mask);
+    dmask = mask;  // shared device copy, uploaded on first use
   }
   auto keep = std::make_shared<Tensor>(dmask);
   n.aux = keep;
@@ -979,7 +1027,7 @@ NodeRef ExpressionGraph::embed(NodeRef table, const IntMat& ids) {
   n.bwd = [aux, e, vocab](ExpressionGraph& g, Node& n) {
     const float* go = g.gradSrc(n);
     float* dst = accPtr(g, n.inputs[0], vocab * e);
-    scatterPlanAdd(aux->plan, dst, go, e, 1.f);
+    scatterPlanAdd(g, aux->plan, dst, go, e, 1.f);
   };
   return addNode(std::move(n));
 }
@@ -992,7 +1040,7 @@ NodeRef ExpressionGraph::scaleAddConst(NodeRef x, Real s, const Tensor& pe) {
   n.op = "posenc";
   n.shape = x.shape;
   n.inputs = {x.index};
-  auto c = std::make_shared<Tensor>(uploadTensor(*this, pe));
+  auto c = sharedConst(pe);
   n.aux = c;
   int64_t period = pe.size();
   n.fwd = [c, s, period](ExpressionGraph& g, Node& n) {
@@ -1020,7 +1068,7 @@ NodeRef ExpressionGraph::maskBlend(NodeRef a, NodeRef b, const Tensor& m) {
   n.op = "maskBlend";
   n.shape = a.shape;
   n.inputs = {a.index, b.index};
-  auto dm = std::make_shared<Tensor>(uploadTensor(*this, m));
+  auto dm = sharedConst(m);
   n.aux = dm;
   int64_t rows = a.shape[0], cols = a.shape[1];
   n.fwd = [dm, rows, cols](ExpressionGraph& g, Node& n) {
@@ -1082,7 +1130,7 @@ NodeRef ExpressionGraph::attention(NodeRef q, NodeRef k, NodeRef v, const Tensor
   n.inputs = {q.index, k.index, v.index};
   auto aux = std::make_shared<AttAux>();
   if(!keyMask.empty()) {
-    aux->mask = uploadTensor(*this, keyMask);
+    aux->mask = keyMask;  // shared device copy of the batch mask
     aux->hasMask = true;
   }
   n.aux = aux;
@@ -1176,7 +1224,7 @@ NodeRef ExpressionGraph::crossEntropy(NodeRef logits, const IntMat& targets, con
     for(int64_t r = 0; r < positions; ++r)  // graph.cpp:898-902 (sum of m in row order)
       if(m[r] != Real(0))
         count += m[r];
-    aux->mask = uploadTensor(*this, mask);
+    aux->mask = mask;  // shared device copy of the batch mask
     aux->hasMask = true;
   }
   aux->count = count;

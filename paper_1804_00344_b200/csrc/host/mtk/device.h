@@ -6,6 +6,7 @@
 #include <cstddef>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "mtk/tensor.h"
 #include "mtk_cuda.h"
@@ -31,6 +32,11 @@ public:
   float* scratch(size_t bytes);  // stream-ordered scratch, grows on demand
   size_t scratchBytes() const { return scratchBytes_; }
 
+  // Asynchronous host->device copy on the compute stream through a pinned
+  // staging ring (a pageable cudaMemcpyAsync may block the host until the
+  // stream drains, which would serialise graph building with the GPU).
+  void upload(void* dst, const void* src, size_t bytes);
+
   void sync();        // synchronise the compute stream
   // synchronise, read and clear the flag word, throw the mapped error
   void checkFlags(const std::string& where);
@@ -46,6 +52,15 @@ private:
   Precision precision_ = Precision::TF32;
   std::shared_ptr<DeviceBuffer> scratch_;
   size_t scratchBytes_ = 0;
+  // pinned staging ring
+  struct Pending {
+    size_t begin, end;
+    void* event;
+  };
+  char* pinned_ = nullptr;
+  size_t pinnedBytes_ = 0, head_ = 0;
+  std::vector<Pending> inflight_;
+  std::vector<void*> eventPool_;
 };
 
 // Map an mtkc status code to the reference's exception types.

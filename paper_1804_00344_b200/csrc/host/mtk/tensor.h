@@ -100,6 +100,7 @@ private:
     std::vector<Real> data;
     bool valid = false;
     bool dirty = false;
+    std::shared_ptr<DeviceBuffer> devbuf;  // device copy shared by all copies of the tensor
   };
   void ensureDevice() const;
   void ensureHost() const;

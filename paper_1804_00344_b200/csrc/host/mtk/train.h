@@ -133,8 +133,11 @@ public:
   // (one synchronisation) unless `readLoss` is false.
   UpdateResult update(const std::vector<const Batch*>& batches, int64_t updateIndex,
                       bool readLoss = true);
+  // accumulated host milliseconds in graph build / forward / backward
+  std::vector<double> hostTimes() const { return {hostTimes_[0], hostTimes_[1], hostTimes_[2]}; }
 
 private:
+  double hostTimes_[3] = {0, 0, 0};
   const Model& model_;
   ExpressionGraph& g_;
   Adam& adam_;

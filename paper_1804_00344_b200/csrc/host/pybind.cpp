@@ -118,6 +118,7 @@ PYBIND11_MODULE(_mtk, m) {
   m.def("h2d_bytes", [] { return (uint64_t)mtkc_h2d_bytes(); });
   m.def("d2h_bytes", [] { return (uint64_t)mtkc_d2h_bytes(); });
   m.def("prof_enable", [](bool on) { MTKC(mtkc_prof_enable(on ? 1 : 0)); });
+  m.def("gpu_sleep", [](int64_t us) { MTKC(mtkc_gpu_sleep(us, Device::get().stream())); });
   // CUDA events on the compute stream (the stream every kernel runs on)
   m.def("event_record", [] {
     void* e = nullptr;
@@ -463,7 +464,8 @@ PYBIND11_MODULE(_mtk, m) {
            [](SyncStepper& s, const std::vector<const Batch*>& batches, int64_t u, bool read) {
              return s.update(batches, u, read);
            },
-           py::arg("batches"), py::arg("update_index"), py::arg("read_loss") = true);
+           py::arg("batches"), py::arg("update_index"), py::arg("read_loss") = true)
+      .def("host_times", &SyncStepper::hostTimes);
 
   m.def("mix_seed", &mixSeed);
 }

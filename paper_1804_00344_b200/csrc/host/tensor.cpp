@@ -40,16 +40,43 @@ void Shape::pad4(int64_t out[4]) const {
 
 // --------------------------------------------------------- DeviceBuffer
 
+// Caching device allocator: cudaMalloc/cudaFree synchronise the device, so
+// steady-state training must never call them.  Freed blocks go to a size-
+// keyed free list and are reused.  Every kernel runs on the one compute
+// stream, so a block released by the host may be handed out again at once:
+// work queued later on the stream runs after all work that used it.
+namespace {
+struct BlockCache {
+  std::map<size_t, std::vector<void*>> free;
+  static size_t round(size_t bytes) {
+    if(bytes <= ((size_t)1 << 20))
+      return (bytes + 511) & ~(size_t)511;
+    return (bytes + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);
+  }
+};
+BlockCache& cache() {
+  static BlockCache* c = new BlockCache();  // process lifetime
+  return *c;
+}
+}  // namespace
+
 DeviceBuffer::DeviceBuffer(size_t n) : elems(n) {
   Device::get();
+  size_t bytes = BlockCache::round(std::max<size_t>(n, 1) * sizeof(float));
+  auto& fl = cache().free[bytes];
+  if(!fl.empty()) {
+    ptr = (float*)fl.back();
+    fl.pop_back();
+    return;
+  }
   void* p = nullptr;
-  MTKC(mtkc_malloc(&p, std::max<size_t>(n, 1) * sizeof(float)));
+  MTKC(mtkc_malloc(&p, bytes));
   ptr = (float*)p;
 }
 
 DeviceBuffer::~DeviceBuffer() {
   if(owned && ptr)
-    mtkc_free(ptr);
+    cache().free[BlockCache::round(std::max<size_t>(elems, 1) * sizeof(float))].push_back(ptr);
 }
 
 // ---------------------------------------------------------------- Tensor
@@ -79,14 +106,20 @@ Tensor::Tensor(Shape shape, std::shared_ptr<DeviceBuffer> buf, int64_t offset)
 
 void Tensor::ensureDevice() const {
   if(!buf_) {
-    buf_ = std::make_shared<DeviceBuffer>((size_t)size());
-    off_ = 0;
-    if(!host_ || !host_->valid)
-      MTKC(mtkc_memset(buf_->ptr, 0, (size_t)size() * sizeof(float), Device::get().stream()));
+    if(host_ && host_->devbuf) {  // another copy of this tensor already uploaded
+      buf_ = host_->devbuf;
+      off_ = 0;
+    } else {
+      buf_ = std::make_shared<DeviceBuffer>((size_t)size());
+      off_ = 0;
+      if(host_)
+        host_->devbuf = buf_;
+      if(!host_ || !host_->valid)
+        MTKC(mtkc_memset(buf_->ptr, 0, (size_t)size() * sizeof(float), Device::get().stream()));
+    }
   }
   if(host_ && host_->dirty) {
-    MTKC(mtkc_memcpy_h2d(buf_->ptr + off_, host_->data.data(), (size_t)size() * sizeof(float),
-                         Device::get().stream()));
+    Device::get().upload(buf_->ptr + off_, host_->data.data(), (size_t)size() * sizeof(float));
     host_->dirty = false;
   }
 }

@@ -248,9 +248,16 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
     g_.setSeed(mixSeed(opts_.seed, updateIndex, i));
     Real w = (Real)tokens[(size_t)i] / (Real)total;  // train.cpp:262-266
     g_.setLossScale(w);
+    auto t0 = std::chrono::steady_clock::now();
     NodeRef loss = model_.buildLoss(g_, *batches[(size_t)i]);
+    auto t1 = std::chrono::steady_clock::now();
     g_.forward();
+    auto t2 = std::chrono::steady_clock::now();
     g_.backward(loss);
+    auto t3 = std::chrono::steady_clock::now();
+    hostTimes_[0] += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    hostTimes_[1] += std::chrono::duration<double, std::milli>(t2 - t1).count();
+    hostTimes_[2] += std::chrono::duration<double, std::milli>(t3 - t2).count();
     MTKC(mtkc_axpy(lossAcc_->ptr, loss.val().devc(), w, 1, d.stream()));
   }
   g_.setLossScale(1);

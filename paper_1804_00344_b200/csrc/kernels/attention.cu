@@ -356,6 +356,220 @@ int set_smem(const void* fn, size_t bytes) {
       "attention smem attribute");
 }
 
+// ---------------------------------------------------------------------------
+// Single-tile fast path: tq, tk <= 64 and dk <= 64 (every BASELINE config:
+// sentences of 17..33 tokens, d_k = 64).  One CTA of 256 threads owns one
+// (batch row, head); all operands sit in shared memory and every product is
+// a 64x64 register-tiled micro-GEMM (each thread a 4x4 block, float4 smem
+// reads, FMA).  Row reductions of the softmax stay inside a 16-lane group.
+constexpr int T64 = 64;
+constexpr int TILE = T64 * T64;  // floats per staged 64x64 operand
+
+// acc[4][4] += sum_k At[k][m] * Bt[k][n] for this thread's rows m = 4ty..,
+// columns n = 4tx..
+__device__ __forceinline__ void mm64(const float* At, const float* Bt, int K, float acc[4][4],
+                                     int ty, int tx) {
+#pragma unroll 4
+  for(int k = 0; k < K; ++k) {
+    float4 a = *reinterpret_cast<const float4*>(At + k * T64 + ty * 4);
+    float4 b = *reinterpret_cast<const float4*>(Bt + k * T64 + tx * 4);
+    float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for(int i = 0; i < 4; ++i)
+#pragma unroll
+      for(int j = 0; j < 4; ++j)
+        acc[i][j] = __fmaf_rn(av[i], bv[j], acc[i][j]);
+  }
+}
+
+// dst[r][c] = src[(row0 + r) * ld + col0 + c] (natural) or dst[c][r]
+// (transposed), zero outside [rows x cols].
+__device__ __forceinline__ void stage(float* dst, const float* src, int64_t ld, int rows,
+                                      int cols, bool transpose) {
+  for(int e = threadIdx.x; e < TILE; e += blockDim.x) {
+    int r = e / T64, c = e % T64;
+    float v = (r < rows && c < cols) ? src[(int64_t)r * ld + c] : 0.f;
+    if(transpose)
+      dst[c * T64 + r] = v;
+    else
+      dst[r * T64 + c] = v;
+  }
+}
+
+__device__ __forceinline__ float grp_max(float v) {
+#pragma unroll
+  for(int o = 8; o > 0; o >>= 1)
+    v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float grp_sum(float v) {
+#pragma unroll
+  for(int o = 8; o > 0; o >>= 1)
+    v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(256) attn_fwd_tile_kernel(AttP p) {
+  extern __shared__ float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  float* Qt = sm;             // [dk][i]
+  float* Kt = Qt + TILE;      // [dk][j]
+  float* V = Kt + TILE;       // [j][c]
+  float* Pt = V + TILE;       // [j][i]
+  const int h = blockIdx.x;
+  const int64_t bi = blockIdx.y;
+  const int tq = (int)p.tq, tk = (int)p.tk, dk = (int)p.dk;
+  const int64_t hoff = (int64_t)h * dk;
+  stage(Qt, p.q + bi * p.tq * p.ldq + hoff, p.ldq, tq, dk, true);
+  stage(Kt, p.k + bi * p.tk * p.ldk + hoff, p.ldk, tk, dk, true);
+  stage(V, p.v + bi * p.tk * p.ldk + hoff, p.ldk, tk, dk, false);
+  __syncthreads();
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float s[4][4] = {};
+  mm64(Qt, Kt, dk, s, ty, tx);
+  float* P = p.probs + ((bi * p.heads + h) * p.tq) * p.tk;
+#pragma unroll
+  for(int a = 0; a < 4; ++a) {
+    int i = ty * 4 + a;
+    bool ok[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for(int c = 0; c < 4; ++c) {
+      int j = tx * 4 + c;
+      ok[c] = i < tq && j < tk && key_ok(p, bi, i, j);
+      s[a][c] = p.scale * s[a][c];
+      if(ok[c])
+        mx = fmaxf(mx, s[a][c]);
+    }
+    mx = grp_max(mx);
+    bool any = mx != -INFINITY;
+    float e[4], sum = 0.f;
+#pragma unroll
+    for(int c = 0; c < 4; ++c) {
+      e[c] = ok[c] ? expf(s[a][c] - mx) : 0.f;
+      sum += e[c];
+    }
+    sum = grp_sum(sum);
+    if(i < tq && !any && tx == 0 && p.flags)
+      atomicOr(p.flags, MTKC_FLAG_MASKED_ROW);
+#pragma unroll
+    for(int c = 0; c < 4; ++c) {
+      int j = tx * 4 + c;
+      float y = any ? e[c] / sum : 0.f;
+      Pt[j * T64 + i] = y;
+      if(i < tq && j < tk)
+        P[(int64_t)i * tk + j] = y;
+    }
+  }
+  __syncthreads();
+  float o[4][4] = {};
+  mm64(Pt, V, tk, o, ty, tx);
+#pragma unroll
+  for(int a = 0; a < 4; ++a) {
+    int i = ty * 4 + a;
+    if(i >= tq)
+      continue;
+    float* dst = p.out + (bi * p.tq + i) * p.ldo + hoff;
+#pragma unroll
+    for(int c = 0; c < 4; ++c) {
+      int col = tx * 4 + c;
+      if(col < dk)
+        dst[col] = o[a][c];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) attn_bwd_tile_kernel(AttBP p) {
+  extern __shared__ float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  float* dO = sm;            // [i][c]
+  float* B1 = dO + TILE;     // dOt [c][i], then Q [i][c]
+  float* B2 = B1 + TILE;     // Vt [c][j], then K [j][c]
+  float* Pn = B2 + TILE;     // P [i][j]
+  float* dS = Pn + TILE;     // [i][j]
+  float* dSt = dS + TILE;    // [j][i]
+  const int h = blockIdx.x;
+  const int64_t bi = blockIdx.y;
+  const int tq = (int)p.tq, tk = (int)p.tk, dk = (int)p.dk;
+  const int64_t hoff = (int64_t)h * dk;
+  const float* go = p.gout + bi * p.tq * p.ldo + hoff;
+  stage(dO, go, p.ldo, tq, dk, false);
+  stage(B1, go, p.ldo, tq, dk, true);
+  stage(B2, p.v + bi * p.tk * p.ldk + hoff, p.ldk, tk, dk, true);
+  stage(Pn, p.probs + ((bi * p.heads + h) * p.tq) * p.tk, p.tk, tq, tk, false);
+  __syncthreads();
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float dp[4][4] = {};
+  mm64(B1, B2, dk, dp, ty, tx);  // dP = dO V^T
+  float* G = p.ds + ((bi * p.heads + h) * p.tq) * p.tk;
+#pragma unroll
+  for(int a = 0; a < 4; ++a) {
+    int i = ty * 4 + a;
+    float pv[4], d = 0.f;
+#pragma unroll
+    for(int c = 0; c < 4; ++c) {
+      pv[c] = Pn[i * T64 + tx * 4 + c];
+      d += dp[a][c] * pv[c];
+    }
+    d = grp_sum(d);
+#pragma unroll
+    for(int c = 0; c < 4; ++c) {
+      int j = tx * 4 + c;
+      float gval = p.scale * (pv[c] * (dp[a][c] - d));
+      dS[i * T64 + j] = gval;
+      dSt[j * T64 + i] = gval;
+      if(i < tq && j < tk)
+        G[(int64_t)i * tk + j] = gval;
+    }
+  }
+  __syncthreads();
+  stage(B1, p.q + bi * p.tq * p.ldq + hoff, p.ldq, tq, dk, false);
+  stage(B2, p.k + bi * p.tk * p.ldk + hoff, p.ldk, tk, dk, false);
+  __syncthreads();
+  float acc[4][4];
+  auto store = [&](float* base, int64_t ld, int rows, int acc_mode) {
+#pragma unroll
+    for(int a = 0; a < 4; ++a) {
+      int r = ty * 4 + a;
+      if(r >= rows)
+        continue;
+#pragma unroll
+      for(int c = 0; c < 4; ++c) {
+        int col = tx * 4 + c;
+        if(col < dk) {
+          float* dst = base + (int64_t)r * ld + col;
+          *dst = acc_mode ? *dst + acc[a][c] : acc[a][c];
+        }
+      }
+    }
+  };
+  // dQ = dS K
+  for(auto& r : acc)
+    for(float& x : r)
+      x = 0.f;
+  mm64(dSt, B2, tk, acc, ty, tx);
+  store(p.gq + bi * p.tq * p.ldq + hoff, p.ldq, tq, p.accQ);
+  // dK = dS^T Q
+  for(auto& r : acc)
+    for(float& x : r)
+      x = 0.f;
+  mm64(dS, B1, tq, acc, ty, tx);
+  store(p.gk + bi * p.tk * p.ldk + hoff, p.ldk, tk, p.accK);
+  // dV = P^T dO
+  for(auto& r : acc)
+    for(float& x : r)
+      x = 0.f;
+  mm64(Pn, dO, tq, acc, ty, tx);
+  store(p.gv + bi * p.tk * p.ldk + hoff, p.ldk, tk, p.accV);
+}
+
+bool tile_path(int64_t tq, int64_t tk, int64_t dk, int64_t ldq, int64_t ldk, int64_t ldo) {
+  (void)ldq;
+  (void)ldk;
+  (void)ldo;
+  return tq <= T64 && tk <= T64 && dk <= T64 && dk % 4 == 0 && !getenv("MTK_ATTN_GENERIC");
+}
+
 }  // namespace
 
 extern "C" {
@@ -370,6 +584,15 @@ int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_
     return fail(MTKC_DIMENSION, "fused attention supports tk <= 512 and head dim <= 128");
   ProfScope prof(S(stream), "attention", 4.0 * b * heads * tq * tk * dk);
   AttP p{out, ldo, probs, q, ldq, k, v, ldk, key_mask, b, tq, tk, heads, dk, scale, causal, flags};
+  if(tile_path(tq, tk, dk, ldq, ldk, ldo)) {
+    size_t smem = 4 * TILE * sizeof(float);
+    int rc = set_smem((const void*)attn_fwd_tile_kernel, smem);
+    if(rc)
+      return rc;
+    attn_fwd_tile_kernel<<<dim3((unsigned)heads, (unsigned)b), 256, smem, S(stream)>>>(p);
+    MTKC_POST_LAUNCH("attn_fwd_tile_kernel");
+    return MTKC_OK;
+  }
   size_t smem = sizeof(float) * ((size_t)QB * (dk + 1) + (size_t)KC * (dk + 1) +
                                  (size_t)QB * (tk + 1));
   int rc = set_smem((const void*)attn_fwd_kernel, smem);
@@ -394,6 +617,15 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
   ProfScope prof(S(stream), "attention", 8.0 * b * heads * tq * tk * dk);
   AttBP p{gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, dsbuf, b, tq, tk, heads, dk, scale,
           accumulate_q, accumulate_k, accumulate_v};
+  if(tile_path(tq, tk, dk, ldq, ldk, ldo)) {
+    size_t smem = 6 * TILE * sizeof(float);
+    int rc = set_smem((const void*)attn_bwd_tile_kernel, smem);
+    if(rc)
+      return rc;
+    attn_bwd_tile_kernel<<<dim3((unsigned)heads, (unsigned)b), 256, smem, S(stream)>>>(p);
+    MTKC_POST_LAUNCH("attn_bwd_tile_kernel");
+    return MTKC_OK;
+  }
   size_t smemA = sizeof(float) * ((size_t)QB * (dk + 1) + (size_t)KC * (dk + 1) +
                                   (size_t)QB * (tk + 1));
   int rc = set_smem((const void*)attn_bwd_q_kernel, smemA);

@@ -37,6 +37,19 @@ __global__ void binary_kernel(BinP p) {
   }
 }
 
+// same-shape operands: contiguous, 16-byte vectors
+__global__ void binary_same4_kernel(int op, float4* out, const float4* a, const float4* b,
+                                    int64_t n4, int* flags) {
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    float4 x = a[i], y = b[i];
+    if(op == MTKC_DIV && flags && (y.x == 0.f || y.y == 0.f || y.z == 0.f || y.w == 0.f))
+      atomicOr(flags, MTKC_FLAG_DIV_ZERO);
+    out[i] = make_float4(apply_binary(op, x.x, y.x), apply_binary(op, x.y, y.y),
+                         apply_binary(op, x.z, y.z), apply_binary(op, x.w, y.w));
+  }
+}
+
 __global__ void unary_kernel(int op, float* out, const float* a, int64_t n) {
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x)
@@ -232,6 +245,15 @@ int mtkc_ewise_binary(int op, float* out, const int64_t od[4], const float* a,
   }
   if(p.n == 0)
     return MTKC_OK;
+  bool same = true;
+  for(int i = 0; i < 4; ++i)
+    same &= ad[i] == od[i] && bd[i] == od[i];
+  if(same && p.n % 4 == 0 && ((uintptr_t)out | (uintptr_t)a | (uintptr_t)b) % 16 == 0) {
+    binary_same4_kernel<<<grid1d(p.n / 4, 256), 256, 0, S(stream)>>>(
+        op, (float4*)out, (const float4*)a, (const float4*)b, p.n / 4, flags);
+    MTKC_POST_LAUNCH("binary_same4_kernel");
+    return MTKC_OK;
+  }
   binary_kernel<<<grid1d(p.n, 256), 256, 0, S(stream)>>>(p);
   MTKC_POST_LAUNCH("binary_kernel");
   return MTKC_OK;

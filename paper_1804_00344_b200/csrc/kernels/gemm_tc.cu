@@ -5,15 +5,18 @@
 // Data stays fp32 in HBM (the reference's storage type); operands are fed
 // to tcgen05.mma kind::tf32 straight from TMA-staged shared memory and
 // accumulate in fp32 in TMEM.  Every transpose case is a descriptor choice,
-// not a copy: op(A)/op(B) are loaded K-major or MN-major with 128-byte
-// swizzle, so dW = X^T dY and dX = dY W^T read the forward activations in
-// place.
+// not a copy: op(A)/op(B) are loaded K-major (128-byte swizzle) or MN-major
+// (128-byte swizzle with 32-byte atoms, the tf32 MN-major layout), so
+// dW = X^T dY and dX = dY W^T read the forward activations in place.
 //
-// Structure (one CTA per 128 x BN output tile, optionally split over K):
-//   warp 0      TMA producer   (one elected lane, ST-stage mbarrier ring)
-//   warp 1      MMA issuer     (one elected lane; owns the TMEM allocation)
-//   warps 2..5  epilogue       (tcgen05.ld 32x32b -> alpha/beta/bias/relu/
-//                               gate -> st.global, or split-K partials)
+// Persistent, warp-specialised kernel (one CTA per SM):
+//   warp 0      TMA producer   (one lane; ST-stage smem ring, mbarriers)
+//   warp 1      MMA issuer     (one lane; owns a double-buffered TMEM
+//                               accumulator, 2 x BN fp32 columns)
+//   warps 2..5  epilogue       (tcgen05.ld 32x32b -> per-warp smem transpose
+//                               -> alpha/bias/ReLU/gate/beta*C -> coalesced
+//                               128-byte row stores, or split-K partials)
+// The epilogue of tile i overlaps the main loop of tile i+1.
 #include <cuda.h>
 
 #include <cstring>
@@ -27,8 +30,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per 128-byte swizzle row
-constexpr int ST = 4;   // pipeline stages
 constexpr int TC_THREADS = 192;
+constexpr int EPI_STRIDE = 33;  // padded 32x32 transpose tile
 
 // ---------------------------------------------------------------- PTX
 
@@ -44,6 +47,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -141,38 +148,58 @@ struct TcP {
   float* part;  // split-K partials [splits][M][N] (ld = N), or nullptr
   int kbPerSplit;
   int numKb;
+  int mt, nt, splits;
+  int numTiles;
+  int tmaStore;  // 1: epilogue writes C (or 3-d partials) through a TMA store map
+  int dbg;  // profiling switches (MTK_GEMM_DEBUG): 1 = no epilogue stores, 2 = no MMAs
+};
+
+template <int BN>
+struct TcSmem {
+  static constexpr uint32_t A_BYTES = BM * BK * 4;
+  static constexpr uint32_t B_BYTES = BN * BK * 4;
+  static constexpr int ST = BN == 256 ? 3 : 4;
+  // per epilogue warp: two 32x32 fp32 staging tiles (128B-swizzled, TMA store)
+  static constexpr size_t EPI_BYTES = 4 * 2 * 32 * 32 * sizeof(float);
+  static constexpr size_t BYTES = 1024 + ST * (size_t)(A_BYTES + B_BYTES) + EPI_BYTES + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tf32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
-                        const __grid_constant__ CUtensorMap mapB, TcP p) {
-  constexpr uint32_t A_BYTES = BM * BK * 4;
-  constexpr uint32_t B_BYTES = BN * BK * 4;
-  constexpr uint32_t TMEM_COLS = BN;
+                        const __grid_constant__ CUtensorMap mapB,
+                        const __grid_constant__ CUtensorMap mapC, TcP p) {
+  using L = TcSmem<BN>;
+  constexpr int ST = L::ST;
+  constexpr uint32_t A_BYTES = L::A_BYTES, B_BYTES = L::B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // align to 1024 B without leaving the shared address space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + ST * A_BYTES;
-  uint64_t* full = (uint64_t*)(sB + ST * B_BYTES);
+  float* sEpi = (float*)(sB + ST * B_BYTES);
+  uint64_t* full = (uint64_t*)((uint8_t*)sEpi + L::EPI_BYTES);
   uint64_t* empty = full + ST;
-  uint64_t* tmemFull = empty + ST;
-  uint32_t* tmemSlot = (uint32_t*)(tmemFull + 1);
+  uint64_t* tfull = empty + ST;   // [2] MMA -> epilogue
+  uint64_t* tempty = tfull + 2;   // [2] epilogue -> MMA
+  uint32_t* tmemSlot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int kb0 = blockIdx.z * p.kbPerSplit;
-  const int kb1 = min(p.numKb, kb0 + p.kbPerSplit);
-  const int nkb = kb1 - kb0;
 
   if(warp == 0 && lane == 0) {
     prefetch_tmap(&mapA);
     prefetch_tmap(&mapB);
+    if(p.tmaStore)
+      prefetch_tmap(&mapC);
     for(int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmemFull, 1);
+    for(int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -186,30 +213,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmemSlot;
+  const int tilesPerSplit = p.mt * p.nt;
+
+  auto tileCoords = [&](int t, int& m0, int& n0, int& kb0, int& nkb, int& split) {
+    split = t / tilesPerSplit;
+    int rem = t - split * tilesPerSplit;
+    m0 = (rem % p.mt) * BM;
+    n0 = (rem / p.mt) * BN;
+    kb0 = split * p.kbPerSplit;
+    nkb = min(p.numKb, kb0 + p.kbPerSplit) - kb0;
+  };
 
   if(warp == 0) {
     if(lane == 0) {
-      for(int i = 0; i < nkb; ++i) {
-        int s = i % ST;
-        if(i >= ST)
-          mbar_wait(&empty[s], ((i / ST) - 1) & 1);
-        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-        int k0 = (kb0 + i) * BK;
-        uint8_t* a = sA + s * A_BYTES;
-        uint8_t* b = sB + s * B_BYTES;
-        if(A_MN) {
+      int i = 0;  // global k-block counter (ring position)
+      for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x) {
+        int m0, n0, kb0, nkb, split;
+        tileCoords(t, m0, n0, kb0, nkb, split);
+        for(int kb = 0; kb < nkb; ++kb, ++i) {
+          int s = i % ST;
+          if(i >= ST)
+            mbar_wait(&empty[s], ((i / ST) - 1) & 1);
+          mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+          int k0 = (kb0 + kb) * BK;
+          uint8_t* a = sA + s * A_BYTES;
+          uint8_t* b = sB + s * B_BYTES;
+          if(A_MN) {
 #pragma unroll
-          for(int j = 0; j < BM / 32; ++j)
-            tma_load_2d(a + j * (BK * 128), &mapA, &full[s], m0 + j * 32, k0);
-        } else {
-          tma_load_2d(a, &mapA, &full[s], k0, m0);
-        }
-        if(B_MN) {
+            for(int j = 0; j < BM / 32; ++j)
+              tma_load_2d(a + j * (BK * 128), &mapA, &full[s], m0 + j * 32, k0);
+          } else {
+            tma_load_2d(a, &mapA, &full[s], k0, m0);
+          }
+          if(B_MN) {
 #pragma unroll
-          for(int j = 0; j < BN / 32; ++j)
-            tma_load_2d(b + j * (BK * 128), &mapB, &full[s], n0 + j * 32, k0);
-        } else {
-          tma_load_2d(b, &mapB, &full[s], k0, n0);
+            for(int j = 0; j < BN / 32; ++j)
+              tma_load_2d(b + j * (BK * 128), &mapB, &full[s], n0 + j * 32, k0);
+          } else {
+            tma_load_2d(b, &mapB, &full[s], k0, n0);
+          }
         }
       }
     }
@@ -218,83 +260,167 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
                            ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
-    for(int i = 0; i < nkb; ++i) {
-      int s = i % ST;
-      mbar_wait(&full[s], (i / ST) & 1);
+    int i = 0, lt = 0;
+    for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x, ++lt) {
+      int m0, n0, kb0, nkb, split;
+      tileCoords(t, m0, n0, kb0, nkb, split);
+      const int acc = lt & 1;
+      if(lt >= 2)
+        mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
       tc_fence_after();
-      if(lane == 0) {
-        uint32_t aBase = smem_u32(sA + s * A_BYTES);
-        uint32_t bBase = smem_u32(sB + s * B_BYTES);
+      const uint32_t tacc = tmem + (uint32_t)(acc * BN);
+      for(int kb = 0; kb < nkb; ++kb, ++i) {
+        int s = i % ST;
+        mbar_wait(&full[s], (i / ST) & 1);
+        tc_fence_after();
+        if(lane == 0) {
+          uint32_t aBase = smem_u32(sA + s * A_BYTES);
+          uint32_t bBase = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-        for(int kk = 0; kk < BK / 8; ++kk) {
-          // K-major (SW128): advance 8 tf32 = 32 B inside the swizzled row;
-          //   8-row atoms are 1024 B apart (SBO).
-          // MN-major (SW128 with 32 B atomicity): 128 B of M/N per K-row,
-          //   4-row atoms 512 B apart (SBO), 32-element M/N chunks one TMA
-          //   box (BK rows) apart (LBO); advance 8 K-rows = 1024 B.
-          uint64_t ad = A_MN ? umma_desc(aBase + kk * 1024, BK * 128, 512, 1)
-                             : umma_desc(aBase + kk * 32, 16, 1024, 2);
-          uint64_t bd = B_MN ? umma_desc(bBase + kk * 1024, BK * 128, 512, 1)
-                             : umma_desc(bBase + kk * 32, 16, 1024, 2);
-          mma_tf32(tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          for(int kk = 0; kk < BK / 8; ++kk) {
+            // K-major (SW128): advance 8 tf32 = 32 B inside the swizzled row;
+            //   8-row atoms are 1024 B apart (SBO).
+            // MN-major (SW128 with 32 B atomicity): 128 B of M/N per K-row,
+            //   4-row atoms 512 B apart (SBO), 32-element M/N chunks one TMA
+            //   box (BK rows) apart (LBO); advance 8 K-rows = 1024 B.
+            uint64_t ad = A_MN ? umma_desc(aBase + kk * 1024, BK * 128, 512, 1)
+                               : umma_desc(aBase + kk * 32, 16, 1024, 2);
+            uint64_t bd = B_MN ? umma_desc(bBase + kk * 1024, BK * 128, 512, 1)
+                               : umma_desc(bBase + kk * 32, 16, 1024, 2);
+            if(!(p.dbg & 2))
+              mma_tf32(tacc, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
+        __syncwarp();
       }
+      if(lane == 0)
+        mma_commit(&tfull[acc]);
       __syncwarp();
     }
-    if(lane == 0) {
-      if(nkb > 0)
-        mma_commit(tmemFull);
-    }
-    __syncwarp();
   } else {
-    // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+    // epilogue warps 2..5 -> TMEM lane quarter q = warp % 4
     const int q = warp & 3;
-    const int64_t row = m0 + q * 32 + lane;
-    if(nkb > 0) {
-      mbar_wait(tmemFull, 0);
+    // two swizzled 32x32 staging tiles per warp (TMA-store mode); the
+    // fallback path reuses the first one as a padded transpose buffer
+    float* stage0 = sEpi + q * 2 * 1024;
+    int chunk = 0;  // chunks handed to the TMA engine by this warp
+    int lt = 0;
+    for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x, ++lt) {
+      int m0, n0, kb0, nkb, split;
+      tileCoords(t, m0, n0, kb0, nkb, split);
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
-    }
-    const bool rowOk = row < p.M;
+      const int64_t rowBase = m0 + q * 32;
 #pragma unroll 1
-    for(int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      if(nkb > 0) {
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-      } else {
+      for(int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+        if(c0 + 32 >= BN) {  // accumulator fully read: hand it back to the MMA warp
+          tc_fence_before();
+          if(lane == 0)
+            mbar_arrive(&tempty[acc]);
+        }
+        if(n0 + c0 >= p.N || rowBase >= p.M || (p.dbg & 1))
+          continue;
+        const int64_t col0 = n0 + c0;
+        const int64_t row = rowBase + lane;  // this lane's output row
+        if(p.tmaStore) {
+          if(!p.part) {
+            const bool rowOk = row < p.M;
 #pragma unroll
-        for(int i = 0; i < 32; ++i)
-          v[i] = 0.f;
-      }
-      if(!rowOk || n0 + c0 >= p.N)
-        continue;
-      const int64_t col0 = n0 + c0;
-      if(p.part) {
-        float* dst = p.part + ((int64_t)blockIdx.z * p.M + row) * p.N + col0;
+            for(int i = 0; i < 32; ++i) {
+              float x = p.alpha == 1.f ? v[i] : p.alpha * v[i];
+              if(p.bias)
+                x = x + (col0 + i < p.N ? p.bias[col0 + i] : 0.f);
+              if(p.epi == MTKC_EPI_RELU)
+                x = x > 0.f ? x : 0.f;
+              v[i] = x;
+            }
+            if((p.gate || p.beta != 0.f) && rowOk) {
+              const float* grow = p.gate ? p.gate + row * p.ldc + col0 : nullptr;
+              const float* crow = p.C + row * p.ldc + col0;
 #pragma unroll
-        for(int i = 0; i < 32; ++i)
-          if(col0 + i < p.N)
-            dst[i] = v[i];
-        continue;
-      }
-      float* dst = p.C + row * p.ldc + col0;
-      const float* gt = p.gate ? p.gate + row * p.ldc + col0 : nullptr;
+              for(int i = 0; i < 32; ++i) {
+                if(col0 + i >= p.N)
+                  break;
+                float x = v[i];
+                if(grow)
+                  x = grow[i] > 0.f ? x : 0.f;
+                if(p.beta != 0.f)
+                  x = (p.beta == 1.f ? crow[i] : p.beta * crow[i]) + x;
+                v[i] = x;
+              }
+            }
+          }
+          float* stage = stage0 + (chunk & 1) * 1024;
+          if(chunk >= 2) {  // the TMA engine must have finished reading this buffer
+            if(lane == 0)
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+          }
+          // row `lane` = 128 B; 16-byte chunk j lands at j ^ (lane % 8) (SWIZZLE_128B)
 #pragma unroll
-      for(int i = 0; i < 32; ++i) {
-        if(col0 + i >= p.N)
-          break;
-        float x = p.alpha == 1.f ? v[i] : p.alpha * v[i];
-        if(p.bias)
-          x = x + p.bias[col0 + i];
-        if(p.epi == MTKC_EPI_RELU)
-          x = x > 0.f ? x : 0.f;
-        if(gt)
-          x = gt[i] > 0.f ? x : 0.f;
-        if(p.beta != 0.f)
-          x = (p.beta == 1.f ? dst[i] : p.beta * dst[i]) + x;
-        dst[i] = x;
+          for(int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(stage + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if(lane == 0) {
+            if(p.part)
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                  ::"l"((uint64_t)&mapC), "r"(smem_u32(stage)), "r"((int)col0), "r"((int)rowBase),
+                  "r"(split)
+                  : "memory");
+            else
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                  ::"l"((uint64_t)&mapC), "r"(smem_u32(stage)), "r"((int)col0), "r"((int)rowBase)
+                  : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          ++chunk;
+          continue;
+        }
+        // fallback: padded transpose through shared memory, coalesced row stores
+        float* st = stage0;
+#pragma unroll
+        for(int i2 = 0; i2 < 32; ++i2)
+          st[lane * EPI_STRIDE + i2] = v[i2];
+        __syncwarp();
+        const int64_t col = col0 + lane;
+        const bool colOk = col < p.N;
+        const float bcol = (p.bias && colOk && !p.part) ? p.bias[col] : 0.f;
+        const int rows = (int)min((int64_t)32, p.M - rowBase);
+        for(int r = 0; r < rows; ++r) {
+          float x = st[r * EPI_STRIDE + lane];
+          const int64_t rr = rowBase + r;
+          if(!colOk)
+            continue;
+          if(p.part) {
+            p.part[((int64_t)split * p.M + rr) * p.N + col] = x;
+            continue;
+          }
+          float* dst = p.C + rr * p.ldc + col;
+          x = p.alpha == 1.f ? x : p.alpha * x;
+          if(p.bias)
+            x = x + bcol;
+          if(p.epi == MTKC_EPI_RELU)
+            x = x > 0.f ? x : 0.f;
+          if(p.gate)
+            x = p.gate[rr * p.ldc + col] > 0.f ? x : 0.f;
+          if(p.beta != 0.f)
+            x = (p.beta == 1.f ? *dst : p.beta * *dst) + x;
+          *dst = x;
+        }
+        __syncwarp();
       }
     }
+    if(lane == 0)
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -374,15 +500,33 @@ bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int
   CUresult r = fn(m, tma_tf32_round() ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                   2, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   mnMajor ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
+// store map over C [rows x cols] (ld elements), or over split-K partials
+// [depth][rows][cols]; 32x32 boxes, 128-byte swizzle (matches the staging tile)
+bool make_store_map(CUtensorMap* m, float* base, int64_t cols, int64_t rows, int64_t ld,
+                    int64_t depth) {
+  EncodeFn fn = encode_fn();
+  if(!fn)
+    return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)depth};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)(ld * rows) * 4};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, depth > 1 ? 3 : 2, (void*)base, dims,
+                  strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_sms = 0;
+
 template <int BN, bool A_MN, bool B_MN>
-int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcP& p, dim3 grid,
+int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const TcP& p,
               cudaStream_t st) {
-  constexpr size_t smem = 1024 + ST * (size_t)(BM * BK * 4 + BN * BK * 4) + 256;
+  constexpr size_t smem = TcSmem<BN>::BYTES;
   auto kern = gemm_tf32_tc_kernel<BN, A_MN, B_MN>;
   static bool attr = false;
   if(!attr) {
@@ -392,24 +536,23 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcP& p, dim3 g
       return cuda_status(e, "gemm_tf32_tc smem attribute");
     attr = true;
   }
-  kern<<<grid, TC_THREADS, smem, st>>>(ma, mb, p);
+  int grid = std::min(p.numTiles, g_sms);
+  kern<<<grid, TC_THREADS, smem, st>>>(ma, mb, mc, p);
   MTKC_POST_LAUNCH("gemm_tf32_tc_kernel");
   return MTKC_OK;
 }
 
 template <int BN>
 int dispatch_majors(bool aMN, bool bMN, const CUtensorMap& ma, const CUtensorMap& mb,
-                    const TcP& p, dim3 grid, cudaStream_t st) {
+                    const CUtensorMap& mc, const TcP& p, cudaStream_t st) {
   if(!aMN && !bMN)
-    return launch_tc<BN, false, false>(ma, mb, p, grid, st);
+    return launch_tc<BN, false, false>(ma, mb, mc, p, st);
   if(!aMN && bMN)
-    return launch_tc<BN, false, true>(ma, mb, p, grid, st);
+    return launch_tc<BN, false, true>(ma, mb, mc, p, st);
   if(aMN && !bMN)
-    return launch_tc<BN, true, false>(ma, mb, p, grid, st);
-  return launch_tc<BN, true, true>(ma, mb, p, grid, st);
+    return launch_tc<BN, true, false>(ma, mb, mc, p, st);
+  return launch_tc<BN, true, true>(ma, mb, mc, p, st);
 }
-
-int g_sms = 0;
 
 }  // namespace
 
@@ -423,8 +566,6 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
     return false;
   if(a.lda % 4 || a.ldb % 4 || ((uintptr_t)a.A % 16) || ((uintptr_t)a.B % 16))
     return false;
-  if(a.gate && (a.ldc != a.N && a.gate == nullptr))
-    return false;
   // operand majors: op(A) is K-major iff stored untransposed
   const bool aMN = a.transA != 0, bMN = a.transB == 0;
   if(!g_sms) {
@@ -435,21 +576,27 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
       g_sms = 148;
   }
   const int64_t mt = cdiv(a.M, BM);
-  int BN = 256;
-  if(mt * cdiv(a.N, 256) < g_sms || a.N <= 128)
-    BN = 128;
+  // wide tiles only when they still give every SM at least one tile
+  int BN = (a.N >= 256 && mt * cdiv(a.N, 256) >= g_sms) ? 256 : 128;
   const int64_t nt = cdiv(a.N, BN);
   const int numKb = (int)cdiv(a.K, BK);
-  // split K when the tile grid leaves SMs idle and K is long
+  // Split K to fill the machine: pick the split count (each split keeping
+  // >= 24 k-blocks) that maximises the wave efficiency of the persistent
+  // grid, tiles*s / (SMs * ceil(tiles*s / SMs)); ties go to fewer splits.
   int splits = 1;
   const int64_t tiles = mt * nt;
-  if(tiles < g_sms && numKb >= 8 && a.workspace) {
-    splits = (int)std::min<int64_t>(std::max<int64_t>(1, (g_sms + tiles - 1) / tiles),
-                                    numKb / 4);
-    size_t need = (size_t)splits * (size_t)a.M * (size_t)a.N * sizeof(float);
-    while(splits > 1 && need > a.workspace_bytes) {
-      --splits;
-      need = (size_t)splits * (size_t)a.M * (size_t)a.N * sizeof(float);
+  if(a.workspace && numKb >= 16) {
+    double best = (double)tiles / (double)(g_sms * cdiv(tiles, g_sms));
+    for(int s = 2; s <= 16 && numKb / s >= 24; ++s) {
+      size_t need = (size_t)s * (size_t)a.M * (size_t)a.N * sizeof(float);
+      if(need > a.workspace_bytes)
+        break;
+      double eff = (double)(tiles * s) / (double)(g_sms * cdiv(tiles * s, g_sms));
+      // partial sums cost an extra write+read of M*N per split: demand a real gain
+      if(eff > best * 1.08) {
+        best = eff;
+        splits = s;
+      }
     }
   }
   const int kbPer = (int)cdiv(numKb, splits);
@@ -484,9 +631,26 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
   p.part = splits > 1 ? a.workspace : nullptr;
   p.kbPerSplit = kbPer;
   p.numKb = numKb;
-  dim3 grid((unsigned)nt, (unsigned)mt, (unsigned)splits);
-  *rc = BN == 256 ? dispatch_majors<256>(aMN, bMN, ma, mb, p, grid, st)
-                  : dispatch_majors<128>(aMN, bMN, ma, mb, p, grid, st);
+  p.mt = (int)mt;
+  p.nt = (int)nt;
+  p.splits = splits;
+  p.numTiles = (int)(mt * nt * splits);
+  {
+    const char* e = getenv("MTK_GEMM_DEBUG");
+    p.dbg = e ? atoi(e) : 0;
+  }
+  CUtensorMap mc;
+  std::memset(&mc, 0, sizeof(mc));
+  if(p.part)
+    p.tmaStore = (a.N % 4 == 0) && ((uintptr_t)a.workspace % 16 == 0) &&
+                 make_store_map(&mc, a.workspace, a.N, a.M, a.N, splits);
+  else
+    p.tmaStore = (a.ldc % 4 == 0) && ((uintptr_t)a.C % 16 == 0) &&
+                 make_store_map(&mc, a.C, a.N, a.M, a.ldc, 1);
+  if(getenv("MTK_GEMM_NO_TMA_STORE"))
+    p.tmaStore = 0;
+  *rc = BN == 256 ? dispatch_majors<256>(aMN, bMN, ma, mb, mc, p, st)
+                  : dispatch_majors<128>(aMN, bMN, ma, mb, mc, p, st);
   if(*rc == MTKC_OK && splits > 1) {
     splitk_reduce_kernel<<<grid1d(a.M * a.N, 256), 256, 0, st>>>(
         a.workspace, splits, a.M, a.N, a.C, a.ldc, a.alpha, a.beta, a.bias, a.epilogue, a.gate);

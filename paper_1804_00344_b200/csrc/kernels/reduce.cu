@@ -1,6 +1,7 @@
 // Reductions: reduceInto (tensor.cpp:322-368) and its graph backward
 // (graph.cpp:488-521); deterministic column sums for bias/gain gradients;
 // the allFinite scan (tensor.cpp:95-100) as a device flag.
+#include "colred.cuh"
 #include "common.cuh"
 
 using namespace mtkc;
@@ -65,33 +66,7 @@ __global__ void reduce_bwd_kernel(int op, float* gin, const float* gout, const f
   }
 }
 
-constexpr int CS_ROWS = 128;  // rows per partial
-constexpr int CS_COLS = 128;  // columns per CTA (one per thread)
-
-// partial[rb][c] = sum_{r in block rb} in[r][c]
-__global__ void colsum_partial_kernel(float* part, const float* in, int64_t rows, int64_t cols) {
-  int64_t c = (int64_t)blockIdx.x * CS_COLS + threadIdx.x;
-  int64_t r0 = (int64_t)blockIdx.y * CS_ROWS;
-  if(c >= cols)
-    return;
-  int64_t r1 = min(rows, r0 + CS_ROWS);
-  float acc = 0.f;
-  for(int64_t r = r0; r < r1; ++r)
-    acc += in[r * cols + c];
-  part[(int64_t)blockIdx.y * cols + c] = acc;
-}
-
-__global__ void colsum_final_kernel(float* out, const float* part, int64_t nparts, int64_t cols,
-                                    int accumulate) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if(c >= cols)
-    return;
-  float acc = accumulate ? out[c] : 0.f;
-  float s = 0.f;
-  for(int64_t p = 0; p < nparts; ++p)
-    s += part[p * cols + c];
-  out[c] = acc + s;
-}
+constexpr int CS_ROWS = 128;  // below this many rows a single pass is used
 
 // single-level variant (no workspace): one thread per column walks all rows
 __global__ void colsum_direct_kernel(float* out, const float* in, int64_t rows, int64_t cols,
@@ -152,19 +127,20 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
                 float* workspace, size_t workspace_bytes, void* stream) {
   if(rows <= 0 || cols <= 0)
     return MTKC_OK;
-  int64_t nparts = cdiv(rows, CS_ROWS);
-  if(nparts <= 1 || !workspace || workspace_bytes < (size_t)(nparts * cols) * sizeof(float)) {
+  ProfScope prof(S(stream), "colsum", 4.0 * rows * cols);
+  if(rows <= CS_ROWS || !workspace || workspace_bytes < colred_workspace_bytes(1, rows, cols)) {
     colsum_direct_kernel<<<(unsigned)cdiv(cols, 128), 128, 0, S(stream)>>>(out, in, rows, cols,
                                                                           accumulate);
     MTKC_POST_LAUNCH("colsum_direct_kernel");
     return MTKC_OK;
   }
-  dim3 g((unsigned)cdiv(cols, CS_COLS), (unsigned)nparts);
-  colsum_partial_kernel<<<g, CS_COLS, 0, S(stream)>>>(workspace, in, rows, cols);
-  MTKC_POST_LAUNCH("colsum_partial_kernel");
-  colsum_final_kernel<<<(unsigned)cdiv(cols, 128), 128, 0, S(stream)>>>(out, workspace, nparts,
-                                                                      cols, accumulate);
-  MTKC_POST_LAUNCH("colsum_final_kernel");
+  int64_t nblk = cdiv(rows, CR_ROWS);
+  colred_partial_kernel<1><<<dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
+                             S(stream)>>>(workspace, in, nullptr, rows, cols);
+  MTKC_POST_LAUNCH("colred_partial_kernel");
+  colred_final_kernel<1><<<(unsigned)cdiv(cols, 128), 128, 0, S(stream)>>>(
+      out, nullptr, workspace, nblk, cols, accumulate);
+  MTKC_POST_LAUNCH("colred_final_kernel");
   return MTKC_OK;
 }
 

@@ -81,6 +81,25 @@ uint64_t mtkc_launch_count(void) { return g_launches.load(); }
 uint64_t mtkc_h2d_bytes(void) { return g_h2d.load(); }
 uint64_t mtkc_d2h_bytes(void) { return g_d2h.load(); }
 
+__global__ void sleep_kernel(int64_t ns) {
+  int64_t t0 = (int64_t)clock64();
+  (void)t0;
+  uint64_t start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  for(;;) {
+    uint64_t now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if((int64_t)(now - start) >= ns)
+      break;
+    __nanosleep(10000);
+  }
+}
+
+int mtkc_gpu_sleep(int64_t us, void* stream) {
+  sleep_kernel<<<1, 1, 0, S(stream)>>>(us * 1000);
+  return cuda_status(cudaGetLastError(), "sleep_kernel");
+}
+
 int mtkc_prof_enable(int on) {
   g_prof = on != 0;
   return MTKC_OK;
@@ -212,6 +231,10 @@ int mtkc_event_record(void* ev, void* stream) {
 
 int mtkc_stream_wait_event(void* stream, void* ev) {
   return cuda_status(cudaStreamWaitEvent(S(stream), (cudaEvent_t)ev, 0), "cudaStreamWaitEvent");
+}
+
+int mtkc_event_sync(void* ev) {
+  return cuda_status(cudaEventSynchronize((cudaEvent_t)ev), "cudaEventSynchronize");
 }
 
 int mtkc_event_elapsed_ms(void* start, void* stop, float* ms) {

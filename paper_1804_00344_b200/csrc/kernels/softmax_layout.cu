@@ -157,6 +157,54 @@ __global__ void scatter_add_kernel(float* out, const float* src, const int32_t* 
   }
 }
 
+// Chunked scatter-add: CTA per chunk; single-chunk segments add straight
+// into the table row in position order (bit-exact with the reference loop),
+// chunks of long segments write partial sums.
+__global__ void scatter_chunk_kernel(float* out, const float* src, const int32_t* perm,
+                                     const int32_t* cstart, const int32_t* crow,
+                                     const int32_t* cslot, float* partial, int64_t cols,
+                                     float scale) {
+  int64_t c = blockIdx.x;
+  int32_t k0 = cstart[c], k1 = cstart[c + 1];
+  int32_t slot = cslot[c];
+  float* dst = slot < 0 ? out + (int64_t)crow[c] * cols : partial + (int64_t)slot * cols;
+  for(int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
+    float acc = slot < 0 ? dst[j] : 0.f;
+    int32_t k = k0;
+    for(; k + 4 <= k1; k += 4) {  // four independent loads in flight
+      float v0 = src[(int64_t)perm[k] * cols + j], v1 = src[(int64_t)perm[k + 1] * cols + j];
+      float v2 = src[(int64_t)perm[k + 2] * cols + j], v3 = src[(int64_t)perm[k + 3] * cols + j];
+      if(scale != 1.f) {
+        v0 *= scale;
+        v1 *= scale;
+        v2 *= scale;
+        v3 *= scale;
+      }
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for(; k < k1; ++k) {
+      float v = src[(int64_t)perm[k] * cols + j];
+      acc += scale == 1.f ? v : scale * v;
+    }
+    dst[j] = acc;
+  }
+}
+
+__global__ void scatter_multi_kernel(float* out, const float* partial, const int32_t* mfirst,
+                                     const int32_t* mrow, int64_t cols) {
+  int64_t m = blockIdx.x;
+  float* dst = out + (int64_t)mrow[m] * cols;
+  for(int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
+    float acc = dst[j];
+    for(int32_t s = mfirst[m]; s < mfirst[m + 1]; ++s)
+      acc += partial[(int64_t)s * cols + j];
+    dst[j] = acc;
+  }
+}
+
 // out[n,:] = table[id,:]*s + pe[n % t,:]; exact gather when s == 1, pe == 0.
 __global__ void embed_kernel(float* out, const float* table, const int32_t* ids, int64_t n,
                              int64_t e, int64_t vocab, float s, const float* pe, int64_t t,
@@ -309,6 +357,26 @@ int mtkc_scatter_add_rows(float* out, const float* src, const int32_t* perm,
   scatter_add_kernel<<<(unsigned)n_uniq, threads, 0, S(stream)>>>(out, src, perm, seg_start,
                                                                   uniq, cols, scale);
   MTKC_POST_LAUNCH("scatter_add_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_scatter_add_rows_chunked(float* out, const float* src, const int32_t* perm,
+                                  const int32_t* chunk_start, const int32_t* chunk_row,
+                                  const int32_t* chunk_slot, int64_t n_chunks,
+                                  const int32_t* multi_first, const int32_t* multi_row,
+                                  int64_t n_multi, float* partial, int64_t cols, float scale,
+                                  void* stream) {
+  if(n_chunks <= 0 || cols <= 0)
+    return MTKC_OK;
+  int threads = cols >= 512 ? 512 : (int)((cols + 31) / 32 * 32);
+  scatter_chunk_kernel<<<(unsigned)n_chunks, threads, 0, S(stream)>>>(
+      out, src, perm, chunk_start, chunk_row, chunk_slot, partial, cols, scale);
+  MTKC_POST_LAUNCH("scatter_chunk_kernel");
+  if(n_multi > 0) {
+    scatter_multi_kernel<<<(unsigned)n_multi, threads, 0, S(stream)>>>(out, partial, multi_first,
+                                                                       multi_row, cols);
+    MTKC_POST_LAUNCH("scatter_multi_kernel");
+  }
   return MTKC_OK;
 }
 

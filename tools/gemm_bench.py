@@ -1,0 +1,45 @@
+"""Micro-benchmark of mtkc_gemm on the Transformer-base step's GEMM shapes.
+usage: python tools/gemm_bench.py [reps]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_1804_00344_b200 import cabi
+
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+R = 6629
+shapes = [  # (name, M, N, K, transA, transB)
+    ("logits fwd  H.E^T", R, 32000, 512, 0, 1),
+    ("logits dH = dL.E", R, 512, 32000, 0, 0),
+    ("logits dE = dL^T.H", 32000, 512, R, 1, 0),
+    ("proj fwd x.W", R, 512, 512, 0, 0),
+    ("proj dX = dY.W^T", R, 512, 512, 0, 1),
+    ("proj dW = X^T.dY", 512, 512, R, 1, 0),
+    ("ffn1 fwd", R, 2048, 512, 0, 0),
+    ("ffn2 dX", R, 2048, 512, 0, 1),
+    ("ffn1 dW", 512, 2048, R, 1, 0),
+    ("square 8192", 8192, 8192, 8192, 0, 0),
+]
+ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+stream = torch.cuda.current_stream().cuda_stream
+for name, M, N, K, ta, tb in shapes:
+    A = torch.randn((K, M) if ta else (M, K), device="cuda")
+    B = torch.randn((N, K) if tb else (K, N), device="cuda")
+    C = torch.empty(M, N, device="cuda")
+    args = dict(trans_a=ta, trans_b=tb, precision=1, workspace=ws.data_ptr(),
+                workspace_bytes=ws.numel(), stream=stream)
+    for _ in range(3):
+        cabi.gemm(M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, **args)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        cabi.gemm(M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, **args)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    tf = 2.0 * M * N * K / ms / 1e9
+    ref = (A.t() if ta else A) @ (B.t() if tb else B)
+    err = ((C - ref).abs().max() / ref.abs().max()).item()
+    print(f"{name:22s} M{M:6d} N{N:6d} K{K:6d}  {ms*1e3:9.1f} us  {tf:7.1f} TF/s  relerr {err:.1e}", flush=True)
