@@ -285,6 +285,96 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
                             void* stream);
 
 /* ======================================================================== */
+/* fused GRU block, pointwise part (gruCell graph.cpp:648-813, gruPre        */
+/* :633-645).  The matrix products come from mtkc_gemm: hu = h[Uz|Ur|Uh]     */
+/* and xw = x[Wz|Wr|Wx] ([b x 3d] each, ld 3d; xw NULL for transition-only   */
+/* blocks).  Forward per row:                                                */
+/*   z = sig(LNz(hu_z + xw_z + bz)), r = sig(LNr(hu_r + xw_r + br)),         */
+/*   ac = LNx(xw_x) (0 without input) + (r*hu_h + bh), ht = tanh(ac),        */
+/*   h' = (1-z)*ht + z*h.   LN is applied iff the ln pointers are non-NULL.  */
+/* cache [b x 3d]: z | r | ht;  lnc [b x 3d] xhat_z | xhat_r | xhat_x and    */
+/* lnrs [b x 3]: inverse std per gate (LN only).                             */
+/* Backward per row from go = dL/dh': dpz, dpr = grads of the pre-LN gate    */
+/* sums (U/W/bias products), duh = dL/d(h Uh), dac = dL/d(ac) (bh grad),      */
+/* dax = dL/d(x Wx) (LN-inverted dac); gh (+)= go*z; lnparts [b x 6d] holds   */
+/* per-row dgain/dbias terms (z, r, x) for a column reduction.               */
+/* ======================================================================== */
+typedef struct mtkc_gru_args {
+  int64_t b, d;
+  const float* h;      /* [b x d] state fed to the block */
+  const float* hu;     /* [b x 3d] */
+  const float* xw;     /* [b x 3d] or NULL */
+  const float* bz;
+  const float* br;
+  const float* bh;
+  const float* lnGz;   /* LN gains/biases or NULL (no layer norm) */
+  const float* lnBz;
+  const float* lnGr;
+  const float* lnBr;
+  const float* lnGx;
+  const float* lnBx;
+  float eps;
+  float* hout;         /* [b x d] */
+  float* cache;        /* [b x 3d] */
+  float* lnc;          /* [b x 3d] (LN only) */
+  float* lnrs;         /* [b x 3]  (LN only) */
+  /* backward */
+  const float* go;     /* [b x d] */
+  float* gh;           /* [b x d] */
+  int accumulate_h;
+  float* dpz;          /* [b x d] each */
+  float* dpr;
+  float* duh;
+  float* dac;
+  float* dax;          /* may alias dac when there is no LN */
+  float* lnparts;      /* [b x 6d] (LN only) */
+} mtkc_gru_args;
+
+int mtkc_gru_forward(const mtkc_gru_args* a, void* stream);
+int mtkc_gru_backward(const mtkc_gru_args* a, void* stream);
+
+/* ======================================================================== */
+/* Bahdanau MLP attention core (BahdanauAttention::apply layers.cpp:59-79),  */
+/* fused: given wq = query*W [b x a] and uk = keys*U [b x s x a] (GEMMs, the */
+/* latter computed once per batch), per row and source position j:           */
+/*   t_j = tanh(LN(wq + uk_j)) (LN optional), e_j = t_j . v,                 */
+/*   w = masked softmax_j(e), ctx = sum_j w_j keys_j.                        */
+/* Backward produces d(wq), d(uk), d(keys) and per-row partials of d(v) and  */
+/* the LN gain/bias gradients (column-summed over b by the caller).          */
+/* ======================================================================== */
+typedef struct mtkc_bahdanau_args {
+  int64_t b, s, a, kd;
+  const float* wq;     /* [b x a] */
+  const float* uk;     /* [b x s x a] */
+  const float* v;      /* [a] */
+  const float* keys;   /* [b x s x kd] */
+  const float* mask;   /* [b x s] or NULL */
+  const float* lnG;    /* [a] or NULL (no layer norm) */
+  const float* lnB;
+  float eps;
+  float* t;            /* [b x s x a] saved tanh */
+  float* lnxh;         /* [b x s x a] (LN only) */
+  float* lnrs;         /* [b x s]     (LN only) */
+  float* w;            /* [b x s] attention weights */
+  float* ctx;          /* [b x kd] */
+  int* flags;
+  /* backward */
+  const float* gctx;   /* [b x kd] */
+  float* gkeys;
+  int acc_keys;
+  float* gwq;
+  int acc_wq;
+  float* guk;
+  int acc_uk;
+  float* gv_part;      /* [b x a] */
+  float* glnG_part;    /* [b x a] (LN only) */
+  float* glnB_part;    /* [b x a] (LN only) */
+} mtkc_bahdanau_args;
+
+int mtkc_bahdanau_forward(const mtkc_bahdanau_args* a, void* stream);
+int mtkc_bahdanau_backward(const mtkc_bahdanau_args* a, void* stream);
+
+/* ======================================================================== */
 /* cross-entropy over the vocabulary (crossEntropy graph.cpp:859-924)       */
 /* fwd: per row lse = max + log(sum exp(x - max)); row_loss = m*(lse - x_y); */
 /* loss = sum(row_loss)/count (deterministic single-block sum).              */

@@ -402,13 +402,21 @@ NodeRef ExpressionGraph::param(const std::string& name, const Shape& shape,
     throw ContractError("parameter " + name + " redefined with shape " + shape.str() + " (was " +
                         it->second.value.shape().str() + ")");
   }
+  // One node per parameter per graph generation: layers re-reference their
+  // weights every time step (layers.cpp:216-224); sharing the node lets the
+  // product cache below see repeated products of the same operands.
+  auto pn = paramNode_.find(name);
+  if(pn != paramNode_.end())
+    return NodeRef{this, pn->second, generation_, shape};
   Node n;
   n.op = "param";
   n.shape = shape;
   n.isParam = true;
   n.paramName = name;
   n.value = it->second.value;
-  return addNode(std::move(n));
+  NodeRef r = addNode(std::move(n));
+  paramNode_[name] = r.index;
+  return r;
 }
 
 NodeRef ExpressionGraph::constant(const Tensor& t) {
@@ -562,6 +570,20 @@ void gemmAccum(float* dst, int acc, const Shape& ds, const float* x, const Shape
 NodeRef ExpressionGraph::dot(NodeRef a, NodeRef b, bool transA, bool transB) {
   checkRef(a);
   checkRef(b);
+  // Identical products are computed once per generation (e.g. the Bahdanau
+  // key projection keys*U, which the decoder re-requests at every target
+  // position, layers.cpp:68); every use accumulates into the one node's
+  // gradient, exactly the sum the reference forms over its copies.
+  auto key = std::make_tuple(a.index, b.index, transA, transB);
+  auto cached = dotCache_.find(key);
+  if(cached != dotCache_.end())
+    return NodeRef{this, cached->second, generation_, nodes_[(size_t)cached->second].shape};
+  NodeRef r = dotImpl(a, b, transA, transB);
+  dotCache_[key] = r.index;
+  return r;
+}
+
+NodeRef ExpressionGraph::dotImpl(NodeRef a, NodeRef b, bool transA, bool transB) {
   auto opRows = [](const Shape& s, bool t) { return t ? s.back() : s[s.rank() - 2]; };
   auto opCols = [](const Shape& s, bool t) { return t ? s[s.rank() - 2] : s.back(); };
   if(a.shape.rank() < 2 || b.shape.rank() < 2)
@@ -1310,6 +1332,8 @@ void ExpressionGraph::backward(NodeRef loss) {
 
 void ExpressionGraph::clear() {
   nodes_.clear();
+  paramNode_.clear();
+  dotCache_.clear();
   computed_ = 0;
   ++generation_;
   arena_.reset();

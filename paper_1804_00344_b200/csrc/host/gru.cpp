@@ -1,16 +1,219 @@
 // Fused GRU block (gruCell, reference graph.cpp:648-813).
+//
+// Forward: h*[Uz|Ur|Uh] and x*[Wz|Wr|Wx] as tcgen05 GEMMs into [b x 3d]
+// buffers, then one pointwise kernel per row (bias, optional per-gate layer
+// norm, sigmoid/tanh, state interpolation).  Backward: one pointwise kernel
+// producing the gate pre-activation gradients, then the transposed GEMMs
+// for dh, dU, dx, dW, column sums for the biases and layer-norm parameters.
 #include "mtk/device.h"
 #include "mtk/graph.h"
 
 namespace mtk {
 
+namespace {
+
+void* stream() { return Device::get().stream(); }
+
+void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA, const float* B,
+          int64_t ldb, bool tB, float* C, int64_t ldc, float beta) {
+  Device& d = Device::get();
+  mtkc_gemm_args g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.batch = 1;
+  g.A = A;
+  g.lda = lda;
+  g.transA = tA;
+  g.B = B;
+  g.ldb = ldb;
+  g.transB = tB;
+  g.C = C;
+  g.ldc = ldc;
+  g.alpha = 1.f;
+  g.beta = beta;
+  g.precision = (int)d.precision();
+  g.workspace = d.scratch(64 << 20);
+  g.workspace_bytes = d.scratchBytes();
+  MTKC(mtkc_gemm(&g, d.stream()));
+}
+
+void colsumInto(ExpressionGraph::GradDst dst, const float* in, int64_t rows, int64_t cols) {
+  Device& dev = Device::get();
+  size_t ws = (size_t)((rows + 127) / 128) * (size_t)cols * sizeof(float) * 2;
+  float* w = dev.scratch(ws);
+  MTKC(mtkc_colsum(dst.ptr, in, rows, cols, dst.accumulate, w, dev.scratchBytes(), dev.stream()));
+}
+
+struct GruAux {
+  Tensor hu, xw, cache, lnc, lnrs;
+};
+
+}  // namespace
+
 NodeRef ExpressionGraph::gruCell(NodeRef state, NodeRef input, const GruParams& p,
                                  bool layerNorm) {
-  (void)state;
-  (void)input;
-  (void)p;
-  (void)layerNorm;
-  throw ContractError("gruCell: not built yet");
+  checkRef(state);
+  bool hasInput = input.valid();
+  if(hasInput)
+    checkRef(input);
+  if(state.shape.rank() != 2)
+    throw DimensionError("gru state must be rank 2 [batch x d], got " + state.shape.str());
+  int64_t b = state.shape[0], d = state.shape.back();
+  if(hasInput && input.shape[0] != b)
+    throw DimensionError("gru input batch mismatch: " + input.shape.str() + " vs " +
+                         state.shape.str());
+  int64_t e = hasInput ? input.shape.back() : 0;
+  Node n;
+  n.op = "gruCell";
+  n.shape = state.shape;
+  // input slots follow the reference (graph.cpp:665-687)
+  n.inputs = {state.index, p.Uz.index, p.bz.index, p.Ur.index, p.br.index, p.Uh.index,
+              p.bh.index};
+  int xSlot = -1, wSlot = -1, lnSlot = -1;
+  if(hasInput) {
+    xSlot = (int)n.inputs.size();
+    n.inputs.push_back(input.index);
+    wSlot = (int)n.inputs.size();
+    n.inputs.push_back(p.Wz.index);
+    n.inputs.push_back(p.Wr.index);
+    n.inputs.push_back(p.Wx.index);
+  }
+  if(layerNorm) {
+    lnSlot = (int)n.inputs.size();
+    n.inputs.push_back(p.lnGz.index);
+    n.inputs.push_back(p.lnBz.index);
+    n.inputs.push_back(p.lnGr.index);
+    n.inputs.push_back(p.lnBr.index);
+    if(hasInput) {
+      n.inputs.push_back(p.lnGx.index);
+      n.inputs.push_back(p.lnBx.index);
+    }
+  }
+  auto aux = std::make_shared<GruAux>();
+  n.aux = aux;
+
+  n.fwd = [=](ExpressionGraph& g, Node& n) {
+    aux->hu = g.allocTensor(Shape({b, 3 * d}));
+    aux->cache = g.allocTensor(Shape({b, 3 * d}));
+    const float* h = g.valPtr(n.inputs[0]);
+    float* hu = aux->hu.dev();
+    gemm(b, d, d, h, d, false, g.valPtr(n.inputs[1]), d, false, hu, 3 * d, 0.f);
+    gemm(b, d, d, h, d, false, g.valPtr(n.inputs[3]), d, false, hu + d, 3 * d, 0.f);
+    gemm(b, d, d, h, d, false, g.valPtr(n.inputs[5]), d, false, hu + 2 * d, 3 * d, 0.f);
+    mtkc_gru_args a{};
+    a.b = b;
+    a.d = d;
+    a.h = h;
+    a.hu = hu;
+    if(hasInput) {
+      aux->xw = g.allocTensor(Shape({b, 3 * d}));
+      float* xw = aux->xw.dev();
+      const float* x = g.valPtr(n.inputs[xSlot]);
+      for(int k = 0; k < 3; ++k)
+        gemm(b, d, e, x, e, false, g.valPtr(n.inputs[wSlot + k]), d, false, xw + k * d, 3 * d,
+             0.f);
+      a.xw = xw;
+    }
+    a.bz = g.valPtr(n.inputs[2]);
+    a.br = g.valPtr(n.inputs[4]);
+    a.bh = g.valPtr(n.inputs[6]);
+    if(layerNorm) {
+      aux->lnc = g.allocTensor(Shape({b, 3 * d}));
+      aux->lnrs = g.allocTensor(Shape({b, 3}));
+      a.lnGz = g.valPtr(n.inputs[lnSlot]);
+      a.lnBz = g.valPtr(n.inputs[lnSlot + 1]);
+      a.lnGr = g.valPtr(n.inputs[lnSlot + 2]);
+      a.lnBr = g.valPtr(n.inputs[lnSlot + 3]);
+      if(hasInput) {
+        a.lnGx = g.valPtr(n.inputs[lnSlot + 4]);
+        a.lnBx = g.valPtr(n.inputs[lnSlot + 5]);
+      }
+      a.lnc = aux->lnc.dev();
+      a.lnrs = aux->lnrs.dev();
+    }
+    a.eps = 1e-9f;  // graph.cpp:690
+    a.hout = n.value.dev();
+    a.cache = aux->cache.dev();
+    MTKC(mtkc_gru_forward(&a, stream()));
+  };
+
+  n.bwd = [=](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    Tensor dpz = g.allocTensor(Shape({b, d})), dpr = g.allocTensor(Shape({b, d}));
+    Tensor duh = g.allocTensor(Shape({b, d})), dac = g.allocTensor(Shape({b, d}));
+    Tensor dax = (hasInput && layerNorm) ? g.allocTensor(Shape({b, d})) : dac;
+    Tensor lnparts;
+    mtkc_gru_args a{};
+    a.b = b;
+    a.d = d;
+    a.h = g.valPtr(n.inputs[0]);
+    a.hu = aux->hu.devc();
+    a.xw = hasInput ? aux->xw.devc() : nullptr;
+    a.cache = aux->cache.dev();
+    if(layerNorm) {
+      lnparts = g.allocTensor(Shape({b, 6 * d}));
+      a.lnGz = g.valPtr(n.inputs[lnSlot]);
+      a.lnGr = g.valPtr(n.inputs[lnSlot + 2]);
+      if(hasInput)
+        a.lnGx = g.valPtr(n.inputs[lnSlot + 4]);
+      a.lnc = aux->lnc.dev();
+      a.lnrs = aux->lnrs.dev();
+      a.lnparts = lnparts.dev();
+    }
+    a.go = go;
+    auto gh = g.gradDst(n.inputs[0]);
+    a.gh = gh.ptr;
+    a.accumulate_h = gh.accumulate;
+    a.dpz = dpz.dev();
+    a.dpr = dpr.dev();
+    a.duh = duh.dev();
+    a.dac = dac.dev();
+    a.dax = dax.dev();
+    MTKC(mtkc_gru_backward(&a, stream()));
+    const float* h = a.h;
+    // dh += dpz Uz^T + dpr Ur^T + duh Uh^T   (graph.cpp:772, 802)
+    gemm(b, d, d, a.dpz, d, false, g.valPtr(n.inputs[1]), d, true, gh.ptr, d, 1.f);
+    gemm(b, d, d, a.dpr, d, false, g.valPtr(n.inputs[3]), d, true, gh.ptr, d, 1.f);
+    gemm(b, d, d, a.duh, d, false, g.valPtr(n.inputs[5]), d, true, gh.ptr, d, 1.f);
+    // dU += h^T dpre   (graph.cpp:773, 803)
+    const float* gsrc[3] = {a.dpz, a.dpr, a.duh};
+    for(int k = 0; k < 3; ++k) {
+      auto dU = g.gradDst(n.inputs[1 + 2 * k]);
+      gemm(d, d, b, h, d, true, gsrc[k], d, false, dU.ptr, d, dU.accumulate ? 1.f : 0.f);
+    }
+    // biases (graph.cpp:771, 801)
+    colsumInto(g.gradDst(n.inputs[2]), a.dpz, b, d);
+    colsumInto(g.gradDst(n.inputs[4]), a.dpr, b, d);
+    colsumInto(g.gradDst(n.inputs[6]), a.dac, b, d);
+    if(hasInput) {
+      const float* x = g.valPtr(n.inputs[xSlot]);
+      const float* wsrc[3] = {a.dpz, a.dpr, a.dax};
+      auto dx = g.gradDst(n.inputs[xSlot]);
+      for(int k = 0; k < 3; ++k) {
+        float beta = (k == 0 && !dx.accumulate) ? 0.f : 1.f;
+        gemm(b, e, d, wsrc[k], d, false, g.valPtr(n.inputs[wSlot + k]), d, true, dx.ptr, e, beta);
+      }
+      for(int k = 0; k < 3; ++k) {
+        auto dW = g.gradDst(n.inputs[wSlot + k]);
+        gemm(e, d, b, x, e, true, wsrc[k], d, false, dW.ptr, d, dW.accumulate ? 1.f : 0.f);
+      }
+    }
+    if(layerNorm) {  // per-gate LN gain/bias grads: one column sum, then slices
+      int nln = hasInput ? 6 : 4;
+      Tensor sums = g.allocTensor(Shape({6 * d}));
+      colsumInto(ExpressionGraph::GradDst{sums.dev(), 0, nullptr}, lnparts.devc(), b, 6 * d);
+      for(int k = 0; k < nln; ++k) {
+        auto dst = g.gradDst(n.inputs[lnSlot + k]);
+        if(dst.accumulate)
+          MTKC(mtkc_axpy(dst.ptr, sums.devc() + k * d, 1.f, d, stream()));
+        else
+          MTKC(mtkc_memcpy_d2d(dst.ptr, sums.devc() + k * d, (size_t)d * sizeof(float),
+                               stream()));
+      }
+    }
+  };
+  return addNode(std::move(n));
 }
 
 }  // namespace mtk

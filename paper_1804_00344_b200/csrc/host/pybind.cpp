@@ -159,6 +159,7 @@ PYBIND11_MODULE(_mtk, m) {
       .def("dev_ptr", [](const Tensor& t) { return (uintptr_t)t.devc(); });
 
   py::class_<NodeRef>(m, "NodeRef")
+      .def(py::init<>())
       .def_property_readonly("shape", [](const NodeRef& r) { return tupleOf(r.shape); })
       .def_readonly("index", &NodeRef::index)
       .def("valid", &NodeRef::valid)

@@ -562,7 +562,7 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
     return false;
   if(a.batch != 1)
     return false;
-  if(a.M < 64 || a.N < 32 || a.K < 8)
+  if(a.M < 1 || a.N < 8 || a.K < 8)
     return false;
   if(a.lda % 4 || a.ldb % 4 || ((uintptr_t)a.A % 16) || ((uintptr_t)a.B % 16))
     return false;

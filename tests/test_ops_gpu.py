@@ -223,3 +223,41 @@ def test_adam_graph_and_nonfinite_abort():  # test_train.cpp:86-113
         a2.update(g2, 0.1)
     assert a2.step() == 0
     assert np.all(g2.param_value("p") == 0.5)
+
+
+@pytest.mark.parametrize("ln,e", [(False, 6), (True, 6), (False, 0), (True, 0), (True, 40)])
+def test_gru_cell(ln, e):
+    """Fused GRU block (graph.cpp:648-813) incl. layer norm and
+    transition-only blocks, forward and every gradient."""
+    rng = np.random.default_rng(6)
+    b, d = 5, 24 if e != 40 else 64
+    names = ["Uz", "Ur", "Uh", "bz", "br", "bh"] + (["Wz", "Wr", "Wx"] if e else [])
+    if ln:
+        names += ["lnGz", "lnBz", "lnGr", "lnBr"] + (["lnGx", "lnBx"] if e else [])
+    shapes = {n: (d, d) if n[0] == "U" else (e, d) if n[0] == "W" else (d,) for n in names}
+    W = {n: (rng.normal(size=shapes[n]) * 0.4).astype(np.float32) for n in names}
+    packed = np.concatenate([W[n].ravel() for n in names])
+    h = rng.normal(size=(b, d)).astype(np.float32)
+    x = rng.normal(size=(b, e)).astype(np.float32) if e else None
+    G = rng.normal(size=(b, d)).astype(np.float32)
+    out, gh, gx, gw = R.op_gru(h, x, packed, ln, G, e, d)
+    g = M.ExpressionGraph(1)
+    gp = M.GruParams()
+    for n in names:
+        setattr(gp, n, _param(g, n, W[n]))
+    nh = _param(g, "h", h)
+    nx = _param(g, "x", x) if e else M.NodeRef()
+    o = g.gru_cell(nh, nx, gp, ln)
+    loss = _seeded(g, o, G)
+    g.forward()
+    g.zero_grads()
+    g.backward(loss)
+    _close(o.val(), out, 2e-6)
+    _close(g.param_grad("h"), gh, 2e-5)
+    if e:
+        _close(g.param_grad("x"), gx, 2e-5)
+    off = 0
+    for n in names:
+        sz = W[n].size
+        _close(g.param_grad(n).ravel(), gw[off:off + sz], 5e-5)
+        off += sz
