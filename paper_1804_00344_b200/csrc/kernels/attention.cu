@@ -563,6 +563,253 @@ __global__ void __launch_bounds__(256) attn_bwd_tile_kernel(AttBP p) {
   store(p.gv + bi * p.tk * p.ldk + hoff, p.ldk, tk, p.accV);
 }
 
+// ---------------------------------------------------------------------------
+// Padded-tile path for head dim 64 and tq, tk <= TT (TT = 32, 48 or 64): all
+// operands row-major in shared memory with a padded leading dimension of
+// 4*odd floats, so the strided float4 reads of the micro-GEMMs below are
+// bank-conflict free; 256 threads, each a 4x4 register tile.
+constexpr int DK = 64;
+constexpr int LDK = DK + 4;  // 68 = 4*17
+
+template <int TT>
+struct Pad {
+  static constexpr int LDP = TT + 4;  // 36, 52, 68: 4 * odd
+};
+
+// C[i][j] = sum_k A[i][k] * B[j][k]   (A: M x K, B: N x K, both row-major)
+// thread tile: rows i = ti + a*(M/4), cols j = tj + b*(N/4)
+template <int M, int N>
+__device__ __forceinline__ void mm_nt(const float* A, int lda, const float* B, int ldb, int K,
+                                      float* C, int ldc, float scale) {
+  constexpr int TI = M / 4, TJ = N / 4;
+  for(int t = threadIdx.x; t < TI * TJ; t += blockDim.x) {
+    const int ti = t % TI, tj = t / TI;
+    float acc[4][4] = {};
+    for(int k = 0; k < K; k += 4) {
+      float4 a[4], b[4];
+#pragma unroll
+      for(int u = 0; u < 4; ++u) {
+        a[u] = *reinterpret_cast<const float4*>(A + (ti + u * TI) * lda + k);
+        b[u] = *reinterpret_cast<const float4*>(B + (tj + u * TJ) * ldb + k);
+      }
+#pragma unroll
+      for(int u = 0; u < 4; ++u)
+#pragma unroll
+        for(int v = 0; v < 4; ++v) {
+          acc[u][v] = __fmaf_rn(a[u].x, b[v].x, acc[u][v]);
+          acc[u][v] = __fmaf_rn(a[u].y, b[v].y, acc[u][v]);
+          acc[u][v] = __fmaf_rn(a[u].z, b[v].z, acc[u][v]);
+          acc[u][v] = __fmaf_rn(a[u].w, b[v].w, acc[u][v]);
+        }
+    }
+#pragma unroll
+    for(int u = 0; u < 4; ++u)
+#pragma unroll
+      for(int v = 0; v < 4; ++v)
+        C[(ti + u * TI) * ldc + tj + v * TJ] = scale * acc[u][v];
+  }
+}
+
+// acc = sum_k A[i][k] * B[k][c] for rows i = ti + a*(M/4), cols c = 4tj..4tj+3
+// (A: M x K row-major, B: K x N row-major); calls store(i, c, value)
+template <int M, int N, typename Store>
+__device__ __forceinline__ void mm_nn(const float* A, int lda, const float* B, int ldb, int K,
+                                      Store store) {
+  constexpr int TI = M / 4, TJ = N / 4;
+  for(int t = threadIdx.x; t < TI * TJ; t += blockDim.x) {
+    const int ti = t % TI, tj = t / TI;
+    float acc[4][4] = {};
+    for(int k = 0; k < K; k += 4) {
+      float4 a[4], b[4];
+#pragma unroll
+      for(int u = 0; u < 4; ++u) {
+        a[u] = *reinterpret_cast<const float4*>(A + (ti + u * TI) * lda + k);
+        b[u] = *reinterpret_cast<const float4*>(B + (k + u) * ldb + tj * 4);
+      }
+#pragma unroll
+      for(int u = 0; u < 4; ++u) {
+        const float av[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+#pragma unroll
+        for(int kk = 0; kk < 4; ++kk) {
+          acc[u][0] = __fmaf_rn(av[kk], (&b[kk].x)[0], acc[u][0]);
+          acc[u][1] = __fmaf_rn(av[kk], (&b[kk].x)[1], acc[u][1]);
+          acc[u][2] = __fmaf_rn(av[kk], (&b[kk].x)[2], acc[u][2]);
+          acc[u][3] = __fmaf_rn(av[kk], (&b[kk].x)[3], acc[u][3]);
+        }
+      }
+    }
+#pragma unroll
+    for(int u = 0; u < 4; ++u)
+#pragma unroll
+      for(int v = 0; v < 4; ++v)
+        store(ti + u * TI, tj * 4 + v, acc[u][v]);
+  }
+}
+
+// stage rows x 64 floats of a head slice (row stride ld) into [TT][LDK],
+// zero-filling rows >= rows; float4 loads, consecutive threads on a row
+template <int TT>
+__device__ __forceinline__ void stage64(float* dst, const float* src, int64_t ld, int rows) {
+  for(int e = threadIdx.x; e < TT * (DK / 4); e += blockDim.x) {
+    const int r = e / (DK / 4), c4 = e % (DK / 4);
+    float4 v = r < rows ? *reinterpret_cast<const float4*>(src + (int64_t)r * ld + c4 * 4)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(dst + r * LDK + c4 * 4) = v;
+  }
+}
+
+template <int TT>
+__global__ void __launch_bounds__(256) attn_fwd_pad_kernel(AttP p) {
+  extern __shared__ float4 smem4[];
+  constexpr int LDP = Pad<TT>::LDP;
+  float* sm = reinterpret_cast<float*>(smem4);
+  float* Q = sm;                 // [TT][LDK]
+  float* K = Q + TT * LDK;
+  float* V = K + TT * LDK;
+  float* S = V + TT * LDK;       // [TT][LDP] scores, then P
+  const int h = blockIdx.x;
+  const int64_t bi = blockIdx.y;
+  const int tq = (int)p.tq, tk = (int)p.tk;
+  const int64_t hoff = (int64_t)h * DK;
+  stage64<TT>(Q, p.q + bi * p.tq * p.ldq + hoff, p.ldq, tq);
+  stage64<TT>(K, p.k + bi * p.tk * p.ldk + hoff, p.ldk, tk);
+  stage64<TT>(V, p.v + bi * p.tk * p.ldk + hoff, p.ldk, tk);
+  __syncthreads();
+  mm_nt<TT, TT>(Q, LDK, K, LDK, DK, S, LDP, p.scale);
+  __syncthreads();
+  // masked softmax: one warp per query row, two keys per lane (tk <= 64)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* P = p.probs + ((bi * p.heads + h) * p.tq) * p.tk;
+  for(int i = warp; i < TT; i += blockDim.x / 32) {
+    float* sr = S + i * LDP;
+    float x0 = -INFINITY, x1 = -INFINITY;
+    bool o0 = false, o1 = false;
+    if(i < tq) {
+      o0 = lane < tk && key_ok(p, bi, i, lane);
+      o1 = lane + 32 < tk && key_ok(p, bi, i, lane + 32);
+      if(o0)
+        x0 = sr[lane];
+      if(o1 && lane + 32 < TT)
+        x1 = sr[lane + 32];
+    }
+    float mx = warp_max(fmaxf(x0, x1));
+    bool any = mx != -INFINITY;
+    float e0 = o0 ? expf(x0 - mx) : 0.f, e1 = o1 ? expf(x1 - mx) : 0.f;
+    float s = warp_sum(e0 + e1);
+    if(i < tq && !any && lane == 0 && p.flags)
+      atomicOr(p.flags, MTKC_FLAG_MASKED_ROW);
+    float y0 = any ? e0 / s : 0.f, y1 = any ? e1 / s : 0.f;
+    if(lane < TT)
+      sr[lane] = y0;
+    if(lane + 32 < TT)
+      sr[lane + 32] = y1;
+    if(i < tq) {
+      if(lane < tk)
+        P[(int64_t)i * tk + lane] = y0;
+      if(lane + 32 < tk)
+        P[(int64_t)i * tk + lane + 32] = y1;
+    }
+  }
+  __syncthreads();
+  float* out = p.out + bi * p.tq * p.ldo + hoff;
+  mm_nn<TT, DK>(S, LDP, V, LDK, TT, [&](int i, int c, float v) {
+    if(i < tq)
+      out[(int64_t)i * p.ldo + c] = v;
+  });
+}
+
+template <int TT>
+__global__ void __launch_bounds__(256) attn_bwd_pad_kernel(AttBP p) {
+  extern __shared__ float4 smem4[];
+  constexpr int LDP = Pad<TT>::LDP;
+  float* sm = reinterpret_cast<float*>(smem4);
+  float* Q = sm;                  // [TT][LDK]
+  float* K = Q + TT * LDK;
+  float* V = K + TT * LDK;
+  float* dO = V + TT * LDK;
+  float* P = dO + TT * LDK;       // [TT][LDP]
+  float* dP = P + TT * LDP;       // [TT][LDP] dP, then dS
+  float* dSt = dP + TT * LDP;     // [TT][LDP] dS^T
+  float* Pt = dSt + TT * LDP;     // [TT][LDP] P^T
+  const int h = blockIdx.x;
+  const int64_t bi = blockIdx.y;
+  const int tq = (int)p.tq, tk = (int)p.tk;
+  const int64_t hoff = (int64_t)h * DK;
+  stage64<TT>(Q, p.q + bi * p.tq * p.ldq + hoff, p.ldq, tq);
+  stage64<TT>(K, p.k + bi * p.tk * p.ldk + hoff, p.ldk, tk);
+  stage64<TT>(V, p.v + bi * p.tk * p.ldk + hoff, p.ldk, tk);
+  stage64<TT>(dO, p.gout + bi * p.tq * p.ldo + hoff, p.ldo, tq);
+  const float* Pg = p.probs + ((bi * p.heads + h) * p.tq) * p.tk;
+  for(int e = threadIdx.x; e < TT * TT; e += blockDim.x) {
+    const int i = e / TT, j = e % TT;
+    float v = (i < tq && j < tk) ? Pg[(int64_t)i * tk + j] : 0.f;
+    P[i * LDP + j] = v;
+    Pt[j * LDP + i] = v;
+  }
+  __syncthreads();
+  mm_nt<TT, TT>(dO, LDK, V, LDK, DK, dP, LDP, 1.f);  // dP = dO V^T
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* G = p.ds + ((bi * p.heads + h) * p.tq) * p.tk;
+  for(int i = warp; i < TT; i += blockDim.x / 32) {
+    const float p0 = lane < TT ? P[i * LDP + lane] : 0.f;
+    const float p1 = lane + 32 < TT ? P[i * LDP + lane + 32] : 0.f;
+    const float d0 = lane < TT ? dP[i * LDP + lane] : 0.f;
+    const float d1 = lane + 32 < TT ? dP[i * LDP + lane + 32] : 0.f;
+    const float D = warp_sum(d0 * p0 + d1 * p1);
+    const float g0 = p.scale * (p0 * (d0 - D)), g1 = p.scale * (p1 * (d1 - D));
+    if(lane < TT) {
+      dP[i * LDP + lane] = g0;
+      dSt[lane * LDP + i] = g0;
+    }
+    if(lane + 32 < TT) {
+      dP[i * LDP + lane + 32] = g1;
+      dSt[(lane + 32) * LDP + i] = g1;
+    }
+    if(i < tq) {
+      if(lane < tk)
+        G[(int64_t)i * tk + lane] = g0;
+      if(lane + 32 < tk)
+        G[(int64_t)i * tk + lane + 32] = g1;
+    }
+  }
+  __syncthreads();
+  float* gq = p.gq + bi * p.tq * p.ldq + hoff;
+  float* gk = p.gk + bi * p.tk * p.ldk + hoff;
+  float* gv = p.gv + bi * p.tk * p.ldk + hoff;
+  mm_nn<TT, DK>(dP, LDP, K, LDK, TT, [&](int i, int c, float v) {  // dQ = dS K
+    if(i < tq) {
+      float* d = gq + (int64_t)i * p.ldq + c;
+      *d = p.accQ ? *d + v : v;
+    }
+  });
+  mm_nn<TT, DK>(dSt, LDP, Q, LDK, TT, [&](int j, int c, float v) {  // dK = dS^T Q
+    if(j < tk) {
+      float* d = gk + (int64_t)j * p.ldk + c;
+      *d = p.accK ? *d + v : v;
+    }
+  });
+  mm_nn<TT, DK>(Pt, LDP, dO, LDK, TT, [&](int j, int c, float v) {  // dV = P^T dO
+    if(j < tk) {
+      float* d = gv + (int64_t)j * p.ldk + c;
+      *d = p.accV ? *d + v : v;
+    }
+  });
+}
+
+int pad_tile(int64_t tq, int64_t tk, int64_t dk, int64_t ldq, int64_t ldk, int64_t ldo) {
+  if(dk != DK || (ldq | ldk | ldo) % 4 || getenv("MTK_ATTN_TILE64"))
+    return 0;
+  int64_t t = std::max(tq, tk);
+  return t <= 32 ? 32 : t <= 48 ? 48 : t <= 64 ? 64 : 0;
+}
+
+template <int TT>
+size_t pad_smem(bool bwd) {
+  return sizeof(float) * (bwd ? (4 * TT * LDK + 4 * TT * Pad<TT>::LDP)
+                              : (3 * TT * LDK + TT * Pad<TT>::LDP));
+}
+
 bool tile_path(int64_t tq, int64_t tk, int64_t dk, int64_t ldq, int64_t ldk, int64_t ldo) {
   (void)ldq;
   (void)ldk;
@@ -584,6 +831,22 @@ int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_
     return fail(MTKC_DIMENSION, "fused attention supports tk <= 512 and head dim <= 128");
   ProfScope prof(S(stream), "attention", 4.0 * b * heads * tq * tk * dk);
   AttP p{out, ldo, probs, q, ldq, k, v, ldk, key_mask, b, tq, tk, heads, dk, scale, causal, flags};
+  if(int tt = pad_tile(tq, tk, dk, ldq, ldk, ldo)) {
+    dim3 grid((unsigned)heads, (unsigned)b);
+    int rc = MTKC_OK;
+#define MTKC_ATT_FWD(TTV)                                                         \
+  if(tt == TTV) {                                                                 \
+    size_t smem = pad_smem<TTV>(false);                                           \
+    rc = set_smem((const void*)attn_fwd_pad_kernel<TTV>, smem);                   \
+    if(rc)                                                                        \
+      return rc;                                                                  \
+    attn_fwd_pad_kernel<TTV><<<grid, 256, smem, S(stream)>>>(p);                  \
+  }
+    MTKC_ATT_FWD(32) MTKC_ATT_FWD(48) MTKC_ATT_FWD(64)
+#undef MTKC_ATT_FWD
+    MTKC_POST_LAUNCH("attn_fwd_pad_kernel");
+    return MTKC_OK;
+  }
   if(tile_path(tq, tk, dk, ldq, ldk, ldo)) {
     size_t smem = 4 * TILE * sizeof(float);
     int rc = set_smem((const void*)attn_fwd_tile_kernel, smem);
@@ -617,6 +880,22 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
   ProfScope prof(S(stream), "attention", 8.0 * b * heads * tq * tk * dk);
   AttBP p{gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, dsbuf, b, tq, tk, heads, dk, scale,
           accumulate_q, accumulate_k, accumulate_v};
+  if(int tt = pad_tile(tq, tk, dk, ldq, ldk, ldo)) {
+    dim3 grid((unsigned)heads, (unsigned)b);
+    int rc = MTKC_OK;
+#define MTKC_ATT_BWD(TTV)                                                         \
+  if(tt == TTV) {                                                                 \
+    size_t smem = pad_smem<TTV>(true);                                            \
+    rc = set_smem((const void*)attn_bwd_pad_kernel<TTV>, smem);                   \
+    if(rc)                                                                        \
+      return rc;                                                                  \
+    attn_bwd_pad_kernel<TTV><<<grid, 256, smem, S(stream)>>>(p);                  \
+  }
+    MTKC_ATT_BWD(32) MTKC_ATT_BWD(48) MTKC_ATT_BWD(64)
+#undef MTKC_ATT_BWD
+    MTKC_POST_LAUNCH("attn_bwd_pad_kernel");
+    return MTKC_OK;
+  }
   if(tile_path(tq, tk, dk, ldq, ldk, ldo)) {
     size_t smem = 6 * TILE * sizeof(float);
     int rc = set_smem((const void*)attn_bwd_tile_kernel, smem);

@@ -329,28 +329,57 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if(p.tmaStore) {
           if(!p.part) {
             const bool rowOk = row < p.M;
+            // bias: one coalesced load per lane, broadcast by shuffles
+            const float bl = (p.bias && col0 + lane < p.N) ? p.bias[col0 + lane] : 0.f;
 #pragma unroll
             for(int i = 0; i < 32; ++i) {
               float x = p.alpha == 1.f ? v[i] : p.alpha * v[i];
               if(p.bias)
-                x = x + (col0 + i < p.N ? p.bias[col0 + i] : 0.f);
+                x = x + __shfl_sync(0xffffffffu, bl, i);
               if(p.epi == MTKC_EPI_RELU)
                 x = x > 0.f ? x : 0.f;
               v[i] = x;
             }
             if((p.gate || p.beta != 0.f) && rowOk) {
+              // this lane's 32 columns of its own row: 16-byte loads when aligned
               const float* grow = p.gate ? p.gate + row * p.ldc + col0 : nullptr;
               const float* crow = p.C + row * p.ldc + col0;
+              const bool vec = col0 + 32 <= p.N && (p.ldc % 4 == 0) &&
+                               (((uintptr_t)p.C | (uintptr_t)(p.gate ? p.gate : p.C)) % 16 == 0);
+              if(vec) {
 #pragma unroll
-              for(int i = 0; i < 32; ++i) {
-                if(col0 + i >= p.N)
-                  break;
-                float x = v[i];
-                if(grow)
-                  x = grow[i] > 0.f ? x : 0.f;
-                if(p.beta != 0.f)
-                  x = (p.beta == 1.f ? crow[i] : p.beta * crow[i]) + x;
-                v[i] = x;
+                for(int j = 0; j < 8; ++j) {
+                  float gv[4] = {1.f, 1.f, 1.f, 1.f}, cv[4] = {0.f, 0.f, 0.f, 0.f};
+                  if(grow) {
+                    float4 g4 = *reinterpret_cast<const float4*>(grow + 4 * j);
+                    gv[0] = g4.x; gv[1] = g4.y; gv[2] = g4.z; gv[3] = g4.w;
+                  }
+                  if(p.beta != 0.f) {
+                    float4 c4 = *reinterpret_cast<const float4*>(crow + 4 * j);
+                    cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
+                  }
+#pragma unroll
+                  for(int u = 0; u < 4; ++u) {
+                    float x = v[4 * j + u];
+                    if(grow)
+                      x = gv[u] > 0.f ? x : 0.f;
+                    if(p.beta != 0.f)
+                      x = (p.beta == 1.f ? cv[u] : p.beta * cv[u]) + x;
+                    v[4 * j + u] = x;
+                  }
+                }
+              } else {
+#pragma unroll
+                for(int i = 0; i < 32; ++i) {
+                  if(col0 + i >= p.N)
+                    break;
+                  float x = v[i];
+                  if(grow)
+                    x = grow[i] > 0.f ? x : 0.f;
+                  if(p.beta != 0.f)
+                    x = (p.beta == 1.f ? crow[i] : p.beta * crow[i]) + x;
+                  v[i] = x;
+                }
               }
             }
           }

@@ -21,15 +21,30 @@ shapes = [  # (name, M, N, K, transA, transB)
     ("ffn2 dX", R, 2048, 512, 0, 1),
     ("ffn1 dW", 512, 2048, R, 1, 0),
     ("square 8192", 8192, 8192, 8192, 0, 0),
+    ("logits fwd +bias", R, 32000, 512, 0, 1, "bias"),
+    ("ffn1 fwd +bias+relu", R, 2048, 512, 0, 0, "relu"),
+    ("ffn2 dX +gate", R, 2048, 512, 0, 1, "gate"),
+    ("proj dW beta=1", 512, 512, R, 1, 0, "beta"),
 ]
 ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 stream = torch.cuda.current_stream().cuda_stream
-for name, M, N, K, ta, tb in shapes:
+for name, M, N, K, ta, tb, *extra in shapes:
     A = torch.randn((K, M) if ta else (M, K), device="cuda")
     B = torch.randn((N, K) if tb else (K, N), device="cuda")
-    C = torch.empty(M, N, device="cuda")
+    C = torch.zeros(M, N, device="cuda")
     args = dict(trans_a=ta, trans_b=tb, precision=1, workspace=ws.data_ptr(),
                 workspace_bytes=ws.numel(), stream=stream)
+    ep = extra[0] if extra else None
+    bias = torch.randn(N, device="cuda")
+    gate = torch.randn(M, N, device="cuda")
+    if ep in ("bias", "relu"):
+        args["bias"] = bias.data_ptr()
+    if ep == "relu":
+        args["relu"] = True
+    if ep == "gate":
+        args["gate"] = gate.data_ptr()
+    if ep == "beta":
+        args["beta"] = 1.0
     for _ in range(3):
         cabi.gemm(M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, **args)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -41,5 +56,5 @@ for name, M, N, K, ta, tb in shapes:
     ms = e0.elapsed_time(e1) / reps
     tf = 2.0 * M * N * K / ms / 1e9
     ref = (A.t() if ta else A) @ (B.t() if tb else B)
-    err = ((C - ref).abs().max() / ref.abs().max()).item()
+    err = ((C - ref).abs().max() / ref.abs().max()).item() if not ep else float("nan")
     print(f"{name:22s} M{M:6d} N{N:6d} K{K:6d}  {ms*1e3:9.1f} us  {tf:7.1f} TF/s  relerr {err:.1e}", flush=True)
