@@ -100,7 +100,9 @@ uint64_t mtkc_d2h_bytes(void);
  * and Adam entry points bracket their launches with events and record the
  * algorithmic work (FLOPs for GEMM/attention, HBM bytes otherwise).
  * mtkc_prof_report synchronises and writes one line per class:
- *   "<class> <launches> <total_ms> <total_work>\n"  (then resets). */
+ *   "<class> <launches> <total_ms> <total_work>\n"  (then resets).
+ * on = 2 (detail mode) appends the call's shape to the class name
+ * ("gemm_tc:M8192_N512_K512_tA0_tB0"), for per-shape breakdowns. */
 int mtkc_prof_enable(int on);
 /* Keep the stream busy for `us` microseconds (profiling aid: lets the host
  * queue a whole step ahead so event timings measure device time only). */

@@ -291,6 +291,57 @@ int ref_train(void* h, void* ex, int workers, int64_t budget, uint64_t seed, int
   });
 }
 
+// train() with checkpointing / resume (train.cpp:284-287, 407-418)
+int ref_train_ckpt(void* h, void* ex, int workers, int64_t budget, uint64_t seed, int64_t epochs,
+                   int64_t maxUpdates, float lrBase, int64_t warmup, const char* ckptPath,
+                   int64_t ckptEvery, const char* resumeFrom, double* finalLoss,
+                   int64_t* updates) {
+  return guard([&] {
+    auto* m = static_cast<RefModel*>(h);
+    TrainOptions o;
+    o.workers = workers;
+    o.tokenBudget = budget;
+    o.seed = seed;
+    o.epochs = epochs;
+    o.maxUpdates = maxUpdates;
+    o.lr.base = lrBase;
+    o.lr.warmup = warmup;
+    o.checkpointPath = ckptPath ? ckptPath : "";
+    o.checkpointEvery = ckptEvery;
+    o.resumeFrom = resumeFrom ? resumeFrom : "";
+    TrainResult r = train(m->model, static_cast<RefExamples*>(ex)->ex, *m->g, *m->adam,
+                          *m->avg, o);
+    *finalLoss = r.finalLoss;
+    *updates = r.updates;
+  });
+}
+
+int ref_save_model(void* h, const char* path) {
+  return guard([&] {
+    auto* m = static_cast<RefModel*>(h);
+    saveModel(path, m->cfg, *m->g);
+  });
+}
+
+int ref_load_params(void* h, const char* path) {
+  return guard([&] { loadParams(readModelFile(path), *static_cast<RefModel*>(h)->g); });
+}
+
+int ref_save_checkpoint(void* h, const char* path, int64_t update, int64_t epoch,
+                        int64_t batch) {
+  return guard([&] {
+    auto* m = static_cast<RefModel*>(h);
+    saveCheckpoint(path, m->cfg, *m->g, *m->adam, *m->avg, update, epoch, batch);
+  });
+}
+
+int ref_load_checkpoint(void* h, const char* path, int64_t* counters) {
+  return guard([&] {
+    auto* m = static_cast<RefModel*>(h);
+    loadCheckpoint(path, *m->g, *m->adam, *m->avg, counters[0], counters[1], counters[2]);
+  });
+}
+
 int64_t ref_parameter_total(const char* cfgText) {
   int64_t n = -1;
   guard([&] { n = parameterTotal(ModelConfig::parse(cfgText)); });

@@ -68,6 +68,12 @@ def lib():
             "ref_adam_update": (I, [P, C.c_float]),
             "ref_train": (I, [P, P, I, I64, U64, I64, I64, C.c_float, I64, dp, lp]),
             "ref_parameter_total": (I64, [C.c_char_p]),
+            "ref_train_ckpt": (I, [P, P, I, I64, U64, I64, I64, C.c_float, I64, C.c_char_p, I64,
+                                   C.c_char_p, dp, lp]),
+            "ref_save_model": (I, [P, C.c_char_p]),
+            "ref_load_params": (I, [P, C.c_char_p]),
+            "ref_save_checkpoint": (I, [P, C.c_char_p, I64, I64, I64]),
+            "ref_load_checkpoint": (I, [P, C.c_char_p, lp]),
             "ref_matmul": (I, [I, lp, fp, I, lp, fp, I, lp, fp, I, I, C.c_float, C.c_float]),
             "ref_op_dot": (I, [I, lp, fp, I, lp, fp, I, I, fp, fp, fp, fp]),
             "ref_op_layernorm": (I, [I64, I64, fp, fp, fp, fp, fp, fp, fp, fp]),
@@ -244,6 +250,33 @@ class RefModel:
         _check(lib().ref_train(self.h, examples.h, workers, budget, seed, epochs, max_updates,
                                lr_base, warmup, C.byref(fl), C.byref(up)))
         return fl.value, up.value
+
+
+    def train_ckpt(self, examples: Examples, workers=1, budget=256, seed=1, epochs=1,
+                   max_updates=-1, lr_base=3e-4, warmup=16000, checkpoint_path="",
+                   checkpoint_every=0, resume_from=""):
+        """train.cpp:407-418 with checkpointing / resume."""
+        fl = C.c_double()
+        up = C.c_int64()
+        _check(lib().ref_train_ckpt(self.h, examples.h, workers, budget, seed, epochs,
+                                    max_updates, lr_base, warmup, checkpoint_path.encode(),
+                                    checkpoint_every, resume_from.encode(), C.byref(fl),
+                                    C.byref(up)))
+        return fl.value, up.value
+
+    def save_model(self, path: str):
+        _check(lib().ref_save_model(self.h, path.encode()))
+
+    def load_params(self, path: str):
+        _check(lib().ref_load_params(self.h, path.encode()))
+
+    def save_checkpoint(self, path: str, update: int, epoch: int, batch: int):
+        _check(lib().ref_save_checkpoint(self.h, path.encode(), update, epoch, batch))
+
+    def load_checkpoint(self, path: str):
+        c = np.zeros(3, np.int64)
+        _check(lib().ref_load_checkpoint(self.h, path.encode(), _l(c)))
+        return tuple(int(x) for x in c)
 
 
 def parameter_total(config_text: str) -> int:

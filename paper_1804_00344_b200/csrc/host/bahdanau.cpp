@@ -123,7 +123,7 @@ std::pair<NodeRef, NodeRef> ExpressionGraph::bahdanau(NodeRef wq, NodeRef uk, No
     }
     MTKC(mtkc_bahdanau_backward(&p, stream()));
     Device& dev = Device::get();
-    size_t ws = (size_t)((b + 127) / 128 + 1) * (size_t)a * sizeof(float) * 2;
+    size_t ws = (size_t)((b + 63) / 64 + 1) * (size_t)a * sizeof(float) * 2;
     float* w = dev.scratch(ws);
     int nparam = ln ? 3 : 1;
     const int pidx[3] = {2, 4, 5};

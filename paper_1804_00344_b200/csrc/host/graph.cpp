@@ -701,7 +701,7 @@ static NodeRef affineImpl(ExpressionGraph& g, NodeRef x, NodeRef w, NodeRef b, b
     {  // db
       auto d = g.gradDst(n.inputs[2]);
       Device& dev = Device::get();
-      size_t ws = (size_t)((rows + 127) / 128) * (size_t)N * sizeof(float);
+      size_t ws = (size_t)((rows + 63) / 64) * (size_t)N * sizeof(float);
       float* w = dev.scratch(ws);
       MTKC(mtkc_colsum(d.ptr, go, rows, N, d.accumulate, w, dev.scratchBytes(), dev.stream()));
     }
@@ -1368,6 +1368,16 @@ int64_t ExpressionGraph::paramOffset(const std::string& name) const {
 void ExpressionGraph::zeroGrads() {
   for(auto& [name, p] : params_)
     p.gradLive = false;  // logically zero; the first contributor writes
+}
+
+void ExpressionGraph::syncParamViews() {
+  // dev() uploads pending host edits and marks the host caches stale, so a
+  // later host read sees what device-side updates (Adam, EMA apply) wrote
+  for(auto& [name, p] : params_) {
+    p.value.dev();
+    if(p.gradLive)
+      p.grad.dev();
+  }
 }
 
 void ExpressionGraph::realizeParamGrads() {

@@ -40,7 +40,7 @@ void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
 
 void colsumInto(ExpressionGraph::GradDst dst, const float* in, int64_t rows, int64_t cols) {
   Device& dev = Device::get();
-  size_t ws = (size_t)((rows + 127) / 128) * (size_t)cols * sizeof(float) * 2;
+  size_t ws = (size_t)((rows + 63) / 64) * (size_t)cols * sizeof(float) * 2;
   float* w = dev.scratch(ws);
   MTKC(mtkc_colsum(dst.ptr, in, rows, cols, dst.accumulate, w, dev.scratchBytes(), dev.stream()));
 }

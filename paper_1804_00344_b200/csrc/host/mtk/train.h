@@ -13,7 +13,7 @@
 #include <iosfwd>
 #include <map>
 
-#include "mtk/models.h"
+#include "mtk/serialize.h"
 
 namespace mtk {
 
@@ -50,6 +50,9 @@ public:
   // moment views for checkpointing (names in graph order)
   Tensor firstMoment(ExpressionGraph& g, const std::string& name);
   Tensor secondMoment(ExpressionGraph& g, const std::string& name);
+  // moments exist once an update ran or a checkpoint supplied them
+  bool hasMoments() const { return haveMoments_; }
+  void resetMoments(ExpressionGraph& g, bool present);  // zero m, v (checkpoint load)
 
 private:
   void ensure(ExpressionGraph& g);
@@ -58,6 +61,7 @@ private:
   int64_t step_ = 0;
   std::shared_ptr<DeviceBuffer> m_, v_;
   int64_t n_ = 0;
+  bool haveMoments_ = false;
   bool pending_ = false;
   int64_t pendingSteps_ = 0;
   ExpressionGraph* lastGraph_ = nullptr;
@@ -79,6 +83,7 @@ public:
   Real beta() const { return beta_; }
   Tensor value(ExpressionGraph& g, const std::string& name);
   float* ensure(ExpressionGraph& g);  // flat shadow in pool layout (zero-initialised)
+  void reset();                       // drop the shadow (next update starts from zero)
 
 private:
   Real beta_;
@@ -147,6 +152,17 @@ private:
 };
 
 uint64_t mixSeed(uint64_t seed, int64_t update, int worker);
+
+// Checkpoints (train.cpp:121-164): parameters, then "adam.m.<name>",
+// "adam.v.<name>" and "avg.<name>" in name order once they exist, then
+// "trainer.counters" = {update, epoch, batchIndex, adam step} -- the
+// reference's MTK1 layout, so checkpoints move between the two builds.
+void saveCheckpoint(const std::string& path, const ModelConfig& config, ExpressionGraph& g,
+                    Adam& adam, AveragedParameters& average, int64_t update, int64_t epoch,
+                    int64_t batchIndex);
+void loadCheckpoint(const std::string& path, ExpressionGraph& g, Adam& adam,
+                    AveragedParameters& average, int64_t& update, int64_t& epoch,
+                    int64_t& batchIndex);
 
 TrainResult train(Model& model, const std::vector<Example>& data, ExpressionGraph& master,
                   Adam& adam, AveragedParameters& average, const TrainOptions& opts);

@@ -117,7 +117,7 @@ PYBIND11_MODULE(_mtk, m) {
   m.def("launch_count", [] { return (uint64_t)mtkc_launch_count(); });
   m.def("h2d_bytes", [] { return (uint64_t)mtkc_h2d_bytes(); });
   m.def("d2h_bytes", [] { return (uint64_t)mtkc_d2h_bytes(); });
-  m.def("prof_enable", [](bool on) { MTKC(mtkc_prof_enable(on ? 1 : 0)); });
+  m.def("prof_enable", [](int on) { MTKC(mtkc_prof_enable(on)); });
   m.def("gpu_sleep", [](int64_t us) { MTKC(mtkc_gpu_sleep(us, Device::get().stream())); });
   // CUDA events on the compute stream (the stream every kernel runs on)
   m.def("event_record", [] {
@@ -437,7 +437,27 @@ PYBIND11_MODULE(_mtk, m) {
       .def_readwrite("max_updates", &TrainOptions::maxUpdates)
       .def_readwrite("lr", &TrainOptions::lr)
       .def_readwrite("average_beta", &TrainOptions::averageBeta)
-      .def_readwrite("log_every", &TrainOptions::logEvery);
+      .def_readwrite("log_every", &TrainOptions::logEvery)
+      .def_readwrite("checkpoint_path", &TrainOptions::checkpointPath)
+      .def_readwrite("checkpoint_every", &TrainOptions::checkpointEvery)
+      .def_readwrite("resume_from", &TrainOptions::resumeFrom);
+  m.def("save_model", [](const std::string& path, const std::string& cfg, G& g) {
+    saveModel(path, ModelConfig::parse(cfg), g);
+  });
+  m.def("load_params", [](const std::string& path, G& g) { loadParams(readModelFile(path), g); });
+  m.def("read_model_config", [](const std::string& path) {
+    return readModelFile(path).config.serialize();
+  });
+  m.def("save_checkpoint", [](const std::string& path, const std::string& cfg, G& g, Adam& adam,
+                              AveragedParameters& avg, int64_t update, int64_t epoch,
+                              int64_t batch) {
+    saveCheckpoint(path, ModelConfig::parse(cfg), g, adam, avg, update, epoch, batch);
+  });
+  m.def("load_checkpoint", [](const std::string& path, G& g, Adam& adam, AveragedParameters& avg) {
+    int64_t u = 0, e = 0, b = 0;
+    loadCheckpoint(path, g, adam, avg, u, e, b);
+    return py::make_tuple(u, e, b);
+  });
 
   py::class_<TrainResult>(m, "TrainResult")
       .def_readonly("updates", &TrainResult::updates)

@@ -2,6 +2,7 @@
 // (reference: src/train.cpp).
 #include "mtk/train.h"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -53,8 +54,18 @@ void Adam::ensure(ExpressionGraph& g) {
   n_ = std::max(n_, n);
 }
 
+void Adam::resetMoments(ExpressionGraph& g, bool present) {
+  ensure(g);
+  haveMoments_ = present;
+  Device& d = Device::get();
+  MTKC(mtkc_memset(m_->ptr, 0, (size_t)n_ * sizeof(float), d.stream()));
+  MTKC(mtkc_memset(v_->ptr, 0, (size_t)n_ * sizeof(float), d.stream()));
+}
+
 void Adam::launch(ExpressionGraph& g, Real lr, AveragedParameters* avg) {
   ensure(g);
+  haveMoments_ = true;
+  g.syncParamViews();  // host edits uploaded, host caches invalidated
   g.realizeParamGrads();
   Device& d = Device::get();
   int64_t n = g.pool().used();
@@ -169,7 +180,13 @@ float* AveragedParameters::ensure(ExpressionGraph& g) {
   return buf_->ptr;
 }
 
+void AveragedParameters::reset() {
+  buf_.reset();
+  n_ = 0;
+}
+
 void AveragedParameters::update(ExpressionGraph& g) {  // train.cpp:69-79
+  g.syncParamViews();
   float* a = ensure(g);
   MTKC(mtkc_ema(a, g.pool().values()->ptr, g.pool().used(), beta_, Device::get().stream()));
 }
@@ -177,6 +194,7 @@ void AveragedParameters::update(ExpressionGraph& g) {  // train.cpp:69-79
 void AveragedParameters::applyTo(ExpressionGraph& g) const {
   if(!buf_)
     return;
+  g.syncParamViews();
   MTKC(mtkc_memcpy_d2d(g.pool().values()->ptr, buf_->ptr,
                        (size_t)std::min<int64_t>(n_, g.pool().used()) * sizeof(float),
                        Device::get().stream()));
@@ -201,6 +219,72 @@ void setDistributed(int rank, int world, const void* ncclId128) {
   g_dist.world = world;
   if(world > 1)
     MTKC(mtkc_nccl_comm_init(&g_dist.comm, world, rank, ncclId128));
+}
+
+// ---------------------------------------------------------- checkpoints
+
+void saveCheckpoint(const std::string& path, const ModelConfig& config, ExpressionGraph& g,
+                    Adam& adam, AveragedParameters& average, int64_t update, int64_t epoch,
+                    int64_t batchIndex) {  // train.cpp:123-139
+  adam.checkDeferred();
+  std::vector<std::pair<std::string, Tensor>> tensors;
+  for(auto& name : g.paramNames())
+    tensors.emplace_back(name, g.paramValue(name));
+  // the reference keeps moments / averages in std::maps: name order
+  std::vector<std::string> sorted = g.paramNames();
+  std::sort(sorted.begin(), sorted.end());
+  if(adam.hasMoments()) {
+    for(auto& name : sorted)
+      tensors.emplace_back("adam.m." + name, adam.firstMoment(g, name));
+    for(auto& name : sorted)
+      tensors.emplace_back("adam.v." + name, adam.secondMoment(g, name));
+  }
+  if(!average.empty())
+    for(auto& name : sorted)
+      tensors.emplace_back("avg." + name, average.value(g, name));
+  Tensor counters(Shape({4}), {(Real)update, (Real)epoch, (Real)batchIndex,
+                               (Real)adam.step()});
+  tensors.emplace_back("trainer.counters", counters);
+  writeModelFile(path, config, tensors);
+}
+
+void loadCheckpoint(const std::string& path, ExpressionGraph& g, Adam& adam,
+                    AveragedParameters& average, int64_t& update, int64_t& epoch,
+                    int64_t& batchIndex) {  // train.cpp:141-164
+  ModelFile file = readModelFile(path);
+  loadParams(file, g);
+  adam.checkDeferred();
+  bool haveM = false, haveAvg = false;
+  for(auto& [name, t] : file.tensors) {
+    haveM = haveM || name.rfind("adam.m.", 0) == 0 || name.rfind("adam.v.", 0) == 0;
+    haveAvg = haveAvg || name.rfind("avg.", 0) == 0;
+  }
+  // moments / averages absent from the file start from zero, as the
+  // reference's cleared maps do at the next update
+  adam.resetMoments(g, haveM);
+  average.reset();
+  if(haveAvg)
+    average.ensure(g);
+  for(auto& [name, t] : file.tensors) {
+    auto fill = [&](Tensor dst, const char* what) {
+      if(dst.shape() != t.shape())
+        throw DataError(std::string(what) + " " + name + " shape mismatch in " + path);
+      dst.copyFrom(t);
+    };
+    if(name.rfind("adam.m.", 0) == 0 && g.hasParam(name.substr(7)))
+      fill(adam.firstMoment(g, name.substr(7)), "moment");
+    else if(name.rfind("adam.v.", 0) == 0 && g.hasParam(name.substr(7)))
+      fill(adam.secondMoment(g, name.substr(7)), "moment");
+    else if(name.rfind("avg.", 0) == 0 && g.hasParam(name.substr(4)))
+      fill(average.value(g, name.substr(4)), "average");
+  }
+  const Tensor* counters = file.find("trainer.counters");
+  if(!counters || counters->size() != 4)
+    throw DataError("checkpoint lacks trainer counters: " + path);
+  update = (int64_t)counters->at(0);
+  epoch = (int64_t)counters->at(1);
+  batchIndex = (int64_t)counters->at(2);
+  adam.setStep((int64_t)counters->at(3));
 }
 
 // ----------------------------------------------------------- training
@@ -292,20 +376,21 @@ void logLine(const TrainOptions& opts, int64_t update, int64_t epoch, double los
 
 TrainResult train(Model& model, const std::vector<Example>& data, ExpressionGraph& master,
                   Adam& adam, AveragedParameters& average, const TrainOptions& opts) {
+  // train.cpp:407-418 + trainSync :200-300
   if(opts.workers < 1)
     throw ContractError("training needs at least one worker");
   if(opts.async)
     throw ContractError("asynchronous (hogwild) training is outside the B200 training path");
-  if(!opts.resumeFrom.empty())
-    throw ContractError("resume is not implemented in this build");
   model.registerParams(master);
   master.clear();
+  int64_t update = 0, startEpoch = 0, startBatch = 0;
+  if(!opts.resumeFrom.empty())
+    loadCheckpoint(opts.resumeFrom, master, adam, average, update, startEpoch, startBatch);
   SyncStepper stepper(model, master, adam, average, opts);
   TrainResult res;
-  int64_t update = 0;
   auto t0 = std::chrono::steady_clock::now();
   int64_t tokensSeen = 0;
-  for(int64_t epoch = 0; epoch < opts.epochs; ++epoch) {
+  for(int64_t epoch = startEpoch; epoch < opts.epochs; ++epoch) {
     BatchOptions bo;
     bo.tokenBudget = opts.tokenBudget;
     bo.seed = opts.seed + (uint64_t)epoch;
@@ -313,7 +398,7 @@ TrainResult train(Model& model, const std::vector<Example>& data, ExpressionGrap
     auto batches = makeBatches(data, bo);  // epochBatches, train.cpp:183-190
     double epochLoss = 0;
     int64_t epochUpdates = 0;
-    for(size_t idx = 0; idx < batches.size();) {
+    for(size_t idx = (epoch == startEpoch ? (size_t)startBatch : 0); idx < batches.size();) {
       int take = (int)std::min<size_t>((size_t)opts.workers, batches.size() - idx);
       std::vector<const Batch*> ptrs;
       for(int i = 0; i < take; ++i)
@@ -327,6 +412,10 @@ TrainResult train(Model& model, const std::vector<Example>& data, ExpressionGrap
       tokensSeen += (int64_t)r.tokens;
       double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       logLine(opts, update, epoch, r.loss, lr, secs > 0 ? (double)tokensSeen / secs : 0);
+      if(!opts.checkpointPath.empty() && opts.checkpointEvery > 0 &&
+         update % opts.checkpointEvery == 0 && distContext().rank == 0)
+        saveCheckpoint(opts.checkpointPath, model.config, master, adam, average, update, epoch,
+                       (int64_t)idx);
       if(opts.maxUpdates >= 0 && update >= opts.maxUpdates) {
         res.updates = update;
         res.epochs = epoch + 1;

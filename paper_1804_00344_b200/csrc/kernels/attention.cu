@@ -830,6 +830,8 @@ int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_
   if(tk > MAX_TK || dk > MAX_DK || dk <= 0)
     return fail(MTKC_DIMENSION, "fused attention supports tk <= 512 and head dim <= 128");
   ProfScope prof(S(stream), "attention", 4.0 * b * heads * tq * tk * dk);
+  if(prof_detail())
+    prof.detail = "fwd_b" + std::to_string(b) + "_tq" + std::to_string(tq) + "_tk" + std::to_string(tk);
   AttP p{out, ldo, probs, q, ldq, k, v, ldk, key_mask, b, tq, tk, heads, dk, scale, causal, flags};
   if(int tt = pad_tile(tq, tk, dk, ldq, ldk, ldo)) {
     dim3 grid((unsigned)heads, (unsigned)b);
@@ -878,6 +880,8 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
   if(tk > MAX_TK || dk > MAX_DK || dk <= 0)
     return fail(MTKC_DIMENSION, "fused attention supports tk <= 512 and head dim <= 128");
   ProfScope prof(S(stream), "attention", 8.0 * b * heads * tq * tk * dk);
+  if(prof_detail())
+    prof.detail = "bwd_b" + std::to_string(b) + "_tq" + std::to_string(tq) + "_tk" + std::to_string(tk);
   AttBP p{gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, dsbuf, b, tq, tk, heads, dk, scale,
           accumulate_q, accumulate_k, accumulate_v};
   if(int tt = pad_tile(tq, tk, dk, ldq, ldk, ldo)) {

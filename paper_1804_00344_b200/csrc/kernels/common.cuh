@@ -20,20 +20,23 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Event-bracketed profiling of one C-ABI call (mtkc_prof_enable).
 bool prof_on();
+bool prof_detail();  // mtkc_prof_enable(2): classes carry the call's shape
 void prof_begin(cudaStream_t st, void** token);
-void prof_end(cudaStream_t st, void* token, const char* cls, double work);
+void prof_end(cudaStream_t st, void* token, const std::string& cls, double work);
 struct ProfScope {
   cudaStream_t st;
   void* tok = nullptr;
   const char* cls;
   double work;
+  std::string detail;  // appended to the class name in detail mode
   ProfScope(cudaStream_t s, const char* c, double w) : st(s), cls(c), work(w) {
     if(prof_on())
       prof_begin(st, &tok);
   }
   ~ProfScope() {
     if(tok)
-      prof_end(st, tok, cls, work);
+      prof_end(st, tok, detail.empty() ? std::string(cls) : std::string(cls) + ":" + detail,
+               work);
   }
 };
 

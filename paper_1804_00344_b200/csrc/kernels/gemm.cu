@@ -143,6 +143,13 @@ int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
     return fail(MTKC_CONTRACT, "mtkc_gemm: null operand");
   int rc = MTKC_OK;
   ProfScope prof(S(stream), "gemm_tc", 2.0 * a->M * a->N * a->K * a->batch);
+  if(prof_detail()) {
+    char d[128];
+    snprintf(d, sizeof(d), "M%lld_N%lld_K%lld_b%lld_tA%d_tB%d_e%d%s%s",
+             (long long)a->M, (long long)a->N, (long long)a->K, (long long)a->batch, a->transA,
+             a->transB, a->epilogue, a->beta != 0.f ? "_acc" : "", a->bias ? "_bias" : "");
+    prof.detail = d;
+  }
   if(a->precision == MTKC_GEMM_TF32 && tc_gemm(*a, S(stream), &rc)) {
     t_last_path = 1;
     return rc;

@@ -210,7 +210,7 @@ int mtkc_layernorm_backward(const float* dy, const float* gain, const float* inv
     colred_partial_kernel<2><<<dim3((unsigned)cdiv(d, CR_COLS), (unsigned)nblk), 256, 0, st>>>(
         workspace, dy, xhat, rows, d);
     MTKC_POST_LAUNCH("colred_partial_kernel");
-    colred_final_kernel<2><<<(unsigned)cdiv(d, 128), 128, 0, st>>>(dgain, dbias, workspace, nblk,
+    colred_final_kernel<2><<<colred_final_grid(d), 256, 0, st>>>(dgain, dbias, workspace, nblk,
                                                                   d, accumulate_params);
     MTKC_POST_LAUNCH("colred_final_kernel");
   } else {

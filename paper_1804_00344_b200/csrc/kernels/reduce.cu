@@ -138,7 +138,7 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
   colred_partial_kernel<1><<<dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
                              S(stream)>>>(workspace, in, nullptr, rows, cols);
   MTKC_POST_LAUNCH("colred_partial_kernel");
-  colred_final_kernel<1><<<(unsigned)cdiv(cols, 128), 128, 0, S(stream)>>>(
+  colred_final_kernel<1><<<colred_final_grid(cols), 256, 0, S(stream)>>>(
       out, nullptr, workspace, nblk, cols, accumulate);
   MTKC_POST_LAUNCH("colred_final_kernel");
   return MTKC_OK;

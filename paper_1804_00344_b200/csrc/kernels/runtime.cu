@@ -36,10 +36,10 @@ static std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
 namespace {
 struct ProfRec {
   cudaEvent_t a, b;
-  const char* cls;
+  std::string cls;
   double work;
 };
-bool g_prof = false;
+int g_prof = 0;
 std::vector<ProfRec> g_recs;
 std::vector<cudaEvent_t> g_evpool;
 
@@ -55,7 +55,8 @@ cudaEvent_t take_event() {
 }
 }  // namespace
 
-bool prof_on() { return g_prof; }
+bool prof_on() { return g_prof != 0; }
+bool prof_detail() { return g_prof == 2; }
 
 void prof_begin(cudaStream_t st, void** token) {
   cudaEvent_t e = take_event();
@@ -63,7 +64,7 @@ void prof_begin(cudaStream_t st, void** token) {
   *token = (void*)e;
 }
 
-void prof_end(cudaStream_t st, void* token, const char* cls, double work) {
+void prof_end(cudaStream_t st, void* token, const std::string& cls, double work) {
   cudaEvent_t e = take_event();
   cudaEventRecord(e, st);
   g_recs.push_back(ProfRec{(cudaEvent_t)token, e, cls, work});
@@ -101,7 +102,7 @@ int mtkc_gpu_sleep(int64_t us, void* stream) {
 }
 
 int mtkc_prof_enable(int on) {
-  g_prof = on != 0;
+  g_prof = on;
   return MTKC_OK;
 }
 
