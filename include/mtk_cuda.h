@@ -285,6 +285,20 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
                             int64_t b, int64_t tq, int64_t tk, int heads, int64_t dk,
                             float scale, int accumulate_q, int accumulate_k, int accumulate_v,
                             void* stream);
+/* Same node on the tensor cores (mma.sync m16n8k8 tf32, fp32 accumulate):  */
+/* the TF32-precision path for head dim 64 and tq, tk <= 64 (every BASELINE */
+/* config); rows 16-byte aligned.  Arguments as above (no dsbuf).           */
+int mtkc_attention_tc_supported(int64_t tq, int64_t tk, int64_t dk);
+int mtkc_attention_tc(float* out, int64_t ldo, float* probs, const float* q, int64_t ldq,
+                      const float* k, const float* v, int64_t ldk, const float* key_mask,
+                      int64_t b, int64_t tq, int64_t tk, int heads, int64_t dk, float scale,
+                      int causal, int* flags, void* stream);
+int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* probs,
+                               const float* q, int64_t ldq, const float* k, const float* v,
+                               int64_t ldk, float* gq, float* gk, float* gv, int64_t b,
+                               int64_t tq, int64_t tk, int heads, int64_t dk, float scale,
+                               int accumulate_q, int accumulate_k, int accumulate_v,
+                               void* stream);
 
 /* ======================================================================== */
 /* fused GRU block, pointwise part (gruCell graph.cpp:648-813, gruPre        */

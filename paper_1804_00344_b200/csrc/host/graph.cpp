@@ -1157,19 +1157,31 @@ NodeRef ExpressionGraph::attention(NodeRef q, NodeRef k, NodeRef v, const Tensor
   }
   n.aux = aux;
   float scale = (float)(1.0 / std::sqrt((double)dk));  // layers.cpp:106
+  const bool tensorCore = Device::get().precision() == Precision::TF32 &&
+                          mtkc_attention_tc_supported(tq, tk, dk) &&
+                          std::getenv("MTK_ATTN_SIMT") == nullptr;
   n.fwd = [=](ExpressionGraph& g, Node& n) {
     aux->probs = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));
-    MTKC(mtkc_attention(n.value.dev(), d, aux->probs.dev(), g.valPtr(n.inputs[0]), d,
-                        g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d,
-                        aux->hasMask ? aux->mask.devc() : nullptr, b, tq, tk, heads, dk, scale,
-                        causal ? 1 : 0, Device::get().flags(), stream()));
+    // TF32 mode: tensor-core kernels (mma.sync tf32); FP32 mode: the
+    // CUDA-core kernels with the reference's summation order
+    auto fn = tensorCore ? mtkc_attention_tc : mtkc_attention;
+    MTKC(fn(n.value.dev(), d, aux->probs.dev(), g.valPtr(n.inputs[0]), d, g.valPtr(n.inputs[1]),
+            g.valPtr(n.inputs[2]), d, aux->hasMask ? aux->mask.devc() : nullptr, b, tq, tk, heads,
+            dk, scale, causal ? 1 : 0, Device::get().flags(), stream()));
   };
   n.bwd = [=](ExpressionGraph& g, Node& n) {
     const float* go = g.gradSrc(n);
-    Tensor ds = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));
     auto dq = g.gradDst(n.inputs[0]);
     auto dkk = g.gradDst(n.inputs[1]);
     auto dv = g.gradDst(n.inputs[2]);
+    if(tensorCore) {
+      MTKC(mtkc_attention_tc_backward(go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d,
+                                      g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d, dq.ptr,
+                                      dkk.ptr, dv.ptr, b, tq, tk, heads, dk, scale, dq.accumulate,
+                                      dkk.accumulate, dv.accumulate, stream()));
+      return;
+    }
+    Tensor ds = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));
     MTKC(mtkc_attention_backward(go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d,
                                  g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d, dq.ptr, dkk.ptr,
                                  dv.ptr, ds.dev(), b, tq, tk, heads, dk, scale, dq.accumulate,

@@ -257,7 +257,11 @@ std::pair<std::shared_ptr<DeviceBuffer>, int64_t> Arena::alloc(int64_t elements)
   while(cur_ < slabs_.size() && slabs_[cur_].used + n > slabs_[cur_].buf->elems)
     ++cur_;
   if(cur_ == slabs_.size()) {
-    size_t slabElems = std::max(n, ((size_t)256 << 20) / sizeof(float));
+    // geometric growth (each new slab as large as everything reserved so
+    // far, 256 MiB .. 4 GiB): a few cudaMallocs instead of one per 256 MiB
+    size_t grow = std::min<size_t>(std::max<size_t>(reservedBytes(), (size_t)256 << 20),
+                                   (size_t)4 << 30);
+    size_t slabElems = std::max(n, grow / sizeof(float));
     slabs_.push_back(Slab{std::make_shared<DeviceBuffer>(slabElems), 0});
   }
   Slab& s = slabs_[cur_];

@@ -4,8 +4,12 @@
 // mtkc_malloc'd slab.
 #include "common.cuh"
 
+#include <execinfo.h>
+
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -31,6 +35,39 @@ int cuda_status(cudaError_t e, const char* where) {
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
 static std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+
+// MTK_TRACE_BLOCK=<us>: report (with a host backtrace) every runtime call that
+// blocked the host longer than <us> microseconds -- finds hidden syncs.
+namespace {
+double trace_block_us() {
+  static double us = [] {
+    const char* e = std::getenv("MTK_TRACE_BLOCK");
+    return e ? std::atof(e) : -1.0;
+  }();
+  return us;
+}
+struct BlockTimer {
+  const char* what;
+  std::chrono::steady_clock::time_point t0;
+  explicit BlockTimer(const char* w) : what(w) {
+    if(trace_block_us() >= 0)
+      t0 = std::chrono::steady_clock::now();
+  }
+  ~BlockTimer() {
+    double lim = trace_block_us();
+    if(lim < 0)
+      return;
+    double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+                    .count();
+    if(us < lim)
+      return;
+    std::fprintf(stderr, "[mtk block] %s %.0f us\n", what, us);
+    void* bt[12];
+    int n = backtrace(bt, 12);
+    backtrace_symbols_fd(bt + 1, n - 1, 2);
+  }
+};
+}  // namespace
 
 // ------------------------------------------------------------ profiling
 namespace {
@@ -160,10 +197,14 @@ int mtkc_sm_count(int* count) {
 }
 
 int mtkc_malloc(void** ptr, size_t bytes) {
+  BlockTimer bt("cudaMalloc");
   return cuda_status(cudaMalloc(ptr, bytes), "cudaMalloc");
 }
 
-int mtkc_free(void* ptr) { return cuda_status(cudaFree(ptr), "cudaFree"); }
+int mtkc_free(void* ptr) {
+  BlockTimer bt("cudaFree");
+  return cuda_status(cudaFree(ptr), "cudaFree");
+}
 
 int mtkc_host_alloc_pinned(void** ptr, size_t bytes) {
   return cuda_status(cudaMallocHost(ptr, bytes), "cudaMallocHost");
@@ -175,6 +216,7 @@ int mtkc_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
   if(!bytes)
     return MTKC_OK;
   g_h2d.fetch_add(bytes, std::memory_order_relaxed);
+  BlockTimer bt("memcpy_h2d");
   return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S(stream)),
                      "cudaMemcpyAsync(H2D)");
 }
@@ -183,6 +225,7 @@ int mtkc_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
   if(!bytes)
     return MTKC_OK;
   g_d2h.fetch_add(bytes, std::memory_order_relaxed);
+  BlockTimer bt("memcpy_d2h");
   return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(stream)),
                      "cudaMemcpyAsync(D2H)");
 }
@@ -212,6 +255,7 @@ int mtkc_stream_destroy(void* stream) {
 }
 
 int mtkc_stream_sync(void* stream) {
+  BlockTimer bt("stream_sync");
   return cuda_status(cudaStreamSynchronize(S(stream)), "cudaStreamSynchronize");
 }
 
@@ -235,6 +279,7 @@ int mtkc_stream_wait_event(void* stream, void* ev) {
 }
 
 int mtkc_event_sync(void* ev) {
+  BlockTimer bt("event_sync");
   return cuda_status(cudaEventSynchronize((cudaEvent_t)ev), "cudaEventSynchronize");
 }
 

@@ -261,3 +261,42 @@ def test_gru_cell(ln, e):
         sz = W[n].size
         _close(g.param_grad(n).ravel(), gw[off:off + sz], 5e-5)
         off += sz
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("shape", [(2, 5, 5, 128, 2), (3, 33, 33, 256, 4), (4, 29, 17, 512, 8),
+                                   (2, 64, 64, 128, 2), (5, 1, 7, 64, 1), (3, 16, 47, 192, 3)])
+def test_attention_tensor_core_tf32(causal, shape):
+    """TF32 mode runs the mma.sync tensor-core attention (attention_tc.cu);
+    tolerance 5e-3 of the output scale (tf32 operands: 10-bit mantissa)."""
+    b, tq, tk, d, h = shape
+    if causal and tq > tk:
+        pytest.skip("causal rule needs tk >= tq for a non-empty first row")
+    M.set_precision("tf32")
+    rng = np.random.default_rng(11)
+    q = rng.normal(size=(b, tq, d)).astype(np.float32)
+    k = rng.normal(size=(b, tk, d)).astype(np.float32)
+    v = rng.normal(size=(b, tk, d)).astype(np.float32)
+    km = np.ones((b, tk), np.float32)
+    km[-1, max(1, tk // 2):] = 0
+    if causal:
+        km[:] = 1
+    G = rng.normal(size=(b, tq, d)).astype(np.float32)
+    out, gq, gk, gv = R.op_mha(q, k, v, km, causal, h, G)
+    for accumulate in (False, True):
+        g = M.ExpressionGraph(1)
+        nq, nk, nv = _param(g, "q", q), _param(g, "k", k), _param(g, "v", v)
+        o = g.attention(nq, nk, nv, km, causal, h)
+        loss = _seeded(g, o, G)
+        if accumulate:  # second consumer of q/k/v: gradients accumulate (+=)
+            loss = g.add(loss, g.reduce(M.ReduceOp.Sum, g.reshape(g.add(g.add(nq, nk), nv)
+                                                                   if tq == tk else nq,
+                                                                   [1, b * tq * d]), 1))
+        g.forward()
+        g.zero_grads()
+        g.backward(loss)
+        _close(o.val(), out, 5e-3)
+        extra = 1.0 if accumulate else 0.0
+        _close(g.param_grad("q"), gq + extra, 5e-3)
+        _close(g.param_grad("k"), gk + (extra if tq == tk else 0.0), 5e-3)
+        _close(g.param_grad("v"), gv + (extra if tq == tk else 0.0), 5e-3)

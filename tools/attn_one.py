@@ -3,7 +3,7 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_1804_00344_b200 import mtk as M
-b, t, d, h = 250, 33, 512, 8
+b, t, d, h = int(os.environ.get("B", 250)), int(os.environ.get("T", 33)), 512, 8
 rng = np.random.default_rng(0)
 g = M.ExpressionGraph(1)
 q = g.param("q", [b, t, d], rng.normal(size=(b, t, d)).astype(np.float32))

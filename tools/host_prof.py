@@ -36,6 +36,20 @@ print("host ms/step total %.2f  build %.2f  forward %.2f  backward %.2f" % (
     (t1 - t0) * 1e3 / n, (h1[0] - h0[0]) / n, (h1[1] - h0[1]) / n, (h1[2] - h0[2]) / n))
 M.sync()
 
+# unthrottled host cost: launch queue empty at the start of every step
+hs = []
+for i in range(8, 14):
+    M.sync()
+    h0 = st.host_times()
+    t0 = time.perf_counter()
+    st.update([batches[i]], i, False)
+    t1 = time.perf_counter()
+    h1 = st.host_times()
+    hs.append(((t1 - t0) * 1e3, h1[0] - h0[0], h1[1] - h0[1], h1[2] - h0[2]))
+M.sync()
+for h in hs:
+    print("queue-empty step: host %.2f ms (build %.2f fwd %.2f bwd %.2f)" % h)
+
 # host cost of one GEMM call (GPU kept busy so launches do not block)
 A = torch.randn(6629, 512, device="cuda")
 B = torch.randn(512, 512, device="cuda")
