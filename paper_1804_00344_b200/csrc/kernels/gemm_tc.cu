@@ -30,7 +30,11 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per 128-byte swizzle row
-constexpr int TC_THREADS = 192;
+#ifndef MTK_EPI_WARPS
+#define MTK_EPI_WARPS 4
+#endif
+constexpr int EPI_WARPS = MTK_EPI_WARPS;  // 4 (one per TMEM lane quarter) or 8 (two)
+constexpr int TC_THREADS = 64 + 32 * EPI_WARPS;  // producer, MMA, epilogue warps
 constexpr int EPI_STRIDE = 33;  // padded 32x32 transpose tile
 
 // ---------------------------------------------------------------- PTX
@@ -158,17 +162,23 @@ template <int BN>
 struct TcSmem {
   static constexpr uint32_t A_BYTES = BM * BK * 4;
   static constexpr uint32_t B_BYTES = BN * BK * 4;
-  static constexpr int ST = BN == 256 ? 3 : 4;
-  // per epilogue warp: two 32x32 fp32 staging tiles (128B-swizzled, TMA store)
-  static constexpr size_t EPI_BYTES = 4 * 2 * 32 * 32 * sizeof(float);
+  // pipeline depth: as many stages as fit next to the epilogue staging
+  // (227 KB): 6 x 32 KB for BN=128, 4 x 48 KB for BN=256.  fp32 operands
+  // make a k-block short in FLOPs, so depth is what covers L2/HBM latency.
+  static constexpr int ST = EPI_WARPS == 8 ? (BN == 256 ? 3 : 5) : (BN == 256 ? 4 : 6);
+  // per epilogue warp (8): two 32x32 fp32 staging tiles (128B-swizzled, TMA store)
+  static constexpr size_t EPI_BYTES = EPI_WARPS * 2 * 32 * 32 * sizeof(float);
   static constexpr size_t BYTES = 1024 + ST * (size_t)(A_BYTES + B_BYTES) + EPI_BYTES + 256;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+// LOADS: the epilogue reads beta*C and/or a ReLU gate (TMA-loaded boxes);
+// a separate instantiation so the common bias/ReLU epilogue stays lean.
+template <int BN, bool A_MN, bool B_MN, bool LOADS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tf32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
                         const __grid_constant__ CUtensorMap mapB,
-                        const __grid_constant__ CUtensorMap mapC, TcP p) {
+                        const __grid_constant__ CUtensorMap mapC,
+                        const __grid_constant__ CUtensorMap mapG, TcP p) {
   using L = TcSmem<BN>;
   constexpr int ST = L::ST;
   constexpr uint32_t A_BYTES = L::A_BYTES, B_BYTES = L::B_BYTES;
@@ -183,7 +193,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;   // [2] MMA -> epilogue
   uint64_t* tempty = tfull + 2;   // [2] epilogue -> MMA
-  uint32_t* tmemSlot = (uint32_t*)(tempty + 2);
+  uint64_t* ldbar = tempty + 2;   // [8] TMA loads of C / gate boxes, per epilogue warp
+  uint32_t* tmemSlot = (uint32_t*)(ldbar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -192,13 +203,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     prefetch_tmap(&mapB);
     if(p.tmaStore)
       prefetch_tmap(&mapC);
+    if(p.gate && p.tmaStore)
+      prefetch_tmap(&mapG);
+    for(int w = 0; w < 8; ++w)
+      mbar_init(&ldbar[w], 1);
     for(int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for(int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty[a], EPI_WARPS);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -299,12 +314,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quarter q = warp % 4
-    const int q = warp & 3;
+    // epilogue warps 2..9: TMEM lane quarter q = warp % 4 (the quarter a
+    // warp may access), column half h = (warp - 2) / 4 of the tile
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int cBeg = h * (BN * 4 / EPI_WARPS), cEnd = cBeg + BN * 4 / EPI_WARPS;
     // two swizzled 32x32 staging tiles per warp (TMA-store mode); the
     // fallback path reuses the first one as a padded transpose buffer
-    float* stage0 = sEpi + q * 2 * 1024;
+    float* stage0 = sEpi + ew * 2 * 1024;
     int chunk = 0;  // chunks handed to the TMA engine by this warp
+    uint32_t ldPhase = 0;  // TMA C / gate box loads completed by this warp
     int lt = 0;
     for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x, ++lt) {
       int m0, n0, kb0, nkb, split;
@@ -314,10 +332,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
       const int64_t rowBase = m0 + q * 32;
 #pragma unroll 1
-      for(int c0 = 0; c0 < BN; c0 += 32) {
+      for(int c0 = cBeg; c0 < cEnd; c0 += 32) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
-        if(c0 + 32 >= BN) {  // accumulator fully read: hand it back to the MMA warp
+        if(c0 + 32 >= cEnd) {  // our share read: hand it back to the MMA warp
           tc_fence_before();
           if(lane == 0)
             mbar_arrive(&tempty[acc]);
@@ -325,11 +343,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if(n0 + c0 >= p.N || rowBase >= p.M || (p.dbg & 1))
           continue;
         const int64_t col0 = n0 + c0;
-        const int64_t row = rowBase + lane;  // this lane's output row
         if(p.tmaStore) {
+          float* stage = stage0 + (chunk & 1) * 1024;
+          // the TMA engine must have finished reading this buffer (chunk - 2)
+          // before it is refilled: early when a C / gate box lands in it,
+          // otherwise as late as possible (after the arithmetic)
+          constexpr bool loads = LOADS;  // host: LOADS iff !part && (beta != 0 || gate)
+          if(chunk >= 2 && loads) {
+            if(lane == 0)
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+          }
+          // 16-byte chunk j of row `lane` sits at j ^ (lane % 8) (SWIZZLE_128B),
+          // both for the TMA-loaded C / gate boxes and for the store staging
+          float* srow = stage + lane * 32;
+          const int sw = lane & 7;
           if(!p.part) {
-            const bool rowOk = row < p.M;
-            // bias: one coalesced load per lane, broadcast by shuffles
+            const bool needC = LOADS && p.beta != 0.f, needG = LOADS && p.gate != nullptr;
+            float* grow = stage;  // gate box buffer
+            if(needC || needG) {
+              // C and/or the ReLU gate arrive as swizzled 32x32 boxes by TMA
+              // (coalesced, async) instead of per-lane strided row reads
+              if(needC && needG) {
+                grow = stage0 + ((chunk + 1) & 1) * 1024;
+                if(lane == 0)
+                  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+              }
+              if(lane == 0) {
+                mbar_expect_tx(&ldbar[ew], (needC ? 4096u : 0u) + (needG ? 4096u : 0u));
+                if(needC)
+                  tma_load_2d(stage, &mapC, &ldbar[ew], (int)col0, (int)rowBase);
+                if(needG)
+                  tma_load_2d(grow, &mapG, &ldbar[ew], (int)col0, (int)rowBase);
+              }
+              mbar_wait(&ldbar[ew], ldPhase & 1);
+              ++ldPhase;
+            }
+            grow += lane * 32;
+            // alpha, bias (one coalesced load per lane, broadcast by shuffles), ReLU
             const float bl = (p.bias && col0 + lane < p.N) ? p.bias[col0 + lane] : 0.f;
 #pragma unroll
             for(int i = 0; i < 32; ++i) {
@@ -340,59 +392,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 x = x > 0.f ? x : 0.f;
               v[i] = x;
             }
-            if((p.gate || p.beta != 0.f) && rowOk) {
-              // this lane's 32 columns of its own row: 16-byte loads when aligned
-              const float* grow = p.gate ? p.gate + row * p.ldc + col0 : nullptr;
-              const float* crow = p.C + row * p.ldc + col0;
-              const bool vec = col0 + 32 <= p.N && (p.ldc % 4 == 0) &&
-                               (((uintptr_t)p.C | (uintptr_t)(p.gate ? p.gate : p.C)) % 16 == 0);
-              if(vec) {
+            // ReLU gate, then beta*C, from the TMA-loaded boxes (straight-line
+            // loops under uniform branches)
+            if(needG) {
 #pragma unroll
-                for(int j = 0; j < 8; ++j) {
-                  float gv[4] = {1.f, 1.f, 1.f, 1.f}, cv[4] = {0.f, 0.f, 0.f, 0.f};
-                  if(grow) {
-                    float4 g4 = *reinterpret_cast<const float4*>(grow + 4 * j);
-                    gv[0] = g4.x; gv[1] = g4.y; gv[2] = g4.z; gv[3] = g4.w;
-                  }
-                  if(p.beta != 0.f) {
-                    float4 c4 = *reinterpret_cast<const float4*>(crow + 4 * j);
-                    cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
-                  }
+              for(int j = 0; j < 8; ++j) {
+                const float4 g4 = *reinterpret_cast<const float4*>(grow + ((j ^ sw) * 4));
+                v[4 * j] = g4.x > 0.f ? v[4 * j] : 0.f;
+                v[4 * j + 1] = g4.y > 0.f ? v[4 * j + 1] : 0.f;
+                v[4 * j + 2] = g4.z > 0.f ? v[4 * j + 2] : 0.f;
+                v[4 * j + 3] = g4.w > 0.f ? v[4 * j + 3] : 0.f;
+              }
+            }
+            if(needC) {
+              const float beta = p.beta;
 #pragma unroll
-                  for(int u = 0; u < 4; ++u) {
-                    float x = v[4 * j + u];
-                    if(grow)
-                      x = gv[u] > 0.f ? x : 0.f;
-                    if(p.beta != 0.f)
-                      x = (p.beta == 1.f ? cv[u] : p.beta * cv[u]) + x;
-                    v[4 * j + u] = x;
-                  }
-                }
-              } else {
-#pragma unroll
-                for(int i = 0; i < 32; ++i) {
-                  if(col0 + i >= p.N)
-                    break;
-                  float x = v[i];
-                  if(grow)
-                    x = grow[i] > 0.f ? x : 0.f;
-                  if(p.beta != 0.f)
-                    x = (p.beta == 1.f ? crow[i] : p.beta * crow[i]) + x;
-                  v[i] = x;
+              for(int j = 0; j < 8; ++j) {
+                const float4 c4 = *reinterpret_cast<const float4*>(srow + ((j ^ sw) * 4));
+                if(beta == 1.f) {
+                  v[4 * j] = c4.x + v[4 * j];
+                  v[4 * j + 1] = c4.y + v[4 * j + 1];
+                  v[4 * j + 2] = c4.z + v[4 * j + 2];
+                  v[4 * j + 3] = c4.w + v[4 * j + 3];
+                } else {
+                  v[4 * j] = beta * c4.x + v[4 * j];
+                  v[4 * j + 1] = beta * c4.y + v[4 * j + 1];
+                  v[4 * j + 2] = beta * c4.z + v[4 * j + 2];
+                  v[4 * j + 3] = beta * c4.w + v[4 * j + 3];
                 }
               }
             }
+            __syncwarp();  // every lane has read its C / gate row before the overwrite
           }
-          float* stage = stage0 + (chunk & 1) * 1024;
-          if(chunk >= 2) {  // the TMA engine must have finished reading this buffer
+          if(chunk >= 2 && !loads) {
             if(lane == 0)
               asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             __syncwarp();
           }
-          // row `lane` = 128 B; 16-byte chunk j lands at j ^ (lane % 8) (SWIZZLE_128B)
 #pragma unroll
           for(int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(stage + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+            *reinterpret_cast<float4*>(srow + ((j ^ sw) * 4)) =
                 make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -460,28 +499,53 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-// C = alpha*sum_s part[s] (+bias, relu, gate) + beta*C  (fixed split order)
+// C = alpha*sum_s part[s] (+bias, relu, gate) + beta*C  (fixed split order).
+// Grid-stride over (row, 4-column group); float4 when N and ldc allow.
+template <bool VEC>
 __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t M, int64_t N,
                                      float* C, int64_t ldc, float alpha, float beta,
                                      const float* bias, int epi, const float* gate) {
-  int64_t total = M * N;
+  const int64_t groups = (N + 3) / 4, total = M * groups, plane = M * N;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / N, c = i % N;
-    float acc = 0.f;
-    for(int s = 0; s < splits; ++s)
-      acc += part[(int64_t)s * total + i];
-    float x = alpha == 1.f ? acc : alpha * acc;
-    if(bias)
-      x = x + bias[c];
-    if(epi == MTKC_EPI_RELU)
-      x = x > 0.f ? x : 0.f;
+    const int64_t r = i / groups, c = (i - r * groups) * 4;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if(VEC) {
+      for(int s = 0; s < splits; ++s) {
+        float4 x = *reinterpret_cast<const float4*>(part + s * plane + r * N + c);
+        acc[0] += x.x;
+        acc[1] += x.y;
+        acc[2] += x.z;
+        acc[3] += x.w;
+      }
+    } else {
+      for(int s = 0; s < splits; ++s)
+        for(int u = 0; u < 4; ++u)
+          if(c + u < N)
+            acc[u] += part[s * plane + r * N + c + u];
+    }
+    float out[4];
     float* dst = C + r * ldc + c;
-    if(gate)
-      x = gate[r * ldc + c] > 0.f ? x : 0.f;
-    if(beta != 0.f)
-      x = (beta == 1.f ? *dst : beta * *dst) + x;
-    *dst = x;
+    for(int u = 0; u < 4; ++u) {
+      if(!VEC && c + u >= N)
+        break;
+      float x = alpha == 1.f ? acc[u] : alpha * acc[u];
+      if(bias)
+        x = x + bias[c + u];
+      if(epi == MTKC_EPI_RELU)
+        x = x > 0.f ? x : 0.f;
+      if(gate)
+        x = gate[r * ldc + c + u] > 0.f ? x : 0.f;
+      if(beta != 0.f)
+        x = (beta == 1.f ? dst[u] : beta * dst[u]) + x;
+      out[u] = x;
+    }
+    if(VEC) {
+      *reinterpret_cast<float4*>(dst) = make_float4(out[0], out[1], out[2], out[3]);
+    } else {
+      for(int u = 0; u < 4 && c + u < N; ++u)
+        dst[u] = out[u];
+    }
   }
 }
 
@@ -552,11 +616,11 @@ bool make_store_map(CUtensorMap* m, float* base, int64_t cols, int64_t rows, int
 
 int g_sms = 0;
 
-template <int BN, bool A_MN, bool B_MN>
-int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const TcP& p,
-              cudaStream_t st) {
+template <int BN, bool A_MN, bool B_MN, bool LOADS>
+int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+              const CUtensorMap& mg, const TcP& p, cudaStream_t st) {
   constexpr size_t smem = TcSmem<BN>::BYTES;
-  auto kern = gemm_tf32_tc_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_tf32_tc_kernel<BN, A_MN, B_MN, LOADS>;
   static bool attr = false;
   if(!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -566,21 +630,22 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& m
     attr = true;
   }
   int grid = std::min(p.numTiles, g_sms);
-  kern<<<grid, TC_THREADS, smem, st>>>(ma, mb, mc, p);
+  kern<<<grid, TC_THREADS, smem, st>>>(ma, mb, mc, mg, p);
   MTKC_POST_LAUNCH("gemm_tf32_tc_kernel");
   return MTKC_OK;
 }
 
-template <int BN>
+template <int BN, bool LOADS>
 int dispatch_majors(bool aMN, bool bMN, const CUtensorMap& ma, const CUtensorMap& mb,
-                    const CUtensorMap& mc, const TcP& p, cudaStream_t st) {
+                    const CUtensorMap& mc, const CUtensorMap& mg, const TcP& p,
+                    cudaStream_t st) {
   if(!aMN && !bMN)
-    return launch_tc<BN, false, false>(ma, mb, mc, p, st);
+    return launch_tc<BN, false, false, LOADS>(ma, mb, mc, mg, p, st);
   if(!aMN && bMN)
-    return launch_tc<BN, false, true>(ma, mb, mc, p, st);
+    return launch_tc<BN, false, true, LOADS>(ma, mb, mc, mg, p, st);
   if(aMN && !bMN)
-    return launch_tc<BN, true, false>(ma, mb, mc, p, st);
-  return launch_tc<BN, true, true>(ma, mb, mc, p, st);
+    return launch_tc<BN, true, false, LOADS>(ma, mb, mc, mg, p, st);
+  return launch_tc<BN, true, true, LOADS>(ma, mb, mc, mg, p, st);
 }
 
 }  // namespace
@@ -676,13 +741,32 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
   else
     p.tmaStore = (a.ldc % 4 == 0) && ((uintptr_t)a.C % 16 == 0) &&
                  make_store_map(&mc, a.C, a.N, a.M, a.ldc, 1);
+  // the ReLU gate is read as TMA boxes too (same geometry as C)
+  CUtensorMap mg;
+  std::memset(&mg, 0, sizeof(mg));
+  if(p.tmaStore && !p.part && a.gate)
+    p.tmaStore = ((uintptr_t)a.gate % 16 == 0) &&
+                 make_store_map(&mg, const_cast<float*>(a.gate), a.N, a.M, a.ldc, 1);
   if(getenv("MTK_GEMM_NO_TMA_STORE"))
     p.tmaStore = 0;
-  *rc = BN == 256 ? dispatch_majors<256>(aMN, bMN, ma, mb, mc, p, st)
-                  : dispatch_majors<128>(aMN, bMN, ma, mb, mc, p, st);
+  const bool loads = p.tmaStore && !p.part && (a.beta != 0.f || a.gate != nullptr);
+  if(loads)
+    *rc = BN == 256 ? dispatch_majors<256, true>(aMN, bMN, ma, mb, mc, mg, p, st)
+                    : dispatch_majors<128, true>(aMN, bMN, ma, mb, mc, mg, p, st);
+  else
+    *rc = BN == 256 ? dispatch_majors<256, false>(aMN, bMN, ma, mb, mc, mg, p, st)
+                    : dispatch_majors<128, false>(aMN, bMN, ma, mb, mc, mg, p, st);
   if(*rc == MTKC_OK && splits > 1) {
-    splitk_reduce_kernel<<<grid1d(a.M * a.N, 256), 256, 0, st>>>(
-        a.workspace, splits, a.M, a.N, a.C, a.ldc, a.alpha, a.beta, a.bias, a.epilogue, a.gate);
+    const bool vec = a.N % 4 == 0 && a.ldc % 4 == 0 && (uintptr_t)a.C % 16 == 0 &&
+                     (uintptr_t)a.workspace % 16 == 0;
+    const unsigned grid = grid1d(a.M * cdiv(a.N, 4), 256);
+    if(vec)
+      splitk_reduce_kernel<true><<<grid, 256, 0, st>>>(a.workspace, splits, a.M, a.N, a.C, a.ldc,
+                                                        a.alpha, a.beta, a.bias, a.epilogue, a.gate);
+    else
+      splitk_reduce_kernel<false><<<grid, 256, 0, st>>>(a.workspace, splits, a.M, a.N, a.C,
+                                                         a.ldc, a.alpha, a.beta, a.bias,
+                                                         a.epilogue, a.gate);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if(e != cudaSuccess)

@@ -20,17 +20,20 @@ def _dev(torch, a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
 
 
-def _run(torch, a, b, ta, tb, alpha=1.0, beta=0.0, c0=None, precision=0, bias=None, relu=False):
+def _run(torch, a, b, ta, tb, alpha=1.0, beta=0.0, c0=None, precision=0, bias=None, relu=False,
+         gate=None):
     M = a.shape[1] if ta else a.shape[0]
     K = a.shape[0] if ta else a.shape[1]
     N = b.shape[0] if tb else b.shape[1]
     A, B = _dev(torch, a), _dev(torch, b)
     Cd = _dev(torch, c0 if c0 is not None else np.zeros((M, N), np.float32))
     bd = _dev(torch, bias) if bias is not None else None
+    gd = _dev(torch, gate) if gate is not None else None
     ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
     path = cabi.gemm(M, N, K, A.data_ptr(), a.shape[1], B.data_ptr(), b.shape[1], Cd.data_ptr(), N,
                      trans_a=ta, trans_b=tb, alpha=alpha, beta=beta,
                      bias=bd.data_ptr() if bd is not None else None, relu=relu,
+                     gate=gd.data_ptr() if gd is not None else None,
                      precision=precision, workspace=ws.data_ptr(), workspace_bytes=ws.numel())
     torch.cuda.synchronize()
     return Cd.cpu().numpy(), path
@@ -87,3 +90,31 @@ def test_tf32_epilogues(cuda):
     got, _ = _run(torch, a, b, 0, 0, alpha=0.5, beta=1.0, c0=c0, precision=1)
     want = 0.5 * exact + c0
     assert np.all(np.abs(got - want) <= 4e-3 * bound)
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 384), (200, 96, 300), (70, 8192, 96), (333, 64, 2050)])
+def test_tf32_epilogue_combinations(cuda, shape):
+    """bias (vector and ragged), ReLU gate (TMA-loaded box), beta*C (TMA-loaded
+    box), gate+beta together, and the split-K reduction (long K)."""
+    import torch
+    rng = np.random.default_rng(4)
+    M, K, N = shape
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    c0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    gate = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    exact = a.astype(np.float64) @ b.astype(np.float64)
+    tol = 4e-3 * (np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64) + 1)
+    cases = [
+        (dict(bias=bias), exact + bias),
+        (dict(bias=bias, relu=True), np.maximum(exact + bias, 0)),
+        (dict(gate=gate), np.where(gate > 0, exact, 0)),
+        (dict(beta=1.0, c0=c0), exact + c0),
+        (dict(beta=2.0, c0=c0, gate=gate, alpha=0.5), 2.0 * c0 + np.where(gate > 0, 0.5 * exact, 0)),
+    ]
+    for kw, want in cases:
+        got, path = _run(torch, a, b, 0, 0, precision=1, **kw)
+        assert path == 1 or N % 4, "tensor-core path not taken"  # TMA needs 16-B row pitch
+        err = np.abs(got - want)
+        assert np.all(err <= tol), (kw.keys(), float(np.max(err - tol)))

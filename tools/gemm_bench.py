@@ -3,10 +3,11 @@ usage: python tools/gemm_bench.py [reps]"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("MTK_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 from paper_1804_00344_b200 import cabi
+print("# lib", cabi.LIB_PATH)
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 R = 6629
