@@ -258,6 +258,21 @@ int mtkc_layernorm_backward(const float* dy, const float* gain, const float* inv
                             int64_t rows, int64_t d, int accumulate_dx, int accumulate_params,
                             float* workspace, size_t workspace_bytes, void* stream);
 
+/* Vectorised variant (d % 4 == 0, d <= 2048, 16-byte aligned rows): the    */
+/* forward caches only mean/inv_std per row (no xhat tensor); the backward  */
+/* recomputes xhat from x and fuses the dgain/dbias column reductions into  */
+/* the dx pass (deterministic; workspace >= ..._workspace_bytes).           */
+int mtkc_layernorm_fast_supported(int64_t d);
+int mtkc_layernorm_stats(float* out, const float* x, const float* gain, const float* bias,
+                         float eps, float* mean, float* inv_std, int64_t rows, int64_t d,
+                         void* stream);
+size_t mtkc_layernorm_stats_workspace_bytes(int64_t rows, int64_t d);
+int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* gain,
+                                  const float* mean, const float* inv_std, float* dx,
+                                  float* dgain, float* dbias, int64_t rows, int64_t d,
+                                  int accumulate_dx, int accumulate_params, float* workspace,
+                                  size_t workspace_bytes, void* stream);
+
 /* ======================================================================== */
 /* embedding (embed graph.cpp:595-622) fused with positional encoding       */
 /* (addPositionalEncoding layers.cpp:175-179): out = E[id]*s + pe[pos]       */

@@ -966,7 +966,8 @@ NodeRef ExpressionGraph::softmax(NodeRef a, Tensor mask) {
 
 namespace {
 struct LnCache {
-  Tensor invStd, xhat;
+  Tensor invStd, xhat, mean;
+  bool fast = false;  // mean/invStd cache, xhat recomputed (mtkc_layernorm_stats)
 };
 }  // namespace
 
@@ -987,11 +988,21 @@ NodeRef ExpressionGraph::layerNorm(NodeRef x, NodeRef gain, NodeRef bias, Real e
   n.aux = cache;
   int64_t rows = x.shape.size() / d;
   n.fwd = [cache, eps, d, rows](ExpressionGraph& g, Node& n) {
+    const float* xin = g.valPtr(n.inputs[0]);
+    const float* gp = g.valPtr(n.inputs[1]);
+    const float* bp = g.valPtr(n.inputs[2]);
     cache->invStd = g.allocTensor(Shape({rows}));
+    cache->fast = mtkc_layernorm_fast_supported(d) &&
+                  (((uintptr_t)xin | (uintptr_t)gp | (uintptr_t)bp) % 16) == 0;
+    if(cache->fast) {
+      cache->mean = g.allocTensor(Shape({rows}));
+      MTKC(mtkc_layernorm_stats(n.value.dev(), xin, gp, bp, eps, cache->mean.dev(),
+                                cache->invStd.dev(), rows, d, stream()));
+      return;
+    }
     cache->xhat = g.allocTensor(n.shape);
-    MTKC(mtkc_layernorm(n.value.dev(), g.valPtr(n.inputs[0]), g.valPtr(n.inputs[1]),
-                        g.valPtr(n.inputs[2]), eps, cache->invStd.dev(), cache->xhat.dev(), rows,
-                        d, stream()));
+    MTKC(mtkc_layernorm(n.value.dev(), xin, gp, bp, eps, cache->invStd.dev(), cache->xhat.dev(),
+                        rows, d, stream()));
   };
   n.bwd = [cache, d, rows](ExpressionGraph& g, Node& n) {
     const float* go = g.gradSrc(n);
@@ -1003,6 +1014,17 @@ NodeRef ExpressionGraph::layerNorm(NodeRef x, NodeRef gain, NodeRef bias, Real e
       dg.accumulate = db.accumulate = 1;
     }
     Device& dev = Device::get();
+    if(cache->fast && (((uintptr_t)go | (uintptr_t)dx.ptr) % 16) == 0) {
+      float* w = dev.scratch(mtkc_layernorm_stats_workspace_bytes(rows, d));
+      MTKC(mtkc_layernorm_stats_backward(go, g.valPtr(n.inputs[0]), g.valPtr(n.inputs[1]),
+                                         cache->mean.devc(), cache->invStd.devc(), dx.ptr, dg.ptr,
+                                         db.ptr, rows, d, dx.accumulate, dg.accumulate, w,
+                                         dev.scratchBytes(), dev.stream()));
+      return;
+    }
+    if(cache->fast) {  // misaligned gradient buffers: materialise xhat for the generic kernel
+      throw ContractError("layer norm backward: gradient rows not 16-byte aligned");
+    }
     size_t ws = (size_t)((rows + 63) / 64) * 2 * (size_t)d * sizeof(float);
     float* w = dev.scratch(ws);
     MTKC(mtkc_layernorm_backward(go, g.valPtr(n.inputs[1]), cache->invStd.devc(),

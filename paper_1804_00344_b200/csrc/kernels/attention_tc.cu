@@ -267,7 +267,7 @@ __device__ __forceinline__ void store2(float* d, float a, float b, int acc) {
 
 template <int TT>
 __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
-  constexpr int NW = TT / 16, NT = TT / 8, LP = PStride<TT>::v;
+  constexpr int NT = TT / 8, LP = PStride<TT>::v;
   extern __shared__ float4 smem4[];
   float* Q = reinterpret_cast<float*>(smem4);  // [TT][L8]
   float* K = Q + TT * L8;                       // [TT][L8]

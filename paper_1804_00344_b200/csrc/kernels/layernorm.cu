@@ -8,6 +8,8 @@
 // Backward: one warp per row for dx (row in registers, one read of dy and
 // xhat); dgain/dbias are column reductions over rows in a fixed order
 // (colred.cuh) so results are bitwise reproducible run to run.
+#include <algorithm>
+
 #include "colred.cuh"
 #include "common.cuh"
 
@@ -151,6 +153,148 @@ __global__ void ln_param_direct_kernel(const float* dy, const float* xhat, float
   dbias[j] = (acc ? dbias[j] : 0.f) + sb;
 }
 
+// ---------------------------------------------------------------------------
+// Vectorised path (d % 4 == 0, d <= 128*NV): no xhat tensor.  The forward
+// caches only (mean, invStd) per row; the backward recomputes
+// xhat = (x - mean) * invStd from the layer input (same float expression as
+// the forward, so the same bits) and fuses the gain/bias column reductions
+// into the dx pass: each CTA owns a block of rows, accumulates
+// sum(dy*xhat) / sum(dy) per column in registers, combines its 8 warps in a
+// fixed order and writes one partial row pair; colred_final_kernel<2> sums
+// the partials in a fixed order.  HBM per element: forward 8 B (read x,
+// write y), backward 12 B (read dy, x; write dx) instead of 12 B + 20 B.
+
+template <int NV>
+__global__ void __launch_bounds__(LN_WARPS * 32)
+    ln_fwd4_kernel(float* out, const float* x, const float* g, const float* b, float eps,
+                   float* mean, float* invStd, int64_t rows, int64_t d) {
+  const int64_t row = blockIdx.x * (int64_t)LN_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if(row >= rows)
+    return;
+  const float* xr = x + row * d;
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t c = 128 * k + 4 * lane;
+    v[k] = c < d ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+  s = warp_sum(s);
+  const float mu = s / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t c = 128 * k + 4 * lane;
+    if(c < d) {
+      const float a = v[k].x - mu, bb = v[k].y - mu, cc = v[k].z - mu, dd = v[k].w - mu;
+      q += (a * a + bb * bb) + (cc * cc + dd * dd);
+    }
+  }
+  q = warp_sum(q);
+  const float rs = 1.f / sqrtf(q / (float)d + eps);
+  if(lane == 0) {
+    mean[row] = mu;
+    invStd[row] = rs;
+  }
+  float* o = out + row * d;
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t c = 128 * k + 4 * lane;
+    if(c < d) {
+      const float4 g4 = __ldg(reinterpret_cast<const float4*>(g + c));
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(b + c));
+      float4 y;
+      y.x = g4.x * ((v[k].x - mu) * rs) + b4.x;
+      y.y = g4.y * ((v[k].y - mu) * rs) + b4.y;
+      y.z = g4.z * ((v[k].z - mu) * rs) + b4.z;
+      y.w = g4.w * ((v[k].w - mu) * rs) + b4.w;
+      *reinterpret_cast<float4*>(o + c) = y;
+    }
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(LN_WARPS * 32)
+    ln_bwd4_kernel(const float* dy, const float* x, const float* g, const float* mean,
+                   const float* invStd, float* dx, float* part, int64_t rows, int64_t d,
+                   int64_t rowsPerCta, int accDx) {
+  extern __shared__ float4 red4[];  // [LN_WARPS][2][d/4] (param partials only)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4 gg[NV], sg[NV], sb[NV];
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t c = 128 * k + 4 * lane;
+    gg[k] = c < d ? __ldg(reinterpret_cast<const float4*>(g + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    sg[k] = sb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int64_t r0 = blockIdx.x * rowsPerCta, r1 = min(rows, r0 + rowsPerCta);
+  for(int64_t row = r0 + w; row < r1; row += LN_WARPS) {
+    const float mu = mean[row], rs = invStd[row];
+    float4 dy4[NV], xh[NV], h[NV];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for(int k = 0; k < NV; ++k) {
+      const int64_t c = 128 * k + 4 * lane;
+      if(c < d) {
+        dy4[k] = *reinterpret_cast<const float4*>(dy + row * d + c);
+        const float4 x4 = *reinterpret_cast<const float4*>(x + row * d + c);
+        xh[k] = make_float4((x4.x - mu) * rs, (x4.y - mu) * rs, (x4.z - mu) * rs,
+                            (x4.w - mu) * rs);
+      } else {
+        dy4[k] = xh[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      h[k] = make_float4(dy4[k].x * gg[k].x, dy4[k].y * gg[k].y, dy4[k].z * gg[k].z,
+                         dy4[k].w * gg[k].w);
+      s1 += (h[k].x + h[k].y) + (h[k].z + h[k].w);
+      s2 += (h[k].x * xh[k].x + h[k].y * xh[k].y) + (h[k].z * xh[k].z + h[k].w * xh[k].w);
+      sg[k].x += dy4[k].x * xh[k].x;
+      sg[k].y += dy4[k].y * xh[k].y;
+      sg[k].z += dy4[k].z * xh[k].z;
+      sg[k].w += dy4[k].w * xh[k].w;
+      f4add(sb[k], dy4[k]);
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    const float m1 = s1 / (float)d, m2 = s2 / (float)d;
+#pragma unroll
+    for(int k = 0; k < NV; ++k) {
+      const int64_t c = 128 * k + 4 * lane;
+      if(c < d) {
+        float4 o;
+        o.x = rs * (h[k].x - m1 - xh[k].x * m2);
+        o.y = rs * (h[k].y - m1 - xh[k].y * m2);
+        o.z = rs * (h[k].z - m1 - xh[k].z * m2);
+        o.w = rs * (h[k].w - m1 - xh[k].w * m2);
+        float4* dst = reinterpret_cast<float4*>(dx + row * d + c);
+        if(accDx)
+          f4add(o, *dst);
+        *dst = o;
+      }
+    }
+  }
+  if(!part)
+    return;
+  const int64_t d4 = d / 4;
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t c4 = 32 * k + lane;
+    if(c4 < d4) {
+      red4[(w * 2 + 0) * d4 + c4] = sg[k];
+      red4[(w * 2 + 1) * d4 + c4] = sb[k];
+    }
+  }
+  __syncthreads();
+  for(int64_t e = threadIdx.x; e < 2 * d4; e += LN_WARPS * 32) {
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for(int ww = 0; ww < LN_WARPS; ++ww)
+      f4add(t, red4[ww * 2 * d4 + e]);
+    reinterpret_cast<float4*>(part)[blockIdx.x * 2 * d4 + e] = t;  // [blk][q][d]
+  }
+}
+
 template <template <int> class K, typename... Args>
 void launch_v(int64_t d, dim3 grid, cudaStream_t st, Args... args);
 
@@ -217,6 +361,78 @@ int mtkc_layernorm_backward(const float* dy, const float* gain, const float* inv
     ln_param_direct_kernel<<<(unsigned)cdiv(d, 128), 128, 0, st>>>(dy, xhat, dgain, dbias, rows,
                                                                    d, accumulate_params);
     MTKC_POST_LAUNCH("ln_param_direct_kernel");
+  }
+  return MTKC_OK;
+}
+
+int mtkc_layernorm_fast_supported(int64_t d) { return d >= 4 && d % 4 == 0 && d <= 2048; }
+
+int mtkc_layernorm_stats(float* out, const float* x, const float* gain, const float* bias,
+                         float eps, float* mean, float* inv_std, int64_t rows, int64_t d,
+                         void* stream) {
+  if(rows <= 0)
+    return MTKC_OK;
+  if(!mtkc_layernorm_fast_supported(d) || ((uintptr_t)x | (uintptr_t)out | (uintptr_t)gain |
+                                           (uintptr_t)bias) % 16)
+    return fail(MTKC_DIMENSION, "mtkc_layernorm_stats needs d % 4 == 0, d <= 2048, aligned rows");
+  cudaStream_t st = S(stream);
+  ProfScope prof(st, "layernorm", 8.0 * rows * d);  // read x, write y
+  dim3 grid((unsigned)cdiv(rows, LN_WARPS));
+  const int nv = (int)cdiv(d, 128);
+#define LN4_FWD(NVV)                                                                   \
+  if(nv <= NVV) {                                                                      \
+    ln_fwd4_kernel<NVV><<<grid, LN_WARPS * 32, 0, st>>>(out, x, gain, bias, eps, mean, \
+                                                        inv_std, rows, d);              \
+  } else
+  LN4_FWD(1) LN4_FWD(2) LN4_FWD(4) LN4_FWD(8) LN4_FWD(16) {}
+#undef LN4_FWD
+  MTKC_POST_LAUNCH("ln_fwd4_kernel");
+  return MTKC_OK;
+}
+
+size_t mtkc_layernorm_stats_workspace_bytes(int64_t rows, int64_t d) {
+  int64_t rpc = std::max<int64_t>(LN_WARPS, cdiv(cdiv(rows, 2 * 148), LN_WARPS) * LN_WARPS);
+  return (size_t)cdiv(rows, rpc) * 2 * (size_t)d * sizeof(float);
+}
+
+int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* gain,
+                                  const float* mean, const float* inv_std, float* dx,
+                                  float* dgain, float* dbias, int64_t rows, int64_t d,
+                                  int accumulate_dx, int accumulate_params, float* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  if(rows <= 0)
+    return MTKC_OK;
+  if(!mtkc_layernorm_fast_supported(d) ||
+     ((uintptr_t)x | (uintptr_t)dy | (uintptr_t)dx | (uintptr_t)gain) % 16)
+    return fail(MTKC_DIMENSION, "mtkc_layernorm_stats_backward needs d % 4 == 0, d <= 2048");
+  cudaStream_t st = S(stream);
+  ProfScope prof(st, "layernorm", 12.0 * rows * d);  // read dy, x; write dx
+  // about two CTAs per SM, rows per CTA a multiple of the warp count
+  const int64_t rpc = std::max<int64_t>(LN_WARPS, cdiv(cdiv(rows, 2 * 148), LN_WARPS) * LN_WARPS);
+  const int64_t nblk = cdiv(rows, rpc);
+  float* part = nullptr;
+  if(dgain) {
+    if(!workspace || workspace_bytes < (size_t)nblk * 2 * (size_t)d * sizeof(float))
+      return fail(MTKC_CONTRACT, "layer norm backward workspace too small");
+    part = workspace;
+  }
+  const size_t smem = part ? (size_t)LN_WARPS * 2 * (size_t)d * sizeof(float) : 0;
+  const int nv = (int)cdiv(d, 128);
+#define LN4_BWD(NVV)                                                                         \
+  if(nv <= NVV) {                                                                            \
+    if(smem > 48 * 1024)                                                                     \
+      cudaFuncSetAttribute(ln_bwd4_kernel<NVV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                       \
+    ln_bwd4_kernel<NVV><<<(unsigned)nblk, LN_WARPS * 32, smem, st>>>(                        \
+        dy, x, gain, mean, inv_std, dx, part, rows, d, rpc, accumulate_dx);                  \
+  } else
+  LN4_BWD(1) LN4_BWD(2) LN4_BWD(4) LN4_BWD(8) LN4_BWD(16) {}
+#undef LN4_BWD
+  MTKC_POST_LAUNCH("ln_bwd4_kernel");
+  if(part) {
+    colred_final_kernel<2><<<colred_final_grid(d), 256, 0, st>>>(dgain, dbias, part, nblk, d,
+                                                                  accumulate_params);
+    MTKC_POST_LAUNCH("colred_final_kernel");
   }
   return MTKC_OK;
 }

@@ -64,7 +64,7 @@ def test_dot_fwd_bwd_bitexact(ta, tb, batched):
     assert np.array_equal(g.param_grad("b"), gb)
 
 
-@pytest.mark.parametrize("rows,d", [(7, 33), (300, 512), (64, 1024), (5, 2000)])
+@pytest.mark.parametrize("rows,d", [(7, 33), (300, 512), (64, 1024), (5, 2000), (9000, 512), (3, 4), (5, 2052)])
 def test_layernorm(rows, d):
     rng = np.random.default_rng(1)
     x = rng.normal(size=(rows, d)).astype(np.float32) * 3 + 1
