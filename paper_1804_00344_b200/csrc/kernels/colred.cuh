@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(256) colred_partial_kernel(float* part, const 
   }
 }
 
-// out_q[c] (+)= sum_rb part[rb][q][c]; block = 32 columns x 8 row-block lanes
+// out_q[c] (+)= sum_rb part[rb][q][c]; block = 32 columns x 8 row-block lanes.
+// Lane ry sums row blocks ry, ry+8, ... in order, eight loads per quantity in
+// flight per batch (the kernel is latency-bound: few CTAs, short rows).
 template <int NQ>
 __global__ void __launch_bounds__(256) colred_final_kernel(float* out0, float* out1,
                                                            const float* part, int64_t nblk,
@@ -119,24 +121,19 @@ __global__ void __launch_bounds__(256) colred_final_kernel(float* out0, float* o
   for(int q = 0; q < NQ; ++q)
     s[q] = 0.f;
   if(c < cols) {
-    int64_t rb = ry;
-    for(; rb + 24 < nblk; rb += 32) {  // four independent loads per quantity in flight
-      float v[4][NQ];
+    for(int64_t rb = ry; rb < nblk; rb += 64) {
+      float v[8][NQ];
 #pragma unroll
-      for(int u = 0; u < 4; ++u)
+      for(int u = 0; u < 8; ++u)
 #pragma unroll
         for(int q = 0; q < NQ; ++q)
-          v[u][q] = part[((rb + 8 * u) * NQ + q) * cols + c];
+          v[u][q] = rb + 8 * u < nblk ? __ldcg(part + ((rb + 8 * u) * NQ + q) * cols + c) : 0.f;
 #pragma unroll
-      for(int u = 0; u < 4; ++u)
+      for(int u = 0; u < 8; ++u)
 #pragma unroll
         for(int q = 0; q < NQ; ++q)
           s[q] += v[u][q];
     }
-    for(; rb < nblk; rb += 8)
-#pragma unroll
-      for(int q = 0; q < NQ; ++q)
-        s[q] += part[(rb * NQ + q) * cols + c];
   }
 #pragma unroll
   for(int q = 0; q < NQ; ++q)

@@ -511,12 +511,21 @@ __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t M, i
     const int64_t r = i / groups, c = (i - r * groups) * 4;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     if(VEC) {
-      for(int s = 0; s < splits; ++s) {
-        float4 x = *reinterpret_cast<const float4*>(part + s * plane + r * N + c);
-        acc[0] += x.x;
-        acc[1] += x.y;
-        acc[2] += x.z;
-        acc[3] += x.w;
+      // eight partial loads in flight, summed in split order
+      for(int s0 = 0; s0 < splits; s0 += 8) {
+        float4 x[8];
+#pragma unroll
+        for(int u = 0; u < 8; ++u)
+          x[u] = s0 + u < splits ? __ldcs(reinterpret_cast<const float4*>(part + (s0 + u) * plane +
+                                                                           r * N + c))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for(int u = 0; u < 8; ++u) {
+          acc[0] += x[u].x;
+          acc[1] += x[u].y;
+          acc[2] += x[u].z;
+          acc[3] += x[u].w;
+        }
       }
     } else {
       for(int s = 0; s < splits; ++s)
@@ -671,7 +680,12 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
   }
   const int64_t mt = cdiv(a.M, BM);
   // wide tiles only when they still give every SM at least one tile
-  int BN = (a.N >= 256 && mt * cdiv(a.N, 256) >= g_sms) ? 256 : 128;
+  // wide tiles halve the re-reads of A (the L2->SM operand traffic that
+  // bounds fp32-storage GEMMs) -- worth a partly idle wave; narrow tiles only
+  // when there are so few wide tiles that split-K would have to fill the GPU
+  int BN = (a.N >= 256 && mt * cdiv(a.N, 256) >= 32) ? 256 : 128;
+  if(const char* e = getenv("MTK_GEMM_BN"))  // tuning override (tools/gemm_bench.py)
+    BN = (atoi(e) == 256 && a.N >= 256) ? 256 : 128;
   const int64_t nt = cdiv(a.N, BN);
   const int numKb = (int)cdiv(a.K, BK);
   // Split K to fill the machine: pick the split count (each split keeping

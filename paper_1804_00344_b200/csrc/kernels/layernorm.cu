@@ -230,47 +230,80 @@ __global__ void __launch_bounds__(LN_WARPS * 32)
     sg[k] = sb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int64_t r0 = blockIdx.x * rowsPerCta, r1 = min(rows, r0 + rowsPerCta);
-  for(int64_t row = r0 + w; row < r1; row += LN_WARPS) {
-    const float mu = mean[row], rs = invStd[row];
-    float4 dy4[NV], xh[NV], h[NV];
-    float s1 = 0.f, s2 = 0.f;
+  // two rows per iteration: both rows' loads are in flight before the
+  // first reduction (the kernel is latency-bound at one row per warp)
+  // rows in flight per warp: 1 (two rows cost occupancy and measured slower)
+  constexpr int RP = 1;
+  for(int64_t rowA = r0 + w; rowA < r1; rowA += RP * LN_WARPS) {
+    float4 dy4[RP][NV], xh[RP][NV], h[RP][NV];
+    float mu[RP], rs[RP], s1[RP], s2[RP];
+    bool ok[RP];
 #pragma unroll
-    for(int k = 0; k < NV; ++k) {
-      const int64_t c = 128 * k + 4 * lane;
-      if(c < d) {
-        dy4[k] = *reinterpret_cast<const float4*>(dy + row * d + c);
-        const float4 x4 = *reinterpret_cast<const float4*>(x + row * d + c);
-        xh[k] = make_float4((x4.x - mu) * rs, (x4.y - mu) * rs, (x4.z - mu) * rs,
-                            (x4.w - mu) * rs);
-      } else {
-        dy4[k] = xh[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for(int e = 0; e < RP; ++e) {
+      const int64_t row = rowA + e * LN_WARPS;
+      ok[e] = row < r1;
+      s1[e] = s2[e] = 0.f;
+      mu[e] = ok[e] ? mean[row] : 0.f;
+      rs[e] = ok[e] ? invStd[row] : 0.f;
+#pragma unroll
+      for(int k = 0; k < NV; ++k) {
+        const int64_t c = 128 * k + 4 * lane;
+        if(ok[e] && c < d) {
+          dy4[e][k] = *reinterpret_cast<const float4*>(dy + row * d + c);
+          xh[e][k] = *reinterpret_cast<const float4*>(x + row * d + c);
+        } else {
+          dy4[e][k] = xh[e][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
-      h[k] = make_float4(dy4[k].x * gg[k].x, dy4[k].y * gg[k].y, dy4[k].z * gg[k].z,
-                         dy4[k].w * gg[k].w);
-      s1 += (h[k].x + h[k].y) + (h[k].z + h[k].w);
-      s2 += (h[k].x * xh[k].x + h[k].y * xh[k].y) + (h[k].z * xh[k].z + h[k].w * xh[k].w);
-      sg[k].x += dy4[k].x * xh[k].x;
-      sg[k].y += dy4[k].y * xh[k].y;
-      sg[k].z += dy4[k].z * xh[k].z;
-      sg[k].w += dy4[k].w * xh[k].w;
-      f4add(sb[k], dy4[k]);
     }
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    const float m1 = s1 / (float)d, m2 = s2 / (float)d;
 #pragma unroll
-    for(int k = 0; k < NV; ++k) {
-      const int64_t c = 128 * k + 4 * lane;
-      if(c < d) {
-        float4 o;
-        o.x = rs * (h[k].x - m1 - xh[k].x * m2);
-        o.y = rs * (h[k].y - m1 - xh[k].y * m2);
-        o.z = rs * (h[k].z - m1 - xh[k].z * m2);
-        o.w = rs * (h[k].w - m1 - xh[k].w * m2);
-        float4* dst = reinterpret_cast<float4*>(dx + row * d + c);
-        if(accDx)
-          f4add(o, *dst);
-        *dst = o;
+    for(int e = 0; e < RP; ++e) {
+      const bool any = ok[e];
+#pragma unroll
+      for(int k = 0; k < NV; ++k) {
+        const int64_t c = 128 * k + 4 * lane;
+        if(any && c < d) {
+          const float4 x4 = xh[e][k];
+          xh[e][k] = make_float4((x4.x - mu[e]) * rs[e], (x4.y - mu[e]) * rs[e],
+                                 (x4.z - mu[e]) * rs[e], (x4.w - mu[e]) * rs[e]);
+        }
+        const float4 d4v = dy4[e][k];
+        h[e][k] = make_float4(d4v.x * gg[k].x, d4v.y * gg[k].y, d4v.z * gg[k].z, d4v.w * gg[k].w);
+        s1[e] += (h[e][k].x + h[e][k].y) + (h[e][k].z + h[e][k].w);
+        s2[e] += (h[e][k].x * xh[e][k].x + h[e][k].y * xh[e][k].y) +
+                 (h[e][k].z * xh[e][k].z + h[e][k].w * xh[e][k].w);
+        sg[k].x += d4v.x * xh[e][k].x;
+        sg[k].y += d4v.y * xh[e][k].y;
+        sg[k].z += d4v.z * xh[e][k].z;
+        sg[k].w += d4v.w * xh[e][k].w;
+        f4add(sb[k], d4v);
+      }
+    }
+#pragma unroll
+    for(int e = 0; e < RP; ++e) {
+      s1[e] = warp_sum(s1[e]);
+      s2[e] = warp_sum(s2[e]);
+    }
+#pragma unroll
+    for(int e = 0; e < RP; ++e) {
+      if(!ok[e])
+        continue;
+      const int64_t row = rowA + e * LN_WARPS;
+      const float m1 = s1[e] / (float)d, m2 = s2[e] / (float)d;
+#pragma unroll
+      for(int k = 0; k < NV; ++k) {
+        const int64_t c = 128 * k + 4 * lane;
+        if(c < d) {
+          float4 o;
+          o.x = rs[e] * (h[e][k].x - m1 - xh[e][k].x * m2);
+          o.y = rs[e] * (h[e][k].y - m1 - xh[e][k].y * m2);
+          o.z = rs[e] * (h[e][k].z - m1 - xh[e][k].z * m2);
+          o.w = rs[e] * (h[e][k].w - m1 - xh[e][k].w * m2);
+          float4* dst = reinterpret_cast<float4*>(dx + row * d + c);
+          if(accDx)
+            f4add(o, *dst);
+          *dst = o;
+        }
       }
     }
   }
@@ -365,7 +398,7 @@ int mtkc_layernorm_backward(const float* dy, const float* gain, const float* inv
   return MTKC_OK;
 }
 
-int mtkc_layernorm_fast_supported(int64_t d) { return d >= 4 && d % 4 == 0 && d <= 2048; }
+int mtkc_layernorm_fast_supported(int64_t d) { return d >= 4 && d % 4 == 0 && d <= 1024; }
 
 int mtkc_layernorm_stats(float* out, const float* x, const float* gain, const float* bias,
                          float eps, float* mean, float* inv_std, int64_t rows, int64_t d,
@@ -374,9 +407,11 @@ int mtkc_layernorm_stats(float* out, const float* x, const float* gain, const fl
     return MTKC_OK;
   if(!mtkc_layernorm_fast_supported(d) || ((uintptr_t)x | (uintptr_t)out | (uintptr_t)gain |
                                            (uintptr_t)bias) % 16)
-    return fail(MTKC_DIMENSION, "mtkc_layernorm_stats needs d % 4 == 0, d <= 2048, aligned rows");
+    return fail(MTKC_DIMENSION, "mtkc_layernorm_stats needs d % 4 == 0, d <= 1024, aligned rows");
   cudaStream_t st = S(stream);
   ProfScope prof(st, "layernorm", 8.0 * rows * d);  // read x, write y
+  if(prof_detail())
+    prof.detail = "fwd4_r" + std::to_string(rows) + "_d" + std::to_string(d);
   dim3 grid((unsigned)cdiv(rows, LN_WARPS));
   const int nv = (int)cdiv(d, 128);
 #define LN4_FWD(NVV)                                                                   \
@@ -384,7 +419,7 @@ int mtkc_layernorm_stats(float* out, const float* x, const float* gain, const fl
     ln_fwd4_kernel<NVV><<<grid, LN_WARPS * 32, 0, st>>>(out, x, gain, bias, eps, mean, \
                                                         inv_std, rows, d);              \
   } else
-  LN4_FWD(1) LN4_FWD(2) LN4_FWD(4) LN4_FWD(8) LN4_FWD(16) {}
+  LN4_FWD(1) LN4_FWD(2) LN4_FWD(4) LN4_FWD(8) {}
 #undef LN4_FWD
   MTKC_POST_LAUNCH("ln_fwd4_kernel");
   return MTKC_OK;
@@ -404,9 +439,11 @@ int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* 
     return MTKC_OK;
   if(!mtkc_layernorm_fast_supported(d) ||
      ((uintptr_t)x | (uintptr_t)dy | (uintptr_t)dx | (uintptr_t)gain) % 16)
-    return fail(MTKC_DIMENSION, "mtkc_layernorm_stats_backward needs d % 4 == 0, d <= 2048");
+    return fail(MTKC_DIMENSION, "mtkc_layernorm_stats_backward needs d % 4 == 0, d <= 1024");
   cudaStream_t st = S(stream);
   ProfScope prof(st, "layernorm", 12.0 * rows * d);  // read dy, x; write dx
+  if(prof_detail())
+    prof.detail = "bwd4_r" + std::to_string(rows) + "_d" + std::to_string(d);
   // about two CTAs per SM, rows per CTA a multiple of the warp count
   const int64_t rpc = std::max<int64_t>(LN_WARPS, cdiv(cdiv(rows, 2 * 148), LN_WARPS) * LN_WARPS);
   const int64_t nblk = cdiv(rows, rpc);
@@ -426,7 +463,7 @@ int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* 
     ln_bwd4_kernel<NVV><<<(unsigned)nblk, LN_WARPS * 32, smem, st>>>(                        \
         dy, x, gain, mean, inv_std, dx, part, rows, d, rpc, accumulate_dx);                  \
   } else
-  LN4_BWD(1) LN4_BWD(2) LN4_BWD(4) LN4_BWD(8) LN4_BWD(16) {}
+  LN4_BWD(1) LN4_BWD(2) LN4_BWD(4) LN4_BWD(8) {}
 #undef LN4_BWD
   MTKC_POST_LAUNCH("ln_bwd4_kernel");
   if(part) {

@@ -80,6 +80,89 @@ __global__ void colsum_direct_kernel(float* out, const float* in, int64_t rows, 
   out[c] = (accumulate ? out[c] : 0.f) + s;
 }
 
+// One-launch deterministic column sum: colred_partial_kernel's stage 1, then
+// the last CTA to finish a 128-column slab (atomic ticket) sums that slab's
+// row-block partials in fixed row-block order -- the result does not depend
+// on which CTA is last.  Tickets reset themselves for the next call.
+constexpr int CS_MAX_SLABS = 8192;
+__device__ unsigned int g_colsum_ticket[CS_MAX_SLABS];
+
+__global__ void __launch_bounds__(256) colsum_onepass_kernel(float* out, float* part,
+                                                             const float* a, int64_t rows,
+                                                             int64_t cols, int acc) {
+  __shared__ float4 red[8][32];
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * CR_COLS + lane * 4;
+  const int64_t r0 = (int64_t)blockIdx.y * CR_ROWS + w;
+  const int64_t nblk = gridDim.y;
+  float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if(c < cols) {  // cols % 4 == 0 (host)
+    float4 xa[CR_RPW];
+#pragma unroll
+    for(int i = 0; i < CR_RPW; ++i) {
+      const int64_t r = r0 + 8 * i;
+      xa[i] = r < rows ? __ldg(reinterpret_cast<const float4*>(a + r * cols + c))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for(int i = 0; i < CR_RPW; ++i)
+      f4add(s0, xa[i]);
+  }
+  red[w][lane] = s0;
+  __syncthreads();
+  if(w == 0 && c < cols) {
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for(int k = 0; k < 8; ++k)
+      f4add(t, red[k][lane]);
+    *reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * cols + c) = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if(threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&g_colsum_ticket[blockIdx.x], 1u);
+    last = prev == (unsigned)(nblk - 1);
+  }
+  __syncthreads();
+  if(!last)
+    return;
+  __threadfence();
+  // slab total: warp w sums row blocks w, w+8, ... (in order), then the 8
+  // warps combine in fixed order
+  float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+  if(c < cols)
+    for(int64_t rb = w; rb < nblk; rb += 64) {  // eight loads in flight, summed in order
+      float4 v[8];
+#pragma unroll
+      for(int u = 0; u < 8; ++u)
+        v[u] = rb + 8 * u < nblk
+                   ? __ldcg(reinterpret_cast<const float4*>(part + (rb + 8 * u) * cols + c))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for(int u = 0; u < 8; ++u)
+        f4add(t, v[u]);
+    }
+  red[w][lane] = t;
+  __syncthreads();
+  if(w == 0) {
+    if(c < cols) {
+      float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for(int k = 0; k < 8; ++k)
+        f4add(u, red[k][lane]);
+      float4* o = reinterpret_cast<float4*>(out + c);
+      if(acc) {
+        float4 prevv = *o;
+        u = make_float4(prevv.x + u.x, prevv.y + u.y, prevv.z + u.z, prevv.w + u.w);
+      }
+      *o = u;
+    }
+    if(lane == 0)
+      g_colsum_ticket[blockIdx.x] = 0u;
+  }
+}
+
 __global__ void finite_kernel(const float* in, int64_t n, int* flags) {
   bool bad = false;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -128,6 +211,8 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
   if(rows <= 0 || cols <= 0)
     return MTKC_OK;
   ProfScope prof(S(stream), "colsum", 4.0 * rows * cols);
+  if(prof_detail())
+    prof.detail = "r" + std::to_string(rows) + "_c" + std::to_string(cols);
   if(rows <= CS_ROWS || !workspace || workspace_bytes < colred_workspace_bytes(1, rows, cols)) {
     colsum_direct_kernel<<<(unsigned)cdiv(cols, 128), 128, 0, S(stream)>>>(out, in, rows, cols,
                                                                           accumulate);
@@ -135,6 +220,13 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
     return MTKC_OK;
   }
   int64_t nblk = cdiv(rows, CR_ROWS);
+  if(cols % 4 == 0 && cdiv(cols, CR_COLS) <= CS_MAX_SLABS && nblk <= 65535 &&
+     ((uintptr_t)in | (uintptr_t)out | (uintptr_t)workspace) % 16 == 0) {
+    colsum_onepass_kernel<<<dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
+                            S(stream)>>>(out, workspace, in, rows, cols, accumulate);
+    MTKC_POST_LAUNCH("colsum_onepass_kernel");
+    return MTKC_OK;
+  }
   colred_partial_kernel<1><<<dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
                              S(stream)>>>(workspace, in, nullptr, rows, cols);
   MTKC_POST_LAUNCH("colred_partial_kernel");

@@ -300,3 +300,30 @@ def test_attention_tensor_core_tf32(causal, shape):
         _close(g.param_grad("q"), gq + extra, 5e-3)
         _close(g.param_grad("k"), gk + (extra if tq == tk else 0.0), 5e-3)
         _close(g.param_grad("v"), gv + (extra if tq == tk else 0.0), 5e-3)
+
+
+@pytest.mark.parametrize("rows,cols", [(8184, 512), (100, 36), (1000, 30), (3000, 2048), (777, 1000)])
+def test_colsum_deterministic(rows, cols):
+    """Bias-gradient column sums (affine backward): one-pass kernel with a
+    last-CTA fixed-order finish; bitwise stable run to run, accumulate mode."""
+    import ctypes as C
+    import torch
+    from paper_1804_00344_b200 import cabi
+    rng = np.random.default_rng(rows)
+    x = rng.normal(size=(rows, cols)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    outs = []
+    for acc in (0, 0, 1):
+        if acc == 0:
+            out = torch.zeros(cols, device="cuda")
+        cabi.check(cabi.lib().mtkc_colsum(C.c_void_p(out.data_ptr()), C.c_void_p(xd.data_ptr()),
+                                          C.c_int64(rows), C.c_int64(cols), C.c_int(acc),
+                                          C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()),
+                                          C.c_void_p(0)))
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy().copy())
+    want = x.astype(np.float64).sum(0)
+    assert np.abs(outs[0] - want).max() <= 1e-5 * np.abs(x).sum(0).max()
+    assert np.array_equal(outs[0], outs[1])
+    assert np.abs(outs[2] - 2 * want).max() <= 2e-5 * np.abs(x).sum(0).max()
