@@ -4,6 +4,7 @@
 #include "mtk/graph.h"
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1339,7 +1340,9 @@ void ExpressionGraph::forward() {
   computed_ = nodes_.size();
 }
 
-void ExpressionGraph::backward(NodeRef loss) {
+void ExpressionGraph::backward(NodeRef loss) { backward(loss, nullptr); }
+
+void ExpressionGraph::backward(NodeRef loss, const std::function<void(int)>& afterNode) {
   checkRef(loss);
   if(inference_)
     throw ContractError("backward() called on an inference-mode graph");
@@ -1358,10 +1361,60 @@ void ExpressionGraph::backward(NodeRef loss) {
   }
   for(int i = loss.index; i >= 0; --i) {
     Node& n = nodes_[(size_t)i];
-    if(n.alias >= 0 || !n.bwd || !n.gradLive)
-      continue;
-    n.bwd(*this, n);
+    if(!(n.alias >= 0 || !n.bwd || !n.gradLive))
+      n.bwd(*this, n);
+    if(afterNode)
+      afterNode(i);
   }
+}
+
+std::vector<ExpressionGraph::GradBucket> ExpressionGraph::gradBuckets(int64_t targetElems) const {
+  // lowest consumer index per (alias-resolved) node
+  std::vector<int> firstUse(nodes_.size(), INT_MAX);
+  for(size_t i = 0; i < nodes_.size(); ++i)
+    for(int in : nodes_[i].inputs) {
+      int r = resolve(in);
+      firstUse[(size_t)r] = std::min(firstUse[(size_t)r], (int)i);
+    }
+  struct P {
+    int64_t off;
+    int ready;
+  };
+  std::vector<P> ps;
+  for(auto& [name, p] : params_) {
+    auto it = paramNode_.find(name);
+    int ready = it == paramNode_.end() ? INT_MAX : firstUse[(size_t)it->second];
+    ps.push_back({p.offset, ready});
+  }
+  std::sort(ps.begin(), ps.end(), [](const P& a, const P& b) { return a.off < b.off; });
+  std::vector<GradBucket> out;
+  const int64_t used = pool_.used();
+  for(size_t k = 0; k < ps.size();) {
+    GradBucket b{ps[k].off, 0, INT_MAX};
+    size_t j = k;
+    for(; j < ps.size(); ++j) {
+      int64_t next = j + 1 < ps.size() ? ps[j + 1].off : used;
+      b.readyAfter = std::min(b.readyAfter, ps[j].ready);
+      b.end = next;
+      if(b.end - b.begin >= targetElems) {
+        ++j;
+        break;
+      }
+    }
+    if(k == 0)
+      b.begin = 0;
+    out.push_back(b);
+    k = j;
+  }
+  return out;
+}
+
+void ExpressionGraph::realizeParamGradsRange(int64_t begin, int64_t end) {
+  for(auto& [name, p] : params_)
+    if(!p.gradLive && p.offset >= begin && p.offset < end) {
+      p.grad.setZero();
+      p.gradLive = true;
+    }
 }
 
 void ExpressionGraph::clear() {

@@ -98,7 +98,9 @@ struct DistContext {
   int world = 1;
   void* comm = nullptr;  // ncclComm_t
 };
-void setDistributed(int rank, int world, const void* ncclId128);
+// world == 1 with forceComm creates a one-rank NCCL communicator, so the
+// exchange path (buckets, streams, events) runs on a single GPU too.
+void setDistributed(int rank, int world, const void* ncclId128, bool forceComm = false);
 DistContext& distContext();
 
 struct TrainOptions {
@@ -115,6 +117,11 @@ struct TrainOptions {
   std::string resumeFrom;
   int64_t logEvery = 0;
   std::ostream* log = nullptr;
+  // data-parallel gradient exchange: bucketed NCCL all-reduces issued on a
+  // communication stream during the backward sweep (each bucket as soon as
+  // its gradients are final), or one all-reduce after the backward
+  bool overlapAllreduce = true;
+  int64_t bucketElems = (int64_t)8 << 20;  // 32 MiB of fp32 gradients
 };
 
 struct TrainResult {
@@ -149,6 +156,14 @@ private:
   AveragedParameters& avg_;
   TrainOptions opts_;
   std::shared_ptr<DeviceBuffer> lossAcc_;
+  void* commStream_ = nullptr;       // NCCL stream (bucketed all-reduce)
+  std::vector<void*> events_;        // compute -> comm "bucket ready" events
+  void* commDone_ = nullptr;         // comm -> compute "exchange finished"
+  int64_t bucketsIssued_ = 0;        // telemetry (tests)
+
+public:
+  int64_t bucketsIssued() const { return bucketsIssued_; }
+  ~SyncStepper();
 };
 
 uint64_t mixSeed(uint64_t seed, int64_t update, int worker);

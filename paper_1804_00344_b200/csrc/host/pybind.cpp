@@ -146,10 +146,13 @@ PYBIND11_MODULE(_mtk, m) {
     MTKC(mtkc_nccl_unique_id(id));
     return py::bytes(id, 128);
   });
-  m.def("set_distributed", [](int rank, int world, py::bytes id) {
-    std::string s = id;
-    setDistributed(rank, world, s.data());
-  });
+  m.def(
+      "set_distributed",
+      [](int rank, int world, py::bytes id, bool forceComm) {
+        std::string s = id;
+        setDistributed(rank, world, s.data(), forceComm);
+      },
+      py::arg("rank"), py::arg("world"), py::arg("id"), py::arg("force_comm") = false);
 
   // ---------------------------------------------------------- tensors
   py::class_<Tensor>(m, "Tensor")
@@ -250,7 +253,7 @@ PYBIND11_MODULE(_mtk, m) {
       .def("mask_blend",
            [](G& g, NodeRef a, NodeRef b, FArr m) { return g.maskBlend(a, b, fromNumpy(m)); })
       .def("forward", &G::forward)
-      .def("backward", &G::backward)
+      .def("backward", [](G& g, NodeRef loss) { g.backward(loss); })
       .def("clear", &G::clear)
       .def("set_seed", &G::setSeed)
       .def("set_loss_scale", &G::setLossScale)
@@ -440,7 +443,9 @@ PYBIND11_MODULE(_mtk, m) {
       .def_readwrite("log_every", &TrainOptions::logEvery)
       .def_readwrite("checkpoint_path", &TrainOptions::checkpointPath)
       .def_readwrite("checkpoint_every", &TrainOptions::checkpointEvery)
-      .def_readwrite("resume_from", &TrainOptions::resumeFrom);
+      .def_readwrite("resume_from", &TrainOptions::resumeFrom)
+      .def_readwrite("overlap_allreduce", &TrainOptions::overlapAllreduce)
+      .def_readwrite("bucket_elems", &TrainOptions::bucketElems);
   m.def("save_model", [](const std::string& path, const std::string& cfg, G& g) {
     saveModel(path, ModelConfig::parse(cfg), g);
   });
@@ -486,7 +491,8 @@ PYBIND11_MODULE(_mtk, m) {
              return s.update(batches, u, read);
            },
            py::arg("batches"), py::arg("update_index"), py::arg("read_loss") = true)
-      .def("host_times", &SyncStepper::hostTimes);
+      .def("host_times", &SyncStepper::hostTimes)
+      .def("buckets_issued", &SyncStepper::bucketsIssued);
 
   m.def("mix_seed", &mixSeed);
 }

@@ -213,11 +213,15 @@ DistContext g_dist;
 
 DistContext& distContext() { return g_dist; }
 
-void setDistributed(int rank, int world, const void* ncclId128) {
+void setDistributed(int rank, int world, const void* ncclId128, bool forceComm) {
   Device::get();
+  if(g_dist.comm) {  // re-initialisation (tests): drop the old communicator
+    mtkc_nccl_comm_destroy(g_dist.comm);
+    g_dist.comm = nullptr;
+  }
   g_dist.rank = rank;
   g_dist.world = world;
-  if(world > 1)
+  if(world > 1 || forceComm)
     MTKC(mtkc_nccl_comm_init(&g_dist.comm, world, rank, ncclId128));
 }
 
@@ -305,6 +309,15 @@ SyncStepper::SyncStepper(const Model& model, ExpressionGraph& g, Adam& adam,
   lossAcc_ = std::make_shared<DeviceBuffer>(64);
 }
 
+SyncStepper::~SyncStepper() {
+  for(void* e : events_)
+    mtkc_event_destroy(e);
+  if(commDone_)
+    mtkc_event_destroy(commDone_);
+  if(commStream_)
+    mtkc_stream_destroy(commStream_);
+}
+
 UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64_t updateIndex,
                                  bool readLoss) {
   DistContext& dc = distContext();
@@ -324,6 +337,18 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
   Device& d = Device::get();
   MTKC(mtkc_memset(lossAcc_->ptr, 0, sizeof(float), d.stream()));
   g_.zeroGrads();
+  const bool exchange = dc.comm != nullptr;
+  const bool overlap = exchange && opts_.overlapAllreduce;
+  if(overlap && !commStream_) {
+    MTKC(mtkc_stream_create(&commStream_));
+    MTKC(mtkc_event_create(&commDone_));
+  }
+  // the rank's last local worker (its backward finalises the gradients)
+  int lastLocal = -1;
+  for(int j = 0; j < L; ++j)
+    if(dc.rank * L + j < take)
+      lastLocal = j;
+  bool issuedAll = false;
   for(int j = 0; j < L; ++j) {
     int i = dc.rank * L + j;
     if(i >= take)
@@ -337,7 +362,42 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
     auto t1 = std::chrono::steady_clock::now();
     g_.forward();
     auto t2 = std::chrono::steady_clock::now();
-    g_.backward(loss);
+    if(overlap && j == lastLocal) {
+      // Bucketed all-reduce overlapped with the backward sweep: a bucket is
+      // a contiguous range of the flat gradient pool; once the sweep has
+      // passed the lowest-index consumer of every parameter in it, the
+      // compute stream records an event and the comm stream all-reduces
+      // the range while the backward continues.
+      auto buckets = g_.gradBuckets(opts_.bucketElems);
+      std::sort(buckets.begin(), buckets.end(),
+                [](const ExpressionGraph::GradBucket& a, const ExpressionGraph::GradBucket& b) {
+                  return a.readyAfter > b.readyAfter;
+                });
+      while(events_.size() < buckets.size()) {
+        void* e = nullptr;
+        MTKC(mtkc_event_create(&e));
+        events_.push_back(e);
+      }
+      size_t next = 0;
+      float* grads = g_.pool().grads()->ptr;
+      auto issue = [&](size_t k) {
+        const auto& b = buckets[k];
+        g_.realizeParamGradsRange(b.begin, b.end);
+        MTKC(mtkc_event_record(events_[k], d.stream()));
+        MTKC(mtkc_stream_wait_event(commStream_, events_[k]));
+        MTKC(mtkc_allreduce_sum(dc.comm, grads + b.begin, b.end - b.begin, commStream_));
+        ++bucketsIssued_;
+      };
+      g_.backward(loss, [&](int node) {
+        while(next < buckets.size() && buckets[next].readyAfter >= node)
+          issue(next++);
+      });
+      while(next < buckets.size())
+        issue(next++);
+      issuedAll = true;
+    } else {
+      g_.backward(loss);
+    }
     auto t3 = std::chrono::steady_clock::now();
     hostTimes_[0] += std::chrono::duration<double, std::milli>(t1 - t0).count();
     hostTimes_[1] += std::chrono::duration<double, std::milli>(t2 - t1).count();
@@ -345,9 +405,17 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
     MTKC(mtkc_axpy(lossAcc_->ptr, loss.val().devc(), w, 1, d.stream()));
   }
   g_.setLossScale(1);
-  if(dc.world > 1) {
-    g_.realizeParamGrads();
-    MTKC(mtkc_allreduce_sum(dc.comm, g_.pool().grads()->ptr, g_.pool().used(), d.stream()));
+  if(exchange) {
+    if(issuedAll) {
+      // compute stream waits for the last bucket before Adam reads the pool
+      MTKC(mtkc_event_record(commDone_, commStream_));
+      MTKC(mtkc_stream_wait_event(d.stream(), commDone_));
+    } else {
+      // rank without a batch at the epoch tail, or overlap disabled: the
+      // whole pool in one all-reduce (idle ranks contribute zeros)
+      g_.realizeParamGrads();
+      MTKC(mtkc_allreduce_sum(dc.comm, g_.pool().grads()->ptr, g_.pool().used(), d.stream()));
+    }
     MTKC(mtkc_allreduce_sum(dc.comm, lossAcc_->ptr, 1, d.stream()));
   }
   Real lr = opts_.lr(adam_.step() + 1);
