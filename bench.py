@@ -139,6 +139,18 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def traffic_per_call(config, cls, calls_per_step):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the class per C-ABI call,
+    from the committed ncu capture of one update (tools/traffic.py)."""
+    path = os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)["classes"][cls]
+        return round(j["dram_bytes"] / max(calls_per_step, 1)), os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
+
+
 # ------------------------------------------------------------ CPU reference
 
 def cpu_reference(cfg_text, vocab, seconds_budget, threads=None, steps=1):
@@ -281,10 +293,13 @@ def run_b200(a):
         per_launch_s = c["ms"] / max(c["launches"], 1) / 1e3
         achieved = per_launch_work / per_launch_s / (1e12 if tensor else 1e9)
         peak = tflops if tensor else hbm
+        traffic, tsrc = traffic_per_call(a.config, dom, c["launches"])
         roof = {"bound": "tensor" if tensor else "hbm", "kernel": dom,
                 "achieved": round(achieved, 2), "peak": peak,
                 "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "peak_source": f"{src} (bf16 dense, sustained)",
+                "traffic": traffic, "traffic_source": tsrc,
+                "algorithmic_per_launch": per_launch_work,
+                "peak_source": f"{src} (bf16 dense, sustained)",
                 "share_of_step": round(c["ms"] / step_ms, 4),
                 "note": "GEMMs run tcgen05 kind::tf32 on fp32 storage; tf32 dense peak is half the bf16 denominator"}
     breakdown = {k: {"ms_per_step": round(v["ms"], 3), "share": round(v["ms"] / step_ms, 4),
