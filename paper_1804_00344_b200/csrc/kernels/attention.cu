@@ -49,6 +49,7 @@ __device__ __forceinline__ bool key_ok(const AttP& p, int64_t bi, int64_t i, int
 }
 
 __global__ void __launch_bounds__(ATT_T) attn_fwd_kernel(AttP p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float sm[];
   const int64_t dk = p.dk, ldS = p.tk + 1;
   float* Qs = sm;                       // [QB][dk+1]
@@ -182,6 +183,7 @@ struct AttBP {
 // Pass A, per (query block, head, batch row):
 //   dP = dO V^T ; D = rowsum(dP*P) ; G = scale * P*(dP - D) -> ds ; dQ (+)= G K
 __global__ void __launch_bounds__(ATT_T) attn_bwd_q_kernel(AttBP p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float sm[];
   const int64_t dk = p.dk, ldS = p.tk + 1;
   float* Os = sm;                   // dO block [QB][dk+1]
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(ATT_T) attn_bwd_q_kernel(AttBP p) {
 // Pass B, per (key chunk, head, batch row): dK (+)= G^T Q, dV (+)= P^T dO,
 // summing over queries in ascending order.
 __global__ void __launch_bounds__(ATT_T) attn_bwd_kv_kernel(AttBP p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float sm[];
   const int64_t dk = p.dk;
   float* Qs = sm;                     // [QB][dk+1] query chunk (Q then dO)
@@ -410,6 +413,7 @@ __device__ __forceinline__ float grp_sum(float v) {
 }
 
 __global__ void __launch_bounds__(256) attn_fwd_tile_kernel(AttP p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   float* Qt = sm;             // [dk][i]
@@ -480,6 +484,7 @@ __global__ void __launch_bounds__(256) attn_fwd_tile_kernel(AttP p) {
 }
 
 __global__ void __launch_bounds__(256) attn_bwd_tile_kernel(AttBP p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   float* dO = sm;            // [i][c]
@@ -660,6 +665,7 @@ __device__ __forceinline__ void stage64(float* dst, const float* src, int64_t ld
 
 template <int TT>
 __global__ void __launch_bounds__(256) attn_fwd_pad_kernel(AttP p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float4 smem4[];
   constexpr int LDP = Pad<TT>::LDP;
   float* sm = reinterpret_cast<float*>(smem4);
@@ -720,6 +726,7 @@ __global__ void __launch_bounds__(256) attn_fwd_pad_kernel(AttP p) {
 
 template <int TT>
 __global__ void __launch_bounds__(256) attn_bwd_pad_kernel(AttBP p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float4 smem4[];
   constexpr int LDP = Pad<TT>::LDP;
   float* sm = reinterpret_cast<float*>(smem4);
@@ -842,7 +849,7 @@ int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_
     rc = set_smem((const void*)attn_fwd_pad_kernel<TTV>, smem);                   \
     if(rc)                                                                        \
       return rc;                                                                  \
-    attn_fwd_pad_kernel<TTV><<<grid, 256, smem, S(stream)>>>(p);                  \
+    ::mtkc::launch(attn_fwd_pad_kernel<TTV>, grid, 256, smem, S(stream), p);                  \
   }
     MTKC_ATT_FWD(32) MTKC_ATT_FWD(48) MTKC_ATT_FWD(64)
 #undef MTKC_ATT_FWD
@@ -854,7 +861,7 @@ int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_
     int rc = set_smem((const void*)attn_fwd_tile_kernel, smem);
     if(rc)
       return rc;
-    attn_fwd_tile_kernel<<<dim3((unsigned)heads, (unsigned)b), 256, smem, S(stream)>>>(p);
+    ::mtkc::launch(attn_fwd_tile_kernel, dim3((unsigned)heads, (unsigned)b), 256, smem, S(stream), p);
     MTKC_POST_LAUNCH("attn_fwd_tile_kernel");
     return MTKC_OK;
   }
@@ -864,7 +871,7 @@ int mtkc_attention(float* out, int64_t ldo, float* probs, const float* q, int64_
   if(rc)
     return rc;
   dim3 grid((unsigned)cdiv(tq, QB), (unsigned)heads, (unsigned)b);
-  attn_fwd_kernel<<<grid, ATT_T, smem, S(stream)>>>(p);
+  ::mtkc::launch(attn_fwd_kernel, grid, ATT_T, smem, S(stream), p);
   MTKC_POST_LAUNCH("attn_fwd_kernel");
   return MTKC_OK;
 }
@@ -893,7 +900,7 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
     rc = set_smem((const void*)attn_bwd_pad_kernel<TTV>, smem);                   \
     if(rc)                                                                        \
       return rc;                                                                  \
-    attn_bwd_pad_kernel<TTV><<<grid, 256, smem, S(stream)>>>(p);                  \
+    ::mtkc::launch(attn_bwd_pad_kernel<TTV>, grid, 256, smem, S(stream), p);                  \
   }
     MTKC_ATT_BWD(32) MTKC_ATT_BWD(48) MTKC_ATT_BWD(64)
 #undef MTKC_ATT_BWD
@@ -905,7 +912,7 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
     int rc = set_smem((const void*)attn_bwd_tile_kernel, smem);
     if(rc)
       return rc;
-    attn_bwd_tile_kernel<<<dim3((unsigned)heads, (unsigned)b), 256, smem, S(stream)>>>(p);
+    ::mtkc::launch(attn_bwd_tile_kernel, dim3((unsigned)heads, (unsigned)b), 256, smem, S(stream), p);
     MTKC_POST_LAUNCH("attn_bwd_tile_kernel");
     return MTKC_OK;
   }
@@ -915,14 +922,14 @@ int mtkc_attention_backward(const float* gout, int64_t ldo, const float* probs,
   if(rc)
     return rc;
   dim3 gA((unsigned)cdiv(tq, QB), (unsigned)heads, (unsigned)b);
-  attn_bwd_q_kernel<<<gA, ATT_T, smemA, S(stream)>>>(p);
+  ::mtkc::launch(attn_bwd_q_kernel, gA, ATT_T, smemA, S(stream), p);
   MTKC_POST_LAUNCH("attn_bwd_q_kernel");
   size_t smemB = sizeof(float) * (2 * (size_t)QB * (dk + 1) + 2 * (size_t)QB * (KC + 1));
   rc = set_smem((const void*)attn_bwd_kv_kernel, smemB);
   if(rc)
     return rc;
   dim3 gB((unsigned)cdiv(tk, KC), (unsigned)heads, (unsigned)b);
-  attn_bwd_kv_kernel<<<gB, ATT_T, smemB, S(stream)>>>(p);
+  ::mtkc::launch(attn_bwd_kv_kernel, gB, ATT_T, smemB, S(stream), p);
   MTKC_POST_LAUNCH("attn_bwd_kv_kernel");
   return MTKC_OK;
 }

@@ -124,6 +124,7 @@ constexpr size_t bwd_smem() {
 
 template <int TT>
 __global__ void __launch_bounds__(TT * 2) attn_tc_fwd_kernel(TcAttP p) {
+  MTKC_PDL_ENTRY();
   constexpr int NW = TT / 16, NT = TT / 8;
   extern __shared__ float4 smem4[];
   float* Q = reinterpret_cast<float*>(smem4);  // [TT][L4], later P (same rows per warp)
@@ -267,6 +268,7 @@ __device__ __forceinline__ void store2(float* d, float a, float b, int acc) {
 
 template <int TT>
 __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
+  MTKC_PDL_ENTRY();
   constexpr int NT = TT / 8, LP = PStride<TT>::v;
   extern __shared__ float4 smem4[];
   float* Q = reinterpret_cast<float*>(smem4);  // [TT][L8]
@@ -464,7 +466,7 @@ int mtkc_attention_tc(float* out, int64_t ldo, float* probs, const float* q, int
     size_t smem = fwd_smem<TTV>();                                                \
     if(int rc = set_smem_attr((const void*)attn_tc_fwd_kernel<TTV>, smem))        \
       return rc;                                                                  \
-    attn_tc_fwd_kernel<TTV><<<grid, TTV * 2, smem, S(stream)>>>(p);               \
+    ::mtkc::launch(attn_tc_fwd_kernel<TTV>, grid, TTV * 2, smem, S(stream), p);               \
   }
   MTKC_TC_FWD(16) MTKC_TC_FWD(32) MTKC_TC_FWD(48) MTKC_TC_FWD(64)
 #undef MTKC_TC_FWD
@@ -496,7 +498,7 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
     size_t smem = bwd_smem<TTV>();                                                \
     if(int rc = set_smem_attr((const void*)attn_tc_bwd_kernel<TTV>, smem))        \
       return rc;                                                                  \
-    attn_tc_bwd_kernel<TTV><<<grid, TTV * 2, smem, S(stream)>>>(p);               \
+    ::mtkc::launch(attn_tc_bwd_kernel<TTV>, grid, TTV * 2, smem, S(stream), p);               \
   }
   MTKC_TC_BWD(16) MTKC_TC_BWD(32) MTKC_TC_BWD(48) MTKC_TC_BWD(64)
 #undef MTKC_TC_BWD

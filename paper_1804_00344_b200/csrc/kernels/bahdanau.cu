@@ -14,6 +14,7 @@ constexpr int BT = 256;  // threads
 constexpr int BW = BT / 32;
 
 __global__ void __launch_bounds__(BT) bahdanau_fwd_kernel(mtkc_bahdanau_args p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float sm[];
   float* e = sm;             // [s]
   float* wsh = e + p.s;      // [s]
@@ -92,6 +93,7 @@ __global__ void __launch_bounds__(BT) bahdanau_fwd_kernel(mtkc_bahdanau_args p) 
 }
 
 __global__ void __launch_bounds__(BT) bahdanau_bwd_kernel(mtkc_bahdanau_args p) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float sm[];
   const int64_t A = p.a, S = p.s, KD = p.kd;
   float* dw = sm;                // [s]
@@ -221,7 +223,7 @@ int mtkc_bahdanau_forward(const mtkc_bahdanau_args* a, void* stream) {
   int rc = set_smem((const void*)bahdanau_fwd_kernel, smem);
   if(rc)
     return rc;
-  bahdanau_fwd_kernel<<<(unsigned)a->b, BT, smem, S(stream)>>>(*a);
+  ::mtkc::launch(bahdanau_fwd_kernel, (unsigned)a->b, BT, smem, S(stream), *a);
   MTKC_POST_LAUNCH("bahdanau_fwd_kernel");
   return MTKC_OK;
 }
@@ -236,7 +238,7 @@ int mtkc_bahdanau_backward(const mtkc_bahdanau_args* a, void* stream) {
   int rc = set_smem((const void*)bahdanau_bwd_kernel, smem);
   if(rc)
     return rc;
-  bahdanau_bwd_kernel<<<(unsigned)a->b, BT, smem, S(stream)>>>(*a);
+  ::mtkc::launch(bahdanau_bwd_kernel, (unsigned)a->b, BT, smem, S(stream), *a);
   MTKC_POST_LAUNCH("bahdanau_bwd_kernel");
   return MTKC_OK;
 }

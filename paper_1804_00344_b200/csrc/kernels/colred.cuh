@@ -31,6 +31,7 @@ template <int NQ>
 __global__ void __launch_bounds__(256) colred_partial_kernel(float* part, const float* a,
                                                              const float* b, int64_t rows,
                                                              int64_t cols) {
+  MTKC_PDL_ENTRY();
   __shared__ float4 red[8][NQ][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * CR_COLS + lane * 4;
@@ -113,6 +114,7 @@ template <int NQ>
 __global__ void __launch_bounds__(256) colred_final_kernel(float* out0, float* out1,
                                                            const float* part, int64_t nblk,
                                                            int64_t cols, int acc) {
+  MTKC_PDL_ENTRY();
   __shared__ float red[8][NQ][32];
   const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * 32 + cx;

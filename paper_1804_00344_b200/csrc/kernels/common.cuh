@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <string>
+#include <utility>
 
 #include "mtk_cuda.h"
 
@@ -40,7 +41,45 @@ struct ProfScope {
   }
 };
 
-// Launch check used after every <<<>>>: counts the launch and converts a
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Every kernel is launched with
+// programmatic stream serialisation, so its CTAs may be scheduled while the
+// previous kernel on the stream is still draining (its launch latency and
+// prologue overlap the predecessor's tail).  Correctness: every kernel
+// executes MTKC_PDL_ENTRY() -- griddepcontrol.wait, which blocks until the
+// preceding grid has completed and its memory is visible -- before touching
+// any global memory, and only then lets its own dependents launch
+// (griddepcontrol.launch_dependents), so at most one grid waits ahead.
+// MTK_NO_PDL=1 launches without the attribute (plain stream order).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#define MTKC_PDL_ENTRY()     \
+  do {                       \
+    ::mtkc::pdl_wait();      \
+    ::mtkc::pdl_trigger();   \
+  } while(0)
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// Launch check used after every launch: counts the launch and converts a
 // launch failure into MTKC_CUDA with the kernel name.
 #define MTKC_POST_LAUNCH(name)                                  \
   do {                                                          \

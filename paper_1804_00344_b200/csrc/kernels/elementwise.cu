@@ -20,6 +20,7 @@ struct BinP {
 };
 
 __global__ void binary_kernel(BinP p) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n;
       i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = i;
@@ -40,6 +41,7 @@ __global__ void binary_kernel(BinP p) {
 // same-shape operands: contiguous, 16-byte vectors
 __global__ void binary_same4_kernel(int op, float4* out, const float4* a, const float4* b,
                                     int64_t n4, int* flags) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
       i += (int64_t)gridDim.x * blockDim.x) {
     float4 x = a[i], y = b[i];
@@ -51,6 +53,7 @@ __global__ void binary_same4_kernel(int op, float4* out, const float4* a, const 
 }
 
 __global__ void unary_kernel(int op, float* out, const float* a, int64_t n) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x)
     out[i] = apply_unary(op, a[i]);
@@ -59,6 +62,7 @@ __global__ void unary_kernel(int op, float* out, const float* a, int64_t n) {
 // graph.cpp:200-218
 __global__ void unary_bwd_kernel(int op, float* gx, const float* go, const float* y,
                                  const float* x, int64_t n) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x) {
     float g = go[i];
@@ -105,6 +109,7 @@ struct BinBwdP {
 // One thread per target element; sums its broadcast positions in output
 // row-major order, the order accumulateReduced visits them (tensor.cpp:214-222).
 __global__ void binary_bwd_kernel(BinBwdP p) {
+  MTKC_PDL_ENTRY();
   for(int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < p.tn;
       t += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = t;
@@ -134,6 +139,7 @@ __global__ void binary_bwd_kernel(BinBwdP p) {
 }
 
 __global__ void scale_shift_kernel(float* out, const float* a, float s, float c, int64_t n) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x) {
     float v = a[i];
@@ -146,12 +152,14 @@ __global__ void scale_shift_kernel(float* out, const float* a, float s, float c,
 }
 
 __global__ void axpy_kernel(float* out, const float* a, float alpha, int64_t n) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x)
     out[i] += alpha == 1.f ? a[i] : alpha * a[i];
 }
 
 __global__ void axpy4_kernel(float4* out, const float4* a, float alpha, int64_t n4) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
       i += (int64_t)gridDim.x * blockDim.x) {
     float4 o = out[i], x = a[i];
@@ -170,6 +178,7 @@ __global__ void axpy4_kernel(float4* out, const float4* a, float alpha, int64_t 
 }
 
 __global__ void fill_kernel(float* out, float v, int64_t n) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x)
     out[i] = v;
@@ -179,6 +188,7 @@ __global__ void fill_kernel(float* out, float v, int64_t n) {
 // notM = addScalar(neg(m), 1) then add(mul(hn, m), mul(h, notM)).
 __global__ void mask_blend_kernel(float* out, const float* a, const float* b, const float* m,
                                   int64_t rows, int64_t cols) {
+  MTKC_PDL_ENTRY();
   int64_t n = rows * cols;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -190,6 +200,7 @@ __global__ void mask_blend_kernel(float* out, const float* a, const float* b, co
 
 __global__ void mask_blend_bwd_kernel(float* ga, float* gb, const float* go, const float* m,
                                       int64_t rows, int64_t cols, int acc_a, int acc_b) {
+  MTKC_PDL_ENTRY();
   int64_t n = rows * cols;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -205,6 +216,7 @@ __global__ void mask_blend_bwd_kernel(float* ga, float* gb, const float* go, con
 
 __global__ void scale_add_periodic_kernel(float* out, const float* x, float s, const float* c,
                                           int64_t n, int64_t period) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x) {
     float v = x[i];
@@ -215,6 +227,7 @@ __global__ void scale_add_periodic_kernel(float* out, const float* x, float s, c
 }
 
 __global__ void relu_mask_kernel(float* gx, const float* gate, int64_t n) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x)
     if(!(gate[i] > 0.f))
@@ -249,12 +262,12 @@ int mtkc_ewise_binary(int op, float* out, const int64_t od[4], const float* a,
   for(int i = 0; i < 4; ++i)
     same &= ad[i] == od[i] && bd[i] == od[i];
   if(same && p.n % 4 == 0 && ((uintptr_t)out | (uintptr_t)a | (uintptr_t)b) % 16 == 0) {
-    binary_same4_kernel<<<grid1d(p.n / 4, 256), 256, 0, S(stream)>>>(
+    ::mtkc::launch(binary_same4_kernel, grid1d(p.n / 4, 256), 256, 0, S(stream), 
         op, (float4*)out, (const float4*)a, (const float4*)b, p.n / 4, flags);
     MTKC_POST_LAUNCH("binary_same4_kernel");
     return MTKC_OK;
   }
-  binary_kernel<<<grid1d(p.n, 256), 256, 0, S(stream)>>>(p);
+  ::mtkc::launch(binary_kernel, grid1d(p.n, 256), 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("binary_kernel");
   return MTKC_OK;
 }
@@ -262,7 +275,7 @@ int mtkc_ewise_binary(int op, float* out, const int64_t od[4], const float* a,
 int mtkc_ewise_unary(int op, float* out, const float* a, int64_t n, void* stream) {
   if(n <= 0)
     return MTKC_OK;
-  unary_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(op, out, a, n);
+  ::mtkc::launch(unary_kernel, grid1d(n, 256), 256, 0, S(stream), op, out, a, n);
   MTKC_POST_LAUNCH("unary_kernel");
   return MTKC_OK;
 }
@@ -271,7 +284,7 @@ int mtkc_unary_backward(int op, float* gx, const float* go, const float* y, cons
                         int64_t n, void* stream) {
   if(n <= 0)
     return MTKC_OK;
-  unary_bwd_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(op, gx, go, y, x, n);
+  ::mtkc::launch(unary_bwd_kernel, grid1d(n, 256), 256, 0, S(stream), op, gx, go, y, x, n);
   MTKC_POST_LAUNCH("unary_bwd_kernel");
   return MTKC_OK;
 }
@@ -303,7 +316,7 @@ int mtkc_binary_backward(int op, int which, float* gtarget, const int64_t td[4],
   p.tn = prod4(td);
   if(p.tn == 0)
     return MTKC_OK;
-  binary_bwd_kernel<<<grid1d(p.tn, 128), 128, 0, S(stream)>>>(p);
+  ::mtkc::launch(binary_bwd_kernel, grid1d(p.tn, 128), 128, 0, S(stream), p);
   MTKC_POST_LAUNCH("binary_bwd_kernel");
   return MTKC_OK;
 }
@@ -311,7 +324,7 @@ int mtkc_binary_backward(int op, int which, float* gtarget, const int64_t td[4],
 int mtkc_scale_shift(float* out, const float* a, float s, float c, int64_t n, void* stream) {
   if(n <= 0)
     return MTKC_OK;
-  scale_shift_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(out, a, s, c, n);
+  ::mtkc::launch(scale_shift_kernel, grid1d(n, 256), 256, 0, S(stream), out, a, s, c, n);
   MTKC_POST_LAUNCH("scale_shift_kernel");
   return MTKC_OK;
 }
@@ -320,10 +333,10 @@ int mtkc_axpy(float* out, const float* a, float alpha, int64_t n, void* stream) 
   if(n <= 0)
     return MTKC_OK;
   if(n % 4 == 0 && ((uintptr_t)out % 16 == 0) && ((uintptr_t)a % 16 == 0)) {
-    axpy4_kernel<<<grid1d(n / 4, 256), 256, 0, S(stream)>>>((float4*)out, (const float4*)a,
+    ::mtkc::launch(axpy4_kernel, grid1d(n / 4, 256), 256, 0, S(stream), (float4*)out, (const float4*)a,
                                                             alpha, n / 4);
   } else {
-    axpy_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(out, a, alpha, n);
+    ::mtkc::launch(axpy_kernel, grid1d(n, 256), 256, 0, S(stream), out, a, alpha, n);
   }
   MTKC_POST_LAUNCH("axpy_kernel");
   return MTKC_OK;
@@ -339,7 +352,7 @@ int mtkc_accumulate_reduced(float* out, const int64_t od[4], const float* src,
 int mtkc_fill(float* out, float v, int64_t n, void* stream) {
   if(n <= 0)
     return MTKC_OK;
-  fill_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(out, v, n);
+  ::mtkc::launch(fill_kernel, grid1d(n, 256), 256, 0, S(stream), out, v, n);
   MTKC_POST_LAUNCH("fill_kernel");
   return MTKC_OK;
 }
@@ -348,7 +361,7 @@ int mtkc_scale_add_periodic(float* out, const float* x, float s, const float* c,
                             int64_t period, void* stream) {
   if(n <= 0)
     return MTKC_OK;
-  scale_add_periodic_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(out, x, s, c, n, period);
+  ::mtkc::launch(scale_add_periodic_kernel, grid1d(n, 256), 256, 0, S(stream), out, x, s, c, n, period);
   MTKC_POST_LAUNCH("scale_add_periodic_kernel");
   return MTKC_OK;
 }
@@ -356,7 +369,7 @@ int mtkc_scale_add_periodic(float* out, const float* x, float s, const float* c,
 int mtkc_relu_mask(float* gx, const float* gate, int64_t n, void* stream) {
   if(n <= 0)
     return MTKC_OK;
-  relu_mask_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(gx, gate, n);
+  ::mtkc::launch(relu_mask_kernel, grid1d(n, 256), 256, 0, S(stream), gx, gate, n);
   MTKC_POST_LAUNCH("relu_mask_kernel");
   return MTKC_OK;
 }
@@ -365,7 +378,7 @@ int mtkc_mask_blend(float* out, const float* a, const float* b, const float* m, 
                     int64_t cols, void* stream) {
   if(rows * cols <= 0)
     return MTKC_OK;
-  mask_blend_kernel<<<grid1d(rows * cols, 256), 256, 0, S(stream)>>>(out, a, b, m, rows, cols);
+  ::mtkc::launch(mask_blend_kernel, grid1d(rows * cols, 256), 256, 0, S(stream), out, a, b, m, rows, cols);
   MTKC_POST_LAUNCH("mask_blend_kernel");
   return MTKC_OK;
 }
@@ -375,7 +388,7 @@ int mtkc_mask_blend_backward(float* ga, float* gb, const float* go, const float*
                              void* stream) {
   if(rows * cols <= 0)
     return MTKC_OK;
-  mask_blend_bwd_kernel<<<grid1d(rows * cols, 256), 256, 0, S(stream)>>>(
+  ::mtkc::launch(mask_blend_bwd_kernel, grid1d(rows * cols, 256), 256, 0, S(stream), 
       ga, gb, go, m, rows, cols, accumulate_a, accumulate_b);
   MTKC_POST_LAUNCH("mask_blend_bwd_kernel");
   return MTKC_OK;

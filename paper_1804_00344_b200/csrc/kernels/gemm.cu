@@ -40,6 +40,7 @@ struct GemmP {
 };
 
 __global__ void __launch_bounds__(256) gemm_fp32_kernel(GemmP p) {
+  MTKC_PDL_ENTRY();
   __shared__ float As[TK][TM + 1];
   __shared__ float Bs[TK][TN + 1];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -180,7 +181,7 @@ int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
   p.foldBatch = (a->batch > 1 && a->strideC == 0) ? 1 : 0;
   dim3 grid((unsigned)cdiv(a->N, TN), (unsigned)cdiv(a->M, TM),
             p.foldBatch ? 1u : (unsigned)a->batch);
-  gemm_fp32_kernel<<<grid, 256, 0, S(stream)>>>(p);
+  ::mtkc::launch(gemm_fp32_kernel, grid, 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("gemm_fp32_kernel");
   return MTKC_OK;
 }

@@ -227,6 +227,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // PDL: barrier init, TMEM allocation and descriptor prefetch above overlap
+  // the previous kernel's tail; wait for it before any operand is read
+  MTKC_PDL_ENTRY();
   const uint32_t tmem = *tmemSlot;
   const int tilesPerSplit = p.mt * p.nt;
 
@@ -505,6 +508,7 @@ template <bool VEC>
 __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t M, int64_t N,
                                      float* C, int64_t ldc, float alpha, float beta,
                                      const float* bias, int epi, const float* gate) {
+  MTKC_PDL_ENTRY();
   const int64_t groups = (N + 3) / 4, total = M * groups, plane = M * N;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -639,7 +643,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& m
     attr = true;
   }
   int grid = std::min(p.numTiles, g_sms);
-  kern<<<grid, TC_THREADS, smem, st>>>(ma, mb, mc, mg, p);
+  ::mtkc::launch(kern, grid, TC_THREADS, smem, st, ma, mb, mc, mg, p);
   MTKC_POST_LAUNCH("gemm_tf32_tc_kernel");
   return MTKC_OK;
 }
@@ -775,10 +779,10 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
                      (uintptr_t)a.workspace % 16 == 0;
     const unsigned grid = grid1d(a.M * cdiv(a.N, 4), 256);
     if(vec)
-      splitk_reduce_kernel<true><<<grid, 256, 0, st>>>(a.workspace, splits, a.M, a.N, a.C, a.ldc,
+      ::mtkc::launch(splitk_reduce_kernel<true>, grid, 256, 0, st, a.workspace, splits, a.M, a.N, a.C, a.ldc,
                                                         a.alpha, a.beta, a.bias, a.epilogue, a.gate);
     else
-      splitk_reduce_kernel<false><<<grid, 256, 0, st>>>(a.workspace, splits, a.M, a.N, a.C,
+      ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, a.workspace, splits, a.M, a.N, a.C,
                                                          a.ldc, a.alpha, a.beta, a.bias,
                                                          a.epilogue, a.gate);
     count_launch();

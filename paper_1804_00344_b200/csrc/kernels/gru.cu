@@ -34,6 +34,7 @@ __device__ __forceinline__ void block_sums(float (&v)[NQ], float* red) {
 __device__ __forceinline__ float sigm(float a) { return 1.f / (1.f + expf(-a)); }
 
 __global__ void __launch_bounds__(GT) gru_fwd_kernel(mtkc_gru_args p) {
+  MTKC_PDL_ENTRY();
   __shared__ float red[6 * 32];
   const int64_t r = blockIdx.x, d = p.d;
   const bool hasX = p.xw != nullptr, ln = p.lnGz != nullptr;
@@ -115,6 +116,7 @@ __device__ __forceinline__ float ln_dx(float dy, float g, float xh, float rs, fl
 }
 
 __global__ void __launch_bounds__(GT) gru_bwd_kernel(mtkc_gru_args p) {
+  MTKC_PDL_ENTRY();
   __shared__ float red[6 * 32];
   const int64_t r = blockIdx.x, d = p.d;
   const bool hasX = p.xw != nullptr, ln = p.lnGz != nullptr;
@@ -193,7 +195,7 @@ int mtkc_gru_forward(const mtkc_gru_args* a, void* stream) {
   if(a->d > (int64_t)GT * GV)
     return fail(MTKC_DIMENSION, "gru: state dim above 2048");
   ProfScope prof(S(stream), "gru", 4.0 * a->b * a->d * 10);
-  gru_fwd_kernel<<<(unsigned)a->b, GT, 0, S(stream)>>>(*a);
+  ::mtkc::launch(gru_fwd_kernel, (unsigned)a->b, GT, 0, S(stream), *a);
   MTKC_POST_LAUNCH("gru_fwd_kernel");
   return MTKC_OK;
 }
@@ -204,7 +206,7 @@ int mtkc_gru_backward(const mtkc_gru_args* a, void* stream) {
   if(a->d > (int64_t)GT * GV)
     return fail(MTKC_DIMENSION, "gru: state dim above 2048");
   ProfScope prof(S(stream), "gru", 4.0 * a->b * a->d * 14);
-  gru_bwd_kernel<<<(unsigned)a->b, GT, 0, S(stream)>>>(*a);
+  ::mtkc::launch(gru_bwd_kernel, (unsigned)a->b, GT, 0, S(stream), *a);
   MTKC_POST_LAUNCH("gru_bwd_kernel");
   return MTKC_OK;
 }

@@ -23,6 +23,7 @@ template <int V>
 __global__ void __launch_bounds__(LN_WARPS * 32)
     ln_fwd_kernel(float* out, const float* x, const float* g, const float* b, float eps,
                   float* invStd, float* xhat, int64_t rows, int64_t d) {
+  MTKC_PDL_ENTRY();
   int64_t row = blockIdx.x * (int64_t)LN_WARPS + (threadIdx.x >> 5);
   int lane = threadIdx.x & 31;
   if(row >= rows)
@@ -90,6 +91,7 @@ template <int V>
 __global__ void __launch_bounds__(LN_WARPS * 32)
     ln_bwd_dx_kernel(const float* dy, const float* g, const float* invStd, const float* xhat,
                      float* dx, int64_t rows, int64_t d, int accDx) {
+  MTKC_PDL_ENTRY();
   int64_t row = blockIdx.x * (int64_t)LN_WARPS + (threadIdx.x >> 5);
   int lane = threadIdx.x & 31;
   if(row >= rows)
@@ -141,6 +143,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32)
 // no-workspace fallback: one thread per column over all rows
 __global__ void ln_param_direct_kernel(const float* dy, const float* xhat, float* dgain,
                                        float* dbias, int64_t rows, int64_t d, int acc) {
+  MTKC_PDL_ENTRY();
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if(j >= d)
     return;
@@ -168,6 +171,7 @@ template <int NV>
 __global__ void __launch_bounds__(LN_WARPS * 32)
     ln_fwd4_kernel(float* out, const float* x, const float* g, const float* b, float eps,
                    float* mean, float* invStd, int64_t rows, int64_t d) {
+  MTKC_PDL_ENTRY();
   const int64_t row = blockIdx.x * (int64_t)LN_WARPS + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if(row >= rows)
@@ -220,6 +224,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32)
     ln_bwd4_kernel(const float* dy, const float* x, const float* g, const float* mean,
                    const float* invStd, float* dx, float* part, int64_t rows, int64_t d,
                    int64_t rowsPerCta, int accDx) {
+  MTKC_PDL_ENTRY();
   extern __shared__ float4 red4[];  // [LN_WARPS][2][d/4] (param partials only)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4 gg[NV], sg[NV], sb[NV];
@@ -335,19 +340,19 @@ void launch_v(int64_t d, dim3 grid, cudaStream_t st, Args... args);
   do {                                                                       \
     int v_ = (int)cdiv(d, 32);                                               \
     if(v_ <= 1)                                                              \
-      KERNEL<1><<<grid, LN_WARPS * 32, 0, st>>>(__VA_ARGS__);                \
+      ::mtkc::launch(KERNEL<1>, grid, LN_WARPS * 32, 0, st, __VA_ARGS__);                \
     else if(v_ <= 2)                                                         \
-      KERNEL<2><<<grid, LN_WARPS * 32, 0, st>>>(__VA_ARGS__);                \
+      ::mtkc::launch(KERNEL<2>, grid, LN_WARPS * 32, 0, st, __VA_ARGS__);                \
     else if(v_ <= 4)                                                         \
-      KERNEL<4><<<grid, LN_WARPS * 32, 0, st>>>(__VA_ARGS__);                \
+      ::mtkc::launch(KERNEL<4>, grid, LN_WARPS * 32, 0, st, __VA_ARGS__);                \
     else if(v_ <= 8)                                                         \
-      KERNEL<8><<<grid, LN_WARPS * 32, 0, st>>>(__VA_ARGS__);                \
+      ::mtkc::launch(KERNEL<8>, grid, LN_WARPS * 32, 0, st, __VA_ARGS__);                \
     else if(v_ <= 16)                                                        \
-      KERNEL<16><<<grid, LN_WARPS * 32, 0, st>>>(__VA_ARGS__);               \
+      ::mtkc::launch(KERNEL<16>, grid, LN_WARPS * 32, 0, st, __VA_ARGS__);               \
     else if(v_ <= 32)                                                        \
-      KERNEL<32><<<grid, LN_WARPS * 32, 0, st>>>(__VA_ARGS__);               \
+      ::mtkc::launch(KERNEL<32>, grid, LN_WARPS * 32, 0, st, __VA_ARGS__);               \
     else                                                                     \
-      KERNEL<0><<<grid, LN_WARPS * 32, 0, st>>>(__VA_ARGS__);                \
+      ::mtkc::launch(KERNEL<0>, grid, LN_WARPS * 32, 0, st, __VA_ARGS__);                \
   } while(0)
 
 }  // namespace
@@ -384,14 +389,14 @@ int mtkc_layernorm_backward(const float* dy, const float* gain, const float* inv
     return MTKC_OK;
   if(workspace && workspace_bytes >= colred_workspace_bytes(2, rows, d)) {
     int64_t nblk = cdiv(rows, CR_ROWS);
-    colred_partial_kernel<2><<<dim3((unsigned)cdiv(d, CR_COLS), (unsigned)nblk), 256, 0, st>>>(
+    ::mtkc::launch(colred_partial_kernel<2>, dim3((unsigned)cdiv(d, CR_COLS), (unsigned)nblk), 256, 0, st, 
         workspace, dy, xhat, rows, d);
     MTKC_POST_LAUNCH("colred_partial_kernel");
-    colred_final_kernel<2><<<colred_final_grid(d), 256, 0, st>>>(dgain, dbias, workspace, nblk,
+    ::mtkc::launch(colred_final_kernel<2>, colred_final_grid(d), 256, 0, st, dgain, dbias, workspace, nblk,
                                                                   d, accumulate_params);
     MTKC_POST_LAUNCH("colred_final_kernel");
   } else {
-    ln_param_direct_kernel<<<(unsigned)cdiv(d, 128), 128, 0, st>>>(dy, xhat, dgain, dbias, rows,
+    ::mtkc::launch(ln_param_direct_kernel, (unsigned)cdiv(d, 128), 128, 0, st, dy, xhat, dgain, dbias, rows,
                                                                    d, accumulate_params);
     MTKC_POST_LAUNCH("ln_param_direct_kernel");
   }
@@ -416,7 +421,7 @@ int mtkc_layernorm_stats(float* out, const float* x, const float* gain, const fl
   const int nv = (int)cdiv(d, 128);
 #define LN4_FWD(NVV)                                                                   \
   if(nv <= NVV) {                                                                      \
-    ln_fwd4_kernel<NVV><<<grid, LN_WARPS * 32, 0, st>>>(out, x, gain, bias, eps, mean, \
+    ::mtkc::launch(ln_fwd4_kernel<NVV>, grid, LN_WARPS * 32, 0, st, out, x, gain, bias, eps, mean, \
                                                         inv_std, rows, d);              \
   } else
   LN4_FWD(1) LN4_FWD(2) LN4_FWD(4) LN4_FWD(8) {}
@@ -460,14 +465,14 @@ int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* 
     if(smem > 48 * 1024)                                                                     \
       cudaFuncSetAttribute(ln_bwd4_kernel<NVV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)smem);                                                       \
-    ln_bwd4_kernel<NVV><<<(unsigned)nblk, LN_WARPS * 32, smem, st>>>(                        \
+    ::mtkc::launch(ln_bwd4_kernel<NVV>, (unsigned)nblk, LN_WARPS * 32, smem, st,                         \
         dy, x, gain, mean, inv_std, dx, part, rows, d, rpc, accumulate_dx);                  \
   } else
   LN4_BWD(1) LN4_BWD(2) LN4_BWD(4) LN4_BWD(8) {}
 #undef LN4_BWD
   MTKC_POST_LAUNCH("ln_bwd4_kernel");
   if(part) {
-    colred_final_kernel<2><<<colred_final_grid(d), 256, 0, st>>>(dgain, dbias, part, nblk, d,
+    ::mtkc::launch(colred_final_kernel<2>, colred_final_grid(d), 256, 0, st, dgain, dbias, part, nblk, d,
                                                                   accumulate_params);
     MTKC_POST_LAUNCH("colred_final_kernel");
   }

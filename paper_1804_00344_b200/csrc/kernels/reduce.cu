@@ -10,6 +10,7 @@ namespace {
 
 __global__ void reduce_kernel(int op, float* out, const float* in, int64_t outer, int64_t n,
                               int64_t inner) {
+  MTKC_PDL_ENTRY();
   int64_t total = outer * inner;
   for(int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
       t += (int64_t)gridDim.x * blockDim.x) {
@@ -42,6 +43,7 @@ __global__ void reduce_kernel(int op, float* out, const float* in, int64_t outer
 
 __global__ void reduce_bwd_kernel(int op, float* gin, const float* gout, const float* in,
                                   int64_t outer, int64_t n, int64_t inner) {
+  MTKC_PDL_ENTRY();
   int64_t total = outer * inner;
   for(int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
       t += (int64_t)gridDim.x * blockDim.x) {
@@ -71,6 +73,7 @@ constexpr int CS_ROWS = 128;  // below this many rows a single pass is used
 // single-level variant (no workspace): one thread per column walks all rows
 __global__ void colsum_direct_kernel(float* out, const float* in, int64_t rows, int64_t cols,
                                      int accumulate) {
+  MTKC_PDL_ENTRY();
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if(c >= cols)
     return;
@@ -90,6 +93,7 @@ __device__ unsigned int g_colsum_ticket[CS_MAX_SLABS];
 __global__ void __launch_bounds__(256) colsum_onepass_kernel(float* out, float* part,
                                                              const float* a, int64_t rows,
                                                              int64_t cols, int acc) {
+  MTKC_PDL_ENTRY();
   __shared__ float4 red[8][32];
   __shared__ bool last;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -164,6 +168,7 @@ __global__ void __launch_bounds__(256) colsum_onepass_kernel(float* out, float* 
 }
 
 __global__ void finite_kernel(const float* in, int64_t n, int* flags) {
+  MTKC_PDL_ENTRY();
   bool bad = false;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x)
@@ -173,6 +178,7 @@ __global__ void finite_kernel(const float* in, int64_t n, int* flags) {
 }
 
 __global__ void finite4_kernel(const float4* in, int64_t n4, int* flags) {
+  MTKC_PDL_ENTRY();
   bool bad = false;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -191,7 +197,7 @@ int mtkc_reduce(int op, float* out, const float* in, int64_t outer, int64_t n, i
                 void* stream) {
   if(outer * inner <= 0 || n <= 0)
     return MTKC_OK;
-  reduce_kernel<<<grid1d(outer * inner, 128), 128, 0, S(stream)>>>(op, out, in, outer, n, inner);
+  ::mtkc::launch(reduce_kernel, grid1d(outer * inner, 128), 128, 0, S(stream), op, out, in, outer, n, inner);
   MTKC_POST_LAUNCH("reduce_kernel");
   return MTKC_OK;
 }
@@ -200,7 +206,7 @@ int mtkc_reduce_backward(int op, float* gin, const float* gout, const float* in,
                          int64_t outer, int64_t n, int64_t inner, void* stream) {
   if(op == MTKC_RARGMAX || outer * inner <= 0)
     return MTKC_OK;
-  reduce_bwd_kernel<<<grid1d(outer * inner, 128), 128, 0, S(stream)>>>(op, gin, gout, in, outer,
+  ::mtkc::launch(reduce_bwd_kernel, grid1d(outer * inner, 128), 128, 0, S(stream), op, gin, gout, in, outer,
                                                                        n, inner);
   MTKC_POST_LAUNCH("reduce_bwd_kernel");
   return MTKC_OK;
@@ -214,7 +220,7 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
   if(prof_detail())
     prof.detail = "r" + std::to_string(rows) + "_c" + std::to_string(cols);
   if(rows <= CS_ROWS || !workspace || workspace_bytes < colred_workspace_bytes(1, rows, cols)) {
-    colsum_direct_kernel<<<(unsigned)cdiv(cols, 128), 128, 0, S(stream)>>>(out, in, rows, cols,
+    ::mtkc::launch(colsum_direct_kernel, (unsigned)cdiv(cols, 128), 128, 0, S(stream), out, in, rows, cols,
                                                                           accumulate);
     MTKC_POST_LAUNCH("colsum_direct_kernel");
     return MTKC_OK;
@@ -222,15 +228,15 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
   int64_t nblk = cdiv(rows, CR_ROWS);
   if(cols % 4 == 0 && cdiv(cols, CR_COLS) <= CS_MAX_SLABS && nblk <= 65535 &&
      ((uintptr_t)in | (uintptr_t)out | (uintptr_t)workspace) % 16 == 0) {
-    colsum_onepass_kernel<<<dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
-                            S(stream)>>>(out, workspace, in, rows, cols, accumulate);
+    ::mtkc::launch(colsum_onepass_kernel, dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
+                            S(stream), out, workspace, in, rows, cols, accumulate);
     MTKC_POST_LAUNCH("colsum_onepass_kernel");
     return MTKC_OK;
   }
-  colred_partial_kernel<1><<<dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
-                             S(stream)>>>(workspace, in, nullptr, rows, cols);
+  ::mtkc::launch(colred_partial_kernel<1>, dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
+                             S(stream), workspace, in, nullptr, rows, cols);
   MTKC_POST_LAUNCH("colred_partial_kernel");
-  colred_final_kernel<1><<<colred_final_grid(cols), 256, 0, S(stream)>>>(
+  ::mtkc::launch(colred_final_kernel<1>, colred_final_grid(cols), 256, 0, S(stream), 
       out, nullptr, workspace, nblk, cols, accumulate);
   MTKC_POST_LAUNCH("colred_final_kernel");
   return MTKC_OK;
@@ -240,10 +246,10 @@ int mtkc_check_finite(const float* in, int64_t n, int* flags, void* stream) {
   if(n <= 0)
     return MTKC_OK;
   if(n % 4 == 0 && (uintptr_t)in % 16 == 0)
-    finite4_kernel<<<grid1d(n / 4, 256, 148 * 8), 256, 0, S(stream)>>>((const float4*)in, n / 4,
+    ::mtkc::launch(finite4_kernel, grid1d(n / 4, 256, 148 * 8), 256, 0, S(stream), (const float4*)in, n / 4,
                                                                       flags);
   else
-    finite_kernel<<<grid1d(n, 256, 148 * 8), 256, 0, S(stream)>>>(in, n, flags);
+    ::mtkc::launch(finite_kernel, grid1d(n, 256, 148 * 8), 256, 0, S(stream), in, n, flags);
   MTKC_POST_LAUNCH("finite_kernel");
   return MTKC_OK;
 }

@@ -32,6 +32,11 @@ int cuda_status(cudaError_t e, const char* where) {
   return MTKC_CUDA;
 }
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("MTK_NO_PDL") == nullptr;
+  return on;
+}
+
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
 static std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
@@ -120,6 +125,7 @@ uint64_t mtkc_h2d_bytes(void) { return g_h2d.load(); }
 uint64_t mtkc_d2h_bytes(void) { return g_d2h.load(); }
 
 __global__ void sleep_kernel(int64_t ns) {
+  MTKC_PDL_ENTRY();
   int64_t t0 = (int64_t)clock64();
   (void)t0;
   uint64_t start;
@@ -134,7 +140,7 @@ __global__ void sleep_kernel(int64_t ns) {
 }
 
 int mtkc_gpu_sleep(int64_t us, void* stream) {
-  sleep_kernel<<<1, 1, 0, S(stream)>>>(us * 1000);
+  ::mtkc::launch(sleep_kernel, 1, 1, 0, S(stream), us * 1000);
   return cuda_status(cudaGetLastError(), "sleep_kernel");
 }
 

@@ -22,6 +22,7 @@ struct SmP {
 // One warp per row.  Two passes over the row like the reference: max over
 // unmasked entries, then sum of exp(x - max) over unmasked entries.
 __global__ void softmax_kernel(SmP p) {
+  MTKC_PDL_ENTRY();
   int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
   int lane = threadIdx.x & 31;
   if(row >= p.rows)
@@ -69,6 +70,7 @@ __global__ void softmax_kernel(SmP p) {
 // dx += y * (g - sum(g*y))  (graph.cpp:539-552)
 __global__ void softmax_bwd_kernel(float* gx, const float* y, const float* go, int64_t rows,
                                    int64_t cols) {
+  MTKC_PDL_ENTRY();
   int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
   int lane = threadIdx.x & 31;
   if(row >= rows)
@@ -94,6 +96,7 @@ struct TrP {
 };
 
 __global__ void transpose_kernel(TrP p) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n;
       i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = i;
@@ -111,6 +114,7 @@ __global__ void transpose_kernel(TrP p) {
 __global__ void copy_blocks_kernel(float* dst, int64_t dstStride, int64_t dstOff,
                                    const float* src, int64_t srcStride, int64_t srcOff,
                                    int64_t outer, int64_t len, int acc) {
+  MTKC_PDL_ENTRY();
   int64_t n = outer * len;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -123,6 +127,7 @@ __global__ void copy_blocks_kernel(float* dst, int64_t dstStride, int64_t dstOff
 
 __global__ void gather_rows_kernel(float* out, const float* src, const int32_t* rows, int64_t n,
                                    int64_t cols, int64_t srcRows, int* flags) {
+  MTKC_PDL_ENTRY();
   int64_t total = n * cols;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -143,6 +148,7 @@ __global__ void gather_rows_kernel(float* out, const float* src, const int32_t* 
 __global__ void scatter_add_kernel(float* out, const float* src, const int32_t* perm,
                                    const int32_t* seg, const int32_t* uniq, int64_t cols,
                                    float scale) {
+  MTKC_PDL_ENTRY();
   int64_t u = blockIdx.x;
   int64_t id = uniq[u];
   int32_t s0 = seg[u], s1 = seg[u + 1];
@@ -164,6 +170,7 @@ __global__ void scatter_chunk_kernel(float* out, const float* src, const int32_t
                                      const int32_t* cstart, const int32_t* crow,
                                      const int32_t* cslot, float* partial, int64_t cols,
                                      float scale) {
+  MTKC_PDL_ENTRY();
   int64_t c = blockIdx.x;
   int32_t k0 = cstart[c], k1 = cstart[c + 1];
   int32_t slot = cslot[c];
@@ -195,6 +202,7 @@ __global__ void scatter_chunk_kernel(float* out, const float* src, const int32_t
 
 __global__ void scatter_multi_kernel(float* out, const float* partial, const int32_t* mfirst,
                                      const int32_t* mrow, int64_t cols) {
+  MTKC_PDL_ENTRY();
   int64_t m = blockIdx.x;
   float* dst = out + (int64_t)mrow[m] * cols;
   for(int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
@@ -209,6 +217,7 @@ __global__ void scatter_multi_kernel(float* out, const float* partial, const int
 __global__ void embed_kernel(float* out, const float* table, const int32_t* ids, int64_t n,
                              int64_t e, int64_t vocab, float s, const float* pe, int64_t t,
                              int* flags) {
+  MTKC_PDL_ENTRY();
   int64_t total = n * e;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -232,6 +241,7 @@ __global__ void embed_kernel(float* out, const float* table, const int32_t* ids,
 __global__ void embed4_kernel(float4* out, const float4* table, const int32_t* ids, int64_t n,
                               int64_t e4, int64_t vocab, float s, const float4* pe, int64_t t,
                               int* flags) {
+  MTKC_PDL_ENTRY();
   int64_t total = n * e4;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -290,7 +300,7 @@ int mtkc_softmax(float* out, const float* x, const int64_t xd[4], const float* m
   p.flags = flags;
   if(p.rows <= 0)
     return MTKC_OK;
-  softmax_kernel<<<(unsigned)cdiv(p.rows, 8), 256, 0, S(stream)>>>(p);
+  ::mtkc::launch(softmax_kernel, (unsigned)cdiv(p.rows, 8), 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("softmax_kernel");
   return MTKC_OK;
 }
@@ -299,7 +309,7 @@ int mtkc_softmax_backward(float* gx, const float* y, const float* go, int64_t ro
                           int64_t cols, void* stream) {
   if(rows <= 0)
     return MTKC_OK;
-  softmax_bwd_kernel<<<(unsigned)cdiv(rows, 8), 256, 0, S(stream)>>>(gx, y, go, rows, cols);
+  ::mtkc::launch(softmax_bwd_kernel, (unsigned)cdiv(rows, 8), 256, 0, S(stream), gx, y, go, rows, cols);
   MTKC_POST_LAUNCH("softmax_bwd_kernel");
   return MTKC_OK;
 }
@@ -322,7 +332,7 @@ int mtkc_transpose(float* out, const float* src, const int64_t sd[4], const int 
   p.acc = accumulate;
   if(p.n <= 0)
     return MTKC_OK;
-  transpose_kernel<<<grid1d(p.n, 256), 256, 0, S(stream)>>>(p);
+  ::mtkc::launch(transpose_kernel, grid1d(p.n, 256), 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("transpose_kernel");
   return MTKC_OK;
 }
@@ -332,7 +342,7 @@ int mtkc_copy_blocks(float* dst, int64_t dst_stride, int64_t dst_off, const floa
                      int accumulate, void* stream) {
   if(outer * len <= 0)
     return MTKC_OK;
-  copy_blocks_kernel<<<grid1d(outer * len, 256), 256, 0, S(stream)>>>(
+  ::mtkc::launch(copy_blocks_kernel, grid1d(outer * len, 256), 256, 0, S(stream), 
       dst, dst_stride, dst_off, src, src_stride, src_off, outer, len, accumulate);
   MTKC_POST_LAUNCH("copy_blocks_kernel");
   return MTKC_OK;
@@ -342,7 +352,7 @@ int mtkc_gather_rows(float* out, const float* src, const int32_t* rows, int64_t 
                      int64_t cols, int64_t src_rows, int* flags, void* stream) {
   if(n * cols <= 0)
     return MTKC_OK;
-  gather_rows_kernel<<<grid1d(n * cols, 256), 256, 0, S(stream)>>>(out, src, rows, n, cols,
+  ::mtkc::launch(gather_rows_kernel, grid1d(n * cols, 256), 256, 0, S(stream), out, src, rows, n, cols,
                                                                   src_rows, flags);
   MTKC_POST_LAUNCH("gather_rows_kernel");
   return MTKC_OK;
@@ -354,7 +364,7 @@ int mtkc_scatter_add_rows(float* out, const float* src, const int32_t* perm,
   if(n_uniq <= 0 || cols <= 0)
     return MTKC_OK;
   int threads = cols >= 256 ? 256 : (int)((cols + 31) / 32 * 32);
-  scatter_add_kernel<<<(unsigned)n_uniq, threads, 0, S(stream)>>>(out, src, perm, seg_start,
+  ::mtkc::launch(scatter_add_kernel, (unsigned)n_uniq, threads, 0, S(stream), out, src, perm, seg_start,
                                                                   uniq, cols, scale);
   MTKC_POST_LAUNCH("scatter_add_kernel");
   return MTKC_OK;
@@ -369,11 +379,11 @@ int mtkc_scatter_add_rows_chunked(float* out, const float* src, const int32_t* p
   if(n_chunks <= 0 || cols <= 0)
     return MTKC_OK;
   int threads = cols >= 512 ? 512 : (int)((cols + 31) / 32 * 32);
-  scatter_chunk_kernel<<<(unsigned)n_chunks, threads, 0, S(stream)>>>(
+  ::mtkc::launch(scatter_chunk_kernel, (unsigned)n_chunks, threads, 0, S(stream), 
       out, src, perm, chunk_start, chunk_row, chunk_slot, partial, cols, scale);
   MTKC_POST_LAUNCH("scatter_chunk_kernel");
   if(n_multi > 0) {
-    scatter_multi_kernel<<<(unsigned)n_multi, threads, 0, S(stream)>>>(out, partial, multi_first,
+    ::mtkc::launch(scatter_multi_kernel, (unsigned)n_multi, threads, 0, S(stream), out, partial, multi_first,
                                                                        multi_row, cols);
     MTKC_POST_LAUNCH("scatter_multi_kernel");
   }
@@ -389,10 +399,10 @@ int mtkc_embed(float* out, const float* table, const int32_t* ids, int64_t n, in
   bool vec = e % 4 == 0 && (uintptr_t)out % 16 == 0 && (uintptr_t)table % 16 == 0 &&
              (!pe || (uintptr_t)pe % 16 == 0);
   if(vec)
-    embed4_kernel<<<grid1d(n * e / 4, 256), 256, 0, S(stream)>>>(
+    ::mtkc::launch(embed4_kernel, grid1d(n * e / 4, 256), 256, 0, S(stream), 
         (float4*)out, (const float4*)table, ids, n, e / 4, vocab, s, (const float4*)pe, t, flags);
   else
-    embed_kernel<<<grid1d(n * e, 256), 256, 0, S(stream)>>>(out, table, ids, n, e, vocab, s, pe,
+    ::mtkc::launch(embed_kernel, grid1d(n * e, 256), 256, 0, S(stream), out, table, ids, n, e, vocab, s, pe,
                                                            t, flags);
   MTKC_POST_LAUNCH("embed_kernel");
   return MTKC_OK;

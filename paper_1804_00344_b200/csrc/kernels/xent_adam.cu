@@ -20,6 +20,7 @@ constexpr int XT = 512;
 __global__ void __launch_bounds__(XT) xent_fwd_kernel(const float* logits, const int32_t* tg,
                                                       const float* mask, int64_t V,
                                                       float* stats, float* rowLoss) {
+  MTKC_PDL_ENTRY();
   __shared__ float red[32];
   int64_t r = blockIdx.x;
   const float* x = logits + r * V;
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(XT) xent_fwd_kernel(const float* logits, const
 // loss = sum(row_loss)/count, fixed-order block reduction
 __global__ void __launch_bounds__(1024) loss_sum_kernel(const float* rowLoss, int64_t rows,
                                                         float count, float* loss) {
+  MTKC_PDL_ENTRY();
   __shared__ float red[32];
   float s = 0.f;
   for(int64_t r = threadIdx.x; r < rows; r += blockDim.x)
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(256) xent_bwd_kernel(float* g, const float* lo
                                                        const float* mask, const float* gloss,
                                                        int64_t rows, int64_t V, float count,
                                                        int acc) {
+  MTKC_PDL_ENTRY();
   int64_t r = blockIdx.y;
   float go = gloss[0] / count;
   float m = mask ? mask[r] : 1.f;
@@ -141,6 +144,7 @@ __device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v
 __global__ void adam_ema_kernel(float* th, float* g, float* m, float* v, float* a, int64_t n,
                                 float lr, float b1, float b2, float eps, float c1, float c2,
                                 float ab, int doAvg, int zg, const int* flags) {
+  MTKC_PDL_ENTRY();
   if(flags && (*flags & MTKC_FLAG_NONFINITE))
     return;  // all-or-nothing (train.cpp:51-53)
   int64_t n4 = n / 4;
@@ -174,6 +178,7 @@ __global__ void adam_ema_kernel(float* th, float* g, float* m, float* v, float* 
 }
 
 __global__ void ema_kernel(float* a, const float* th, int64_t n, float b) {
+  MTKC_PDL_ENTRY();
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x)
     a[i] = b * a[i] + (1.f - b) * th[i];
@@ -186,7 +191,7 @@ extern "C" {
 int mtkc_ema(float* avg, const float* theta, int64_t n, float beta, void* stream) {
   if(n <= 0)
     return MTKC_OK;
-  ema_kernel<<<grid1d(n, 256), 256, 0, S(stream)>>>(avg, theta, n, beta);
+  ::mtkc::launch(ema_kernel, grid1d(n, 256), 256, 0, S(stream), avg, theta, n, beta);
   MTKC_POST_LAUNCH("ema_kernel");
   return MTKC_OK;
 }
@@ -197,10 +202,10 @@ int mtkc_xent_forward(const float* logits, const int32_t* targets, const float* 
   if(rows <= 0)
     return MTKC_OK;
   ProfScope prof(S(stream), "xent", 4.0 * rows * vocab);  // read logits
-  xent_fwd_kernel<<<(unsigned)rows, XT, 0, S(stream)>>>(logits, targets, mask, vocab, lse,
+  ::mtkc::launch(xent_fwd_kernel, (unsigned)rows, XT, 0, S(stream), logits, targets, mask, vocab, lse,
                                                        row_loss);
   MTKC_POST_LAUNCH("xent_fwd_kernel");
-  loss_sum_kernel<<<1, 1024, 0, S(stream)>>>(row_loss, rows, count, loss);
+  ::mtkc::launch(loss_sum_kernel, 1, 1024, 0, S(stream), row_loss, rows, count, loss);
   MTKC_POST_LAUNCH("loss_sum_kernel");
   return MTKC_OK;
 }
@@ -215,7 +220,7 @@ int mtkc_xent_backward(float* glogits, const float* logits, const float* lse,
   int64_t per = cdiv(vocab, 4);
   unsigned gx = (unsigned)std::min<int64_t>(cdiv(per, 256), 8);
   dim3 grid(gx, (unsigned)rows);
-  xent_bwd_kernel<<<grid, 256, 0, S(stream)>>>(glogits, logits, lse, targets, mask, gloss, rows,
+  ::mtkc::launch(xent_bwd_kernel, grid, 256, 0, S(stream), glogits, logits, lse, targets, mask, gloss, rows,
                                               vocab, count, accumulate);
   MTKC_POST_LAUNCH("xent_bwd_kernel");
   return MTKC_OK;
@@ -230,7 +235,7 @@ int mtkc_adam_ema(float* theta, float* grad, float* m, float* v, float* avg, int
       (do_avg ? (uintptr_t)avg : 0)) % 16)
     return fail(MTKC_CONTRACT, "adam: buffers must be 16-byte aligned");
   ProfScope prof(S(stream), "adam_ema", (do_avg ? 36.0 : 28.0) * n);
-  adam_ema_kernel<<<grid1d(cdiv(n, 4), 256, 148 * 16), 256, 0, S(stream)>>>(
+  ::mtkc::launch(adam_ema_kernel, grid1d(cdiv(n, 4), 256, 148 * 16), 256, 0, S(stream), 
       theta, grad, m, v, avg, n, lr, beta1, beta2, eps, corr1, corr2, avg_beta, do_avg,
       zero_grad, flags);
   MTKC_POST_LAUNCH("adam_ema_kernel");
