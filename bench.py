@@ -30,7 +30,7 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, ROOT)
+sys.path.insert(0, os.environ.get("MTK_PKG_ROOT") or ROOT)
 
 METRIC = "target words/sec, Transformer-base training step at 1/2/4/8 B200"
 DATA = "synthetic: SURVEY.md 8(d) splitmix64 corpus, lengths 16..32+</s>, ids uniform in [2,V)"

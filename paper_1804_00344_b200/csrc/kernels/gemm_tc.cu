@@ -384,16 +384,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               ++ldPhase;
             }
             grow += lane * 32;
-            // alpha, bias (one coalesced load per lane, broadcast by shuffles), ReLU
-            const float bl = (p.bias && col0 + lane < p.N) ? p.bias[col0 + lane] : 0.f;
+            // alpha, bias, ReLU.  Full aligned chunks read the 32 bias values
+            // as 8 same-address float4 loads (one broadcast transaction each);
+            // ragged chunks use one load per lane broadcast by shuffles.
+            if(p.alpha != 1.f) {
 #pragma unroll
-            for(int i = 0; i < 32; ++i) {
-              float x = p.alpha == 1.f ? v[i] : p.alpha * v[i];
-              if(p.bias)
-                x = x + __shfl_sync(0xffffffffu, bl, i);
-              if(p.epi == MTKC_EPI_RELU)
-                x = x > 0.f ? x : 0.f;
-              v[i] = x;
+              for(int i = 0; i < 32; ++i)
+                v[i] = p.alpha * v[i];
+            }
+            if(p.bias) {
+              if(col0 + 32 <= p.N && ((uintptr_t)(p.bias + col0) & 15) == 0) {
+                const float4* b4p = reinterpret_cast<const float4*>(p.bias + col0);
+#pragma unroll
+                for(int j = 0; j < 8; ++j) {
+                  const float4 b4 = __ldg(b4p + j);
+                  v[4 * j] = v[4 * j] + b4.x;
+                  v[4 * j + 1] = v[4 * j + 1] + b4.y;
+                  v[4 * j + 2] = v[4 * j + 2] + b4.z;
+                  v[4 * j + 3] = v[4 * j + 3] + b4.w;
+                }
+              } else {
+                const float bl = col0 + lane < p.N ? p.bias[col0 + lane] : 0.f;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                  v[i] = v[i] + __shfl_sync(0xffffffffu, bl, i);
+              }
+            }
+            if(p.epi == MTKC_EPI_RELU) {
+#pragma unroll
+              for(int i = 0; i < 32; ++i)
+                v[i] = v[i] > 0.f ? v[i] : 0.f;
             }
             // ReLU gate, then beta*C, from the TMA-loaded boxes (straight-line
             // loops under uniform branches)
