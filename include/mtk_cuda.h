@@ -258,7 +258,7 @@ int mtkc_layernorm_backward(const float* dy, const float* gain, const float* inv
                             int64_t rows, int64_t d, int accumulate_dx, int accumulate_params,
                             float* workspace, size_t workspace_bytes, void* stream);
 
-/* Vectorised variant (d % 4 == 0, d <= 2048, 16-byte aligned rows): the    */
+/* Vectorised variant (d % 4 == 0, d <= 1024, 16-byte aligned rows): the    */
 /* forward caches only mean/inv_std per row (no xhat tensor); the backward  */
 /* recomputes xhat from x and fuses the dgain/dbias column reductions into  */
 /* the dx pass (deterministic; workspace >= ..._workspace_bytes).           */
@@ -400,6 +400,7 @@ typedef struct mtkc_bahdanau_args {
   float* gv_part;      /* [b x a] */
   float* glnG_part;    /* [b x a] (LN only) */
   float* glnB_part;    /* [b x a] (LN only) */
+  float* scratch;      /* [4 x b x s] workspace (scores; dw, de, LN row stats) */
 } mtkc_bahdanau_args;
 
 int mtkc_bahdanau_forward(const mtkc_bahdanau_args* a, void* stream);

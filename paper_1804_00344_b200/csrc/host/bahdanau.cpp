@@ -85,6 +85,8 @@ std::pair<NodeRef, NodeRef> ExpressionGraph::bahdanau(NodeRef wq, NodeRef uk, No
     p.w = aux->w.dev();
     p.ctx = n.value.dev();
     p.flags = Device::get().flags();
+    Tensor scratch = g.allocTensor(Shape({4, b, s}));
+    p.scratch = scratch.dev();
     MTKC(mtkc_bahdanau_forward(&p, stream()));
     if(aux->weightsNode >= 0)
       g.node(aux->weightsNode).value = aux->w;
@@ -121,6 +123,8 @@ std::pair<NodeRef, NodeRef> ExpressionGraph::bahdanau(NodeRef wq, NodeRef uk, No
       p.glnG_part = p.gv_part + b * a;
       p.glnB_part = p.gv_part + 2 * b * a;
     }
+    Tensor scratch = g.allocTensor(Shape({4, b, s}));
+    p.scratch = scratch.dev();
     MTKC(mtkc_bahdanau_backward(&p, stream()));
     Device& dev = Device::get();
     size_t ws = (size_t)((b + 63) / 64 + 1) * (size_t)a * sizeof(float) * 2;

@@ -717,9 +717,12 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
   // grid, tiles*s / (SMs * ceil(tiles*s / SMs)); ties go to fewer splits.
   int splits = 1;
   const int64_t tiles = mt * nt;
-  if(a.workspace && numKb >= 16) {
+  // Skinny products (RNN time steps: M = batch rows, a handful of tiles)
+  // split down to 4 k-blocks per CTA; otherwise keep >= 24 per split.
+  const int minKb = tiles * 4 <= g_sms ? 4 : 24;
+  if(a.workspace && numKb >= 2 * minKb) {
     double best = (double)tiles / (double)(g_sms * cdiv(tiles, g_sms));
-    for(int s = 2; s <= 16 && numKb / s >= 24; ++s) {
+    for(int s = 2; s <= 16 && numKb / s >= minKb; ++s) {
       size_t need = (size_t)s * (size_t)a.M * (size_t)a.N * sizeof(float);
       if(need > a.workspace_bytes)
         break;

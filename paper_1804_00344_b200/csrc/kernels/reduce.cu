@@ -219,7 +219,10 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
   ProfScope prof(S(stream), "colsum", 4.0 * rows * cols);
   if(prof_detail())
     prof.detail = "r" + std::to_string(rows) + "_c" + std::to_string(cols);
-  if(rows <= CS_ROWS || !workspace || workspace_bytes < colred_workspace_bytes(1, rows, cols)) {
+  const bool onepass = cols % 4 == 0 && rows > 8 && workspace &&
+                       workspace_bytes >= colred_workspace_bytes(1, rows, cols);
+  if(!onepass && (rows <= CS_ROWS || !workspace ||
+                  workspace_bytes < colred_workspace_bytes(1, rows, cols))) {
     ::mtkc::launch(colsum_direct_kernel, (unsigned)cdiv(cols, 128), 128, 0, S(stream), out, in, rows, cols,
                                                                           accumulate);
     MTKC_POST_LAUNCH("colsum_direct_kernel");
