@@ -143,6 +143,14 @@ typedef struct mtkc_gemm_args {
 } mtkc_gemm_args;
 
 int mtkc_gemm(const mtkc_gemm_args* args, void* stream);
+/* A group of products of one shape in one launch (the q/k/v projections of
+ * MultiHeadAttention::apply, layers.cpp:100-108, share the input x):
+ * kconcat = 0: C_p = alpha*op(A_p)op(B_p) + bias_p + beta*C_p for each p;
+ * kconcat = 1: C_0 = alpha*sum_p op(A_p)op(B_p) + bias_0 + beta*C_0 (the
+ * dX of the group: sum over the projections).  1 <= nprob <= 3; every
+ * problem has the same M, N, K, leading dims, transposes, alpha, beta and
+ * epilogue; no gate when nprob > 1.  Falls back to sequential mtkc_gemm. */
+int mtkc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, void* stream);
 /* which path the last mtkc_gemm on this thread used: 0 simt, 1 tcgen05 */
 int mtkc_gemm_last_path(void);
 

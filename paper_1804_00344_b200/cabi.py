@@ -33,7 +33,7 @@ class GemmArgs(C.Structure):
 def declared_symbols() -> list[str]:
     """Every function the public header declares."""
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|uint64_t)\s+(mtkc_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|uint64_t|size_t)\s+(mtkc_\w+)\s*\(", text, re.M)))
 
 
 def lib():
@@ -46,6 +46,7 @@ def lib():
         L.mtkc_last_error.restype = C.c_char_p
         L.mtkc_launch_count.restype = C.c_uint64
         L.mtkc_gemm.argtypes = [C.POINTER(GemmArgs), C.c_void_p]
+        L.mtkc_gemm_group.argtypes = [C.POINTER(GemmArgs), C.c_int, C.c_int, C.c_void_p]
         _lib = L
     return _lib
 
@@ -62,6 +63,17 @@ def gemm(M, N, K, A, lda, B, ldb, Cp, ldc, trans_a=False, trans_b=False, alpha=1
                  Cp, ldc, stride_c, alpha, beta, bias, 1 if relu else 0, gate, precision,
                  workspace, workspace_bytes)
     check(lib().mtkc_gemm(C.byref(g), stream))
+    return lib().mtkc_gemm_last_path()
+
+
+def gemm_group(M, N, K, probs, lda, ldb, ldc, trans_a=False, trans_b=False, alpha=1.0, beta=0.0,
+               kconcat=False, precision=1, workspace=None, workspace_bytes=0, stream=None):
+    """mtkc_gemm_group: probs = [(A, B, C, bias-or-None), ...] device pointers."""
+    arr = (GemmArgs * len(probs))()
+    for i, (A, B, Cp, bias) in enumerate(probs):
+        arr[i] = GemmArgs(M, N, K, 1, A, lda, 0, int(trans_a), B, ldb, 0, int(trans_b), Cp, ldc, 0,
+                          alpha, beta, bias, 0, None, precision, workspace, workspace_bytes)
+    check(lib().mtkc_gemm_group(arr, len(probs), int(kconcat), stream))
     return lib().mtkc_gemm_last_path()
 
 

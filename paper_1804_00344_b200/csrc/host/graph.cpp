@@ -710,6 +710,158 @@ static NodeRef affineImpl(ExpressionGraph& g, NodeRef x, NodeRef w, NodeRef b, b
   return g.addNode(std::move(n));
 }
 
+namespace {
+// Siblings of an affineGroup: the q/k/v projections of one attention input.
+struct AffineGroup {
+  std::vector<int> members;  // affine node indices, ascending
+  std::vector<ExpressionGraph::Fn> fwd0, bwd0;  // the members' own fwd/bwd
+  int x = -1;
+  std::vector<int> W, b;  // parameter node indices per member
+  int64_t rows = 0, K = 0, N = 0;
+  bool fwdDone = false;
+  uint64_t bwdDone = ~0ull;  // backward sweep that already ran the group
+};
+
+mtkc_gemm_args groupArgs(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
+                         const float* B, int64_t ldb, bool tB, float* C, int64_t ldc, float beta,
+                         const float* bias) {
+  Device& d = Device::get();
+  mtkc_gemm_args g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.batch = 1;
+  g.A = A;
+  g.lda = lda;
+  g.transA = tA;
+  g.B = B;
+  g.ldb = ldb;
+  g.transB = tB;
+  g.C = C;
+  g.ldc = ldc;
+  g.alpha = 1.f;
+  g.beta = beta;
+  g.bias = bias;
+  g.epilogue = MTKC_EPI_NONE;
+  g.precision = (int)d.precision();
+  g.workspace = d.scratch(64 << 20);
+  g.workspace_bytes = d.scratchBytes();
+  return g;
+}
+}  // namespace
+
+std::vector<NodeRef> ExpressionGraph::affineGroup(NodeRef x, const std::vector<NodeRef>& Ws,
+                                                  const std::vector<NodeRef>& bs) {
+  if(Ws.size() != bs.size() || Ws.empty() || Ws.size() > 3)
+    throw ContractError("affineGroup takes 1..3 (W, b) pairs");
+  std::vector<NodeRef> out;
+  for(size_t i = 0; i < Ws.size(); ++i)
+    out.push_back(affine(x, Ws[i], bs[i]));
+  if(out.size() < 2)
+    return out;
+  for(auto& w : Ws)
+    if(w.shape != Ws[0].shape)
+      return out;  // unequal shapes: separate launches
+  auto grp = std::make_shared<AffineGroup>();
+  grp->x = x.index;
+  grp->K = x.shape.back();
+  grp->N = Ws[0].shape[1];
+  grp->rows = x.shape.size() / grp->K;
+  for(size_t i = 0; i < out.size(); ++i) {
+    Node& n = nodes_[(size_t)out[i].index];
+    grp->members.push_back(out[i].index);
+    grp->fwd0.push_back(n.fwd);
+    grp->bwd0.push_back(n.bwd);
+    grp->W.push_back(Ws[i].index);
+    grp->b.push_back(bs[i].index);
+    n.group = grp;
+  }
+  const size_t G = out.size();
+  // forward: the first member computes every member's output in one launch
+  for(size_t i = 0; i < G; ++i) {
+    nodes_[(size_t)out[i].index].fwd = [grp, G](ExpressionGraph& g, Node&) {
+      if(grp->fwdDone)
+        return;
+      grp->fwdDone = true;
+      mtkc_gemm_args probs[3];
+      for(size_t j = 0; j < G; ++j) {
+        Node& m = g.node(grp->members[j]);
+        if(m.value.empty())
+          m.value = g.allocTensor(m.shape);
+        probs[j] = groupArgs(grp->rows, grp->N, grp->K, g.valPtr(grp->x), grp->K, false,
+                             g.valPtr(grp->W[j]), grp->N, false, m.value.dev(), grp->N, 0.f,
+                             g.valPtr(grp->b[j]));
+      }
+      MTKC(mtkc_gemm_group(probs, (int)G, 0, Device::get().stream()));
+    };
+  }
+  // backward: the first live member reached by the sweep (highest index)
+  // does dX, dW and db for every live member
+  for(size_t i = 0; i < G; ++i) {
+    nodes_[(size_t)out[i].index].bwd = [grp, G, i](ExpressionGraph& g, Node& n) {
+      if(grp->bwdDone == g.backwardCount_)
+        return;
+      std::vector<size_t> live;
+      for(size_t j = G; j-- > 0;)
+        if(g.node(grp->members[j]).gradLive)
+          live.push_back(j);
+      if(live.size() < 2) {
+        grp->bwd0[i](g, n);
+        return;
+      }
+      grp->bwdDone = g.backwardCount_;
+      const int64_t rows = grp->rows, K = grp->K, N = grp->N;
+      Device& dev = Device::get();
+      const float* dY[3];
+      for(size_t q = 0; q < live.size(); ++q)
+        dY[q] = g.gradSrc(g.node(grp->members[live[q]]));
+      {  // dX (+)= sum_j dY_j W_j^T: one K-concatenated product
+        auto d = g.gradDst(grp->x, true);
+        if(d.gate) {  // ReLU-gated producer: per-member products keep the gate epilogue
+          for(size_t q = 0; q < live.size(); ++q) {
+            auto dq = q == 0 ? d : g.gradDst(grp->x, true);
+            gemm(rows, K, N, dY[q], N, false, g.valPtr(grp->W[live[q]]), N, true, dq.ptr, K,
+                 dq.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, dq.gate);
+          }
+        } else {
+          mtkc_gemm_args probs[3];
+          for(size_t q = 0; q < live.size(); ++q)
+            probs[q] = groupArgs(rows, K, N, dY[q], N, false, g.valPtr(grp->W[live[q]]), N, true,
+                                 d.ptr, K, d.accumulate ? 1.f : 0.f, nullptr);
+          MTKC(mtkc_gemm_group(probs, (int)live.size(), 1, dev.stream()));
+        }
+      }
+      {  // dW_j (+)= X^T dY_j: one grouped launch when the accumulate flags agree
+        ExpressionGraph::GradDst dw[3];
+        bool same = true;
+        for(size_t q = 0; q < live.size(); ++q) {
+          dw[q] = g.gradDst(grp->W[live[q]]);
+          same = same && dw[q].accumulate == dw[0].accumulate;
+        }
+        if(same) {
+          mtkc_gemm_args probs[3];
+          for(size_t q = 0; q < live.size(); ++q)
+            probs[q] = groupArgs(K, N, rows, g.valPtr(grp->x), K, true, dY[q], N, false,
+                                 dw[q].ptr, N, dw[q].accumulate ? 1.f : 0.f, nullptr);
+          MTKC(mtkc_gemm_group(probs, (int)live.size(), 0, dev.stream()));
+        } else {
+          for(size_t q = 0; q < live.size(); ++q)
+            gemm(K, N, rows, g.valPtr(grp->x), K, true, dY[q], N, false, dw[q].ptr, N,
+                 dw[q].accumulate ? 1.f : 0.f);
+        }
+      }
+      for(size_t q = 0; q < live.size(); ++q) {  // db_j
+        auto d = g.gradDst(grp->b[live[q]]);
+        size_t ws = (size_t)((rows + 63) / 64) * (size_t)N * sizeof(float);
+        float* w = dev.scratch(ws);
+        MTKC(mtkc_colsum(d.ptr, dY[q], rows, N, d.accumulate, w, dev.scratchBytes(),
+                         dev.stream()));
+      }
+    };
+  }
+  return out;
+}
+
 NodeRef ExpressionGraph::affine(NodeRef x, NodeRef w, NodeRef b, bool transW) {
   return affineImpl(*this, x, w, b, transW, false);
 }
@@ -1344,6 +1496,7 @@ void ExpressionGraph::backward(NodeRef loss) { backward(loss, nullptr); }
 
 void ExpressionGraph::backward(NodeRef loss, const std::function<void(int)>& afterNode) {
   checkRef(loss);
+  ++backwardCount_;
   if(inference_)
     throw ContractError("backward() called on an inference-mode graph");
   if(loss.shape.size() != 1)

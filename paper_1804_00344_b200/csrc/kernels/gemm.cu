@@ -12,6 +12,8 @@
 
 namespace mtkc {
 bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc);  // gemm_tc.cu
+bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStream_t st,
+                   int* rc);
 }
 
 using namespace mtkc;
@@ -183,6 +185,40 @@ int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
             p.foldBatch ? 1u : (unsigned)a->batch);
   ::mtkc::launch(gemm_fp32_kernel, grid, 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("gemm_fp32_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, void* stream) {
+  if(!probs || nprob < 1)
+    return fail(MTKC_CONTRACT, "mtkc_gemm_group: no problems");
+  const mtkc_gemm_args& a = probs[0];
+  if(a.precision == MTKC_GEMM_TF32 && nprob <= 3) {
+    int rc = MTKC_OK;
+    ProfScope prof(S(stream), "gemm_tc", 2.0 * a.M * a.N * a.K * nprob);
+    if(prof_detail()) {
+      char d[128];
+      snprintf(d, sizeof(d), "group%d%s_M%lld_N%lld_K%lld_tA%d_tB%d%s%s", nprob,
+               kconcat ? "k" : "", (long long)a.M, (long long)a.N, (long long)a.K, a.transA,
+               a.transB, a.beta != 0.f ? "_acc" : "", a.bias ? "_bias" : "");
+      prof.detail = d;
+    }
+    if(tc_gemm_group(probs, nprob, kconcat, S(stream), &rc)) {
+      t_last_path = 1;
+      return rc;
+    }
+  }
+  // same semantics, one product at a time
+  for(int q = 0; q < nprob; ++q) {
+    mtkc_gemm_args b = probs[q];
+    if(kconcat && q > 0) {
+      b.C = a.C;
+      b.ldc = a.ldc;
+      b.beta = 1.f;
+      b.bias = nullptr;
+    }
+    if(int rc = mtkc_gemm(&b, stream))
+      return rc;
+  }
   return MTKC_OK;
 }
 

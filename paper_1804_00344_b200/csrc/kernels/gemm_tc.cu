@@ -155,7 +155,19 @@ struct TcP {
   int mt, nt, splits;
   int numTiles;
   int tmaStore;  // 1: epilogue writes C (or 3-d partials) through a TMA store map
+  // problem groups (mtkc_gemm_group): nprob products of one shape in one
+  // launch.  kconcat = 0: independent outputs C_p = op(A_p) op(B_p) (+bias_p);
+  // kconcat = 1: one output C = sum_p op(A_p) op(B_p) (the K dimensions
+  // concatenated: k-block kb of the sweep is block kb % nkbProb of problem
+  // kb / nkbProb).  Problem 0 is the plain single GEMM.
+  int nprob, kconcat, nkbProb;
+  const float* biasP[3];
+  float* CP[3];
   int dbg;  // profiling switches (MTK_GEMM_DEBUG): 1 = no epilogue stores, 2 = no MMAs
+};
+
+struct TcMaps {
+  CUtensorMap a[3], b[3], c[3], g;
 };
 
 template <int BN>
@@ -175,10 +187,7 @@ struct TcSmem {
 // a separate instantiation so the common bias/ReLU epilogue stays lean.
 template <int BN, bool A_MN, bool B_MN, bool LOADS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    gemm_tf32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
-                        const __grid_constant__ CUtensorMap mapB,
-                        const __grid_constant__ CUtensorMap mapC,
-                        const __grid_constant__ CUtensorMap mapG, TcP p) {
+    gemm_tf32_tc_kernel(const __grid_constant__ TcMaps maps, TcP p) {
   using L = TcSmem<BN>;
   constexpr int ST = L::ST;
   constexpr uint32_t A_BYTES = L::A_BYTES, B_BYTES = L::B_BYTES;
@@ -199,12 +208,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if(warp == 0 && lane == 0) {
-    prefetch_tmap(&mapA);
-    prefetch_tmap(&mapB);
-    if(p.tmaStore)
-      prefetch_tmap(&mapC);
+    for(int q = 0; q < p.nprob; ++q) {
+      prefetch_tmap(&maps.a[q]);
+      prefetch_tmap(&maps.b[q]);
+      if(p.tmaStore && (q == 0 || !p.kconcat))
+        prefetch_tmap(&maps.c[q]);
+    }
     if(p.gate && p.tmaStore)
-      prefetch_tmap(&mapG);
+      prefetch_tmap(&maps.g);
     for(int w = 0; w < 8; ++w)
       mbar_init(&ldbar[w], 1);
     for(int s = 0; s < ST; ++s) {
@@ -232,8 +243,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   MTKC_PDL_ENTRY();
   const uint32_t tmem = *tmemSlot;
   const int tilesPerSplit = p.mt * p.nt;
+  const int tilesPerProb = tilesPerSplit * p.splits;
+  const int nOut = p.kconcat ? 1 : p.nprob;  // output problems
 
+  // tile t -> (output problem, split, m0, n0, k-block range); with kconcat
+  // the k range runs over the concatenated k-blocks of all problems
+  int tprob = 0;
   auto tileCoords = [&](int t, int& m0, int& n0, int& kb0, int& nkb, int& split) {
+    tprob = p.kconcat ? 0 : t / tilesPerProb;
+    t -= tprob * tilesPerProb;
     split = t / tilesPerSplit;
     int rem = t - split * tilesPerSplit;
     m0 = (rem % p.mt) * BM;
@@ -253,22 +271,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if(i >= ST)
             mbar_wait(&empty[s], ((i / ST) - 1) & 1);
           mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-          int k0 = (kb0 + kb) * BK;
+          const int kbg = kb0 + kb;
+          const int pk = p.kconcat ? kbg / p.nkbProb : tprob;  // problem of this k-block
+          const int k0 = (p.kconcat ? kbg - pk * p.nkbProb : kbg) * BK;
+          const CUtensorMap* mapA = &maps.a[pk];
+          const CUtensorMap* mapB = &maps.b[pk];
           uint8_t* a = sA + s * A_BYTES;
           uint8_t* b = sB + s * B_BYTES;
           if(A_MN) {
 #pragma unroll
             for(int j = 0; j < BM / 32; ++j)
-              tma_load_2d(a + j * (BK * 128), &mapA, &full[s], m0 + j * 32, k0);
+              tma_load_2d(a + j * (BK * 128), mapA, &full[s], m0 + j * 32, k0);
           } else {
-            tma_load_2d(a, &mapA, &full[s], k0, m0);
+            tma_load_2d(a, mapA, &full[s], k0, m0);
           }
           if(B_MN) {
 #pragma unroll
             for(int j = 0; j < BN / 32; ++j)
-              tma_load_2d(b + j * (BK * 128), &mapB, &full[s], n0 + j * 32, k0);
+              tma_load_2d(b + j * (BK * 128), mapB, &full[s], n0 + j * 32, k0);
           } else {
-            tma_load_2d(b, &mapB, &full[s], k0, n0);
+            tma_load_2d(b, mapB, &full[s], k0, n0);
           }
         }
       }
@@ -334,6 +356,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const int64_t rowBase = m0 + q * 32;
+      const CUtensorMap* mapC = &maps.c[p.part ? 0 : tprob];
+      const float* biasT = p.biasP[tprob];
+      float* CT = p.CP[tprob];
+      const int zpart = split * nOut + tprob;  // partial plane of this tile
 #pragma unroll 1
       for(int c0 = cBeg; c0 < cEnd; c0 += 32) {
         float v[32];
@@ -376,9 +402,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if(lane == 0) {
                 mbar_expect_tx(&ldbar[ew], (needC ? 4096u : 0u) + (needG ? 4096u : 0u));
                 if(needC)
-                  tma_load_2d(stage, &mapC, &ldbar[ew], (int)col0, (int)rowBase);
+                  tma_load_2d(stage, mapC, &ldbar[ew], (int)col0, (int)rowBase);
                 if(needG)
-                  tma_load_2d(grow, &mapG, &ldbar[ew], (int)col0, (int)rowBase);
+                  tma_load_2d(grow, &maps.g, &ldbar[ew], (int)col0, (int)rowBase);
               }
               mbar_wait(&ldbar[ew], ldPhase & 1);
               ++ldPhase;
@@ -392,9 +418,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               for(int i = 0; i < 32; ++i)
                 v[i] = p.alpha * v[i];
             }
-            if(p.bias) {
-              if(col0 + 32 <= p.N && ((uintptr_t)(p.bias + col0) & 15) == 0) {
-                const float4* b4p = reinterpret_cast<const float4*>(p.bias + col0);
+            if(biasT) {
+              if(col0 + 32 <= p.N && ((uintptr_t)(biasT + col0) & 15) == 0) {
+                const float4* b4p = reinterpret_cast<const float4*>(biasT + col0);
 #pragma unroll
                 for(int j = 0; j < 8; ++j) {
                   const float4 b4 = __ldg(b4p + j);
@@ -404,7 +430,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                   v[4 * j + 3] = v[4 * j + 3] + b4.w;
                 }
               } else {
-                const float bl = col0 + lane < p.N ? p.bias[col0 + lane] : 0.f;
+                const float bl = col0 + lane < p.N ? biasT[col0 + lane] : 0.f;
 #pragma unroll
                 for(int i = 0; i < 32; ++i)
                   v[i] = v[i] + __shfl_sync(0xffffffffu, bl, i);
@@ -462,13 +488,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if(p.part)
               asm volatile(
                   "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
-                  ::"l"((uint64_t)&mapC), "r"(smem_u32(stage)), "r"((int)col0), "r"((int)rowBase),
-                  "r"(split)
+                  ::"l"((uint64_t)mapC), "r"(smem_u32(stage)), "r"((int)col0), "r"((int)rowBase),
+                  "r"(zpart)
                   : "memory");
             else
               asm volatile(
                   "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
-                  ::"l"((uint64_t)&mapC), "r"(smem_u32(stage)), "r"((int)col0), "r"((int)rowBase)
+                  ::"l"((uint64_t)mapC), "r"(smem_u32(stage)), "r"((int)col0), "r"((int)rowBase)
                   : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -483,7 +509,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
         const int64_t col = col0 + lane;
         const bool colOk = col < p.N;
-        const float bcol = (p.bias && colOk && !p.part) ? p.bias[col] : 0.f;
+        const float bcol = (biasT && colOk && !p.part) ? biasT[col] : 0.f;
         const int rows = (int)min((int64_t)32, p.M - rowBase);
         for(int r = 0; r < rows; ++r) {
           float x = st[r * EPI_STRIDE + lane];
@@ -491,12 +517,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if(!colOk)
             continue;
           if(p.part) {
-            p.part[((int64_t)split * p.M + rr) * p.N + col] = x;
+            p.part[((int64_t)zpart * p.M + rr) * p.N + col] = x;
             continue;
           }
-          float* dst = p.C + rr * p.ldc + col;
+          float* dst = CT + rr * p.ldc + col;
           x = p.alpha == 1.f ? x : p.alpha * x;
-          if(p.bias)
+          if(biasT)
             x = x + bcol;
           if(p.epi == MTKC_EPI_RELU)
             x = x > 0.f ? x : 0.f;
@@ -525,11 +551,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // C = alpha*sum_s part[s] (+bias, relu, gate) + beta*C  (fixed split order).
 // Grid-stride over (row, 4-column group); float4 when N and ldc allow.
 template <bool VEC>
-__global__ void splitk_reduce_kernel(const float* part, int splits, int64_t M, int64_t N,
-                                     float* C, int64_t ldc, float alpha, float beta,
+__global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plane, int64_t M,
+                                     int64_t N, float* C, int64_t ldc, float alpha, float beta,
                                      const float* bias, int epi, const float* gate) {
   MTKC_PDL_ENTRY();
-  const int64_t groups = (N + 3) / 4, total = M * groups, plane = M * N;
+  const int64_t groups = (N + 3) / 4, total = M * groups;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
       i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / groups, c = (i - r * groups) * 4;
@@ -650,8 +676,7 @@ bool make_store_map(CUtensorMap* m, float* base, int64_t cols, int64_t rows, int
 int g_sms = 0;
 
 template <int BN, bool A_MN, bool B_MN, bool LOADS>
-int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-              const CUtensorMap& mg, const TcP& p, cudaStream_t st) {
+int launch_tc(const TcMaps& maps, const TcP& p, cudaStream_t st) {
   constexpr size_t smem = TcSmem<BN>::BYTES;
   auto kern = gemm_tf32_tc_kernel<BN, A_MN, B_MN, LOADS>;
   static bool attr = false;
@@ -663,35 +688,48 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& m
     attr = true;
   }
   int grid = std::min(p.numTiles, g_sms);
-  ::mtkc::launch(kern, grid, TC_THREADS, smem, st, ma, mb, mc, mg, p);
+  ::mtkc::launch(kern, grid, TC_THREADS, smem, st, maps, p);
   MTKC_POST_LAUNCH("gemm_tf32_tc_kernel");
   return MTKC_OK;
 }
 
 template <int BN, bool LOADS>
-int dispatch_majors(bool aMN, bool bMN, const CUtensorMap& ma, const CUtensorMap& mb,
-                    const CUtensorMap& mc, const CUtensorMap& mg, const TcP& p,
-                    cudaStream_t st) {
+int dispatch_majors(bool aMN, bool bMN, const TcMaps& maps, const TcP& p, cudaStream_t st) {
   if(!aMN && !bMN)
-    return launch_tc<BN, false, false, LOADS>(ma, mb, mc, mg, p, st);
+    return launch_tc<BN, false, false, LOADS>(maps, p, st);
   if(!aMN && bMN)
-    return launch_tc<BN, false, true, LOADS>(ma, mb, mc, mg, p, st);
+    return launch_tc<BN, false, true, LOADS>(maps, p, st);
   if(aMN && !bMN)
-    return launch_tc<BN, true, false, LOADS>(ma, mb, mc, mg, p, st);
-  return launch_tc<BN, true, true, LOADS>(ma, mb, mc, mg, p, st);
+    return launch_tc<BN, true, false, LOADS>(maps, p, st);
+  return launch_tc<BN, true, true, LOADS>(maps, p, st);
 }
 
 }  // namespace
 
 // Returns false when the tensor-core path does not apply (caller falls back).
-bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
+// probs[0..nprob): one shape (M, N, K, strides, transposes, alpha, beta,
+// epilogue) with per-problem A, B, C, bias.  kconcat: C = sum_p op(A_p)op(B_p)
+// into probs[0].C (bias from probs[0]).
+bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStream_t st,
+                   int* rc) {
+  const mtkc_gemm_args& a = probs[0];
   if(getenv("MTK_DISABLE_TC"))
     return false;
-  if(a.batch != 1)
+  if(nprob < 1 || nprob > 3)
+    return false;
+  for(int q = 0; q < nprob; ++q) {
+    const mtkc_gemm_args& b = probs[q];
+    if(b.batch != 1 || b.M != a.M || b.N != a.N || b.K != a.K || b.lda != a.lda ||
+       b.ldb != a.ldb || b.ldc != a.ldc || b.transA != a.transA || b.transB != a.transB)
+      return false;
+    if(((uintptr_t)b.A % 16) || ((uintptr_t)b.B % 16))
+      return false;
+  }
+  if(nprob > 1 && a.gate)
     return false;
   if(a.M < 1 || a.N < 8 || a.K < 8)
     return false;
-  if(a.lda % 4 || a.ldb % 4 || ((uintptr_t)a.A % 16) || ((uintptr_t)a.B % 16))
+  if(a.lda % 4 || a.ldb % 4)
     return false;
   // operand majors: op(A) is K-major iff stored untransposed
   const bool aMN = a.transA != 0, bMN = a.transB == 0;
@@ -702,28 +740,29 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
     if(g_sms <= 0)
       g_sms = 148;
   }
+  const int nOut = kconcat ? 1 : nprob;
   const int64_t mt = cdiv(a.M, BM);
-  // wide tiles only when they still give every SM at least one tile
   // wide tiles halve the re-reads of A (the L2->SM operand traffic that
   // bounds fp32-storage GEMMs) -- worth a partly idle wave; narrow tiles only
   // when there are so few wide tiles that split-K would have to fill the GPU
-  int BN = (a.N >= 256 && mt * cdiv(a.N, 256) >= 32) ? 256 : 128;
+  int BN = (a.N >= 256 && mt * cdiv(a.N, 256) * nOut >= 32) ? 256 : 128;
   if(const char* e = getenv("MTK_GEMM_BN"))  // tuning override (tools/gemm_bench.py)
     BN = (atoi(e) == 256 && a.N >= 256) ? 256 : 128;
   const int64_t nt = cdiv(a.N, BN);
-  const int numKb = (int)cdiv(a.K, BK);
-  // Split K to fill the machine: pick the split count (each split keeping
-  // >= 24 k-blocks) that maximises the wave efficiency of the persistent
-  // grid, tiles*s / (SMs * ceil(tiles*s / SMs)); ties go to fewer splits.
+  const int nkbProb = (int)cdiv(a.K, BK);
+  const int numKb = kconcat ? nkbProb * nprob : nkbProb;
+  // Split K to fill the machine: pick the split count that maximises the
+  // wave efficiency of the persistent grid, tiles*s / (SMs*ceil(tiles*s/SMs));
+  // ties go to fewer splits.  Skinny products (RNN time steps: M = batch
+  // rows, a handful of tiles) split down to 4 k-blocks per CTA; otherwise
+  // keep >= 24 per split.
   int splits = 1;
-  const int64_t tiles = mt * nt;
-  // Skinny products (RNN time steps: M = batch rows, a handful of tiles)
-  // split down to 4 k-blocks per CTA; otherwise keep >= 24 per split.
+  const int64_t tiles = mt * nt * nOut;
   const int minKb = tiles * 4 <= g_sms ? 4 : 24;
   if(a.workspace && numKb >= 2 * minKb) {
     double best = (double)tiles / (double)(g_sms * cdiv(tiles, g_sms));
     for(int s = 2; s <= 16 && numKb / s >= minKb; ++s) {
-      size_t need = (size_t)s * (size_t)a.M * (size_t)a.N * sizeof(float);
+      size_t need = (size_t)s * nOut * (size_t)a.M * (size_t)a.N * sizeof(float);
       if(need > a.workspace_bytes)
         break;
       double eff = (double)(tiles * s) / (double)(g_sms * cdiv(tiles * s, g_sms));
@@ -737,22 +776,27 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
   const int kbPer = (int)cdiv(numKb, splits);
   splits = (int)cdiv(numKb, kbPer);
 
-  CUtensorMap ma, mb;
-  bool ok;
-  if(aMN)  // storage [K x M], M contiguous
-    ok = make_map(&ma, a.A, a.M, a.K, a.lda, 32, BK, true);
-  else     // storage [M x K]
-    ok = make_map(&ma, a.A, a.K, a.M, a.lda, BK, BM, false);
-  if(!ok)
-    return false;
-  if(bMN)  // storage [K x N]
-    ok = make_map(&mb, a.B, a.N, a.K, a.ldb, 32, BK, true);
-  else     // storage [N x K]
-    ok = make_map(&mb, a.B, a.K, a.N, a.ldb, BK, (uint32_t)BN, false);
-  if(!ok)
-    return false;
+  TcMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  for(int q = 0; q < nprob; ++q) {
+    const mtkc_gemm_args& b = probs[q];
+    bool ok;
+    if(aMN)  // storage [K x M], M contiguous
+      ok = make_map(&maps.a[q], b.A, a.M, a.K, a.lda, 32, BK, true);
+    else     // storage [M x K]
+      ok = make_map(&maps.a[q], b.A, a.K, a.M, a.lda, BK, BM, false);
+    if(!ok)
+      return false;
+    if(bMN)  // storage [K x N]
+      ok = make_map(&maps.b[q], b.B, a.N, a.K, a.ldb, 32, BK, true);
+    else     // storage [N x K]
+      ok = make_map(&maps.b[q], b.B, a.K, a.N, a.ldb, BK, (uint32_t)BN, false);
+    if(!ok)
+      return false;
+  }
 
   TcP p;
+  std::memset(&p, 0, sizeof(p));
   p.M = a.M;
   p.N = a.N;
   p.K = a.K;
@@ -763,57 +807,72 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
   p.bias = a.bias;
   p.epi = a.epilogue;
   p.gate = a.gate;
+  p.nprob = nprob;
+  p.kconcat = kconcat;
+  p.nkbProb = nkbProb;
+  for(int q = 0; q < nOut; ++q) {
+    p.biasP[q] = probs[q].bias;
+    p.CP[q] = probs[q].C;
+  }
   p.part = splits > 1 ? a.workspace : nullptr;
   p.kbPerSplit = kbPer;
   p.numKb = numKb;
   p.mt = (int)mt;
   p.nt = (int)nt;
   p.splits = splits;
-  p.numTiles = (int)(mt * nt * splits);
+  p.numTiles = (int)(mt * nt * splits * nOut);
   {
     const char* e = getenv("MTK_GEMM_DEBUG");
     p.dbg = e ? atoi(e) : 0;
   }
-  CUtensorMap mc;
-  std::memset(&mc, 0, sizeof(mc));
-  if(p.part)
-    p.tmaStore = (a.N % 4 == 0) && ((uintptr_t)a.workspace % 16 == 0) &&
-                 make_store_map(&mc, a.workspace, a.N, a.M, a.N, splits);
-  else
-    p.tmaStore = (a.ldc % 4 == 0) && ((uintptr_t)a.C % 16 == 0) &&
-                 make_store_map(&mc, a.C, a.N, a.M, a.ldc, 1);
+  bool store = true;
+  if(p.part) {
+    store = (a.N % 4 == 0) && ((uintptr_t)a.workspace % 16 == 0) &&
+            make_store_map(&maps.c[0], a.workspace, a.N, a.M, a.N, (int64_t)splits * nOut);
+  } else {
+    for(int q = 0; q < nOut && store; ++q)
+      store = (a.ldc % 4 == 0) && ((uintptr_t)probs[q].C % 16 == 0) &&
+              make_store_map(&maps.c[q], probs[q].C, a.N, a.M, a.ldc, 1);
+  }
   // the ReLU gate is read as TMA boxes too (same geometry as C)
-  CUtensorMap mg;
-  std::memset(&mg, 0, sizeof(mg));
-  if(p.tmaStore && !p.part && a.gate)
-    p.tmaStore = ((uintptr_t)a.gate % 16 == 0) &&
-                 make_store_map(&mg, const_cast<float*>(a.gate), a.N, a.M, a.ldc, 1);
+  if(store && !p.part && a.gate)
+    store = ((uintptr_t)a.gate % 16 == 0) &&
+            make_store_map(&maps.g, const_cast<float*>(a.gate), a.N, a.M, a.ldc, 1);
+  p.tmaStore = store ? 1 : 0;
   if(getenv("MTK_GEMM_NO_TMA_STORE"))
     p.tmaStore = 0;
   const bool loads = p.tmaStore && !p.part && (a.beta != 0.f || a.gate != nullptr);
   if(loads)
-    *rc = BN == 256 ? dispatch_majors<256, true>(aMN, bMN, ma, mb, mc, mg, p, st)
-                    : dispatch_majors<128, true>(aMN, bMN, ma, mb, mc, mg, p, st);
+    *rc = BN == 256 ? dispatch_majors<256, true>(aMN, bMN, maps, p, st)
+                    : dispatch_majors<128, true>(aMN, bMN, maps, p, st);
   else
-    *rc = BN == 256 ? dispatch_majors<256, false>(aMN, bMN, ma, mb, mc, mg, p, st)
-                    : dispatch_majors<128, false>(aMN, bMN, ma, mb, mc, mg, p, st);
+    *rc = BN == 256 ? dispatch_majors<256, false>(aMN, bMN, maps, p, st)
+                    : dispatch_majors<128, false>(aMN, bMN, maps, p, st);
   if(*rc == MTKC_OK && splits > 1) {
-    const bool vec = a.N % 4 == 0 && a.ldc % 4 == 0 && (uintptr_t)a.C % 16 == 0 &&
-                     (uintptr_t)a.workspace % 16 == 0;
-    const unsigned grid = grid1d(a.M * cdiv(a.N, 4), 256);
-    if(vec)
-      ::mtkc::launch(splitk_reduce_kernel<true>, grid, 256, 0, st, a.workspace, splits, a.M, a.N, a.C, a.ldc,
-                                                        a.alpha, a.beta, a.bias, a.epilogue, a.gate);
-    else
-      ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, a.workspace, splits, a.M, a.N, a.C,
-                                                         a.ldc, a.alpha, a.beta, a.bias,
-                                                         a.epilogue, a.gate);
-    count_launch();
-    cudaError_t e = cudaGetLastError();
-    if(e != cudaSuccess)
-      *rc = cuda_status(e, "splitk_reduce_kernel");
+    for(int q = 0; q < nOut && *rc == MTKC_OK; ++q) {
+      const mtkc_gemm_args& b = probs[q];
+      const float* part = a.workspace + (int64_t)q * a.M * a.N;
+      const int64_t sstride = (int64_t)nOut * a.M * a.N;  // between splits
+      const bool vec = a.N % 4 == 0 && a.ldc % 4 == 0 && (uintptr_t)b.C % 16 == 0 &&
+                       (uintptr_t)a.workspace % 16 == 0;
+      const unsigned grid = grid1d(a.M * cdiv(a.N, 4), 256);
+      if(vec)
+        ::mtkc::launch(splitk_reduce_kernel<true>, grid, 256, 0, st, part, splits, sstride, a.M,
+                       a.N, b.C, a.ldc, a.alpha, a.beta, b.bias, a.epilogue, a.gate);
+      else
+        ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, part, splits, sstride, a.M,
+                       a.N, b.C, a.ldc, a.alpha, a.beta, b.bias, a.epilogue, a.gate);
+      count_launch();
+      cudaError_t e = cudaGetLastError();
+      if(e != cudaSuccess)
+        *rc = cuda_status(e, "splitk_reduce_kernel");
+    }
   }
   return true;
+}
+
+bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
+  return tc_gemm_group(&a, 1, 0, st, rc);
 }
 
 }  // namespace mtkc

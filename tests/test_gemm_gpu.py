@@ -118,3 +118,53 @@ def test_tf32_epilogue_combinations(cuda, shape):
         assert path == 1 or N % 4, "tensor-core path not taken"  # TMA needs 16-B row pitch
         err = np.abs(got - want)
         assert np.all(err <= tol), (kw.keys(), float(np.max(err - tol)))
+
+
+@pytest.mark.parametrize("shape", [(300, 128, 256), (1000, 512, 512), (64, 8192, 96), (517, 40, 2050)])
+def test_tf32_gemm_group(cuda, shape):
+    """mtkc_gemm_group: three products of one shape in one launch -- independent
+    outputs with per-problem bias (q/k/v forward), the K-concatenated sum into
+    one output with beta (their dX), and transposed-A products with split-K
+    (their dW)."""
+    import torch
+    rng = np.random.default_rng(5)
+    M, K, N = shape
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    As = [rng.uniform(-1, 1, (M, K)).astype(np.float32) for _ in range(3)]
+    Bs = [rng.uniform(-1, 1, (K, N)).astype(np.float32) for _ in range(3)]
+    bs = [rng.uniform(-1, 1, N).astype(np.float32) for _ in range(3)]
+    dA, dB, db = [dev(x) for x in As], [dev(x) for x in Bs], [dev(x) for x in bs]
+    tol = lambda a, b: 4e-3 * (np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64) + 1)
+    # independent outputs sharing A (forward of q/k/v)
+    Cs = [torch.zeros(M, N, device="cuda") for _ in range(3)]
+    path = cabi.gemm_group(M, N, K, [(dA[0].data_ptr(), dB[q].data_ptr(), Cs[q].data_ptr(),
+                                     db[q].data_ptr()) for q in range(3)], K, N, N,
+                           workspace=ws.data_ptr(), workspace_bytes=ws.numel())
+    torch.cuda.synchronize()
+    assert path == 1 or N % 4
+    for q in range(3):
+        want = As[0].astype(np.float64) @ Bs[q] + bs[q]
+        assert np.all(np.abs(Cs[q].cpu().numpy() - want) <= tol(As[0], Bs[q])), q
+    # K-concatenated sum with beta = 1 (dX = sum_q dY_q W_q^T)
+    c0 = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    Cd = dev(c0)
+    cabi.gemm_group(M, N, K, [(dA[q].data_ptr(), dB[q].data_ptr(), Cd.data_ptr(), None)
+                              for q in range(3)], K, N, N, beta=1.0, kconcat=True,
+                    workspace=ws.data_ptr(), workspace_bytes=ws.numel())
+    torch.cuda.synchronize()
+    want = c0 + sum(As[q].astype(np.float64) @ Bs[q] for q in range(3))
+    bound = sum(tol(As[q], Bs[q]) for q in range(3))
+    assert np.all(np.abs(Cd.cpu().numpy() - want) <= bound)
+    # transposed A shared, long contraction (dW_q = X^T dY_q), beta = 0
+    Xt = [dev(x) for x in As]  # storage [M x K] read as op(A) = A^T  -> [K x M] @ [M x N]
+    Ys = [dev(rng.uniform(-1, 1, (M, N)).astype(np.float32)) for _ in range(3)]
+    Ws = [torch.zeros(K, N, device="cuda") for _ in range(3)]
+    cabi.gemm_group(K, N, M, [(Xt[0].data_ptr(), Ys[q].data_ptr(), Ws[q].data_ptr(), None)
+                              for q in range(3)], K, N, N, trans_a=True,
+                    workspace=ws.data_ptr(), workspace_bytes=ws.numel())
+    torch.cuda.synchronize()
+    for q in range(3):
+        y = Ys[q].cpu().numpy()
+        want = As[0].T.astype(np.float64) @ y
+        assert np.all(np.abs(Ws[q].cpu().numpy() - want) <= tol(As[0].T, y)), q
