@@ -38,6 +38,36 @@ void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
   MTKC(mtkc_gemm(&g, d.stream()));
 }
 
+// n <= 3 products of one shape in one launch (mtkc_gemm_group): independent
+// outputs C[k] (kconcat = false) or C[0] += sum_k A[k] op(B[k]) (kconcat)
+void gemmGroup(int n, bool kconcat, int64_t M, int64_t N, int64_t K, const float* const* A,
+               int64_t lda, bool tA, const float* const* B, int64_t ldb, bool tB,
+               float* const* C, int64_t ldc, const float* beta) {
+  Device& d = Device::get();
+  mtkc_gemm_args g[3];
+  for(int k = 0; k < n; ++k) {
+    g[k] = mtkc_gemm_args{};
+    g[k].M = M;
+    g[k].N = N;
+    g[k].K = K;
+    g[k].batch = 1;
+    g[k].A = A[k];
+    g[k].lda = lda;
+    g[k].transA = tA;
+    g[k].B = B[k];
+    g[k].ldb = ldb;
+    g[k].transB = tB;
+    g[k].C = C[kconcat ? 0 : k];
+    g[k].ldc = ldc;
+    g[k].alpha = 1.f;
+    g[k].beta = beta[kconcat ? 0 : k];
+    g[k].precision = (int)d.precision();
+    g[k].workspace = d.scratch(64 << 20);
+    g[k].workspace_bytes = d.scratchBytes();
+  }
+  MTKC(mtkc_gemm_group(g, n, kconcat ? 1 : 0, d.stream()));
+}
+
 void colsumInto(ExpressionGraph::GradDst dst, const float* in, int64_t rows, int64_t cols) {
   Device& dev = Device::get();
   size_t ws = (size_t)((rows + 63) / 64) * (size_t)cols * sizeof(float) * 2;
@@ -98,9 +128,13 @@ NodeRef ExpressionGraph::gruCell(NodeRef state, NodeRef input, const GruParams& 
     aux->cache = g.allocTensor(Shape({b, 3 * d}));
     const float* h = g.valPtr(n.inputs[0]);
     float* hu = aux->hu.dev();
-    gemm(b, d, d, h, d, false, g.valPtr(n.inputs[1]), d, false, hu, 3 * d, 0.f);
-    gemm(b, d, d, h, d, false, g.valPtr(n.inputs[3]), d, false, hu + d, 3 * d, 0.f);
-    gemm(b, d, d, h, d, false, g.valPtr(n.inputs[5]), d, false, hu + 2 * d, 3 * d, 0.f);
+    {  // h [Uz|Ur|Uh]: one grouped launch
+      const float* A[3] = {h, h, h};
+      const float* B[3] = {g.valPtr(n.inputs[1]), g.valPtr(n.inputs[3]), g.valPtr(n.inputs[5])};
+      float* C[3] = {hu, hu + d, hu + 2 * d};
+      const float beta[3] = {0.f, 0.f, 0.f};
+      gemmGroup(3, false, b, d, d, A, d, false, B, d, false, C, 3 * d, beta);
+    }
     mtkc_gru_args a{};
     a.b = b;
     a.d = d;
@@ -110,9 +144,12 @@ NodeRef ExpressionGraph::gruCell(NodeRef state, NodeRef input, const GruParams& 
       aux->xw = g.allocTensor(Shape({b, 3 * d}));
       float* xw = aux->xw.dev();
       const float* x = g.valPtr(n.inputs[xSlot]);
-      for(int k = 0; k < 3; ++k)
-        gemm(b, d, e, x, e, false, g.valPtr(n.inputs[wSlot + k]), d, false, xw + k * d, 3 * d,
-             0.f);
+      const float* A[3] = {x, x, x};
+      const float* B[3] = {g.valPtr(n.inputs[wSlot]), g.valPtr(n.inputs[wSlot + 1]),
+                           g.valPtr(n.inputs[wSlot + 2])};
+      float* C[3] = {xw, xw + d, xw + 2 * d};
+      const float beta[3] = {0.f, 0.f, 0.f};
+      gemmGroup(3, false, b, d, e, A, e, false, B, d, false, C, 3 * d, beta);
       a.xw = xw;
     }
     a.bz = g.valPtr(n.inputs[2]);
@@ -173,14 +210,29 @@ NodeRef ExpressionGraph::gruCell(NodeRef state, NodeRef input, const GruParams& 
     MTKC(mtkc_gru_backward(&a, stream()));
     const float* h = a.h;
     // dh += dpz Uz^T + dpr Ur^T + duh Uh^T   (graph.cpp:772, 802)
-    gemm(b, d, d, a.dpz, d, false, g.valPtr(n.inputs[1]), d, true, gh.ptr, d, 1.f);
-    gemm(b, d, d, a.dpr, d, false, g.valPtr(n.inputs[3]), d, true, gh.ptr, d, 1.f);
-    gemm(b, d, d, a.duh, d, false, g.valPtr(n.inputs[5]), d, true, gh.ptr, d, 1.f);
-    // dU += h^T dpre   (graph.cpp:773, 803)
     const float* gsrc[3] = {a.dpz, a.dpr, a.duh};
-    for(int k = 0; k < 3; ++k) {
-      auto dU = g.gradDst(n.inputs[1 + 2 * k]);
-      gemm(d, d, b, h, d, true, gsrc[k], d, false, dU.ptr, d, dU.accumulate ? 1.f : 0.f);
+    const float* Us[3] = {g.valPtr(n.inputs[1]), g.valPtr(n.inputs[3]), g.valPtr(n.inputs[5])};
+    {  // one K-concatenated launch; FP32 mode falls back to z, r, h in order
+      float* C[1] = {gh.ptr};
+      const float beta[1] = {1.f};
+      gemmGroup(3, true, b, d, d, gsrc, d, false, Us, d, true, C, d, beta);
+    }
+    // dU += h^T dpre   (graph.cpp:773, 803)
+    {
+      const float* hs[3] = {h, h, h};
+      float* C[3];
+      float beta[3];
+      for(int k = 0; k < 3; ++k) {
+        auto dU = g.gradDst(n.inputs[1 + 2 * k]);
+        C[k] = dU.ptr;
+        beta[k] = dU.accumulate ? 1.f : 0.f;
+      }
+      if(beta[0] == beta[1] && beta[1] == beta[2]) {
+        gemmGroup(3, false, d, d, b, hs, d, true, gsrc, d, false, C, d, beta);
+      } else {
+        for(int k = 0; k < 3; ++k)
+          gemm(d, d, b, h, d, true, gsrc[k], d, false, C[k], d, beta[k]);
+      }
     }
     // biases (graph.cpp:771, 801)
     colsumInto(g.gradDst(n.inputs[2]), a.dpz, b, d);
@@ -190,13 +242,26 @@ NodeRef ExpressionGraph::gruCell(NodeRef state, NodeRef input, const GruParams& 
       const float* x = g.valPtr(n.inputs[xSlot]);
       const float* wsrc[3] = {a.dpz, a.dpr, a.dax};
       auto dx = g.gradDst(n.inputs[xSlot]);
-      for(int k = 0; k < 3; ++k) {
-        float beta = (k == 0 && !dx.accumulate) ? 0.f : 1.f;
-        gemm(b, e, d, wsrc[k], d, false, g.valPtr(n.inputs[wSlot + k]), d, true, dx.ptr, e, beta);
+      const float* Ws[3] = {g.valPtr(n.inputs[wSlot]), g.valPtr(n.inputs[wSlot + 1]),
+                            g.valPtr(n.inputs[wSlot + 2])};
+      {
+        float* C[1] = {dx.ptr};
+        const float beta[1] = {dx.accumulate ? 1.f : 0.f};
+        gemmGroup(3, true, b, e, d, wsrc, d, false, Ws, d, true, C, e, beta);
       }
+      const float* xs[3] = {x, x, x};
+      float* C[3];
+      float beta[3];
       for(int k = 0; k < 3; ++k) {
         auto dW = g.gradDst(n.inputs[wSlot + k]);
-        gemm(e, d, b, x, e, true, wsrc[k], d, false, dW.ptr, d, dW.accumulate ? 1.f : 0.f);
+        C[k] = dW.ptr;
+        beta[k] = dW.accumulate ? 1.f : 0.f;
+      }
+      if(beta[0] == beta[1] && beta[1] == beta[2]) {
+        gemmGroup(3, false, e, d, b, xs, e, true, wsrc, d, false, C, d, beta);
+      } else {
+        for(int k = 0; k < 3; ++k)
+          gemm(e, d, b, x, e, true, wsrc[k], d, false, C[k], d, beta[k]);
       }
     }
     if(layerNorm) {  // per-gate LN gain/bias grads: one column sum, then slices
