@@ -205,6 +205,11 @@ int mtkc_reduce_backward(int op, float* gin, const float* gout, const float* in,
 /* out[c] (+)= sum_r in[r*cols + c]; deterministic two-level (bias grads) */
 int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int accumulate,
                 float* workspace, size_t workspace_bytes, void* stream);
+/* n <= 3 column sums of one shape in one launch (bias gradients of grouped
+ * projections / GRU gates); workspace >= n * ceil(rows/64) * cols floats. */
+int mtkc_colsum_group(float* const* outs, const float* const* ins, const int* accumulate, int n,
+                      int64_t rows, int64_t cols, float* workspace, size_t workspace_bytes,
+                      void* stream);
 /* flags |= MTKC_FLAG_NONFINITE if any in[i] is not finite (allFinite) */
 int mtkc_check_finite(const float* in, int64_t n, int* flags, void* stream);
 

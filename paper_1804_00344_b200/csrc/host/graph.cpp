@@ -850,12 +850,18 @@ std::vector<NodeRef> ExpressionGraph::affineGroup(NodeRef x, const std::vector<N
                  dw[q].accumulate ? 1.f : 0.f);
         }
       }
-      for(size_t q = 0; q < live.size(); ++q) {  // db_j
-        auto d = g.gradDst(grp->b[live[q]]);
-        size_t ws = (size_t)((rows + 63) / 64) * (size_t)N * sizeof(float);
+      {  // db_j: one launch
+        float* outs[3];
+        int acc[3];
+        for(size_t q = 0; q < live.size(); ++q) {
+          auto d = g.gradDst(grp->b[live[q]]);
+          outs[q] = d.ptr;
+          acc[q] = d.accumulate;
+        }
+        size_t ws = live.size() * (size_t)((rows + 63) / 64) * (size_t)N * sizeof(float);
         float* w = dev.scratch(ws);
-        MTKC(mtkc_colsum(d.ptr, dY[q], rows, N, d.accumulate, w, dev.scratchBytes(),
-                         dev.stream()));
+        MTKC(mtkc_colsum_group(outs, dY, acc, (int)live.size(), rows, N, w, dev.scratchBytes(),
+                               dev.stream()));
       }
     };
   }

@@ -235,9 +235,15 @@ NodeRef ExpressionGraph::gruCell(NodeRef state, NodeRef input, const GruParams& 
       }
     }
     // biases (graph.cpp:771, 801)
-    colsumInto(g.gradDst(n.inputs[2]), a.dpz, b, d);
-    colsumInto(g.gradDst(n.inputs[4]), a.dpr, b, d);
-    colsumInto(g.gradDst(n.inputs[6]), a.dac, b, d);
+    {  // the three gate biases in one launch
+      auto gz = g.gradDst(n.inputs[2]), gr = g.gradDst(n.inputs[4]), gb = g.gradDst(n.inputs[6]);
+      float* outs[3] = {gz.ptr, gr.ptr, gb.ptr};
+      const float* ins[3] = {a.dpz, a.dpr, a.dac};
+      const int acc[3] = {gz.accumulate, gr.accumulate, gb.accumulate};
+      Device& dev = Device::get();
+      float* w = dev.scratch((size_t)3 * ((b + 63) / 64) * (size_t)d * sizeof(float));
+      MTKC(mtkc_colsum_group(outs, ins, acc, 3, b, d, w, dev.scratchBytes(), dev.stream()));
+    }
     if(hasInput) {
       const float* x = g.valPtr(n.inputs[xSlot]);
       const float* wsrc[3] = {a.dpz, a.dpr, a.dax};

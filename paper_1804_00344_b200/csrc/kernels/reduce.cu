@@ -90,10 +90,22 @@ __global__ void colsum_direct_kernel(float* out, const float* in, int64_t rows, 
 constexpr int CS_MAX_SLABS = 8192;
 __device__ unsigned int g_colsum_ticket[CS_MAX_SLABS];
 
-__global__ void __launch_bounds__(256) colsum_onepass_kernel(float* out, float* part,
-                                                             const float* a, int64_t rows,
-                                                             int64_t cols, int acc) {
+struct ColsumGroup {
+  float* out[3];
+  const float* in[3];
+  int acc[3];
+};
+
+// gridDim.z = problems of a group (same shape): partial rows of problem z
+// at part + z*nblk*cols, tickets at z*slabs + slab
+__global__ void __launch_bounds__(256) colsum_onepass_kernel(ColsumGroup grp, float* part,
+                                                             int64_t rows, int64_t cols) {
   MTKC_PDL_ENTRY();
+  const int z = blockIdx.z;
+  float* out = grp.out[z];
+  const float* a = grp.in[z];
+  const int acc = grp.acc[z];
+  part += (int64_t)z * gridDim.y * cols;
   __shared__ float4 red[8][32];
   __shared__ bool last;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -125,7 +137,7 @@ __global__ void __launch_bounds__(256) colsum_onepass_kernel(float* out, float* 
   __threadfence();
   __syncthreads();
   if(threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&g_colsum_ticket[blockIdx.x], 1u);
+    const unsigned prev = atomicAdd(&g_colsum_ticket[z * gridDim.x + blockIdx.x], 1u);
     last = prev == (unsigned)(nblk - 1);
   }
   __syncthreads();
@@ -163,7 +175,7 @@ __global__ void __launch_bounds__(256) colsum_onepass_kernel(float* out, float* 
       *o = u;
     }
     if(lane == 0)
-      g_colsum_ticket[blockIdx.x] = 0u;
+      g_colsum_ticket[z * gridDim.x + blockIdx.x] = 0u;
   }
 }
 
@@ -231,8 +243,12 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
   int64_t nblk = cdiv(rows, CR_ROWS);
   if(cols % 4 == 0 && cdiv(cols, CR_COLS) <= CS_MAX_SLABS && nblk <= 65535 &&
      ((uintptr_t)in | (uintptr_t)out | (uintptr_t)workspace) % 16 == 0) {
-    ::mtkc::launch(colsum_onepass_kernel, dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256, 0,
-                            S(stream), out, workspace, in, rows, cols, accumulate);
+    ColsumGroup grp{};
+    grp.out[0] = out;
+    grp.in[0] = in;
+    grp.acc[0] = accumulate;
+    ::mtkc::launch(colsum_onepass_kernel, dim3((unsigned)cdiv(cols, CR_COLS), (unsigned)nblk), 256,
+                   0, S(stream), grp, workspace, rows, cols);
     MTKC_POST_LAUNCH("colsum_onepass_kernel");
     return MTKC_OK;
   }
@@ -242,6 +258,40 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
   ::mtkc::launch(colred_final_kernel<1>, colred_final_grid(cols), 256, 0, S(stream), 
       out, nullptr, workspace, nblk, cols, accumulate);
   MTKC_POST_LAUNCH("colred_final_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_colsum_group(float* const* outs, const float* const* ins, const int* accumulate, int n,
+                      int64_t rows, int64_t cols, float* workspace, size_t workspace_bytes,
+                      void* stream) {
+  if(n < 1 || rows <= 0 || cols <= 0)
+    return MTKC_OK;
+  const int64_t nblk = cdiv(rows, CR_ROWS), slabs = cdiv(cols, CR_COLS);
+  bool ok = n <= 3 && cols % 4 == 0 && rows > 8 && slabs * n <= CS_MAX_SLABS && nblk <= 65535 &&
+            workspace && workspace_bytes >= (size_t)n * colred_workspace_bytes(1, rows, cols) &&
+            (uintptr_t)workspace % 16 == 0;
+  for(int q = 0; q < n && ok; ++q)
+    ok = ((uintptr_t)ins[q] | (uintptr_t)outs[q]) % 16 == 0;
+  if(!ok) {  // one problem at a time
+    for(int q = 0; q < n; ++q)
+      if(int rc = mtkc_colsum(outs[q], ins[q], rows, cols, accumulate[q], workspace,
+                              workspace_bytes, stream))
+        return rc;
+    return MTKC_OK;
+  }
+  ProfScope prof(S(stream), "colsum", 4.0 * n * rows * cols);
+  if(prof_detail())
+    prof.detail = "group" + std::to_string(n) + "_r" + std::to_string(rows) + "_c" +
+                  std::to_string(cols);
+  ColsumGroup grp{};
+  for(int q = 0; q < n; ++q) {
+    grp.out[q] = outs[q];
+    grp.in[q] = ins[q];
+    grp.acc[q] = accumulate[q];
+  }
+  ::mtkc::launch(colsum_onepass_kernel, dim3((unsigned)slabs, (unsigned)nblk, (unsigned)n), 256, 0,
+                 S(stream), grp, workspace, rows, cols);
+  MTKC_POST_LAUNCH("colsum_onepass_kernel");
   return MTKC_OK;
 }
 

@@ -327,3 +327,33 @@ def test_colsum_deterministic(rows, cols):
     assert np.abs(outs[0] - want).max() <= 1e-5 * np.abs(x).sum(0).max()
     assert np.array_equal(outs[0], outs[1])
     assert np.abs(outs[2] - 2 * want).max() <= 2e-5 * np.abs(x).sum(0).max()
+
+
+def test_colsum_group_matches_single():
+    """mtkc_colsum_group (three bias gradients per launch) equals three
+    mtkc_colsum calls bitwise, with per-problem accumulate flags."""
+    import ctypes as C
+    import torch
+    from paper_1804_00344_b200 import cabi
+    rng = np.random.default_rng(9)
+    rows, cols = 700, 1024
+    xs = [torch.from_numpy(rng.normal(size=(rows, cols)).astype(np.float32)).cuda() for _ in range(3)]
+    base = [torch.from_numpy(rng.normal(size=cols).astype(np.float32)).cuda() for _ in range(3)]
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    acc = [0, 1, 1]
+    single = [b.clone() for b in base]
+    for q in range(3):
+        cabi.check(cabi.lib().mtkc_colsum(C.c_void_p(single[q].data_ptr()), C.c_void_p(xs[q].data_ptr()),
+                                          C.c_int64(rows), C.c_int64(cols), C.c_int(acc[q]),
+                                          C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()),
+                                          C.c_void_p(0)))
+    grouped = [b.clone() for b in base]
+    outs = (C.c_void_p * 3)(*[g.data_ptr() for g in grouped])
+    ins = (C.c_void_p * 3)(*[x.data_ptr() for x in xs])
+    accs = (C.c_int * 3)(*acc)
+    cabi.check(cabi.lib().mtkc_colsum_group(outs, ins, accs, C.c_int(3), C.c_int64(rows),
+                                            C.c_int64(cols), C.c_void_p(ws.data_ptr()),
+                                            C.c_size_t(ws.numel()), C.c_void_p(0)))
+    torch.cuda.synchronize()
+    for q in range(3):
+        assert torch.equal(single[q], grouped[q]), q
