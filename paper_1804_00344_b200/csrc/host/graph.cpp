@@ -456,12 +456,27 @@ NodeRef ExpressionGraph::binary(const std::string& name, EwiseOp op, NodeRef a, 
     pad4(n.shape, od);
     pad4(sa, ad);
     pad4(sb, bd);
+    bool aliased = false;
     for(int which = 0; which < 2; ++which) {
       const Shape& st = which == 0 ? sa : sb;
       int idx = n.inputs[(size_t)which];
       bool same = st == n.shape;
       if(op == EwiseOp::Add && same) {
+        // residual adds: the first operand whose gradient buffer does not
+        // exist yet shares this node's gradient buffer instead of receiving
+        // a copy (only this node reads its own gradient, so later
+        // contributions to the operand may update the shared buffer)
+        Node& in = g.node(g.resolve(idx));
+        if(!aliased && !in.isParam && !in.gate && !in.gradLive && in.grad.empty() &&
+           in.alias < 0 && in.shape == n.shape) {
+          in.grad = n.grad;
+          in.gradLive = true;
+          aliased = true;
+          continue;
+        }
         auto d = g.gradDst(idx);
+        if(d.ptr == go)
+          continue;  // already sharing (an earlier sweep aliased it)
         if(d.accumulate)
           MTKC(mtkc_axpy(d.ptr, go, 1.f, st.size(), stream()));
         else
