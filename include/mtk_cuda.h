@@ -140,6 +140,8 @@ typedef struct mtkc_gemm_args {
   int precision;        /* MTKC_GEMM_FP32 | MTKC_GEMM_TF32                   */
   float* workspace;     /* split-K scratch (may be NULL)                     */
   size_t workspace_bytes;
+  const float* addend;  /* optional: the beta term reads addend (laid out like C)
+                           instead of C -- a fused residual add, C write-only */
 } mtkc_gemm_args;
 
 int mtkc_gemm(const mtkc_gemm_args* args, void* stream);

@@ -27,6 +27,7 @@ class GemmArgs(C.Structure):
         ("alpha", C.c_float), ("beta", C.c_float),
         ("bias", C.c_void_p), ("epilogue", C.c_int), ("gate", C.c_void_p),
         ("precision", C.c_int), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+        ("addend", C.c_void_p),
     ]
 
 
@@ -58,10 +59,10 @@ def check(rc: int):
 
 def gemm(M, N, K, A, lda, B, ldb, Cp, ldc, trans_a=False, trans_b=False, alpha=1.0, beta=0.0,
          bias=None, relu=False, gate=None, precision=1, workspace=None, workspace_bytes=0,
-         stream=None, batch=1, stride_a=0, stride_b=0, stride_c=0):
+         stream=None, batch=1, stride_a=0, stride_b=0, stride_c=0, addend=None):
     g = GemmArgs(M, N, K, batch, A, lda, stride_a, int(trans_a), B, ldb, stride_b, int(trans_b),
                  Cp, ldc, stride_c, alpha, beta, bias, 1 if relu else 0, gate, precision,
-                 workspace, workspace_bytes)
+                 workspace, workspace_bytes, addend)
     check(lib().mtkc_gemm(C.byref(g), stream))
     return lib().mtkc_gemm_last_path()
 

@@ -687,7 +687,7 @@ static NodeRef affineImpl(ExpressionGraph& g, NodeRef x, NodeRef w, NodeRef b, b
   std::vector<int64_t> dims = x.shape.dims();
   dims.back() = N;
   ExpressionGraph::Node n;
-  n.op = relu ? "affineRelu" : "affine";
+  n.op = relu ? "affineRelu" : (transW ? "affineT" : "affine");
   n.shape = Shape(dims);
   n.inputs = {x.index, w.index, b.index};
   int64_t rows = x.shape.size() / K;
@@ -881,6 +881,73 @@ std::vector<NodeRef> ExpressionGraph::affineGroup(NodeRef x, const std::vector<N
     };
   }
   return out;
+}
+
+NodeRef ExpressionGraph::residualAdd(NodeRef r, NodeRef z) {
+  checkRef(r);
+  checkRef(z);
+  Node& zn = nodes_[(size_t)z.index];
+  const bool fusable = Device::get().precision() == Precision::TF32 &&
+                       z.index == (int)nodes_.size() - 1 && zn.op == "affine" && !zn.group &&
+                       zn.alias < 0 && zn.shape == r.shape && r.index != z.index &&
+                       (size_t)z.index >= computed_;
+  if(!fusable)
+    return add(r, z);
+  // z = x op(W) + b  ->  z = x op(W) + b + r : the affine forward with beta = 1
+  // and the addend r (graph.cpp:139-176 add semantics, fused)
+  zn.op = "affineResidual";
+  zn.inputs.push_back(r.index);
+  auto fwd0 = zn.fwd;
+  auto bwd0 = zn.bwd;
+  const int64_t K = nodes_[(size_t)zn.inputs[0]].shape.back();
+  (void)fwd0;
+  const int64_t N = zn.shape.back();
+  const bool transW = false;  // only op "affine" (x W, not x W^T) is folded
+  const int64_t rows = zn.shape.size() / N;
+  zn.fwd = [rows, K, N, transW](ExpressionGraph& g, Node& n) {
+    Device& d = Device::get();
+    mtkc_gemm_args a{};
+    a.M = rows;
+    a.N = N;
+    a.K = K;
+    a.batch = 1;
+    a.A = g.valPtr(n.inputs[0]);
+    a.lda = K;
+    a.B = g.valPtr(n.inputs[1]);
+    a.ldb = transW ? K : N;
+    a.transB = transW;
+    a.C = n.value.dev();
+    a.ldc = N;
+    a.alpha = 1.f;
+    a.beta = 1.f;
+    a.bias = g.valPtr(n.inputs[2]);
+    a.addend = g.valPtr(n.inputs[3]);
+    a.precision = (int)d.precision();
+    a.workspace = d.scratch(64 << 20);
+    a.workspace_bytes = d.scratchBytes();
+    MTKC(mtkc_gemm(&a, d.stream()));
+  };
+  zn.bwd = [bwd0](ExpressionGraph& g, Node& n) {
+    // d(residual) = d(out): share the gradient buffer when the residual
+    // operand has none yet (as the add backward does), else add into it
+    const float* go = g.gradSrc(n);
+    Node& in = g.node(g.resolve(n.inputs[3]));
+    if(!in.isParam && !in.gate && !in.gradLive && in.grad.empty() && in.alias < 0 &&
+       in.shape == n.shape) {
+      in.grad = n.grad;
+      in.gradLive = true;
+    } else {
+      auto d = g.gradDst(n.inputs[3]);
+      if(d.ptr != go) {
+        if(d.accumulate)
+          MTKC(mtkc_axpy(d.ptr, go, 1.f, n.shape.size(), stream()));
+        else
+          MTKC(mtkc_memcpy_d2d(d.ptr, go, (size_t)n.shape.size() * sizeof(float), stream()));
+      }
+    }
+    bwd0(g, n);  // dX, dW, db of the affine part (inputs 0..2)
+  };
+  return z;
 }
 
 NodeRef ExpressionGraph::affine(NodeRef x, NodeRef w, NodeRef b, bool transW) {

@@ -33,6 +33,7 @@ struct GemmP {
   int64_t ldb, sB;
   int tB;
   float* C;
+  const float* Cin;  // source of the beta term: C, or the addend
   int64_t ldc, sC;
   float alpha, beta;
   const float* bias;
@@ -49,6 +50,7 @@ __global__ void __launch_bounds__(256) gemm_fp32_kernel(GemmP p) {
   const int64_t row0 = (int64_t)blockIdx.y * TM, col0 = (int64_t)blockIdx.x * TN;
   const int64_t zb = p.foldBatch ? 0 : blockIdx.z;
   float* C = p.C + zb * p.sC;
+  const float* Cin = p.Cin + zb * p.sC;
   float acc[4][4];
   const bool gated = p.gate != nullptr;
 #pragma unroll
@@ -58,7 +60,7 @@ __global__ void __launch_bounds__(256) gemm_fp32_kernel(GemmP p) {
       int64_t r = row0 + ty * 4 + i, c = col0 + tx * 4 + j;
       float v = 0.f;
       if(!gated && p.beta != 0.f && r < p.M && c < p.N) {
-        v = C[r * p.ldc + c];
+        v = Cin[r * p.ldc + c];
         if(p.beta != 1.f)
           v = __fmul_rn(v, p.beta);
       }
@@ -125,7 +127,8 @@ __global__ void __launch_bounds__(256) gemm_fp32_kernel(GemmP p) {
       if(gated) {
         v = p.gate[zb * p.sC + r * p.ldc + c] > 0.f ? v : 0.f;
         if(p.beta != 0.f)
-          v = __fadd_rn(p.beta == 1.f ? *dst : __fmul_rn(p.beta, *dst), v);
+          v = __fadd_rn(p.beta == 1.f ? Cin[r * p.ldc + c] : __fmul_rn(p.beta, Cin[r * p.ldc + c]),
+                        v);
       }
       *dst = v;
     }
@@ -173,6 +176,7 @@ int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
   p.sB = a->strideB;
   p.tB = a->transB;
   p.C = a->C;
+  p.Cin = a->addend ? a->addend : a->C;
   p.ldc = a->ldc;
   p.sC = a->strideC;
   p.alpha = a->alpha;

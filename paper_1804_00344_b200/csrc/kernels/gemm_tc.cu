@@ -161,13 +161,15 @@ struct TcP {
   // concatenated: k-block kb of the sweep is block kb % nkbProb of problem
   // kb / nkbProb).  Problem 0 is the plain single GEMM.
   int nprob, kconcat, nkbProb;
+  int hasAddend;  // beta term read through maps.r (fused residual), C write-only
+  const float* addend;
   const float* biasP[3];
   float* CP[3];
   int dbg;  // profiling switches (MTK_GEMM_DEBUG): 1 = no epilogue stores, 2 = no MMAs
 };
 
 struct TcMaps {
-  CUtensorMap a[3], b[3], c[3], g;
+  CUtensorMap a[3], b[3], c[3], g, r;  // r: addend (source of the beta term)
 };
 
 template <int BN>
@@ -216,6 +218,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     if(p.gate && p.tmaStore)
       prefetch_tmap(&maps.g);
+    if(p.hasAddend && p.tmaStore)
+      prefetch_tmap(&maps.r);
     for(int w = 0; w < 8; ++w)
       mbar_init(&ldbar[w], 1);
     for(int s = 0; s < ST; ++s) {
@@ -402,7 +406,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if(lane == 0) {
                 mbar_expect_tx(&ldbar[ew], (needC ? 4096u : 0u) + (needG ? 4096u : 0u));
                 if(needC)
-                  tma_load_2d(stage, mapC, &ldbar[ew], (int)col0, (int)rowBase);
+                  tma_load_2d(stage, p.hasAddend ? &maps.r : mapC, &ldbar[ew], (int)col0,
+                              (int)rowBase);
                 if(needG)
                   tma_load_2d(grow, &maps.g, &ldbar[ew], (int)col0, (int)rowBase);
               }
@@ -528,8 +533,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             x = x > 0.f ? x : 0.f;
           if(p.gate)
             x = p.gate[rr * p.ldc + col] > 0.f ? x : 0.f;
-          if(p.beta != 0.f)
-            x = (p.beta == 1.f ? *dst : p.beta * *dst) + x;
+          if(p.beta != 0.f) {
+            const float cv = p.addend ? p.addend[rr * p.ldc + col] : *dst;
+            x = (p.beta == 1.f ? cv : p.beta * cv) + x;
+          }
           *dst = x;
         }
         __syncwarp();
@@ -553,7 +560,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 template <bool VEC>
 __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plane, int64_t M,
                                      int64_t N, float* C, int64_t ldc, float alpha, float beta,
-                                     const float* bias, int epi, const float* gate) {
+                                     const float* bias, int epi, const float* gate,
+                                     const float* Cin) {
   MTKC_PDL_ENTRY();
   const int64_t groups = (N + 3) / 4, total = M * groups;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -585,6 +593,7 @@ __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plan
     }
     float out[4];
     float* dst = C + r * ldc + c;
+    const float* src = Cin + r * ldc + c;
     for(int u = 0; u < 4; ++u) {
       if(!VEC && c + u >= N)
         break;
@@ -596,7 +605,7 @@ __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plan
       if(gate)
         x = gate[r * ldc + c + u] > 0.f ? x : 0.f;
       if(beta != 0.f)
-        x = (beta == 1.f ? dst[u] : beta * dst[u]) + x;
+        x = (beta == 1.f ? src[u] : beta * src[u]) + x;
       out[u] = x;
     }
     if(VEC) {
@@ -725,7 +734,7 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     if(((uintptr_t)b.A % 16) || ((uintptr_t)b.B % 16))
       return false;
   }
-  if(nprob > 1 && a.gate)
+  if(nprob > 1 && (a.gate || a.addend))
     return false;
   if(a.M < 1 || a.N < 8 || a.K < 8)
     return false;
@@ -808,6 +817,8 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   p.epi = a.epilogue;
   p.gate = a.gate;
   p.nprob = nprob;
+  p.addend = a.addend;
+  p.hasAddend = a.addend != nullptr;
   p.kconcat = kconcat;
   p.nkbProb = nkbProb;
   for(int q = 0; q < nOut; ++q) {
@@ -838,6 +849,9 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   if(store && !p.part && a.gate)
     store = ((uintptr_t)a.gate % 16 == 0) &&
             make_store_map(&maps.g, const_cast<float*>(a.gate), a.N, a.M, a.ldc, 1);
+  if(store && !p.part && a.addend)
+    store = ((uintptr_t)a.addend % 16 == 0) &&
+            make_store_map(&maps.r, const_cast<float*>(a.addend), a.N, a.M, a.ldc, 1);
   p.tmaStore = store ? 1 : 0;
   if(getenv("MTK_GEMM_NO_TMA_STORE"))
     p.tmaStore = 0;
@@ -858,10 +872,12 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
       const unsigned grid = grid1d(a.M * cdiv(a.N, 4), 256);
       if(vec)
         ::mtkc::launch(splitk_reduce_kernel<true>, grid, 256, 0, st, part, splits, sstride, a.M,
-                       a.N, b.C, a.ldc, a.alpha, a.beta, b.bias, a.epilogue, a.gate);
+                       a.N, b.C, a.ldc, a.alpha, a.beta, b.bias, a.epilogue, a.gate,
+                       a.addend ? a.addend : b.C);
       else
         ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, part, splits, sstride, a.M,
-                       a.N, b.C, a.ldc, a.alpha, a.beta, b.bias, a.epilogue, a.gate);
+                       a.N, b.C, a.ldc, a.alpha, a.beta, b.bias, a.epilogue, a.gate,
+                       a.addend ? a.addend : b.C);
       count_launch();
       cudaError_t e = cudaGetLastError();
       if(e != cudaSuccess)

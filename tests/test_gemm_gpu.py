@@ -168,3 +168,31 @@ def test_tf32_gemm_group(cuda, shape):
         y = Ys[q].cpu().numpy()
         want = As[0].T.astype(np.float64) @ y
         assert np.all(np.abs(Ws[q].cpu().numpy() - want) <= tol(As[0].T, y)), q
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("shape", [(300, 256, 512), (70, 8192, 96), (33, 40, 50)])
+def test_gemm_addend(cuda, prec, shape):
+    """Fused residual: C = A B + bias + beta * R with R a separate tensor
+    (mtkc_gemm_args.addend); C is write-only.  FP32 and TF32 paths, incl. the
+    split-K reduction (long K) and ragged shapes."""
+    import torch
+    rng = np.random.default_rng(7)
+    M, K, N = shape
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    r = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    A, B, Bi, Rd = (torch.from_numpy(x).cuda() for x in (a, b, bias, r))
+    Cd = torch.full((M, N), float("nan"), device="cuda")
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    cabi.gemm(M, N, K, A.data_ptr(), K, B.data_ptr(), N, Cd.data_ptr(), N, beta=1.0,
+              bias=Bi.data_ptr(), addend=Rd.data_ptr(), precision=prec,
+              workspace=ws.data_ptr(), workspace_bytes=ws.numel())
+    torch.cuda.synchronize()
+    want = a.astype(np.float64) @ b + bias + r
+    tol = 4e-3 * (np.abs(a).astype(np.float64) @ np.abs(b) + 2)
+    got = Cd.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    assert np.all(np.abs(got - want) <= tol)
+    assert torch.equal(Rd.cpu(), torch.from_numpy(r))  # addend untouched
