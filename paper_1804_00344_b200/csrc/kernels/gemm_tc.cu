@@ -352,6 +352,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float* stage0 = sEpi + ew * 2 * 1024;
     int chunk = 0;  // chunks handed to the TMA engine by this warp
     uint32_t ldPhase = 0;  // TMA C / gate box loads completed by this warp
+    // LOADS with one extra source (beta*C / addend, or the ReLU gate): each
+    // lane prefetches its row's 32 values of the NEXT chunk into registers
+    // while the current chunk is processed (the load latency hides behind the
+    // TMEM read and the stores); both sources together use TMA boxes.
+    const bool pf = LOADS && !p.part && p.tmaStore && ((p.beta != 0.f) != (p.gate != nullptr));
+    float nx[32];
+    auto loadChunk = [&](int tt, int cc) {
+      const int pr = p.kconcat ? 0 : tt / tilesPerProb;
+      const int r2 = (tt - pr * tilesPerProb) % tilesPerSplit;
+      const int64_t row = (int64_t)(r2 % p.mt) * BM + q * 32 + lane;
+      const int64_t col = (int64_t)(r2 / p.mt) * BN + cc;
+      const float* src = p.gate ? p.gate : (p.hasAddend ? p.addend : p.CP[pr]);
+      src += row * p.ldc + col;
+      if(row < p.M && col + 32 <= p.N && ((uintptr_t)src & 15) == 0) {
+#pragma unroll
+        for(int j = 0; j < 8; ++j) {
+          const float4 x4 = *reinterpret_cast<const float4*>(src + 4 * j);
+          nx[4 * j] = x4.x;
+          nx[4 * j + 1] = x4.y;
+          nx[4 * j + 2] = x4.z;
+          nx[4 * j + 3] = x4.w;
+        }
+      } else {
+#pragma unroll
+        for(int i = 0; i < 32; ++i)
+          nx[i] = (row < p.M && col + i < p.N) ? src[i] : 0.f;
+      }
+    };
+    if(pf && (int)blockIdx.x < p.numTiles)
+      loadChunk(blockIdx.x, cBeg);
     int lt = 0;
     for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x, ++lt) {
       int m0, n0, kb0, nkb, split;
@@ -366,6 +396,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int zpart = split * nOut + tprob;  // partial plane of this tile
 #pragma unroll 1
       for(int c0 = cBeg; c0 < cEnd; c0 += 32) {
+        float cur[32];
+        if(pf) {
+#pragma unroll
+          for(int i = 0; i < 32; ++i)
+            cur[i] = nx[i];
+          const int tn = c0 + 32 < cEnd ? t : t + (int)gridDim.x;
+          if(tn < p.numTiles)
+            loadChunk(tn, c0 + 32 < cEnd ? c0 + 32 : cBeg);
+        }
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
         if(c0 + 32 >= cEnd) {  // our share read: hand it back to the MMA warp
@@ -381,7 +420,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // the TMA engine must have finished reading this buffer (chunk - 2)
           // before it is refilled: early when a C / gate box lands in it,
           // otherwise as late as possible (after the arithmetic)
-          constexpr bool loads = LOADS;  // host: LOADS iff !part && (beta != 0 || gate)
+          // boxes land in the staging buffer (LOADS without prefetch): wait early
+          const bool loads = LOADS && !pf;
           if(chunk >= 2 && loads) {
             if(lane == 0)
               asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -394,7 +434,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if(!p.part) {
             const bool needC = LOADS && p.beta != 0.f, needG = LOADS && p.gate != nullptr;
             float* grow = stage;  // gate box buffer
-            if(needC || needG) {
+            if((needC || needG) && !pf) {
               // C and/or the ReLU gate arrive as swizzled 32x32 boxes by TMA
               // (coalesced, async) instead of per-lane strided row reads
               if(needC && needG) {
@@ -448,7 +488,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             // ReLU gate, then beta*C, from the TMA-loaded boxes (straight-line
             // loops under uniform branches)
-            if(needG) {
+            if(pf) {
+              if(needG) {
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                  v[i] = cur[i] > 0.f ? v[i] : 0.f;
+              } else {
+                const float beta = p.beta;
+#pragma unroll
+                for(int i = 0; i < 32; ++i)
+                  v[i] = (beta == 1.f ? cur[i] : beta * cur[i]) + v[i];
+              }
+            } else if(needG) {
 #pragma unroll
               for(int j = 0; j < 8; ++j) {
                 const float4 g4 = *reinterpret_cast<const float4*>(grow + ((j ^ sw) * 4));
@@ -458,7 +509,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 v[4 * j + 3] = g4.w > 0.f ? v[4 * j + 3] : 0.f;
               }
             }
-            if(needC) {
+            if(needC && !pf) {
               const float beta = p.beta;
 #pragma unroll
               for(int j = 0; j < 8; ++j) {
