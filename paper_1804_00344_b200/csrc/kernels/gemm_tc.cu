@@ -79,6 +79,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
 }
@@ -162,6 +171,7 @@ struct TcP {
   // kb / nkbProb).  Problem 0 is the plain single GEMM.
   int nprob, kconcat, nkbProb;
   int hasAddend;  // beta term read through maps.r (fused residual), C write-only
+  int a3d, b3d;   // MN-major operand loaded as one 3-d box (all 32-column atoms)
   const float* addend;
   const float* biasP[3];
   float* CP[3];
@@ -283,16 +293,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t* a = sA + s * A_BYTES;
           uint8_t* b = sB + s * B_BYTES;
           if(A_MN) {
-#pragma unroll
-            for(int j = 0; j < BM / 32; ++j)
-              tma_load_2d(a + j * (BK * 128), mapA, &full[s], m0 + j * 32, k0);
+            if(p.a3d)
+              tma_load_3d(a, mapA, &full[s], 0, k0, m0 / 32);
+            else
+              for(int j = 0; j < BM / 32; ++j)
+                tma_load_2d(a + j * (BK * 128), mapA, &full[s], m0 + j * 32, k0);
           } else {
             tma_load_2d(a, mapA, &full[s], k0, m0);
           }
           if(B_MN) {
-#pragma unroll
-            for(int j = 0; j < BN / 32; ++j)
-              tma_load_2d(b + j * (BK * 128), mapB, &full[s], n0 + j * 32, k0);
+            if(p.b3d)
+              tma_load_3d(b, mapB, &full[s], 0, k0, n0 / 32);
+            else
+              for(int j = 0; j < BN / 32; ++j)
+                tma_load_2d(b + j * (BK * 128), mapB, &full[s], n0 + j * 32, k0);
           } else {
             tma_load_2d(b, mapB, &full[s], k0, n0);
           }
@@ -716,6 +730,25 @@ bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int
   return r == CUDA_SUCCESS;
 }
 
+// MN-major operand [rows x cols] (cols contiguous, cols % 32 == 0) as a 3-d
+// tensor (32, rows, cols/32): one box of nbox 32-column atoms x boxRows rows
+// lands exactly like nbox separate 2-d boxes (atom j at j * boxRows * 128 B)
+bool make_map3(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld,
+               uint32_t boxRows, uint32_t nbox) {
+  EncodeFn fn = encode_fn();
+  if(!fn || cols % 32)
+    return false;
+  cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(cols / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
+  cuuint32_t box[3] = {32, boxRows, nbox};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, tma_tf32_round() ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                  3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // store map over C [rows x cols] (ld elements), or over split-K partials
 // [depth][rows][cols]; 32x32 boxes, 128-byte swizzle (matches the staging tile)
 bool make_store_map(CUtensorMap* m, float* base, int64_t cols, int64_t rows, int64_t ld,
@@ -838,16 +871,22 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
 
   TcMaps maps;
   std::memset(&maps, 0, sizeof(maps));
+  const bool no3d = getenv("MTK_GEMM_NO_3D") != nullptr;
+  const bool a3d = aMN && a.M % 32 == 0 && !no3d, b3d = bMN && a.N % 32 == 0 && !no3d;
   for(int q = 0; q < nprob; ++q) {
     const mtkc_gemm_args& b = probs[q];
     bool ok;
-    if(aMN)  // storage [K x M], M contiguous
+    if(aMN && a3d)
+      ok = make_map3(&maps.a[q], b.A, a.M, a.K, a.lda, BK, BM / 32);
+    else if(aMN)  // storage [K x M], M contiguous
       ok = make_map(&maps.a[q], b.A, a.M, a.K, a.lda, 32, BK, true);
     else     // storage [M x K]
       ok = make_map(&maps.a[q], b.A, a.K, a.M, a.lda, BK, BM, false);
     if(!ok)
       return false;
-    if(bMN)  // storage [K x N]
+    if(bMN && b3d)
+      ok = make_map3(&maps.b[q], b.B, a.N, a.K, a.ldb, BK, (uint32_t)BN / 32);
+    else if(bMN)  // storage [K x N]
       ok = make_map(&maps.b[q], b.B, a.N, a.K, a.ldb, 32, BK, true);
     else     // storage [N x K]
       ok = make_map(&maps.b[q], b.B, a.K, a.N, a.ldb, BK, (uint32_t)BN, false);
@@ -868,6 +907,8 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   p.epi = a.epilogue;
   p.gate = a.gate;
   p.nprob = nprob;
+  p.a3d = a3d;
+  p.b3d = b3d;
   p.addend = a.addend;
   p.hasAddend = a.addend != nullptr;
   p.kconcat = kconcat;
