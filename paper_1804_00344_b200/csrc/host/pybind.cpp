@@ -335,6 +335,13 @@ PYBIND11_MODULE(_mtk, m) {
       }))
       .def("rows", &Batch::rows)
       .def("target_tokens", &Batch::targetTokenCount)
+      .def("padded_slots",  // rows x (padded source + padded target length)
+           [](const Batch& b) {
+             int64_t n = 0;
+             for(auto& s : b.sourceIds)
+               n += s.size();
+             return n + b.targetIds.size();
+           })
       .def("source_tokens", &Batch::sourceTokenCount)
       .def("src_ids",
            [](const Batch& b) {
