@@ -41,8 +41,14 @@ __global__ void __launch_bounds__(GT) gru_fwd_kernel(mtkc_gru_args p) {
   const float* hu = p.hu + r * 3 * d;
   const float* xw = hasX ? p.xw + r * 3 * d : nullptr;
   float az[GV], ar[GV], ax[GV];
-  int n = 0;
-  for(int64_t j = threadIdx.x; j < d; j += GT, ++n) {
+#pragma unroll
+  for(int n = 0; n < GV; ++n)
+    az[n] = ar[n] = ax[n] = 0.f;
+#pragma unroll
+  for(int n = 0; n < GV; ++n) {
+    const int64_t j = threadIdx.x + (int64_t)n * GT;
+    if(j >= d)
+      break;
     // gruPre: h*U, then + x*W, then + b (graph.cpp:636-644)
     float z = hu[j], rr = hu[d + j];
     if(hasX) {
@@ -56,7 +62,8 @@ __global__ void __launch_bounds__(GT) gru_fwd_kernel(mtkc_gru_args p) {
   float rsz = 0.f, rsr = 0.f, rsx = 0.f;
   if(ln) {  // two-pass statistics per gate (tensor.cpp:545-572)
     float s[3] = {0.f, 0.f, 0.f};
-    for(int k = 0; k < n; ++k) {
+#pragma unroll
+    for(int k = 0; k < GV; ++k) {  // entries past d are 0
       s[0] += az[k];
       s[1] += ar[k];
       s[2] += ax[k];
@@ -64,7 +71,10 @@ __global__ void __launch_bounds__(GT) gru_fwd_kernel(mtkc_gru_args p) {
     block_sums<3>(s, red);
     float mz = s[0] / (float)d, mr = s[1] / (float)d, mx = s[2] / (float)d;
     float q[3] = {0.f, 0.f, 0.f};
-    for(int k = 0; k < n; ++k) {
+#pragma unroll
+    for(int k = 0; k < GV; ++k) {
+      if(threadIdx.x + (int64_t)k * GT >= d)
+        break;
       float cz = az[k] - mz, cr = ar[k] - mr, cx = ax[k] - mx;
       q[0] += cz * cz;
       q[1] += cr * cr;
@@ -80,8 +90,11 @@ __global__ void __launch_bounds__(GT) gru_fwd_kernel(mtkc_gru_args p) {
       p.lnrs[r * 3 + 2] = rsx;
     }
     float* xh = p.lnc + r * 3 * d;
-    int k = 0;
-    for(int64_t j = threadIdx.x; j < d; j += GT, ++k) {
+    #pragma unroll
+    for(int k = 0; k < GV; ++k) {
+      const int64_t j = threadIdx.x + (int64_t)k * GT;
+      if(j >= d)
+        break;
       float hz = (az[k] - mz) * rsz, hr = (ar[k] - mr) * rsr;
       xh[j] = hz;
       xh[d + j] = hr;
@@ -97,8 +110,11 @@ __global__ void __launch_bounds__(GT) gru_fwd_kernel(mtkc_gru_args p) {
   float* cache = p.cache + r * 3 * d;
   const float* h = p.h + r * d;
   float* ho = p.hout + r * d;
-  int k = 0;
-  for(int64_t j = threadIdx.x; j < d; j += GT, ++k) {
+  #pragma unroll
+  for(int k = 0; k < GV; ++k) {
+    const int64_t j = threadIdx.x + (int64_t)k * GT;
+    if(j >= d)
+      break;
     float z = sigm(az[k]), rr = sigm(ar[k]);
     float ac = ax[k] + (rr * hu[2 * d + j] + p.bh[j]);  // graph.cpp:737-738
     float ht = tanhf(ac);
@@ -125,8 +141,14 @@ __global__ void __launch_bounds__(GT) gru_bwd_kernel(mtkc_gru_args p) {
   const float* h = p.h + r * d;
   const float* go = p.go + r * d;
   float daz[GV], dar[GV], dacv[GV];
-  int n = 0;
-  for(int64_t j = threadIdx.x; j < d; j += GT, ++n) {  // graph.cpp:755-770
+#pragma unroll
+  for(int n = 0; n < GV; ++n)
+    daz[n] = dar[n] = dacv[n] = 0.f;
+#pragma unroll
+  for(int n = 0; n < GV; ++n) {  // graph.cpp:755-770
+    const int64_t j = threadIdx.x + (int64_t)n * GT;
+    if(j >= d)
+      break;
     float g = go[j], z = cache[j], rr = cache[d + j], ht = cache[2 * d + j];
     float dz = g * (h[j] - ht);
     float dht = g * (1.f - z);
@@ -141,8 +163,11 @@ __global__ void __launch_bounds__(GT) gru_bwd_kernel(mtkc_gru_args p) {
     dar[n] = dr * rr * (1.f - rr);
   }
   if(!ln) {
-    int k = 0;
-    for(int64_t j = threadIdx.x; j < d; j += GT, ++k) {
+    #pragma unroll
+    for(int k = 0; k < GV; ++k) {
+      const int64_t j = threadIdx.x + (int64_t)k * GT;
+      if(j >= d)
+        break;
       p.dpz[r * d + j] = daz[k];
       p.dpr[r * d + j] = dar[k];
       if(hasX && p.dax != p.dac)
@@ -153,8 +178,11 @@ __global__ void __launch_bounds__(GT) gru_bwd_kernel(mtkc_gru_args p) {
   const float* xh = p.lnc + r * 3 * d;
   const float rsz = p.lnrs[r * 3], rsr = p.lnrs[r * 3 + 1], rsx = p.lnrs[r * 3 + 2];
   float s[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  int k = 0;
-  for(int64_t j = threadIdx.x; j < d; j += GT, ++k) {
+  #pragma unroll
+  for(int k = 0; k < GV; ++k) {
+    const int64_t j = threadIdx.x + (int64_t)k * GT;
+    if(j >= d)
+      break;
     float hz = daz[k] * p.lnGz[j], hr = dar[k] * p.lnGr[j];
     s[0] += hz;
     s[1] += hz * xh[j];
@@ -169,8 +197,11 @@ __global__ void __launch_bounds__(GT) gru_bwd_kernel(mtkc_gru_args p) {
   block_sums<6>(s, red);
   const float fd = (float)d;
   float* lp = p.lnparts + r * 6 * d;
-  k = 0;
-  for(int64_t j = threadIdx.x; j < d; j += GT, ++k) {
+  #pragma unroll
+  for(int k = 0; k < GV; ++k) {
+    const int64_t j = threadIdx.x + (int64_t)k * GT;
+    if(j >= d)
+      break;
     p.dpz[r * d + j] = ln_dx(daz[k], p.lnGz[j], xh[j], rsz, s[0] / fd, s[1] / fd);
     p.dpr[r * d + j] = ln_dx(dar[k], p.lnGr[j], xh[d + j], rsr, s[2] / fd, s[3] / fd);
     lp[j] = daz[k] * xh[j];
