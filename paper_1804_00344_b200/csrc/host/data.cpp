@@ -2,6 +2,10 @@
 #include "mtk/data.h"
 
 #include <algorithm>
+#include <fstream>
+#include <sstream>
+
+#include <algorithm>
 
 namespace mtk {
 
@@ -168,6 +172,168 @@ std::vector<Batch> makeBatches(const std::vector<Example>& examples, const Batch
   if(skippedCount)
     *skippedCount = skipped;
   return batches;
+}
+
+// ----------------------------------------------------------- Vocabulary
+// (reference data.cpp:13-122; same reserved ids, ordering and errors)
+
+Vocabulary::Vocabulary() {
+  add("</s>");
+  add("<unk>");
+}
+
+void Vocabulary::add(const std::string& token) {
+  if(tok2id_.count(token))
+    throw DataError("duplicate token in vocabulary: " + token);
+  tok2id_[token] = (int32_t)id2tok_.size();
+  id2tok_.push_back(token);
+}
+
+namespace {
+std::vector<std::string> splitTokens(const std::string& line) {
+  std::vector<std::string> out;
+  std::istringstream is(line);
+  std::string tok;
+  while(is >> tok)
+    out.push_back(tok);
+  return out;
+}
+}  // namespace
+
+Vocabulary Vocabulary::build(const std::vector<std::string>& corpusPaths, size_t maxSize) {
+  std::unordered_map<std::string, int64_t> freq;
+  bool any = false;
+  for(auto& path : corpusPaths)
+    for(auto& line : readLines(path))
+      for(auto& tok : splitTokens(line)) {
+        ++freq[tok];
+        any = true;
+      }
+  if(!any)
+    throw DataError("cannot build a vocabulary from an empty corpus");
+  std::vector<std::pair<std::string, int64_t>> sorted(freq.begin(), freq.end());
+  std::sort(sorted.begin(), sorted.end(), [](const auto& a, const auto& b) {
+    if(a.second != b.second)
+      return a.second > b.second;  // descending frequency
+    return a.first < b.first;      // ties lexicographic
+  });
+  Vocabulary v;
+  for(auto& [tok, n] : sorted) {
+    if((size_t)v.size() >= maxSize)
+      break;
+    if(tok == "</s>" || tok == "<unk>")
+      throw DataError("reserved token redefined in corpus: " + tok);
+    v.add(tok);
+  }
+  return v;
+}
+
+Vocabulary Vocabulary::load(const std::string& path) {
+  std::ifstream in(path);
+  if(!in)
+    throw IoError("cannot open vocabulary file: " + path);
+  Vocabulary v;
+  v.id2tok_.clear();
+  v.tok2id_.clear();
+  std::string line;
+  while(std::getline(in, line)) {
+    if(!line.empty() && line.back() == '\r')
+      line.pop_back();
+    v.add(line);
+  }
+  if(v.size() < 2 || v.id2tok_[0] != "</s>" || v.id2tok_[1] != "<unk>")
+    throw DataError("vocabulary file must start with </s> and <unk>: " + path);
+  return v;
+}
+
+void Vocabulary::save(const std::string& path) const {
+  std::ofstream out(path);
+  if(!out)
+    throw IoError("cannot write vocabulary file: " + path);
+  for(auto& tok : id2tok_)
+    out << tok << "\n";
+}
+
+int32_t Vocabulary::id(const std::string& token) const {
+  auto it = tok2id_.find(token);
+  return it == tok2id_.end() ? kUnk : it->second;
+}
+
+const std::string& Vocabulary::token(int32_t id) const {
+  if(id < 0 || id >= size())
+    throw DataError("token id out of range: " + std::to_string(id));
+  return id2tok_[(size_t)id];
+}
+
+std::vector<int32_t> Vocabulary::encode(const std::string& line) const {
+  std::vector<int32_t> out;
+  for(auto& tok : splitTokens(line))
+    out.push_back(id(tok));
+  return out;
+}
+
+std::string Vocabulary::decode(const std::vector<int32_t>& ids) const {
+  std::string out;
+  for(size_t i = 0; i < ids.size(); ++i) {
+    if(ids[i] == kEos)
+      break;
+    if(!out.empty())
+      out += ' ';
+    out += token(ids[i]);
+  }
+  return out;
+}
+
+// ------------------------------------------------------------- corpus IO
+
+std::vector<std::string> readLines(const std::string& path) {
+  std::ifstream in(path);
+  if(!in)
+    throw IoError("cannot open file: " + path);
+  std::vector<std::string> lines;
+  std::string line;
+  while(std::getline(in, line)) {
+    if(!line.empty() && line.back() == '\r')
+      line.pop_back();
+    lines.push_back(line);
+  }
+  return lines;
+}
+
+std::vector<Example> readParallelCorpus(const std::vector<std::string>& sourcePaths,
+                                        const std::string& targetPath,
+                                        const std::vector<const Vocabulary*>& sourceVocabs,
+                                        const Vocabulary* targetVocab) {
+  std::vector<std::vector<std::string>> sourceLines;
+  for(auto& p : sourcePaths)
+    sourceLines.push_back(readLines(p));
+  std::vector<std::string> targetLines;
+  if(!targetPath.empty())
+    targetLines = readLines(targetPath);
+  size_t n = sourceLines.empty() ? targetLines.size() : sourceLines[0].size();
+  for(auto& s : sourceLines)
+    if(s.size() != n)
+      throw DataError("corpus streams are not sentence-aligned");
+  if(!targetPath.empty() && targetLines.size() != n)
+    throw DataError("target corpus not aligned with source corpus");
+  std::vector<Example> out;
+  for(size_t i = 0; i < n; ++i) {
+    Example ex;
+    ex.id = i;
+    for(size_t s = 0; s < sourceLines.size(); ++s)
+      ex.sources.push_back(sourceVocabs[s]->encode(sourceLines[s][i]));
+    if(!targetPath.empty()) {
+      ex.target = targetVocab->encode(targetLines[i]);
+      ex.hasTarget = true;
+    }
+    out.push_back(std::move(ex));
+  }
+  return out;
+}
+
+std::vector<int32_t> invertR2l(std::vector<int32_t> tokens) {
+  std::reverse(tokens.begin(), tokens.end());
+  return tokens;
 }
 
 }  // namespace mtk
