@@ -11,6 +11,7 @@
 #pragma once
 
 #include <iosfwd>
+#include <algorithm>
 #include <map>
 
 #include "mtk/serialize.h"
@@ -40,6 +41,11 @@ public:
   // synchronisation inside the step).
   void updateAsync(ExpressionGraph& g, Real lr, AveragedParameters* avg = nullptr);
   void checkDeferred();
+  // the oldest `steps` unchecked updates were verified finite on the device
+  // (pipelined loss read): they no longer count toward a rollback
+  void markVerified(int64_t steps) { pendingSteps_ = std::max<int64_t>(0, pendingSteps_ - steps); }
+  // device word holding the non-finite flag of the pending updates
+  static const int* flagWord();
   // Single-tensor variant (train.cpp:30-47) with its own moments per name.
   void updateTensor(const std::string& name, Tensor& value, const Tensor& grad, Real lr,
                     int64_t step);
@@ -145,6 +151,14 @@ public:
   // (one synchronisation) unless `readLoss` is false.
   UpdateResult update(const std::vector<const Batch*>& batches, int64_t updateIndex,
                       bool readLoss = true);
+  // Pipelined variant for training loops: launches update `updateIndex`,
+  // queues an asynchronous copy of its loss (and of the non-finite flag) to
+  // pinned host memory, then waits only for the PREVIOUS update's copy and
+  // returns that update's result (loss NaN on the first call).  The host
+  // stays one update ahead of the device; errors surface one update late.
+  UpdateResult updatePipelined(const std::vector<const Batch*>& batches, int64_t updateIndex);
+  // result of the last pipelined update (waits for it)
+  UpdateResult flushPipelined();
   // accumulated host milliseconds in graph build / forward / backward
   std::vector<double> hostTimes() const { return {hostTimes_[0], hostTimes_[1], hostTimes_[2]}; }
 
@@ -160,6 +174,12 @@ private:
   std::vector<void*> events_;        // compute -> comm "bucket ready" events
   void* commDone_ = nullptr;         // comm -> compute "exchange finished"
   int64_t bucketsIssued_ = 0;        // telemetry (tests)
+  // pipelined loss read: two pinned slots {loss, flag} and their events
+  float* pinned_ = nullptr;
+  void* slotEvent_[2] = {nullptr, nullptr};
+  double slotTokens_[2] = {0, 0};
+  int64_t pipeCount_ = 0;
+  UpdateResult collect(int slot);
 
 public:
   int64_t bucketsIssued() const { return bucketsIssued_; }

@@ -498,6 +498,12 @@ PYBIND11_MODULE(_mtk, m) {
              return s.update(batches, u, read);
            },
            py::arg("batches"), py::arg("update_index"), py::arg("read_loss") = true)
+      .def("update_pipelined",
+           [](SyncStepper& s, const std::vector<const Batch*>& batches, int64_t u) {
+             return s.updatePipelined(batches, u);
+           },
+           py::arg("batches"), py::arg("update_index"))
+      .def("flush_pipelined", &SyncStepper::flushPipelined)
       .def("host_times", &SyncStepper::hostTimes)
       .def("buckets_issued", &SyncStepper::bucketsIssued);
 

@@ -309,7 +309,14 @@ SyncStepper::SyncStepper(const Model& model, ExpressionGraph& g, Adam& adam,
   lossAcc_ = std::make_shared<DeviceBuffer>(64);
 }
 
+const int* Adam::flagWord() { return adamFlag(); }
+
 SyncStepper::~SyncStepper() {
+  for(void* e : slotEvent_)
+    if(e)
+      mtkc_event_destroy(e);
+  if(pinned_)
+    mtkc_host_free_pinned(pinned_);
   for(void* e : events_)
     mtkc_event_destroy(e);
   if(commDone_)
@@ -429,6 +436,53 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
     d.checkFlags("training step");
     r.loss = l;
   }
+  return r;
+}
+
+UpdateResult SyncStepper::collect(int slot) {
+  UpdateResult r;
+  r.tokens = slotTokens_[slot];
+  MTKC(mtkc_event_sync(slotEvent_[slot]));
+  const int flag = reinterpret_cast<const int*>(pinned_)[2 * slot + 1];
+  if(flag & MTKC_FLAG_NONFINITE) {
+    adam_.checkDeferred();  // synchronises, rolls back the skipped updates, throws
+  }
+  adam_.markVerified(1);
+  r.loss = pinned_[2 * slot];
+  return r;
+}
+
+UpdateResult SyncStepper::updatePipelined(const std::vector<const Batch*>& batches,
+                                          int64_t updateIndex) {
+  Device& d = Device::get();
+  if(!pinned_) {
+    void* p = nullptr;
+    MTKC(mtkc_host_alloc_pinned(&p, 4 * sizeof(float)));
+    pinned_ = (float*)p;
+    MTKC(mtkc_event_create(&slotEvent_[0]));
+    MTKC(mtkc_event_create(&slotEvent_[1]));
+  }
+  UpdateResult launched = update(batches, updateIndex, false);
+  const int slot = (int)(pipeCount_ & 1);
+  MTKC(mtkc_memcpy_d2h(pinned_ + 2 * slot, lossAcc_->ptr, sizeof(float), d.stream()));
+  MTKC(mtkc_memcpy_d2h(pinned_ + 2 * slot + 1, Adam::flagWord(), sizeof(int), d.stream()));
+  MTKC(mtkc_event_record(slotEvent_[slot], d.stream()));
+  slotTokens_[slot] = launched.tokens;
+  ++pipeCount_;
+  if(pipeCount_ == 1) {
+    UpdateResult r;
+    r.loss = std::nan("");
+    return r;
+  }
+  return collect(1 - slot);  // the previous update
+}
+
+UpdateResult SyncStepper::flushPipelined() {
+  if(pipeCount_ == 0)
+    return UpdateResult{};
+  UpdateResult r = collect((int)((pipeCount_ - 1) & 1));
+  pipeCount_ = 0;
+  Device::get().checkFlags("training step");
   return r;
 }
 

@@ -195,3 +195,40 @@ def test_rnn_step_parity(cuda, arch, ln):
         dlt = np.linalg.norm(g.param_grad(n) - grads[n])
         assert dlt <= 1e-3 * np.linalg.norm(grads[n]) + 1e-6 * G, (n, dlt, np.linalg.norm(grads[n]))
     M.set_precision("tf32")
+
+
+def test_pipelined_updates_equal_synchronous(cuda):
+    """SyncStepper.update_pipelined returns each update's loss one call late;
+    losses and parameters equal the synchronous update() sequence bitwise."""
+    cfg = config_text(arch="transformer", vocab=200, emb=64, heads=4, layers=1)
+    src, tgt = synth.corpus(48, 200)
+    ex = M.Examples([list(map(int, s)) for s in src], [list(map(int, t)) for t in tgt])
+    batches = M.make_batches(ex, 8 * 66, 1, True)
+
+    def run(pipelined):
+        model = M.Model(cfg)
+        g = M.ExpressionGraph(3)
+        model.register_params(g)
+        g.clear()
+        adam = M.Adam(M.adam_defaults_for(cfg))
+        avg = M.AveragedParameters()
+        opts = M.TrainOptions()
+        opts.token_budget = 8 * 66
+        st = M.SyncStepper(model, g, adam, avg, opts)
+        losses = []
+        for u in range(4):
+            if pipelined:
+                r = st.update_pipelined([batches[u]], u)
+                if u > 0:
+                    losses.append(r.loss)
+            else:
+                losses.append(st.update([batches[u]], u, True).loss)
+        if pipelined:
+            losses.append(st.flush_pipelined().loss)
+        return losses, {n: g.param_value(n).copy() for n in g.param_names()}
+
+    l1, p1 = run(False)
+    l2, p2 = run(True)
+    assert l1 == l2
+    for n in p1:
+        assert np.array_equal(p1[n], p2[n]), n
