@@ -29,7 +29,13 @@ namespace mtkc {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 32;  // fp32 elements per 128-byte swizzle row
+#ifndef MTK_BK
+#define MTK_BK 32
+#endif
+// K extent of one pipeline stage: 32 fp32 = one 128-byte swizzle row, or 64
+// (two atom columns per stage: half the barrier round trips per K)
+constexpr int BK = MTK_BK;
+constexpr int KA = BK / 32;  // 128-byte atom columns per K-major stage
 #ifndef MTK_EPI_WARPS
 #define MTK_EPI_WARPS 4
 #endif
@@ -172,6 +178,7 @@ struct TcP {
   int nprob, kconcat, nkbProb;
   int hasAddend;  // beta term read through maps.r (fused residual), C write-only
   int a3d, b3d;   // MN-major operand loaded as one 3-d box (all 32-column atoms)
+  int ak3d, bk3d; // K-major operand with KA > 1: one 3-d box over the atom columns
   const float* addend;
   const float* biasP[3];
   float* CP[3];
@@ -189,7 +196,8 @@ struct TcSmem {
   // pipeline depth: as many stages as fit next to the epilogue staging
   // (227 KB): 6 x 32 KB for BN=128, 4 x 48 KB for BN=256.  fp32 operands
   // make a k-block short in FLOPs, so depth is what covers L2/HBM latency.
-  static constexpr int ST = EPI_WARPS == 8 ? (BN == 256 ? 3 : 5) : (BN == 256 ? 4 : 6);
+  static constexpr int ST = KA == 2 ? (BN == 256 ? 2 : 3)
+                                    : (EPI_WARPS == 8 ? (BN == 256 ? 3 : 5) : (BN == 256 ? 4 : 6));
   // per epilogue warp (8): two 32x32 fp32 staging tiles (128B-swizzled, TMA store)
   static constexpr size_t EPI_BYTES = EPI_WARPS * 2 * 32 * 32 * sizeof(float);
   static constexpr size_t BYTES = 1024 + ST * (size_t)(A_BYTES + B_BYTES) + EPI_BYTES + 256;
@@ -298,8 +306,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             else
               for(int j = 0; j < BM / 32; ++j)
                 tma_load_2d(a + j * (BK * 128), mapA, &full[s], m0 + j * 32, k0);
-          } else {
+          } else if(KA == 1) {
             tma_load_2d(a, mapA, &full[s], k0, m0);
+          } else if(p.ak3d) {  // [KA][BM][32]
+            tma_load_3d(a, mapA, &full[s], 0, m0, k0 / 32);
+          } else {
+            for(int c = 0; c < KA; ++c)
+              tma_load_2d(a + c * (BM * 128), mapA, &full[s], k0 + c * 32, m0);
           }
           if(B_MN) {
             if(p.b3d)
@@ -307,8 +320,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             else
               for(int j = 0; j < BN / 32; ++j)
                 tma_load_2d(b + j * (BK * 128), mapB, &full[s], n0 + j * 32, k0);
-          } else {
+          } else if(KA == 1) {
             tma_load_2d(b, mapB, &full[s], k0, n0);
+          } else if(p.bk3d) {  // [KA][BN][32]
+            tma_load_3d(b, mapB, &full[s], 0, n0, k0 / 32);
+          } else {
+            for(int c = 0; c < KA; ++c)
+              tma_load_2d(b + c * (BN * 128), mapB, &full[s], k0 + c * 32, n0);
           }
         }
       }
@@ -341,10 +359,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // MN-major (SW128 with 32 B atomicity): 128 B of M/N per K-row,
             //   4-row atoms 512 B apart (SBO), 32-element M/N chunks one TMA
             //   box (BK rows) apart (LBO); advance 8 K-rows = 1024 B.
+            // K-major with KA > 1: atom column kk / 4 is a full [rows][32]
+            //   block (rows * 128 B) after the previous one.
             uint64_t ad = A_MN ? umma_desc(aBase + kk * 1024, BK * 128, 512, 1)
-                               : umma_desc(aBase + kk * 32, 16, 1024, 2);
+                               : umma_desc(aBase + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16,
+                                           1024, 2);
             uint64_t bd = B_MN ? umma_desc(bBase + kk * 1024, BK * 128, 512, 1)
-                               : umma_desc(bBase + kk * 32, 16, 1024, 2);
+                               : umma_desc(bBase + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16,
+                                           1024, 2);
             if(!(p.dbg & 2))
               mma_tf32(tacc, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
           }
@@ -749,6 +771,25 @@ bool make_map3(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, in
   return r == CUDA_SUCCESS;
 }
 
+// K-major operand [rows x K] (K contiguous, K % 32 == 0) as a 3-d tensor
+// (32, rows, K/32): one box of KA atom columns x boxRows rows lands as
+// [KA][boxRows][32] (atom column c at c * boxRows * 128 B)
+bool make_mapk3(CUtensorMap* m, const float* base, int64_t K, int64_t rows, int64_t ld,
+                uint32_t boxRows) {
+  EncodeFn fn = encode_fn();
+  if(!fn || K % 32)
+    return false;
+  cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(K / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
+  cuuint32_t box[3] = {32, boxRows, (cuuint32_t)KA};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, tma_tf32_round() ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                  3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // store map over C [rows x cols] (ld elements), or over split-K partials
 // [depth][rows][cols]; 32x32 boxes, 128-byte swizzle (matches the staging tile)
 bool make_store_map(CUtensorMap* m, float* base, int64_t cols, int64_t rows, int64_t ld,
@@ -873,6 +914,8 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   std::memset(&maps, 0, sizeof(maps));
   const bool no3d = getenv("MTK_GEMM_NO_3D") != nullptr;
   const bool a3d = aMN && a.M % 32 == 0 && !no3d, b3d = bMN && a.N % 32 == 0 && !no3d;
+  const bool ak3d = KA > 1 && !aMN && a.K % 32 == 0 && !no3d;
+  const bool bk3d = KA > 1 && !bMN && a.K % 32 == 0 && !no3d;
   for(int q = 0; q < nprob; ++q) {
     const mtkc_gemm_args& b = probs[q];
     bool ok;
@@ -880,16 +923,20 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
       ok = make_map3(&maps.a[q], b.A, a.M, a.K, a.lda, BK, BM / 32);
     else if(aMN)  // storage [K x M], M contiguous
       ok = make_map(&maps.a[q], b.A, a.M, a.K, a.lda, 32, BK, true);
+    else if(ak3d)  // storage [M x K], KA atom columns per stage in one box
+      ok = make_mapk3(&maps.a[q], b.A, a.K, a.M, a.lda, BM);
     else     // storage [M x K]
-      ok = make_map(&maps.a[q], b.A, a.K, a.M, a.lda, BK, BM, false);
+      ok = make_map(&maps.a[q], b.A, a.K, a.M, a.lda, 32, BM, false);
     if(!ok)
       return false;
     if(bMN && b3d)
       ok = make_map3(&maps.b[q], b.B, a.N, a.K, a.ldb, BK, (uint32_t)BN / 32);
     else if(bMN)  // storage [K x N]
       ok = make_map(&maps.b[q], b.B, a.N, a.K, a.ldb, 32, BK, true);
+    else if(bk3d)
+      ok = make_mapk3(&maps.b[q], b.B, a.K, a.N, a.ldb, (uint32_t)BN);
     else     // storage [N x K]
-      ok = make_map(&maps.b[q], b.B, a.K, a.N, a.ldb, BK, (uint32_t)BN, false);
+      ok = make_map(&maps.b[q], b.B, a.K, a.N, a.ldb, 32, (uint32_t)BN, false);
     if(!ok)
       return false;
   }
@@ -909,6 +956,8 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   p.nprob = nprob;
   p.a3d = a3d;
   p.b3d = b3d;
+  p.ak3d = ak3d;
+  p.bk3d = bk3d;
   p.addend = a.addend;
   p.hasAddend = a.addend != nullptr;
   p.kconcat = kconcat;

@@ -6,6 +6,9 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+# A/B runs: an alternative build of the package (tools/ab_*.sh)
+if os.environ.get("MTK_PKG_ROOT"):
+    sys.path.insert(0, os.environ["MTK_PKG_ROOT"])
 
 
 def pytest_configure(config):
