@@ -13,6 +13,7 @@
 //   ref_train             -> train() / trainSync     (train.cpp:200-300, 408-420)
 //   ref_matmul            -> matmulInto              (tensor.cpp:258-306)
 //   ref_op_*              -> single graph ops with a seeded upstream gradient
+#include "mtk/search.h"
 #include "mtk/serialize.h"
 #include "mtk/train.h"
 
@@ -339,6 +340,50 @@ int ref_load_checkpoint(void* h, const char* path, int64_t* counters) {
   return guard([&] {
     auto* m = static_cast<RefModel*>(h);
     loadCheckpoint(path, *m->g, *m->adam, *m->avg, counters[0], counters[1], counters[2]);
+  });
+}
+
+// search.cpp:66-187 beamSearch on batch i with this model (one scorer).
+// Output per sentence, hypotheses in rank order: out_counts[sentence] =
+// number of hypotheses; hypothesis h: out_lens[h] tokens appended to
+// out_tokens, out_scores[h] = score.  Capacities: max_hyps, max_tokens.
+int ref_beam_search(void* h, void* bs, int64_t i, int beam, double alpha, int64_t lenFactor,
+                    int64_t* out_counts, int64_t* out_lens, double* out_scores,
+                    int32_t* out_tokens, int64_t max_hyps, int64_t max_tokens) {
+  return guard([&] {
+    auto* m = static_cast<RefModel*>(h);
+    const Batch& b = static_cast<RefBatches*>(bs)->b[(size_t)i];
+    Scorer sc{"m0", &m->model, m->g.get(), 1.0};
+    SearchOptions o;
+    o.beamSize = beam;
+    o.alpha = alpha;
+    o.maxLengthFactor = lenFactor;
+    auto res = beamSearch({sc}, b, o);
+    int64_t nh = 0, nt = 0;
+    for(size_t s = 0; s < res.size(); ++s) {
+      out_counts[s] = (int64_t)res[s].size();
+      for(auto& hyp : res[s]) {
+        if(nh >= max_hyps || nt + (int64_t)hyp.tokens.size() > max_tokens)
+          throw ContractError("ref_beam_search: output capacity");
+        out_lens[nh] = (int64_t)hyp.tokens.size();
+        out_scores[nh] = hyp.score;
+        for(auto t : hyp.tokens)
+          out_tokens[nt++] = t;
+        ++nh;
+      }
+    }
+  });
+}
+
+// search.cpp:189-215 scoreBatch: per row the total log-probability
+int ref_score_batch(void* h, void* bs, int64_t i, double* out_scores) {
+  return guard([&] {
+    auto* m = static_cast<RefModel*>(h);
+    const Batch& b = static_cast<RefBatches*>(bs)->b[(size_t)i];
+    Scorer sc{"m0", &m->model, m->g.get(), 1.0};
+    auto res = scoreBatch(sc, b);
+    for(size_t r = 0; r < res.size(); ++r)
+      out_scores[r] = res[r].score;
   });
 }
 

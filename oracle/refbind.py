@@ -68,6 +68,8 @@ def lib():
             "ref_adam_update": (I, [P, C.c_float]),
             "ref_train": (I, [P, P, I, I64, U64, I64, I64, C.c_float, I64, dp, lp]),
             "ref_parameter_total": (I64, [C.c_char_p]),
+            "ref_beam_search": (I, [P, P, I64, I, C.c_double, I64, lp, lp, dp, ip, I64, I64]),
+            "ref_score_batch": (I, [P, P, I64, dp]),
             "ref_train_ckpt": (I, [P, P, I, I64, U64, I64, I64, C.c_float, I64, C.c_char_p, I64,
                                    C.c_char_p, dp, lp]),
             "ref_save_model": (I, [P, C.c_char_p]),
@@ -263,6 +265,33 @@ class RefModel:
                                     checkpoint_every, resume_from.encode(), C.byref(fl),
                                     C.byref(up)))
         return fl.value, up.value
+
+    def beam_search(self, batches: "BatchSet", i: int, rows: int, beam=5, alpha=0.6,
+                    len_factor=3):
+        """search.cpp beamSearch: per sentence [(tokens, score), ...] best first."""
+        cap_h, cap_t = rows * beam * 2 + 8, rows * beam * 2 * 256
+        counts = np.zeros(rows, np.int64)
+        lens = np.zeros(cap_h, np.int64)
+        scores = np.zeros(cap_h, np.float64)
+        toks = np.zeros(cap_t, np.int32)
+        _check(lib().ref_beam_search(self.h, batches.h, i, beam, alpha, len_factor, _l(counts),
+                                     _l(lens), scores.ctypes.data_as(C.POINTER(C.c_double)),
+                                     _i(toks), cap_h, cap_t))
+        out, h, t = [], 0, 0
+        for s in range(rows):
+            hyps = []
+            for _ in range(int(counts[s])):
+                n = int(lens[h])
+                hyps.append((toks[t:t + n].tolist(), float(scores[h])))
+                t += n
+                h += 1
+            out.append(hyps)
+        return out
+
+    def score_batch(self, batches: "BatchSet", i: int, rows: int):
+        out = np.zeros(rows, np.float64)
+        _check(lib().ref_score_batch(self.h, batches.h, i, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
 
     def save_model(self, path: str):
         _check(lib().ref_save_model(self.h, path.encode()))

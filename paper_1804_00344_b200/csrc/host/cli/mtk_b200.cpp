@@ -1,23 +1,26 @@
 // mtk-b200: the reference's `mtk` command line (tools/mtk.cpp) for the
 // training path, on the B200 backend.
 //
-// Subcommands: vocab, train (the §8(f) training driver); same option names,
+// Subcommands: vocab, train, translate, score; same option names,
 // defaults, `--config` option files (key: value per line, command line wins,
 // tools/mtk.cpp:429-456) and exit codes: 0 success, 1 usage error, 2 data/io
 // error, 3 numeric error (tools/mtk.cpp:546-594).  CLI11 (absent from the
-// reference tree) is replaced by a small option table.  Decoding subcommands
-// (translate, score, rescore, bleu) are outside the training path.
+// reference tree) is replaced by a small option table.  rescore / bleu are
+// not provided.
 #include <cstdlib>
 #include <fstream>
 #include <functional>
+#include <iomanip>
 #include <iostream>
 #include <map>
+#include <memory>
 #include <sstream>
 #include <string>
 #include <vector>
 
 #include "mtk/data.h"
 #include "mtk/models.h"
+#include "mtk/search.h"
 #include "mtk/serialize.h"
 #include "mtk/train.h"
 
@@ -340,6 +343,138 @@ int runTrain(const TrainArgs& a) {  // tools/mtk.cpp:166-241
   return 0;
 }
 
+struct TranslateArgs {  // tools/mtk.cpp:77-88
+  std::vector<std::string> models, vocabs, inputs;
+  std::string output = "-";
+  std::string nBestFile;
+  int64_t beamSize = 5;
+  double alpha = 0.6;
+  int64_t nBest = 1;
+  int64_t miniBatchTokens = 512;
+  int64_t maxLengthFactor = 3;
+};
+
+struct ScoreArgs {  // tools/mtk.cpp:90-96
+  std::string model;
+  std::vector<std::string> vocabs, inputs;
+  std::string output = "-";
+  int64_t miniBatchTokens = 512;
+};
+
+struct Loaded {
+  std::unique_ptr<ExpressionGraph> graph;
+  Model model;
+};
+
+Loaded loadOne(const std::string& path) {  // tools/mtk.cpp:130-135
+  Loaded lm;
+  lm.graph = std::make_unique<ExpressionGraph>(1, /*inference=*/true);
+  lm.model = loadModel(path, *lm.graph);
+  return lm;
+}
+
+std::ostream& openOutput(const std::string& path, std::ofstream& file) {
+  if(path == "-")
+    return std::cout;
+  file.open(path);
+  if(!file)
+    throw IoError("cannot write output file: " + path);
+  return file;
+}
+
+int runTranslate(const TranslateArgs& a) {  // tools/mtk.cpp:243-292
+  std::vector<Loaded> loaded;
+  for(auto& p : a.models)
+    loaded.push_back(loadOne(p));
+  const ModelConfig& c0 = loaded[0].model.config;
+  for(auto& lm : loaded) {
+    if(lm.model.config.targetVocab != c0.targetVocab)
+      throw DataError("ensemble members disagree on the target vocabulary size");
+    if(lm.model.config.rightLeft != c0.rightLeft)
+      throw DataError("cannot ensemble left-to-right and right-to-left models");
+    if(lm.model.config.sourceArity != c0.sourceArity)
+      throw DataError("ensemble members disagree on the number of source streams");
+  }
+  if((int64_t)a.inputs.size() != (int64_t)c0.sourceArity)
+    throw DataError("expected " + std::to_string(c0.sourceArity) + " input file(s)");
+  if(a.vocabs.size() != a.inputs.size() + 1)
+    throw DataError("--vocabs must list the source vocabularies plus the target vocabulary");
+  std::vector<Vocabulary> vocabs;
+  for(auto& p : a.vocabs)
+    vocabs.push_back(Vocabulary::load(p));
+  std::vector<Scorer> scorers;
+  for(size_t i = 0; i < loaded.size(); ++i)
+    scorers.push_back({"F" + std::to_string(i), &loaded[i].model, loaded[i].graph.get(), 1.0});
+  std::vector<std::vector<std::string>> streams;
+  for(auto& p : a.inputs)
+    streams.push_back(readLines(p));
+  std::vector<Vocabulary> srcVocabs(vocabs.begin(), vocabs.end() - 1);
+  TranslateOptions opts;
+  opts.beamSize = (int)a.beamSize;
+  opts.alpha = a.alpha;
+  opts.nBest = (int)a.nBest;
+  opts.maxLengthFactor = a.maxLengthFactor;
+  opts.tokenBudget = a.miniBatchTokens;
+  TranslateOutput result = translateLines(scorers, vocabs.back(), streams, srcVocabs, opts);
+  std::ofstream file;
+  std::ostream& out = openOutput(a.output, file);
+  for(auto& line : result.best)
+    out << line << "\n";
+  if(!a.nBestFile.empty()) {
+    std::ofstream nb(a.nBestFile);
+    if(!nb)
+      throw IoError("cannot write n-best file: " + a.nBestFile);
+    for(auto& line : result.nbestLines)
+      nb << line << "\n";
+  }
+  std::cerr << "translated " << result.best.size() << " sentences, " << std::fixed
+            << std::setprecision(1) << result.wordsPerSecond << " words/s\n";
+  return 0;
+}
+
+int runScore(const ScoreArgs& a) {  // tools/mtk.cpp:294-340
+  Loaded lm = loadOne(a.model);
+  const ModelConfig& cfg = lm.model.config;
+  if((int64_t)a.inputs.size() != (int64_t)cfg.sourceArity + 1)
+    throw DataError("expected " + std::to_string(cfg.sourceArity) +
+                    " source file(s) plus one target file");
+  if(a.vocabs.size() != a.inputs.size())
+    throw DataError("--vocabs must list one vocabulary per input file");
+  std::vector<Vocabulary> vocabs;
+  for(auto& p : a.vocabs)
+    vocabs.push_back(Vocabulary::load(p));
+  std::vector<const Vocabulary*> srcV;
+  std::vector<std::string> srcPaths;
+  for(size_t i = 0; i + 1 < a.inputs.size(); ++i) {
+    srcV.push_back(&vocabs[i]);
+    srcPaths.push_back(a.inputs[i]);
+  }
+  auto data = readParallelCorpus(srcPaths, a.inputs.back(), srcV, &vocabs.back());
+  if(cfg.rightLeft)
+    for(auto& ex : data)
+      ex.target = invertR2l(ex.target);
+  std::vector<Hypothesis> results(data.size());
+  BatchOptions bo;
+  bo.tokenBudget = a.miniBatchTokens;
+  bo.shuffle = false;
+  Scorer scorer{"F0", &lm.model, lm.graph.get(), 1.0};
+  for(auto& batch : makeBatches(data, bo)) {
+    auto scored = scoreBatch(scorer, batch);
+    for(size_t r = 0; r < scored.size(); ++r)
+      results[batch.sentenceIds[r]] = std::move(scored[r]);
+  }
+  std::ofstream file;
+  std::ostream& out = openOutput(a.output, file);
+  out << std::fixed << std::setprecision(6);
+  for(size_t i = 0; i < results.size(); ++i) {
+    out << i << ' ' << results[i].score;
+    for(double sc : results[i].tokenScores)
+      out << ' ' << sc;
+    out << "\n";
+  }
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -381,19 +516,46 @@ int main(int argc, char** argv) {
   train.add("quiet", Opt::Flag, &ta.quiet, "suppress progress output");
   train.add("seed", Opt::Int, &ta.seed, "random seed (default: MTK_SEED or 1)");
 
+  TranslateArgs xa;
+  Command translate{"translate", "translate text", {}};
+  translate.add("models", Opt::StrList, &xa.models, "model file(s); several = ensemble", true);
+  translate.add("vocabs", Opt::StrList, &xa.vocabs, "source vocab(s) then target vocab", true);
+  translate.add("input", Opt::StrList, &xa.inputs, "input file per source stream", true);
+  translate.add("output", Opt::Str, &xa.output, "output file ('-' = stdout)");
+  translate.add("n-best-file", Opt::Str, &xa.nBestFile, "write the n-best list here");
+  translate.add("beam-size", Opt::Int, &xa.beamSize, "beam size");
+  translate.add("alpha", Opt::Num, &xa.alpha, "length normalization exponent");
+  translate.add("n-best", Opt::Int, &xa.nBest, "hypotheses per sentence in the n-best list");
+  translate.add("mini-batch-tokens", Opt::Int, &xa.miniBatchTokens, "token budget per batch");
+  translate.add("max-length-factor", Opt::Int, &xa.maxLengthFactor,
+                "maximum output length as a multiple of the source length");
+
+  ScoreArgs sa;
+  Command score{"score", "force-decode and print log-probabilities", {}};
+  score.add("model", Opt::Str, &sa.model, "model file", true);
+  score.add("vocabs", Opt::StrList, &sa.vocabs, "vocabulary per input file", true);
+  score.add("input", Opt::StrList, &sa.inputs, "source file(s) then target file", true);
+  score.add("output", Opt::Str, &sa.output, "output file ('-' = stdout)");
+  score.add("mini-batch-tokens", Opt::Int, &sa.miniBatchTokens, "token budget per batch");
+
   std::vector<std::string> args(argv + 1, argv + argc);
   Command* cmd = nullptr;
   try {
     if(args.empty() || args[0] == "--help" || args[0] == "-h") {
-      std::cerr << "usage: mtk-b200 {vocab|train} [options]; --help per subcommand\n";
+      std::cerr << "usage: mtk-b200 {vocab|train|translate|score} [options]; --help per "
+                   "subcommand\n";
       return args.empty() ? 1 : 0;
     }
     if(args[0] == "vocab")
       cmd = &vocab;
     else if(args[0] == "train")
       cmd = &train;
+    else if(args[0] == "translate")
+      cmd = &translate;
+    else if(args[0] == "score")
+      cmd = &score;
     else
-      throw UsageError("unknown subcommand '" + args[0] + "' (vocab, train)");
+      throw UsageError("unknown subcommand '" + args[0] + "' (vocab, train, translate, score)");
     parse(*cmd, std::vector<std::string>(args.begin() + 1, args.end()));
   } catch(const UsageError& e) {
     std::cerr << e.what() << "\n";
@@ -406,7 +568,13 @@ int main(int argc, char** argv) {
     return 2;
   }
   try {
-    return cmd == &vocab ? runVocab(va) : runTrain(ta);
+    if(cmd == &vocab)
+      return runVocab(va);
+    if(cmd == &train)
+      return runTrain(ta);
+    if(cmd == &translate)
+      return runTranslate(xa);
+    return runScore(sa);
   } catch(const DataError& e) {
     std::cerr << "data error: " << e.what() << "\n";
     return 2;

@@ -8,6 +8,7 @@
 #include <sstream>
 
 #include "mtk/device.h"
+#include "mtk/search.h"
 #include "mtk/train.h"
 
 namespace py = pybind11;
@@ -392,6 +393,34 @@ PYBIND11_MODULE(_mtk, m) {
       .def_property_readonly("config", [](const Model& mo) { return mo.config; })
       .def("register_params", &Model::registerParams)
       .def("build_loss", [](const Model& mo, G& g, const Batch& b) { return mo.buildLoss(g, b); });
+
+  // decoding (search.cpp): per sentence [(tokens, score, token_scores), ...]
+  m.def(
+      "beam_search",
+      [](const Model& mo, G& g, const Batch& b, int beam, double alpha, int64_t lenFactor) {
+        SearchOptions o;
+        o.beamSize = beam;
+        o.alpha = alpha;
+        o.maxLengthFactor = lenFactor;
+        auto res = beamSearch({Scorer{"m0", &mo, &g, 1.0}}, b, o);
+        py::list out;
+        for(auto& list : res) {
+          py::list hyps;
+          for(auto& h : list)
+            hyps.append(py::make_tuple(h.tokens, h.score, h.tokenScores));
+          out.append(hyps);
+        }
+        return out;
+      },
+      py::arg("model"), py::arg("graph"), py::arg("batch"), py::arg("beam") = 5,
+      py::arg("alpha") = 0.6, py::arg("max_length_factor") = 3);
+  m.def("score_batch", [](const Model& mo, G& g, const Batch& b) {
+    auto res = scoreBatch(Scorer{"m0", &mo, &g, 1.0}, b);
+    py::list out;
+    for(auto& h : res)
+      out.append(py::make_tuple(h.tokens, h.score, h.tokenScores));
+    return out;
+  });
 
   m.def("parameter_total", [](const std::string& cfg) {
     return parameterTotal(ModelConfig::parse(cfg));

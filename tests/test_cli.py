@@ -24,7 +24,7 @@ def write(path, lines):
 
 def test_cli_usage_and_data_errors(tmp_path):
     assert run().returncode == 1
-    assert run("translate").returncode == 1            # outside the training path
+    assert run("translate").returncode == 1            # missing required options
     assert run("train", "--model", "m").returncode == 1  # missing required options
     assert run("train", "--bogus", "1").returncode == 1
     r = run("vocab", "--corpus", str(tmp_path / "missing.txt"), "--output", str(tmp_path / "v"))
@@ -85,3 +85,58 @@ def test_cli_train_matches_reference(cuda, tmp_path):
     for n in ref.param_names():
         a, b = g.param_value(n), ref.param(n)
         assert np.allclose(a, b, rtol=1e-6, atol=1e-6 * max(1.0, np.abs(b).max())), n
+
+
+@pytest.mark.gpu
+def test_cli_translate_and_score(cuda, tmp_path):
+    """`translate` (beam search, n-best file in the reference's
+    "id ||| text ||| F0=... ||| score" format) and `score` (forced decoding)
+    on a model trained by `train`; outputs agree with the Python API
+    (beam_search / score_batch, themselves pinned to the reference in
+    tests/test_search_gpu.py)."""
+    from paper_1804_00344_b200 import mtk as M, synth
+    V = 40
+    src, tgt = synth.corpus(24, V)
+    tok = lambda ids: " ".join(f"w{int(i)}" for i in ids)
+    s_path = write(tmp_path / "s.txt", [tok(s) for s in src])
+    t_path = write(tmp_path / "t.txt", [tok(t) for t in tgt])
+    vocab = write(tmp_path / "vocab.txt", ["</s>", "<unk>"] + [f"w{i}" for i in range(2, V)])
+    model = str(tmp_path / "model.mtk")
+    env = dict(os.environ, MTK_PRECISION="fp32")
+    r = run("train", "--model", model, "--train-sets", s_path, t_path, "--vocabs", vocab, vocab,
+            "--arch", "transformer", "--emb-dim", "32", "--heads", "2", "--layers", "1",
+            "--dropout", "0", "--tying", "all", "--max-updates", "20", "--lr", "0.01",
+            "--warmup", "1", "--mini-batch-tokens", "400", "--quiet", env=env)
+    assert r.returncode == 0, r.stderr
+    out, nb = tmp_path / "out.txt", tmp_path / "nbest.txt"
+    r = run("translate", "--models", model, "--vocabs", vocab, vocab, "--input", s_path,
+            "--output", str(out), "--n-best-file", str(nb), "--n-best", "2", "--beam-size", "3",
+            "--mini-batch-tokens", "4096", env=env)
+    assert r.returncode == 0, r.stderr
+    best = out.read_text().split("\n")[:-1]
+    assert len(best) == len(src)
+    lines = nb.read_text().split("\n")[:-1]
+    assert all(len(ln.split(" ||| ")) == 4 and " F0=" in ln for ln in lines)
+    r = run("score", "--model", model, "--vocabs", vocab, vocab, "--input", s_path, t_path,
+            "--output", str(tmp_path / "scores.txt"), env=env)
+    assert r.returncode == 0, r.stderr
+    scores = [float(ln.split()[1]) for ln in (tmp_path / "scores.txt").read_text().split("\n")[:-1]]
+    assert len(scores) == len(src)
+
+    M.set_precision("fp32")
+    try:
+        m = M.Model(M.read_model_config(model))
+        g = M.ExpressionGraph(1)
+        m.register_params(g)
+        M.load_params(model, g)
+        ex = M.Examples([list(map(int, s)) for s in src], [list(map(int, t)) for t in tgt])
+        for b in M.make_batches(ex, 100000, 1, False):
+            ids = b.sentence_ids()
+            hyps = M.beam_search(m, g, b, beam=3, alpha=0.6, max_length_factor=3)
+            sc = M.score_batch(m, g, b)
+            for r_, sid in enumerate(ids):
+                toks = [t for t in hyps[r_][0][0] if t != 0]
+                assert best[sid] == tok(toks), sid
+                assert abs(scores[sid] - sc[r_][1]) <= 1e-5 * max(1.0, abs(sc[r_][1])), sid
+    finally:
+        M.set_precision("tf32")
