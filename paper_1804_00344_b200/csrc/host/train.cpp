@@ -375,11 +375,15 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
       // passed the lowest-index consumer of every parameter in it, the
       // compute stream records an event and the comm stream all-reduces
       // the range while the backward continues.
+      // Every rank issues the buckets in the same graph-independent order
+      // (descending pool offset: parameters created last, whose gradients
+      // the sweep finalises first, go first), each once it and all buckets
+      // before it are final -- NCCL needs identical collective sequences
+      // on all ranks, whatever each rank's batch shape.
       auto buckets = g_.gradBuckets(opts_.bucketElems);
-      std::sort(buckets.begin(), buckets.end(),
-                [](const ExpressionGraph::GradBucket& a, const ExpressionGraph::GradBucket& b) {
-                  return a.readyAfter > b.readyAfter;
-                });
+      std::stable_sort(buckets.begin(), buckets.end(),
+                       [](const ExpressionGraph::GradBucket& a,
+                          const ExpressionGraph::GradBucket& b) { return a.begin > b.begin; });
       while(events_.size() < buckets.size()) {
         void* e = nullptr;
         MTKC(mtkc_event_create(&e));
@@ -417,9 +421,19 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
       // compute stream waits for the last bucket before Adam reads the pool
       MTKC(mtkc_event_record(commDone_, commStream_));
       MTKC(mtkc_stream_wait_event(d.stream(), commDone_));
+    } else if(overlap) {
+      // rank without a batch at the epoch tail: zero gradients, the same
+      // bucket sequence as the working ranks (identical collective order)
+      g_.realizeParamGrads();
+      auto buckets = g_.gradBuckets(opts_.bucketElems);
+      std::stable_sort(buckets.begin(), buckets.end(),
+                       [](const ExpressionGraph::GradBucket& a,
+                          const ExpressionGraph::GradBucket& b) { return a.begin > b.begin; });
+      float* grads = g_.pool().grads()->ptr;
+      for(auto& b : buckets)
+        MTKC(mtkc_allreduce_sum(dc.comm, grads + b.begin, b.end - b.begin, d.stream()));
     } else {
-      // rank without a batch at the epoch tail, or overlap disabled: the
-      // whole pool in one all-reduce (idle ranks contribute zeros)
+      // overlap disabled: the whole pool in one all-reduce
       g_.realizeParamGrads();
       MTKC(mtkc_allreduce_sum(dc.comm, g_.pool().grads()->ptr, g_.pool().used(), d.stream()));
     }
