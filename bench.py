@@ -31,6 +31,10 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# load every kernel image when the context is created (before timing), not
+# at a variant's first launch inside a timed step (lazy loading stalls a
+# fresh box for tens of milliseconds on a cold file cache)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 sys.path.insert(0, os.environ.get("MTK_PKG_ROOT") or ROOT)
 
 METRIC = "target words/sec, Transformer-base training step at 1/2/4/8 B200"
@@ -238,15 +242,20 @@ def run_b200(a):
     clocks.start()
     l0 = M.launch_count()
     e0 = M.event_record()
+    marks = [e0]
     words = 0.0
     th0 = time.perf_counter()
     for _ in range(a.steps):
         grp = group(u)
         words += sum(b.target_tokens() for b in grp)
         stepper.update(grp, u, False)
+        marks.append(M.event_record())  # per-step device time (diagnostics)
         u += 1
     host_ms = (time.perf_counter() - th0) * 1e3 / a.steps
-    e1 = M.event_record()
+    e1 = marks[-1]
+    step_list = [M.event_elapsed_ms_keep(marks[i], marks[i + 1]) for i in range(a.steps)]
+    for m in marks[1:-1]:
+        M.event_destroy(m)
     ms = M.event_elapsed_ms(e0, e1)
     launches = M.launch_count() - l0
     clk = clocks.stop()
@@ -344,6 +353,9 @@ def run_b200(a):
                     "loss_last": losses[-1] if losses else None},
             "gpu_launches": int(launches),
             "host_submit_ms_per_step": round(host_ms, 3),
+            "step_ms": {"min": round(min(step_list), 3),
+                        "median": round(statistics.median(step_list), 3),
+                        "max": round(max(step_list), 3)},
             "roofline": roof,
             "kernel_breakdown": breakdown,
             "cpu_baseline": cpu,

@@ -127,6 +127,13 @@ PYBIND11_MODULE(_mtk, m) {
     MTKC(mtkc_event_record(e, Device::get().stream()));
     return (uintptr_t)e;
   });
+  m.def("event_elapsed_ms_keep", [](uintptr_t a, uintptr_t b) {  // events stay alive
+    Device::get().sync();
+    float ms = 0;
+    MTKC(mtkc_event_elapsed_ms((void*)a, (void*)b, &ms));
+    return ms;
+  });
+  m.def("event_destroy", [](uintptr_t a) { mtkc_event_destroy((void*)a); });
   m.def("event_elapsed_ms", [](uintptr_t a, uintptr_t b) {
     Device::get().sync();
     float ms = 0;

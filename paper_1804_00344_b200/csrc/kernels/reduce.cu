@@ -127,14 +127,16 @@ __global__ void __launch_bounds__(256) colsum_onepass_kernel(ColsumGroup grp, fl
   }
   red[w][lane] = s0;
   __syncthreads();
-  if(w == 0 && c < cols) {
-    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+  if(w == 0) {
+    if(c < cols) {
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for(int k = 0; k < 8; ++k)
-      f4add(t, red[k][lane]);
-    *reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * cols + c) = t;
+      for(int k = 0; k < 8; ++k)
+        f4add(t, red[k][lane]);
+      *reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * cols + c) = t;
+    }
+    __threadfence();  // only the writers publish before the ticket
   }
-  __threadfence();
   __syncthreads();
   if(threadIdx.x == 0) {
     const unsigned prev = atomicAdd(&g_colsum_ticket[z * gridDim.x + blockIdx.x], 1u);
