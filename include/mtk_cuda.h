@@ -323,12 +323,15 @@ int mtkc_attention_tc(float* out, int64_t ldo, float* probs, const float* q, int
                       const float* k, const float* v, int64_t ldk, const float* key_mask,
                       int64_t b, int64_t tq, int64_t tk, int heads, int64_t dk, float scale,
                       int causal, int* flags, void* stream);
+/* colpart (optional, [3][b][heads*dk]): per sentence, the column sums of
+ * this call's dq / dk / dv contributions -- the bias gradients of the q/k/v
+ * projections after a [b]-row column sum, without re-reading dq/dk/dv. */
 int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* probs,
                                const float* q, int64_t ldq, const float* k, const float* v,
                                int64_t ldk, float* gq, float* gk, float* gv, int64_t b,
                                int64_t tq, int64_t tk, int heads, int64_t dk, float scale,
                                int accumulate_q, int accumulate_k, int accumulate_v,
-                               void* stream);
+                               float* colpart, void* stream);
 
 /* ======================================================================== */
 /* fused GRU block, pointwise part (gruCell graph.cpp:648-813, gruPre        */

@@ -210,6 +210,7 @@ ExpressionGraph::GradDst ExpressionGraph::gradDst(int nodeIndex, bool supportsGa
   }
   if(n.grad.empty())
     n.grad = allocTensor(n.shape);
+  ++n.gradTouch;
   int acc = n.gradLive ? 1 : 0;
   n.gradLive = true;
   if(n.gate && !supportsGate)
@@ -735,6 +736,14 @@ struct AffineGroup {
   int64_t rows = 0, K = 0, N = 0;
   bool fwdDone = false;
   uint64_t bwdDone = ~0ull;  // backward sweep that already ran the group
+  // column sums of the members' output gradients produced by their consumer
+  // (the attention backward): [3][colRows][N], slot per member; valid for
+  // the sweep colValid while no one else touched the gradients
+  Tensor colpart;
+  int64_t colRows = 0;
+  uint64_t colValid = ~0ull;
+  int colSlot[3] = {-1, -1, -1};
+  uint32_t colTouch[3] = {0, 0, 0};
 };
 
 mtkc_gemm_args groupArgs(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
@@ -865,17 +874,25 @@ std::vector<NodeRef> ExpressionGraph::affineGroup(NodeRef x, const std::vector<N
                  dw[q].accumulate ? 1.f : 0.f);
         }
       }
-      {  // db_j: one launch
+      {  // db_j: one launch, over the consumer's per-sentence column sums
+         // when the attention backward produced them, else over dY
         float* outs[3];
+        const float* ins[3];
         int acc[3];
+        bool useCol = grp->colValid == g.backwardCount_;
+        for(size_t q = 0; q < live.size() && useCol; ++q)
+          useCol = grp->colSlot[live[q]] >= 0 &&
+                   g.node(grp->members[live[q]]).gradTouch == grp->colTouch[live[q]];
+        const int64_t crow = useCol ? grp->colRows : rows;
         for(size_t q = 0; q < live.size(); ++q) {
           auto d = g.gradDst(grp->b[live[q]]);
           outs[q] = d.ptr;
           acc[q] = d.accumulate;
+          ins[q] = useCol ? grp->colpart.devc() + grp->colSlot[live[q]] * grp->colRows * N : dY[q];
         }
-        size_t ws = live.size() * (size_t)((rows + 63) / 64) * (size_t)N * sizeof(float);
+        size_t ws = live.size() * (size_t)((crow + 63) / 64) * (size_t)N * sizeof(float);
         float* w = dev.scratch(ws);
-        MTKC(mtkc_colsum_group(outs, dY, acc, (int)live.size(), rows, N, w, dev.scratchBytes(),
+        MTKC(mtkc_colsum_group(outs, ins, acc, (int)live.size(), crow, N, w, dev.scratchBytes(),
                                dev.stream()));
       }
     };
@@ -1438,10 +1455,35 @@ NodeRef ExpressionGraph::attention(NodeRef q, NodeRef k, NodeRef v, const Tensor
     auto dkk = g.gradDst(n.inputs[1]);
     auto dv = g.gradDst(n.inputs[2]);
     if(tensorCore) {
+      // grouped q/k/v projections written fresh here: let the kernel emit
+      // their per-sentence column sums (the bias gradients without a re-read)
+      float* colpart = nullptr;
+      auto grp = std::static_pointer_cast<AffineGroup>(g.node(n.inputs[1]).group);
+      if(grp && !dkk.accumulate && !dv.accumulate) {
+        int slots[3] = {-1, -1, -1};
+        bool ok = grp->members.size() <= 3;
+        for(size_t j = 0; j < grp->members.size() && ok; ++j) {
+          const int idx = grp->members[j];
+          const int slot = idx == n.inputs[0] ? 0 : idx == n.inputs[1] ? 1
+                                                 : idx == n.inputs[2] ? 2 : -1;
+          ok = slot >= 0 && !(slot == 0 && dq.accumulate);
+          slots[j] = slot;
+        }
+        if(ok) {
+          grp->colpart = g.allocTensor(Shape({3, b, d}));
+          grp->colRows = b;
+          for(size_t j = 0; j < grp->members.size(); ++j) {
+            grp->colSlot[j] = slots[j];
+            grp->colTouch[j] = g.node(grp->members[j]).gradTouch;
+          }
+          grp->colValid = g.backwardCount_;
+          colpart = grp->colpart.dev();
+        }
+      }
       MTKC(mtkc_attention_tc_backward(go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d,
                                       g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d, dq.ptr,
                                       dkk.ptr, dv.ptr, b, tq, tk, heads, dk, scale, dq.accumulate,
-                                      dkk.accumulate, dv.accumulate, stream()));
+                                      dkk.accumulate, dv.accumulate, colpart, stream()));
       return;
     }
     Tensor ds = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));

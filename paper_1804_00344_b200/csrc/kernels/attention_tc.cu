@@ -102,6 +102,7 @@ struct TcAttBP {
   int tq, tk, heads;
   float scale;
   int accQ, accK, accV;
+  float* colpart;  // optional [3][b][heads*64]: column sums of this CTA's dq/dk/dv
 };
 
 // strides (floats): L4 = 4*odd mod 32 for row-fragment reads (g*L + t),
@@ -119,7 +120,26 @@ constexpr size_t fwd_smem() {
 }
 template <int TT>
 constexpr size_t bwd_smem() {
-  return sizeof(float) * ((size_t)TT * L8 * 2 + (size_t)TT * L4 * 2 + 2 * (size_t)TT * PStride<TT>::v);
+  return sizeof(float) * ((size_t)TT * L8 * 2 + (size_t)TT * L4 * 2 +
+                          2 * (size_t)TT * PStride<TT>::v + 3 * (TT / 16) * DKT);
+}
+
+// column sums of a warp's 16 x 64 accumulator tile: sum rows (g, g+8) of
+// each lane, then across the 8 lanes sharing t; lanes with g == 0 hold the
+// totals of columns jd*8 + 2t + {0,1}
+__device__ __forceinline__ void tile_colsum(const float (&o)[DKT / 8][4], float* dst, int g,
+                                            int t) {
+#pragma unroll
+  for(int jd = 0; jd < DKT / 8; ++jd)
+#pragma unroll
+    for(int e = 0; e < 2; ++e) {
+      float v = o[jd][e] + o[jd][2 + e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      if(g == 0)
+        dst[jd * 8 + 2 * t + e] = v;
+    }
 }
 
 template <int TT>
@@ -277,6 +297,7 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
   float* dO = V + TT * L4;                      // [TT][L4]
   float* P = dO + TT * L4;                      // [TT][LP]
   float* dS = P + TT * LP;                      // [TT][LP]
+  float* csum = dS + TT * LP;                   // [3][TT/16][64] per-warp column sums
   const int h = blockIdx.x, bi = blockIdx.y;
   const int tq = p.tq, tk = p.tk;
   const int hoff = h * DKT;
@@ -295,6 +316,8 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
       cp_async4(P + r * LP + c, gP + (ok ? r * tk + c : 0), ok);
     }
   }
+  for(int e = threadIdx.x; e < 3 * (TT / 16) * DKT; e += TT * 2)
+    csum[e] = 0.f;
   cp_async_wait_all();
   __syncthreads();
 
@@ -302,6 +325,7 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
   const int g = lane >> 2, t = lane & 3;
   const int m0 = warp * 16;
   const int r0 = m0 + g, r1 = r0 + 8;
+  constexpr int NWB = TT / 16;
 
   // phase 1 (query rows m0..m0+15): dP = dO V^T, D = rowsum(dP*P),
   // dS = scale * P * (dP - D)   (graph.cpp:539-552 with the MHA scale)
@@ -374,6 +398,8 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
       if(r1 < tq)
         store2(gq + (int64_t)r1 * p.ldq + col, o[jd][2], o[jd][3], p.accQ);
     }
+    if(p.colpart)  // padded rows contribute exact zeros
+      tile_colsum(o, csum + (0 * NWB + warp) * DKT, g, t);
   }
   // phase 3 (key rows m0..m0+15): dK = dS^T Q, dV = P^T dO
   if(m0 < tk) {
@@ -413,6 +439,22 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
         store2(gk + (int64_t)r1 * p.ldk + col, ok[jd][2], ok[jd][3], p.accK);
         store2(gv + (int64_t)r1 * p.ldk + col, ov[jd][2], ov[jd][3], p.accV);
       }
+    }
+    if(p.colpart) {
+      tile_colsum(ok, csum + (1 * NWB + warp) * DKT, g, t);
+      tile_colsum(ov, csum + (2 * NWB + warp) * DKT, g, t);
+    }
+  }
+  if(p.colpart) {  // this CTA's column sums, warps combined in fixed order
+    __syncthreads();
+    const int64_t hd = (int64_t)p.heads * DKT, B = gridDim.y;
+    for(int e = threadIdx.x; e < 3 * DKT; e += TT * 2) {
+      const int which = e / DKT, c = e % DKT;
+      float v = 0.f;
+#pragma unroll
+      for(int w = 0; w < NWB; ++w)
+        v += csum[(which * NWB + w) * DKT + c];
+      p.colpart[((int64_t)which * B + bi) * hd + hoff + c] = v;
     }
   }
 }
@@ -479,7 +521,7 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
                                int64_t ldk, float* gq, float* gk, float* gv, int64_t b,
                                int64_t tq, int64_t tk, int heads, int64_t dk, float scale,
                                int accumulate_q, int accumulate_k, int accumulate_v,
-                               void* stream) {
+                               float* colpart, void* stream) {
   if(b <= 0 || tq <= 0 || tk <= 0)
     return MTKC_OK;
   int tt = tc_tile(tq, tk, dk, ldq, ldk, ldo, {gout, q, k, v, gq, gk, gv});
@@ -491,7 +533,7 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
     prof.detail = "tcbwd_b" + std::to_string(b) + "_tq" + std::to_string(tq) + "_tk" +
                   std::to_string(tk);
   TcAttBP p{gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, (int)tq, (int)tk, heads, scale,
-            accumulate_q, accumulate_k, accumulate_v};
+            accumulate_q, accumulate_k, accumulate_v, colpart};
   dim3 grid((unsigned)heads, (unsigned)b);
 #define MTKC_TC_BWD(TTV)                                                          \
   if(tt == TTV) {                                                                 \
