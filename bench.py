@@ -245,6 +245,7 @@ def run_b200(a):
     marks = [e0]
     words = 0.0
     th0 = time.perf_counter()
+    th0_mono = time.monotonic()
     for _ in range(a.steps):
         grp = group(u)
         words += sum(b.target_tokens() for b in grp)
@@ -252,6 +253,9 @@ def run_b200(a):
         marks.append(M.event_record())  # per-step device time (diagnostics)
         u += 1
     host_ms = (time.perf_counter() - th0) * 1e3 / a.steps
+    if os.environ.get("MTK_TRACE_BLOCK"):
+        print(f"[bench] timed region host {th0_mono:.6f} .. {time.monotonic():.6f}",
+              file=sys.stderr)
     e1 = marks[-1]
     step_list = [M.event_elapsed_ms_keep(marks[i], marks[i + 1]) for i in range(a.steps)]
     for m in marks[1:-1]:

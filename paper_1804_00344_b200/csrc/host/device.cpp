@@ -56,7 +56,9 @@ Device& Device::get() {
 float* Device::scratch(size_t bytes) {
   if(bytes <= scratchBytes_ && scratch_)
     return scratch_->ptr;
-  size_t want = std::max(bytes, (size_t)256 << 20);
+  // generous first reservation (HBM is plentiful; a regrow costs a stream
+  // sync + cudaMalloc, tens of milliseconds on a fresh process), then double
+  size_t want = std::max(std::max(bytes, (size_t)1 << 30), 2 * scratchBytes_);
   sync();
   scratch_ = std::make_shared<DeviceBuffer>(want / sizeof(float));
   scratchBytes_ = want;

@@ -66,7 +66,9 @@ struct BlockTimer {
                     .count();
     if(us < lim)
       return;
-    std::fprintf(stderr, "[mtk block] %s %.0f us\n", what, us);
+    double now = std::chrono::duration<double>(
+                     std::chrono::steady_clock::now().time_since_epoch()).count();
+    std::fprintf(stderr, "[mtk block] %s %.0f us at %.6f\n", what, us, now);
     void* bt[12];
     int n = backtrace(bt, 12);
     backtrace_symbols_fd(bt + 1, n - 1, 2);
