@@ -188,6 +188,15 @@ Tensor& ExpressionGraph::nodeGrad(int index, uint64_t gen) {
 }
 
 NodeRef ExpressionGraph::addNode(Node n) {
+  // gradients flow only toward parameters: constants and anything built
+  // from constants alone are skipped by the backward sweep, and ops skip
+  // the input gradients nobody needs (e.g. dot(mask, context))
+  if(!n.isParam) {
+    bool any = false;
+    for(int in : n.inputs)
+      any = any || nodes_[(size_t)resolve(in)].needsGrad;
+    n.needsGrad = any;
+  }
   nodes_.push_back(std::move(n));
   return NodeRef{this, (int)nodes_.size() - 1, generation_, nodes_.back().shape};
 }
@@ -461,6 +470,8 @@ NodeRef ExpressionGraph::binary(const std::string& name, EwiseOp op, NodeRef a, 
     for(int which = 0; which < 2; ++which) {
       const Shape& st = which == 0 ? sa : sb;
       int idx = n.inputs[(size_t)which];
+      if(!g.node(g.resolve(idx)).needsGrad)
+        continue;  // constant operand (mask, scale table)
       bool same = st == n.shape;
       if(op == EwiseOp::Add && same) {
         // residual adds: the first operand whose gradient buffer does not
@@ -647,14 +658,14 @@ NodeRef ExpressionGraph::dotImpl(NodeRef a, NodeRef b, bool transA, bool transB)
     Node& nb = g.node(n.inputs[1]);
     Shape sa = na.shape, sb = nb.shape, so = n.shape;
     // graph.cpp:322-330
-    {
+    if(na.needsGrad) {
       auto d = g.gradDst(n.inputs[0]);
       if(!transA)
         gemmAccum(d.ptr, d.accumulate, sa, go, so, false, g.valPtr(n.inputs[1]), sb, !transB);
       else
         gemmAccum(d.ptr, d.accumulate, sa, g.valPtr(n.inputs[1]), sb, transB, go, so, true);
     }
-    {
+    if(nb.needsGrad) {
       auto d = g.gradDst(n.inputs[1]);
       if(!transB)
         gemmAccum(d.ptr, d.accumulate, sb, g.valPtr(n.inputs[0]), sa, !transA, go, so, false);
@@ -1644,7 +1655,7 @@ void ExpressionGraph::backward(NodeRef loss, const std::function<void(int)>& aft
   }
   for(int i = loss.index; i >= 0; --i) {
     Node& n = nodes_[(size_t)i];
-    if(!(n.alias >= 0 || !n.bwd || !n.gradLive))
+    if(!(n.alias >= 0 || !n.bwd || !n.gradLive || !n.needsGrad))
       n.bwd(*this, n);
     if(afterNode)
       afterNode(i);
