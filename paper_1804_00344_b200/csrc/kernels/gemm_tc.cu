@@ -644,12 +644,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // C = alpha*sum_s part[s] (+bias, relu, gate) + beta*C  (fixed split order).
 // Grid-stride over (row, 4-column group); float4 when N and ldc allow.
+// per output problem (blockIdx.y): destination, bias and beta source
+struct ReduceOut {
+  float* C[3];
+  const float* bias[3];
+  const float* Cin[3];
+};
+
 template <bool VEC>
 __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plane, int64_t M,
-                                     int64_t N, float* C, int64_t ldc, float alpha, float beta,
-                                     const float* bias, int epi, const float* gate,
-                                     const float* Cin) {
+                                     int64_t N, ReduceOut outs, int64_t ldc, float alpha,
+                                     float beta, int epi, const float* gate) {
   MTKC_PDL_ENTRY();
+  // problem q's partials start at part + q*M*N; splits are `plane` apart
+  const int q = blockIdx.y;
+  part += (int64_t)q * M * N;
+  float* C = outs.C[q];
+  const float* bias = outs.bias[q];
+  const float* Cin = outs.Cin[q];
   const int64_t groups = (N + 3) / 4, total = M * groups;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
       i += (int64_t)gridDim.x * blockDim.x) {
@@ -1003,27 +1015,28 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   else
     *rc = BN == 256 ? dispatch_majors<256, false>(aMN, bMN, maps, p, st)
                     : dispatch_majors<128, false>(aMN, bMN, maps, p, st);
-  if(*rc == MTKC_OK && splits > 1) {
-    for(int q = 0; q < nOut && *rc == MTKC_OK; ++q) {
-      const mtkc_gemm_args& b = probs[q];
-      const float* part = a.workspace + (int64_t)q * a.M * a.N;
-      const int64_t sstride = (int64_t)nOut * a.M * a.N;  // between splits
-      const bool vec = a.N % 4 == 0 && a.ldc % 4 == 0 && (uintptr_t)b.C % 16 == 0 &&
-                       (uintptr_t)a.workspace % 16 == 0;
-      const unsigned grid = grid1d(a.M * cdiv(a.N, 4), 256);
-      if(vec)
-        ::mtkc::launch(splitk_reduce_kernel<true>, grid, 256, 0, st, part, splits, sstride, a.M,
-                       a.N, b.C, a.ldc, a.alpha, a.beta, b.bias, a.epilogue, a.gate,
-                       a.addend ? a.addend : b.C);
-      else
-        ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, part, splits, sstride, a.M,
-                       a.N, b.C, a.ldc, a.alpha, a.beta, b.bias, a.epilogue, a.gate,
-                       a.addend ? a.addend : b.C);
-      count_launch();
-      cudaError_t e = cudaGetLastError();
-      if(e != cudaSuccess)
-        *rc = cuda_status(e, "splitk_reduce_kernel");
+  if(*rc == MTKC_OK && splits > 1) {  // one launch for every output problem
+    ReduceOut outs{};
+    bool vec = a.N % 4 == 0 && a.ldc % 4 == 0 && (uintptr_t)a.workspace % 16 == 0;
+    for(int q = 0; q < nOut; ++q) {
+      outs.C[q] = probs[q].C;
+      outs.bias[q] = probs[q].bias;
+      outs.Cin[q] = a.addend ? a.addend : probs[q].C;
+      vec = vec && (uintptr_t)probs[q].C % 16 == 0;
     }
+    const int64_t sstride = (int64_t)nOut * a.M * a.N;  // between splits
+    const dim3 grid(grid1d(a.M * cdiv(a.N, 4), 256, 148 * 32 / std::max(1, nOut)),
+                    (unsigned)nOut);
+    if(vec)
+      ::mtkc::launch(splitk_reduce_kernel<true>, grid, 256, 0, st, a.workspace, splits, sstride,
+                     a.M, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue, a.gate);
+    else
+      ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, a.workspace, splits,
+                     sstride, a.M, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue, a.gate);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if(e != cudaSuccess)
+      *rc = cuda_status(e, "splitk_reduce_kernel");
   }
   return true;
 }
