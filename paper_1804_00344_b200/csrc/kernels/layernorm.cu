@@ -431,7 +431,7 @@ int mtkc_layernorm_stats(float* out, const float* x, const float* gain, const fl
 }
 
 size_t mtkc_layernorm_stats_workspace_bytes(int64_t rows, int64_t d) {
-  int64_t rpc = std::max<int64_t>(LN_WARPS, cdiv(cdiv(rows, 4 * 148), LN_WARPS) * LN_WARPS);
+  int64_t rpc = std::max<int64_t>(LN_WARPS, cdiv(cdiv(rows, 2 * 148), LN_WARPS) * LN_WARPS);
   return (size_t)cdiv(rows, rpc) * 2 * (size_t)d * sizeof(float);
 }
 
@@ -449,8 +449,8 @@ int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* 
   ProfScope prof(st, "layernorm", 12.0 * rows * d);  // read dy, x; write dx
   if(prof_detail())
     prof.detail = "bwd4_r" + std::to_string(rows) + "_d" + std::to_string(d);
-  // about four CTAs per SM (latency hiding), rows per CTA a multiple of the warp count
-  const int64_t rpc = std::max<int64_t>(LN_WARPS, cdiv(cdiv(rows, 4 * 148), LN_WARPS) * LN_WARPS);
+  // about two CTAs per SM, rows per CTA a multiple of the warp count
+  const int64_t rpc = std::max<int64_t>(LN_WARPS, cdiv(cdiv(rows, 2 * 148), LN_WARPS) * LN_WARPS);
   const int64_t nblk = cdiv(rows, rpc);
   float* part = nullptr;
   if(dgain) {
