@@ -142,7 +142,21 @@ typedef struct mtkc_gemm_args {
   size_t workspace_bytes;
   const float* addend;  /* optional: the beta term reads addend (laid out like C)
                            instead of C -- a fused residual add, C write-only */
+  float* colsum;        /* optional: the sums over k of one operand, written
+                           (or added, colsum_accumulate) next to the product --
+                           the bias gradient db = colsum(dY) of the dW GEMM
+                           (affine backward), read from the tiles the product
+                           already stages.  colsum_of = MTKC_COLSUM_B: [N],
+                           colsum[n] = sum_k op(B)[k][n]; MTKC_COLSUM_A: [M],
+                           colsum[m] = sum_k op(A)[m][k].  TF32 precision sums
+                           the tf32-rounded operand in fp32 (deterministic,
+                           fixed order); FP32 precision runs mtkc_colsum. */
+  int colsum_of;
+  int colsum_accumulate;
 } mtkc_gemm_args;
+
+#define MTKC_COLSUM_A 1
+#define MTKC_COLSUM_B 2
 
 int mtkc_gemm(const mtkc_gemm_args* args, void* stream);
 /* A group of products of one shape in one launch (the q/k/v projections of

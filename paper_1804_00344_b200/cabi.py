@@ -28,6 +28,7 @@ class GemmArgs(C.Structure):
         ("bias", C.c_void_p), ("epilogue", C.c_int), ("gate", C.c_void_p),
         ("precision", C.c_int), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("addend", C.c_void_p),
+        ("colsum", C.c_void_p), ("colsum_of", C.c_int), ("colsum_accumulate", C.c_int),
     ]
 
 
@@ -59,21 +60,27 @@ def check(rc: int):
 
 def gemm(M, N, K, A, lda, B, ldb, Cp, ldc, trans_a=False, trans_b=False, alpha=1.0, beta=0.0,
          bias=None, relu=False, gate=None, precision=1, workspace=None, workspace_bytes=0,
-         stream=None, batch=1, stride_a=0, stride_b=0, stride_c=0, addend=None):
+         stream=None, batch=1, stride_a=0, stride_b=0, stride_c=0, addend=None, colsum=None,
+         colsum_of=0, colsum_accumulate=False):
     g = GemmArgs(M, N, K, batch, A, lda, stride_a, int(trans_a), B, ldb, stride_b, int(trans_b),
                  Cp, ldc, stride_c, alpha, beta, bias, 1 if relu else 0, gate, precision,
-                 workspace, workspace_bytes, addend)
+                 workspace, workspace_bytes, addend, colsum, colsum_of, int(colsum_accumulate))
     check(lib().mtkc_gemm(C.byref(g), stream))
     return lib().mtkc_gemm_last_path()
 
 
 def gemm_group(M, N, K, probs, lda, ldb, ldc, trans_a=False, trans_b=False, alpha=1.0, beta=0.0,
-               kconcat=False, precision=1, workspace=None, workspace_bytes=0, stream=None):
-    """mtkc_gemm_group: probs = [(A, B, C, bias-or-None), ...] device pointers."""
+               kconcat=False, precision=1, workspace=None, workspace_bytes=0, stream=None,
+               colsum_of=0, colsum_accumulate=False):
+    """mtkc_gemm_group: probs = [(A, B, C, bias-or-None[, colsum-or-None]), ...] device
+    pointers."""
     arr = (GemmArgs * len(probs))()
-    for i, (A, B, Cp, bias) in enumerate(probs):
+    for i, pr in enumerate(probs):
+        A, B, Cp, bias = pr[:4]
+        cs = pr[4] if len(pr) > 4 else None
         arr[i] = GemmArgs(M, N, K, 1, A, lda, 0, int(trans_a), B, ldb, 0, int(trans_b), Cp, ldc, 0,
-                          alpha, beta, bias, 0, None, precision, workspace, workspace_bytes)
+                          alpha, beta, bias, 0, None, precision, workspace, workspace_bytes, None,
+                          cs, colsum_of if cs else 0, int(colsum_accumulate))
     check(lib().mtkc_gemm_group(arr, len(probs), int(kconcat), stream))
     return lib().mtkc_gemm_last_path()
 

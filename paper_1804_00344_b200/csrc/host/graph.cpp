@@ -219,7 +219,6 @@ ExpressionGraph::GradDst ExpressionGraph::gradDst(int nodeIndex, bool supportsGa
   }
   if(n.grad.empty())
     n.grad = allocTensor(n.shape);
-  ++n.gradTouch;
   int acc = n.gradLive ? 1 : 0;
   n.gradLive = true;
   if(n.gate && !supportsGate)
@@ -250,7 +249,8 @@ float* accPtr(ExpressionGraph& g, int idx, int64_t elems) {
 void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA, const float* B,
           int64_t ldb, bool tB, float* C, int64_t ldc, float beta, const float* bias = nullptr,
           int epi = MTKC_EPI_NONE, const float* gate = nullptr, int64_t batch = 1,
-          int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
+          int64_t sA = 0, int64_t sB = 0, int64_t sC = 0, float* colsum = nullptr,
+          int colsumOf = 0, int colsumAcc = 0) {
   Device& d = Device::get();
   mtkc_gemm_args g{};
   g.M = M;
@@ -276,6 +276,9 @@ void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
   g.precision = (int)d.precision();
   g.workspace = d.scratch(64 << 20);
   g.workspace_bytes = d.scratchBytes();
+  g.colsum = colsum;
+  g.colsum_of = colsumOf;
+  g.colsum_accumulate = colsumAcc;
   MTKC(mtkc_gemm(&g, d.stream()));
 }
 
@@ -717,21 +720,17 @@ static NodeRef affineImpl(ExpressionGraph& g, NodeRef x, NodeRef w, NodeRef b, b
       gemm(rows, K, N, go, N, false, g.valPtr(n.inputs[1]), transW ? K : N, !transW, d.ptr, K,
            d.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, d.gate);
     }
-    {  // dW
+    {  // dW, with db = colsum(dY) summed from the dY tiles the product stages
       auto d = g.gradDst(n.inputs[1]);
+      auto db = g.gradDst(n.inputs[2]);
       if(!transW)
         gemm(K, N, rows, g.valPtr(n.inputs[0]), K, true, go, N, false, d.ptr, N,
-             d.accumulate ? 1.f : 0.f);
+             d.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, nullptr, 1, 0, 0, 0, db.ptr,
+             MTKC_COLSUM_B, db.accumulate);
       else
         gemm(N, K, rows, go, N, true, g.valPtr(n.inputs[0]), K, false, d.ptr, K,
-             d.accumulate ? 1.f : 0.f);
-    }
-    {  // db
-      auto d = g.gradDst(n.inputs[2]);
-      Device& dev = Device::get();
-      size_t ws = (size_t)((rows + 63) / 64) * (size_t)N * sizeof(float);
-      float* w = dev.scratch(ws);
-      MTKC(mtkc_colsum(d.ptr, go, rows, N, d.accumulate, w, dev.scratchBytes(), dev.stream()));
+             d.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, nullptr, 1, 0, 0, 0, db.ptr,
+             MTKC_COLSUM_A, db.accumulate);
     }
   };
   return g.addNode(std::move(n));
@@ -747,14 +746,6 @@ struct AffineGroup {
   int64_t rows = 0, K = 0, N = 0;
   bool fwdDone = false;
   uint64_t bwdDone = ~0ull;  // backward sweep that already ran the group
-  // column sums of the members' output gradients produced by their consumer
-  // (the attention backward): [3][colRows][N], slot per member; valid for
-  // the sweep colValid while no one else touched the gradients
-  Tensor colpart;
-  int64_t colRows = 0;
-  uint64_t colValid = ~0ull;
-  int colSlot[3] = {-1, -1, -1};
-  uint32_t colTouch[3] = {0, 0, 0};
 };
 
 mtkc_gemm_args groupArgs(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
@@ -866,45 +857,32 @@ std::vector<NodeRef> ExpressionGraph::affineGroup(NodeRef x, const std::vector<N
           MTKC(mtkc_gemm_group(probs, (int)live.size(), 1, dev.stream()));
         }
       }
-      {  // dW_j (+)= X^T dY_j: one grouped launch when the accumulate flags agree
-        ExpressionGraph::GradDst dw[3];
+      {  // dW_j (+)= X^T dY_j and db_j (+)= colsum(dY_j): one grouped launch
+         // when the accumulate flags agree
+        ExpressionGraph::GradDst dw[3], db[3];
         bool same = true;
         for(size_t q = 0; q < live.size(); ++q) {
           dw[q] = g.gradDst(grp->W[live[q]]);
-          same = same && dw[q].accumulate == dw[0].accumulate;
+          db[q] = g.gradDst(grp->b[live[q]]);
+          same = same && dw[q].accumulate == dw[0].accumulate &&
+                 db[q].accumulate == db[0].accumulate;
         }
         if(same) {
           mtkc_gemm_args probs[3];
-          for(size_t q = 0; q < live.size(); ++q)
+          for(size_t q = 0; q < live.size(); ++q) {
             probs[q] = groupArgs(K, N, rows, g.valPtr(grp->x), K, true, dY[q], N, false,
                                  dw[q].ptr, N, dw[q].accumulate ? 1.f : 0.f, nullptr);
+            probs[q].colsum = db[q].ptr;
+            probs[q].colsum_of = MTKC_COLSUM_B;
+            probs[q].colsum_accumulate = db[q].accumulate;
+          }
           MTKC(mtkc_gemm_group(probs, (int)live.size(), 0, dev.stream()));
         } else {
           for(size_t q = 0; q < live.size(); ++q)
             gemm(K, N, rows, g.valPtr(grp->x), K, true, dY[q], N, false, dw[q].ptr, N,
-                 dw[q].accumulate ? 1.f : 0.f);
+                 dw[q].accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, nullptr, 1, 0, 0, 0,
+                 db[q].ptr, MTKC_COLSUM_B, db[q].accumulate);
         }
-      }
-      {  // db_j: one launch, over the consumer's per-sentence column sums
-         // when the attention backward produced them, else over dY
-        float* outs[3];
-        const float* ins[3];
-        int acc[3];
-        bool useCol = grp->colValid == g.backwardCount_;
-        for(size_t q = 0; q < live.size() && useCol; ++q)
-          useCol = grp->colSlot[live[q]] >= 0 &&
-                   g.node(grp->members[live[q]]).gradTouch == grp->colTouch[live[q]];
-        const int64_t crow = useCol ? grp->colRows : rows;
-        for(size_t q = 0; q < live.size(); ++q) {
-          auto d = g.gradDst(grp->b[live[q]]);
-          outs[q] = d.ptr;
-          acc[q] = d.accumulate;
-          ins[q] = useCol ? grp->colpart.devc() + grp->colSlot[live[q]] * grp->colRows * N : dY[q];
-        }
-        size_t ws = live.size() * (size_t)((crow + 63) / 64) * (size_t)N * sizeof(float);
-        float* w = dev.scratch(ws);
-        MTKC(mtkc_colsum_group(outs, ins, acc, (int)live.size(), crow, N, w, dev.scratchBytes(),
-                               dev.stream()));
       }
     };
   }
@@ -1466,35 +1444,10 @@ NodeRef ExpressionGraph::attention(NodeRef q, NodeRef k, NodeRef v, const Tensor
     auto dkk = g.gradDst(n.inputs[1]);
     auto dv = g.gradDst(n.inputs[2]);
     if(tensorCore) {
-      // grouped q/k/v projections written fresh here: let the kernel emit
-      // their per-sentence column sums (the bias gradients without a re-read)
-      float* colpart = nullptr;
-      auto grp = std::static_pointer_cast<AffineGroup>(g.node(n.inputs[1]).group);
-      if(grp && !dkk.accumulate && !dv.accumulate) {
-        int slots[3] = {-1, -1, -1};
-        bool ok = grp->members.size() <= 3;
-        for(size_t j = 0; j < grp->members.size() && ok; ++j) {
-          const int idx = grp->members[j];
-          const int slot = idx == n.inputs[0] ? 0 : idx == n.inputs[1] ? 1
-                                                 : idx == n.inputs[2] ? 2 : -1;
-          ok = slot >= 0 && !(slot == 0 && dq.accumulate);
-          slots[j] = slot;
-        }
-        if(ok) {
-          grp->colpart = g.allocTensor(Shape({3, b, d}));
-          grp->colRows = b;
-          for(size_t j = 0; j < grp->members.size(); ++j) {
-            grp->colSlot[j] = slots[j];
-            grp->colTouch[j] = g.node(grp->members[j]).gradTouch;
-          }
-          grp->colValid = g.backwardCount_;
-          colpart = grp->colpart.dev();
-        }
-      }
       MTKC(mtkc_attention_tc_backward(go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d,
                                       g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d, dq.ptr,
                                       dkk.ptr, dv.ptr, b, tq, tk, heads, dk, scale, dq.accumulate,
-                                      dkk.accumulate, dv.accumulate, colpart, stream()));
+                                      dkk.accumulate, dv.accumulate, nullptr, stream()));
       return;
     }
     Tensor ds = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));

@@ -11,9 +11,9 @@
 #include "common.cuh"
 
 namespace mtkc {
-bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc);  // gemm_tc.cu
+bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc, bool* csFused);  // gemm_tc.cu
 bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStream_t st,
-                   int* rc);
+                   int* rc, bool* csFused);
 }
 
 using namespace mtkc;
@@ -21,6 +21,25 @@ using namespace mtkc;
 namespace {
 
 thread_local int t_last_path = 0;
+
+// The operand sums of mtkc_gemm_args.colsum as a separate pass (FP32
+// precision, or a tensor-core launch that could not fuse them): column sums
+// of the stored MN-major operand with mtkc_colsum's summation order.
+int colsum_after(const mtkc_gemm_args& a, void* stream) {
+  if(!a.colsum)
+    return MTKC_OK;
+  if(a.batch != 1)
+    return fail(MTKC_CONTRACT, "mtkc_gemm: colsum needs batch == 1");
+  if(a.colsum_of == MTKC_COLSUM_B && !a.transB && a.ldb == a.N)
+    return mtkc_colsum(a.colsum, a.B, a.K, a.N, a.colsum_accumulate, a.workspace,
+                       a.workspace_bytes, stream);
+  if(a.colsum_of == MTKC_COLSUM_A && a.transA && a.lda == a.M)
+    return mtkc_colsum(a.colsum, a.A, a.K, a.M, a.colsum_accumulate, a.workspace,
+                       a.workspace_bytes, stream);
+  return fail(MTKC_CONTRACT,
+              "mtkc_gemm: colsum needs a densely stored MN-major operand (B untransposed with "
+              "ldb == N, or A transposed with lda == M)");
+}
 
 constexpr int TM = 64, TN = 64, TK = 16;
 
@@ -156,8 +175,11 @@ int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
              a->transB, a->epilogue, a->beta != 0.f ? "_acc" : "", a->bias ? "_bias" : "");
     prof.detail = d;
   }
-  if(a->precision == MTKC_GEMM_TF32 && tc_gemm(*a, S(stream), &rc)) {
+  bool csFused = false;
+  if(a->precision == MTKC_GEMM_TF32 && tc_gemm(*a, S(stream), &rc, &csFused)) {
     t_last_path = 1;
+    if(rc == MTKC_OK && !csFused)
+      rc = colsum_after(*a, stream);
     return rc;
   }
   prof.cls = "gemm_simt";
@@ -189,7 +211,7 @@ int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
             p.foldBatch ? 1u : (unsigned)a->batch);
   ::mtkc::launch(gemm_fp32_kernel, grid, 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("gemm_fp32_kernel");
-  return MTKC_OK;
+  return colsum_after(*a, stream);
 }
 
 int mtkc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, void* stream) {
@@ -206,8 +228,11 @@ int mtkc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, void* s
                a.transB, a.beta != 0.f ? "_acc" : "", a.bias ? "_bias" : "");
       prof.detail = d;
     }
-    if(tc_gemm_group(probs, nprob, kconcat, S(stream), &rc)) {
+    bool csFused = false;
+    if(tc_gemm_group(probs, nprob, kconcat, S(stream), &rc, &csFused)) {
       t_last_path = 1;
+      for(int q = 0; q < nprob && rc == MTKC_OK && !csFused; ++q)
+        rc = colsum_after(probs[q], stream);
       return rc;
     }
   }

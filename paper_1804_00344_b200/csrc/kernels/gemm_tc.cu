@@ -16,6 +16,9 @@
 //   warps 2..5  epilogue       (tcgen05.ld 32x32b -> per-warp smem transpose
 //                               -> alpha/bias/ReLU/gate/beta*C -> coalesced
 //                               128-byte row stores, or split-K partials)
+//   warp 6      operand sums   (optional: sums over k of the MN-major operand
+//                               straight from the staged tiles -- the bias
+//                               gradient colsum(dY) of a dW product)
 // The epilogue of tile i overlaps the main loop of tile i+1.
 #include <cuda.h>
 
@@ -40,7 +43,8 @@ constexpr int KA = BK / 32;  // 128-byte atom columns per K-major stage
 #define MTK_EPI_WARPS 4
 #endif
 constexpr int EPI_WARPS = MTK_EPI_WARPS;  // 4 (one per TMEM lane quarter) or 8 (two)
-constexpr int TC_THREADS = 64 + 32 * EPI_WARPS;  // producer, MMA, epilogue warps
+constexpr int CS_WARP = 2 + EPI_WARPS;          // operand-sum warp
+constexpr int TC_THREADS = 96 + 32 * EPI_WARPS;  // producer, MMA, epilogue, operand-sum warps
 constexpr int EPI_STRIDE = 33;  // padded 32x32 transpose tile
 
 // ---------------------------------------------------------------- PTX
@@ -182,6 +186,13 @@ struct TcP {
   const float* addend;
   const float* biasP[3];
   float* CP[3];
+  // fused operand sums (mtkc_gemm_args.colsum): csOp 1 = A (rows of op(A),
+  // length M, tiles with n0 == 0), 2 = B (columns of op(B), length N, tiles
+  // with m0 == 0); split-K writes partials csPart[nOut][splits][csLen]
+  int csOp, csAcc;
+  int64_t csLen;
+  float* csOut[3];
+  float* csPart;
   int dbg;  // profiling switches (MTK_GEMM_DEBUG): 1 = no epilogue stores, 2 = no MMAs
 };
 
@@ -242,7 +253,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&ldbar[w], 1);
     for(int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], p.csOp ? 2 : 1);  // MMA commit (+ operand-sum warp)
     }
     for(int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -378,7 +389,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mma_commit(&tfull[acc]);
       __syncwarp();
     }
-  } else {
+  } else if(warp < CS_WARP) {
     // epilogue warps 2..9: TMEM lane quarter q = warp % 4 (the quarter a
     // warp may access), column half h = (warp - 2) / 4 of the tile
     const int ew = warp - 2, q = warp & 3, h = ew >> 2;
@@ -632,6 +643,72 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if(lane == 0)
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
+  } else if(p.csOp) {
+    // operand sums over k, read from the MN-major stages the MMA consumes.
+    // A stage holds 32-column atoms of BK rows x 128 B (atom j at j*BK*128),
+    // 128-byte swizzled in 32-byte units: unit u of row k sits at u ^ (k & 3)
+    // (Swizzle<2,5,2>).  Lane 8r + c reads 16-byte chunk c of rows k = r
+    // (mod 4), whose logical columns 8*((c>>1) ^ r) + 4*(c&1) + 0..3 are the
+    // same for every such k; lanes l, l^10, l^20, l^30 hold the same columns.
+    constexpr int CH = (BN > BM ? BN : BM) / 32;
+    const bool sumB = p.csOp == 2;
+    const int nch = sumB ? BN / 32 : BM / 32;
+    const uint32_t sBytes = sumB ? B_BYTES : A_BYTES;
+    const uint8_t* sOp = (sumB ? sB : sA) + (lane >> 3) * 128 + (lane & 7) * 16;
+    int i = 0;
+    for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x) {
+      int m0, n0, kb0, nkb, split;
+      tileCoords(t, m0, n0, kb0, nkb, split);
+      const bool on = sumB ? (B_MN && m0 == 0) : (A_MN && n0 == 0);
+      float4 acc[CH];
+#pragma unroll
+      for(int c = 0; c < CH; ++c)
+        acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for(int kb = 0; kb < nkb; ++kb, ++i) {
+        const int s = i % ST;
+        mbar_wait(&full[s], (i / ST) & 1);
+        if(on) {
+          const uint8_t* base = sOp + s * sBytes;
+#pragma unroll
+          for(int c = 0; c < CH; ++c)
+            if(c < nch) {
+#pragma unroll
+              for(int kr = 0; kr < BK / 4; ++kr) {
+                const float4 x = *reinterpret_cast<const float4*>(base + c * (BK * 128) + kr * 512);
+                acc[c].x += x.x;
+                acc[c].y += x.y;
+                acc[c].z += x.z;
+                acc[c].w += x.w;
+              }
+            }
+        }
+        __syncwarp();
+        if(lane == 0)
+          mbar_arrive(&empty[s]);
+      }
+      if(!on)
+        continue;
+      const int64_t len = p.csLen, base0 = sumB ? n0 : m0;
+      float* dst = p.splits > 1 ? p.csPart + ((int64_t)tprob * p.splits + split) * len
+                                : p.csOut[tprob];
+      const bool add = p.splits == 1 && p.csAcc;
+#pragma unroll
+      for(int c = 0; c < CH; ++c)
+        if(c < nch) {
+          float v[4] = {acc[c].x, acc[c].y, acc[c].z, acc[c].w};
+#pragma unroll
+          for(int e = 0; e < 4; ++e) {
+            v[e] += __shfl_xor_sync(0xffffffffu, v[e], 10);
+            v[e] += __shfl_xor_sync(0xffffffffu, v[e], 20);
+          }
+          const int64_t col = base0 + c * 32 + lane * 4;  // lanes 0..7: r = 0
+          if(lane < 8)
+#pragma unroll
+            for(int e = 0; e < 4; ++e)
+              if(col + e < len)
+                dst[col + e] = add ? dst[col + e] + v[e] : v[e];
+        }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -649,6 +726,11 @@ struct ReduceOut {
   float* C[3];
   const float* bias[3];
   const float* Cin[3];
+  // fused operand sums: partials [nOut][splits][csLen] -> cs[q] (+=, csAcc)
+  float* cs[3];
+  const float* csPart;
+  int64_t csLen;
+  int csAcc;
 };
 
 template <bool VEC>
@@ -712,6 +794,17 @@ __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plan
     } else {
       for(int u = 0; u < 4 && c + u < N; ++u)
         dst[u] = out[u];
+    }
+  }
+  if(outs.csPart) {  // operand sums: splits added in order
+    const float* cp = outs.csPart + (int64_t)q * splits * outs.csLen;
+    float* cs = outs.cs[q];
+    for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < outs.csLen;
+        i += (int64_t)gridDim.x * blockDim.x) {
+      float x = 0.f;
+      for(int s = 0; s < splits; ++s)
+        x += cp[s * outs.csLen + i];
+      cs[i] = outs.csAcc ? cs[i] + x : x;
     }
   }
 }
@@ -855,9 +948,12 @@ int dispatch_majors(bool aMN, bool bMN, const TcMaps& maps, const TcP& p, cudaSt
 // Returns false when the tensor-core path does not apply (caller falls back).
 // probs[0..nprob): one shape (M, N, K, strides, transposes, alpha, beta,
 // epilogue) with per-problem A, B, C, bias.  kconcat: C = sum_p op(A_p)op(B_p)
-// into probs[0].C (bias from probs[0]).
+// into probs[0].C (bias from probs[0]).  *csFused: the operand sums the
+// problems ask for (colsum) were produced by this launch; when false the
+// caller runs them separately.
 bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStream_t st,
-                   int* rc) {
+                   int* rc, bool* csFused) {
+  *csFused = false;
   const mtkc_gemm_args& a = probs[0];
   if(getenv("MTK_DISABLE_TC"))
     return false;
@@ -879,6 +975,16 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     return false;
   // operand majors: op(A) is K-major iff stored untransposed
   const bool aMN = a.transA != 0, bMN = a.transB == 0;
+  // fused operand sums: every problem asks for the same MN-major operand
+  int csOp = 0;
+  if(a.colsum && !kconcat && !getenv("MTK_NO_FUSED_COLSUM")) {
+    csOp = (a.colsum_of == MTKC_COLSUM_B && bMN) ? 2 : (a.colsum_of == MTKC_COLSUM_A && aMN) ? 1 : 0;
+    for(int q = 1; q < nprob; ++q)
+      if(!probs[q].colsum || probs[q].colsum_of != a.colsum_of ||
+         probs[q].colsum_accumulate != a.colsum_accumulate)
+        csOp = 0;
+  }
+  const int64_t csLen = csOp == 2 ? a.N : a.M;
   if(!g_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -908,7 +1014,8 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   if(a.workspace && numKb >= 2 * minKb) {
     double best = (double)tiles / (double)(g_sms * cdiv(tiles, g_sms));
     for(int s = 2; s <= 16 && numKb / s >= minKb; ++s) {
-      size_t need = (size_t)s * nOut * (size_t)a.M * (size_t)a.N * sizeof(float);
+      size_t need = (size_t)s * nOut * ((size_t)a.M * (size_t)a.N + (csOp ? csLen : 0)) *
+                    sizeof(float);
       if(need > a.workspace_bytes)
         break;
       double eff = (double)(tiles * s) / (double)(g_sms * cdiv(tiles * s, g_sms));
@@ -977,8 +1084,13 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   for(int q = 0; q < nOut; ++q) {
     p.biasP[q] = probs[q].bias;
     p.CP[q] = probs[q].C;
+    p.csOut[q] = csOp ? probs[q].colsum : nullptr;
   }
   p.part = splits > 1 ? a.workspace : nullptr;
+  p.csOp = csOp;
+  p.csAcc = a.colsum_accumulate;
+  p.csLen = csLen;
+  p.csPart = (csOp && splits > 1) ? a.workspace + (size_t)splits * nOut * a.M * a.N : nullptr;
   p.kbPerSplit = kbPer;
   p.numKb = numKb;
   p.mt = (int)mt;
@@ -1022,8 +1134,12 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
       outs.C[q] = probs[q].C;
       outs.bias[q] = probs[q].bias;
       outs.Cin[q] = a.addend ? a.addend : probs[q].C;
+      outs.cs[q] = p.csOut[q];
       vec = vec && (uintptr_t)probs[q].C % 16 == 0;
     }
+    outs.csPart = p.csPart;
+    outs.csLen = csLen;
+    outs.csAcc = a.colsum_accumulate;
     const int64_t sstride = (int64_t)nOut * a.M * a.N;  // between splits
     const dim3 grid(grid1d(a.M * cdiv(a.N, 4), 256, 148 * 32 / std::max(1, nOut)),
                     (unsigned)nOut);
@@ -1038,11 +1154,12 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     if(e != cudaSuccess)
       *rc = cuda_status(e, "splitk_reduce_kernel");
   }
+  *csFused = csOp != 0;
   return true;
 }
 
-bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc) {
-  return tc_gemm_group(&a, 1, 0, st, rc);
+bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc, bool* csFused) {
+  return tc_gemm_group(&a, 1, 0, st, rc, csFused);
 }
 
 }  // namespace mtkc

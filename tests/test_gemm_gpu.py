@@ -196,3 +196,86 @@ def test_gemm_addend(cuda, prec, shape):
     assert np.all(np.isfinite(got))
     assert np.all(np.abs(got - want) <= tol)
     assert torch.equal(Rd.cpu(), torch.from_numpy(r))  # addend untouched
+
+
+def _colsum_direct(torch, x, out, acc, ws):
+    import ctypes as C
+    rows, cols = x.shape
+    cabi.check(cabi.lib().mtkc_colsum(C.c_void_p(out.data_ptr()), C.c_void_p(x.data_ptr()),
+                                      C.c_int64(rows), C.c_int64(cols), C.c_int(int(acc)),
+                                      C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()), None))
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("which", ["B", "A"])
+@pytest.mark.parametrize("shape", [(512, 512, 8184), (96, 40, 300), (256, 520, 1000),
+                                   (2048, 512, 4096)])
+def test_gemm_fused_colsum(cuda, prec, which, shape):
+    """mtkc_gemm_args.colsum: the bias gradient db = colsum(dY) produced by the
+    dW product itself.  which = "B": dW = X^T dY (colsum of op(B) = dY);
+    "A": dW = dY^T X (the tied output layer; row sums of op(A) = dY^T).
+    Both with and without split-K, fresh and accumulating.  FP32 precision:
+    bit-identical to mtkc_colsum; TF32: the sums of the tf32-rounded operand,
+    |db - db64| <= 2^-11 sum|dY| (+ fp32 accumulation)."""
+    import torch
+    rng = np.random.default_rng(11)
+    M, N, K = shape  # op(A) M x K, op(B) K x N ; K = token rows
+    dy_cols = N if which == "B" else M
+    x_cols = M if which == "B" else N
+    dy = rng.uniform(-1, 1, (K, dy_cols)).astype(np.float32)
+    x = rng.uniform(-1, 1, (K, x_cols)).astype(np.float32)
+    Dy, X = _dev(torch, dy), _dev(torch, x)
+    A, B = (X, Dy) if which == "B" else (Dy, X)
+    lda, ldb = (x_cols, dy_cols) if which == "B" else (dy_cols, x_cols)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    ws2 = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    want = dy.astype(np.float64).sum(0)
+    for acc in (False, True):
+        cs0 = rng.uniform(-1, 1, dy_cols).astype(np.float32)
+        cs = _dev(torch, cs0) if acc else torch.full((dy_cols,), float("nan"), device="cuda")
+        Cd = torch.zeros(M, N, device="cuda")
+        cabi.gemm(M, N, K, A.data_ptr(), lda, B.data_ptr(), ldb, Cd.data_ptr(), N, trans_a=True,
+                  precision=prec, workspace=ws.data_ptr(), workspace_bytes=ws.numel(),
+                  colsum=cs.data_ptr(), colsum_of=2 if which == "B" else 1,
+                  colsum_accumulate=acc)
+        torch.cuda.synchronize()
+        got = cs.cpu().numpy()
+        if prec == 0:
+            ref = _dev(torch, cs0) if acc else torch.zeros(dy_cols, device="cuda")
+            _colsum_direct(torch, Dy, ref, acc, ws2)
+            torch.cuda.synchronize()
+            assert np.array_equal(got, ref.cpu().numpy())
+        else:
+            base = cs0.astype(np.float64) if acc else 0.0
+            tol = 2.0 ** -11 * np.abs(dy).astype(np.float64).sum(0) * 1.05 + 1e-5 * (1 + np.abs(base))
+            assert np.all(np.abs(got - (base + want)) <= tol), float(np.max(np.abs(got - base - want) - tol))
+        if acc:  # the product itself is unaffected by the fused sums
+            a64 = x.T.astype(np.float64) if which == "B" else dy.T.astype(np.float64)
+            b64 = dy.astype(np.float64) if which == "B" else x.astype(np.float64)
+            c = Cd.cpu().numpy()
+            assert np.all(np.abs(c - a64 @ b64) <= 4e-3 * (np.abs(a64) @ np.abs(b64) + 1))
+
+
+def test_gemm_group_fused_colsum(cuda):
+    """Grouped dW_q = X^T dY_q with db_q = colsum(dY_q) in the same launch."""
+    import torch
+    rng = np.random.default_rng(12)
+    rows, K, N = 8184, 512, 512
+    x = rng.uniform(-1, 1, (rows, K)).astype(np.float32)
+    dys = [rng.uniform(-1, 1, (rows, N)).astype(np.float32) for _ in range(3)]
+    X, Dy = _dev(torch, x), [_dev(torch, d) for d in dys]
+    Ws = [torch.zeros(K, N, device="cuda") for _ in range(3)]
+    cs = [torch.full((N,), float("nan"), device="cuda") for _ in range(3)]
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    path = cabi.gemm_group(K, N, rows, [(X.data_ptr(), Dy[q].data_ptr(), Ws[q].data_ptr(), None,
+                                         cs[q].data_ptr()) for q in range(3)], K, N, N,
+                           trans_a=True, workspace=ws.data_ptr(), workspace_bytes=ws.numel(),
+                           colsum_of=2)
+    torch.cuda.synchronize()
+    assert path == 1
+    for q in range(3):
+        want = dys[q].astype(np.float64).sum(0)
+        tol = 2.0 ** -11 * np.abs(dys[q]).astype(np.float64).sum(0) * 1.05 + 1e-5
+        assert np.all(np.abs(cs[q].cpu().numpy() - want) <= tol), q
+        w = x.T.astype(np.float64) @ dys[q]
+        assert np.all(np.abs(Ws[q].cpu().numpy() - w) <= 4e-3 * (np.abs(x.T) @ np.abs(dys[q]) + 1)), q
