@@ -235,80 +235,58 @@ __global__ void __launch_bounds__(LN_WARPS * 32)
     sg[k] = sb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int64_t r0 = blockIdx.x * rowsPerCta, r1 = min(rows, r0 + rowsPerCta);
-  // two rows per iteration: both rows' loads are in flight before the
-  // first reduction (the kernel is latency-bound at one row per warp)
-  // rows in flight per warp: 1 (two rows cost occupancy and measured slower)
-  constexpr int RP = 1;
-  for(int64_t rowA = r0 + w; rowA < r1; rowA += RP * LN_WARPS) {
-    float4 dy4[RP][NV], xh[RP][NV], h[RP][NV];
-    float mu[RP], rs[RP], s1[RP], s2[RP];
-    bool ok[RP];
+  // one row per warp iteration; every load of the row (dy, x, and the dx
+  // being accumulated into) is issued before the first reduction, so a row
+  // costs one memory round trip
+  for(int64_t row = r0 + w; row < r1; row += LN_WARPS) {
+    float4 dy4[NV], xh[NV], prev[NV];
+    const float mu = mean[row], rs = invStd[row];
 #pragma unroll
-    for(int e = 0; e < RP; ++e) {
-      const int64_t row = rowA + e * LN_WARPS;
-      ok[e] = row < r1;
-      s1[e] = s2[e] = 0.f;
-      mu[e] = ok[e] ? mean[row] : 0.f;
-      rs[e] = ok[e] ? invStd[row] : 0.f;
-#pragma unroll
-      for(int k = 0; k < NV; ++k) {
-        const int64_t c = 128 * k + 4 * lane;
-        if(ok[e] && c < d) {
-          dy4[e][k] = *reinterpret_cast<const float4*>(dy + row * d + c);
-          xh[e][k] = *reinterpret_cast<const float4*>(x + row * d + c);
-        } else {
-          dy4[e][k] = xh[e][k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+    for(int k = 0; k < NV; ++k) {
+      const int64_t c = 128 * k + 4 * lane;
+      dy4[k] = xh[k] = prev[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if(c < d) {
+        dy4[k] = *reinterpret_cast<const float4*>(dy + row * d + c);
+        xh[k] = *reinterpret_cast<const float4*>(x + row * d + c);
+        if(accDx)
+          prev[k] = *reinterpret_cast<const float4*>(dx + row * d + c);
       }
     }
+    float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for(int e = 0; e < RP; ++e) {
-      const bool any = ok[e];
-#pragma unroll
-      for(int k = 0; k < NV; ++k) {
-        const int64_t c = 128 * k + 4 * lane;
-        if(any && c < d) {
-          const float4 x4 = xh[e][k];
-          xh[e][k] = make_float4((x4.x - mu[e]) * rs[e], (x4.y - mu[e]) * rs[e],
-                                 (x4.z - mu[e]) * rs[e], (x4.w - mu[e]) * rs[e]);
-        }
-        const float4 d4v = dy4[e][k];
-        h[e][k] = make_float4(d4v.x * gg[k].x, d4v.y * gg[k].y, d4v.z * gg[k].z, d4v.w * gg[k].w);
-        s1[e] += (h[e][k].x + h[e][k].y) + (h[e][k].z + h[e][k].w);
-        s2[e] += (h[e][k].x * xh[e][k].x + h[e][k].y * xh[e][k].y) +
-                 (h[e][k].z * xh[e][k].z + h[e][k].w * xh[e][k].w);
-        sg[k].x += d4v.x * xh[e][k].x;
-        sg[k].y += d4v.y * xh[e][k].y;
-        sg[k].z += d4v.z * xh[e][k].z;
-        sg[k].w += d4v.w * xh[e][k].w;
-        f4add(sb[k], d4v);
+    for(int k = 0; k < NV; ++k) {
+      const int64_t c = 128 * k + 4 * lane;
+      if(c < d) {
+        const float4 x4 = xh[k];
+        xh[k] = make_float4((x4.x - mu) * rs, (x4.y - mu) * rs, (x4.z - mu) * rs, (x4.w - mu) * rs);
       }
+      const float4 d4v = dy4[k];
+      const float4 h = make_float4(d4v.x * gg[k].x, d4v.y * gg[k].y, d4v.z * gg[k].z,
+                                   d4v.w * gg[k].w);
+      s1 += (h.x + h.y) + (h.z + h.w);
+      s2 += (h.x * xh[k].x + h.y * xh[k].y) + (h.z * xh[k].z + h.w * xh[k].w);
+      sg[k].x += d4v.x * xh[k].x;
+      sg[k].y += d4v.y * xh[k].y;
+      sg[k].z += d4v.z * xh[k].z;
+      sg[k].w += d4v.w * xh[k].w;
+      f4add(sb[k], d4v);
     }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    const float m1 = s1 / (float)d, m2 = s2 / (float)d;
 #pragma unroll
-    for(int e = 0; e < RP; ++e) {
-      s1[e] = warp_sum(s1[e]);
-      s2[e] = warp_sum(s2[e]);
-    }
-#pragma unroll
-    for(int e = 0; e < RP; ++e) {
-      if(!ok[e])
-        continue;
-      const int64_t row = rowA + e * LN_WARPS;
-      const float m1 = s1[e] / (float)d, m2 = s2[e] / (float)d;
-#pragma unroll
-      for(int k = 0; k < NV; ++k) {
-        const int64_t c = 128 * k + 4 * lane;
-        if(c < d) {
-          float4 o;
-          o.x = rs[e] * (h[e][k].x - m1 - xh[e][k].x * m2);
-          o.y = rs[e] * (h[e][k].y - m1 - xh[e][k].y * m2);
-          o.z = rs[e] * (h[e][k].z - m1 - xh[e][k].z * m2);
-          o.w = rs[e] * (h[e][k].w - m1 - xh[e][k].w * m2);
-          float4* dst = reinterpret_cast<float4*>(dx + row * d + c);
-          if(accDx)
-            f4add(o, *dst);
-          *dst = o;
-        }
+    for(int k = 0; k < NV; ++k) {
+      const int64_t c = 128 * k + 4 * lane;
+      if(c < d) {
+        const float4 d4v = dy4[k];
+        float4 o;
+        o.x = rs * (d4v.x * gg[k].x - m1 - xh[k].x * m2);
+        o.y = rs * (d4v.y * gg[k].y - m1 - xh[k].y * m2);
+        o.z = rs * (d4v.z * gg[k].z - m1 - xh[k].z * m2);
+        o.w = rs * (d4v.w * gg[k].w - m1 - xh[k].w * m2);
+        if(accDx)
+          f4add(o, prev[k]);
+        *reinterpret_cast<float4*>(dx + row * d + c) = o;
       }
     }
   }
