@@ -22,6 +22,7 @@ e2e     = same through the public training-loop call (update_pipelined: the
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -82,7 +83,11 @@ def barrier(world):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md).  The
+    sampler starts before the warm-up (nvidia-smi's own start-up stalls the
+    driver for a moment -- not inside the timed steps); only samples that
+    arrive between mark() and stop() are kept (the last earlier one if the
+    timed region is shorter than the 200 ms sampling period)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -91,7 +96,8 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (arrival time, line)
+        self.t0 = None
 
     def start(self):
         try:
@@ -106,11 +112,16 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def mark(self):
+        self.t0 = time.monotonic()
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.monotonic()
+        time.sleep(0.25)  # let the sample straddling the end arrive
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -119,7 +130,12 @@ class Clocks:
         self.t.join(timeout=2)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = self.t0 if self.t0 is not None else 0.0
+        inside = [ln for t, ln in self.lines if t0 <= t <= t1 + 0.25]
+        if not inside:
+            before = [ln for t, ln in self.lines if t < t0]
+            inside = before[-1:]
+        for ln in inside:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -224,6 +240,8 @@ def run_b200(a):
     def group(u):
         return batches[u * world:(u + 1) * world]
 
+    clocks = Clocks(local)
+    clocks.start()
     u = 0
     for _ in range(a.warmup):
         stepper.update(group(u), u, True)
@@ -236,10 +254,10 @@ def run_b200(a):
     stepper.update(group(big), u, True)
 
     # ---- value: device-timed, inputs uploaded per step, no host sync inside
-    clocks = Clocks(local)
     barrier(world)
     M.sync()
-    clocks.start()
+    gc.disable()  # no collector pauses inside the timed / e2e loops
+    clocks.mark()
     l0 = M.launch_count()
     e0 = M.event_record()
     marks = [e0]
@@ -287,6 +305,7 @@ def run_b200(a):
     et = all_max(time.perf_counter() - t0, world)
     h2d = (M.h2d_bytes() - h0) / e2e_steps
     d2h = (M.d2h_bytes() - d0) / e2e_steps
+    gc.enable()
 
     # ---- per-kernel-class device time (events around each C-ABI call)
     M.sync()

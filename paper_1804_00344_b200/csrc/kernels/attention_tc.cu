@@ -59,13 +59,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 // rows x 64 floats (row stride ld) -> smem [TT][LD], rows >= rows zero-filled;
-// 2*TT threads move 16*TT 16-byte chunks: exactly 8 per thread
-template <int TT, int LD>
+// NTH threads (2*TT or 4*TT) move 16*TT 16-byte chunks: 16*TT/NTH per thread
+template <int TT, int LD, int NTH = 2 * TT>
 __device__ __forceinline__ void stage(float* dst, const float* src, int64_t ld, int rows) {
   const int c4 = threadIdx.x & 15, rb = threadIdx.x >> 4;
 #pragma unroll
-  for(int i = 0; i < 8; ++i) {
-    const int r = rb + i * (TT / 8);
+  for(int i = 0; i < 16 * TT / NTH; ++i) {
+    const int r = rb + i * (NTH / 16);
     const float* s = src + (int64_t)(r < rows ? r : 0) * ld + c4 * 4;
     cp_async16(dst + r * LD + c4 * 4, s, r < rows);
   }
@@ -118,19 +118,24 @@ template <int TT>
 constexpr size_t fwd_smem() {
   return sizeof(float) * ((size_t)TT * L4 * 2 + (size_t)TT * L8 + TT);
 }
+// backward: V's region is reused for dS once phase 1 is done
+template <int TT>
+constexpr int bwd_vs() {
+  return TT * L4 > TT * PStride<TT>::v ? TT * L4 : TT * PStride<TT>::v;
+}
 template <int TT>
 constexpr size_t bwd_smem() {
-  return sizeof(float) * ((size_t)TT * L8 * 2 + (size_t)TT * L4 * 2 +
-                          2 * (size_t)TT * PStride<TT>::v + 3 * (TT / 16) * DKT);
+  return sizeof(float) * ((size_t)TT * L8 * 2 + (size_t)bwd_vs<TT>() + (size_t)TT * L4 +
+                          (size_t)TT * PStride<TT>::v + 2 * TT + 3 * (TT / 16) * DKT);
 }
 
-// column sums of a warp's 16 x 64 accumulator tile: sum rows (g, g+8) of
+// column sums of a warp's 16 x 8*NJ accumulator tile: sum rows (g, g+8) of
 // each lane, then across the 8 lanes sharing t; lanes with g == 0 hold the
 // totals of columns jd*8 + 2t + {0,1}
-__device__ __forceinline__ void tile_colsum(const float (&o)[DKT / 8][4], float* dst, int g,
-                                            int t) {
+template <int NJ>
+__device__ __forceinline__ void tile_colsum(const float (&o)[NJ][4], float* dst, int g, int t) {
 #pragma unroll
-  for(int jd = 0; jd < DKT / 8; ++jd)
+  for(int jd = 0; jd < NJ; ++jd)
 #pragma unroll
     for(int e = 0; e < 2; ++e) {
       float v = o[jd][e] + o[jd][2 + e];
@@ -286,72 +291,80 @@ __device__ __forceinline__ void store2(float* d, float a, float b, int acc) {
   *p2 = make_float2(a, b);
 }
 
+// Two warps per 16-row block (4*TT threads): the warp pair splits the keys
+// of dP = dO V^T (exchanging the row sums D through shared memory) and the
+// 64 output columns of dQ / dK / dV, so a CTA keeps twice the warps busy
+// and V's smem is recycled for dS -- ~3x the resident warps per SM.
 template <int TT>
-__global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
+__global__ void __launch_bounds__(TT * 4) attn_tc_bwd_kernel(TcAttBP p) {
   MTKC_PDL_ENTRY();
-  constexpr int NT = TT / 8, LP = PStride<TT>::v;
+  constexpr int NT = TT / 8, NH = NT / 2, LP = PStride<TT>::v, NTH = TT * 4;
+  constexpr int NWB = TT / 16, NJ = DKT / 16;  // row blocks; 8-col tiles per half
   extern __shared__ float4 smem4[];
   float* Q = reinterpret_cast<float*>(smem4);  // [TT][L8]
   float* K = Q + TT * L8;                       // [TT][L8]
-  float* V = K + TT * L8;                       // [TT][L4]
-  float* dO = V + TT * L4;                      // [TT][L4]
+  float* V = K + TT * L8;                       // [TT][L4], then dS [TT][LP]
+  float* dS = V;
+  float* dO = V + bwd_vs<TT>();                 // [TT][L4]
   float* P = dO + TT * L4;                      // [TT][LP]
-  float* dS = P + TT * LP;                      // [TT][LP]
-  float* csum = dS + TT * LP;                   // [3][TT/16][64] per-warp column sums
+  float* Dp = P + TT * LP;                      // [2][TT] row sums of dP*P per key half
+  float* csum = Dp + 2 * TT;                    // [3][NWB][64] per-row-block column sums
   const int h = blockIdx.x, bi = blockIdx.y;
   const int tq = p.tq, tk = p.tk;
   const int hoff = h * DKT;
-  stage<TT, L8>(Q, p.q + (int64_t)bi * tq * p.ldq + hoff, p.ldq, tq);
-  stage<TT, L8>(K, p.k + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
-  stage<TT, L4>(V, p.v + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
-  stage<TT, L4>(dO, p.gout + (int64_t)bi * tq * p.ldo + hoff, p.ldo, tq);
+  stage<TT, L8, NTH>(Q, p.q + (int64_t)bi * tq * p.ldq + hoff, p.ldq, tq);
+  stage<TT, L8, NTH>(K, p.k + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
+  stage<TT, L4, NTH>(V, p.v + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
+  stage<TT, L4, NTH>(dO, p.gout + (int64_t)bi * tq * p.ldo + hoff, p.ldo, tq);
   {
     const float* gP = p.probs + ((int64_t)bi * p.heads + h) * tq * tk;
-    // 2*TT threads: thread covers column c = tid % TT of rows tid / TT + 2i
+    // thread covers column c = tid % TT of rows tid / TT + 4i
     const int c = threadIdx.x % TT, rb = threadIdx.x / TT;
 #pragma unroll
-    for(int i = 0; i < TT / 2; ++i) {
-      const int r = rb + 2 * i;
+    for(int i = 0; i < TT / 4; ++i) {
+      const int r = rb + 4 * i;
       const bool ok = r < tq && c < tk;
       cp_async4(P + r * LP + c, gP + (ok ? r * tk + c : 0), ok);
     }
   }
-  for(int e = threadIdx.x; e < 3 * (TT / 16) * DKT; e += TT * 2)
-    csum[e] = 0.f;
+  if(p.colpart)
+    for(int e = threadIdx.x; e < 3 * NWB * DKT; e += NTH)
+      csum[e] = 0.f;
   cp_async_wait_all();
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int m0 = warp * 16;
+  const int rbk = warp % NWB, half = warp / NWB;
+  const int m0 = rbk * 16;
   const int r0 = m0 + g, r1 = r0 + 8;
-  constexpr int NWB = TT / 16;
 
-  // phase 1 (query rows m0..m0+15): dP = dO V^T, D = rowsum(dP*P),
+  // phase 1 (query rows m0..m0+15, this warp's half of the keys):
+  // dP = dO V^T, D = rowsum(dP*P) over both halves,
   // dS = scale * P * (dP - D)   (graph.cpp:539-552 with the MHA scale)
-  {
-    float dp[NT][4];
+  float dp[NH][4];
 #pragma unroll
-    for(int j = 0; j < NT; ++j)
-      dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
-    if(m0 < tq) {
-      const float* A0 = dO + r0 * L4;
-      const float* A1 = A0 + 8 * L4;
+  for(int j = 0; j < NH; ++j)
+    dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
+  if(m0 < tq) {
+    const float* A0 = dO + r0 * L4;
+    const float* A1 = A0 + 8 * L4;
 #pragma unroll
-      for(int kk = 0; kk < DKT / 8; ++kk) {
-        const int c = kk * 8 + t;
-        uint32_t a0 = tf32(A0[c]), a1 = tf32(A1[c]), a2 = tf32(A0[c + 4]), a3 = tf32(A1[c + 4]);
+    for(int kk = 0; kk < DKT / 8; ++kk) {
+      const int c = kk * 8 + t;
+      uint32_t a0 = tf32(A0[c]), a1 = tf32(A1[c]), a2 = tf32(A0[c + 4]), a3 = tf32(A1[c + 4]);
 #pragma unroll
-        for(int j = 0; j < NT; ++j) {
-          const float* Vr = V + (j * 8 + g) * L4 + c;
-          mma8(dp[j], a0, a1, a2, a3, tf32(Vr[0]), tf32(Vr[4]));
-        }
+      for(int j = 0; j < NH; ++j) {
+        const float* Vr = V + ((half * NH + j) * 8 + g) * L4 + c;
+        mma8(dp[j], a0, a1, a2, a3, tf32(Vr[0]), tf32(Vr[4]));
       }
     }
+  }
+  {
     float D0 = 0.f, D1 = 0.f;
 #pragma unroll
-    for(int j = 0; j < NT; ++j) {
-      const int c = j * 8 + 2 * t;
+    for(int j = 0; j < NH; ++j) {
+      const int c = (half * NH + j) * 8 + 2 * t;
       D0 += dp[j][0] * P[r0 * LP + c] + dp[j][1] * P[r0 * LP + c + 1];
       D1 += dp[j][2] * P[r1 * LP + c] + dp[j][3] * P[r1 * LP + c + 1];
     }
@@ -359,9 +372,17 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
     D0 += __shfl_xor_sync(0xffffffffu, D0, 2);
     D1 += __shfl_xor_sync(0xffffffffu, D1, 1);
     D1 += __shfl_xor_sync(0xffffffffu, D1, 2);
+    if(t == 0) {
+      Dp[half * TT + r0] = D0;
+      Dp[half * TT + r1] = D1;
+    }
+  }
+  __syncthreads();  // D halves exchanged; every read of V is done (dS reuses it)
+  {
+    const float D0 = Dp[r0] + Dp[TT + r0], D1 = Dp[r1] + Dp[TT + r1];
 #pragma unroll
-    for(int j = 0; j < NT; ++j) {
-      const int c = j * 8 + 2 * t;
+    for(int j = 0; j < NH; ++j) {
+      const int c = (half * NH + j) * 8 + 2 * t;
 #pragma unroll
       for(int e = 0; e < 2; ++e) {
         dS[r0 * LP + c + e] = p.scale * (P[r0 * LP + c + e] * (dp[j][e] - D0));
@@ -371,27 +392,27 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
   }
   __syncthreads();
 
-  // phase 2 (query rows): dQ = dS K   (keys outer, 8 output tiles inner)
+  // phase 2 (query rows, this warp's 32 columns): dQ = dS K
   if(m0 < tq) {
     const float* A0 = dS + r0 * LP;
     const float* A1 = A0 + 8 * LP;
-    float o[DKT / 8][4];
+    float o[NJ][4];
 #pragma unroll
-    for(int jd = 0; jd < DKT / 8; ++jd)
+    for(int jd = 0; jd < NJ; ++jd)
       o[jd][0] = o[jd][1] = o[jd][2] = o[jd][3] = 0.f;
 #pragma unroll
     for(int kk = 0; kk < NT; ++kk) {
       const int c = kk * 8 + t;
       const uint32_t a0 = tf32(A0[c]), a1 = tf32(A1[c]), a2 = tf32(A0[c + 4]),
                      a3 = tf32(A1[c + 4]);
-      const float* Kr = K + c * L8 + g;
+      const float* Kr = K + c * L8 + half * 32 + g;
 #pragma unroll
-      for(int jd = 0; jd < DKT / 8; ++jd)
+      for(int jd = 0; jd < NJ; ++jd)
         mma8(o[jd], a0, a1, a2, a3, tf32(Kr[jd * 8]), tf32(Kr[jd * 8 + 4 * L8]));
     }
-    float* gq = p.gq + (int64_t)bi * tq * p.ldq + hoff;
+    float* gq = p.gq + (int64_t)bi * tq * p.ldq + hoff + half * 32;
 #pragma unroll
-    for(int jd = 0; jd < DKT / 8; ++jd) {
+    for(int jd = 0; jd < NJ; ++jd) {
       const int col = jd * 8 + 2 * t;
       if(r0 < tq)
         store2(gq + (int64_t)r0 * p.ldq + col, o[jd][0], o[jd][1], p.accQ);
@@ -399,13 +420,13 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
         store2(gq + (int64_t)r1 * p.ldq + col, o[jd][2], o[jd][3], p.accQ);
     }
     if(p.colpart)  // padded rows contribute exact zeros
-      tile_colsum(o, csum + (0 * NWB + warp) * DKT, g, t);
+      tile_colsum<NJ>(o, csum + (0 * NWB + rbk) * DKT + half * 32, g, t);
   }
-  // phase 3 (key rows m0..m0+15): dK = dS^T Q, dV = P^T dO
+  // phase 3 (key rows m0..m0+15, this warp's 32 columns): dK = dS^T Q, dV = P^T dO
   if(m0 < tk) {
-    float ok[DKT / 8][4], ov[DKT / 8][4];
+    float ok[NJ][4], ov[NJ][4];
 #pragma unroll
-    for(int jd = 0; jd < DKT / 8; ++jd) {
+    for(int jd = 0; jd < NJ; ++jd) {
       ok[jd][0] = ok[jd][1] = ok[jd][2] = ok[jd][3] = 0.f;
       ov[jd][0] = ov[jd][1] = ov[jd][2] = ov[jd][3] = 0.f;
     }
@@ -418,18 +439,18 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
                      s3 = tf32(S0[4 * LP + 8]);
       const uint32_t p0 = tf32(P0[0]), p1 = tf32(P0[8]), p2 = tf32(P0[4 * LP]),
                      p3 = tf32(P0[4 * LP + 8]);
-      const float* Qr = Q + q0 * L8 + g;
-      const float* Or = dO + q0 * L4 + g;
+      const float* Qr = Q + q0 * L8 + half * 32 + g;
+      const float* Or = dO + q0 * L4 + half * 32 + g;
 #pragma unroll
-      for(int jd = 0; jd < DKT / 8; ++jd) {
+      for(int jd = 0; jd < NJ; ++jd) {
         mma8(ok[jd], s0, s1, s2, s3, tf32(Qr[jd * 8]), tf32(Qr[jd * 8 + 4 * L8]));
         mma8(ov[jd], p0, p1, p2, p3, tf32(Or[jd * 8]), tf32(Or[jd * 8 + 4 * L4]));
       }
     }
-    float* gk = p.gk + (int64_t)bi * tk * p.ldk + hoff;
-    float* gv = p.gv + (int64_t)bi * tk * p.ldk + hoff;
+    float* gk = p.gk + (int64_t)bi * tk * p.ldk + hoff + half * 32;
+    float* gv = p.gv + (int64_t)bi * tk * p.ldk + hoff + half * 32;
 #pragma unroll
-    for(int jd = 0; jd < DKT / 8; ++jd) {
+    for(int jd = 0; jd < NJ; ++jd) {
       const int col = jd * 8 + 2 * t;
       if(r0 < tk) {
         store2(gk + (int64_t)r0 * p.ldk + col, ok[jd][0], ok[jd][1], p.accK);
@@ -441,14 +462,14 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_bwd_kernel(TcAttBP p) {
       }
     }
     if(p.colpart) {
-      tile_colsum(ok, csum + (1 * NWB + warp) * DKT, g, t);
-      tile_colsum(ov, csum + (2 * NWB + warp) * DKT, g, t);
+      tile_colsum<NJ>(ok, csum + (1 * NWB + rbk) * DKT + half * 32, g, t);
+      tile_colsum<NJ>(ov, csum + (2 * NWB + rbk) * DKT + half * 32, g, t);
     }
   }
-  if(p.colpart) {  // this CTA's column sums, warps combined in fixed order
+  if(p.colpart) {  // this CTA's column sums, row blocks combined in fixed order
     __syncthreads();
     const int64_t hd = (int64_t)p.heads * DKT, B = gridDim.y;
-    for(int e = threadIdx.x; e < 3 * DKT; e += TT * 2) {
+    for(int e = threadIdx.x; e < 3 * DKT; e += NTH) {
       const int which = e / DKT, c = e % DKT;
       float v = 0.f;
 #pragma unroll
@@ -540,7 +561,7 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
     size_t smem = bwd_smem<TTV>();                                                \
     if(int rc = set_smem_attr((const void*)attn_tc_bwd_kernel<TTV>, smem))        \
       return rc;                                                                  \
-    ::mtkc::launch(attn_tc_bwd_kernel<TTV>, grid, TTV * 2, smem, S(stream), p);               \
+    ::mtkc::launch(attn_tc_bwd_kernel<TTV>, grid, TTV * 4, smem, S(stream), p);               \
   }
   MTKC_TC_BWD(16) MTKC_TC_BWD(32) MTKC_TC_BWD(48) MTKC_TC_BWD(64)
 #undef MTKC_TC_BWD
