@@ -116,7 +116,7 @@ struct PStride {
 
 template <int TT>
 constexpr size_t fwd_smem() {
-  return sizeof(float) * ((size_t)TT * L4 * 2 + (size_t)TT * L8 + TT);
+  return sizeof(float) * ((size_t)TT * L4 * 2 + (size_t)TT * L8 + 5 * TT);
 }
 // backward: V's region is reused for dS once phase 1 is done
 template <int TT>
@@ -147,47 +147,54 @@ __device__ __forceinline__ void tile_colsum(const float (&o)[NJ][4], float* dst,
     }
 }
 
+// Two warps per 16-row block (4*TT threads): the pair splits the keys of
+// S = Q K^T (row max / sum exchanged through shared memory) and the 64
+// output columns of O = P V.
 template <int TT>
-__global__ void __launch_bounds__(TT * 2) attn_tc_fwd_kernel(TcAttP p) {
+__global__ void __launch_bounds__(TT * 4) attn_tc_fwd_kernel(TcAttP p) {
   MTKC_PDL_ENTRY();
-  constexpr int NW = TT / 16, NT = TT / 8;
+  constexpr int NT = TT / 8, NH = NT / 2, NTH = TT * 4, NWB = TT / 16, NJ = DKT / 16;
   extern __shared__ float4 smem4[];
-  float* Q = reinterpret_cast<float*>(smem4);  // [TT][L4], later P (same rows per warp)
+  float* Q = reinterpret_cast<float*>(smem4);  // [TT][L4], later P
   float* K = Q + TT * L4;                       // [TT][L4]
   float* V = K + TT * L4;                       // [TT][L8]
   float* mk = V + TT * L8;                      // [TT] key usable (mask)
+  float* xch = mk + TT;                         // [2][2][TT] row max / row sum per key half
   const int h = blockIdx.x, bi = blockIdx.y;
   const int tq = p.tq, tk = p.tk;
   const int hoff = h * DKT;
-  stage<TT, L4>(Q, p.q + (int64_t)bi * tq * p.ldq + hoff, p.ldq, tq);
-  stage<TT, L4>(K, p.k + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
-  stage<TT, L8>(V, p.v + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
-  for(int j = threadIdx.x; j < TT; j += NW * 32)
+  stage<TT, L4, NTH>(Q, p.q + (int64_t)bi * tq * p.ldq + hoff, p.ldq, tq);
+  stage<TT, L4, NTH>(K, p.k + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
+  stage<TT, L8, NTH>(V, p.v + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
+  for(int j = threadIdx.x; j < TT; j += NTH)
     mk[j] = (j < tk && (!p.mask || p.mask[(int64_t)bi * tk + j] != 0.f)) ? 1.f : 0.f;
   cp_async_wait_all();
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int m0 = warp * 16;
-  if(m0 >= tq)
-    return;
+  const int rbk = warp % NWB, half = warp / NWB;
+  const int m0 = rbk * 16;
+  const bool live = m0 < tq;  // uniform per row block (both warps of the pair)
 
-  // S = Q K^T (16 x 8*nt per warp)
-  float s[NT][4];
+  // S = Q K^T over this warp's key half (16 x 8*NH)
+  float s[NH][4];
 #pragma unroll
-  for(int j = 0; j < NT; ++j)
+  for(int j = 0; j < NH; ++j)
     s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
   const float* Qr0 = Q + (m0 + g) * L4;
   const float* Qr1 = Qr0 + 8 * L4;
+  if(live) {
 #pragma unroll
-  for(int kk = 0; kk < DKT / 8; ++kk) {
-    const int c = kk * 8 + t;
-    uint32_t a0 = tf32(Qr0[c]), a1 = tf32(Qr1[c]), a2 = tf32(Qr0[c + 4]), a3 = tf32(Qr1[c + 4]);
+    for(int kk = 0; kk < DKT / 8; ++kk) {
+      const int c = kk * 8 + t;
+      uint32_t a0 = tf32(Qr0[c]), a1 = tf32(Qr1[c]), a2 = tf32(Qr0[c + 4]),
+               a3 = tf32(Qr1[c + 4]);
 #pragma unroll
-    for(int j = 0; j < NT; ++j) {  // padded keys are zero rows: no guards
-      const float* Kr = K + (j * 8 + g) * L4 + c;
-      mma8(s[j], a0, a1, a2, a3, tf32(Kr[0]), tf32(Kr[4]));
+      for(int j = 0; j < NH; ++j) {  // padded keys are zero rows: no guards
+        const float* Kr = K + ((half * NH + j) * 8 + g) * L4 + c;
+        mma8(s[j], a0, a1, a2, a3, tf32(Kr[0]), tf32(Kr[4]));
+      }
     }
   }
 
@@ -197,10 +204,10 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_fwd_kernel(TcAttP p) {
   const int lim1 = p.causal ? tk - tq + r1 : tk - 1;
   float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-  for(int j = 0; j < NT; ++j) {
+  for(int j = 0; j < NH; ++j) {
 #pragma unroll
     for(int e = 0; e < 2; ++e) {
-      const int c = j * 8 + 2 * t + e;
+      const int c = (half * NH + j) * 8 + 2 * t + e;
       const bool ok = mk[c] != 0.f;  // 0 past tk
       s[j][e] = (ok && c <= lim0) ? p.scale * s[j][e] : -INFINITY;
       s[j][2 + e] = (ok && c <= lim1) ? p.scale * s[j][2 + e] : -INFINITY;
@@ -212,9 +219,16 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_fwd_kernel(TcAttP p) {
   mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
   mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
   mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+  if(t == 0) {
+    xch[half * TT + r0] = mx0;
+    xch[half * TT + r1] = mx1;
+  }
+  __syncthreads();
+  mx0 = fmaxf(xch[r0], xch[TT + r0]);
+  mx1 = fmaxf(xch[r1], xch[TT + r1]);
   float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
-  for(int j = 0; j < NT; ++j)
+  for(int j = 0; j < NH; ++j)
 #pragma unroll
     for(int e = 0; e < 2; ++e) {
       s[j][e] = s[j][e] == -INFINITY ? 0.f : __expf(s[j][e] - mx0);
@@ -226,53 +240,60 @@ __global__ void __launch_bounds__(TT * 2) attn_tc_fwd_kernel(TcAttP p) {
   sum0 += __shfl_xor_sync(0xffffffffu, sum0, 2);
   sum1 += __shfl_xor_sync(0xffffffffu, sum1, 1);
   sum1 += __shfl_xor_sync(0xffffffffu, sum1, 2);
+  if(t == 0) {
+    xch[2 * TT + half * TT + r0] = sum0;
+    xch[2 * TT + half * TT + r1] = sum1;
+  }
+  __syncthreads();  // also: every read of Q is done, P may overwrite it
+  sum0 = xch[2 * TT + r0] + xch[3 * TT + r0];
+  sum1 = xch[2 * TT + r1] + xch[3 * TT + r1];
   const bool any0 = mx0 != -INFINITY, any1 = mx1 != -INFINITY;
-  if(t == 0 && p.flags && ((r0 < tq && !any0) || (r1 < tq && !any1)))
+  if(live && half == 0 && t == 0 && p.flags && ((r0 < tq && !any0) || (r1 < tq && !any1)))
     atomicOr(p.flags, MTKC_FLAG_MASKED_ROW);
 
   const float inv0 = any0 ? 1.f / sum0 : 0.f, inv1 = any1 ? 1.f / sum1 : 0.f;
-  // P over this warp's own Q rows (Q is dead for them); zero past tk
-  __syncwarp();
   float* P0 = Q + r0 * L4;
   float* P1 = Q + r1 * L4;
 #pragma unroll
-  for(int j = 0; j < NT; ++j) {
-    const int c = j * 8 + 2 * t;
+  for(int j = 0; j < NH; ++j) {
+    const int c = (half * NH + j) * 8 + 2 * t;
     *reinterpret_cast<float2*>(P0 + c) = make_float2(s[j][0] * inv0, s[j][1] * inv0);
     *reinterpret_cast<float2*>(P1 + c) = make_float2(s[j][2] * inv1, s[j][3] * inv1);
   }
-  __syncwarp();
-  // probabilities to HBM: the warp's rows of the [tq x tk] block
+  __syncthreads();
+  if(!live)
+    return;
+  // probabilities to HBM: this warp's 8 rows of the block's [16 x tk] slice
   {
-    const int rows = min(16, tq - m0);
-    float* gP = p.probs + (((int64_t)bi * p.heads + h) * tq + m0) * tk;
+    const int rows = min(8, tq - m0 - half * 8);
+    float* gP = p.probs + (((int64_t)bi * p.heads + h) * tq + m0 + half * 8) * tk;
+    const float* Ps = Q + (m0 + half * 8) * L4;
 #pragma unroll
-    for(int r = 0; r < 16; ++r)
+    for(int r = 0; r < 8; ++r)
       if(r < rows) {
 #pragma unroll
         for(int c = lane; c < TT; c += 32)
           if(c < tk)
-            gP[r * tk + c] = Q[(m0 + r) * L4 + c];
+            gP[r * tk + c] = Ps[r * L4 + c];
       }
   }
-  // O = P V (16 x 64 per warp): keys outer, the 8 independent 16x8 output
-  // tiles inner (ILP across accumulators instead of one dependent chain)
-  float o[DKT / 8][4];
+  // O = P V over this warp's 32 columns: keys outer, 4 output tiles inner
+  float o[NJ][4];
 #pragma unroll
-  for(int jd = 0; jd < DKT / 8; ++jd)
+  for(int jd = 0; jd < NJ; ++jd)
     o[jd][0] = o[jd][1] = o[jd][2] = o[jd][3] = 0.f;
 #pragma unroll
   for(int kk = 0; kk < NT; ++kk) {
     const int c = kk * 8 + t;
     const uint32_t a0 = tf32(P0[c]), a1 = tf32(P1[c]), a2 = tf32(P0[c + 4]), a3 = tf32(P1[c + 4]);
-    const float* Vr = V + c * L8 + g;
+    const float* Vr = V + c * L8 + half * 32 + g;
 #pragma unroll
-    for(int jd = 0; jd < DKT / 8; ++jd)
+    for(int jd = 0; jd < NJ; ++jd)
       mma8(o[jd], a0, a1, a2, a3, tf32(Vr[jd * 8]), tf32(Vr[jd * 8 + 4 * L8]));
   }
-  float* out = p.out + (int64_t)bi * tq * p.ldo + hoff;
+  float* out = p.out + (int64_t)bi * tq * p.ldo + hoff + half * 32;
 #pragma unroll
-  for(int jd = 0; jd < DKT / 8; ++jd) {
+  for(int jd = 0; jd < NJ; ++jd) {
     const int col = jd * 8 + 2 * t;
     if(r0 < tq)
       *reinterpret_cast<float2*>(out + (int64_t)r0 * p.ldo + col) = make_float2(o[jd][0], o[jd][1]);
@@ -529,7 +550,7 @@ int mtkc_attention_tc(float* out, int64_t ldo, float* probs, const float* q, int
     size_t smem = fwd_smem<TTV>();                                                \
     if(int rc = set_smem_attr((const void*)attn_tc_fwd_kernel<TTV>, smem))        \
       return rc;                                                                  \
-    ::mtkc::launch(attn_tc_fwd_kernel<TTV>, grid, TTV * 2, smem, S(stream), p);               \
+    ::mtkc::launch(attn_tc_fwd_kernel<TTV>, grid, TTV * 4, smem, S(stream), p);               \
   }
   MTKC_TC_FWD(16) MTKC_TC_FWD(32) MTKC_TC_FWD(48) MTKC_TC_FWD(64)
 #undef MTKC_TC_FWD
