@@ -187,9 +187,12 @@ struct TcP {
   const float* biasP[3];
   float* CP[3];
   // fused operand sums (mtkc_gemm_args.colsum): csOp 1 = A (rows of op(A),
-  // length M, tiles with n0 == 0), 2 = B (columns of op(B), length N, tiles
-  // with m0 == 0); split-K writes partials csPart[nOut][splits][csLen]
-  int csOp, csAcc;
+  // length M), 2 = B (columns of op(B), length N).  The R = nt (A) or mt (B)
+  // tiles sharing an operand block split its k-blocks round-robin (tile i
+  // sums k-blocks kb % R == i), so no CTA carries all the extra smem reads;
+  // with csSlots = splits * R > 1 the partials go to
+  // csPart[nOut][csSlots][csLen] (slot split * R + i), summed by the reduce
+  int csOp, csAcc, csSlots, csR;
   int64_t csLen;
   float* csOut[3];
   float* csPart;
@@ -659,7 +662,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x) {
       int m0, n0, kb0, nkb, split;
       tileCoords(t, m0, n0, kb0, nkb, split);
-      const bool on = sumB ? (B_MN && m0 == 0) : (A_MN && n0 == 0);
+      // the first csR tiles of the operand block take its k-blocks in turn
+      const int R = p.csR, ri = sumB ? m0 / BM : n0 / BN;
+      const bool on = (sumB ? B_MN : A_MN) && ri < R;
       float4 acc[CH];
 #pragma unroll
       for(int c = 0; c < CH; ++c)
@@ -667,7 +672,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for(int kb = 0; kb < nkb; ++kb, ++i) {
         const int s = i % ST;
         mbar_wait(&full[s], (i / ST) & 1);
-        if(on) {
+        if(on && (kb0 + kb) % R == ri) {
           const uint8_t* base = sOp + s * sBytes;
 #pragma unroll
           for(int c = 0; c < CH; ++c)
@@ -689,9 +694,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if(!on)
         continue;
       const int64_t len = p.csLen, base0 = sumB ? n0 : m0;
-      float* dst = p.splits > 1 ? p.csPart + ((int64_t)tprob * p.splits + split) * len
-                                : p.csOut[tprob];
-      const bool add = p.splits == 1 && p.csAcc;
+      float* dst = p.csSlots > 1
+                       ? p.csPart + ((int64_t)tprob * p.csSlots + split * R + ri) * len
+                       : p.csOut[tprob];
+      const bool add = p.csSlots == 1 && p.csAcc;
 #pragma unroll
       for(int c = 0; c < CH; ++c)
         if(c < nch) {
@@ -726,11 +732,11 @@ struct ReduceOut {
   float* C[3];
   const float* bias[3];
   const float* Cin[3];
-  // fused operand sums: partials [nOut][splits][csLen] -> cs[q] (+=, csAcc)
+  // fused operand sums: partials [nOut][csSlots][csLen] -> cs[q] (+=, csAcc)
   float* cs[3];
   const float* csPart;
   int64_t csLen;
-  int csAcc;
+  int csAcc, csSlots;
 };
 
 template <bool VEC>
@@ -797,13 +803,21 @@ __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plan
     }
   }
   if(outs.csPart) {  // operand sums: splits added in order
-    const float* cp = outs.csPart + (int64_t)q * splits * outs.csLen;
+    const float* cp = outs.csPart + (int64_t)q * outs.csSlots * outs.csLen;
     float* cs = outs.cs[q];
     for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < outs.csLen;
         i += (int64_t)gridDim.x * blockDim.x) {
       float x = 0.f;
-      for(int s = 0; s < splits; ++s)
-        x += cp[s * outs.csLen + i];
+      for(int s0 = 0; s0 < outs.csSlots; s0 += 8) {  // eight loads in flight
+        float y[8];
+#pragma unroll
+        for(int u = 0; u < 8; ++u)
+          y[u] = s0 + u < outs.csSlots ? cp[(s0 + u) * outs.csLen + i] : 0.f;
+#pragma unroll
+        for(int u = 0; u < 8; ++u)
+          if(s0 + u < outs.csSlots)
+            x += y[u];
+      }
       cs[i] = outs.csAcc ? cs[i] + x : x;
     }
   }
@@ -1001,6 +1015,10 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   if(const char* e = getenv("MTK_GEMM_BN"))  // tuning override (tools/gemm_bench.py)
     BN = (atoi(e) == 256 && a.N >= 256) ? 256 : 128;
   const int64_t nt = cdiv(a.N, BN);
+  // tiles sharing the summed operand's k-blocks (MTK_CS_DIST=0: one tile);
+  // capped so the reduce sums at most ~32 partial slots per column
+  static const bool csDist = !getenv("MTK_CS_DIST") || getenv("MTK_CS_DIST")[0] != '0';
+  const int64_t csTiles = csOp == 2 ? mt : nt;
   const int nkbProb = (int)cdiv(a.K, BK);
   const int numKb = kconcat ? nkbProb * nprob : nkbProb;
   // Split K to fill the machine: pick the split count that maximises the
@@ -1014,7 +1032,7 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   if(a.workspace && numKb >= 2 * minKb) {
     double best = (double)tiles / (double)(g_sms * cdiv(tiles, g_sms));
     for(int s = 2; s <= 16 && numKb / s >= minKb; ++s) {
-      size_t need = (size_t)s * nOut * ((size_t)a.M * (size_t)a.N + (csOp ? csLen : 0)) *
+      size_t need = (size_t)s * nOut * ((size_t)a.M * (size_t)a.N + (csOp ? csLen * csTiles : 0)) *
                     sizeof(float);
       if(need > a.workspace_bytes)
         break;
@@ -1028,6 +1046,7 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   }
   const int kbPer = (int)cdiv(numKb, splits);
   splits = (int)cdiv(numKb, kbPer);
+  const int64_t csR = csDist ? std::max<int64_t>(1, std::min<int64_t>(csTiles, 32 / splits)) : 1;
 
   TcMaps maps;
   std::memset(&maps, 0, sizeof(maps));
@@ -1090,7 +1109,20 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   p.csOp = csOp;
   p.csAcc = a.colsum_accumulate;
   p.csLen = csLen;
-  p.csPart = (csOp && splits > 1) ? a.workspace + (size_t)splits * nOut * a.M * a.N : nullptr;
+  p.csSlots = csOp ? (int)(splits * csR) : 0;
+  p.csR = (int)csR;
+  p.csPart = nullptr;
+  if(p.csSlots > 1) {
+    const size_t off = splits > 1 ? (size_t)splits * nOut * a.M * a.N : 0;
+    const size_t need = (off + (size_t)nOut * p.csSlots * csLen) * sizeof(float);
+    if(!a.workspace || need > a.workspace_bytes) {
+      p.csOp = 0;  // no room for the partials: the caller sums separately
+      p.csSlots = 0;
+      csOp = 0;
+    } else {
+      p.csPart = a.workspace + off;
+    }
+  }
   p.kbPerSplit = kbPer;
   p.numKb = numKb;
   p.mt = (int)mt;
@@ -1140,6 +1172,7 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     outs.csPart = p.csPart;
     outs.csLen = csLen;
     outs.csAcc = a.colsum_accumulate;
+    outs.csSlots = p.csSlots;
     const int64_t sstride = (int64_t)nOut * a.M * a.N;  // between splits
     const dim3 grid(grid1d(a.M * cdiv(a.N, 4), 256, 148 * 32 / std::max(1, nOut)),
                     (unsigned)nOut);
@@ -1149,6 +1182,23 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     else
       ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, a.workspace, splits,
                      sstride, a.M, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue, a.gate);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if(e != cudaSuccess)
+      *rc = cuda_status(e, "splitk_reduce_kernel");
+  }
+  if(*rc == MTKC_OK && splits == 1 && p.csPart) {  // operand-sum partials only
+    ReduceOut outs{};
+    for(int q = 0; q < nOut; ++q)
+      outs.cs[q] = p.csOut[q];
+    outs.csPart = p.csPart;
+    outs.csLen = csLen;
+    outs.csAcc = a.colsum_accumulate;
+    outs.csSlots = p.csSlots;
+    const dim3 grid(grid1d(csLen, 256, 148), (unsigned)nOut);
+    ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, (const float*)nullptr, 1,
+                   (int64_t)0, (int64_t)0, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue,
+                   (const float*)nullptr);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if(e != cudaSuccess)
