@@ -42,16 +42,46 @@ void Shape::pad4(int64_t out[4]) const {
 
 // Caching device allocator: cudaMalloc/cudaFree synchronise the device, so
 // steady-state training must never call them.  Freed blocks go to a size-
-// keyed free list and are reused.  Every kernel runs on the one compute
-// stream, so a block released by the host may be handed out again at once:
-// work queued later on the stream runs after all work that used it.
+// keyed free list and are reused.  Small blocks (batch masks, index vectors:
+// a new batch shape brings new sizes) are carved from 64 MB slabs in
+// power-of-two / 1.5x size classes, so a size first seen inside a timed
+// step costs no cudaMalloc.  Every kernel runs on the one compute stream, so
+// a block released by the host may be handed out again at once: work queued
+// later on the stream runs after all work that used it.
 namespace {
 struct BlockCache {
+  static constexpr size_t SMALL = (size_t)1 << 20, SLAB = (size_t)64 << 20;
   std::map<size_t, std::vector<void*>> free;
+  char* slab = nullptr;
+  size_t slabLeft = 0;
   static size_t round(size_t bytes) {
-    if(bytes <= ((size_t)1 << 20))
-      return (bytes + 511) & ~(size_t)511;
+    if(bytes <= SMALL) {
+      size_t p = 512;
+      while(p < bytes) {
+        if(p >= 1024 && p + p / 2 >= bytes)
+          return p + p / 2;
+        p <<= 1;
+      }
+      return p;
+    }
     return (bytes + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);
+  }
+  void* take(size_t bytes) {
+    if(bytes > SMALL) {
+      void* p = nullptr;
+      MTKC(mtkc_malloc(&p, bytes));
+      return p;
+    }
+    if(slabLeft < bytes) {
+      void* p = nullptr;
+      MTKC(mtkc_malloc(&p, SLAB));
+      slab = (char*)p;
+      slabLeft = SLAB;
+    }
+    void* p = slab;
+    slab += bytes;
+    slabLeft -= bytes;
+    return p;
   }
 };
 BlockCache& cache() {
@@ -69,9 +99,7 @@ DeviceBuffer::DeviceBuffer(size_t n) : elems(n) {
     fl.pop_back();
     return;
   }
-  void* p = nullptr;
-  MTKC(mtkc_malloc(&p, bytes));
-  ptr = (float*)p;
+  ptr = (float*)cache().take(bytes);
 }
 
 DeviceBuffer::~DeviceBuffer() {
