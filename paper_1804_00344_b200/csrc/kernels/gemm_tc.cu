@@ -98,6 +98,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// one box of a tensor map into L2 (no shared-memory destination)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   (uint64_t)map),
+               "r"(x), "r"(y)
+               : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
 }
@@ -437,9 +445,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int m0, n0, kb0, nkb, split;
       tileCoords(t, m0, n0, kb0, nkb, split);
       const int acc = lt & 1;
+      const int64_t rowBase = m0 + q * 32;
+      // the epilogue's extra sources (residual / beta*C, ReLU gate) of this
+      // warp's rows into L2 while the tile's main loop still runs
+      if(LOADS && p.tmaStore && !p.part && lane == 0 && rowBase < p.M) {
+        const int pr = p.kconcat ? 0 : t / tilesPerProb;
+        const CUtensorMap* src0 = p.beta != 0.f ? (p.hasAddend ? &maps.r : &maps.c[pr]) : nullptr;
+        const CUtensorMap* src1 = p.gate ? &maps.g : nullptr;
+        for(int c0 = cBeg; c0 < cEnd && n0 + c0 < p.N; c0 += 32) {
+          if(src0)
+            tma_prefetch_2d(src0, n0 + c0, (int)rowBase);
+          if(src1)
+            tma_prefetch_2d(src1, n0 + c0, (int)rowBase);
+        }
+      }
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
-      const int64_t rowBase = m0 + q * 32;
       const CUtensorMap* mapC = &maps.c[p.part ? 0 : tprob];
       const float* biasT = p.biasP[tprob];
       float* CT = p.CP[tprob];
