@@ -153,6 +153,13 @@ typedef struct mtkc_gemm_args {
                            fixed order); FP32 precision runs mtkc_colsum. */
   int colsum_of;
   int colsum_accumulate;
+  uint32_t* relu_mask_out;   /* optional (batch 1): bit c%32 of word
+                                [r * ceil(N/32) + c/32] = (C[r][c] > 0) after the
+                                epilogue -- the ReLU gate of the consumer's
+                                backward at 1/32 of the bytes of C */
+  const uint32_t* gate_mask; /* optional (batch 1), instead of gate: C[r][c] is
+                                zeroed where that bit of a relu_mask_out-style
+                                mask (same N) is 0 */
 } mtkc_gemm_args;
 
 #define MTKC_COLSUM_A 1

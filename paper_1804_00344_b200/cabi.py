@@ -29,6 +29,7 @@ class GemmArgs(C.Structure):
         ("precision", C.c_int), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("addend", C.c_void_p),
         ("colsum", C.c_void_p), ("colsum_of", C.c_int), ("colsum_accumulate", C.c_int),
+        ("relu_mask_out", C.c_void_p), ("gate_mask", C.c_void_p),
     ]
 
 
@@ -61,10 +62,11 @@ def check(rc: int):
 def gemm(M, N, K, A, lda, B, ldb, Cp, ldc, trans_a=False, trans_b=False, alpha=1.0, beta=0.0,
          bias=None, relu=False, gate=None, precision=1, workspace=None, workspace_bytes=0,
          stream=None, batch=1, stride_a=0, stride_b=0, stride_c=0, addend=None, colsum=None,
-         colsum_of=0, colsum_accumulate=False):
+         colsum_of=0, colsum_accumulate=False, relu_mask_out=None, gate_mask=None):
     g = GemmArgs(M, N, K, batch, A, lda, stride_a, int(trans_a), B, ldb, stride_b, int(trans_b),
                  Cp, ldc, stride_c, alpha, beta, bias, 1 if relu else 0, gate, precision,
-                 workspace, workspace_bytes, addend, colsum, colsum_of, int(colsum_accumulate))
+                 workspace, workspace_bytes, addend, colsum, colsum_of, int(colsum_accumulate),
+                 relu_mask_out, gate_mask)
     check(lib().mtkc_gemm(C.byref(g), stream))
     return lib().mtkc_gemm_last_path()
 

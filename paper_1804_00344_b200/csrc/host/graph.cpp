@@ -215,7 +215,7 @@ ExpressionGraph::GradDst ExpressionGraph::gradDst(int nodeIndex, bool supportsGa
     Param& p = paramOf(n);
     int acc = p.gradLive ? 1 : 0;
     p.gradLive = true;
-    return {p.grad.dev(), acc, nullptr};
+    return {p.grad.dev(), acc, nullptr, nullptr};
   }
   if(n.grad.empty())
     n.grad = allocTensor(n.shape);
@@ -223,7 +223,8 @@ ExpressionGraph::GradDst ExpressionGraph::gradDst(int nodeIndex, bool supportsGa
   n.gradLive = true;
   if(n.gate && !supportsGate)
     n.gradGated = false;
-  return {n.grad.dev(), acc, supportsGate ? n.gate : nullptr};
+  return {n.grad.dev(), acc, supportsGate ? n.gate : nullptr,
+          supportsGate ? n.gateMask : nullptr};
 }
 
 const float* ExpressionGraph::gradSrc(Node& n) {
@@ -250,7 +251,8 @@ void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
           int64_t ldb, bool tB, float* C, int64_t ldc, float beta, const float* bias = nullptr,
           int epi = MTKC_EPI_NONE, const float* gate = nullptr, int64_t batch = 1,
           int64_t sA = 0, int64_t sB = 0, int64_t sC = 0, float* colsum = nullptr,
-          int colsumOf = 0, int colsumAcc = 0) {
+          int colsumOf = 0, int colsumAcc = 0, const uint32_t* gateMask = nullptr,
+          uint32_t* maskOut = nullptr) {
   Device& d = Device::get();
   mtkc_gemm_args g{};
   g.M = M;
@@ -279,6 +281,11 @@ void gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool tA,
   g.colsum = colsum;
   g.colsum_of = colsumOf;
   g.colsum_accumulate = colsumAcc;
+  if(gateMask) {  // the bit form replaces the float gate
+    g.gate = nullptr;
+    g.gate_mask = gateMask;
+  }
+  g.relu_mask_out = maskOut;
   MTKC(mtkc_gemm(&g, d.stream()));
 }
 
@@ -707,18 +714,27 @@ static NodeRef affineImpl(ExpressionGraph& g, NodeRef x, NodeRef w, NodeRef b, b
   n.inputs = {x.index, w.index, b.index};
   int64_t rows = x.shape.size() / K;
   n.fwd = [rows, K, N, transW, relu](ExpressionGraph& g, ExpressionGraph::Node& n) {
+    // TF32: the ReLU also leaves its gate as a bit mask for the consumer's dX
+    uint32_t* bits = nullptr;
+    if(relu && Device::get().precision() == Precision::TF32) {
+      n.gateBits = g.allocTensor(Shape({rows, (N + 31) / 32}));
+      bits = reinterpret_cast<uint32_t*>(n.gateBits.dev());
+    }
     gemm(rows, N, K, g.valPtr(n.inputs[0]), K, false, g.valPtr(n.inputs[1]), transW ? K : N,
          transW, n.value.dev(), N, 0.f, g.valPtr(n.inputs[2]),
-         relu ? MTKC_EPI_RELU : MTKC_EPI_NONE);
-    if(relu)
+         relu ? MTKC_EPI_RELU : MTKC_EPI_NONE, nullptr, 1, 0, 0, 0, nullptr, 0, 0, nullptr, bits);
+    if(relu) {
       n.gate = n.value.devc();
+      n.gateMask = bits;
+    }
   };
   n.bwd = [rows, K, N, transW](ExpressionGraph& g, ExpressionGraph::Node& n) {
     const float* go = g.gradSrc(n);
     {  // dX = dY op(W)^T
       auto d = g.gradDst(n.inputs[0], true);
       gemm(rows, K, N, go, N, false, g.valPtr(n.inputs[1]), transW ? K : N, !transW, d.ptr, K,
-           d.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, d.gate);
+           d.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, d.gate, 1, 0, 0, 0, nullptr, 0, 0,
+           d.gateMask);
     }
     {  // dW, with db = colsum(dY) summed from the dY tiles the product stages
       auto d = g.gradDst(n.inputs[1]);
@@ -847,7 +863,8 @@ std::vector<NodeRef> ExpressionGraph::affineGroup(NodeRef x, const std::vector<N
           for(size_t q = 0; q < live.size(); ++q) {
             auto dq = q == 0 ? d : g.gradDst(grp->x, true);
             gemm(rows, K, N, dY[q], N, false, g.valPtr(grp->W[live[q]]), N, true, dq.ptr, K,
-                 dq.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, dq.gate);
+                 dq.accumulate ? 1.f : 0.f, nullptr, MTKC_EPI_NONE, dq.gate, 1, 0, 0, 0, nullptr, 0,
+                 0, dq.gateMask);
           }
         } else {
           mtkc_gemm_args probs[3];

@@ -22,6 +22,21 @@ namespace {
 
 thread_local int t_last_path = 0;
 
+// relu_mask_out after a CUDA-core product: one warp per 32-column word
+__global__ void relu_mask_pack_kernel(const float* C, int64_t ldc, int64_t M, int64_t N,
+                                      uint32_t* mask) {
+  MTKC_PDL_ENTRY();
+  const int64_t mw = (N + 31) / 32, words = M * mw;
+  const int lane = threadIdx.x & 31;
+  for(int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; w < words;
+      w += (int64_t)gridDim.x * blockDim.x / 32) {
+    const int64_t r = w / mw, c = (w - r * mw) * 32 + lane;
+    const uint32_t bits = __ballot_sync(0xffffffffu, c < N && C[r * ldc + c] > 0.f);
+    if(lane == 0)
+      mask[w] = bits;
+  }
+}
+
 // The operand sums of mtkc_gemm_args.colsum as a separate pass (FP32
 // precision, or a tensor-core launch that could not fuse them): column sums
 // of the stored MN-major operand with mtkc_colsum's summation order.
@@ -58,6 +73,8 @@ struct GemmP {
   const float* bias;
   int epi;
   const float* gate;
+  const uint32_t* gateMask;  // bit mask form of the gate (batch 1), words per row mw
+  int64_t mw;
   int foldBatch;  // sum over batch into one C
 };
 
@@ -71,7 +88,7 @@ __global__ void __launch_bounds__(256) gemm_fp32_kernel(GemmP p) {
   float* C = p.C + zb * p.sC;
   const float* Cin = p.Cin + zb * p.sC;
   float acc[4][4];
-  const bool gated = p.gate != nullptr;
+  const bool gated = p.gate != nullptr || p.gateMask != nullptr;
 #pragma unroll
   for(int i = 0; i < 4; ++i)
 #pragma unroll
@@ -144,7 +161,9 @@ __global__ void __launch_bounds__(256) gemm_fp32_kernel(GemmP p) {
         v = v > 0.f ? v : 0.f;
       float* dst = C + r * p.ldc + c;
       if(gated) {
-        v = p.gate[zb * p.sC + r * p.ldc + c] > 0.f ? v : 0.f;
+        const bool on = p.gateMask ? ((p.gateMask[r * p.mw + (c >> 5)] >> (c & 31)) & 1u) != 0
+                                   : p.gate[zb * p.sC + r * p.ldc + c] > 0.f;
+        v = on ? v : 0.f;
         if(p.beta != 0.f)
           v = __fadd_rn(p.beta == 1.f ? Cin[r * p.ldc + c] : __fmul_rn(p.beta, Cin[r * p.ldc + c]),
                         v);
@@ -206,11 +225,20 @@ int mtkc_gemm(const mtkc_gemm_args* a, void* stream) {
   p.bias = a->bias;
   p.epi = a->epilogue;
   p.gate = a->gate;
+  p.gateMask = a->gate_mask;
+  p.mw = (a->N + 31) / 32;
+  if((a->gate_mask || a->relu_mask_out) && a->batch != 1)
+    return fail(MTKC_CONTRACT, "mtkc_gemm: relu masks need batch == 1");
   p.foldBatch = (a->batch > 1 && a->strideC == 0) ? 1 : 0;
   dim3 grid((unsigned)cdiv(a->N, TN), (unsigned)cdiv(a->M, TM),
             p.foldBatch ? 1u : (unsigned)a->batch);
   ::mtkc::launch(gemm_fp32_kernel, grid, 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("gemm_fp32_kernel");
+  if(a->relu_mask_out) {
+    ::mtkc::launch(relu_mask_pack_kernel, grid1d(a->M * ((a->N + 31) / 32) * 32, 256, 148 * 16),
+                   256, 0, S(stream), (const float*)a->C, a->ldc, a->M, a->N, a->relu_mask_out);
+    MTKC_POST_LAUNCH("relu_mask_pack_kernel");
+  }
   return colsum_after(*a, stream);
 }
 

@@ -201,6 +201,11 @@ struct TcP {
   // with csSlots = splits * R > 1 the partials go to
   // csPart[nOut][csSlots][csLen] (slot split * R + i), summed by the reduce
   int csOp, csAcc, csSlots, csR;
+  // ReLU gate as a bit mask: maskOut written by a ReLU producer, gateMask
+  // read by the consumer's dX product; maskW words per row
+  uint32_t* maskOut;
+  const uint32_t* gateMask;
+  int64_t maskW;
   int64_t csLen;
   float* csOut[3];
   float* csPart;
@@ -465,6 +470,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const float* biasT = p.biasP[tprob];
       float* CT = p.CP[tprob];
       const int zpart = split * nOut + tprob;  // partial plane of this tile
+      // relu_mask_out words of this lane's row, stored once per tile (a full
+      // 16/32-byte run per row instead of one 4-byte store per chunk)
+      constexpr int MWN = BN * 4 / EPI_WARPS / 32;
+      uint32_t mwords[MWN];
+#pragma unroll
+      for(int j = 0; j < MWN; ++j)
+        mwords[j] = 0;
 #pragma unroll 1
       for(int c0 = cBeg; c0 < cEnd; c0 += 32) {
         float cur[32];
@@ -477,6 +489,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             loadChunk(tn, c0 + 32 < cEnd ? c0 + 32 : cBeg);
         }
         float v[32];
+        uint32_t gm = 0;  // gate-mask word of this lane's row and chunk (issued early)
+        if(p.gateMask && !p.part && rowBase + lane < p.M && n0 + c0 < p.N)
+          gm = __ldg(p.gateMask + (rowBase + lane) * p.maskW + (n0 + c0) / 32);
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
         if(c0 + 32 >= cEnd) {  // our share read: hand it back to the MMA warp
           tc_fence_before();
@@ -557,6 +572,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               for(int i = 0; i < 32; ++i)
                 v[i] = v[i] > 0.f ? v[i] : 0.f;
             }
+            if(p.gateMask) {
+#pragma unroll
+              for(int i = 0; i < 32; ++i)
+                v[i] = ((gm >> i) & 1u) ? v[i] : 0.f;
+            }
             // ReLU gate, then beta*C, from the TMA-loaded boxes (straight-line
             // loops under uniform branches)
             if(pf) {
@@ -597,6 +617,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                   v[4 * j + 3] = beta * c4.w + v[4 * j + 3];
                 }
               }
+            }
+            if(p.maskOut) {  // after beta*C: bits of the stored C, written per tile
+              uint32_t w = 0;
+#pragma unroll
+              for(int i = 0; i < 32; ++i)
+                w |= (v[i] > 0.f && col0 + i < p.N) ? (1u << i) : 0u;
+              mwords[(c0 - cBeg) >> 5] = w;
             }
             __syncwarp();  // every lane has read its C / gate row before the overwrite
           }
@@ -641,6 +668,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for(int r = 0; r < rows; ++r) {
           float x = st[r * EPI_STRIDE + lane];
           const int64_t rr = rowBase + r;
+          if(p.maskOut && !p.part) {  // bits of the final value (lanes = columns)
+            float y = p.alpha == 1.f ? x : p.alpha * x;
+            if(biasT)
+              y = y + bcol;
+            if(p.epi == MTKC_EPI_RELU)
+              y = y > 0.f ? y : 0.f;
+            if(p.gate)
+              y = (colOk && p.gate[rr * p.ldc + col] > 0.f) ? y : 0.f;
+            if(p.gateMask)
+              y = (colOk && ((p.gateMask[rr * p.maskW + col0 / 32] >> lane) & 1u)) ? y : 0.f;
+            if(p.beta != 0.f && colOk) {
+              const float cv = p.addend ? p.addend[rr * p.ldc + col] : CT[rr * p.ldc + col];
+              y = (p.beta == 1.f ? cv : p.beta * cv) + y;
+            }
+            const uint32_t bits = __ballot_sync(0xffffffffu, colOk && y > 0.f);
+            if(lane == 0)
+              p.maskOut[rr * p.maskW + col0 / 32] = bits;
+          }
           if(!colOk)
             continue;
           if(p.part) {
@@ -655,6 +700,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             x = x > 0.f ? x : 0.f;
           if(p.gate)
             x = p.gate[rr * p.ldc + col] > 0.f ? x : 0.f;
+          if(p.gateMask)
+            x = ((p.gateMask[rr * p.maskW + col0 / 32] >> lane) & 1u) ? x : 0.f;
           if(p.beta != 0.f) {
             const float cv = p.addend ? p.addend[rr * p.ldc + col] : *dst;
             x = (p.beta == 1.f ? cv : p.beta * cv) + x;
@@ -662,6 +709,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           *dst = x;
         }
         __syncwarp();
+      }
+      if(p.maskOut && p.tmaStore && !p.part && rowBase + lane < p.M && n0 + cBeg < p.N) {
+        uint32_t* dst = p.maskOut + (rowBase + lane) * p.maskW + (n0 + cBeg) / 32;
+        const int nw = (int)min((int64_t)MWN, p.maskW - (n0 + cBeg) / 32);
+        if(nw == MWN && ((uintptr_t)dst & 15) == 0) {
+#pragma unroll
+          for(int j = 0; j < MWN; j += 4)
+            *reinterpret_cast<uint4*>(dst + j) =
+                make_uint4(mwords[j], mwords[j + 1], mwords[j + 2], mwords[j + 3]);
+        } else {
+          for(int j = 0; j < nw; ++j)
+            dst[j] = mwords[j];
+        }
       }
     }
     if(lane == 0)
@@ -763,7 +823,8 @@ struct ReduceOut {
 template <bool VEC>
 __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plane, int64_t M,
                                      int64_t N, ReduceOut outs, int64_t ldc, float alpha,
-                                     float beta, int epi, const float* gate) {
+                                     float beta, int epi, const float* gate,
+                                     const uint32_t* gateMask) {
   MTKC_PDL_ENTRY();
   // problem q's partials start at part + q*M*N; splits are `plane` apart
   const int q = blockIdx.y;
@@ -812,6 +873,8 @@ __global__ void splitk_reduce_kernel(const float* part, int splits, int64_t plan
         x = x > 0.f ? x : 0.f;
       if(gate)
         x = gate[r * ldc + c + u] > 0.f ? x : 0.f;
+      if(gateMask)
+        x = ((gateMask[r * ((N + 31) / 32) + (c + u) / 32] >> ((c + u) & 31)) & 1u) ? x : 0.f;
       if(beta != 0.f)
         x = (beta == 1.f ? src[u] : beta * src[u]) + x;
       out[u] = x;
@@ -1002,7 +1065,7 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     if(((uintptr_t)b.A % 16) || ((uintptr_t)b.B % 16))
       return false;
   }
-  if(nprob > 1 && (a.gate || a.addend))
+  if(nprob > 1 && (a.gate || a.addend || a.gate_mask || a.relu_mask_out))
     return false;
   if(a.M < 1 || a.N < 8 || a.K < 8)
     return false;
@@ -1050,7 +1113,7 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   int splits = 1;
   const int64_t tiles = mt * nt * nOut;
   const int minKb = tiles * 4 <= g_sms ? 4 : 24;
-  if(a.workspace && numKb >= 2 * minKb) {
+  if(a.workspace && numKb >= 2 * minKb && !a.relu_mask_out) {  // masks: no split
     double best = (double)tiles / (double)(g_sms * cdiv(tiles, g_sms));
     for(int s = 2; s <= 16 && numKb / s >= minKb; ++s) {
       size_t need = (size_t)s * nOut * ((size_t)a.M * (size_t)a.N + (csOp ? csLen * csTiles : 0)) *
@@ -1130,6 +1193,9 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   p.csOp = csOp;
   p.csAcc = a.colsum_accumulate;
   p.csLen = csLen;
+  p.maskOut = a.relu_mask_out;
+  p.gateMask = a.gate_mask;
+  p.maskW = (a.N + 31) / 32;
   p.csSlots = csOp ? (int)(splits * csR) : 0;
   p.csR = (int)csR;
   p.csPart = nullptr;
@@ -1199,10 +1265,11 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
                     (unsigned)nOut);
     if(vec)
       ::mtkc::launch(splitk_reduce_kernel<true>, grid, 256, 0, st, a.workspace, splits, sstride,
-                     a.M, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue, a.gate);
+                     a.M, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue, a.gate, a.gate_mask);
     else
       ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, a.workspace, splits,
-                     sstride, a.M, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue, a.gate);
+                     sstride, a.M, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue, a.gate,
+                     a.gate_mask);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if(e != cudaSuccess)
@@ -1219,7 +1286,7 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     const dim3 grid(grid1d(csLen, 256, 148), (unsigned)nOut);
     ::mtkc::launch(splitk_reduce_kernel<false>, grid, 256, 0, st, (const float*)nullptr, 1,
                    (int64_t)0, (int64_t)0, a.N, outs, a.ldc, a.alpha, a.beta, a.epilogue,
-                   (const float*)nullptr);
+                   (const float*)nullptr, (const uint32_t*)nullptr);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if(e != cudaSuccess)

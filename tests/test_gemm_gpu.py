@@ -279,3 +279,46 @@ def test_gemm_group_fused_colsum(cuda):
         assert np.all(np.abs(cs[q].cpu().numpy() - want) <= tol), q
         w = x.T.astype(np.float64) @ dys[q]
         assert np.all(np.abs(Ws[q].cpu().numpy() - w) <= 4e-3 * (np.abs(x.T) @ np.abs(dys[q]) + 1)), q
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("shape", [(300, 70, 96), (1000, 2048, 512), (64, 2048, 8192)])
+def test_gemm_relu_bitmask(cuda, prec, shape):
+    """relu_mask_out / gate_mask: the ReLU producer's gate packed to one bit per
+    element (word [r][c/32], bits past N zero), and a consumer gated by it
+    equals the same consumer gated by the float ReLU output (bitwise) --
+    direct epilogue, split-K reduction (long K) and the CUDA-core path."""
+    import torch
+    rng = np.random.default_rng(13)
+    M, N, K = shape
+    mw = (N + 31) // 32
+    a = _dev(torch, rng.uniform(-1, 1, (M, 64)))
+    b = _dev(torch, rng.uniform(-1, 1, (64, N)))
+    bias = _dev(torch, rng.uniform(-0.5, 0.5, N))
+    h = torch.zeros(M, N, device="cuda")
+    mask = torch.full((M, mw), -1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    cabi.gemm(M, N, 64, a.data_ptr(), 64, b.data_ptr(), N, h.data_ptr(), N, bias=bias.data_ptr(),
+              relu=True, precision=prec, workspace=ws.data_ptr(), workspace_bytes=ws.numel(),
+              relu_mask_out=mask.data_ptr())
+    torch.cuda.synchronize()
+    hv = h.cpu().numpy()
+    words = mask.cpu().numpy().view(np.uint32)
+    bits = (words[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1
+    bits = bits.reshape(M, mw * 32)
+    assert np.array_equal(bits[:, :N] == 1, hv > 0)
+    assert not bits[:, N:].any()
+    # consumer: dH = dY W^T gated, K = the consumer's contraction
+    dy = _dev(torch, rng.uniform(-1, 1, (M, K)))
+    w = _dev(torch, rng.uniform(-1, 1, (N, K)))
+    outs = []
+    for use_mask in (False, True):
+        o = torch.zeros(M, N, device="cuda")
+        cabi.gemm(M, N, K, dy.data_ptr(), K, w.data_ptr(), K, o.data_ptr(), N, trans_b=True,
+                  gate=None if use_mask else h.data_ptr(),
+                  gate_mask=mask.data_ptr() if use_mask else None, precision=prec,
+                  workspace=ws.data_ptr(), workspace_bytes=ws.numel())
+        torch.cuda.synchronize()
+        outs.append(o.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.all(outs[1][hv <= 0] == 0)
