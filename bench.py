@@ -226,7 +226,7 @@ def run_b200(a):
     opts.seed = 1
     stepper = M.SyncStepper(model, g, adam, avg, opts)
 
-    prof_steps, e2e_steps = 2, max(3, min(a.steps, 10))
+    prof_steps, e2e_steps = 2, max(3, min(a.steps, 20))
     updates = a.warmup + a.steps + e2e_steps + prof_steps
     per_batch = max(1, budget // 70)
     n_pairs = int(updates * world * per_batch * 1.15) + 64

@@ -458,6 +458,17 @@ int mtkc_xent_backward(float* glogits, const float* logits, const float* lse,
                        const int32_t* targets, const float* mask, const float* gloss,
                        int64_t rows, int64_t vocab, float count, int accumulate,
                        void* stream);
+/* TF32-precision variants: same outputs from one pass over each row (online
+ * max / rescaled sum), exp via ex2.approx (relative error ~2^-21 per term);
+ * the backward needs vocab % 4 == 0 and 16-byte aligned rows (else it runs
+ * mtkc_xent_backward). */
+int mtkc_xent_forward_fast(const float* logits, const int32_t* targets, const float* mask,
+                           int64_t rows, int64_t vocab, float* lse, float* row_loss, float* loss,
+                           float count, void* stream);
+int mtkc_xent_backward_fast(float* glogits, const float* logits, const float* lse,
+                            const int32_t* targets, const float* mask, const float* gloss,
+                            int64_t rows, int64_t vocab, float count, int accumulate,
+                            void* stream);
 
 /* ======================================================================== */
 /* optimizer (Adam::updateTensor train.cpp:30-47, Adam::update :49-59,      */

@@ -1558,7 +1558,9 @@ NodeRef ExpressionGraph::crossEntropy(NodeRef logits, const IntMat& targets, con
       throw ContractError("cross entropy over a fully-masked batch");
     aux->stats = g.allocTensor(Shape({positions, 2}));
     aux->rowLoss = g.allocTensor(Shape({positions}));
-    MTKC(mtkc_xent_forward(g.valPtr(n.inputs[0]), (const int32_t*)aux->tg->ptr + aux->tgOff,
+    // TF32 mode: the one-pass kernels (the FP32 path keeps the reference's order)
+    const bool fast = Device::get().precision() == Precision::TF32;
+    MTKC((fast ? mtkc_xent_forward_fast : mtkc_xent_forward)(g.valPtr(n.inputs[0]), (const int32_t*)aux->tg->ptr + aux->tgOff,
                            aux->hasMask ? aux->mask.devc() : nullptr, positions, vocab,
                            aux->stats.dev(), aux->rowLoss.dev(), n.value.dev(), aux->count,
                            stream()));
@@ -1566,7 +1568,8 @@ NodeRef ExpressionGraph::crossEntropy(NodeRef logits, const IntMat& targets, con
   n.bwd = [aux, vocab, positions](ExpressionGraph& g, Node& n) {
     const float* go = g.gradSrc(n);
     auto d = g.gradDst(n.inputs[0]);
-    MTKC(mtkc_xent_backward(d.ptr, g.valPtr(n.inputs[0]), aux->stats.devc(),
+    const bool fast = Device::get().precision() == Precision::TF32;
+    MTKC((fast ? mtkc_xent_backward_fast : mtkc_xent_backward)(d.ptr, g.valPtr(n.inputs[0]), aux->stats.devc(),
                             (const int32_t*)aux->tg->ptr + aux->tgOff,
                             aux->hasMask ? aux->mask.devc() : nullptr, go, positions, vocab,
                             aux->count, d.accumulate, stream()));

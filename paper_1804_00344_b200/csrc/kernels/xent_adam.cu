@@ -124,6 +124,90 @@ __global__ void __launch_bounds__(256) xent_bwd_kernel(float* g, const float* lo
   }
 }
 
+// TF32-mode variants (mtkc_xent_forward_fast / _backward_fast): the same
+// stats / loss / gradient from ONE pass over each row -- running max and
+// rescaled sum (online softmax), exp as ex2.approx (__expf, rel. err ~2^-21)
+// and a reciprocal instead of a division per element.
+__global__ void __launch_bounds__(XT) xent_fwd_fast_kernel(const float* logits,
+                                                           const int32_t* tg, const float* mask,
+                                                           int64_t V, float* stats,
+                                                           float* rowLoss) {
+  MTKC_PDL_ENTRY();
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  const float* x = logits + r * V;
+  float mx = -INFINITY, s = 0.f;
+  auto add4 = [&](float a, float b, float c, float d) {
+    const float m4 = fmaxf(fmaxf(a, b), fmaxf(c, d));
+    if(m4 > mx) {
+      s = mx == -INFINITY ? 0.f : s * __expf(mx - m4);
+      mx = m4;
+    }
+    s += (__expf(a - mx) + __expf(b - mx)) + (__expf(c - mx) + __expf(d - mx));
+  };
+  if(V % 4 == 0 && ((uintptr_t)x % 16 == 0)) {
+    const float4* x4 = (const float4*)x;
+    int64_t j = threadIdx.x;
+    for(; j + XT < V / 4; j += 2 * XT) {  // two loads in flight
+      const float4 u = __ldcs(x4 + j), v = __ldcs(x4 + j + XT);
+      add4(u.x, u.y, u.z, u.w);
+      add4(v.x, v.y, v.z, v.w);
+    }
+    if(j < V / 4) {
+      const float4 u = __ldcs(x4 + j);
+      add4(u.x, u.y, u.z, u.w);
+    }
+  } else {
+    for(int64_t j = threadIdx.x; j < V; j += XT)
+      add4(x[j], -INFINITY, -INFINITY, -INFINITY);
+  }
+  // combine (max, sum) pairs across the block in a fixed order
+  const float M = block_max(mx, red);
+  float sc = mx == -INFINITY ? 0.f : s * __expf(mx - M);
+  sc = block_sum(sc, red);
+  if(threadIdx.x == 0) {
+    stats[2 * r] = M;
+    stats[2 * r + 1] = sc;
+    float m = mask ? mask[r] : 1.f;
+    float l = 0.f;
+    if(m != 0.f)
+      l = m * (M + logf(sc) - x[tg[r]]);
+    rowLoss[r] = l;
+  }
+}
+
+__global__ void __launch_bounds__(256) xent_bwd_fast_kernel(float* g, const float* logits,
+                                                            const float* stats,
+                                                            const int32_t* tg, const float* mask,
+                                                            const float* gloss, int64_t V,
+                                                            float count, int acc) {
+  MTKC_PDL_ENTRY();
+  const int64_t r = blockIdx.y;
+  const float m = mask ? mask[r] : 1.f;
+  const float gm = (gloss[0] / count) * m;
+  const float mx = stats[2 * r], scale = m != 0.f ? gm / stats[2 * r + 1] : 0.f;
+  const int32_t y = tg[r];
+  const float4* x4 = reinterpret_cast<const float4*>(logits + r * V);
+  float4* g4 = reinterpret_cast<float4*>(g + r * V);
+  for(int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < V / 4;
+      j += (int64_t)gridDim.x * blockDim.x) {
+    const float4 xv = __ldcs(x4 + j);
+    float4 o = acc ? g4[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    o.x += scale * __expf(xv.x - mx);
+    o.y += scale * __expf(xv.y - mx);
+    o.z += scale * __expf(xv.z - mx);
+    o.w += scale * __expf(xv.w - mx);
+    const int64_t d = (int64_t)y - 4 * j;
+    if(m != 0.f && d >= 0 && d < 4) {
+      if(d == 0) o.x -= gm;
+      if(d == 1) o.y -= gm;
+      if(d == 2) o.z -= gm;
+      if(d == 3) o.w -= gm;
+    }
+    g4[j] = o;
+  }
+}
+
 // One element of the reference's Adam + EMA, with separately rounded ops
 // (kernels are compiled with -fmad=false) in the reference's order.
 __device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v, float& a,
@@ -223,6 +307,37 @@ int mtkc_xent_backward(float* glogits, const float* logits, const float* lse,
   ::mtkc::launch(xent_bwd_kernel, grid, 256, 0, S(stream), glogits, logits, lse, targets, mask, gloss, rows,
                                               vocab, count, accumulate);
   MTKC_POST_LAUNCH("xent_bwd_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_xent_forward_fast(const float* logits, const int32_t* targets, const float* mask,
+                           int64_t rows, int64_t vocab, float* lse, float* row_loss, float* loss,
+                           float count, void* stream) {
+  if(rows <= 0)
+    return MTKC_OK;
+  ProfScope prof(S(stream), "xent", 4.0 * rows * vocab);  // read logits once
+  ::mtkc::launch(xent_fwd_fast_kernel, (unsigned)rows, XT, 0, S(stream), logits, targets, mask,
+                 vocab, lse, row_loss);
+  MTKC_POST_LAUNCH("xent_fwd_fast_kernel");
+  ::mtkc::launch(loss_sum_kernel, 1, 1024, 0, S(stream), row_loss, rows, count, loss);
+  MTKC_POST_LAUNCH("loss_sum_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_xent_backward_fast(float* glogits, const float* logits, const float* lse,
+                            const int32_t* targets, const float* mask, const float* gloss,
+                            int64_t rows, int64_t vocab, float count, int accumulate,
+                            void* stream) {
+  if(rows <= 0)
+    return MTKC_OK;
+  if(vocab % 4 || ((uintptr_t)logits | (uintptr_t)glogits) % 16)
+    return mtkc_xent_backward(glogits, logits, lse, targets, mask, gloss, rows, vocab, count,
+                              accumulate, stream);
+  ProfScope prof(S(stream), "xent", (accumulate ? 12.0 : 8.0) * rows * vocab);
+  const unsigned gx = (unsigned)std::min<int64_t>(cdiv(vocab / 4, 256), 8);
+  ::mtkc::launch(xent_bwd_fast_kernel, dim3(gx, (unsigned)rows), 256, 0, S(stream), glogits,
+                 logits, lse, targets, mask, gloss, vocab, count, accumulate);
+  MTKC_POST_LAUNCH("xent_bwd_fast_kernel");
   return MTKC_OK;
 }
 

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 from oracle import refbind as R
-from paper_1804_00344_b200 import mtk as M
+from paper_1804_00344_b200 import cabi, mtk as M
 
 pytestmark = pytest.mark.gpu
 
@@ -357,3 +357,43 @@ def test_colsum_group_matches_single():
     torch.cuda.synchronize()
     for q in range(3):
         assert torch.equal(single[q], grouped[q]), q
+
+
+@pytest.mark.parametrize("rows,vocab", [(37, 1000), (64, 32000), (5, 36)])
+def test_xent_fast_matches_exact(rows, vocab):
+    """mtkc_xent_forward_fast / _backward_fast (TF32 mode: one pass, online
+    max/sum, ex2.approx) against the reference-order kernels: row stats, loss
+    and logits gradient within 1e-5 relative; masked rows give zero loss and
+    gradient; accumulate adds."""
+    import ctypes as C
+    import torch
+    L = cabi.lib()
+    rng = np.random.default_rng(21)
+    x = torch.from_numpy(rng.normal(0, 3, (rows, vocab)).astype(np.float32)).cuda()
+    tg = torch.from_numpy(rng.integers(0, vocab, rows).astype(np.int32)).cuda()
+    mask = torch.from_numpy((rng.uniform(size=rows) > 0.2).astype(np.float32)).cuda()
+    go = torch.tensor([1.7], device="cuda")
+    cnt = float(mask.sum().item())
+    p = lambda t: C.c_void_p(t.data_ptr())
+    res = {}
+    for name in ("exact", "fast"):
+        fwd = L.mtkc_xent_forward if name == "exact" else L.mtkc_xent_forward_fast
+        bwd = L.mtkc_xent_backward if name == "exact" else L.mtkc_xent_backward_fast
+        stats = torch.zeros(rows, 2, device="cuda")
+        rl = torch.zeros(rows, device="cuda")
+        loss = torch.zeros(1, device="cuda")
+        cabi.check(fwd(p(x), p(tg), p(mask), C.c_int64(rows), C.c_int64(vocab), p(stats), p(rl),
+                       p(loss), C.c_float(cnt), None))
+        g = torch.full((rows, vocab), 0.25, device="cuda")
+        cabi.check(bwd(p(g), p(x), p(stats), p(tg), p(mask), p(go), C.c_int64(rows),
+                       C.c_int64(vocab), C.c_float(cnt), C.c_int(1), None))
+        torch.cuda.synchronize()
+        res[name] = (stats.cpu().numpy(), rl.cpu().numpy(), loss.item(), g.cpu().numpy())
+    (s0, r0, l0, g0), (s1, r1, l1, g1) = res["exact"], res["fast"]
+    assert np.array_equal(s0[:, 0], s1[:, 0])  # the row max is exact either way
+    assert np.allclose(s1[:, 1], s0[:, 1], rtol=1e-5)
+    assert np.allclose(r1, r0, rtol=1e-5, atol=1e-6)
+    assert abs(l1 - l0) <= 1e-5 * abs(l0)
+    assert np.all(r1[mask.cpu().numpy() == 0] == 0)
+    assert np.allclose(g1, g0, rtol=1e-5, atol=1e-7)
+    assert np.all(g1[mask.cpu().numpy() == 0] == 0.25)
