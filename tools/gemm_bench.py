@@ -10,7 +10,7 @@ from paper_1804_00344_b200 import cabi
 print("# lib", cabi.LIB_PATH)
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-R = 6629
+R = int(os.environ.get("MTK_BENCH_ROWS", "8184"))
 shapes = [  # (name, M, N, K, transA, transB)
     ("logits fwd  H.E^T", R, 32000, 512, 0, 1),
     ("logits dH = dL.E", R, 512, 32000, 0, 0),
