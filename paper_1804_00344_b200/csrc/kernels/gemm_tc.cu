@@ -209,7 +209,8 @@ struct TcP {
   int64_t csLen;
   float* csOut[3];
   float* csPart;
-  int dbg;  // profiling switches (MTK_GEMM_DEBUG): 1 = no epilogue stores, 2 = no MMAs
+  int dbg;  // profiling switches (MTK_GEMM_DEBUG): 1 = no epilogue stores, 2 = no MMAs,
+            // 4 = C / addend / gate through TMA boxes instead of per-lane prefetch
 };
 
 struct TcMaps {
@@ -419,7 +420,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // lane prefetches its row's 32 values of the NEXT chunk into registers
     // while the current chunk is processed (the load latency hides behind the
     // TMEM read and the stores); both sources together use TMA boxes.
-    const bool pf = LOADS && !p.part && p.tmaStore && ((p.beta != 0.f) != (p.gate != nullptr));
+    const bool pf = LOADS && !p.part && p.tmaStore && !(p.dbg & 4) &&
+                    ((p.beta != 0.f) != (p.gate != nullptr));
     float nx[32];
     auto loadChunk = [&](int tt, int cc) {
       const int pr = p.kconcat ? 0 : tt / tilesPerProb;
