@@ -311,6 +311,128 @@ __global__ void __launch_bounds__(LN_WARPS * 32)
   }
 }
 
+// Same backward, rows staged through shared memory with cp.async: each warp
+// keeps row i+1's dy / x / dx in flight (LNS stages) while it reduces row i,
+// so the rows in flight per SM are not bounded by the register file.  Each
+// lane copies and later reads back only its own 16-byte chunks (no warp
+// barrier needed); arithmetic identical to ln_bwd4_kernel.
+constexpr int LNS = 2;
+template <int NV>
+__global__ void __launch_bounds__(LN_WARPS * 32)
+    ln_bwd4_async_kernel(const float* dy, const float* x, const float* g, const float* mean,
+                         const float* invStd, float* dx, float* part, int64_t rows, int64_t d,
+                         int64_t rowsPerCta, int accDx) {
+  MTKC_PDL_ENTRY();
+  extern __shared__ float4 sm4[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // [LN_WARPS][LNS][3][NV*32] float4 row stages; after the row loop the
+  // same space holds the partials [LN_WARPS][2][d/4]
+  float4* stg = sm4 + (size_t)w * LNS * 3 * NV * 32;
+  float4* red4 = sm4;
+  float4 gg[NV], sg[NV], sb[NV];
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t c = 128 * k + 4 * lane;
+    gg[k] = c < d ? __ldg(reinterpret_cast<const float4*>(g + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    sg[k] = sb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int64_t r0 = blockIdx.x * rowsPerCta, r1 = min(rows, r0 + rowsPerCta);
+  auto issue = [&](int64_t row, int st) {
+    float4* b = stg + st * 3 * NV * 32;
+#pragma unroll
+    for(int k = 0; k < NV; ++k) {
+      const int64_t c = 128 * k + 4 * lane;
+      if(c < d) {
+        const uint32_t o = (uint32_t)__cvta_generic_to_shared(b + k * 32 + lane);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(o), "l"(dy + row * d + c)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(o + NV * 32 * 16),
+                     "l"(x + row * d + c)
+                     : "memory");
+        if(accDx)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(o + 2 * NV * 32 * 16),
+                       "l"(dx + row * d + c)
+                       : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int it = 0;
+  if(r0 + w < r1)
+    issue(r0 + w, 0);
+  for(int64_t row = r0 + w; row < r1; row += LN_WARPS, ++it) {
+    const int st = it % LNS;
+    if(row + LN_WARPS < r1) {
+      issue(row + LN_WARPS, (it + 1) % LNS);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    const float4* b = stg + st * 3 * NV * 32;
+    const float mu = mean[row], rs = invStd[row];
+    float4 dy4[NV], xh[NV];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for(int k = 0; k < NV; ++k) {
+      const int64_t c = 128 * k + 4 * lane;
+      dy4[k] = xh[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if(c < d) {
+        dy4[k] = b[k * 32 + lane];
+        const float4 x4 = b[NV * 32 + k * 32 + lane];
+        xh[k] = make_float4((x4.x - mu) * rs, (x4.y - mu) * rs, (x4.z - mu) * rs, (x4.w - mu) * rs);
+      }
+      const float4 d4v = dy4[k];
+      const float4 h = make_float4(d4v.x * gg[k].x, d4v.y * gg[k].y, d4v.z * gg[k].z,
+                                   d4v.w * gg[k].w);
+      s1 += (h.x + h.y) + (h.z + h.w);
+      s2 += (h.x * xh[k].x + h.y * xh[k].y) + (h.z * xh[k].z + h.w * xh[k].w);
+      sg[k].x += d4v.x * xh[k].x;
+      sg[k].y += d4v.y * xh[k].y;
+      sg[k].z += d4v.z * xh[k].z;
+      sg[k].w += d4v.w * xh[k].w;
+      f4add(sb[k], d4v);
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    const float m1 = s1 / (float)d, m2 = s2 / (float)d;
+#pragma unroll
+    for(int k = 0; k < NV; ++k) {
+      const int64_t c = 128 * k + 4 * lane;
+      if(c < d) {
+        const float4 d4v = dy4[k];
+        float4 o;
+        o.x = rs * (d4v.x * gg[k].x - m1 - xh[k].x * m2);
+        o.y = rs * (d4v.y * gg[k].y - m1 - xh[k].y * m2);
+        o.z = rs * (d4v.z * gg[k].z - m1 - xh[k].z * m2);
+        o.w = rs * (d4v.w * gg[k].w - m1 - xh[k].w * m2);
+        if(accDx)
+          f4add(o, b[2 * NV * 32 + k * 32 + lane]);
+        *reinterpret_cast<float4*>(dx + row * d + c) = o;
+      }
+    }
+  }
+  if(!part)
+    return;
+  __syncthreads();  // every warp is done with its stages
+  const int64_t d4 = d / 4;
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t c4 = 32 * k + lane;
+    if(c4 < d4) {
+      red4[(w * 2 + 0) * d4 + c4] = sg[k];
+      red4[(w * 2 + 1) * d4 + c4] = sb[k];
+    }
+  }
+  __syncthreads();
+  for(int64_t e = threadIdx.x; e < 2 * d4; e += LN_WARPS * 32) {
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for(int ww = 0; ww < LN_WARPS; ++ww)
+      f4add(t, red4[ww * 2 * d4 + e]);
+    reinterpret_cast<float4*>(part)[blockIdx.x * 2 * d4 + e] = t;  // [blk][q][d]
+  }
+}
+
 template <template <int> class K, typename... Args>
 void launch_v(int64_t d, dim3 grid, cudaStream_t st, Args... args);
 
@@ -445,6 +567,23 @@ int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* 
                            (int)smem);                                                       \
     ::mtkc::launch(ln_bwd4_kernel<NVV>, (unsigned)nblk, LN_WARPS * 32, smem, st,                         \
         dy, x, gain, mean, inv_std, dx, part, rows, d, rpc, accumulate_dx);                  \
+  } else
+  static const bool async = !getenv("MTK_LN_SYNC");
+  if(async && nv <= 4) {
+    const size_t smemA = 0;
+#define LN4_BWDA(NVV)                                                                         \
+  if(nv <= NVV) {                                                                             \
+    const size_t sm = std::max((size_t)LN_WARPS * LNS * 3 * NVV * 32 * 16,                     \
+                               part ? (size_t)LN_WARPS * 2 * d * 4 : (size_t)0);              \
+    if(sm > 48 * 1024)                                                                        \
+      cudaFuncSetAttribute(ln_bwd4_async_kernel<NVV>,                                         \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);             \
+    ::mtkc::launch(ln_bwd4_async_kernel<NVV>, (unsigned)nblk, LN_WARPS * 32, sm, st, dy, x,     \
+                   gain, mean, inv_std, dx, part, rows, d, rpc, accumulate_dx);               \
+  } else
+    LN4_BWDA(1) LN4_BWDA(2) LN4_BWDA(4) {}
+#undef LN4_BWDA
+    (void)smemA;
   } else
   LN4_BWD(1) LN4_BWD(2) LN4_BWD(4) LN4_BWD(8) {}
 #undef LN4_BWD
