@@ -1306,6 +1306,11 @@ struct EmbedAux {
   std::shared_ptr<DeviceBuffer> ids;
   int64_t off = 0;
   ScatterPlan plan;
+  // folded positional encoding (scaleAddConst on a fresh embedding):
+  // out = E[id] * scale + pe[pos], gradient scattered as scale * go
+  float scale = 1.f;
+  std::shared_ptr<Tensor> pe;
+  int64_t t = 1;
 };
 }  // namespace
 
@@ -1330,12 +1335,13 @@ NodeRef ExpressionGraph::embed(NodeRef table, const IntMat& ids) {
   int64_t cnt = ids.size();
   n.fwd = [aux, cnt, e, vocab](ExpressionGraph& g, Node& n) {
     MTKC(mtkc_embed(n.value.dev(), g.valPtr(n.inputs[0]), (const int32_t*)aux->ids->ptr + aux->off,
-                    cnt, e, vocab, 1.f, nullptr, 1, Device::get().flags(), stream()));
+                    cnt, e, vocab, aux->scale, aux->pe ? aux->pe->devc() : nullptr, aux->t,
+                    Device::get().flags(), stream()));
   };
   n.bwd = [aux, e, vocab](ExpressionGraph& g, Node& n) {
     const float* go = g.gradSrc(n);
     float* dst = accPtr(g, n.inputs[0], vocab * e);
-    scatterPlanAdd(g, aux->plan, dst, go, e, 1.f);
+    scatterPlanAdd(g, aux->plan, dst, go, e, aux->scale);
   };
   return addNode(std::move(n));
 }
@@ -1344,6 +1350,22 @@ NodeRef ExpressionGraph::scaleAddConst(NodeRef x, Real s, const Tensor& pe) {
   checkRef(x);
   if(x.shape.size() % pe.size() != 0)
     throw DimensionError("shapes not broadcastable: " + x.shape.str() + " vs " + pe.shape().str());
+  // x * s + pe on an embedding nobody has consumed yet: fold into the gather
+  // (one kernel forward, the scale into the scatter backward; same roundings:
+  // s * E[id] then + pe, and s * go per position before the scatter sum)
+  Node& xn = nodes_[(size_t)x.index];
+  if(xn.op == "embed" && x.index == (int)nodes_.size() - 1 && (size_t)x.index >= computed_ &&
+     xn.alias < 0 && x.shape.rank() == 3 && pe.shape().rank() == 2 &&
+     pe.shape()[0] == x.shape[1] && pe.shape()[1] == x.shape[2]) {
+    auto ea = std::static_pointer_cast<EmbedAux>(xn.aux);
+    if(ea->scale == 1.f && !ea->pe) {
+      ea->scale = s;
+      ea->pe = sharedConst(pe);
+      ea->t = x.shape[1];
+      xn.op = "embedPosenc";
+      return x;
+    }
+  }
   Node n;
   n.op = "posenc";
   n.shape = x.shape;
