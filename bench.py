@@ -117,11 +117,15 @@ class Clocks:
     def mark(self):
         self.t0 = time.monotonic()
 
-    def stop(self):
+    def stop(self, t_end=None):
+        """t_end: end of the timed region (monotonic); called after later work
+        so the sample straddling the end has arrived and the GPU never idles
+        between the timed and the e2e legs (an idle gap lets the clocks drop)."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        t1 = time.monotonic()
-        time.sleep(0.25)  # let the sample straddling the end arrive
+        t1 = t_end if t_end is not None else time.monotonic()
+        if t_end is None:
+            time.sleep(0.25)  # let the sample straddling the end arrive
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -262,6 +266,7 @@ def run_b200(a):
     e0 = M.event_record()
     marks = [e0]
     words = 0.0
+    u_timed = u  # the e2e leg replays these batches (same workload mix)
     th0 = time.perf_counter()
     th0_mono = time.monotonic()
     for _ in range(a.steps):
@@ -280,7 +285,7 @@ def run_b200(a):
         M.event_destroy(m)
     ms = M.event_elapsed_ms(e0, e1)
     launches = M.launch_count() - l0
-    clk = clocks.stop()
+    t_timed_end = time.monotonic()
     ms_max = all_max(ms, world)
     value = words / (ms_max / 1e3)
 
@@ -294,7 +299,7 @@ def run_b200(a):
     ewords = 0.0
     losses = []
     for k in range(e2e_steps):
-        grp = group(u)
+        grp = group(u_timed + k % a.steps)  # the timed region's batches, in order
         ewords += sum(b.target_tokens() for b in grp)
         r = stepper.update_pipelined(grp, u)
         if k > 0:
@@ -306,6 +311,7 @@ def run_b200(a):
     h2d = (M.h2d_bytes() - h0) / e2e_steps
     d2h = (M.d2h_bytes() - d0) / e2e_steps
     gc.enable()
+    clk = clocks.stop(t_timed_end)
 
     # ---- per-kernel-class device time (events around each C-ABI call)
     M.sync()
