@@ -255,7 +255,10 @@ def run_b200(a):
     # warm-up update is part of warm-up): no allocation inside timed steps
     n_meas = a.steps + e2e_steps
     big = max(range(u, u + n_meas), key=lambda k: sum(b.padded_slots() for b in group(k)))
-    stepper.update(group(big), u, True)
+    # (through the pipelined call, so its pinned loss slots and events exist
+    # before the e2e leg: their first-use allocation costs 5-30 ms)
+    stepper.update_pipelined(group(big), u)
+    stepper.flush_pipelined()
 
     # ---- value: device-timed, inputs uploaded per step, no host sync inside
     barrier(world)
@@ -302,6 +305,8 @@ def run_b200(a):
         grp = group(u_timed + k % a.steps)  # the timed region's batches, in order
         ewords += sum(b.target_tokens() for b in grp)
         r = stepper.update_pipelined(grp, u)
+        if os.environ.get("MTK_E2E_TRACE"):
+            print(f"[e2e] step {k} t={time.perf_counter() - t0:.4f}", file=sys.stderr)
         if k > 0:
             losses.append(r.loss)
         u += 1
