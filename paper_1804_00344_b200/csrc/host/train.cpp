@@ -307,6 +307,13 @@ SyncStepper::SyncStepper(const Model& model, ExpressionGraph& g, Adam& adam,
   if(opts.workers < 1)
     throw ContractError("training needs at least one worker");
   lossAcc_ = std::make_shared<DeviceBuffer>(64);
+  // pinned loss slots and their events for updatePipelined: allocated here,
+  // not on the first pipelined call (a pinned allocation costs milliseconds)
+  void* p = nullptr;
+  MTKC(mtkc_host_alloc_pinned(&p, 4 * sizeof(float)));
+  pinned_ = (float*)p;
+  MTKC(mtkc_event_create(&slotEvent_[0]));
+  MTKC(mtkc_event_create(&slotEvent_[1]));
 }
 
 const int* Adam::flagWord() { return adamFlag(); }
@@ -469,13 +476,6 @@ UpdateResult SyncStepper::collect(int slot) {
 UpdateResult SyncStepper::updatePipelined(const std::vector<const Batch*>& batches,
                                           int64_t updateIndex) {
   Device& d = Device::get();
-  if(!pinned_) {
-    void* p = nullptr;
-    MTKC(mtkc_host_alloc_pinned(&p, 4 * sizeof(float)));
-    pinned_ = (float*)p;
-    MTKC(mtkc_event_create(&slotEvent_[0]));
-    MTKC(mtkc_event_create(&slotEvent_[1]));
-  }
   UpdateResult launched = update(batches, updateIndex, false);
   const int slot = (int)(pipeCount_ & 1);
   MTKC(mtkc_memcpy_d2h(pinned_ + 2 * slot, lossAcc_->ptr, sizeof(float), d.stream()));
