@@ -235,6 +235,11 @@ int mtkc_colsum_group(float* const* outs, const float* const* ins, const int* ac
                       void* stream);
 /* flags |= MTKC_FLAG_NONFINITE if any in[i] is not finite (allFinite) */
 int mtkc_check_finite(const float* in, int64_t n, int* flags, void* stream);
+/* *dst |= *src on the device (stream-ordered): the step's device error bits
+ * join the optimizer's skip word, so a step the reference would have thrown
+ * in (graph.cpp:602-606, tensor.cpp:161-165, :424-425) never updates the
+ * parameters (train.cpp:49-59 runs only after a clean forward/backward) */
+int mtkc_flag_or(int* dst, const int* src, void* stream);
 
 /* ======================================================================== */
 /* softmax (softmaxInto tensor.cpp:393-440; graph softmax :526-555)          */

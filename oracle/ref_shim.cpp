@@ -17,6 +17,7 @@
 #include "mtk/serialize.h"
 #include "mtk/train.h"
 
+#include <cctype>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -597,3 +598,132 @@ int ref_op_gru(int64_t b, int64_t e, int64_t d, int ln, const float* h, const fl
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- op programs
+// A tiny stack program over the reference's ExpressionGraph op constructors
+// (graph.h:72-110), for op-level parity of the elementwise / broadcast /
+// reduce / layout rows (graph.cpp:139-524).  Tokens (whitespace separated):
+//   pK                  push parameter K (inputs[K], named "pK")
+//   dup                 push the top node again (self-operand cases)
+//   add sub mul div     binary, trailing-dim broadcast (graph.cpp:139-237)
+//   tanh sigmoid relu exp log neg        unary (graph.cpp:239-268)
+//   scale:S adds:S      scale / addScalar
+//   reshape:d0,d1,...   transpose:p0,p1,...
+//   concat:N:AXIS       slice:AXIS:START:LEN      gather:r0,r1,...
+//   reduce:OP:AXIS:KEEP (OP = sum|max|mean|argmax)   softmax
+// The top of the stack is the output; loss = sum(out * G).
+extern "C" int ref_op_program(const char* prog, int nin, const int* ranks, const int64_t* dims,
+                              const float* const* data, const float* G, float* out,
+                              int64_t out_cap, int64_t* out_dims, int* out_rank,
+                              float* const* grads) {
+  return guard([&] {
+    ExpressionGraph g(1);
+    std::vector<NodeRef> stack, params;
+    std::vector<std::string> names;
+    const int64_t* d = dims;
+    for(int i = 0; i < nin; ++i) {
+      Shape s = shapeOf(ranks[i], d);
+      d += ranks[i];
+      names.push_back("p" + std::to_string(i));
+      params.push_back(g.param(names.back(), s,
+                               inits::fromVector(std::vector<Real>(data[i], data[i] + s.size()))));
+    }
+    auto pop = [&] {
+      if(stack.empty())
+        throw ContractError("op program: stack underflow");
+      NodeRef r = stack.back();
+      stack.pop_back();
+      return r;
+    };
+    auto split = [](const std::string& s, char c) {
+      std::vector<std::string> out;
+      std::stringstream ss(s);
+      std::string tok;
+      while(std::getline(ss, tok, c))
+        out.push_back(tok);
+      return out;
+    };
+    std::stringstream ps(prog);
+    std::string tok;
+    while(ps >> tok) {
+      auto f = split(tok, ':');
+      const std::string& op = f[0];
+      if(op[0] == 'p' && op.size() > 1 && std::isdigit((unsigned char)op[1])) {
+        stack.push_back(params[(size_t)std::stoi(op.substr(1))]);
+      } else if(op == "dup") {
+        NodeRef t = pop();
+        stack.push_back(t);
+        stack.push_back(t);
+      } else if(op == "add" || op == "sub" || op == "mul" || op == "div") {
+        NodeRef b = pop(), a = pop();
+        stack.push_back(op == "add" ? g.add(a, b)
+                        : op == "sub" ? g.sub(a, b)
+                        : op == "mul" ? g.mul(a, b)
+                                      : g.div(a, b));
+      } else if(op == "tanh") {
+        stack.push_back(g.tanh(pop()));
+      } else if(op == "sigmoid") {
+        stack.push_back(g.sigmoid(pop()));
+      } else if(op == "relu") {
+        stack.push_back(g.relu(pop()));
+      } else if(op == "exp") {
+        stack.push_back(g.exp(pop()));
+      } else if(op == "log") {
+        stack.push_back(g.log(pop()));
+      } else if(op == "neg") {
+        stack.push_back(g.neg(pop()));
+      } else if(op == "scale") {
+        stack.push_back(g.scale(pop(), (Real)std::stod(f.at(1))));
+      } else if(op == "adds") {
+        stack.push_back(g.addScalar(pop(), (Real)std::stod(f.at(1))));
+      } else if(op == "reshape") {
+        std::vector<int64_t> s;
+        for(auto& x : split(f.at(1), ','))
+          s.push_back(std::stoll(x));
+        stack.push_back(g.reshape(pop(), Shape(s)));
+      } else if(op == "transpose") {
+        std::vector<int> p;
+        for(auto& x : split(f.at(1), ','))
+          p.push_back(std::stoi(x));
+        stack.push_back(g.transpose(pop(), p));
+      } else if(op == "concat") {
+        int n = std::stoi(f.at(1)), axis = std::stoi(f.at(2));
+        std::vector<NodeRef> parts((size_t)n);
+        for(int i = n - 1; i >= 0; --i)
+          parts[(size_t)i] = pop();
+        stack.push_back(g.concat(parts, axis));
+      } else if(op == "slice") {
+        stack.push_back(g.slice(pop(), std::stoi(f.at(1)), std::stoll(f.at(2)), std::stoll(f.at(3))));
+      } else if(op == "gather") {
+        std::vector<int64_t> rows;
+        for(auto& x : split(f.at(1), ','))
+          rows.push_back(std::stoll(x));
+        stack.push_back(g.gatherRows(pop(), rows));
+      } else if(op == "reduce") {
+        const std::string& r = f.at(1);
+        ReduceOp ro = r == "sum" ? ReduceOp::Sum
+                      : r == "max" ? ReduceOp::Max
+                      : r == "mean" ? ReduceOp::Mean
+                                    : ReduceOp::Argmax;
+        stack.push_back(g.reduce(ro, pop(), std::stoi(f.at(2)), std::stoi(f.at(3)) != 0));
+      } else if(op == "softmax") {
+        stack.push_back(g.softmax(pop()));
+      } else {
+        throw ContractError("op program: unknown token " + tok);
+      }
+    }
+    NodeRef o = pop();
+    if(o.shape.size() > out_cap)
+      throw ContractError("op program: output buffer too small");
+    *out_rank = (int)o.shape.rank();
+    for(int i = 0; i < o.shape.rank(); ++i)
+      out_dims[i] = o.shape[i];
+    NodeRef loss = seededLoss(g, o, G);
+    g.forward();
+    g.zeroGrads();
+    g.backward(loss);
+    copyOut(o.val(), out);
+    for(int i = 0; i < nin; ++i)
+      copyOut(g.paramGrad(names[(size_t)i]), grads[i]);
+  });
+}

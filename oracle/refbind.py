@@ -84,6 +84,8 @@ def lib():
             "ref_op_embed": (I, [I64, I64, fp, I64, I64, ip, fp, fp, fp]),
             "ref_op_gru": (I, [I64, I64, I64, I, fp, fp, fp, fp, fp, fp, fp, fp]),
             "ref_op_mha": (I, [I64, I64, I64, I64, I, fp, fp, fp, fp, I, fp, fp, fp, fp, fp]),
+            "ref_op_program": (I, [C.c_char_p, I, ip, lp, C.POINTER(fp), fp, fp, I64, lp,
+                                   C.POINTER(C.c_int), C.POINTER(fp)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -404,3 +406,21 @@ def op_gru(h, x, packed_w, ln, G, e, d):
     _check(lib().ref_op_gru(b, e, d, int(ln), _f(h), _f(xx), _f(packed_w), _f(G), _f(out),
                             _f(gh), _f(gx), _f(gw)))
     return out, gh, (gx if e > 0 else None), gw
+
+
+def op_program(prog: str, inputs, G):
+    """Run a stack program of reference graph ops (ref_shim.cpp ref_op_program)
+    on parameters `inputs` with loss = sum(out * G).  Returns (out, [grads])."""
+    ins = [f32(a) for a in inputs]
+    ranks = np.asarray([a.ndim for a in ins], np.int32)
+    dims = np.asarray([d for a in ins for d in a.shape] or [0], np.int64)
+    ptrs = (C.POINTER(C.c_float) * max(len(ins), 1))(*[_f(a) for a in ins])
+    grads = [np.zeros_like(a) for a in ins]
+    gptrs = (C.POINTER(C.c_float) * max(len(ins), 1))(*[_f(a) for a in grads])
+    Gf = f32(G).ravel()
+    out = np.zeros(Gf.size, np.float32)
+    odims = np.zeros(4, np.int64)
+    orank = C.c_int()
+    _check(lib().ref_op_program(prog.encode(), len(ins), _i(ranks), _l(dims), ptrs, _f(Gf),
+                                _f(out), out.size, _l(odims), C.byref(orank), gptrs))
+    return out.reshape(tuple(int(x) for x in odims[:orank.value])), grads

@@ -477,6 +477,7 @@ NodeRef ExpressionGraph::binary(const std::string& name, EwiseOp op, NodeRef a, 
     pad4(sa, ad);
     pad4(sb, bd);
     bool aliased = false;
+    int aliasedNode = -1;  // resolved operand that took over n.grad in this sweep
     for(int which = 0; which < 2; ++which) {
       const Shape& st = which == 0 ? sa : sb;
       int idx = n.inputs[(size_t)which];
@@ -494,11 +495,18 @@ NodeRef ExpressionGraph::binary(const std::string& name, EwiseOp op, NodeRef a, 
           in.grad = n.grad;
           in.gradLive = true;
           aliased = true;
+          aliasedNode = g.resolve(idx);
           continue;
         }
         auto d = g.gradDst(idx);
-        if(d.ptr == go)
-          continue;  // already sharing (an earlier sweep aliased it)
+        if(d.ptr == go) {
+          // add(h, h) / add(h, reshape(h)): operand 0 took over this buffer
+          // just now, so operand 1's contribution doubles it in place;
+          // otherwise an earlier sweep aliased it and it already holds go
+          if(g.resolve(idx) == aliasedNode)
+            MTKC(mtkc_axpy(d.ptr, go, 1.f, st.size(), stream()));
+          continue;
+        }
         if(d.accumulate)
           MTKC(mtkc_axpy(d.ptr, go, 1.f, st.size(), stream()));
         else

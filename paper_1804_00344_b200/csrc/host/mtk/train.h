@@ -41,10 +41,13 @@ public:
   // synchronisation inside the step).
   void updateAsync(ExpressionGraph& g, Real lr, AveragedParameters* avg = nullptr);
   void checkDeferred();
-  // the oldest `steps` unchecked updates were verified finite on the device
-  // (pipelined loss read): they no longer count toward a rollback
-  void markVerified(int64_t steps) { pendingSteps_ = std::max<int64_t>(0, pendingSteps_ - steps); }
-  // device word holding the non-finite flag of the pending updates
+  // every update up to and including optimizer step `step` was verified
+  // error-free on the device (pipelined loss read): none of them counts
+  // toward a rollback any more
+  void markVerified(int64_t step) { verifiedStep_ = std::max(verifiedStep_, step); }
+  // device word of the pending updates: MTKC_FLAG_NONFINITE for a non-finite
+  // gradient, plus the device error bits of the step (bad ids, fully-masked
+  // rows, division by zero) -- any bit makes the update a no-op
   static const int* flagWord();
   // Single-tensor variant (train.cpp:30-47) with its own moments per name.
   void updateTensor(const std::string& name, Tensor& value, const Tensor& grad, Real lr,
@@ -52,7 +55,7 @@ public:
 
   int64_t step() const { return step_; }
   const AdamConfig& config() const { return cfg_; }
-  void setStep(int64_t s) { step_ = s; }
+  void setStep(int64_t s) { step_ = verifiedStep_ = s; }
   // moment views for checkpointing (names in graph order)
   Tensor firstMoment(ExpressionGraph& g, const std::string& name);
   Tensor secondMoment(ExpressionGraph& g, const std::string& name);
@@ -69,7 +72,7 @@ private:
   int64_t n_ = 0;
   bool haveMoments_ = false;
   bool pending_ = false;
-  int64_t pendingSteps_ = 0;
+  int64_t verifiedStep_ = 0;  // last optimizer step known to have been applied
   ExpressionGraph* lastGraph_ = nullptr;
   std::map<std::string, std::pair<Tensor, Tensor>> single_;  // updateTensor moments
 };
@@ -178,6 +181,7 @@ private:
   float* pinned_ = nullptr;
   void* slotEvent_[2] = {nullptr, nullptr};
   double slotTokens_[2] = {0, 0};
+  int64_t slotStep_[2] = {0, 0};     // optimizer step each slot's update launched
   int64_t pipeCount_ = 0;
   UpdateResult collect(int slot);
 

@@ -74,6 +74,10 @@ void Adam::launch(ExpressionGraph& g, Real lr, AveragedParameters* avg) {
   if(!pending_)
     MTKC(mtkc_memset(adamFlag(), 0, sizeof(int), d.stream()));
   float* grads = g.pool().grads()->ptr;
+  // a step whose forward/backward raised a device error (bad token id,
+  // fully-masked softmax row, division by zero) must not train the model:
+  // the reference throws before any update (graph.cpp:602-606)
+  MTKC(mtkc_flag_or(adamFlag(), d.flags(), d.stream()));
   MTKC(mtkc_check_finite(grads, n, adamFlag(), d.stream()));
   int64_t step = step_ + 1;
   Real corr1 = Real(1) - (Real)std::pow((double)cfg_.beta1, (double)step);  // train.cpp:37-38
@@ -82,9 +86,10 @@ void Adam::launch(ExpressionGraph& g, Real lr, AveragedParameters* avg) {
   MTKC(mtkc_adam_ema(g.pool().values()->ptr, grads, m_->ptr, v_->ptr, avgPtr, n, lr, cfg_.beta1,
                      cfg_.beta2, cfg_.eps, corr1, corr2, avg ? avg->beta() : 0.f, avg ? 1 : 0,
                      /*zero_grad=*/0, adamFlag(), d.stream()));
+  if(!pending_)
+    verifiedStep_ = step_;
   step_ = step;
   pending_ = true;
-  ++pendingSteps_;
   lastGraph_ = &g;
   g.zeroGrads();  // consumed by the update (train.cpp:57); lazily zero, memory kept
 }
@@ -93,15 +98,20 @@ void Adam::checkDeferred() {
   if(!pending_)
     return;
   pending_ = false;
-  int64_t steps = pendingSteps_;
-  pendingSteps_ = 0;
   Device& d = Device::get();
   int flag = 0;
   MTKC(mtkc_memcpy_d2h(&flag, adamFlag(), sizeof(int), d.stream()));
   d.sync();
-  if(!(flag & MTKC_FLAG_NONFINITE))
+  if(!flag) {
+    verifiedStep_ = step_;
     return;
-  step_ -= steps;  // the device skipped the update(s): parameters unchanged
+  }
+  // the flag is sticky while updates are unchecked: every update after the
+  // last verified one was skipped on the device (parameters unchanged)
+  step_ = verifiedStep_;
+  d.checkFlags("training step");  // device errors of the step: their own exception types
+  if(!(flag & MTKC_FLAG_NONFINITE))
+    throw NumericError("training step rejected by a device error; update aborted");
   ExpressionGraph& g = *lastGraph_;
   std::vector<float> host((size_t)g.pool().used());
   MTKC(mtkc_memcpy_d2h(host.data(), g.pool().grads()->ptr, host.size() * sizeof(float),
@@ -465,10 +475,11 @@ UpdateResult SyncStepper::collect(int slot) {
   r.tokens = slotTokens_[slot];
   MTKC(mtkc_event_sync(slotEvent_[slot]));
   const int flag = reinterpret_cast<const int*>(pinned_)[2 * slot + 1];
-  if(flag & MTKC_FLAG_NONFINITE) {
+  if(flag) {
+    pipeCount_ = 0;  // the pipeline restarts after the error
     adam_.checkDeferred();  // synchronises, rolls back the skipped updates, throws
   }
-  adam_.markVerified(1);
+  adam_.markVerified(slotStep_[slot]);
   r.loss = pinned_[2 * slot];
   return r;
 }
@@ -482,6 +493,7 @@ UpdateResult SyncStepper::updatePipelined(const std::vector<const Batch*>& batch
   MTKC(mtkc_memcpy_d2h(pinned_ + 2 * slot + 1, Adam::flagWord(), sizeof(int), d.stream()));
   MTKC(mtkc_event_record(slotEvent_[slot], d.stream()));
   slotTokens_[slot] = launched.tokens;
+  slotStep_[slot] = adam_.step();
   ++pipeCount_;
   if(pipeCount_ == 1) {
     UpdateResult r;

@@ -191,6 +191,12 @@ __global__ void finite_kernel(const float* in, int64_t n, int* flags) {
     atomicOr(flags, MTKC_FLAG_NONFINITE);
 }
 
+__global__ void flag_or_kernel(int* dst, const int* src) {
+  MTKC_PDL_ENTRY();
+  if(threadIdx.x == 0 && *src)
+    atomicOr(dst, *src);
+}
+
 __global__ void finite4_kernel(const float4* in, int64_t n4, int* flags) {
   MTKC_PDL_ENTRY();
   bool bad = false;
@@ -294,6 +300,12 @@ int mtkc_colsum_group(float* const* outs, const float* const* ins, const int* ac
   ::mtkc::launch(colsum_onepass_kernel, dim3((unsigned)slabs, (unsigned)nblk, (unsigned)n), 256, 0,
                  S(stream), grp, workspace, rows, cols);
   MTKC_POST_LAUNCH("colsum_onepass_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_flag_or(int* dst, const int* src, void* stream) {
+  ::mtkc::launch(flag_or_kernel, 1, 32, 0, S(stream), dst, src);
+  MTKC_POST_LAUNCH("flag_or_kernel");
   return MTKC_OK;
 }
 

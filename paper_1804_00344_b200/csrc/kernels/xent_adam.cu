@@ -229,8 +229,8 @@ __global__ void adam_ema_kernel(float* th, float* g, float* m, float* v, float* 
                                 float lr, float b1, float b2, float eps, float c1, float c2,
                                 float ab, int doAvg, int zg, const int* flags) {
   MTKC_PDL_ENTRY();
-  if(flags && (*flags & MTKC_FLAG_NONFINITE))
-    return;  // all-or-nothing (train.cpp:51-53)
+  if(flags && *flags)
+    return;  // all-or-nothing (train.cpp:51-53); also skipped after a device error
   int64_t n4 = n / 4;
   float4* th4 = (float4*)th;
   float4* g4 = (float4*)g;

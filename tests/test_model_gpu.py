@@ -6,14 +6,15 @@ tokens): same batching, same seeded initial parameters (bit-exact), then
 loss, every parameter gradient and the parameters after one Adam+EMA update
 are compared with oracle/_ref.
 
-Stated tolerances:
-  FP32 GEMMs (reference arithmetic):  loss rel <= 1e-5; per-tensor gradient
-      ||d||_2 <= 1e-3 ||g_ref||_2 + 1e-6 ||G_ref||_2 (G = all gradients; the
-      floor covers tensors whose exact gradient is 0, e.g. attention key biases);
-      parameters after Adam: |d| <= 1e-3 * lr for >= 99.9 % of elements and
-      <= 2 lr everywhere (step 1 moves every element by ~lr*sign(g), so
-      elements whose |g| is near eps = 1e-9 flip with tiny gradient noise).
-  TF32 tensor cores:  loss rel <= 2e-3; gradients ||d|| <= 5e-2 ||g|| + 1e-3 ||G||.
+Stated tolerances (tests/parity_util.py):
+  loss rel <= 1e-5 (FP32 GEMMs, reference arithmetic) / 2e-3 (TF32 tensor
+  cores); per-tensor gradient ||d||_2 <= 1e-4 ||g_ref||_2 (FP32) / 1e-2
+  ||g_ref||_2 (TF32), with an absolute floor only for exactly-zero gradients
+  (attention key biases); parameters after Adam: FP32 |d| <= 1e-3 * lr for
+  >= 99.9 % of elements and <= 2 lr everywhere (step 1 moves every element by
+  ~lr*sign(g), so elements whose |g| is near eps = 1e-9 flip with tiny
+  gradient noise); TF32 step-sign agreement >= 99 % where |g| is not
+  negligible.
 """
 import numpy as np
 import pytest
@@ -21,6 +22,7 @@ import pytest
 from oracle import refbind as R
 from oracle import restate as S
 from paper_1804_00344_b200 import CONFIGS, config_text, mtk as M, synth
+from parity_util import check_adam_fp32, check_adam_sign, check_grads
 
 pytestmark = pytest.mark.gpu
 
@@ -69,29 +71,19 @@ def test_tiny_transformer_step_parity(cuda, ref_state, prec):
     assert list(g.param_names()) == names  # creation order == Adam/MTK1 order
     assert batch.target_tokens() == ref_state["tokens"] == 1619
     rel_loss = abs(loss - ref_state["loss"]) / abs(ref_state["loss"])
-    G = np.sqrt(sum(np.sum(ref_state["grads"][n].astype(np.float64) ** 2) for n in names))
-    tol, floor, ltol = (1e-3, 1e-6, 1e-5) if prec == "fp32" else (5e-2, 1e-3, 2e-3)
-    assert rel_loss <= ltol, rel_loss
-    worst = 0.0
-    for n in names:
-        a, b = g.param_grad(n).astype(np.float64), ref_state["grads"][n].astype(np.float64)
-        d = np.linalg.norm(a - b)
-        assert d <= tol * np.linalg.norm(b) + floor * G, (n, d, np.linalg.norm(b))
-        worst = max(worst, d / (np.linalg.norm(b) + floor * G))
+    assert rel_loss <= (1e-5 if prec == "fp32" else 2e-3), rel_loss
+    check_grads(names, {n: g.param_grad(n) for n in names}, ref_state["grads"], prec, "tiny")
     # one Adam + EMA update (train.cpp:270-272) on the same gradients
     adam = M.Adam(M.adam_defaults_for(CFG))
     avg = M.AveragedParameters(0.9999)
     adam.update(g, ref_state["lr"], avg)
+    after = {n: g.param_value(n) for n in names}
     if prec == "fp32":
-        bad = 0
-        total = 0
+        check_adam_fp32(names, after, ref_state["after"], ref_state["lr"])
         for n in names:
-            d = np.abs(g.param_value(n) - ref_state["after"][n])
-            bad += int(np.sum(d > 1e-3 * ref_state["lr"]))
-            total += d.size
-            assert np.allclose(avg.value(g, n), ref_state["avg"][n], rtol=0, atol=1e-6)
-            assert np.all(d <= 2.0 * ref_state["lr"]), n
-        assert bad <= 1e-3 * total, (bad, total)
+            assert np.allclose(avg.value(g, n), ref_state["avg"][n], rtol=0, atol=1e-6), n
+    else:
+        check_adam_sign(names, ref_state["init"], after, ref_state["after"], ref_state["grads"])
 
 
 def test_init_bitexact(cuda, ref_state):
@@ -189,11 +181,8 @@ def test_rnn_step_parity(cuda, arch, ln):
     l = float(loss.val()[0])
     assert abs(l - rl) <= 1e-5 * abs(rl), (l, rl)
     names = ref.param_names()
-    grads = {n: ref.grad(n).astype(np.float64) for n in names}
-    G = np.sqrt(sum(np.sum(v ** 2) for v in grads.values()))
-    for n in names:
-        dlt = np.linalg.norm(g.param_grad(n) - grads[n])
-        assert dlt <= 1e-3 * np.linalg.norm(grads[n]) + 1e-6 * G, (n, dlt, np.linalg.norm(grads[n]))
+    check_grads(names, {n: g.param_grad(n) for n in names}, {n: ref.grad(n) for n in names},
+                "fp32", f"{arch}{'-ln' if ln else ''}-toy")
     M.set_precision("tf32")
 
 
