@@ -176,6 +176,11 @@ int mtkc_gemm(const mtkc_gemm_args* args, void* stream);
 int mtkc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, void* stream);
 /* which path the last mtkc_gemm on this thread used: 0 simt, 1 tcgen05 */
 int mtkc_gemm_last_path(void);
+/* Cap the persistent tensor-core GEMM grid at `sms` CTAs (0 = every SM).
+ * The data-parallel stepper leaves SMs to NCCL while overlapped gradient
+ * buckets are in flight (a persistent GEMM holding all 148 SMs would queue
+ * the all-reduce kernels behind it); host-side state, not stream-ordered. */
+int mtkc_gemm_set_sm_limit(int sms);
 
 /* ======================================================================== */
 /* elementwise / broadcast (tensor.cpp:111-237, graph.cpp:139-268)          */
@@ -496,6 +501,8 @@ int mtkc_ema(float* avg, const float* theta, int64_t n, float beta, void* stream
 int mtkc_nccl_unique_id(void* id_out_128);
 int mtkc_nccl_comm_init(void** comm, int nranks, int rank, const void* id_128);
 int mtkc_nccl_comm_destroy(void* comm);
+/* number of ranks in the communicator (ncclCommCount) */
+int mtkc_nccl_comm_count(void* comm, int* count);
 int mtkc_allreduce_sum(void* comm, float* buf, int64_t n, void* stream);
 
 #ifdef __cplusplus

@@ -423,4 +423,5 @@ def op_program(prog: str, inputs, G):
     orank = C.c_int()
     _check(lib().ref_op_program(prog.encode(), len(ins), _i(ranks), _l(dims), ptrs, _f(Gf),
                                 _f(out), out.size, _l(odims), C.byref(orank), gptrs))
-    return out.reshape(tuple(int(x) for x in odims[:orank.value])), grads
+    shape = tuple(int(x) for x in odims[:orank.value])
+    return out[:int(np.prod(shape))].reshape(shape), grads

@@ -31,21 +31,4 @@ def native_libraries():
     return [os.path.join(_HERE, n) for n in ("libmtkcuda.so", "libmtkhost.so")]
 
 
-def config_text(arch="transformer", vocab=32000, emb=512, state=1024, heads=8, layers=6,
-                dropout=0.0, tying="all", layer_norm=False, post_norm=False):
-    """ModelConfig text (models.cpp:12-30 key order)."""
-    return (f"architecture: {arch}\nsource-vocab: {vocab}\ntarget-vocab: {vocab}\n"
-            f"emb-dim: {emb}\nstate-dim: {state}\nheads: {heads}\nlayers: {layers}\n"
-            f"dropout: {dropout}\ntying: {tying}\nlayer-norm: {int(layer_norm)}\n"
-            f"post-norm: {int(post_norm)}\n")
-
-
-# The five BASELINE.json configurations (SURVEY.md section 8(d)).
-CONFIGS = {
-    "tiny": dict(arch="transformer", vocab=8000, emb=256, heads=4, layers=2),
-    "shallow": dict(arch="s2s-shallow", vocab=50000, emb=512, state=1024),
-    "deep": dict(arch="s2s-deep", vocab=50000, emb=512, state=1024, layer_norm=True),
-    "base": dict(arch="transformer", vocab=32000, emb=512, heads=8, layers=6),
-    "big": dict(arch="transformer", vocab=32000, emb=1024, heads=16, layers=6),
-}
-TOKEN_BUDGET = {"tiny": 64 * 66, "shallow": 4096, "deep": 4096, "base": 16384, "big": 32768}
+from .configs import CONFIGS, TOKEN_BUDGET, algorithmic_flops, config_text  # noqa: E402,F401

@@ -106,11 +106,14 @@ struct DistContext {
   int rank = 0;
   int world = 1;
   void* comm = nullptr;  // ncclComm_t
+  int ncclSms = 0;       // SMs the GEMMs leave to NCCL while buckets overlap the backward
 };
 // world == 1 with forceComm creates a one-rank NCCL communicator, so the
 // exchange path (buckets, streams, events) runs on a single GPU too.
 void setDistributed(int rank, int world, const void* ncclId128, bool forceComm = false);
 DistContext& distContext();
+// ranks in the NCCL communicator (1 without one)
+int commRanks();
 
 struct TrainOptions {
   int workers = 1;
@@ -191,6 +194,19 @@ public:
 };
 
 uint64_t mixSeed(uint64_t seed, int64_t update, int worker);
+
+// The workers one rank runs in a synchronous update (train.cpp:221-269):
+// worker i handles batches[i]; with L = workers / world, rank r runs workers
+// r*L .. r*L+L-1 that have a batch (ranks past the epoch tail run none and
+// contribute zero gradients), each weighted tokens_i / total -- the weights
+// of all ranks sum to 1, so the NCCL sum of the pre-scaled gradients is the
+// reference's combine.  Pure host logic: identical on every rank.
+struct WorkerShare {
+  int worker;
+  Real weight;
+};
+std::vector<WorkerShare> rankShare(const std::vector<double>& tokens, int workers, int world,
+                                   int rank);
 
 // Checkpoints (train.cpp:121-164): parameters, then "adam.m.<name>",
 // "adam.v.<name>" and "avg.<name>" in name order once they exist, then

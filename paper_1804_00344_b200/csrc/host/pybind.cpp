@@ -154,6 +154,16 @@ PYBIND11_MODULE(_mtk, m) {
     MTKC(mtkc_nccl_unique_id(id));
     return py::bytes(id, 128);
   });
+  m.def("comm_ranks", [] { return commRanks(); });
+  m.def(
+      "rank_share",
+      [](const std::vector<double>& tokens, int workers, int world, int rank) {
+        std::vector<std::pair<int, float>> out;
+        for(auto& s : rankShare(tokens, workers, world, rank))
+          out.emplace_back(s.worker, s.weight);
+        return out;
+      },
+      py::arg("tokens"), py::arg("workers"), py::arg("world"), py::arg("rank"));
   m.def(
       "set_distributed",
       [](int rank, int world, py::bytes id, bool forceComm) {

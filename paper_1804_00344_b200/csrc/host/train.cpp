@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <ostream>
 
@@ -231,8 +232,27 @@ void setDistributed(int rank, int world, const void* ncclId128, bool forceComm) 
   }
   g_dist.rank = rank;
   g_dist.world = world;
+  if(world > 1) {
+    // SMs left to NCCL while buckets overlap the backward: NCCL's channels
+    // are capped to match (defaults only; the user's NCCL_* settings win)
+    const char* e = std::getenv("MTK_NCCL_SMS");
+    g_dist.ncclSms = e ? std::max(0, std::atoi(e)) : 8;
+    if(g_dist.ncclSms > 0) {
+      std::string n = std::to_string(g_dist.ncclSms);
+      setenv("NCCL_MAX_NCHANNELS", n.c_str(), 0);
+      setenv("NCCL_MAX_CTAS", n.c_str(), 0);
+    }
+  }
   if(world > 1 || forceComm)
     MTKC(mtkc_nccl_comm_init(&g_dist.comm, world, rank, ncclId128));
+}
+
+int commRanks() {
+  if(!g_dist.comm)
+    return 1;
+  int n = 0;
+  MTKC(mtkc_nccl_comm_count(g_dist.comm, &n));
+  return n;
 }
 
 // ---------------------------------------------------------- checkpoints
@@ -342,22 +362,41 @@ SyncStepper::~SyncStepper() {
     mtkc_stream_destroy(commStream_);
 }
 
+std::vector<WorkerShare> rankShare(const std::vector<double>& tokens, int workers, int world,
+                                   int rank) {
+  if(world < 1 || rank < 0 || rank >= world)
+    throw ContractError("rank outside the communicator");
+  if(workers % world != 0)
+    throw ContractError("workers must be a multiple of the number of ranks");
+  const int take = (int)tokens.size();
+  if(take < 1 || take > workers)
+    throw ContractError("an update takes between 1 and `workers` batches");
+  double total = 0;
+  for(double t : tokens)
+    total += t;
+  const int L = workers / world;
+  std::vector<WorkerShare> out;
+  for(int j = 0; j < L; ++j) {
+    int i = rank * L + j;
+    if(i >= take)
+      break;
+    out.push_back({i, (Real)tokens[(size_t)i] / (Real)total});  // train.cpp:262-266
+  }
+  return out;
+}
+
 UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64_t updateIndex,
                                  bool readLoss) {
   DistContext& dc = distContext();
   int W = opts_.workers;
-  if(W % dc.world != 0)
-    throw ContractError("workers must be a multiple of the number of ranks");
-  int L = W / dc.world;
   int take = (int)batches.size();
-  if(take < 1 || take > W)
-    throw ContractError("an update takes between 1 and `workers` batches");
   std::vector<double> tokens((size_t)take);
   double total = 0;
   for(int i = 0; i < take; ++i) {
     tokens[(size_t)i] = (double)batches[(size_t)i]->targetTokenCount();
     total += tokens[(size_t)i];
   }
+  const std::vector<WorkerShare> share = rankShare(tokens, W, dc.world, dc.rank);
   Device& d = Device::get();
   MTKC(mtkc_memset(lossAcc_->ptr, 0, sizeof(float), d.stream()));
   g_.zeroGrads();
@@ -368,18 +407,13 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
     MTKC(mtkc_event_create(&commDone_));
   }
   // the rank's last local worker (its backward finalises the gradients)
-  int lastLocal = -1;
-  for(int j = 0; j < L; ++j)
-    if(dc.rank * L + j < take)
-      lastLocal = j;
+  const int lastLocal = (int)share.size() - 1;
   bool issuedAll = false;
-  for(int j = 0; j < L; ++j) {
-    int i = dc.rank * L + j;
-    if(i >= take)
-      break;
+  for(int j = 0; j < (int)share.size(); ++j) {
+    const int i = share[(size_t)j].worker;
     g_.clear();
     g_.setSeed(mixSeed(opts_.seed, updateIndex, i));
-    Real w = (Real)tokens[(size_t)i] / (Real)total;  // train.cpp:262-266
+    const Real w = share[(size_t)j].weight;
     g_.setLossScale(w);
     auto t0 = std::chrono::steady_clock::now();
     NodeRef loss = model_.buildLoss(g_, *batches[(size_t)i]);
@@ -416,12 +450,26 @@ UpdateResult SyncStepper::update(const std::vector<const Batch*>& batches, int64
         MTKC(mtkc_allreduce_sum(dc.comm, grads + b.begin, b.end - b.begin, commStream_));
         ++bucketsIssued_;
       };
+      // from the first bucket on, the persistent GEMMs leave SMs to NCCL
+      const bool capSms = dc.world > 1 && dc.ncclSms > 0;
+      bool capped = false;
+      auto issueCapped = [&](size_t k) {
+        if(capSms && !capped) {
+          int sms = 0;
+          MTKC(mtkc_sm_count(&sms));
+          MTKC(mtkc_gemm_set_sm_limit(std::max(1, sms - dc.ncclSms)));
+          capped = true;
+        }
+        issue(k);
+      };
       g_.backward(loss, [&](int node) {
         while(next < buckets.size() && buckets[next].readyAfter >= node)
-          issue(next++);
+          issueCapped(next++);
       });
       while(next < buckets.size())
-        issue(next++);
+        issueCapped(next++);
+      if(capped)
+        MTKC(mtkc_gemm_set_sm_limit(0));
       issuedAll = true;
     } else {
       g_.backward(loss);

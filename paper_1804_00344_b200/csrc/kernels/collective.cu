@@ -27,6 +27,7 @@ struct Nccl {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
   bool ok = false;
   std::string err;
 };
@@ -46,7 +47,9 @@ Nccl& nccl() {
     n.commDestroy = (decltype(n.commDestroy))dlsym(h, "ncclCommDestroy");
     n.allReduce = (decltype(n.allReduce))dlsym(h, "ncclAllReduce");
     n.errorString = (decltype(n.errorString))dlsym(h, "ncclGetErrorString");
-    n.ok = n.getUniqueId && n.commInitRank && n.commDestroy && n.allReduce && n.errorString;
+    n.commCount = (decltype(n.commCount))dlsym(h, "ncclCommCount");
+    n.ok = n.getUniqueId && n.commInitRank && n.commDestroy && n.allReduce && n.errorString &&
+           n.commCount;
     if(!n.ok)
       n.err = "NCCL library lacks required symbols";
   });
@@ -95,6 +98,11 @@ int mtkc_nccl_comm_init(void** comm, int nranks, int rank, const void* id_128) {
 int mtkc_nccl_comm_destroy(void* comm) {
   NCCL_READY();
   return nccl_status(nccl().commDestroy((ncclComm_t)comm), "ncclCommDestroy");
+}
+
+int mtkc_nccl_comm_count(void* comm, int* count) {
+  NCCL_READY();
+  return nccl_status(nccl().commCount((ncclComm_t)comm, count), "ncclCommCount");
 }
 
 int mtkc_allreduce_sum(void* comm, float* buf, int64_t n, void* stream) {

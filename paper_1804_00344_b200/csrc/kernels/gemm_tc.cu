@@ -1013,6 +1013,8 @@ bool make_store_map(CUtensorMap* m, float* base, int64_t cols, int64_t rows, int
 }
 
 int g_sms = 0;
+int g_sm_limit = 0;  // 0 = every SM; else the persistent grid's cap (SMs left to NCCL)
+inline int gemm_sms() { return g_sm_limit > 0 && g_sm_limit < g_sms ? g_sm_limit : g_sms; }
 
 template <int BN, bool A_MN, bool B_MN, bool LOADS>
 int launch_tc(const TcMaps& maps, const TcP& p, cudaStream_t st) {
@@ -1026,7 +1028,7 @@ int launch_tc(const TcMaps& maps, const TcP& p, cudaStream_t st) {
       return cuda_status(e, "gemm_tf32_tc smem attribute");
     attr = true;
   }
-  int grid = std::min(p.numTiles, g_sms);
+  int grid = std::min(p.numTiles, gemm_sms());
   ::mtkc::launch(kern, grid, TC_THREADS, smem, st, maps, p);
   MTKC_POST_LAUNCH("gemm_tf32_tc_kernel");
   return MTKC_OK;
@@ -1092,6 +1094,7 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     if(g_sms <= 0)
       g_sms = 148;
   }
+  const int sms = gemm_sms();
   const int nOut = kconcat ? 1 : nprob;
   const int64_t mt = cdiv(a.M, BM);
   // wide tiles halve the re-reads of A (the L2->SM operand traffic that
@@ -1114,15 +1117,15 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   // keep >= 24 per split.
   int splits = 1;
   const int64_t tiles = mt * nt * nOut;
-  const int minKb = tiles * 4 <= g_sms ? 4 : 24;
+  const int minKb = tiles * 4 <= sms ? 4 : 24;
   if(a.workspace && numKb >= 2 * minKb && !a.relu_mask_out) {  // masks: no split
-    double best = (double)tiles / (double)(g_sms * cdiv(tiles, g_sms));
+    double best = (double)tiles / (double)(sms * cdiv(tiles, sms));
     for(int s = 2; s <= 16 && numKb / s >= minKb; ++s) {
       size_t need = (size_t)s * nOut * ((size_t)a.M * (size_t)a.N + (csOp ? csLen * csTiles : 0)) *
                     sizeof(float);
       if(need > a.workspace_bytes)
         break;
-      double eff = (double)(tiles * s) / (double)(g_sms * cdiv(tiles * s, g_sms));
+      double eff = (double)(tiles * s) / (double)(sms * cdiv(tiles * s, sms));
       // partial sums cost an extra write+read of M*N per split: demand a real gain
       if(eff > best * 1.08) {
         best = eff;
@@ -1303,3 +1306,12 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc, bool* csFused) {
 }
 
 }  // namespace mtkc
+
+namespace mtkc {
+void gemm_set_sm_limit(int sms) { g_sm_limit = sms > 0 ? sms : 0; }
+}  // namespace mtkc
+
+extern "C" int mtkc_gemm_set_sm_limit(int sms) {
+  mtkc::gemm_set_sm_limit(sms);
+  return MTKC_OK;
+}

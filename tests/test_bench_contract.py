@@ -28,6 +28,9 @@ def test_reference_arm_contract():
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+    assert d["workers_1"]["value"] > 0 and d["workers_1"]["cores"] == 1
+    # the reference arm runs the reference alone: no product library mapped
+    assert d["native_so_mapped"] == ["oracle/_ref/libmtkref.so"], d["native_so_mapped"]
 
 
 @pytest.mark.gpu
