@@ -18,7 +18,11 @@ tensor, with
 Key-projection biases (`*.kB`) have an exactly-zero gradient (softmax is
 invariant to a per-row shift, so sum_j dK_j = 0): their computed values are
 rounding residues of column sums of dK, so their bound is scaled by the
-companion weight gradient ||g_ref(kW)|| instead of their own norm.
+companion weight gradient ||g_ref(kW)|| instead of their own norm.  Tensors
+whose reference gradient is numerically zero (||g_ref|| <= 1e-6 ||G||, e.g.
+the Bahdanau query projection `att*.W` at initialisation, whose gradient
+sum_j de_tj * (v o tanh'_tj) cancels to ~1e-10 ||G|| because sum_j de_tj = 0
+and tanh is nearly linear there) are held to ||d|| <= tol * 1e-6 ||G||.
 """
 from __future__ import annotations
 
@@ -28,14 +32,18 @@ import os
 import numpy as np
 
 GRAD_TOL = {"fp32": 1e-3, "tf32": 3e-2}
+ZERO_REL = 1e-6
 
 
-def _scale(n, ref):
+def _scale(n, ref, G):
     if n.endswith(".kB"):
         w = n[:-2] + "kW"
         if w in ref:
             return float(np.linalg.norm(np.asarray(ref[w], np.float64))), True
-    return float(np.linalg.norm(np.asarray(ref[n], np.float64))), False
+    nb = float(np.linalg.norm(np.asarray(ref[n], np.float64)))
+    if nb <= ZERO_REL * G:
+        return ZERO_REL * G, True
+    return nb, False
 
 
 def grad_ratios(names, mine, ref):
@@ -46,7 +54,7 @@ def grad_ratios(names, mine, ref):
         a = np.asarray(mine[n], np.float64)
         b = np.asarray(ref[n], np.float64)
         d = float(np.linalg.norm(a - b))
-        scale, zero = _scale(n, ref)
+        scale, zero = _scale(n, ref, G)
         out.append((n, d, float(np.linalg.norm(b)),
                     d / scale if scale > 0 else (0.0 if d == 0 else np.inf), zero))
     return out, G
