@@ -408,6 +408,14 @@ typedef struct mtkc_gru_args {
   float* dac;
   float* dax;          /* may alias dac when there is no LN */
   float* lnparts;      /* [b x 6d] (LN only) */
+  /* padding blend folded into the block (maskBlend, models.cpp:170-172 and
+   * 362-363): with blend_mask [b] (0/1 per row) the forward writes
+   * hout = h'*m + prev*(1-m); the backward feeds go*m to the block and
+   * gprev (+)= go*(1-m) (gprev may be gh: the block's input is prev) */
+  const float* blend_mask;
+  const float* blend_prev;   /* [b x d] */
+  float* gprev;              /* [b x d] or NULL (prev not differentiable) */
+  int accumulate_prev;
 } mtkc_gru_args;
 
 int mtkc_gru_forward(const mtkc_gru_args* a, void* stream);

@@ -67,6 +67,26 @@ float* Device::scratch(size_t bytes) {
 
 void Device::sync() { MTKC(mtkc_stream_sync(stream_)); }
 
+void* Device::sideStream() {
+  if(!side_) {
+    MTKC(mtkc_stream_create(&side_));
+    MTKC(mtkc_event_create(&forkEv_));
+    MTKC(mtkc_event_create(&joinEv_));
+  }
+  return side_;
+}
+
+void Device::forkSide() {
+  sideStream();
+  MTKC(mtkc_event_record(forkEv_, stream_));
+  MTKC(mtkc_stream_wait_event(side_, forkEv_));
+}
+
+void Device::joinSide() {
+  MTKC(mtkc_event_record(joinEv_, side_));
+  MTKC(mtkc_stream_wait_event(stream_, joinEv_));
+}
+
 void Device::upload(void* dst, const void* src, size_t bytes) {
   if(!bytes)
     return;

@@ -30,6 +30,12 @@ public:
   void setPrecision(Precision p) { precision_ = p; }
 
   float* scratch(size_t bytes);  // stream-ordered scratch, grows on demand
+  // Second compute stream for independent work inside one op (the two
+  // directions of the bidirectional RNN encoder): forkSide() makes it wait
+  // for the compute stream, joinSide() makes the compute stream wait for it.
+  void* sideStream();
+  void forkSide();
+  void joinSide();
   size_t scratchBytes() const { return scratchBytes_; }
 
   // Asynchronous host->device copy on the compute stream through a pinned
@@ -51,6 +57,9 @@ private:
   int index_ = 0;
   Precision precision_ = Precision::TF32;
   std::shared_ptr<DeviceBuffer> scratch_;
+  void* side_ = nullptr;
+  void* forkEv_ = nullptr;
+  void* joinEv_ = nullptr;
   size_t scratchBytes_ = 0;
   // pinned staging ring
   struct Pending {

@@ -110,6 +110,9 @@ __global__ void __launch_bounds__(GT) gru_fwd_kernel(mtkc_gru_args p) {
   float* cache = p.cache + r * 3 * d;
   const float* h = p.h + r * d;
   float* ho = p.hout + r * d;
+  const bool blend = p.blend_mask != nullptr;
+  const float m = blend ? p.blend_mask[r] : 1.f, notm = 1.f - m;
+  const float* prev = blend ? p.blend_prev + r * d : nullptr;
   #pragma unroll
   for(int k = 0; k < GV; ++k) {
     const int64_t j = threadIdx.x + (int64_t)k * GT;
@@ -121,7 +124,8 @@ __global__ void __launch_bounds__(GT) gru_fwd_kernel(mtkc_gru_args p) {
     cache[j] = z;
     cache[d + j] = rr;
     cache[2 * d + j] = ht;
-    ho[j] = (1.f - z) * ht + z * h[j];
+    float hn = (1.f - z) * ht + z * h[j];
+    ho[j] = blend ? hn * m + prev[j] * notm : hn;  // a*m + b*(1-m)
   }
 }
 
@@ -140,6 +144,9 @@ __global__ void __launch_bounds__(GT) gru_bwd_kernel(mtkc_gru_args p) {
   const float* hu = p.hu + r * 3 * d;
   const float* h = p.h + r * d;
   const float* go = p.go + r * d;
+  const bool blend = p.blend_mask != nullptr;
+  const float m = blend ? p.blend_mask[r] : 1.f, notm = 1.f - m;
+  const bool prevIsH = blend && p.gprev == p.gh;
   float daz[GV], dar[GV], dacv[GV];
 #pragma unroll
   for(int n = 0; n < GV; ++n)
@@ -149,11 +156,22 @@ __global__ void __launch_bounds__(GT) gru_bwd_kernel(mtkc_gru_args p) {
     const int64_t j = threadIdx.x + (int64_t)n * GT;
     if(j >= d)
       break;
-    float g = go[j], z = cache[j], rr = cache[d + j], ht = cache[2 * d + j];
+    float g0 = go[j];
+    float g = blend ? g0 * m : g0;  // maskBlend backward (mul by m / 1-m)
+    float z = cache[j], rr = cache[d + j], ht = cache[2 * d + j];
     float dz = g * (h[j] - ht);
     float dht = g * (1.f - z);
     float ghv = g * z;
-    p.gh[r * d + j] = p.accumulate_h ? p.gh[r * d + j] + ghv : ghv;
+    if(prevIsH) {
+      float t = p.accumulate_h ? p.gh[r * d + j] + ghv : ghv;
+      p.gh[r * d + j] = t + g0 * notm;
+    } else {
+      p.gh[r * d + j] = p.accumulate_h ? p.gh[r * d + j] + ghv : ghv;
+      if(blend && p.gprev) {
+        float gp = g0 * notm;
+        p.gprev[r * d + j] = p.accumulate_prev ? p.gprev[r * d + j] + gp : gp;
+      }
+    }
     float dac = dht * (1.f - ht * ht);
     float dr = dac * hu[2 * d + j];
     p.duh[r * d + j] = dac * rr;
