@@ -66,6 +66,9 @@ def parse():
     p.add_argument("--config", default="base")
     p.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--dropout", type=float, default=None,
+                   help="override the config's dropout (SURVEY 8(d): 0 for parity, 0.1 for "
+                        "throughput); TF32 mode draws device (Philox) masks")
     return p.parse_args()
 
 
@@ -244,7 +247,9 @@ def run_b200(a):
     nccl_ranks = M.comm_ranks()
     if nccl_ranks != world:
         sys.exit(f"bench.py: NCCL communicator has {nccl_ranks} ranks, expected {world}")
-    spec = CONFIGS[a.config]
+    spec = dict(CONFIGS[a.config])
+    if a.dropout is not None:
+        spec["dropout"] = a.dropout
     cfg = config_text(**spec)
     budget = TOKEN_BUDGET[a.config]
     vocab = spec["vocab"]
@@ -493,7 +498,9 @@ def run_reference(a):
     if rank != 0:
         return
     configs = _pure("configs")
-    spec = configs.CONFIGS[a.config]
+    spec = dict(configs.CONFIGS[a.config])
+    if a.dropout is not None:
+        spec["dropout"] = a.dropout
     cfg = configs.config_text(**spec)
     threads = os.cpu_count() or 1
     steps = max(1, min(a.steps, 3))

@@ -223,6 +223,21 @@ int mtkc_mask_blend_backward(float* ga, float* gb, const float* go, const float*
                              int64_t rows, int64_t cols, int accumulate_a, int accumulate_b,
                              void* stream);
 
+/* Device dropout (throughput mode; graph.cpp:817-846 semantics with a
+ * counter-based mask instead of host mt19937_64 draws): element idx of an
+ * [outer x axis_len x inner] tensor uses mask index o*inner + j when
+ * axis_len > 1 (variational dropout along that axis), else idx.  Mask value:
+ * Philox4x32-10(key = seed, counter = mi/4) word mi%4, kept (1/(1-p)) iff its
+ * high 24 bits >= ceil(p * 2^24).  addend != NULL: out = addend + x*m (the
+ * pre-norm residual add(x, dropout(f)), layers.cpp:135). */
+int mtkc_dropout(float* out, const float* x, const float* addend, int64_t n, int64_t inner,
+                 int64_t axis_len, float p, uint64_t seed, void* stream);
+/* gx (+)= go * m with the same mask */
+int mtkc_dropout_backward(float* gx, const float* go, int64_t n, int64_t inner, int64_t axis_len,
+                          float p, uint64_t seed, int accumulate, void* stream);
+/* the mask itself (dropoutMask, graph.cpp:817-830) */
+int mtkc_dropout_mask(float* out, int64_t n, float p, uint64_t seed, void* stream);
+
 /* ======================================================================== */
 /* reductions (reduceInto tensor.cpp:322-368, graph.cpp:463-524)            */
 /* ======================================================================== */

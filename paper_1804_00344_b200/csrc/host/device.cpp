@@ -46,6 +46,11 @@ Device::Device() {
   const char* p = std::getenv("MTK_PRECISION");
   if(p && (std::string(p) == "fp32" || std::string(p) == "FP32"))
     precision_ = Precision::FP32;
+  if(const char* r = std::getenv("MTK_DROPOUT_RNG")) {
+    const std::string v(r);
+    dropoutRng_ = v == "host" ? DropoutRng::Host : v == "device" ? DropoutRng::Device
+                                                                : DropoutRng::Auto;
+  }
 }
 
 Device& Device::get() {

@@ -914,13 +914,63 @@ std::vector<NodeRef> ExpressionGraph::affineGroup(NodeRef x, const std::vector<N
   return out;
 }
 
+// device dropout node state (dropout / dropoutResidual)
+namespace {
+struct DropoutAux {
+  uint64_t key;
+  float p;
+  int64_t inner, axisLen;
+};
+}  // namespace
+
 NodeRef ExpressionGraph::residualAdd(NodeRef r, NodeRef z) {
   checkRef(r);
   checkRef(z);
   Node& zn = nodes_[(size_t)z.index];
+  if(zn.op == "dropout" && z.index == (int)nodes_.size() - 1 && zn.shape == r.shape &&
+     resolve(r.index) != resolve(zn.inputs[0]) && r.index != z.index &&
+     (size_t)z.index >= computed_) {
+    // r + dropout(f) (layers.cpp:135) as one pass: out = r + f * m
+    // forward; d(r) = d(out) (shared buffer, as add's backward), d(f) = d(out) * m
+    zn.op = "dropoutResidual";
+    zn.inputs.push_back(r.index);
+    zn.fwd = [](ExpressionGraph& g, Node& n) {
+      auto* a = static_cast<DropoutAux*>(n.aux.get());
+      MTKC(mtkc_dropout(n.value.dev(), g.valPtr(n.inputs[0]), g.valPtr(n.inputs[1]),
+                        n.value.size(), a->inner, a->axisLen, a->p, a->key, stream()));
+    };
+    zn.bwd = [](ExpressionGraph& g, Node& n) {
+      auto* a = static_cast<DropoutAux*>(n.aux.get());
+      const float* go = g.gradSrc(n);
+      if(g.node(g.resolve(n.inputs[0])).needsGrad) {
+        auto d = g.gradDst(n.inputs[0]);
+        MTKC(mtkc_dropout_backward(d.ptr, go, n.shape.size(), a->inner, a->axisLen, a->p, a->key,
+                                   d.accumulate, stream()));
+      }
+      Node& in = g.node(g.resolve(n.inputs[1]));
+      if(!in.needsGrad)
+        return;
+      if(!in.isParam && !in.gate && !in.gradLive && in.grad.empty() && in.alias < 0 &&
+         in.shape == n.shape) {
+        in.grad = n.grad;
+        in.gradLive = true;
+      } else {
+        auto d = g.gradDst(n.inputs[1]);
+        if(d.ptr != go) {
+          if(d.accumulate)
+            MTKC(mtkc_axpy(d.ptr, go, 1.f, n.shape.size(), stream()));
+          else
+            MTKC(mtkc_memcpy_d2d(d.ptr, go, (size_t)n.shape.size() * sizeof(float), stream()));
+        }
+      }
+    };
+    zn.needsGrad = zn.needsGrad || nodes_[(size_t)resolve(r.index)].needsGrad;
+    return z;
+  }
   const bool fusable = Device::get().precision() == Precision::TF32 &&
                        z.index == (int)nodes_.size() - 1 && zn.op == "affine" && !zn.group &&
                        zn.alias < 0 && zn.shape == r.shape && r.index != z.index &&
+                       resolve(r.index) != resolve(zn.inputs[0]) &&
                        (size_t)z.index >= computed_;
   if(!fusable)
     return add(r, z);
@@ -1508,9 +1558,22 @@ NodeRef ExpressionGraph::attention(NodeRef q, NodeRef k, NodeRef v, const Tensor
 
 // -------------------------------------------------------------- dropout
 
+
 NodeRef ExpressionGraph::dropoutMask(const Shape& shape, Real p) {
   if(p >= Real(1) || p < Real(0))
     throw ContractError("dropout probability must be in [0, 1)");
+  if(!inference_ && p != Real(0) && Device::get().deviceDropout()) {
+    // throughput mode: the mask is generated on the device from one draw of
+    // the graph RNG (kernels/dropout.cu), nothing is uploaded
+    const uint64_t key = rng_();
+    Node n;
+    n.op = "dropoutMask";
+    n.shape = shape;
+    n.fwd = [key, p](ExpressionGraph&, Node& n) {
+      MTKC(mtkc_dropout_mask(n.value.dev(), n.value.size(), (float)p, key, stream()));
+    };
+    return addNode(std::move(n));
+  }
   Tensor mask(shape);
   if(inference_ || p == Real(0)) {
     mask.fill(1);
@@ -1535,6 +1598,35 @@ NodeRef ExpressionGraph::dropout(NodeRef x, Real p, int variationalAxis) {
     if(variationalAxis >= x.shape.rank())
       throw ContractError("variational axis out of range");
     dims[(size_t)variationalAxis] = 1;
+  }
+  if(Device::get().deviceDropout()) {
+    // y = x * m with m recomputed from (key, mask index) forward and backward
+    const uint64_t key = rng_();
+    const int axis = variationalAxis;
+    int64_t inner = 1, axisLen = 1;
+    if(axis >= 0) {
+      axisLen = x.shape[axis];
+      for(int i = axis + 1; i < x.shape.rank(); ++i)
+        inner *= x.shape[i];
+    }
+    Node n;
+    n.op = "dropout";
+    n.shape = x.shape;
+    n.inputs = {x.index};
+    n.aux = std::make_shared<DropoutAux>(DropoutAux{key, (float)p, inner, axisLen});
+    n.fwd = [](ExpressionGraph& g, Node& n) {
+      auto* a = static_cast<DropoutAux*>(n.aux.get());
+      MTKC(mtkc_dropout(n.value.dev(), g.valPtr(n.inputs[0]), nullptr, n.value.size(), a->inner,
+                        a->axisLen, a->p, a->key, stream()));
+    };
+    n.bwd = [](ExpressionGraph& g, Node& n) {
+      auto* a = static_cast<DropoutAux*>(n.aux.get());
+      const float* go = g.gradSrc(n);
+      auto d = g.gradDst(n.inputs[0]);
+      MTKC(mtkc_dropout_backward(d.ptr, go, n.shape.size(), a->inner, a->axisLen, a->p, a->key,
+                                 d.accumulate, stream()));
+    };
+    return addNode(std::move(n));
   }
   NodeRef mask = dropoutMask(Shape(dims), p);
   return mul(x, mask);

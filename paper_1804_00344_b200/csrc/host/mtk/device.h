@@ -17,6 +17,13 @@ namespace mtk {
 // summation order (parity mode); TF32 = tcgen05 tensor cores (default).
 enum class Precision { FP32 = 0, TF32 = 1 };
 
+// Where dropout masks come from.  Host = the reference's own draws (the
+// graph's mt19937_64, graph.cpp:817-830; bit-exact, uploaded as constants);
+// Device = counter-based Philox masks recomputed inside the kernels (never
+// stored or uploaded; keyed by one draw of the same graph RNG).  Auto = Host
+// in FP32 (parity) mode, Device in TF32 (throughput) mode.
+enum class DropoutRng { Auto = 0, Host = 1, Device = 2 };
+
 class Device {
 public:
   static Device& get();  // initialises the device on first use
@@ -28,6 +35,12 @@ public:
   int index() const { return index_; }
   Precision precision() const { return precision_; }
   void setPrecision(Precision p) { precision_ = p; }
+  DropoutRng dropoutRng() const { return dropoutRng_; }
+  void setDropoutRng(DropoutRng r) { dropoutRng_ = r; }
+  bool deviceDropout() const {
+    return dropoutRng_ == DropoutRng::Device ||
+           (dropoutRng_ == DropoutRng::Auto && precision_ == Precision::TF32);
+  }
 
   float* scratch(size_t bytes);  // stream-ordered scratch, grows on demand
   // Second compute stream for independent work inside one op (the two
@@ -56,6 +69,7 @@ private:
   int sms_ = 148;
   int index_ = 0;
   Precision precision_ = Precision::TF32;
+  DropoutRng dropoutRng_ = DropoutRng::Auto;
   std::shared_ptr<DeviceBuffer> scratch_;
   void* side_ = nullptr;
   void* forkEv_ = nullptr;

@@ -113,6 +113,13 @@ PYBIND11_MODULE(_mtk, m) {
     Device::get().setPrecision(p == "fp32" ? Precision::FP32 : Precision::TF32);
   });
   m.def("precision", [] { return Device::get().precision() == Precision::FP32 ? "fp32" : "tf32"; });
+  m.def("set_dropout_rng", [](const std::string& r) {
+    if(r != "auto" && r != "host" && r != "device")
+      throw ContractError("dropout rng must be auto, host or device");
+    Device::get().setDropoutRng(r == "host" ? DropoutRng::Host
+                                : r == "device" ? DropoutRng::Device : DropoutRng::Auto);
+  });
+  m.def("dropout_rng", [] { return Device::get().deviceDropout() ? "device" : "host"; });
   m.def("sync", [] { Device::get().sync(); });
   m.def("check_flags", [] { Device::get().checkFlags("explicit check"); });
   m.def("launch_count", [] { return (uint64_t)mtkc_launch_count(); });
@@ -254,6 +261,9 @@ PYBIND11_MODULE(_mtk, m) {
       .def("embed", [](G& g, NodeRef t, IArr ids) { return g.embed(t, intMatOf(ids)); })
       .def("gru_cell", &G::gruCell)
       .def("dropout", &G::dropout, py::arg("x"), py::arg("p"), py::arg("variational_axis") = -1)
+      .def("dropout_mask",
+           [](G& g, py::sequence shape, float p) { return g.dropoutMask(shapeOf(shape), p); })
+      .def("residual_add", &G::residualAdd, py::arg("r"), py::arg("z"))
       .def("cross_entropy",
            [](G& g, NodeRef l, IArr targets, py::object mask) {
              return g.crossEntropy(l, intMatOf(targets),
