@@ -437,6 +437,73 @@ int mtkc_gru_forward(const mtkc_gru_args* a, void* stream);
 int mtkc_gru_backward(const mtkc_gru_args* a, void* stream);
 
 /* ======================================================================== */
+/* Persistent GRU scan (sequence-level recurrence of RnnEncoder::build and   */
+/* RnnDecoder::step, models.cpp:146-187, 312-382; DeepTransitionCell         */
+/* layers.cpp:183-244; gruCell graph.cpp:633-745; Bahdanau layers.cpp:59-79) */
+/* as ONE cooperative launch over all T steps (both encoder directions in    */
+/* one launch): per block and step the recurrent product h*[Uz|Ur|Uh] is a   */
+/* K-split tcgen05 product over all SMs (fp32 partials, TMA-fed, TMEM        */
+/* accumulators), then a row-wise pointwise phase sums the partials in a     */
+/* fixed order and applies bias / layer norm / gates exactly like            */
+/* mtkc_gru_forward; grid barriers separate the phases.  Outputs are the     */
+/* same time-major buffers the per-step path writes, so the backward and     */
+/* the hoisted weight-gradient products consume them unchanged.              */
+/* ======================================================================== */
+#define MTKC_RNN_MAX_BLOCKS 8
+typedef struct mtkc_rnn_block {
+  const float* U[3];     /* Uz, Ur, Uh [d x d] (reference layout, row-major) */
+  const float* bias[3];  /* bz, br, bh [d] */
+  const float* ln[6];    /* lnGz lnBz lnGr lnBr lnGx lnBx [d] or NULL */
+  const float* W[3];     /* per-step input weights [kd x d] (decoder block 2), or NULL */
+  float* hu;             /* [T*b x 3d] out: h*U per step */
+  float* cache;          /* [T*b x 3d] out: z, r, h~ */
+  float* lnc;            /* [T*b x 3d] out (LN only) */
+  float* lnrs;           /* [T*b x 3]  out (LN only) */
+} mtkc_rnn_block;
+
+typedef struct mtkc_rnn_dir {
+  int reverse;           /* 1: t = T-1 .. 0, state slots t+1 -> t */
+  int nblocks;
+  mtkc_rnn_block blk[MTKC_RNN_MAX_BLOCKS];
+  float* HH;             /* [(T+1)*b x d]; the initial-state slot is pre-filled */
+  float* sout;           /* [(nblocks-1)*T*b x d] outputs of blocks 1..K-1 (block k at k*T*b) */
+  const float* xw1;      /* [T*b x 3d] hoisted input product of block 1, or NULL */
+  float* xw2;            /* [T*b x 3d] out: per-step ctx*W of block 2 (attention) */
+} mtkc_rnn_dir;
+
+typedef struct mtkc_rnn_scan_args {
+  int64_t b, T, d;
+  int ndir;              /* 1 (decoder) or 2 (bidirectional encoder) */
+  float eps;
+  const float* maskT;    /* [T x b] padding blend mask of the last block, or NULL */
+  mtkc_rnn_dir dir[2];
+  /* Bahdanau attention between blocks 1 and 2 (decoder, ndir == 1) */
+  int has_att;
+  int64_t S, a, kd;
+  const float* attW;     /* [d x a] query projection */
+  const float* attV;     /* [a] */
+  const float* attLnG;   /* [a] or NULL */
+  const float* attLnB;
+  const float* keys;     /* [b x S x kd] */
+  const float* uk;       /* [b x S x a] */
+  const float* attMask;  /* [b x S] or NULL */
+  float* wq;             /* [T*b x a] out */
+  float* attT;           /* [T*b*S x a] out: tanh values */
+  float* attWts;         /* [T*b x S] out: softmax weights */
+  float* attLnx;         /* [T*b*S x a] out (LN only) */
+  float* attLnrs;        /* [T*b x S] out (LN only) */
+  float* ctx;            /* [T*b x kd] out */
+  int* flags;
+  float* workspace;
+  size_t workspace_bytes;
+} mtkc_rnn_scan_args;
+
+/* 1 when the persistent path supports these dimensions (d % 32 == 0, ...) */
+int mtkc_rnn_scan_supported(const mtkc_rnn_scan_args* a);
+size_t mtkc_rnn_scan_workspace(const mtkc_rnn_scan_args* a);
+int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream);
+
+/* ======================================================================== */
 /* Bahdanau MLP attention core (BahdanauAttention::apply layers.cpp:59-79),  */
 /* fused: given wq = query*W [b x a] and uk = keys*U [b x s x a] (GEMMs, the */
 /* latter computed once per batch), per row and source position j:           */

@@ -21,6 +21,8 @@
 // one pointwise kernel and one K-concatenated (dz|dr|dh)*U^T product
 // backward, plus the attention between blocks 1 and 2 of the decoder.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "mtk/device.h"
 #include "mtk/graph.h"
@@ -162,7 +164,10 @@ struct Dir {
   bool reverse = false;
   // forward state
   Tensor HH;  // [(T+1)*b x d]: h0 and every blended state H_t
-  std::vector<Tensor> sout, hu, cache, lnc, lnrs;  // per block ([T*b x d] / [T*b x 3d] / [T*b x 3])
+  std::vector<Tensor> hu, cache, lnc, lnrs;  // per block ([T*b x d] / [T*b x 3d] / [T*b x 3])
+  Tensor soutAll;  // outputs of blocks 1..K-1, block k at k*T*b rows ([(K-1)*T*b x d])
+  int64_t soutStride = 0;  // T*b*d
+  float* sout(int64_t k) const { return soutAll.dev() + k * soutStride; }
   Tensor xw1, xw2, ctx, wq, attT, attW, attLnx, attLnrs, attScratch;
   // backward
   Tensor GH;  // [(T+1)*b x d] gradient of HH
@@ -202,14 +207,14 @@ void forwardBegin(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir&
     MTKC(mtkc_memcpy_d2d(HH + h0slot * b * d, h0, (size_t)(b * d) * sizeof(float), c.st));
   else
     MTKC(mtkc_memset(HH + h0slot * b * d, 0, (size_t)(b * d) * sizeof(float), c.st));
-  D.sout.assign((size_t)K, Tensor());
+  if(K > 1)
+    D.soutAll = g.allocTensor(Shape({(K - 1) * T * b, d}));
+  D.soutStride = T * b * d;
   D.hu.assign((size_t)K, Tensor());
   D.cache.assign((size_t)K, Tensor());
   D.lnc.assign((size_t)K, Tensor());
   D.lnrs.assign((size_t)K, Tensor());
   for(int64_t k = 0; k < K; ++k) {
-    if(k < K - 1)
-      D.sout[(size_t)k] = g.allocTensor(Shape({T * b, d}));
     D.hu[(size_t)k] = g.allocTensor(Shape({T * b, d3}));
     D.cache[(size_t)k] = g.allocTensor(Shape({T * b, d3}));
     if(X.ln) {
@@ -305,7 +310,7 @@ void forwardStep(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
       }
       a.eps = 1e-9f;  // graph.cpp:690
       a.cache = D.cache[(size_t)k].dev() + t * b * d3;
-      float* out = k == K - 1 ? HH + hSlot(D, t) * b * d : D.sout[(size_t)k].dev() + t * b * d;
+      float* out = k == K - 1 ? HH + hSlot(D, t) * b * d : D.sout(k) + t * b * d;
       a.hout = out;
       if(k == K - 1 && maskT) {  // keep the old state at padded positions
         a.blend_mask = maskT + t * b;
@@ -343,6 +348,103 @@ void forwardStep(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
       }
     }
   }
+}
+
+// ---------------------------------------------------------- persistent path
+
+// TF32 mode runs the whole forward recurrence as one cooperative kernel
+// (kernels/rnn_persist.cu) when its dimension constraints hold;
+// MTK_RNN_PERSIST=0 selects the per-step launches (forwardStep) instead.
+bool persistEnabled() {
+  const char* e = std::getenv("MTK_RNN_PERSIST");
+  return !(e && e[0] == '0') && Device::get().precision() == Precision::TF32;
+}
+
+void fillDir(ExpressionGraph& g, ExpressionGraph::Node& n, const ScanAux& X, Dir& D,
+             mtkc_rnn_dir& o) {
+  const int64_t K = (int64_t)D.blocks.size();
+  o.reverse = D.reverse ? 1 : 0;
+  o.nblocks = (int)K;
+  for(int64_t k = 0; k < K; ++k) {
+    const BlockSlots& Bk = D.blocks[(size_t)k];
+    mtkc_rnn_block& B = o.blk[k];
+    for(int j = 0; j < 3; ++j) {
+      B.U[j] = g.valPtr(n.inputs[(size_t)Bk.U[j]]);
+      B.bias[j] = g.valPtr(n.inputs[(size_t)Bk.b[j]]);
+      B.W[j] = (k == 1 && X.att) ? g.valPtr(n.inputs[(size_t)Bk.W[j]]) : nullptr;
+    }
+    for(int j = 0; j < 6; ++j)
+      B.ln[j] = (X.ln && Bk.ln[j] >= 0) ? g.valPtr(n.inputs[(size_t)Bk.ln[j]]) : nullptr;
+    B.hu = D.hu[(size_t)k].dev();
+    B.cache = D.cache[(size_t)k].dev();
+    B.lnc = X.ln ? D.lnc[(size_t)k].dev() : nullptr;
+    B.lnrs = X.ln ? D.lnrs[(size_t)k].dev() : nullptr;
+  }
+  o.HH = D.HH.dev();
+  o.sout = K > 1 ? D.soutAll.dev() : nullptr;
+  o.xw1 = D.xw1.empty() ? nullptr : D.xw1.devc();
+  o.xw2 = X.att ? D.xw2.dev() : nullptr;
+}
+
+mtkc_rnn_scan_args scanArgs(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X) {
+  mtkc_rnn_scan_args a{};
+  a.b = X.b;
+  a.T = X.T;
+  a.d = X.d;
+  a.ndir = X.ndir;
+  a.eps = 1e-9f;  // graph.cpp:690
+  a.maskT = X.maskT.empty() ? nullptr : X.maskT.devc();
+  for(int q = 0; q < X.ndir; ++q)
+    fillDir(g, n, X, X.dir[q], a.dir[q]);
+  a.flags = Device::get().flags();
+  if(X.att) {
+    const AttSlots& A = X.A;
+    Dir& D = X.dir[0];
+    a.has_att = 1;
+    a.S = A.S;
+    a.a = A.a;
+    a.kd = A.kd;
+    a.attW = g.valPtr(n.inputs[(size_t)A.W]);
+    a.attV = g.valPtr(n.inputs[(size_t)A.v]);
+    a.attLnG = A.lnG >= 0 ? g.valPtr(n.inputs[(size_t)A.lnG]) : nullptr;
+    a.attLnB = A.lnB >= 0 ? g.valPtr(n.inputs[(size_t)A.lnB]) : nullptr;
+    a.keys = g.valPtr(n.inputs[(size_t)A.keys]);
+    a.uk = g.valPtr(n.inputs[(size_t)A.uk]);
+    a.attMask = A.hasMask ? A.mask.devc() : nullptr;
+    a.wq = D.wq.dev();
+    a.attT = D.attT.dev();
+    a.attWts = D.attW.dev();
+    a.attLnx = A.lnG >= 0 ? D.attLnx.dev() : nullptr;
+    a.attLnrs = A.lnG >= 0 ? D.attLnrs.dev() : nullptr;
+    a.ctx = D.ctx.dev();
+  }
+  return a;
+}
+
+// true when the persistent kernel ran the recurrence (all T steps)
+bool forwardPersistent(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X) {
+  if(!persistEnabled())
+    return false;
+  mtkc_rnn_scan_args a = scanArgs(g, n, X);
+  const bool ok = mtkc_rnn_scan_supported(&a) != 0;
+  Device& dev = Device::get();
+  const size_t need = ok ? mtkc_rnn_scan_workspace(&a) : 0;
+  if(std::getenv("MTK_RNN_DEBUG"))
+    std::fprintf(stderr, "[rnn scan] ndir %d b %lld T %lld d %lld blocks %d att %d: %s, %zu B\n",
+                 a.ndir, (long long)a.b, (long long)a.T, (long long)a.d, a.dir[0].nblocks,
+                 a.has_att, ok ? "persistent" : "per-step", need);
+  if(!ok)
+    return false;
+  // the upper half of the device scratch (ctxFor(1)'s slice; the side
+  // stream is idle while the persistent kernel runs on the compute stream)
+  const size_t total = (size_t)1 << 30;
+  if(need > total / 2)
+    return false;
+  float* base = dev.scratch(total);
+  a.workspace = base + (total / 2) / sizeof(float);
+  a.workspace_bytes = total / 2;
+  MTKC(mtkc_rnn_scan_forward(&a, dev.stream()));
+  return true;
 }
 
 void backwardBegin(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& D,
@@ -403,7 +505,7 @@ void backwardStep(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir&
       const BlockSlots& Bk = D.blocks[(size_t)k];
       Dir::Grads& q = G[(size_t)k];
       const float* go = k == K - 1 ? GH + hSlot(D, t) * b * d : ds[(size_t)k].devc();
-      const float* sIn = k == 0 ? hprev : D.sout[(size_t)k - 1].devc() + t * b * d;
+      const float* sIn = k == 0 ? hprev : D.sout(k - 1) + t * b * d;
       float* gIn = k == 0 ? ghprev : ds[(size_t)k - 1].dev();
       const int accIn = k == 0 ? 1 : 0;
       const float* xw = nullptr;
@@ -511,7 +613,7 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
   for(int64_t k = 0; k < K; ++k) {
     const BlockSlots& Bk = D.blocks[(size_t)k];
     Dir::Grads& q = D.G[(size_t)k];
-    const float* sIn = k == 0 ? HH + (D.reverse ? b * d : 0) : D.sout[(size_t)k - 1].devc();
+    const float* sIn = k == 0 ? HH + (D.reverse ? b * d : 0) : D.sout(k - 1);
     const float* dp[3] = {q.dpz.devc(), q.dpr.devc(), q.duh.devc()};
     {  // dU += S_in^T [dz|dr|duh]  (graph.cpp:773, 803)
       const float* As[3] = {sIn, sIn, sIn};
@@ -579,7 +681,7 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
   if(X.att) {
     {  // attention query projection: dW += S1^T dwq over b*T rows
       auto dst = g.gradDst(n.inputs[(size_t)A.W]);
-      gemm1(c, d, A.a, TB, D.sout[0].devc(), d, true, D.dwq.devc(), A.a, false, dst.ptr, A.a,
+      gemm1(c, d, A.a, TB, D.sout(0), d, true, D.dwq.devc(), A.a, false, dst.ptr, A.a,
             dst.accumulate ? 1.f : 0.f);
     }
     const int np = A.lnG >= 0 ? 3 : 1;
@@ -641,15 +743,26 @@ NodeRef ExpressionGraph::rnnEncoderScan(NodeRef x, const std::vector<GruParams>&
     }
     if(!X->maskT.empty())
       X->maskT.devc();  // uploaded on the compute stream before the fork
-    dev.forkSide();
-    const Ctx c0 = ctxFor(0), c1 = ctxFor(1);
-    forwardBegin(g, n, *X, X->dir[0], c0, nullptr);
-    forwardBegin(g, n, *X, X->dir[1], c1, nullptr);
-    for(int64_t i = 0; i < T; ++i) {  // the two directions' steps interleaved
-      forwardStep(g, n, *X, X->dir[0], c0, i);
-      forwardStep(g, n, *X, X->dir[1], c1, i);
+    if(persistEnabled()) {  // both directions in one cooperative launch
+      const Ctx c0 = ctxFor(0);
+      forwardBegin(g, n, *X, X->dir[0], c0, nullptr);
+      forwardBegin(g, n, *X, X->dir[1], c0, nullptr);
+      if(!forwardPersistent(g, n, *X))
+        for(int64_t i = 0; i < T; ++i) {
+          forwardStep(g, n, *X, X->dir[0], c0, i);
+          forwardStep(g, n, *X, X->dir[1], c0, i);
+        }
+    } else {
+      dev.forkSide();
+      const Ctx c0 = ctxFor(0), c1 = ctxFor(1);
+      forwardBegin(g, n, *X, X->dir[0], c0, nullptr);
+      forwardBegin(g, n, *X, X->dir[1], c1, nullptr);
+      for(int64_t i = 0; i < T; ++i) {  // the two directions' steps interleaved
+        forwardStep(g, n, *X, X->dir[0], c0, i);
+        forwardStep(g, n, *X, X->dir[1], c1, i);
+      }
+      dev.joinSide();
     }
-    dev.joinSide();
     // context [b x s x 2d] = [H_fwd | H_bwd] per position
     Tensor tmp = g.allocTensor(Shape({b, T, d}));
     for(int q = 0; q < 2; ++q) {
@@ -797,8 +910,9 @@ ExpressionGraph::RnnScanOut ExpressionGraph::rnnDecoderScan(
     Dir& D = X->dir[0];
     const Ctx c0 = ctxFor(0);
     forwardBegin(g, n, *X, D, c0, g.valPtr(n.inputs[1]));
-    for(int64_t i = 0; i < T; ++i)
-      forwardStep(g, n, *X, D, c0, i);
+    if(!forwardPersistent(g, n, *X))
+      for(int64_t i = 0; i < T; ++i)
+        forwardStep(g, n, *X, D, c0, i);
     {  // states [b x t x d]
       const int64_t sd[4] = {1, T, b, d};
       const int perm[4] = {0, 2, 1, 3};

@@ -1,0 +1,1046 @@
+// Persistent GRU scan: the whole time loop of a deep-transition GRU stack
+// (RnnEncoder::build / RnnDecoder::step, reference models.cpp:146-187 and
+// 312-382; DeepTransitionCell layers.cpp:183-244; gruCell graph.cpp:633-745;
+// BahdanauAttention::apply layers.cpp:59-79) in ONE cooperative launch.
+//
+// Why: per step and block the recurrence is a skinny product
+// [b x d] x [d x 3d] (b = 60..128 rows) followed by a row-wise pointwise
+// pass.  As separate launches that is ~4 kernels per block-step (GEMM,
+// split-K reduce, GRU pointwise, ...) -- thousands per training step, more
+// host submission time than GPU time.  Here every SM stays resident for the
+// whole sequence and the phases are separated by grid barriers:
+//
+//   PROD  the recurrent product as K-split units (m-tile 128 rows x n-tile
+//         96 gate columns x k-slice) over all CTAs of the direction:
+//         warp 0 issues TMA loads (6-stage ring, 128-byte swizzle), warp 1
+//         issues tcgen05.mma kind::tf32 into a TMEM accumulator, warps 4-7
+//         read it back (tcgen05.ld) and store fp32 partials;
+//   PW    one CTA per batch row: sum the partials in a fixed order (k-slice
+//         0, 1, ...), then bias + per-gate layer norm + sigmoid/tanh gates +
+//         interpolation (+ padding blend), exactly the arithmetic of
+//         gru_fwd_kernel (kernels/gru.cu);
+//   ATT   (decoder, after block 1) the query product s1*W is a PROD phase;
+//         then one CTA per row computes the scores, masked softmax and the
+//         context (the arithmetic of bahdanau_score/ctx_kernel).
+//
+// The weight operands are fed K-major: the host transposes U / W / attW
+// once per forward into the workspace (weights are constant within a step).
+// Both directions of the bidirectional encoder run in one launch on
+// disjoint halves of the grid (separate barriers).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <vector>
+#include <cstdio>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+using namespace mtkc;
+using namespace mtkc::tc;
+
+namespace {
+
+constexpr int RT = 256;        // threads: warp 0 TMA, warp 1 MMA, warps 4..7 epilogue
+constexpr int RST = 6;         // smem ring stages
+constexpr int NTH = 96;        // n-tile of the gate products (3d is a multiple of 96)
+constexpr uint32_t A_STAGE = 128 * 32 * 4;  // 16 KB: 128 rows x 32 fp32
+constexpr uint32_t B_STAGE = NTH * 32 * 4;  // 12 KB
+constexpr int TMEM_COLS = 128;
+constexpr int MAXA = 2048;  // attention width cap (row-phase smem)
+constexpr int MAXS = 1024;  // source positions cap
+constexpr int GV = 8;       // elements per thread in the GRU row phase (d <= 2048)
+
+struct Maps {
+  CUtensorMap hh[2];    // A: state slots [(T+1)*b x d]
+  CUtensorMap sout[2];  // A: intermediate block outputs [(K-1)*T*b x d]
+  CUtensorMap ut[2];    // B: [U_z|U_r|U_h]^T per block, [K*3d x d]
+  CUtensorMap ctx;      // A: contexts [T*b x kd]
+  CUtensorMap w2t;      // B: [W_z|W_r|W_x]^T of block 2, [3d x kd]
+  CUtensorMap watt;     // B: attention W^T [a x d]
+};
+
+struct KP {
+  mtkc_rnn_scan_args a;
+  float* partHu[2];  // [KCh][b][3d] per direction
+  float* partX;      // [KCx][b][3d]
+  float* partQ;      // [KCq][b][a]
+  unsigned* ctr;     // [2] grid-barrier counters (zeroed before launch)
+  unsigned long long* prof;  // MTK_RNN_PROF: CTA 0's phase timestamps, or NULL
+  int KCh, KCx, KCq, NTq;
+};
+
+struct Prod {
+  const CUtensorMap* ma;
+  const CUtensorMap* mb;
+  int aRow0, bRow0, N, NT, KS, KC, nT, mT;
+  float* part;
+  __device__ int units() const { return mT * nT * KC; }
+};
+
+struct Smem {
+  uint8_t* sA;
+  uint8_t* sB;
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* tfull;
+  uint64_t* tempty;
+  uint32_t tmem;
+};
+
+// ------------------------------------------------------------ grid barrier
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// all CTAs of one direction group; counter is monotonic (epoch = phases * n)
+__device__ __forceinline__ void grid_bar(unsigned* ctr, unsigned n, unsigned& epoch) {
+  __syncthreads();
+  if(threadIdx.x == 0) {
+    epoch += n;
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    atomicAdd(ctr, 1u);
+    while(ld_acquire(ctr) < epoch)
+      ;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// CTA 0 records (phase kind, start time) pairs
+__device__ __forceinline__ void mark(unsigned long long* prof, int& np, int kind) {
+  if(prof && blockIdx.x == 0 && threadIdx.x == 0 && np < 8190) {
+    prof[2 * np] = (unsigned long long)kind;
+    prof[2 * np + 1] = gtimer();
+    ++np;
+  }
+}
+
+// ------------------------------------------------------------ PROD phase
+
+__device__ void run_prods(const Prod* P, int np, int gi, int gs, const Smem& sm, uint32_t& ring,
+                          uint32_t& ucnt, int64_t b) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int tot = 0;
+  for(int q = 0; q < np; ++q)
+    tot += P[q].units();
+  auto decode = [&](int u, int& q, int& mt, int& nt, int& kc) {
+    q = 0;
+    while(u >= P[q].units()) {
+      u -= P[q].units();
+      ++q;
+    }
+    mt = u % P[q].mT;
+    u /= P[q].mT;
+    nt = u % P[q].nT;
+    kc = u / P[q].nT;
+  };
+  if(warp == 0) {
+    if(lane == 0) {
+      // the operands were written by generic-proxy stores of other CTAs
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      for(int u = gi; u < tot; u += gs) {
+        int q, mt, nt, kc;
+        decode(u, q, mt, nt, kc);
+        const Prod& pr = P[q];
+        const int nkb = pr.KS / 32;
+        for(int kb = 0; kb < nkb; ++kb, ++ring) {
+          const int s = ring % RST;
+          if(ring >= RST)
+            mbar_wait(&sm.empty[s], ((ring / RST) - 1) & 1);
+          mbar_expect_tx(&sm.full[s], A_STAGE + (uint32_t)pr.NT * 128u);
+          const int k0 = kc * pr.KS + kb * 32;
+          tma_load_2d(sm.sA + s * A_STAGE, pr.ma, &sm.full[s], k0, pr.aRow0 + mt * 128);
+          tma_load_2d(sm.sB + s * B_STAGE, pr.mb, &sm.full[s], k0, pr.bRow0 + nt * pr.NT);
+        }
+      }
+    }
+  } else if(warp == 1) {
+    for(int u = gi; u < tot; u += gs) {
+      int q, mt, nt, kc;
+      decode(u, q, mt, nt, kc);
+      const Prod& pr = P[q];
+      if(ucnt > 0)
+        mbar_wait(&sm.tempty[0], (ucnt - 1) & 1);
+      tc_fence_after();
+      // D=f32, A=B=tf32, both K-major, N>>3, M>>4
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(pr.NT >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      const int nkb = pr.KS / 32;
+      for(int kb = 0; kb < nkb; ++kb, ++ring) {
+        const int s = ring % RST;
+        mbar_wait(&sm.full[s], (ring / RST) & 1);
+        tc_fence_after();
+        if(lane == 0) {
+          const uint32_t aBase = smem_u32(sm.sA + s * A_STAGE);
+          const uint32_t bBase = smem_u32(sm.sB + s * B_STAGE);
+#pragma unroll
+          for(int kk = 0; kk < 4; ++kk)
+            mma_tf32(sm.tmem, umma_desc(aBase + kk * 32, 16, 1024, 2),
+                     umma_desc(bBase + kk * 32, 16, 1024, 2), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&sm.empty[s]);
+        }
+        __syncwarp();
+      }
+      if(lane == 0)
+        mma_commit(&sm.tfull[0]);
+      __syncwarp();
+      ++ucnt;
+    }
+  } else if(warp >= 4) {
+    const int qd = warp & 3;  // TMEM lane quarter this warp may read
+    for(int u = gi; u < tot; u += gs) {
+      int q, mt, nt, kc;
+      decode(u, q, mt, nt, kc);
+      const Prod& pr = P[q];
+      mbar_wait(&sm.tfull[0], ucnt & 1);
+      tc_fence_after();
+      const int64_t row = (int64_t)mt * 128 + qd * 32 + lane;
+      for(int c0 = 0; c0 < pr.NT; c0 += 32) {
+        float v[32];
+        tmem_ld32(sm.tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)c0, v);
+        if(row < b) {
+          float4* dst = reinterpret_cast<float4*>(pr.part + ((int64_t)kc * b + row) * pr.N +
+                                                  (int64_t)nt * pr.NT + c0);
+#pragma unroll
+          for(int j = 0; j < 8; ++j)
+            dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if(lane == 0)
+        mbar_arrive(&sm.tempty[0]);
+      ++ucnt;
+    }
+  }
+}
+
+// ------------------------------------------------------------ row phases
+
+template <int NQ>
+__device__ __forceinline__ void block_sums(float (&v)[NQ], float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for(int q = 0; q < NQ; ++q)
+    v[q] = warp_sum(v[q]);
+  __syncthreads();
+  if(lane == 0)
+#pragma unroll
+    for(int q = 0; q < NQ; ++q)
+      red[q * 32 + w] = v[q];
+  __syncthreads();
+#pragma unroll
+  for(int q = 0; q < NQ; ++q) {
+    float t = lane < RT / 32 ? red[q * 32 + lane] : 0.f;
+    v[q] = warp_sum(t);
+  }
+}
+
+__device__ __forceinline__ float sigm(float a) { return 1.f / (1.f + expf(-a)); }
+
+__device__ __forceinline__ float4 ldcg4(const float* p) {
+  return __ldcg(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ float4 ld4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ void st4(float* p, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void add4(float (&acc)[4], const float4& v) {
+  acc[0] += v.x;
+  acc[1] += v.y;
+  acc[2] += v.z;
+  acc[3] += v.w;
+}
+__device__ __forceinline__ void set4(float (&acc)[4], const float4& v) {
+  acc[0] = v.x;
+  acc[1] = v.y;
+  acc[2] = v.z;
+  acc[3] = v.w;
+}
+
+constexpr int GQ = 2;  // float4 groups per thread in the GRU row phase (d <= 2048)
+
+// One GRU block for batch row r at step t (gru_fwd_kernel's arithmetic).
+// hin: the block's state input row; partials summed in k-slice order.  Each
+// thread owns GQ groups of 4 consecutive columns; every global load of the
+// row is issued before the arithmetic (the phase is latency-bound).
+__device__ void gru_row(const KP& p, const mtkc_rnn_dir& D, int k, int64_t t, int64_t r,
+                        const float* hin, const float* partHu, int KCh, const float* partX,
+                        int KCx, const float* xwHoist, float* out, const float* prevRow,
+                        float blendM, bool blend, float* red) {
+  const int64_t b = p.a.b, d = p.a.d, d3 = 3 * d, d4 = d / 4;
+  const mtkc_rnn_block& B = D.blk[k];
+  const bool ln = B.ln[0] != nullptr;
+  const bool hasX = xwHoist != nullptr || partX != nullptr;
+  const int64_t tr = t * b + r;  // time-major row
+  float hz[GQ][4], hr[GQ][4], hh[GQ][4], xz[GQ][4], xr[GQ][4], xx[GQ][4], hv[GQ][4];
+#pragma unroll
+  for(int q = 0; q < GQ; ++q) {
+    const int64_t g = threadIdx.x + (int64_t)q * RT;
+#pragma unroll
+    for(int i = 0; i < 4; ++i)
+      hz[q][i] = hr[q][i] = hh[q][i] = xz[q][i] = xr[q][i] = xx[q][i] = hv[q][i] = 0.f;
+    if(g >= d4)
+      continue;
+    const int64_t j = 4 * g;
+    for(int kc = 0; kc < KCh; ++kc) {
+      const float* pp = partHu + ((int64_t)kc * b + r) * d3 + j;
+      const float4 a0 = ldcg4(pp), a1 = ldcg4(pp + d), a2 = ldcg4(pp + 2 * d);
+      add4(hz[q], a0);
+      add4(hr[q], a1);
+      add4(hh[q], a2);
+    }
+    if(xwHoist) {
+      const float* xw = xwHoist + tr * d3 + j;
+      set4(xz[q], ld4(xw));
+      set4(xr[q], ld4(xw + d));
+      set4(xx[q], ld4(xw + 2 * d));
+    } else if(partX) {
+      for(int kc = 0; kc < KCx; ++kc) {
+        const float* pp = partX + ((int64_t)kc * b + r) * d3 + j;
+        const float4 a0 = ldcg4(pp), a1 = ldcg4(pp + d), a2 = ldcg4(pp + 2 * d);
+        add4(xz[q], a0);
+        add4(xr[q], a1);
+        add4(xx[q], a2);
+      }
+    }
+    set4(hv[q], ldcg4(hin + j));
+  }
+  float az[GQ][4], ar[GQ][4], ax[GQ][4];
+#pragma unroll
+  for(int q = 0; q < GQ; ++q) {
+    const int64_t g = threadIdx.x + (int64_t)q * RT;
+#pragma unroll
+    for(int i = 0; i < 4; ++i)
+      az[q][i] = ar[q][i] = ax[q][i] = 0.f;
+    if(g >= d4)
+      continue;
+    const int64_t j = 4 * g;
+    float* huOut = B.hu + tr * d3 + j;
+    st4(huOut, hz[q]);
+    st4(huOut + d, hr[q]);
+    st4(huOut + 2 * d, hh[q]);
+    if(partX) {
+      float* xo = D.xw2 + tr * d3 + j;
+      st4(xo, xz[q]);
+      st4(xo + d, xr[q]);
+      st4(xo + 2 * d, xx[q]);
+    }
+    const float4 bz = ld4(B.bias[0] + j), br = ld4(B.bias[1] + j);
+    const float bzv[4] = {bz.x, bz.y, bz.z, bz.w}, brv[4] = {br.x, br.y, br.z, br.w};
+#pragma unroll
+    for(int i = 0; i < 4; ++i) {
+      // gruPre: h*U, then + x*W, then + b (graph.cpp:636-644)
+      float z = hz[q][i], rr = hr[q][i];
+      if(hasX) {
+        z = z + xz[q][i];
+        rr = rr + xr[q][i];
+      }
+      az[q][i] = z + bzv[i];
+      ar[q][i] = rr + brv[i];
+      ax[q][i] = hasX ? xx[q][i] : 0.f;
+    }
+  }
+  if(ln) {  // two-pass statistics per gate (tensor.cpp:545-572)
+    float s[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for(int q = 0; q < GQ; ++q)
+#pragma unroll
+      for(int i = 0; i < 4; ++i) {
+        s[0] += az[q][i];
+        s[1] += ar[q][i];
+        s[2] += ax[q][i];
+      }
+    block_sums<3>(s, red);
+    const float mz = s[0] / (float)d, mr = s[1] / (float)d, mx = s[2] / (float)d;
+    float qv[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for(int q = 0; q < GQ; ++q) {
+      if(threadIdx.x + (int64_t)q * RT >= d4)
+        continue;
+#pragma unroll
+      for(int i = 0; i < 4; ++i) {
+        const float cz = az[q][i] - mz, cr = ar[q][i] - mr, cx = ax[q][i] - mx;
+        qv[0] += cz * cz;
+        qv[1] += cr * cr;
+        qv[2] += cx * cx;
+      }
+    }
+    block_sums<3>(qv, red);
+    const float rsz = 1.f / sqrtf(qv[0] / (float)d + p.a.eps);
+    const float rsr = 1.f / sqrtf(qv[1] / (float)d + p.a.eps);
+    const float rsx = 1.f / sqrtf(qv[2] / (float)d + p.a.eps);
+    if(threadIdx.x == 0) {
+      B.lnrs[tr * 3] = rsz;
+      B.lnrs[tr * 3 + 1] = rsr;
+      B.lnrs[tr * 3 + 2] = rsx;
+    }
+#pragma unroll
+    for(int q = 0; q < GQ; ++q) {
+      const int64_t g = threadIdx.x + (int64_t)q * RT;
+      if(g >= d4)
+        continue;
+      const int64_t j = 4 * g;
+      float* xh = B.lnc + tr * d3 + j;
+      const float4 gz = ld4(B.ln[0] + j), bz = ld4(B.ln[1] + j);
+      const float4 gr = ld4(B.ln[2] + j), br = ld4(B.ln[3] + j);
+      const float gzv[4] = {gz.x, gz.y, gz.z, gz.w}, bzv[4] = {bz.x, bz.y, bz.z, bz.w};
+      const float grv[4] = {gr.x, gr.y, gr.z, gr.w}, brv[4] = {br.x, br.y, br.z, br.w};
+      float xhz[4], xhr[4], xhx[4];
+#pragma unroll
+      for(int i = 0; i < 4; ++i) {
+        xhz[i] = (az[q][i] - mz) * rsz;
+        xhr[i] = (ar[q][i] - mr) * rsr;
+        az[q][i] = gzv[i] * xhz[i] + bzv[i];
+        ar[q][i] = grv[i] * xhr[i] + brv[i];
+      }
+      st4(xh, xhz);
+      st4(xh + d, xhr);
+      if(hasX) {
+        const float4 gx = ld4(B.ln[4] + j), bx = ld4(B.ln[5] + j);
+        const float gxv[4] = {gx.x, gx.y, gx.z, gx.w}, bxv[4] = {bx.x, bx.y, bx.z, bx.w};
+#pragma unroll
+        for(int i = 0; i < 4; ++i) {
+          xhx[i] = (ax[q][i] - mx) * rsx;
+          ax[q][i] = gxv[i] * xhx[i] + bxv[i];
+        }
+        st4(xh + 2 * d, xhx);
+      }
+    }
+  }
+  const float notm = 1.f - blendM;
+#pragma unroll
+  for(int q = 0; q < GQ; ++q) {
+    const int64_t g = threadIdx.x + (int64_t)q * RT;
+    if(g >= d4)
+      continue;
+    const int64_t j = 4 * g;
+    const float4 bh = ld4(B.bias[2] + j);
+    const float bhv[4] = {bh.x, bh.y, bh.z, bh.w};
+    float pv[4] = {0.f, 0.f, 0.f, 0.f};
+    if(blend)
+      set4(pv, ldcg4(prevRow + j));
+    float zc[4], rc[4], hc[4], o[4];
+#pragma unroll
+    for(int i = 0; i < 4; ++i) {
+      const float z = sigm(az[q][i]), rr = sigm(ar[q][i]);
+      const float ac = ax[q][i] + (rr * hh[q][i] + bhv[i]);  // graph.cpp:737-738
+      const float ht = tanhf(ac);
+      zc[i] = z;
+      rc[i] = rr;
+      hc[i] = ht;
+      const float hn = (1.f - z) * ht + z * hv[q][i];
+      o[i] = blend ? hn * blendM + pv[i] * notm : hn;  // a*m + b*(1-m)
+    }
+    float* cache = B.cache + tr * d3 + j;
+    st4(cache, zc);
+    st4(cache + d, rc);
+    st4(cache + 2 * d, hc);
+    st4(out + j, o);
+  }
+}
+
+// Bahdanau attention for batch row r at step t (bahdanau_score_kernel +
+// bahdanau_ctx_kernel arithmetic): wq from the partials, scores per
+// position (one warp each, float4 lanes, the position's loads in flight
+// together), masked softmax, context (float4 columns, positions unrolled).
+constexpr int AQ = MAXA / 128;  // float4 groups per lane over the attention width
+
+__device__ void att_row(const KP& p, int64_t t, int64_t r, float* sW, float* sE, float* sP) {
+  const mtkc_rnn_scan_args& a = p.a;
+  const int64_t b = a.b, A = a.a, S = a.S, KD = a.kd, A4 = A / 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tr = t * b + r;
+  for(int64_t c4 = threadIdx.x; c4 < A4; c4 += RT) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    for(int kc = 0; kc < p.KCq; ++kc)
+      add4(v, ldcg4(p.partQ + ((int64_t)kc * b + r) * A + 4 * c4));
+    st4(sW + 4 * c4, v);
+    st4(a.wq + tr * A + 4 * c4, v);
+  }
+  __syncthreads();
+  const bool ln = a.attLnG != nullptr;
+  const int nq = (int)((A4 + 31) / 32);  // groups per lane (<= AQ)
+  for(int64_t j = warp; j < S; j += RT / 32) {
+    const int64_t rj = r * S + j;    // row of uk / keys
+    const int64_t trj = tr * S + j;  // row of the per-step caches
+    const float* uk = a.uk + rj * A;
+    float x[AQ][4];
+#pragma unroll
+    for(int q = 0; q < AQ; ++q) {
+      const int64_t c4 = lane + 32 * q;
+      if(q < nq && c4 < A4) {
+        const float4 u = ld4(uk + 4 * c4);
+        const float4 w = *reinterpret_cast<const float4*>(sW + 4 * c4);
+        x[q][0] = w.x + u.x;
+        x[q][1] = w.y + u.y;
+        x[q][2] = w.z + u.z;
+        x[q][3] = w.w + u.w;
+      } else {
+        x[q][0] = x[q][1] = x[q][2] = x[q][3] = 0.f;
+      }
+    }
+    float mu = 0.f, rs = 0.f;
+    if(ln) {
+      float s1 = 0.f;
+#pragma unroll
+      for(int q = 0; q < AQ; ++q)
+        s1 += (x[q][0] + x[q][1]) + (x[q][2] + x[q][3]);
+      mu = warp_sum(s1) / (float)A;
+      float s2 = 0.f;
+#pragma unroll
+      for(int q = 0; q < AQ; ++q) {
+        const int64_t c4 = lane + 32 * q;
+        if(q < nq && c4 < A4)
+#pragma unroll
+          for(int i = 0; i < 4; ++i) {
+            const float dd = x[q][i] - mu;
+            s2 += dd * dd;
+          }
+      }
+      rs = 1.f / sqrtf(warp_sum(s2) / (float)A + a.eps);
+      if(lane == 0)
+        a.attLnrs[trj] = rs;
+    }
+    float acc = 0.f;
+#pragma unroll
+    for(int q = 0; q < AQ; ++q) {
+      const int64_t c4 = lane + 32 * q;
+      if(q >= nq || c4 >= A4)
+        continue;
+      const int64_t c = 4 * c4;
+      if(ln) {
+        float xh[4];
+        const float4 g = ld4(a.attLnG + c), bb = ld4(a.attLnB + c);
+        const float gv[4] = {g.x, g.y, g.z, g.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+        for(int i = 0; i < 4; ++i) {
+          xh[i] = (x[q][i] - mu) * rs;
+          x[q][i] = gv[i] * xh[i] + bv[i];
+        }
+        st4(a.attLnx + trj * A + c, xh);
+      }
+      const float4 vv = ld4(a.attV + c);
+      const float vvv[4] = {vv.x, vv.y, vv.z, vv.w};
+      float th[4];
+#pragma unroll
+      for(int i = 0; i < 4; ++i) {
+        th[i] = tanhf(x[q][i]);
+        acc += th[i] * vvv[i];
+      }
+      st4(a.attT + trj * A + c, th);
+    }
+    acc = warp_sum(acc);
+    if(lane == 0)
+      sE[j] = acc;
+  }
+  __syncthreads();
+  if(warp == 0) {  // masked softmax over positions (tensor.cpp:393-440)
+    const float* m = a.attMask ? a.attMask + r * S : nullptr;
+    float mx = -INFINITY;
+    int any = 0;
+    for(int64_t j = lane; j < S; j += 32)
+      if(!m || m[j] != 0.f) {
+        mx = fmaxf(mx, sE[j]);
+        any = 1;
+      }
+    mx = warp_max(mx);
+    any = __any_sync(0xffffffffu, any);
+    if(!any && lane == 0 && a.flags)
+      atomicOr(a.flags, MTKC_FLAG_MASKED_ROW);
+    float sum = 0.f;
+    for(int64_t j = lane; j < S; j += 32)
+      if(!m || m[j] != 0.f)
+        sum += expf(sE[j] - mx);
+    sum = warp_sum(sum);
+    for(int64_t j = lane; j < S; j += 32) {
+      const float y = (any && (!m || m[j] != 0.f)) ? expf(sE[j] - mx) / sum : 0.f;
+      sP[j] = y;
+      a.attWts[tr * S + j] = y;
+    }
+  }
+  __syncthreads();
+  // context: sum over positions in ascending order, 4 positions' loads in flight
+  const float* keys = a.keys + r * S * KD;
+  for(int64_t k4 = threadIdx.x; k4 < KD / 4; k4 += RT) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    int64_t j = 0;
+    for(; j + 4 <= S; j += 4) {
+      float4 kv[4];
+#pragma unroll
+      for(int u = 0; u < 4; ++u)
+        kv[u] = ld4(keys + (j + u) * KD + 4 * k4);
+#pragma unroll
+      for(int u = 0; u < 4; ++u) {
+        const float w = sP[j + u];
+        acc[0] += w * kv[u].x;
+        acc[1] += w * kv[u].y;
+        acc[2] += w * kv[u].z;
+        acc[3] += w * kv[u].w;
+      }
+    }
+    for(; j < S; ++j) {
+      const float4 kv = ld4(keys + j * KD + 4 * k4);
+      const float w = sP[j];
+      acc[0] += w * kv.x;
+      acc[1] += w * kv.y;
+      acc[2] += w * kv.z;
+      acc[3] += w * kv.w;
+    }
+    st4(a.ctx + tr * KD + 4 * k4, acc);
+  }
+  __syncthreads();  // sW / sE / sP are reused by the next row
+}
+
+// ------------------------------------------------------------ kernel
+
+constexpr size_t SMEM_BYTES = 1024 + RST * (size_t)(A_STAGE + B_STAGE) +
+                              (MAXA + 2 * MAXS + 6 * 32) * sizeof(float) + 256;
+
+__global__ void __launch_bounds__(RT, 1)
+    rnn_scan_fwd_kernel(const __grid_constant__ Maps maps, const __grid_constant__ KP p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  Smem sm;
+  sm.sA = base;
+  sm.sB = base + RST * A_STAGE;
+  float* sW = (float*)(sm.sB + RST * B_STAGE);
+  float* sE = sW + MAXA;
+  float* sP = sE + MAXS;
+  float* red = sP + MAXS;
+  uint64_t* bars = (uint64_t*)(red + 6 * 32);
+  sm.full = bars;
+  sm.empty = bars + RST;
+  sm.tfull = bars + 2 * RST;
+  sm.tempty = bars + 2 * RST + 1;
+  uint32_t* tmemSlot = (uint32_t*)(bars + 2 * RST + 2);
+  const int warp = threadIdx.x >> 5;
+  const mtkc_rnn_scan_args& a = p.a;
+
+  if(threadIdx.x == 0) {
+    for(int s = 0; s < RST; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    mbar_init(&sm.tfull[0], 1);
+    mbar_init(&sm.tempty[0], 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for(int q = 0; q < a.ndir; ++q) {
+      prefetch_tmap(&maps.hh[q]);
+      prefetch_tmap(&maps.sout[q]);
+      prefetch_tmap(&maps.ut[q]);
+    }
+    if(a.has_att) {
+      prefetch_tmap(&maps.ctx);
+      prefetch_tmap(&maps.w2t);
+      prefetch_tmap(&maps.watt);
+    }
+  }
+  if(warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmemSlot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  sm.tmem = *tmemSlot;
+
+  const int gs = gridDim.x / a.ndir;
+  const int dir = blockIdx.x / gs, gi = blockIdx.x % gs;
+  const mtkc_rnn_dir& D = a.dir[dir];
+  unsigned* ctr = p.ctr + dir;
+  unsigned epoch = 0;
+  uint32_t ring = 0, ucnt = 0;
+  int npf = 0;
+  const int64_t b = a.b, T = a.T, d = a.d, d3 = 3 * d;
+  const int K = D.nblocks;
+  const int mT = (int)((b + 127) / 128);
+
+  for(int64_t i = 0; i < T; ++i) {
+    const int64_t t = D.reverse ? T - 1 - i : i;
+    const int64_t hp = D.reverse ? t + 1 : t, hs = D.reverse ? t : t + 1;
+    for(int k = 0; k < K; ++k) {
+      const bool attIn = a.has_att && k == 1;
+      Prod P[2];
+      int np = 1;
+      P[0].ma = k == 0 ? &maps.hh[dir] : &maps.sout[dir];
+      P[0].mb = &maps.ut[dir];
+      P[0].aRow0 = (int)(k == 0 ? hp * b : (int64_t)(k - 1) * T * b + t * b);
+      P[0].bRow0 = (int)(k * d3);
+      P[0].N = (int)d3;
+      P[0].NT = NTH;
+      P[0].KC = p.KCh;
+      P[0].KS = (int)(d / p.KCh);
+      P[0].nT = (int)(d3 / NTH);
+      P[0].mT = mT;
+      P[0].part = p.partHu[dir];
+      if(attIn) {
+        P[1].ma = &maps.ctx;
+        P[1].mb = &maps.w2t;
+        P[1].aRow0 = (int)(t * b);
+        P[1].bRow0 = 0;
+        P[1].N = (int)d3;
+        P[1].NT = NTH;
+        P[1].KC = p.KCx;
+        P[1].KS = (int)(a.kd / p.KCx);
+        P[1].nT = (int)(d3 / NTH);
+        P[1].mT = mT;
+        P[1].part = p.partX;
+        np = 2;
+      }
+      mark(p.prof, npf, attIn ? 4 : 0);
+      run_prods(P, np, gi, gs, sm, ring, ucnt, b);
+      mark(p.prof, npf, 5);
+      grid_bar(ctr, gs, epoch);
+      mark(p.prof, npf, 1);
+      const bool last = k == K - 1;
+      for(int64_t r = gi; r < b; r += gs) {
+        const float* hin = k == 0 ? D.HH + (hp * b + r) * d : D.sout + (((int64_t)(k - 1) * T + t) * b + r) * d;
+        float* out = last ? D.HH + (hs * b + r) * d : D.sout + (((int64_t)k * T + t) * b + r) * d;
+        const bool blend = last && a.maskT != nullptr;
+        const float m = blend ? a.maskT[t * b + r] : 1.f;
+        gru_row(p, D, k, t, r, hin, p.partHu[dir], p.KCh, attIn ? p.partX : nullptr, p.KCx,
+                k == 0 ? D.xw1 : nullptr, out, D.HH + (hp * b + r) * d, m, blend, red);
+      }
+      mark(p.prof, npf, 5);
+      grid_bar(ctr, gs, epoch);
+      if(a.has_att && k == 0) {
+        Prod Q;
+        Q.ma = &maps.sout[dir];
+        Q.mb = &maps.watt;
+        Q.aRow0 = (int)(t * b);  // block 1's output (sout block 0)
+        Q.bRow0 = 0;
+        Q.N = (int)a.a;
+        Q.NT = p.NTq;
+        Q.KC = p.KCq;
+        Q.KS = (int)(d / p.KCq);
+        Q.nT = (int)(a.a / p.NTq);
+        Q.mT = mT;
+        Q.part = p.partQ;
+        mark(p.prof, npf, 2);
+        run_prods(&Q, 1, gi, gs, sm, ring, ucnt, b);
+        mark(p.prof, npf, 5);
+        grid_bar(ctr, gs, epoch);
+        mark(p.prof, npf, 3);
+        for(int64_t r = gi; r < b; r += gs)
+          att_row(p, t, r, sW, sE, sP);
+        mark(p.prof, npf, 5);
+        grid_bar(ctr, gs, epoch);
+      }
+    }
+  }
+  mark(p.prof, npf, 6);
+  tc_fence_before();
+  __syncthreads();
+  if(warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem),
+                 "r"(TMEM_COLS));
+}
+
+// weight transposes into the workspace: dst[c * rows + r] = src[r * cols + c]
+struct TJob {
+  const float* src;
+  float* dst;
+  int rows, cols;
+};
+constexpr int MAXJOBS = 2 * 3 * MTKC_RNN_MAX_BLOCKS + 4;
+struct TJobs {
+  TJob j[MAXJOBS];
+  int n;
+};
+
+__global__ void transpose_jobs_kernel(const __grid_constant__ TJobs jobs) {
+  MTKC_PDL_ENTRY();
+  __shared__ float tile[32][33];
+  const TJob& J = jobs.j[blockIdx.z];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  if(r0 >= J.rows || c0 >= J.cols)
+    return;
+  for(int y = threadIdx.y; y < 32; y += 8) {
+    const int r = r0 + y, c = c0 + threadIdx.x;
+    if(r < J.rows && c < J.cols)
+      tile[y][threadIdx.x] = J.src[(int64_t)r * J.cols + c];
+  }
+  __syncthreads();
+  for(int y = threadIdx.y; y < 32; y += 8) {
+    const int c = c0 + y, r = r0 + threadIdx.x;
+    if(r < J.rows && c < J.cols)
+      J.dst[(int64_t)c * J.rows + r] = tile[threadIdx.x][y];
+  }
+}
+
+// ------------------------------------------------------------ host side
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    if(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) ==
+           cudaSuccess &&
+       r == cudaDriverEntryPointSuccess)
+      fn = (EncodeFn)q;
+  });
+  return fn;
+}
+
+bool tf32_round() {
+  const char* e = getenv("MTK_TMA_TF32");
+  return !(e && e[0] == '0');
+}
+
+// K-major operand [rows x K] (row-major, ld = K), box 32 x boxRows, SWIZZLE_128B
+bool kmap(CUtensorMap* m, const float* p, int64_t K, int64_t rows, uint32_t boxRows) {
+  EncodeFn fn = encode_fn();
+  if(!fn)
+    return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 4};
+  cuuint32_t box[2] = {32, boxRows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, tf32_round() ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+            2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// largest divisor kc of nkb (k-blocks) with kc <= target
+int pick_kc(int nkb, int target) {
+  target = std::max(1, std::min(target, nkb));
+  for(int kc = target; kc >= 1; --kc)
+    if(nkb % kc == 0)
+      return kc;
+  return 1;
+}
+
+struct Plan {
+  int G, gs, KCh, KCx, KCq, NTq;
+  size_t offUT[2], offW2T, offWattT, offPH[2], offPX, offPQ, offCtr, total;
+};
+
+int grid_size() {
+  static int sms = 0;
+  if(!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if(sms <= 0)
+      sms = 148;
+  }
+  return sms;
+}
+
+Plan make_plan(const mtkc_rnn_scan_args* a) {
+  Plan P{};
+  const int64_t b = a->b, d = a->d, d3 = 3 * d;
+  P.G = grid_size();
+  P.G -= P.G % a->ndir;
+  P.gs = P.G / a->ndir;
+  const int mT = (int)((b + 127) / 128);
+  const int nTh = (int)(d3 / NTH);
+  P.KCh = pick_kc((int)(d / 32), P.gs / std::max(1, nTh * mT));
+  P.KCx = a->has_att ? pick_kc((int)(a->kd / 32), P.gs / std::max(1, nTh * mT)) : 1;
+  P.NTq = a->has_att ? (a->a % 64 == 0 ? 64 : 32) : 32;
+  P.KCq = a->has_att ? pick_kc((int)(d / 32), P.gs / std::max<int>(1, (int)(a->a / P.NTq) * mT))
+                     : 1;
+  size_t off = 0;
+  auto take = [&](size_t floats) {
+    size_t o = off;
+    off += (floats * sizeof(float) + 255) / 256 * 256;
+    return o;
+  };
+  for(int q = 0; q < a->ndir; ++q)
+    P.offUT[q] = take((size_t)a->dir[q].nblocks * d3 * d);
+  if(a->has_att) {
+    P.offW2T = take((size_t)d3 * a->kd);
+    P.offWattT = take((size_t)a->a * d);
+    P.offPX = take((size_t)P.KCx * b * d3);
+    P.offPQ = take((size_t)P.KCq * b * a->a);
+  }
+  for(int q = 0; q < a->ndir; ++q)
+    P.offPH[q] = take((size_t)P.KCh * b * d3);
+  P.offCtr = take(64);
+  P.total = off;
+  return P;
+}
+
+bool supported(const mtkc_rnn_scan_args* a) {
+  if(a->b <= 0 || a->T <= 0 || a->d <= 0 || a->d % 32 || a->d > 2048)
+    return false;
+  if(a->ndir < 1 || a->ndir > 2 || (a->ndir == 2 && a->has_att))
+    return false;
+  for(int q = 0; q < a->ndir; ++q) {
+    const mtkc_rnn_dir& D = a->dir[q];
+    if(D.nblocks < 1 || D.nblocks > MTKC_RNN_MAX_BLOCKS)
+      return false;
+    if(D.nblocks > 1 && !D.sout)
+      return false;
+  }
+  if(a->has_att) {
+    if(a->dir[0].nblocks < 2 || a->kd % 32 || a->a % 32 || a->a > MAXA || a->S > MAXS ||
+       a->S < 1)
+      return false;
+  }
+  // rows of the A boxes are addressed with 32-bit coordinates
+  if((a->T + 1) * a->b * (int64_t)MTKC_RNN_MAX_BLOCKS > (1ll << 31))
+    return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mtkc_rnn_scan_supported(const mtkc_rnn_scan_args* a) { return supported(a) ? 1 : 0; }
+
+size_t mtkc_rnn_scan_workspace(const mtkc_rnn_scan_args* a) {
+  if(!supported(a))
+    return 0;
+  return make_plan(a).total;
+}
+
+int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream) {
+  if(!supported(a))
+    return fail(MTKC_CONTRACT, "rnn scan: dimensions not supported by the persistent path");
+  const Plan P = make_plan(a);
+  if(!a->workspace || a->workspace_bytes < P.total)
+    return fail(MTKC_CONTRACT, "rnn scan: workspace too small");
+  cudaStream_t st = S(stream);
+  uint8_t* ws = (uint8_t*)a->workspace;
+  const int64_t b = a->b, T = a->T, d = a->d, d3 = 3 * d;
+  ProfScope prof(st, "rnn_scan", 0.0);
+
+  // K-major weight copies (weights are constant within the step)
+  TJobs jobs{};
+  for(int q = 0; q < a->ndir; ++q) {
+    const mtkc_rnn_dir& D = a->dir[q];
+    float* ut = (float*)(ws + P.offUT[q]);
+    for(int k = 0; k < D.nblocks; ++k)
+      for(int g = 0; g < 3; ++g)
+        jobs.j[jobs.n++] = TJob{D.blk[k].U[g], ut + ((int64_t)k * d3 + g * d) * d, (int)d, (int)d};
+  }
+  if(a->has_att) {
+    float* w2t = (float*)(ws + P.offW2T);
+    for(int g = 0; g < 3; ++g)
+      jobs.j[jobs.n++] = TJob{a->dir[0].blk[1].W[g], w2t + (int64_t)g * d * a->kd, (int)a->kd, (int)d};
+    jobs.j[jobs.n++] = TJob{a->attW, (float*)(ws + P.offWattT), (int)d, (int)a->a};
+  }
+  {
+    const int mx = (int)std::max<int64_t>(std::max<int64_t>(d, a->has_att ? a->kd : 0),
+                                          a->has_att ? a->a : 0);
+    dim3 grid((unsigned)((mx + 31) / 32), (unsigned)((mx + 31) / 32), (unsigned)jobs.n);
+    ::mtkc::launch(transpose_jobs_kernel, grid, dim3(32, 8), 0, st, jobs);
+    MTKC_POST_LAUNCH("transpose_jobs_kernel");
+  }
+  if(cudaError_t e = cudaMemsetAsync(ws + P.offCtr, 0, 256, st))
+    return cuda_status(e, "rnn scan counters");
+
+  Maps maps;
+  memset(&maps, 0, sizeof(maps));
+  bool ok = true;
+  for(int q = 0; q < a->ndir; ++q) {
+    const mtkc_rnn_dir& D = a->dir[q];
+    ok = ok && kmap(&maps.hh[q], D.HH, d, (T + 1) * b, 128);
+    ok = ok && kmap(&maps.sout[q], D.nblocks > 1 ? D.sout : D.HH, d,
+                    D.nblocks > 1 ? (int64_t)(D.nblocks - 1) * T * b : (T + 1) * b, 128);
+    ok = ok && kmap(&maps.ut[q], (const float*)(ws + P.offUT[q]), d, (int64_t)D.nblocks * d3, NTH);
+  }
+  if(a->has_att) {
+    ok = ok && kmap(&maps.ctx, a->ctx, a->kd, T * b, 128);
+    ok = ok && kmap(&maps.w2t, (const float*)(ws + P.offW2T), a->kd, d3, NTH);
+    ok = ok && kmap(&maps.watt, (const float*)(ws + P.offWattT), d, a->a, (uint32_t)P.NTq);
+  }
+  if(!ok)
+    return fail(MTKC_CUDA, "rnn scan: tensor map encoding failed");
+
+  KP kp;
+  memset(&kp, 0, sizeof(kp));
+  kp.a = *a;
+  for(int q = 0; q < a->ndir; ++q)
+    kp.partHu[q] = (float*)(ws + P.offPH[q]);
+  kp.partX = a->has_att ? (float*)(ws + P.offPX) : nullptr;
+  kp.partQ = a->has_att ? (float*)(ws + P.offPQ) : nullptr;
+  kp.ctr = (unsigned*)(ws + P.offCtr);
+  kp.KCh = P.KCh;
+  kp.KCx = P.KCx;
+  kp.KCq = P.KCq;
+  kp.NTq = P.NTq;
+
+  static bool attr = false;
+  if(!attr) {
+    cudaError_t e = cudaFuncSetAttribute(rnn_scan_fwd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM_BYTES);
+    if(e != cudaSuccess)
+      return cuda_status(e, "rnn scan smem attribute");
+    attr = true;
+  }
+  // cooperative launch: every CTA resident (the grid barriers need it); no
+  // programmatic serialisation, so no dependent grid can take SMs first
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)P.G);
+  cfg.blockDim = dim3(RT);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeCooperative;
+  attrs[0].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  static unsigned long long* profBuf = nullptr;
+  const bool profOn = getenv("MTK_RNN_PROF") != nullptr;
+  if(profOn) {
+    if(!profBuf)
+      cudaMalloc(&profBuf, 8192 * 2 * sizeof(unsigned long long));
+    cudaMemsetAsync(profBuf, 0, 8192 * 2 * sizeof(unsigned long long), st);
+    kp.prof = profBuf;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, rnn_scan_fwd_kernel, maps, kp);
+  if(e != cudaSuccess)
+    return cuda_status(e, "rnn_scan_fwd_kernel");
+  count_launch();
+  if(profOn) {  // phase durations of CTA 0 (kind: 0 PROD h*U, 4 PROD h*U + ctx*W, 1 PW,
+              // 2 PROD query, 3 ATT, 5 barrier)
+    std::vector<unsigned long long> h(8192 * 2);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), profBuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    double sum[8] = {0}, cnt[8] = {0};
+    for(int i = 0; i + 1 < 8192 && h[2 * i + 3]; ++i) {
+      int k = (int)h[2 * i];
+      sum[k] += (double)(h[2 * i + 3] - h[2 * i + 1]);
+      cnt[k] += 1;
+    }
+    const char* nm[8] = {"prod-hU", "pw", "prod-q", "att", "prod-hU+ctxW", "barrier", "end", "-"};
+    fprintf(stderr, "[rnn prof] ndir %d b %lld T %lld:", a->ndir, (long long)b, (long long)T);
+    for(int k = 0; k < 6; ++k)
+      if(cnt[k] > 0)
+        fprintf(stderr, " %s %.0f x %.2f us", nm[k], cnt[k], sum[k] / cnt[k] / 1e3);
+    fprintf(stderr, "\n");
+  }
+  return MTKC_OK;
+}
+
+}  // extern "C"
