@@ -459,6 +459,10 @@ typedef struct mtkc_rnn_block {
   float* cache;          /* [T*b x 3d] out: z, r, h~ */
   float* lnc;            /* [T*b x 3d] out (LN only) */
   float* lnrs;           /* [T*b x 3]  out (LN only) */
+  /* backward (mtkc_rnn_scan_backward) */
+  float* dGx;            /* [T*b x 3d] out: dpz | dpr | dax (blocks with an input), or NULL */
+  float* dac;            /* [T*b x d] out: candidate pre-activation gradient */
+  float* lnp;            /* [T*b x 6d] out: LN gain/bias partials (LN only) */
 } mtkc_rnn_block;
 
 typedef struct mtkc_rnn_dir {
@@ -469,6 +473,11 @@ typedef struct mtkc_rnn_dir {
   float* sout;           /* [(nblocks-1)*T*b x d] outputs of blocks 1..K-1 (block k at k*T*b) */
   const float* xw1;      /* [T*b x 3d] hoisted input product of block 1, or NULL */
   float* xw2;            /* [T*b x 3d] out: per-step ctx*W of block 2 (attention) */
+  /* backward */
+  float* GH;             /* [(T+1)*b x d] state-slot gradients: pre-filled with the output
+                            gradients (initial-state slot zero); the initial slot receives
+                            the initial-state gradient */
+  float* dG;             /* [nblocks*T*b x 3d] out: dpz | dpr | duh per block (block k at k*T*b) */
 } mtkc_rnn_dir;
 
 typedef struct mtkc_rnn_scan_args {
@@ -493,6 +502,13 @@ typedef struct mtkc_rnn_scan_args {
   float* attLnx;         /* [T*b*S x a] out (LN only) */
   float* attLnrs;        /* [T*b x S] out (LN only) */
   float* ctx;            /* [T*b x kd] out */
+  /* attention backward */
+  const float* ctxGrad;  /* [T*b x kd] gradient reaching the contexts from the readout, or NULL */
+  float* dctx;           /* [T*b x kd] out: total context gradient per step */
+  float* dwq;            /* [T*b x a] out */
+  float* guk;            /* [b x S x a] gradient of uk (written, or added when acc_uk) */
+  int acc_uk;
+  float* vpart;          /* [3][T*b x a] out: v, LN gain, LN bias partials per row */
   int* flags;
   float* workspace;
   size_t workspace_bytes;
@@ -502,6 +518,13 @@ typedef struct mtkc_rnn_scan_args {
 int mtkc_rnn_scan_supported(const mtkc_rnn_scan_args* a);
 size_t mtkc_rnn_scan_workspace(const mtkc_rnn_scan_args* a);
 int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream);
+/* reverse sweep (gru_bwd_kernel / bahdanau backward arithmetic per block and
+ * step; the state-gradient products dG*[Uz|Ur|Uh]^T, dGx*W^T and dwq*attW^T
+ * as K-split tcgen05 phases).  Weight / bias / LN gradients are NOT formed:
+ * the caller sums them over all b*T rows from dG, dGx, dac, lnp, dwq, vpart
+ * (and the key gradient from attWts and dctx) after the sweep. */
+size_t mtkc_rnn_scan_bwd_workspace(const mtkc_rnn_scan_args* a);
+int mtkc_rnn_scan_backward(const mtkc_rnn_scan_args* a, void* stream);
 
 /* ======================================================================== */
 /* Bahdanau MLP attention core (BahdanauAttention::apply layers.cpp:59-79),  */

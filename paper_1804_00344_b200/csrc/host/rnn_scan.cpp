@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "mtk/device.h"
 #include "mtk/graph.h"
@@ -173,7 +174,12 @@ struct Dir {
   Tensor GH;  // [(T+1)*b x d] gradient of HH
   struct Grads {
     Tensor dpz, dpr, duh, dac, dax, lnp;
+    Tensor dGx;  // persistent layout: [dpz | dpr | dax] rows (blocks with an input)
   };
+  // persistent backward layout: [dpz | dpr | duh] rows of every block in one
+  // buffer (block k at k*T*b rows), the A operand of the in-kernel products
+  bool inter = false;
+  Tensor dGall;
   std::vector<Grads> G;       // per block, time-major gate gradients
   std::vector<Tensor> ds;     // gradients of the intermediate block outputs of a step
   Tensor dctx, dwq, vpart;
@@ -447,11 +453,78 @@ bool forwardPersistent(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X)
   return true;
 }
 
+// the persistent backward applies to this scan (checked before the
+// gradient buffers are laid out for it)
+bool persistBwdEligible(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X) {
+  if(!persistEnabled() || (X.att && X.A.kd > 2048))
+    return false;
+  mtkc_rnn_scan_args a = scanArgs(g, n, X);
+  return mtkc_rnn_scan_supported(&a) != 0;
+}
+
+void backwardPersistent(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X) {
+  mtkc_rnn_scan_args a = scanArgs(g, n, X);
+  for(int q = 0; q < X.ndir; ++q) {
+    Dir& D = X.dir[q];
+    mtkc_rnn_dir& o = a.dir[q];
+    o.GH = D.GH.dev();
+    o.dG = D.dGall.dev();
+    for(size_t k = 0; k < D.blocks.size(); ++k) {
+      Dir::Grads& gq = D.G[k];
+      o.blk[k].dGx = gq.dGx.empty() ? nullptr : gq.dGx.dev();
+      o.blk[k].dac = gq.dac.dev();
+      o.blk[k].lnp = gq.lnp.empty() ? nullptr : gq.lnp.dev();
+    }
+  }
+  if(X.att) {
+    Dir& D = X.dir[0];
+    a.ctxGrad = D.ctxGrad;
+    a.dctx = D.dctx.dev();
+    a.dwq = D.dwq.dev();
+    a.guk = D.guk.ptr;
+    a.acc_uk = D.guk.accumulate;
+    a.vpart = D.vpart.dev();
+  }
+  Device& dev = Device::get();
+  const size_t need = mtkc_rnn_scan_bwd_workspace(&a);
+  const size_t total = (size_t)1 << 30;
+  if(need == 0 || need > total / 2)
+    throw ContractError("rnn scan: persistent backward not applicable (workspace " +
+                        std::to_string(need) + " B)");
+  float* base = dev.scratch(total);
+  a.workspace = base + (total / 2) / sizeof(float);
+  a.workspace_bytes = total / 2;
+  MTKC(mtkc_rnn_scan_backward(&a, dev.stream()));
+}
+
 void backwardBegin(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& D,
-                   const float* ctxGrad) {
+                   const float* ctxGrad, bool inter = false) {
   const int64_t b = X.b, T = X.T, d = X.d, K = (int64_t)D.blocks.size();
   const int64_t TB = T * b;
   D.G.assign((size_t)K, Dir::Grads());
+  D.inter = inter;
+  if(inter) {  // persistent kernel layout (mtkc_rnn_scan_backward)
+    D.dGall = g.allocTensor(Shape({K * TB, 3 * d}));
+    for(int64_t k = 0; k < K; ++k) {
+      Dir::Grads& q = D.G[(size_t)k];
+      const bool hasX = D.blocks[(size_t)k].in > 0;
+      q.dac = g.allocTensor(Shape({TB, d}));
+      if(hasX)
+        q.dGx = g.allocTensor(Shape({TB, 3 * d}));
+      if(X.ln)
+        q.lnp = g.allocTensor(Shape({TB, 6 * d}));
+    }
+    D.ctxGrad = ctxGrad;
+    if(X.att) {
+      const AttSlots& A = X.A;
+      D.dctx = g.allocTensor(Shape({TB, A.kd}));
+      D.dwq = g.allocTensor(Shape({TB, A.a}));
+      D.vpart = g.allocTensor(Shape({A.lnG >= 0 ? 3 : 1, TB, A.a}));
+      D.guk = g.gradDst(n.inputs[(size_t)A.uk]);
+      D.gkeys = g.gradDst(n.inputs[(size_t)A.keys]);
+    }
+    return;
+  }
   for(int64_t k = 0; k < K; ++k) {
     const BlockSlots& Bk = D.blocks[(size_t)k];
     const bool hasX = Bk.in > 0;
@@ -614,7 +687,11 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
     const BlockSlots& Bk = D.blocks[(size_t)k];
     Dir::Grads& q = D.G[(size_t)k];
     const float* sIn = k == 0 ? HH + (D.reverse ? b * d : 0) : D.sout(k - 1);
-    const float* dp[3] = {q.dpz.devc(), q.dpr.devc(), q.duh.devc()};
+    const bool inter = D.inter;
+    const int64_t ld = inter ? 3 * d : d;  // row stride of the gate gradients
+    const float* dGk = inter ? D.dGall.devc() + k * TB * 3 * d : nullptr;
+    const float* dp[3] = {inter ? dGk : q.dpz.devc(), inter ? dGk + d : q.dpr.devc(),
+                          inter ? dGk + 2 * d : q.duh.devc()};
     {  // dU += S_in^T [dz|dr|duh]  (graph.cpp:773, 803)
       const float* As[3] = {sIn, sIn, sIn};
       float* C[3];
@@ -624,9 +701,9 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
         C[j] = dst.ptr;
         beta[j] = dst.accumulate ? 1.f : 0.f;
       }
-      gemm3(c, false, d, d, TB, As, d, true, dp, d, false, C, d, beta);
+      gemm3(c, false, d, d, TB, As, d, true, dp, ld, false, C, d, beta);
     }
-    {  // biases (graph.cpp:771, 801): one grouped column sum
+    if(!inter) {  // biases (graph.cpp:771, 801): one grouped column sum
       ExpressionGraph::GradDst gz = g.gradDst(n.inputs[(size_t)Bk.b[0]]),
                                gr = g.gradDst(n.inputs[(size_t)Bk.b[1]]),
                                gb = g.gradDst(n.inputs[(size_t)Bk.b[2]]);
@@ -634,8 +711,21 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
       const float* ins[3] = {q.dpz.devc(), q.dpr.devc(), q.dac.devc()};
       const int acc[3] = {gz.accumulate, gr.accumulate, gb.accumulate};
       MTKC(mtkc_colsum_group(outs, ins, acc, 3, TB, d, c.cs, c.csBytes, c.st));
+    } else {  // sum over the [dpz|dpr|duh] rows, then bz, br slices; bh from dac
+      Tensor sums = g.allocTensor(Shape({3 * d}));
+      colsum(c, ExpressionGraph::GradDst{sums.dev(), 0, nullptr, nullptr}, dGk, TB, 3 * d);
+      for(int j = 0; j < 2; ++j) {
+        auto dst = g.gradDst(n.inputs[(size_t)Bk.b[j]]);
+        if(dst.accumulate)
+          MTKC(mtkc_axpy(dst.ptr, sums.devc() + j * d, 1.f, d, c.st));
+        else
+          MTKC(mtkc_memcpy_d2d(dst.ptr, sums.devc() + j * d, (size_t)d * sizeof(float), c.st));
+      }
+      colsum(c, g.gradDst(n.inputs[(size_t)Bk.b[2]]), q.dac.devc(), TB, d);
     }
-    const float* dx[3] = {q.dpz.devc(), q.dpr.devc(), q.dax.devc()};
+    const float* dGxk = inter && !q.dGx.empty() ? q.dGx.devc() : nullptr;
+    const float* dx[3] = {inter ? dGxk : q.dpz.devc(), inter ? dGxk + d : q.dpr.devc(),
+                          inter ? dGxk + 2 * d : q.dax.devc()};
     const float* xin = nullptr;
     int64_t inDim = 0;
     if(k == 0 && Bk.in > 0) {
@@ -654,14 +744,14 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
         C[j] = dst.ptr;
         beta[j] = dst.accumulate ? 1.f : 0.f;
       }
-      gemm3(c, false, inDim, d, TB, Ax, inDim, true, dx, d, false, C, d, beta);
+      gemm3(c, false, inDim, d, TB, Ax, inDim, true, dx, ld, false, C, d, beta);
       if(k == 0 && dXt) {  // dX (+)= sum_k [dz|dr|dx]_k W_k^T
         const float* Bw[3] = {g.valPtr(n.inputs[(size_t)Bk.W[0]]),
                               g.valPtr(n.inputs[(size_t)Bk.W[1]]),
                               g.valPtr(n.inputs[(size_t)Bk.W[2]])};
         float* C1[1] = {dXt};
         const float b1[1] = {accX ? 1.f : 0.f};
-        gemm3(c, true, TB, X.e, d, dx, d, false, Bw, d, true, C1, X.e, b1);
+        gemm3(c, true, TB, X.e, d, dx, ld, false, Bw, d, true, C1, X.e, b1);
       }
     }
     if(X.ln) {  // per-gate LN gain/bias: one column sum over b*T rows, then slices
@@ -688,6 +778,29 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
     const int slots[3] = {A.v, A.lnG, A.lnB};
     for(int j = 0; j < np; ++j)
       colsum(c, g.gradDst(n.inputs[(size_t)slots[j]]), D.vpart.devc() + j * TB * A.a, TB, A.a);
+    if(D.inter) {  // keys: d(keys)[r] (+)= sum_t w_t[r]^T dctx_t[r], one batched product
+      mtkc_gemm_args q{};
+      q.M = A.S;
+      q.N = A.kd;
+      q.K = T;
+      q.batch = b;
+      q.A = D.attW.devc();
+      q.lda = b * A.S;
+      q.strideA = A.S;
+      q.transA = 1;
+      q.B = D.dctx.devc();
+      q.ldb = b * A.kd;
+      q.strideB = A.kd;
+      q.C = D.gkeys.ptr;
+      q.ldc = A.kd;
+      q.strideC = A.S * A.kd;
+      q.alpha = 1.f;
+      q.beta = D.gkeys.accumulate ? 1.f : 0.f;
+      q.precision = (int)Device::get().precision();
+      q.workspace = c.ws;
+      q.workspace_bytes = c.wsBytes;
+      MTKC(mtkc_gemm(&q, c.st));
+    }
   }
 }
 
@@ -800,14 +913,20 @@ NodeRef ExpressionGraph::rnnEncoderScan(NodeRef x, const std::vector<GruParams>&
     // parameter gradient destinations are resolved before the fork (gradDst
     // is host bookkeeping; a lazily-zero buffer is only written, never read)
     const Ctx c0 = ctxFor(0), c1 = ctxFor(1);
-    backwardBegin(g, n, *X, X->dir[0], nullptr);
-    backwardBegin(g, n, *X, X->dir[1], nullptr);
-    dev.forkSide();
-    for(int64_t i = T - 1; i >= 0; --i) {
-      backwardStep(g, n, *X, X->dir[0], c0, i);
-      backwardStep(g, n, *X, X->dir[1], c1, i);
+    if(persistBwdEligible(g, n, *X)) {  // both directions in one cooperative launch
+      backwardBegin(g, n, *X, X->dir[0], nullptr, true);
+      backwardBegin(g, n, *X, X->dir[1], nullptr, true);
+      backwardPersistent(g, n, *X);
+    } else {
+      backwardBegin(g, n, *X, X->dir[0], nullptr);
+      backwardBegin(g, n, *X, X->dir[1], nullptr);
+      dev.forkSide();
+      for(int64_t i = T - 1; i >= 0; --i) {
+        backwardStep(g, n, *X, X->dir[0], c0, i);
+        backwardStep(g, n, *X, X->dir[1], c1, i);
+      }
+      dev.joinSide();
     }
-    dev.joinSide();
     // the batched weight / bias sums run on the compute stream (each fills
     // the GPU on its own; the column sums' last-CTA tickets are global)
     backwardEnd(g, n, *X, X->dir[0], c0, needX ? dxt[0].dev() : nullptr, 0);
@@ -963,9 +1082,14 @@ ExpressionGraph::RnnScanOut ExpressionGraph::rnnDecoderScan(
     const bool needX = g.node(g.resolve(n.inputs[0])).needsGrad;
     Tensor dxt = needX ? g.allocTensor(Shape({T * b, e})) : Tensor();
     const Ctx c0 = ctxFor(0);
-    backwardBegin(g, n, *X, D, ctxg.empty() ? nullptr : ctxg.devc());
-    for(int64_t i = T - 1; i >= 0; --i)
-      backwardStep(g, n, *X, D, c0, i);
+    if(persistBwdEligible(g, n, *X)) {
+      backwardBegin(g, n, *X, D, ctxg.empty() ? nullptr : ctxg.devc(), true);
+      backwardPersistent(g, n, *X);
+    } else {
+      backwardBegin(g, n, *X, D, ctxg.empty() ? nullptr : ctxg.devc());
+      for(int64_t i = T - 1; i >= 0; --i)
+        backwardStep(g, n, *X, D, c0, i);
+    }
     backwardEnd(g, n, *X, D, c0, needX ? dxt.dev() : nullptr, 0);
     if(needX) {
       auto dst = g.gradDst(n.inputs[0]);

@@ -51,7 +51,6 @@ constexpr uint32_t B_STAGE = NTH * 32 * 4;  // 12 KB
 constexpr int TMEM_COLS = 128;
 constexpr int MAXA = 2048;  // attention width cap (row-phase smem)
 constexpr int MAXS = 1024;  // source positions cap
-constexpr int GV = 8;       // elements per thread in the GRU row phase (d <= 2048)
 
 struct Maps {
   CUtensorMap hh[2];    // A: state slots [(T+1)*b x d]
@@ -609,6 +608,7 @@ __device__ void att_row(const KP& p, int64_t t, int64_t r, float* sW, float* sE,
 
 constexpr size_t SMEM_BYTES = 1024 + RST * (size_t)(A_STAGE + B_STAGE) +
                               (MAXA + 2 * MAXS + 6 * 32) * sizeof(float) + 256;
+constexpr size_t SMEM_BYTES_B = SMEM_BYTES + MAXS * sizeof(float) + 64;
 
 __global__ void __launch_bounds__(RT, 1)
     rnn_scan_fwd_kernel(const __grid_constant__ Maps maps, const __grid_constant__ KP p) {
@@ -752,6 +752,534 @@ __global__ void __launch_bounds__(RT, 1)
   if(warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem),
                  "r"(TMEM_COLS));
+}
+
+// ------------------------------------------------------------ backward
+//
+// Reverse sweep, per step and block k = K-1 .. 0 (backwardStep in
+// csrc/host/rnn_scan.cpp; gru_bwd_kernel / bahdanau_*_kernel arithmetic):
+//   PWB    one CTA per row: the block's output gradient = direct term
+//          (go*z of the block above, or the state slot) + the K-split
+//          partials of the product phase that fed it; GRU (+LN) backward;
+//          writes dG = [dpz|dpr|duh] (the next product's A operand), dGx,
+//          dac, LN partials and the direct part of the input gradient;
+//   PRODB  d(input) = dG * [Uz|Ur|Uh]^T (K = 3d) as K-split partials, plus
+//          (block 2 of the decoder) d(ctx) = dGx * [Wz|Wr|Wx]^T;
+//   ATTB   (decoder) one CTA per row: d(ctx) sum, d(weights) against the
+//          keys, softmax backward, LN backward, d(uk) (accumulated over
+//          steps), d(wq) and the v / LN partials; then PRODQ: the query
+//          projection's input gradient dwq * W^T feeding block 1.
+
+struct BMaps {
+  CUtensorMap dg[2];  // A: [K*T*b x 3d] per direction
+  CUtensorMap uh[2];  // B: [K*d x 3d] per direction ([Uz|Ur|Uh] side by side)
+  CUtensorMap dgx;    // A: block-2 [dpz|dpr|dax] [T*b x 3d]
+  CUtensorMap w2c;    // B: [kd x 3d] ([Wz|Wr|Wx] side by side)
+  CUtensorMap dwq;    // A: [T*b x a]
+  CUtensorMap watt;   // B: attention W as stored [d x a]
+};
+
+struct BKP {
+  mtkc_rnn_scan_args a;
+  float* partB[2];  // [KCb][b][d] per direction
+  float* partC;     // [KCc][b][kd]
+  float* partQ;     // [KCq][b][d]
+  float* dsd[2];    // [K-1][b][d] per direction: direct term go*z into the block below
+  unsigned* ctr;
+  unsigned long long* prof;
+  int KCb, KCc, KCq, NTb, NTc;
+};
+
+__device__ void gru_bwd_row(const BKP& p, const mtkc_rnn_dir& D, int dir, int k, int64_t t,
+                            int64_t r, int64_t hp, const float* base, const float* partIn,
+                            const float* partQ2, bool blend, float blendM, float* red) {
+  const mtkc_rnn_scan_args& a = p.a;
+  const int64_t b = a.b, T = a.T, d = a.d, d3 = 3 * d, d4 = d / 4;
+  const int K = D.nblocks;
+  const mtkc_rnn_block& B = D.blk[k];
+  const bool ln = B.ln[0] != nullptr;
+  const bool hasX = (k == 0 && D.xw1 != nullptr) || (k == 1 && a.has_att);
+  const int64_t tr = t * b + r;
+  const float* sIn = k == 0 ? D.HH + (hp * b + r) * d : D.sout + (((int64_t)(k - 1) * T + t) * b + r) * d;
+  float* ghp = D.GH + (hp * b + r) * d;
+  const float notm = 1.f - blendM;
+  float g0[GQ][4], z[GQ][4], rr[GQ][4], ht[GQ][4], uh[GQ][4], hv[GQ][4];
+#pragma unroll
+  for(int q = 0; q < GQ; ++q) {
+    const int64_t g = threadIdx.x + (int64_t)q * RT;
+#pragma unroll
+    for(int i = 0; i < 4; ++i)
+      g0[q][i] = z[q][i] = rr[q][i] = ht[q][i] = uh[q][i] = hv[q][i] = 0.f;
+    if(g >= d4)
+      continue;
+    const int64_t j = 4 * g;
+    set4(g0[q], ldcg4(base + j));
+    if(partIn)
+      for(int kc = 0; kc < p.KCb; ++kc)
+        add4(g0[q], ldcg4(partIn + ((int64_t)kc * b + r) * d + j));
+    if(partQ2)
+      for(int kc = 0; kc < p.KCq; ++kc)
+        add4(g0[q], ldcg4(partQ2 + ((int64_t)kc * b + r) * d + j));
+    const float* cache = B.cache + tr * d3 + j;
+    set4(z[q], ld4(cache));
+    set4(rr[q], ld4(cache + d));
+    set4(ht[q], ld4(cache + 2 * d));
+    set4(uh[q], ld4(B.hu + tr * d3 + 2 * d + j));
+    set4(hv[q], ldcg4(sIn + j));
+  }
+  float daz[GQ][4], dar[GQ][4], dac[GQ][4], duh[GQ][4];
+#pragma unroll
+  for(int q = 0; q < GQ; ++q) {  // graph.cpp:755-792
+    const int64_t g = threadIdx.x + (int64_t)q * RT;
+#pragma unroll
+    for(int i = 0; i < 4; ++i)
+      daz[q][i] = dar[q][i] = dac[q][i] = duh[q][i] = 0.f;
+    if(g >= d4)
+      continue;
+    const int64_t j = 4 * g;
+    float ghv[4], gp[4];
+#pragma unroll
+    for(int i = 0; i < 4; ++i) {
+      const float gg = blend ? g0[q][i] * blendM : g0[q][i];  // maskBlend backward
+      const float dz = gg * (hv[q][i] - ht[q][i]);
+      const float dht = gg * (1.f - z[q][i]);
+      ghv[i] = gg * z[q][i];
+      gp[i] = g0[q][i] * notm;
+      const float c = dht * (1.f - ht[q][i] * ht[q][i]);
+      const float dr = c * uh[q][i];
+      duh[q][i] = c * rr[q][i];
+      dac[q][i] = c;
+      daz[q][i] = dz * z[q][i] * (1.f - z[q][i]);
+      dar[q][i] = dr * rr[q][i] * (1.f - rr[q][i]);
+    }
+    if(k == 0) {  // input = the previous state slot (accumulating)
+      float o[4];
+      set4(o, ldcg4(ghp + j));
+#pragma unroll
+      for(int i = 0; i < 4; ++i)
+        o[i] = (blend && K == 1) ? (o[i] + ghv[i]) + gp[i] : o[i] + ghv[i];
+      st4(ghp + j, o);
+    } else {
+      st4(p.dsd[dir] + ((int64_t)(k - 1) * b + r) * d + j, ghv);
+      if(blend) {  // last block: gprev (+)= go*(1-m)
+        float o[4];
+        set4(o, ldcg4(ghp + j));
+#pragma unroll
+        for(int i = 0; i < 4; ++i)
+          o[i] += gp[i];
+        st4(ghp + j, o);
+      }
+    }
+  }
+  float dpz[GQ][4], dpr[GQ][4], dax[GQ][4];
+#pragma unroll
+  for(int q = 0; q < GQ; ++q)
+#pragma unroll
+    for(int i = 0; i < 4; ++i) {
+      dpz[q][i] = daz[q][i];
+      dpr[q][i] = dar[q][i];
+      dax[q][i] = dac[q][i];
+    }
+  const float fd = (float)d;
+  if(ln) {
+    const float rsz = B.lnrs[tr * 3], rsr = B.lnrs[tr * 3 + 1], rsx = B.lnrs[tr * 3 + 2];
+    float xz[GQ][4], xr[GQ][4], xx[GQ][4], gz[GQ][4], gr[GQ][4], gx[GQ][4];
+    float s[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for(int q = 0; q < GQ; ++q) {
+      const int64_t g = threadIdx.x + (int64_t)q * RT;
+#pragma unroll
+      for(int i = 0; i < 4; ++i)
+        xz[q][i] = xr[q][i] = xx[q][i] = gz[q][i] = gr[q][i] = gx[q][i] = 0.f;
+      if(g >= d4)
+        continue;
+      const int64_t j = 4 * g;
+      const float* xh = B.lnc + tr * d3 + j;
+      set4(xz[q], ld4(xh));
+      set4(xr[q], ld4(xh + d));
+      set4(gz[q], ld4(B.ln[0] + j));
+      set4(gr[q], ld4(B.ln[2] + j));
+      if(hasX) {
+        set4(xx[q], ld4(xh + 2 * d));
+        set4(gx[q], ld4(B.ln[4] + j));
+      }
+#pragma unroll
+      for(int i = 0; i < 4; ++i) {
+        const float hz = daz[q][i] * gz[q][i], hr = dar[q][i] * gr[q][i];
+        s[0] += hz;
+        s[1] += hz * xz[q][i];
+        s[2] += hr;
+        s[3] += hr * xr[q][i];
+        if(hasX) {
+          const float hx = dac[q][i] * gx[q][i];
+          s[4] += hx;
+          s[5] += hx * xx[q][i];
+        }
+      }
+    }
+    block_sums<6>(s, red);
+#pragma unroll
+    for(int q = 0; q < GQ; ++q) {
+      const int64_t g = threadIdx.x + (int64_t)q * RT;
+      if(g >= d4)
+        continue;
+      const int64_t j = 4 * g;
+      float l0[4], l1[4], l2[4], l3[4], l4[4], l5[4];
+#pragma unroll
+      for(int i = 0; i < 4; ++i) {
+        dpz[q][i] = rsz * (daz[q][i] * gz[q][i] - s[0] / fd - xz[q][i] * (s[1] / fd));
+        dpr[q][i] = rsr * (dar[q][i] * gr[q][i] - s[2] / fd - xr[q][i] * (s[3] / fd));
+        l0[i] = daz[q][i] * xz[q][i];
+        l1[i] = daz[q][i];
+        l2[i] = dar[q][i] * xr[q][i];
+        l3[i] = dar[q][i];
+        if(hasX) {
+          dax[q][i] = rsx * (dac[q][i] * gx[q][i] - s[4] / fd - xx[q][i] * (s[5] / fd));
+          l4[i] = dac[q][i] * xx[q][i];
+          l5[i] = dac[q][i];
+        }
+      }
+      float* lp = B.lnp + tr * 6 * d + j;
+      st4(lp, l0);
+      st4(lp + d, l1);
+      st4(lp + 2 * d, l2);
+      st4(lp + 3 * d, l3);
+      if(hasX) {
+        st4(lp + 4 * d, l4);
+        st4(lp + 5 * d, l5);
+      }
+    }
+  }
+#pragma unroll
+  for(int q = 0; q < GQ; ++q) {
+    const int64_t g = threadIdx.x + (int64_t)q * RT;
+    if(g >= d4)
+      continue;
+    const int64_t j = 4 * g;
+    float* dg = D.dG + (((int64_t)k * T + t) * b + r) * d3 + j;
+    st4(dg, dpz[q]);
+    st4(dg + d, dpr[q]);
+    st4(dg + 2 * d, duh[q]);
+    if(B.dGx) {
+      float* dx = B.dGx + tr * d3 + j;
+      st4(dx, dpz[q]);
+      st4(dx + d, dpr[q]);
+      st4(dx + 2 * d, dax[q]);
+    }
+    st4(B.dac + tr * d + j, dac[q]);
+  }
+}
+
+__device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, float* sC, float* sE,
+                            float* sP, float* sQ) {
+  const mtkc_rnn_scan_args& a = p.a;
+  const int64_t b = a.b, T = a.T, A = a.a, S = a.S, KD = a.kd, A4 = A / 4, K4 = KD / 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tr = t * b + r, TB = T * b;
+  for(int64_t k4 = threadIdx.x; k4 < K4; k4 += RT) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if(a.ctxGrad)
+      set4(v, ld4(a.ctxGrad + tr * KD + 4 * k4));
+    for(int kc = 0; kc < p.KCc; ++kc)
+      add4(v, ldcg4(p.partC + ((int64_t)kc * b + r) * KD + 4 * k4));
+    st4(sC + 4 * k4, v);
+    st4(a.dctx + tr * KD + 4 * k4, v);
+  }
+  __syncthreads();
+  // d(weights)_j = dctx . keys_j  (bahdanau_dw_kernel; the key gradient
+  // sum_t w_tj dctx_t is one batched product after the sweep)
+  for(int64_t j = warp; j < S; j += RT / 32) {
+    const float* keys = a.keys + (r * S + j) * KD;
+    float acc = 0.f;
+    for(int64_t c4 = lane; c4 < K4; c4 += 128) {
+      float4 kv[4], cv[4];
+#pragma unroll
+      for(int u = 0; u < 4; ++u) {
+        const int64_t cc = c4 + 32 * u;
+        kv[u] = cc < K4 ? ld4(keys + 4 * cc) : make_float4(0.f, 0.f, 0.f, 0.f);
+        cv[u] = cc < K4 ? *reinterpret_cast<const float4*>(sC + 4 * cc)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for(int u = 0; u < 4; ++u)
+        acc += cv[u].x * kv[u].x + cv[u].y * kv[u].y + cv[u].z * kv[u].z + cv[u].w * kv[u].w;
+    }
+    acc = warp_sum(acc);
+    if(lane == 0)
+      sE[j] = acc;
+  }
+  __syncthreads();
+  if(warp == 0) {  // softmax backward: de_j = w_j (dw_j - sum_l w_l dw_l)
+    float s = 0.f;
+    for(int64_t j = lane; j < S; j += 32)
+      s += a.attWts[tr * S + j] * sE[j];
+    s = warp_sum(s);
+    __syncwarp();
+    for(int64_t j = lane; j < S; j += 32)
+      sE[j] = a.attWts[tr * S + j] * (sE[j] - s);
+  }
+  __syncthreads();
+  const bool ln = a.attLnG != nullptr;
+  if(ln) {  // LN backward row statistics per position (bahdanau_de_kernel)
+    for(int64_t j = warp; j < S; j += RT / 32) {
+      const int64_t trj = tr * S + j;
+      const float dej = sE[j];
+      float s1 = 0.f, s2 = 0.f;
+      for(int64_t c4 = lane; c4 < A4; c4 += 32) {
+        const float4 tv = ld4(a.attT + trj * A + 4 * c4), xh = ld4(a.attLnx + trj * A + 4 * c4);
+        const float4 vv = ld4(a.attV + 4 * c4), gg = ld4(a.attLnG + 4 * c4);
+        const float tt[4] = {tv.x, tv.y, tv.z, tv.w}, xx[4] = {xh.x, xh.y, xh.z, xh.w};
+        const float v4[4] = {vv.x, vv.y, vv.z, vv.w}, g4[4] = {gg.x, gg.y, gg.z, gg.w};
+#pragma unroll
+        for(int i = 0; i < 4; ++i) {
+          const float h = ((dej * v4[i]) * (1.f - tt[i] * tt[i])) * g4[i];
+          s1 += h;
+          s2 += h * xx[i];
+        }
+      }
+      s1 = warp_sum(s1) / (float)A;
+      s2 = warp_sum(s2) / (float)A;
+      if(lane == 0) {
+        sP[j] = s1;
+        sQ[j] = s2;
+      }
+    }
+    __syncthreads();
+  }
+  // per column (bahdanau_cols_kernel): d(uk), d(wq), v / LN partials;
+  // four positions' loads in flight
+  const bool acc = ii > 0 || a.acc_uk;
+  for(int64_t c4 = threadIdx.x; c4 < A4; c4 += RT) {
+    const int64_t c = 4 * c4;
+    const float4 vv = ld4(a.attV + c);
+    const float vc[4] = {vv.x, vv.y, vv.z, vv.w};
+    float gc[4] = {0.f, 0.f, 0.f, 0.f};
+    if(ln)
+      set4(gc, ld4(a.attLnG + c));
+    float awq[4] = {0.f, 0.f, 0.f, 0.f}, av[4] = {0.f, 0.f, 0.f, 0.f};
+    float ag[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
+    for(int64_t j0 = 0; j0 < S; j0 += 4) {
+      float4 tv[4], xv[4], gv[4];
+#pragma unroll
+      for(int u = 0; u < 4; ++u) {
+        const int64_t j = j0 + u;
+        if(j < S) {
+          tv[u] = ld4(a.attT + (tr * S + j) * A + c);
+          xv[u] = ln ? ld4(a.attLnx + (tr * S + j) * A + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          gv[u] = acc ? ldcg4(a.guk + (r * S + j) * A + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for(int u = 0; u < 4; ++u) {
+        const int64_t j = j0 + u;
+        if(j >= S)
+          break;
+        const float dej = sE[j];
+        const float tt[4] = {tv[u].x, tv[u].y, tv[u].z, tv[u].w};
+        const float xx[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+        float gu[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+        const float rs = ln ? a.attLnrs[tr * S + j] : 0.f;
+#pragma unroll
+        for(int i = 0; i < 4; ++i) {
+          av[i] += tt[i] * dej;
+          const float dln = (dej * vc[i]) * (1.f - tt[i] * tt[i]);
+          float ds = dln;
+          if(ln) {
+            ag[i] += dln * xx[i];
+            ab[i] += dln;
+            ds = rs * (dln * gc[i] - sP[j] - xx[i] * sQ[j]);
+          }
+          gu[i] = acc ? gu[i] + ds : ds;
+          awq[i] += ds;
+        }
+        st4(a.guk + (r * S + j) * A + c, gu);
+      }
+    }
+    st4(a.dwq + tr * A + c, awq);
+    st4(a.vpart + tr * A + c, av);
+    if(ln) {
+      st4(a.vpart + TB * A + tr * A + c, ag);
+      st4(a.vpart + 2 * TB * A + tr * A + c, ab);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(RT, 1)
+    rnn_scan_bwd_kernel(const __grid_constant__ BMaps maps, const __grid_constant__ BKP p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  Smem sm;
+  sm.sA = base;
+  sm.sB = base + RST * A_STAGE;
+  float* sC = (float*)(sm.sB + RST * B_STAGE);
+  float* sE = sC + MAXA;
+  float* sP = sE + MAXS;
+  float* red = sP + MAXS;
+  uint64_t* bars = (uint64_t*)(red + 6 * 32);
+  sm.full = bars;
+  sm.empty = bars + RST;
+  sm.tfull = bars + 2 * RST;
+  sm.tempty = bars + 2 * RST + 1;
+  uint32_t* tmemSlot = (uint32_t*)(bars + 2 * RST + 2);
+  float* sQ = (float*)(tmemSlot + 4);
+  const int warp = threadIdx.x >> 5;
+  const mtkc_rnn_scan_args& a = p.a;
+  if(threadIdx.x == 0) {
+    for(int s = 0; s < RST; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    mbar_init(&sm.tfull[0], 1);
+    mbar_init(&sm.tempty[0], 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for(int q = 0; q < a.ndir; ++q) {
+      prefetch_tmap(&maps.dg[q]);
+      prefetch_tmap(&maps.uh[q]);
+    }
+    if(a.has_att) {
+      prefetch_tmap(&maps.dgx);
+      prefetch_tmap(&maps.w2c);
+      prefetch_tmap(&maps.dwq);
+      prefetch_tmap(&maps.watt);
+    }
+  }
+  if(warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmemSlot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  sm.tmem = *tmemSlot;
+
+  const int gs = gridDim.x / a.ndir;
+  const int dir = blockIdx.x / gs, gi = blockIdx.x % gs;
+  const mtkc_rnn_dir& D = a.dir[dir];
+  unsigned* ctr = p.ctr + dir;
+  unsigned epoch = 0;
+  uint32_t ring = 0, ucnt = 0;
+  int npf = 0;
+  const int64_t b = a.b, T = a.T, d = a.d, d3 = 3 * d;
+  const int K = D.nblocks;
+  const int mT = (int)((b + 127) / 128);
+
+  for(int64_t ii = 0; ii < T; ++ii) {
+    const int64_t t = D.reverse ? ii : T - 1 - ii;
+    const int64_t hp = D.reverse ? t + 1 : t, hs = D.reverse ? t : t + 1;
+    for(int k = K - 1; k >= 0; --k) {
+      const bool att1 = a.has_att && k == 1;
+      const bool last = k == K - 1;
+      mark(p.prof, npf, 1);
+      for(int64_t r = gi; r < b; r += gs) {
+        const float* baseRow = last ? D.GH + (hs * b + r) * d : p.dsd[dir] + ((int64_t)k * b + r) * d;
+        const float* partIn = (!last || ii > 0) ? p.partB[dir] : nullptr;
+        const float* partQ2 = (k == 0 && a.has_att) ? p.partQ : nullptr;
+        const bool blend = last && a.maskT != nullptr;
+        const float m = blend ? a.maskT[t * b + r] : 1.f;
+        gru_bwd_row(p, D, dir, k, t, r, hp, baseRow, partIn, partQ2, blend, m, red);
+      }
+      mark(p.prof, npf, 5);
+      grid_bar(ctr, gs, epoch);
+      Prod P[2];
+      int np = 1;
+      P[0].ma = &maps.dg[dir];
+      P[0].mb = &maps.uh[dir];
+      P[0].aRow0 = (int)(((int64_t)k * T + t) * b);
+      P[0].bRow0 = (int)(k * d);
+      P[0].N = (int)d;
+      P[0].NT = p.NTb;
+      P[0].KC = p.KCb;
+      P[0].KS = (int)(d3 / p.KCb);
+      P[0].nT = (int)(d / p.NTb);
+      P[0].mT = mT;
+      P[0].part = p.partB[dir];
+      if(att1) {
+        P[1].ma = &maps.dgx;
+        P[1].mb = &maps.w2c;
+        P[1].aRow0 = (int)(t * b);
+        P[1].bRow0 = 0;
+        P[1].N = (int)a.kd;
+        P[1].NT = p.NTc;
+        P[1].KC = p.KCc;
+        P[1].KS = (int)(d3 / p.KCc);
+        P[1].nT = (int)(a.kd / p.NTc);
+        P[1].mT = mT;
+        P[1].part = p.partC;
+        np = 2;
+      }
+      mark(p.prof, npf, att1 ? 4 : 0);
+      run_prods(P, np, gi, gs, sm, ring, ucnt, b);
+      mark(p.prof, npf, 5);
+      grid_bar(ctr, gs, epoch);
+      if(att1) {
+        mark(p.prof, npf, 3);
+        for(int64_t r = gi; r < b; r += gs)
+          att_bwd_row(p, ii, t, r, sC, sE, sP, sQ);
+        mark(p.prof, npf, 5);
+        grid_bar(ctr, gs, epoch);
+        Prod Q;
+        Q.ma = &maps.dwq;
+        Q.mb = &maps.watt;
+        Q.aRow0 = (int)(t * b);
+        Q.bRow0 = 0;
+        Q.N = (int)d;
+        Q.NT = p.NTb;
+        Q.KC = p.KCq;
+        Q.KS = (int)(a.a / p.KCq);
+        Q.nT = (int)(d / p.NTb);
+        Q.mT = mT;
+        Q.part = p.partQ;
+        mark(p.prof, npf, 2);
+        run_prods(&Q, 1, gi, gs, sm, ring, ucnt, b);
+        mark(p.prof, npf, 5);
+        grid_bar(ctr, gs, epoch);
+      }
+    }
+  }
+  // the last block-1 product feeds the initial-state slot
+  const int64_t h0 = D.reverse ? T : 0;
+  for(int64_t r = gi; r < b; r += gs)
+    for(int64_t j4 = threadIdx.x; j4 < d / 4; j4 += RT) {
+      float v[4];
+      set4(v, ldcg4(D.GH + (h0 * b + r) * d + 4 * j4));
+      for(int kc = 0; kc < p.KCb; ++kc)
+        add4(v, ldcg4(p.partB[dir] + ((int64_t)kc * b + r) * d + 4 * j4));
+      st4(D.GH + (h0 * b + r) * d + 4 * j4, v);
+    }
+  mark(p.prof, npf, 6);
+  tc_fence_before();
+  __syncthreads();
+  if(warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tmem),
+                 "r"(TMEM_COLS));
+}
+
+// strided copies into the workspace: dst[r * ldd + c] = src[r * lds + c]
+struct CJob {
+  const float* src;
+  float* dst;
+  int rows, cols, lds, ldd;
+};
+struct CJobs {
+  CJob j[2 * 3 * MTKC_RNN_MAX_BLOCKS + 4];
+  int n;
+};
+
+__global__ void copy_jobs_kernel(const __grid_constant__ CJobs jobs) {
+  MTKC_PDL_ENTRY();
+  const CJob& J = jobs.j[blockIdx.y];
+  const int64_t n4 = (int64_t)J.rows * (J.cols / 4);
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (J.cols / 4), c = (i % (J.cols / 4)) * 4;
+    *reinterpret_cast<float4*>(J.dst + r * J.ldd + c) =
+        *reinterpret_cast<const float4*>(J.src + r * J.lds + c);
+  }
 }
 
 // weight transposes into the workspace: dst[c * rows + r] = src[r * cols + c]
@@ -910,6 +1438,61 @@ bool supported(const mtkc_rnn_scan_args* a) {
   return true;
 }
 
+
+struct BPlan {
+  int G, gs, KCb, KCc, KCq, NTb, NTc;
+  size_t offUH[2], offW2C, offPB[2], offPC, offPQ, offDSD[2], offCtr, total;
+};
+
+BPlan make_bplan(const mtkc_rnn_scan_args* a) {
+  BPlan P{};
+  const int64_t b = a->b, d = a->d, d3 = 3 * d;
+  P.G = grid_size();
+  P.G -= P.G % a->ndir;
+  P.gs = P.G / a->ndir;
+  const int mT = (int)((b + 127) / 128);
+  P.NTb = d % 64 == 0 ? 64 : 32;
+  P.NTc = a->has_att ? (a->kd % 64 == 0 ? 64 : 32) : 32;
+  P.KCb = pick_kc((int)(d3 / 32), P.gs / std::max<int>(1, (int)(d / P.NTb) * mT));
+  P.KCc = a->has_att ? pick_kc((int)(d3 / 32), P.gs / std::max<int>(1, (int)(a->kd / P.NTc) * mT)) : 1;
+  P.KCq = a->has_att ? pick_kc((int)(a->a / 32), P.gs / std::max<int>(1, (int)(d / P.NTb) * mT)) : 1;
+  size_t off = 0;
+  auto take = [&](size_t floats) {
+    size_t o = off;
+    off += (floats * sizeof(float) + 255) / 256 * 256;
+    return o;
+  };
+  for(int q = 0; q < a->ndir; ++q) {
+    P.offUH[q] = take((size_t)a->dir[q].nblocks * d * d3);
+    P.offPB[q] = take((size_t)P.KCb * b * d);
+    P.offDSD[q] = take((size_t)std::max(1, a->dir[q].nblocks - 1) * b * d);
+  }
+  if(a->has_att) {
+    P.offW2C = take((size_t)a->kd * d3);
+    P.offPC = take((size_t)P.KCc * b * a->kd);
+    P.offPQ = take((size_t)P.KCq * b * d);
+  }
+  P.offCtr = take(64);
+  P.total = off;
+  return P;
+}
+
+bool bwd_supported(const mtkc_rnn_scan_args* a) {
+  if(!supported(a))
+    return false;
+  for(int q = 0; q < a->ndir; ++q) {
+    const mtkc_rnn_dir& D = a->dir[q];
+    if(!D.GH || !D.dG)
+      return false;
+    for(int k = 0; k < D.nblocks; ++k)
+      if(!D.blk[k].dac || (D.blk[k].ln[0] && !D.blk[k].lnp))
+        return false;
+  }
+  if(a->has_att && (a->kd > MAXA || !a->dctx || !a->dwq || !a->guk || !a->vpart ||
+                    !a->dir[0].blk[1].dGx))
+    return false;
+  return true;
+}
 }  // namespace
 
 extern "C" {
@@ -1043,4 +1626,126 @@ int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream) {
   return MTKC_OK;
 }
 
+size_t mtkc_rnn_scan_bwd_workspace(const mtkc_rnn_scan_args* a) {
+  if(!bwd_supported(a))
+    return 0;
+  return make_bplan(a).total;
+}
+
+int mtkc_rnn_scan_backward(const mtkc_rnn_scan_args* a, void* stream) {
+  if(!bwd_supported(a))
+    return fail(MTKC_CONTRACT, "rnn scan backward: arguments not supported by the persistent path");
+  const BPlan P = make_bplan(a);
+  if(!a->workspace || a->workspace_bytes < P.total)
+    return fail(MTKC_CONTRACT, "rnn scan backward: workspace too small");
+  cudaStream_t st = S(stream);
+  uint8_t* ws = (uint8_t*)a->workspace;
+  const int64_t b = a->b, T = a->T, d = a->d, d3 = 3 * d;
+  ProfScope prof(st, "rnn_scan_bwd", 0.0);
+  // [Uz|Ur|Uh] and [Wz|Wr|Wx] side by side (K-major B operands of the
+  // input-gradient products)
+  CJobs jobs{};
+  for(int q = 0; q < a->ndir; ++q) {
+    const mtkc_rnn_dir& D = a->dir[q];
+    float* uh = (float*)(ws + P.offUH[q]);
+    for(int k = 0; k < D.nblocks; ++k)
+      for(int g = 0; g < 3; ++g)
+        jobs.j[jobs.n++] = CJob{D.blk[k].U[g], uh + (int64_t)k * d * d3 + g * d, (int)d, (int)d,
+                                (int)d, (int)d3};
+  }
+  if(a->has_att) {
+    float* w2c = (float*)(ws + P.offW2C);
+    for(int g = 0; g < 3; ++g)
+      jobs.j[jobs.n++] = CJob{a->dir[0].blk[1].W[g], w2c + g * d, (int)a->kd, (int)d, (int)d,
+                              (int)d3};
+  }
+  ::mtkc::launch(copy_jobs_kernel, dim3(148, (unsigned)jobs.n), 256, 0, st, jobs);
+  MTKC_POST_LAUNCH("copy_jobs_kernel");
+  if(cudaError_t e = cudaMemsetAsync(ws + P.offCtr, 0, 256, st))
+    return cuda_status(e, "rnn scan counters");
+
+  BMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  bool ok = true;
+  for(int q = 0; q < a->ndir; ++q) {
+    const mtkc_rnn_dir& D = a->dir[q];
+    ok = ok && kmap(&maps.dg[q], D.dG, d3, (int64_t)D.nblocks * T * b, 128);
+    ok = ok && kmap(&maps.uh[q], (const float*)(ws + P.offUH[q]), d3, (int64_t)D.nblocks * d,
+                    (uint32_t)P.NTb);
+  }
+  if(a->has_att) {
+    ok = ok && kmap(&maps.dgx, a->dir[0].blk[1].dGx, d3, T * b, 128);
+    ok = ok && kmap(&maps.w2c, (const float*)(ws + P.offW2C), d3, a->kd, (uint32_t)P.NTc);
+    ok = ok && kmap(&maps.dwq, a->dwq, a->a, T * b, 128);
+    ok = ok && kmap(&maps.watt, a->attW, a->a, d, (uint32_t)P.NTb);
+  }
+  if(!ok)
+    return fail(MTKC_CUDA, "rnn scan backward: tensor map encoding failed");
+  BKP kp;
+  memset(&kp, 0, sizeof(kp));
+  kp.a = *a;
+  for(int q = 0; q < a->ndir; ++q) {
+    kp.partB[q] = (float*)(ws + P.offPB[q]);
+    kp.dsd[q] = (float*)(ws + P.offDSD[q]);
+  }
+  kp.partC = a->has_att ? (float*)(ws + P.offPC) : nullptr;
+  kp.partQ = a->has_att ? (float*)(ws + P.offPQ) : nullptr;
+  kp.ctr = (unsigned*)(ws + P.offCtr);
+  kp.KCb = P.KCb;
+  kp.KCc = P.KCc;
+  kp.KCq = P.KCq;
+  kp.NTb = P.NTb;
+  kp.NTc = P.NTc;
+  static bool attr = false;
+  if(!attr) {
+    cudaError_t e = cudaFuncSetAttribute(rnn_scan_bwd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM_BYTES_B);
+    if(e != cudaSuccess)
+      return cuda_status(e, "rnn scan bwd smem attribute");
+    attr = true;
+  }
+  static unsigned long long* profBuf = nullptr;
+  const bool profOn = getenv("MTK_RNN_PROF") != nullptr;
+  if(profOn) {
+    if(!profBuf)
+      cudaMalloc(&profBuf, 8192 * 2 * sizeof(unsigned long long));
+    cudaMemsetAsync(profBuf, 0, 8192 * 2 * sizeof(unsigned long long), st);
+    kp.prof = profBuf;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)P.G);
+  cfg.blockDim = dim3(RT);
+  cfg.dynamicSmemBytes = SMEM_BYTES_B;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeCooperative;
+  attrs[0].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, rnn_scan_bwd_kernel, maps, kp);
+  if(e != cudaSuccess)
+    return cuda_status(e, "rnn_scan_bwd_kernel");
+  count_launch();
+  if(profOn) {  // kinds: 1 PWB, 0 PRODB, 4 PRODB + ctx, 3 ATTB, 2 PRODQ, 5 barrier
+    std::vector<unsigned long long> h(8192 * 2);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), profBuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    double sum[8] = {0}, cnt[8] = {0};
+    for(int i = 0; i + 1 < 8192 && h[2 * i + 3]; ++i) {
+      int k = (int)h[2 * i];
+      sum[k] += (double)(h[2 * i + 3] - h[2 * i + 1]);
+      cnt[k] += 1;
+    }
+    const char* nm[8] = {"prodB", "pwB", "prodQ", "attB", "prodB+ctx", "barrier", "end", "-"};
+    fprintf(stderr, "[rnn prof bwd] ndir %d b %lld T %lld:", a->ndir, (long long)b, (long long)T);
+    for(int k = 0; k < 6; ++k)
+      if(cnt[k] > 0)
+        fprintf(stderr, " %s %.0f x %.2f us", nm[k], cnt[k], sum[k] / cnt[k] / 1e3);
+    fprintf(stderr, "\n");
+  }
+  return MTKC_OK;
+}
+
 }  // extern "C"
+
