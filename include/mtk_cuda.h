@@ -378,6 +378,24 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
                                int64_t tq, int64_t tk, int heads, int64_t dk, float scale,
                                int accumulate_q, int accumulate_k, int accumulate_v,
                                float* colpart, void* stream);
+/* Packed-row (varlen) form: the b sentences' query rows are qoff[i] ..
+ * qoff[i+1]-1 of q / out, their key rows koff[i] .. koff[i+1]-1 of k / v
+ * (device int32 [b+1]); every key within a sentence is real (no mask);
+ * tq_max / tk_max bound the lengths and give probs its [b,heads,tq_max,
+ * tk_max] layout.  Padding rows never exist, so position-wise work before
+ * and after attention runs over real tokens only. */
+int mtkc_attention_tc_varlen(float* out, int64_t ldo, float* probs, const float* q, int64_t ldq,
+                             const float* k, const float* v, int64_t ldk, const int32_t* qoff,
+                             const int32_t* koff, int64_t b, int64_t tq_max, int64_t tk_max,
+                             int heads, int64_t dk, float scale, int causal, int* flags,
+                             void* stream);
+int mtkc_attention_tc_varlen_backward(const float* gout, int64_t ldo, const float* probs,
+                                      const float* q, int64_t ldq, const float* k,
+                                      const float* v, int64_t ldk, float* gq, float* gk,
+                                      float* gv, const int32_t* qoff, const int32_t* koff,
+                                      int64_t b, int64_t tq_max, int64_t tk_max, int heads,
+                                      int64_t dk, float scale, int accumulate_q,
+                                      int accumulate_k, int accumulate_v, void* stream);
 
 /* ======================================================================== */
 /* fused GRU block, pointwise part (gruCell graph.cpp:648-813, gruPre        */

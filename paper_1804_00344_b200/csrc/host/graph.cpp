@@ -1556,6 +1556,84 @@ NodeRef ExpressionGraph::attention(NodeRef q, NodeRef k, NodeRef v, const Tensor
   return addNode(std::move(n));
 }
 
+std::shared_ptr<RowPacking> RowPacking::fromMask(const Tensor& mask) {
+  if(mask.empty() || mask.shape().rank() != 2)
+    return nullptr;
+  const int64_t b = mask.shape()[0], T = mask.shape()[1];
+  const Real* m = mask.data();
+  auto p = std::make_shared<RowPacking>();
+  p->b = b;
+  p->T = T;
+  p->off.assign((size_t)b + 1, 0);
+  for(int64_t i = 0; i < b; ++i) {
+    int64_t len = 0;
+    while(len < T && m[i * T + len] != 0)
+      ++len;
+    for(int64_t t = len; t < T; ++t)
+      if(m[i * T + t] != 0)
+        return nullptr;  // not a prefix
+    if(len == 0)
+      return nullptr;
+    for(int64_t t = 0; t < len; ++t)
+      p->rows.push_back(i * T + t);
+    p->off[(size_t)i + 1] = (int32_t)p->rows.size();
+    p->maxLen = std::max(p->maxLen, len);
+  }
+  return p;
+}
+
+NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef k, NodeRef v,
+                                         const std::shared_ptr<const RowPacking>& qp,
+                                         const std::shared_ptr<const RowPacking>& kp,
+                                         bool causal, int heads) {
+  checkRef(q);
+  checkRef(k);
+  checkRef(v);
+  if(!qp || !kp || qp->b != kp->b)
+    throw ContractError("attentionPacked: packings of different batches");
+  if(q.shape.rank() != 2 || k.shape.rank() != 2 || v.shape != k.shape ||
+     q.shape[0] != qp->n() || k.shape[0] != kp->n() || q.shape[1] != k.shape[1])
+    throw DimensionError("attentionPacked expects q [nq,d], k/v [nk,d]: " + q.shape.str() +
+                         " " + k.shape.str());
+  const int64_t d = q.shape[1], b = qp->b, tq = qp->maxLen, tk = kp->maxLen;
+  if(d % heads != 0)
+    throw DimensionError("model dim not divisible by heads");
+  const int64_t dk = d / heads;
+  if(Device::get().precision() != Precision::TF32 || !mtkc_attention_tc_supported(tq, tk, dk))
+    throw ContractError("attentionPacked: needs the TF32 tensor-core attention path");
+  for(const RowPacking* rp : {qp.get(), kp.get()})
+    if(!rp->dev)
+      rp->dev = uploadIntsTo(*this, rp->off, &rp->devOff);
+  Node n;
+  n.op = "attentionPacked";
+  n.shape = q.shape;
+  n.inputs = {q.index, k.index, v.index};
+  auto aux = std::make_shared<AttAux>();
+  n.aux = aux;
+  const float scale = (float)(1.0 / std::sqrt((double)dk));  // layers.cpp:106
+  std::shared_ptr<const RowPacking> QP = qp, KP = kp;
+  n.fwd = [=](ExpressionGraph& g, Node& n) {
+    aux->probs = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));
+    MTKC(mtkc_attention_tc_varlen(n.value.dev(), d, aux->probs.dev(), g.valPtr(n.inputs[0]), d,
+                                  g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d,
+                                  (const int32_t*)QP->dev->ptr + QP->devOff,
+                                  (const int32_t*)KP->dev->ptr + KP->devOff, b, tq, tk, heads, dk,
+                                  scale, causal ? 1 : 0, Device::get().flags(), stream()));
+  };
+  n.bwd = [=](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    auto dq = g.gradDst(n.inputs[0]);
+    auto dkk = g.gradDst(n.inputs[1]);
+    auto dv = g.gradDst(n.inputs[2]);
+    MTKC(mtkc_attention_tc_varlen_backward(
+        go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d, g.valPtr(n.inputs[1]),
+        g.valPtr(n.inputs[2]), d, dq.ptr, dkk.ptr, dv.ptr,
+        (const int32_t*)QP->dev->ptr + QP->devOff, (const int32_t*)KP->dev->ptr + KP->devOff, b,
+        tq, tk, heads, dk, scale, dq.accumulate, dkk.accumulate, dv.accumulate, stream()));
+  };
+  return addNode(std::move(n));
+}
+
 // -------------------------------------------------------------- dropout
 
 

@@ -85,6 +85,11 @@ struct TcAttP {
   float scale;
   int causal;
   int* flags;
+  // varlen (packed rows): sentence bi's queries are rows qoff[bi] ..
+  // qoff[bi+1]-1, its keys koff[bi] .. koff[bi+1]-1; tq / tk are the maxima
+  // (the probability tensor keeps the padded [b, heads, tq, tk] layout)
+  const int* qoff;
+  const int* koff;
 };
 
 struct TcAttBP {
@@ -103,6 +108,8 @@ struct TcAttBP {
   float scale;
   int accQ, accK, accV;
   float* colpart;  // optional [3][b][heads*64]: column sums of this CTA's dq/dk/dv
+  const int* qoff;  // varlen, as in TcAttP
+  const int* koff;
 };
 
 // strides (floats): L4 = 4*odd mod 32 for row-fragment reads (g*L + t),
@@ -161,11 +168,18 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_fwd_kernel(TcAttP p) {
   float* mk = V + TT * L8;                      // [TT] key usable (mask)
   float* xch = mk + TT;                         // [2][2][TT] row max / row sum per key half
   const int h = blockIdx.x, bi = blockIdx.y;
-  const int tq = p.tq, tk = p.tk;
+  int tq = p.tq, tk = p.tk;
+  int64_t qb = (int64_t)bi * tq, kb = (int64_t)bi * tk;  // first query / key row
+  if(p.qoff) {
+    qb = p.qoff[bi];
+    tq = p.qoff[bi + 1] - (int)qb;
+    kb = p.koff[bi];
+    tk = p.koff[bi + 1] - (int)kb;
+  }
   const int hoff = h * DKT;
-  stage<TT, L4, NTH>(Q, p.q + (int64_t)bi * tq * p.ldq + hoff, p.ldq, tq);
-  stage<TT, L4, NTH>(K, p.k + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
-  stage<TT, L8, NTH>(V, p.v + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
+  stage<TT, L4, NTH>(Q, p.q + qb * p.ldq + hoff, p.ldq, tq);
+  stage<TT, L4, NTH>(K, p.k + kb * p.ldk + hoff, p.ldk, tk);
+  stage<TT, L8, NTH>(V, p.v + kb * p.ldk + hoff, p.ldk, tk);
   for(int j = threadIdx.x; j < TT; j += NTH)
     mk[j] = (j < tk && (!p.mask || p.mask[(int64_t)bi * tk + j] != 0.f)) ? 1.f : 0.f;
   cp_async_wait_all();
@@ -266,7 +280,7 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_fwd_kernel(TcAttP p) {
   // probabilities to HBM: this warp's 8 rows of the block's [16 x tk] slice
   {
     const int rows = min(8, tq - m0 - half * 8);
-    float* gP = p.probs + (((int64_t)bi * p.heads + h) * tq + m0 + half * 8) * tk;
+    float* gP = p.probs + (((int64_t)bi * p.heads + h) * p.tq + m0 + half * 8) * p.tk;
     const float* Ps = Q + (m0 + half * 8) * L4;
 #pragma unroll
     for(int r = 0; r < 8; ++r)
@@ -274,7 +288,7 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_fwd_kernel(TcAttP p) {
 #pragma unroll
         for(int c = lane; c < TT; c += 32)
           if(c < tk)
-            gP[r * tk + c] = Ps[r * L4 + c];
+            gP[r * p.tk + c] = Ps[r * L4 + c];
       }
   }
   // O = P V over this warp's 32 columns: keys outer, 4 output tiles inner
@@ -291,7 +305,7 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_fwd_kernel(TcAttP p) {
     for(int jd = 0; jd < NJ; ++jd)
       mma8(o[jd], a0, a1, a2, a3, tf32(Vr[jd * 8]), tf32(Vr[jd * 8 + 4 * L8]));
   }
-  float* out = p.out + (int64_t)bi * tq * p.ldo + hoff + half * 32;
+  float* out = p.out + qb * p.ldo + hoff + half * 32;
 #pragma unroll
   for(int jd = 0; jd < NJ; ++jd) {
     const int col = jd * 8 + 2 * t;
@@ -331,21 +345,28 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_bwd_kernel(TcAttBP p) {
   float* Dp = P + TT * LP;                      // [2][TT] row sums of dP*P per key half
   float* csum = Dp + 2 * TT;                    // [3][NWB][64] per-row-block column sums
   const int h = blockIdx.x, bi = blockIdx.y;
-  const int tq = p.tq, tk = p.tk;
+  int tq = p.tq, tk = p.tk;
+  int64_t qb = (int64_t)bi * tq, kb = (int64_t)bi * tk;
+  if(p.qoff) {
+    qb = p.qoff[bi];
+    tq = p.qoff[bi + 1] - (int)qb;
+    kb = p.koff[bi];
+    tk = p.koff[bi + 1] - (int)kb;
+  }
   const int hoff = h * DKT;
-  stage<TT, L8, NTH>(Q, p.q + (int64_t)bi * tq * p.ldq + hoff, p.ldq, tq);
-  stage<TT, L8, NTH>(K, p.k + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
-  stage<TT, L4, NTH>(V, p.v + (int64_t)bi * tk * p.ldk + hoff, p.ldk, tk);
-  stage<TT, L4, NTH>(dO, p.gout + (int64_t)bi * tq * p.ldo + hoff, p.ldo, tq);
+  stage<TT, L8, NTH>(Q, p.q + qb * p.ldq + hoff, p.ldq, tq);
+  stage<TT, L8, NTH>(K, p.k + kb * p.ldk + hoff, p.ldk, tk);
+  stage<TT, L4, NTH>(V, p.v + kb * p.ldk + hoff, p.ldk, tk);
+  stage<TT, L4, NTH>(dO, p.gout + qb * p.ldo + hoff, p.ldo, tq);
   {
-    const float* gP = p.probs + ((int64_t)bi * p.heads + h) * tq * tk;
+    const float* gP = p.probs + ((int64_t)bi * p.heads + h) * p.tq * p.tk;
     // thread covers column c = tid % TT of rows tid / TT + 4i
     const int c = threadIdx.x % TT, rb = threadIdx.x / TT;
 #pragma unroll
     for(int i = 0; i < TT / 4; ++i) {
       const int r = rb + 4 * i;
       const bool ok = r < tq && c < tk;
-      cp_async4(P + r * LP + c, gP + (ok ? r * tk + c : 0), ok);
+      cp_async4(P + r * LP + c, gP + (ok ? r * p.tk + c : 0), ok);
     }
   }
   if(p.colpart)
@@ -431,7 +452,7 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_bwd_kernel(TcAttBP p) {
       for(int jd = 0; jd < NJ; ++jd)
         mma8(o[jd], a0, a1, a2, a3, tf32(Kr[jd * 8]), tf32(Kr[jd * 8 + 4 * L8]));
     }
-    float* gq = p.gq + (int64_t)bi * tq * p.ldq + hoff + half * 32;
+    float* gq = p.gq + qb * p.ldq + hoff + half * 32;
 #pragma unroll
     for(int jd = 0; jd < NJ; ++jd) {
       const int col = jd * 8 + 2 * t;
@@ -468,8 +489,8 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_bwd_kernel(TcAttBP p) {
         mma8(ov[jd], p0, p1, p2, p3, tf32(Or[jd * 8]), tf32(Or[jd * 8 + 4 * L4]));
       }
     }
-    float* gk = p.gk + (int64_t)bi * tk * p.ldk + hoff + half * 32;
-    float* gv = p.gv + (int64_t)bi * tk * p.ldk + hoff + half * 32;
+    float* gk = p.gk + kb * p.ldk + hoff + half * 32;
+    float* gv = p.gv + kb * p.ldk + hoff + half * 32;
 #pragma unroll
     for(int jd = 0; jd < NJ; ++jd) {
       const int col = jd * 8 + 2 * t;
@@ -520,6 +541,10 @@ int set_smem_attr(const void* fn, size_t bytes) {
       "cudaFuncSetAttribute(attention_tc)");
 }
 
+// varlen offsets of the current call (set by the _varlen entry points)
+thread_local const int* g_qoff = nullptr;
+thread_local const int* g_koff = nullptr;
+
 }  // namespace
 
 extern "C" {
@@ -543,7 +568,7 @@ int mtkc_attention_tc(float* out, int64_t ldo, float* probs, const float* q, int
     prof.detail = "tcfwd_b" + std::to_string(b) + "_tq" + std::to_string(tq) + "_tk" +
                   std::to_string(tk);
   TcAttP p{out, ldo, probs, q, ldq, k, v, ldk, key_mask, (int)tq, (int)tk, heads, scale, causal,
-           flags};
+           flags, g_qoff, g_koff};
   dim3 grid((unsigned)heads, (unsigned)b);
 #define MTKC_TC_FWD(TTV)                                                          \
   if(tt == TTV) {                                                                 \
@@ -575,7 +600,7 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
     prof.detail = "tcbwd_b" + std::to_string(b) + "_tq" + std::to_string(tq) + "_tk" +
                   std::to_string(tk);
   TcAttBP p{gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, (int)tq, (int)tk, heads, scale,
-            accumulate_q, accumulate_k, accumulate_v, colpart};
+            accumulate_q, accumulate_k, accumulate_v, colpart, g_qoff, g_koff};
   dim3 grid((unsigned)heads, (unsigned)b);
 #define MTKC_TC_BWD(TTV)                                                          \
   if(tt == TTV) {                                                                 \
@@ -588,6 +613,35 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
 #undef MTKC_TC_BWD
   MTKC_POST_LAUNCH("attn_tc_bwd_kernel");
   return MTKC_OK;
+}
+
+int mtkc_attention_tc_varlen(float* out, int64_t ldo, float* probs, const float* q, int64_t ldq,
+                             const float* k, const float* v, int64_t ldk, const int32_t* qoff,
+                             const int32_t* koff, int64_t b, int64_t tq_max, int64_t tk_max,
+                             int heads, int64_t dk, float scale, int causal, int* flags,
+                             void* stream) {
+  g_qoff = qoff;
+  g_koff = koff;
+  int rc = mtkc_attention_tc(out, ldo, probs, q, ldq, k, v, ldk, nullptr, b, tq_max, tk_max,
+                             heads, dk, scale, causal, flags, stream);
+  g_qoff = g_koff = nullptr;
+  return rc;
+}
+
+int mtkc_attention_tc_varlen_backward(const float* gout, int64_t ldo, const float* probs,
+                                      const float* q, int64_t ldq, const float* k,
+                                      const float* v, int64_t ldk, float* gq, float* gk,
+                                      float* gv, const int32_t* qoff, const int32_t* koff,
+                                      int64_t b, int64_t tq_max, int64_t tk_max, int heads,
+                                      int64_t dk, float scale, int accumulate_q,
+                                      int accumulate_k, int accumulate_v, void* stream) {
+  g_qoff = qoff;
+  g_koff = koff;
+  int rc = mtkc_attention_tc_backward(gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, b,
+                                      tq_max, tk_max, heads, dk, scale, accumulate_q,
+                                      accumulate_k, accumulate_v, nullptr, stream);
+  g_qoff = g_koff = nullptr;
+  return rc;
 }
 
 }  // extern "C"

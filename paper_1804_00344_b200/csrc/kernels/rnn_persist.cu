@@ -98,12 +98,13 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 }
 
 // all CTAs of one direction group; counter is monotonic (epoch = phases * n)
+// (bar.sync orders the CTA's writes before thread 0's release; the release
+// reduction is cumulative at gpu scope, the acquire load pairs with it)
 __device__ __forceinline__ void grid_bar(unsigned* ctr, unsigned n, unsigned& epoch) {
   __syncthreads();
   if(threadIdx.x == 0) {
     epoch += n;
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    atomicAdd(ctr, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
     while(ld_acquire(ctr) < epoch)
       ;
   }
@@ -673,6 +674,12 @@ __global__ void __launch_bounds__(RT, 1)
   const int K = D.nblocks;
   const int mT = (int)((b + 127) / 128);
 
+  if(p.prof) {  // barrier microbenchmark: 200 back-to-back barriers
+    mark(p.prof, npf, 7);
+    for(int q = 0; q < 200; ++q)
+      grid_bar(ctr, gs, epoch);
+    mark(p.prof, npf, 5);
+  }
   for(int64_t i = 0; i < T; ++i) {
     const int64_t t = D.reverse ? T - 1 - i : i;
     const int64_t hp = D.reverse ? t + 1 : t, hs = D.reverse ? t : t + 1;
@@ -1616,9 +1623,9 @@ int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream) {
       sum[k] += (double)(h[2 * i + 3] - h[2 * i + 1]);
       cnt[k] += 1;
     }
-    const char* nm[8] = {"prod-hU", "pw", "prod-q", "att", "prod-hU+ctxW", "barrier", "end", "-"};
+    const char* nm[8] = {"prod-hU", "pw", "prod-q", "att", "prod-hU+ctxW", "barrier", "end", "200bars"};
     fprintf(stderr, "[rnn prof] ndir %d b %lld T %lld:", a->ndir, (long long)b, (long long)T);
-    for(int k = 0; k < 6; ++k)
+    for(int k = 0; k < 8; ++k)
       if(cnt[k] > 0)
         fprintf(stderr, " %s %.0f x %.2f us", nm[k], cnt[k], sum[k] / cnt[k] / 1e3);
     fprintf(stderr, "\n");
