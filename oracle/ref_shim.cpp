@@ -113,6 +113,14 @@ void* ref_examples_create(int64_t n, const int32_t* srcTok, const int64_t* srcOf
   return h;
 }
 
+// extra source streams (ape-dual / custom multi-source models): stream s of
+// example i is tokens [off[s*(n+1)+i], off[s*(n+1)+i+1]) of tok
+void ref_examples_add_stream(void* h, int64_t n, const int32_t* tok, const int64_t* off) {
+  auto* e = static_cast<RefExamples*>(h);
+  for(int64_t i = 0; i < n; ++i)
+    e->ex[(size_t)i].sources.emplace_back(tok + off[i], tok + off[i + 1]);
+}
+
 void ref_examples_free(void* h) { delete static_cast<RefExamples*>(h); }
 
 // -------------------------------------------------------------- batches

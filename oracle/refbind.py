@@ -46,6 +46,7 @@ def lib():
         sig = {
             "ref_last_error": (C.c_char_p, []),
             "ref_examples_create": (P, [I64, ip, lp, ip, lp]),
+            "ref_examples_add_stream": (None, [P, I64, ip, lp]),
             "ref_examples_free": (None, [P]),
             "ref_batches_make": (P, [P, I64, U64, I]),
             "ref_batches_count": (I64, [P]),
@@ -127,7 +128,7 @@ def _dims(a):
 class Examples:
     """vector<Example> with one source stream (data.h:38-44)."""
 
-    def __init__(self, sources, targets):
+    def __init__(self, sources, targets, extra_streams=()):
         src = [np.asarray(s, dtype=np.int32) for s in sources]
         tgt = [np.asarray(t, dtype=np.int32) for t in targets]
         soff = np.zeros(len(src) + 1, dtype=np.int64)
@@ -138,6 +139,12 @@ class Examples:
         tflat = np.concatenate(tgt).astype(np.int32) if toff[-1] else np.zeros(1, np.int32)
         self.h = lib().ref_examples_create(len(src), _i(sflat), _l(soff), _i(tflat), _l(toff))
         self.n = len(src)
+        for stream in extra_streams:  # further source streams (multi-source models)
+            xs = [np.asarray(x, dtype=np.int32) for x in stream]
+            xoff = np.zeros(len(xs) + 1, dtype=np.int64)
+            xoff[1:] = np.cumsum([len(x) for x in xs])
+            xflat = np.concatenate(xs).astype(np.int32)
+            lib().ref_examples_add_stream(self.h, len(xs), _i(xflat), _l(xoff))
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

@@ -305,13 +305,16 @@ PYBIND11_MODULE(_mtk, m) {
 
   // ---------------------------------------------------------- data
   py::class_<Examples>(m, "Examples")
-      .def(py::init([](py::list sources, py::list targets) {
+      .def(py::init([](py::list sources, py::list targets, py::list extra) {
              Examples e;
              size_t n = py::len(sources);
              e.ex.resize(n);
              for(size_t i = 0; i < n; ++i) {
                auto s = sources[i].cast<std::vector<int32_t>>();
                e.ex[i].sources = {s};
+               for(auto stream : extra)  // further source streams (multi-source models)
+                 e.ex[i].sources.push_back(
+                     stream.cast<py::list>()[i].cast<std::vector<int32_t>>());
                if(py::len(targets)) {
                  e.ex[i].target = targets[i].cast<std::vector<int32_t>>();
                  e.ex[i].hasTarget = true;
@@ -319,7 +322,8 @@ PYBIND11_MODULE(_mtk, m) {
                e.ex[i].id = i;
              }
              return e;
-           }))
+           }),
+           py::arg("sources"), py::arg("targets"), py::arg("extra_streams") = py::list())
       .def("__len__", [](const Examples& e) { return e.ex.size(); });
 
   // SURVEY.md 8(d) synthetic generator (same formula as synth.py)
