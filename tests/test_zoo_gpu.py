@@ -1,5 +1,7 @@
 """Remaining model zoo (row f4; reference models.cpp:504-623, 678-745):
-`lm` (decoder only, no encoder), `ape-dual` (two deep RNN encoders over two
+`lm` (decoder only, no encoder), `hard-att` (monotone hard attention: the
+gate is realised mid-graph and read on the host to move each row's source
+pointer), `ape-dual` (two deep RNN encoders over two
 source streams, one deep RNN decoder), and `custom` compositions (comma-
 separated encoder kinds + a decoder kind: multi-source Transformer and
 mixed Transformer/RNN encoders feeding an RNN decoder through the ctxW
@@ -31,6 +33,8 @@ def cfg_text(arch, vocab=300, emb=32, state=48, heads=2, layers=1, layer_norm=0,
 
 CASES = {
     "lm": (cfg_text("lm"), 1),
+    "hard-att": (cfg_text("hard-att"), 1),
+    "hard-att-ln": (cfg_text("hard-att", layer_norm=1), 1),
     "ape-dual": (cfg_text("ape-dual", layer_norm=1, arity=2), 2),
     "custom-tf2": (cfg_text("custom", emb=64, state=64, enc="transformer,transformer",
                             dec="transformer", arity=2), 2),
