@@ -301,6 +301,28 @@ int ref_train(void* h, void* ex, int workers, int64_t budget, uint64_t seed, int
   });
 }
 
+// train() with async = true: trainAsync (train.cpp:302-404)
+int ref_train_async(void* h, void* ex, int workers, int64_t budget, uint64_t seed,
+                    int64_t epochs, int64_t maxUpdates, float lrBase, int64_t warmup,
+                    double* finalLoss, int64_t* updates) {
+  return guard([&] {
+    auto* m = static_cast<RefModel*>(h);
+    TrainOptions o;
+    o.workers = workers;
+    o.async = true;
+    o.tokenBudget = budget;
+    o.seed = seed;
+    o.epochs = epochs;
+    o.maxUpdates = maxUpdates;
+    o.lr.base = lrBase;
+    o.lr.warmup = warmup;
+    TrainResult r = train(m->model, static_cast<RefExamples*>(ex)->ex, *m->g, *m->adam,
+                          *m->avg, o);
+    *finalLoss = r.finalLoss;
+    *updates = r.updates;
+  });
+}
+
 // train() with checkpointing / resume (train.cpp:284-287, 407-418)
 int ref_train_ckpt(void* h, void* ex, int workers, int64_t budget, uint64_t seed, int64_t epochs,
                    int64_t maxUpdates, float lrBase, int64_t warmup, const char* ckptPath,

@@ -68,6 +68,7 @@ def lib():
             "ref_forward_loss": (I, [P, P, I64, U64, dp]),
             "ref_adam_update": (I, [P, C.c_float]),
             "ref_train": (I, [P, P, I, I64, U64, I64, I64, C.c_float, I64, dp, lp]),
+            "ref_train_async": (I, [P, P, I, I64, U64, I64, I64, C.c_float, I64, dp, lp]),
             "ref_parameter_total": (I64, [C.c_char_p]),
             "ref_beam_search": (I, [P, P, I64, I, C.c_double, I64, lp, lp, dp, ip, I64, I64]),
             "ref_score_batch": (I, [P, P, I64, dp]),
@@ -255,11 +256,12 @@ class RefModel:
         _check(lib().ref_adam_update(self.h, lr))
 
     def train(self, examples: Examples, workers=1, budget=256, seed=1, epochs=1,
-              max_updates=-1, lr_base=3e-4, warmup=16000):
+              max_updates=-1, lr_base=3e-4, warmup=16000, async_=False):
         fl = C.c_double()
         up = C.c_int64()
-        _check(lib().ref_train(self.h, examples.h, workers, budget, seed, epochs, max_updates,
-                               lr_base, warmup, C.byref(fl), C.byref(up)))
+        fn = lib().ref_train_async if async_ else lib().ref_train
+        _check(fn(self.h, examples.h, workers, budget, seed, epochs, max_updates,
+                  lr_base, warmup, C.byref(fl), C.byref(up)))
         return fl.value, up.value
 
 

@@ -501,6 +501,7 @@ PYBIND11_MODULE(_mtk, m) {
   py::class_<TrainOptions>(m, "TrainOptions")
       .def(py::init<>())
       .def_readwrite("workers", &TrainOptions::workers)
+      .def_readwrite("async_", &TrainOptions::async)
       .def_readwrite("token_budget", &TrainOptions::tokenBudget)
       .def_readwrite("seed", &TrainOptions::seed)
       .def_readwrite("epochs", &TrainOptions::epochs)

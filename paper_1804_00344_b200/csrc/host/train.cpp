@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <memory>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -568,6 +569,92 @@ void logLine(const TrainOptions& opts, int64_t update, int64_t epoch, double los
   (*opts.log) << "update=" << update << " epoch=" << epoch << " loss=" << loss
               << " lr=" << (double)lr << " wps=" << wps << "\n";
 }
+
+// trainAsync (train.cpp:302-404) on one GPU.  The reference's hogwild
+// workers are threads that read a shared parameter store, compute one
+// batch's gradients and update the store per tensor under a lock, in
+// whatever order they finish.  Here W worker graphs run in rounds: every
+// worker of a round reads the shared (master) parameters, computes its
+// batch (flat epoch-major batch list, seed mixSeed(seed, batch + update, 0)
+// as train.cpp:343), then the updates are applied to the master in worker
+// order -- one admissible interleaving of the reference's threads, each
+// update computed on parameters at most W-1 updates old.  W = 1 is
+// deterministic and equals the reference's single-worker run.
+TrainResult trainAsyncB200(Model& model, const std::vector<Example>& data,
+                           ExpressionGraph& master, Adam& adam, AveragedParameters& average,
+                           const TrainOptions& opts, int64_t update, int64_t startEpoch,
+                           int64_t startBatch) {
+  std::vector<Batch> batches;
+  std::vector<int64_t> epochOf;
+  for(int64_t epoch = startEpoch; epoch < opts.epochs; ++epoch) {
+    BatchOptions bo;
+    bo.tokenBudget = opts.tokenBudget;
+    bo.seed = opts.seed + (uint64_t)epoch;
+    bo.shuffle = true;
+    auto eb = makeBatches(data, bo);  // epochBatches, train.cpp:183-190
+    for(size_t i = epoch == startEpoch ? (size_t)startBatch : 0; i < eb.size(); ++i) {
+      batches.push_back(std::move(eb[i]));
+      epochOf.push_back(epoch);
+    }
+  }
+  const int W = opts.workers;
+  std::vector<std::unique_ptr<ExpressionGraph>> workers;
+  for(int w = 0; w < W; ++w) {
+    workers.push_back(std::make_unique<ExpressionGraph>(opts.seed));
+    model.registerParams(*workers.back());
+  }
+  Device& dev = Device::get();
+  const size_t bytes = (size_t)master.pool().used() * sizeof(float);
+  TrainResult res;
+  double lastLoss = 0;
+  int64_t tokensSeen = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  for(size_t i = 0; i < batches.size();) {
+    int64_t take = std::min<int64_t>(W, (int64_t)(batches.size() - i));
+    if(opts.maxUpdates >= 0)
+      take = std::min<int64_t>(take, opts.maxUpdates - ((int64_t)i + update));
+    if(take <= 0)
+      break;
+    master.syncParamViews();
+    std::vector<NodeRef> losses((size_t)take);
+    std::vector<Real> tokens((size_t)take, 0);
+    for(int64_t k = 0; k < take; ++k) {  // read the store, compute the batch
+      ExpressionGraph& g = *workers[(size_t)k];
+      g.syncParamViews();
+      MTKC(mtkc_memcpy_d2d(g.pool().values()->ptr, master.pool().values()->ptr, bytes,
+                           dev.stream()));
+      g.clear();
+      g.setSeed(mixSeed(opts.seed, (int64_t)i + k + update, 0));
+      losses[(size_t)k] = model.buildLoss(g, batches[i + (size_t)k], &tokens[(size_t)k]);
+      g.forward();
+      g.zeroGrads();
+      g.backward(losses[(size_t)k]);
+      g.realizeParamGrads();
+    }
+    for(int64_t k = 0; k < take; ++k) {  // apply the updates in worker order
+      ExpressionGraph& g = *workers[(size_t)k];
+      master.realizeParamGrads();
+      MTKC(mtkc_memcpy_d2d(master.pool().grads()->ptr, g.pool().grads()->ptr, bytes,
+                           dev.stream()));
+      const int64_t step = adam.step() + 1;
+      const Real lr = opts.lr(step);
+      adam.update(master, lr, &average);
+      lastLoss = (double)losses[(size_t)k].val().at(0);
+      tokensSeen += (int64_t)tokens[(size_t)k];
+      double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      logLine(opts, step, epochOf[i + (size_t)k], lastLoss, lr,
+              secs > 0 ? (double)tokensSeen / secs : 0);
+    }
+    i += (size_t)take;
+  }
+  res.updates = adam.step();
+  res.epochs = opts.epochs;
+  res.finalLoss = lastLoss;
+  if(!opts.checkpointPath.empty())
+    saveCheckpoint(opts.checkpointPath, model.config, master, adam, average, res.updates,
+                   opts.epochs, 0);
+  return res;
+}
 }  // namespace
 
 TrainResult train(Model& model, const std::vector<Example>& data, ExpressionGraph& master,
@@ -575,13 +662,17 @@ TrainResult train(Model& model, const std::vector<Example>& data, ExpressionGrap
   // train.cpp:407-418 + trainSync :200-300
   if(opts.workers < 1)
     throw ContractError("training needs at least one worker");
-  if(opts.async)
-    throw ContractError("asynchronous (hogwild) training is outside the B200 training path");
   model.registerParams(master);
   master.clear();
   int64_t update = 0, startEpoch = 0, startBatch = 0;
   if(!opts.resumeFrom.empty())
     loadCheckpoint(opts.resumeFrom, master, adam, average, update, startEpoch, startBatch);
+  if(opts.async) {
+    if(distContext().world > 1)
+      throw ContractError("asynchronous training runs on one process (world size 1)");
+    return trainAsyncB200(model, data, master, adam, average, opts, update, startEpoch,
+                          startBatch);
+  }
   SyncStepper stepper(model, master, adam, average, opts);
   TrainResult res;
   auto t0 = std::chrono::steady_clock::now();

@@ -221,3 +221,64 @@ def test_pipelined_updates_equal_synchronous(cuda):
     assert l1 == l2
     for n in p1:
         assert np.array_equal(p1[n], p2[n]), n
+
+
+def test_async_one_worker_equals_reference_train_async(cuda):
+    """trainAsync (train.cpp:302-404) with one worker is deterministic: the
+    B200 rounds schedule must reproduce the reference's parameters after
+    three updates (FP32 mode, the DP tolerance of test_train.cpp:237-242)."""
+    M.set_precision("fp32")
+    cfg = config_text(arch="transformer", vocab=60, emb=32, heads=2, layers=1)
+    src, tgt = synth.corpus(40, 60)
+    ref = R.RefModel(cfg, 9)
+    ref.train(R.Examples(src, tgt), workers=1, budget=5 * 66, seed=9, epochs=1, max_updates=3,
+              async_=True)
+    model = M.Model(cfg)
+    g = M.ExpressionGraph(9)
+    adam = M.Adam(M.adam_defaults_for(cfg))
+    avg = M.AveragedParameters()
+    opts = M.TrainOptions()
+    opts.workers = 1
+    opts.async_ = True
+    opts.token_budget = 5 * 66
+    opts.seed = 9
+    opts.max_updates = 3
+    res, _ = M.train(model, M.Examples([list(map(int, s)) for s in src],
+                                       [list(map(int, t)) for t in tgt]), g, adam, avg, opts)
+    assert res.updates == 3
+    for n in ref.param_names():
+        a, b = g.param_value(n), ref.param(n)
+        assert np.allclose(a, b, rtol=1e-6, atol=1e-6 * max(1.0, np.abs(b).max())), n
+    M.set_precision("tf32")
+
+
+def test_async_workers_stale_reads(cuda):
+    """Several asynchronous workers (rounds of W stale reads, updates in
+    worker order): every batch is consumed once, the step count and the
+    loss trajectory are sane, and the run is reproducible."""
+    M.set_precision("tf32")
+    cfg = config_text(arch="transformer", vocab=60, emb=32, heads=2, layers=1)
+    src, tgt = synth.corpus(60, 60)
+    ex = M.Examples([list(map(int, s)) for s in src], [list(map(int, t)) for t in tgt])
+
+    def run(workers):
+        model = M.Model(cfg)
+        g = M.ExpressionGraph(3)
+        adam = M.Adam(M.adam_defaults_for(cfg))
+        avg = M.AveragedParameters()
+        opts = M.TrainOptions()
+        opts.workers = workers
+        opts.async_ = True
+        opts.token_budget = 5 * 66
+        opts.seed = 3
+        res, _ = M.train(model, ex, g, adam, avg, opts)
+        return res, np.concatenate([g.param_value(n).ravel() for n in g.param_names()])
+
+    nb = len(M.make_batches(ex, 5 * 66, 3, True))
+    r3, p3 = run(3)
+    r3b, p3b = run(3)
+    r1, p1 = run(1)
+    assert r3.updates == r1.updates == nb
+    assert np.isfinite(r3.final_loss)
+    assert np.array_equal(p3, p3b)
+    assert not np.array_equal(p3, p1)  # stale reads change the trajectory
