@@ -454,6 +454,16 @@ typedef struct mtkc_gru_args {
 int mtkc_gru_forward(const mtkc_gru_args* a, void* stream);
 int mtkc_gru_backward(const mtkc_gru_args* a, void* stream);
 
+/* Fused LSTM cell pointwise (north_star "fused GRU/LSTM cell ops"; the
+ * reference has no LSTM -- pinned against a composition of its primitives).
+ * pre [b x 4d] = h*U + x*W (gate blocks i, f, o, g), bias [4d], c [b x d];
+ * out [b x 2d] = [h' | c'], cache [b x 5d] = [i | f | o | g | tanh(c')].
+ * Backward: gout [b x 2d] -> dpre [b x 4d] (written), dc (+)= d(c) or NULL. */
+int mtkc_lstm_forward(const float* pre, const float* bias, const float* c, float* out,
+                      float* cache, int64_t b, int64_t d, void* stream);
+int mtkc_lstm_backward(const float* gout, const float* cache, const float* c, float* dpre,
+                       float* dc, int accumulate_c, int64_t b, int64_t d, void* stream);
+
 /* ======================================================================== */
 /* Persistent GRU scan (sequence-level recurrence of RnnEncoder::build and   */
 /* RnnDecoder::step, models.cpp:146-187, 312-382; DeepTransitionCell         */

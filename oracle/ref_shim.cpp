@@ -738,6 +738,10 @@ extern "C" int ref_op_program(const char* prog, int nin, const int* ranks, const
         stack.push_back(g.reduce(ro, pop(), std::stoi(f.at(2)), std::stoi(f.at(3)) != 0));
       } else if(op == "softmax") {
         stack.push_back(g.softmax(pop()));
+      } else if(op == "dot") {  // dot[:transA:transB] (graph.cpp:293-332)
+        NodeRef b = pop(), a = pop();
+        const bool ta = f.size() > 1 && f[1] == "1", tb = f.size() > 2 && f[2] == "1";
+        stack.push_back(g.dot(a, b, ta, tb));
       } else {
         throw ContractError("op program: unknown token " + tok);
       }

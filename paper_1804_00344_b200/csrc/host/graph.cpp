@@ -1634,6 +1634,90 @@ NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef k, NodeRef v,
   return addNode(std::move(n));
 }
 
+// ------------------------------------------------------------- LSTM cell
+
+namespace {
+struct LstmAux {
+  Tensor pre, cache;
+};
+}  // namespace
+
+NodeRef ExpressionGraph::lstmCell(NodeRef x, NodeRef h, NodeRef c, NodeRef W, NodeRef U,
+                                  NodeRef bias) {
+  for(const NodeRef* r : {&x, &h, &c, &W, &U, &bias})
+    checkRef(*r);
+  const int64_t b = h.shape[0], d = h.shape.back(), in = x.shape.back();
+  if(h.shape.rank() != 2 || c.shape != h.shape || x.shape.rank() != 2 || x.shape[0] != b ||
+     W.shape != Shape({in, 4 * d}) || U.shape != Shape({d, 4 * d}) || bias.shape.size() != 4 * d)
+    throw DimensionError("lstmCell shapes: x " + x.shape.str() + " h " + h.shape.str() + " c " +
+                         c.shape.str() + " W " + W.shape.str() + " U " + U.shape.str());
+  Node n;
+  n.op = "lstmCell";
+  n.shape = Shape({b, 2 * d});
+  n.inputs = {x.index, h.index, c.index, W.index, U.index, bias.index};
+  auto aux = std::make_shared<LstmAux>();
+  n.aux = aux;
+  n.fwd = [=](ExpressionGraph& g, Node& n) {
+    aux->pre = g.allocTensor(Shape({b, 4 * d}));
+    aux->cache = g.allocTensor(Shape({b, 5 * d}));
+    float* pre = aux->pre.dev();
+    // h*U first, then x*W accumulated into the same buffer (gruPre's order)
+    gemm(b, 4 * d, d, g.valPtr(n.inputs[1]), d, false, g.valPtr(n.inputs[4]), 4 * d, false, pre,
+         4 * d, 0.f);
+    gemm(b, 4 * d, in, g.valPtr(n.inputs[0]), in, false, g.valPtr(n.inputs[3]), 4 * d, false, pre,
+         4 * d, 1.f);
+    MTKC(mtkc_lstm_forward(pre, g.valPtr(n.inputs[5]), g.valPtr(n.inputs[2]), n.value.dev(),
+                           aux->cache.dev(), b, d, stream()));
+  };
+  n.bwd = [=](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    Tensor dpre = g.allocTensor(Shape({b, 4 * d}));
+    const bool needC = g.node(g.resolve(n.inputs[2])).needsGrad;
+    ExpressionGraph::GradDst dc{};
+    if(needC)
+      dc = g.gradDst(n.inputs[2]);
+    MTKC(mtkc_lstm_backward(go, aux->cache.devc(), g.valPtr(n.inputs[2]), dpre.dev(),
+                            needC ? dc.ptr : nullptr, needC ? dc.accumulate : 0, b, d, stream()));
+    const float* dp = dpre.devc();
+    auto want = [&](int slot) { return g.node(g.resolve(n.inputs[(size_t)slot])).needsGrad; };
+    if(want(0)) {  // dx += dpre W^T
+      auto dx = g.gradDst(n.inputs[0]);
+      gemm(b, in, 4 * d, dp, 4 * d, false, g.valPtr(n.inputs[3]), 4 * d, true, dx.ptr, in,
+           dx.accumulate ? 1.f : 0.f);
+    }
+    if(want(1)) {  // dh += dpre U^T
+      auto dh = g.gradDst(n.inputs[1]);
+      gemm(b, d, 4 * d, dp, 4 * d, false, g.valPtr(n.inputs[4]), 4 * d, true, dh.ptr, d,
+           dh.accumulate ? 1.f : 0.f);
+    }
+    if(want(3)) {  // dW += x^T dpre
+      auto dW = g.gradDst(n.inputs[3]);
+      gemm(in, 4 * d, b, g.valPtr(n.inputs[0]), in, true, dp, 4 * d, false, dW.ptr, 4 * d,
+           dW.accumulate ? 1.f : 0.f);
+    }
+    if(want(4)) {  // dU += h^T dpre
+      auto dU = g.gradDst(n.inputs[4]);
+      gemm(d, 4 * d, b, g.valPtr(n.inputs[1]), d, true, dp, 4 * d, false, dU.ptr, 4 * d,
+           dU.accumulate ? 1.f : 0.f);
+    }
+    if(want(5)) {  // db += colsum(dpre)
+      auto db = g.gradDst(n.inputs[5]);
+      Device& dev = Device::get();
+      MTKC(mtkc_colsum(db.ptr, dp, b, 4 * d, db.accumulate, dev.scratch(64 << 20),
+                       dev.scratchBytes(), stream()));
+    }
+  };
+  return addNode(std::move(n));
+}
+
+NodeRef ExpressionGraph::lstmState(NodeRef cell) {
+  return slice(cell, 1, 0, cell.shape[1] / 2);
+}
+
+NodeRef ExpressionGraph::lstmCellState(NodeRef cell) {
+  return slice(cell, 1, cell.shape[1] / 2, cell.shape[1] / 2);
+}
+
 // -------------------------------------------------------------- dropout
 
 

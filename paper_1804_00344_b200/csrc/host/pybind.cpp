@@ -264,6 +264,9 @@ PYBIND11_MODULE(_mtk, m) {
       .def("dropout_mask",
            [](G& g, py::sequence shape, float p) { return g.dropoutMask(shapeOf(shape), p); })
       .def("residual_add", &G::residualAdd, py::arg("r"), py::arg("z"))
+      .def("lstm_cell", &G::lstmCell)
+      .def("lstm_state", &G::lstmState)
+      .def("lstm_cell_state", &G::lstmCellState)
       .def("cross_entropy",
            [](G& g, NodeRef l, IArr targets, py::object mask) {
              return g.crossEntropy(l, intMatOf(targets),
