@@ -1004,7 +1004,8 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   const int minKb = tiles * 4 <= sms ? 4 : 24;
   if(a.workspace && numKb >= 2 * minKb && !a.relu_mask_out) {  // masks: no split
     double best = (double)tiles / (double)(sms * cdiv(tiles, sms));
-    for(int s = 2; s <= 16 && numKb / s >= minKb; ++s) {
+    static const int maxSplit = getenv("MTK_GEMM_MAXSPLIT") ? atoi(getenv("MTK_GEMM_MAXSPLIT")) : 8;
+    for(int s = 2; s <= maxSplit && numKb / s >= minKb; ++s) {
       size_t need = (size_t)s * nOut * ((size_t)a.M * (size_t)a.N + (csOp ? csLen * csTiles : 0)) *
                     sizeof(float);
       if(need > a.workspace_bytes)
