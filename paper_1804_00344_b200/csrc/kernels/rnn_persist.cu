@@ -68,6 +68,12 @@ struct KP {
   float* partQ;      // [KCq][b][a]
   unsigned* ctr;     // [2] grid-barrier counters (zeroed before launch)
   unsigned long long* prof;  // MTK_RNN_PROF: CTA 0's phase timestamps, or NULL
+  // attention row teams: `team` CTAs per batch row (positions / columns
+  // split between them), synchronised per row through teamCtr[r]; scratch
+  // teamBuf [b x S] exchanges the scores
+  int team;
+  unsigned* teamCtr;
+  float* teamBuf;
   int KCh, KCx, KCq, NTq;
 };
 
@@ -95,6 +101,18 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// the `team` CTAs working on one batch row: release-add, acquire-spin
+__device__ __forceinline__ void team_bar(unsigned* ctr, unsigned n, unsigned& epoch) {
+  __syncthreads();
+  if(threadIdx.x == 0) {
+    epoch += n;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    while(ld_acquire(ctr) < epoch)
+      ;
+  }
+  __syncthreads();
 }
 
 // all CTAs of one direction group; counter is monotonic (epoch = phases * n)
@@ -459,7 +477,11 @@ __device__ void gru_row(const KP& p, const mtkc_rnn_dir& D, int k, int64_t t, in
 // together), masked softmax, context (float4 columns, positions unrolled).
 constexpr int AQ = MAXA / 128;  // float4 groups per lane over the attention width
 
-__device__ void att_row(const KP& p, int64_t t, int64_t r, float* sW, float* sE, float* sP) {
+// Team member `m` of `P` (P CTAs per row, P = 1 without teams): scores of
+// the positions j = m, m+P, ... then (P > 1) a team barrier, then the
+// context columns of its 1/P share.
+__device__ void att_row(const KP& p, int64_t t, int64_t r, int m, int P, unsigned& tepoch,
+                        float* sW, float* sE, float* sP) {
   const mtkc_rnn_scan_args& a = p.a;
   const int64_t b = a.b, A = a.a, S = a.S, KD = a.kd, A4 = A / 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,12 +491,13 @@ __device__ void att_row(const KP& p, int64_t t, int64_t r, float* sW, float* sE,
     for(int kc = 0; kc < p.KCq; ++kc)
       add4(v, ldcg4(p.partQ + ((int64_t)kc * b + r) * A + 4 * c4));
     st4(sW + 4 * c4, v);
-    st4(a.wq + tr * A + 4 * c4, v);
+    if(m == 0)
+      st4(a.wq + tr * A + 4 * c4, v);
   }
   __syncthreads();
   const bool ln = a.attLnG != nullptr;
   const int nq = (int)((A4 + 31) / 32);  // groups per lane (<= AQ)
-  for(int64_t j = warp; j < S; j += RT / 32) {
+  for(int64_t j = m + (int64_t)warp * P; j < S; j += (int64_t)(RT / 32) * P) {
     const int64_t rj = r * S + j;    // row of uk / keys
     const int64_t trj = tr * S + j;  // row of the per-step caches
     const float* uk = a.uk + rj * A;
@@ -544,38 +567,49 @@ __device__ void att_row(const KP& p, int64_t t, int64_t r, float* sW, float* sE,
       st4(a.attT + trj * A + c, th);
     }
     acc = warp_sum(acc);
-    if(lane == 0)
+    if(lane == 0) {
       sE[j] = acc;
+      if(P > 1)
+        p.teamBuf[r * S + j] = acc;
+    }
+  }
+  if(P > 1) {  // every member needs all scores
+    team_bar(p.teamCtr + r, (unsigned)P, tepoch);
+    for(int64_t j = threadIdx.x; j < S; j += RT)
+      sE[j] = __ldcg(p.teamBuf + r * S + j);
   }
   __syncthreads();
   if(warp == 0) {  // masked softmax over positions (tensor.cpp:393-440)
-    const float* m = a.attMask ? a.attMask + r * S : nullptr;
+    const float* mk = a.attMask ? a.attMask + r * S : nullptr;
     float mx = -INFINITY;
     int any = 0;
     for(int64_t j = lane; j < S; j += 32)
-      if(!m || m[j] != 0.f) {
+      if(!mk || mk[j] != 0.f) {
         mx = fmaxf(mx, sE[j]);
         any = 1;
       }
     mx = warp_max(mx);
     any = __any_sync(0xffffffffu, any);
-    if(!any && lane == 0 && a.flags)
+    if(!any && lane == 0 && a.flags && m == 0)
       atomicOr(a.flags, MTKC_FLAG_MASKED_ROW);
     float sum = 0.f;
     for(int64_t j = lane; j < S; j += 32)
-      if(!m || m[j] != 0.f)
+      if(!mk || mk[j] != 0.f)
         sum += expf(sE[j] - mx);
     sum = warp_sum(sum);
     for(int64_t j = lane; j < S; j += 32) {
-      const float y = (any && (!m || m[j] != 0.f)) ? expf(sE[j] - mx) / sum : 0.f;
+      const float y = (any && (!mk || mk[j] != 0.f)) ? expf(sE[j] - mx) / sum : 0.f;
       sP[j] = y;
-      a.attWts[tr * S + j] = y;
+      if(m == 0)
+        a.attWts[tr * S + j] = y;
     }
   }
   __syncthreads();
-  // context: sum over positions in ascending order, 4 positions' loads in flight
+  // context: sum over positions in ascending order, 4 positions' loads in
+  // flight; this member's share of the columns
   const float* keys = a.keys + r * S * KD;
-  for(int64_t k4 = threadIdx.x; k4 < KD / 4; k4 += RT) {
+  const int64_t K4 = KD / 4, kb = K4 * m / P, ke = K4 * (m + 1) / P;
+  for(int64_t k4 = kb + threadIdx.x; k4 < ke; k4 += RT) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     int64_t j = 0;
     for(; j + 4 <= S; j += 4) {
@@ -669,6 +703,7 @@ __global__ void __launch_bounds__(RT, 1)
   unsigned* ctr = p.ctr + dir;
   unsigned epoch = 0;
   uint32_t ring = 0, ucnt = 0;
+  unsigned tepoch = 0;  // team barriers passed (every row of this CTA, in order)
   int npf = 0;
   const int64_t b = a.b, T = a.T, d = a.d, d3 = 3 * d;
   const int K = D.nblocks;
@@ -746,8 +781,8 @@ __global__ void __launch_bounds__(RT, 1)
         mark(p.prof, npf, 5);
         grid_bar(ctr, gs, epoch);
         mark(p.prof, npf, 3);
-        for(int64_t r = gi; r < b; r += gs)
-          att_row(p, t, r, sW, sE, sP);
+        for(int64_t u = gi; u < b * p.team; u += gs)  // team member u % team of row u / team
+          att_row(p, t, u / p.team, (int)(u % p.team), p.team, tepoch, sW, sE, sP);
         mark(p.prof, npf, 5);
         grid_bar(ctr, gs, epoch);
       }
@@ -795,6 +830,9 @@ struct BKP {
   unsigned* ctr;
   unsigned long long* prof;
   int KCb, KCc, KCq, NTb, NTc;
+  int team;           // CTAs per batch row in the attention phase (see KP)
+  unsigned* teamCtr;  // [b]
+  float* teamBuf;     // [b x S x 2]
 };
 
 __device__ void gru_bwd_row(const BKP& p, const mtkc_rnn_dir& D, int dir, int k, int64_t t,
@@ -977,8 +1015,8 @@ __device__ void gru_bwd_row(const BKP& p, const mtkc_rnn_dir& D, int dir, int k,
   }
 }
 
-__device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, float* sC, float* sE,
-                            float* sP, float* sQ) {
+__device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int m, int P,
+                            unsigned& tepoch, float* sC, float* sE, float* sP, float* sQ) {
   const mtkc_rnn_scan_args& a = p.a;
   const int64_t b = a.b, T = a.T, A = a.a, S = a.S, KD = a.kd, A4 = A / 4, K4 = KD / 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -990,12 +1028,14 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, floa
     for(int kc = 0; kc < p.KCc; ++kc)
       add4(v, ldcg4(p.partC + ((int64_t)kc * b + r) * KD + 4 * k4));
     st4(sC + 4 * k4, v);
-    st4(a.dctx + tr * KD + 4 * k4, v);
+    if(m == 0)
+      st4(a.dctx + tr * KD + 4 * k4, v);
   }
   __syncthreads();
   // d(weights)_j = dctx . keys_j  (bahdanau_dw_kernel; the key gradient
-  // sum_t w_tj dctx_t is one batched product after the sweep)
-  for(int64_t j = warp; j < S; j += RT / 32) {
+  // sum_t w_tj dctx_t is one batched product after the sweep); positions
+  // j = m, m+P, ... of this team member
+  for(int64_t j = m + (int64_t)warp * P; j < S; j += (int64_t)(RT / 32) * P) {
     const float* keys = a.keys + (r * S + j) * KD;
     float acc = 0.f;
     for(int64_t c4 = lane; c4 < K4; c4 += 128) {
@@ -1012,8 +1052,16 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, floa
         acc += cv[u].x * kv[u].x + cv[u].y * kv[u].y + cv[u].z * kv[u].z + cv[u].w * kv[u].w;
     }
     acc = warp_sum(acc);
-    if(lane == 0)
+    if(lane == 0) {
       sE[j] = acc;
+      if(P > 1)
+        p.teamBuf[(r * S + j) * 2] = acc;
+    }
+  }
+  if(P > 1) {
+    team_bar(p.teamCtr + r, (unsigned)P, tepoch);
+    for(int64_t j = threadIdx.x; j < S; j += RT)
+      sE[j] = __ldcg(p.teamBuf + (r * S + j) * 2);
   }
   __syncthreads();
   if(warp == 0) {  // softmax backward: de_j = w_j (dw_j - sum_l w_l dw_l)
@@ -1028,7 +1076,7 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, floa
   __syncthreads();
   const bool ln = a.attLnG != nullptr;
   if(ln) {  // LN backward row statistics per position (bahdanau_de_kernel)
-    for(int64_t j = warp; j < S; j += RT / 32) {
+    for(int64_t j = m + (int64_t)warp * P; j < S; j += (int64_t)(RT / 32) * P) {
       const int64_t trj = tr * S + j;
       const float dej = sE[j];
       float s1 = 0.f, s2 = 0.f;
@@ -1049,6 +1097,17 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, floa
       if(lane == 0) {
         sP[j] = s1;
         sQ[j] = s2;
+        if(P > 1) {
+          p.teamBuf[(r * S + j) * 2] = s1;
+          p.teamBuf[(r * S + j) * 2 + 1] = s2;
+        }
+      }
+    }
+    if(P > 1) {
+      team_bar(p.teamCtr + r, (unsigned)P, tepoch);
+      for(int64_t j = threadIdx.x; j < S; j += RT) {
+        sP[j] = __ldcg(p.teamBuf + (r * S + j) * 2);
+        sQ[j] = __ldcg(p.teamBuf + (r * S + j) * 2 + 1);
       }
     }
     __syncthreads();
@@ -1056,7 +1115,8 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, floa
   // per column (bahdanau_cols_kernel): d(uk), d(wq), v / LN partials;
   // four positions' loads in flight
   const bool acc = ii > 0 || a.acc_uk;
-  for(int64_t c4 = threadIdx.x; c4 < A4; c4 += RT) {
+  const int64_t cb = A4 * m / P, ce = A4 * (m + 1) / P;  // this member's columns
+  for(int64_t c4 = cb + threadIdx.x; c4 < ce; c4 += RT) {
     const int64_t c = 4 * c4;
     const float4 vv = ld4(a.attV + c);
     const float vc[4] = {vv.x, vv.y, vv.z, vv.w};
@@ -1170,6 +1230,7 @@ __global__ void __launch_bounds__(RT, 1)
   unsigned* ctr = p.ctr + dir;
   unsigned epoch = 0;
   uint32_t ring = 0, ucnt = 0;
+  unsigned tepoch = 0;
   int npf = 0;
   const int64_t b = a.b, T = a.T, d = a.d, d3 = 3 * d;
   const int K = D.nblocks;
@@ -1225,8 +1286,8 @@ __global__ void __launch_bounds__(RT, 1)
       grid_bar(ctr, gs, epoch);
       if(att1) {
         mark(p.prof, npf, 3);
-        for(int64_t r = gi; r < b; r += gs)
-          att_bwd_row(p, ii, t, r, sC, sE, sP, sQ);
+        for(int64_t u = gi; u < b * p.team; u += gs)
+          att_bwd_row(p, ii, t, u / p.team, (int)(u % p.team), p.team, tepoch, sC, sE, sP, sQ);
         mark(p.prof, npf, 5);
         grid_bar(ctr, gs, epoch);
         Prod Q;
@@ -1372,8 +1433,8 @@ int pick_kc(int nkb, int target) {
 }
 
 struct Plan {
-  int G, gs, KCh, KCx, KCq, NTq;
-  size_t offUT[2], offW2T, offWattT, offPH[2], offPX, offPQ, offCtr, total;
+  int G, gs, KCh, KCx, KCq, NTq, team;
+  size_t offUT[2], offW2T, offWattT, offPH[2], offPX, offPQ, offTeamBuf, offCtr, total;
 };
 
 int grid_size() {
@@ -1417,7 +1478,11 @@ Plan make_plan(const mtkc_rnn_scan_args* a) {
   }
   for(int q = 0; q < a->ndir; ++q)
     P.offPH[q] = take((size_t)P.KCh * b * d3);
-  P.offCtr = take(64);
+  P.team = a->has_att ? std::max(1, P.gs / (int)b) : 1;
+  if(getenv("MTK_RNN_TEAM"))
+    P.team = std::max(1, std::min(P.team, atoi(getenv("MTK_RNN_TEAM"))));
+  P.offTeamBuf = take((size_t)b * std::max<int64_t>(a->S, 1) * 2);
+  P.offCtr = take(64 + (size_t)b);  // grid counters, then one team counter per row
   P.total = off;
   return P;
 }
@@ -1447,8 +1512,8 @@ bool supported(const mtkc_rnn_scan_args* a) {
 
 
 struct BPlan {
-  int G, gs, KCb, KCc, KCq, NTb, NTc;
-  size_t offUH[2], offW2C, offPB[2], offPC, offPQ, offDSD[2], offCtr, total;
+  int G, gs, KCb, KCc, KCq, NTb, NTc, team;
+  size_t offUH[2], offW2C, offPB[2], offPC, offPQ, offDSD[2], offTeamBuf, offCtr, total;
 };
 
 BPlan make_bplan(const mtkc_rnn_scan_args* a) {
@@ -1479,7 +1544,11 @@ BPlan make_bplan(const mtkc_rnn_scan_args* a) {
     P.offPC = take((size_t)P.KCc * b * a->kd);
     P.offPQ = take((size_t)P.KCq * b * d);
   }
-  P.offCtr = take(64);
+  P.team = a->has_att ? std::max(1, P.gs / (int)b) : 1;
+  if(getenv("MTK_RNN_TEAM"))
+    P.team = std::max(1, std::min(P.team, atoi(getenv("MTK_RNN_TEAM"))));
+  P.offTeamBuf = take((size_t)b * std::max<int64_t>(a->S, 1) * 2);
+  P.offCtr = take(64 + (size_t)b);
   P.total = off;
   return P;
 }
@@ -1545,7 +1614,7 @@ int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream) {
     ::mtkc::launch(transpose_jobs_kernel, grid, dim3(32, 8), 0, st, jobs);
     MTKC_POST_LAUNCH("transpose_jobs_kernel");
   }
-  if(cudaError_t e = cudaMemsetAsync(ws + P.offCtr, 0, 256, st))
+  if(cudaError_t e = cudaMemsetAsync(ws + P.offCtr, 0, (64 + (size_t)b) * sizeof(float), st))
     return cuda_status(e, "rnn scan counters");
 
   Maps maps;
@@ -1578,6 +1647,9 @@ int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream) {
   kp.KCx = P.KCx;
   kp.KCq = P.KCq;
   kp.NTq = P.NTq;
+  kp.team = P.team;
+  kp.teamCtr = (unsigned*)(ws + P.offCtr) + 64;
+  kp.teamBuf = (float*)(ws + P.offTeamBuf);
 
   static bool attr = false;
   if(!attr) {
@@ -1668,7 +1740,7 @@ int mtkc_rnn_scan_backward(const mtkc_rnn_scan_args* a, void* stream) {
   }
   ::mtkc::launch(copy_jobs_kernel, dim3(148, (unsigned)jobs.n), 256, 0, st, jobs);
   MTKC_POST_LAUNCH("copy_jobs_kernel");
-  if(cudaError_t e = cudaMemsetAsync(ws + P.offCtr, 0, 256, st))
+  if(cudaError_t e = cudaMemsetAsync(ws + P.offCtr, 0, (64 + (size_t)b) * sizeof(float), st))
     return cuda_status(e, "rnn scan counters");
 
   BMaps maps;
@@ -1703,6 +1775,9 @@ int mtkc_rnn_scan_backward(const mtkc_rnn_scan_args* a, void* stream) {
   kp.KCq = P.KCq;
   kp.NTb = P.NTb;
   kp.NTc = P.NTc;
+  kp.team = P.team;
+  kp.teamCtr = (unsigned*)(ws + P.offCtr) + 64;
+  kp.teamBuf = (float*)(ws + P.offTeamBuf);
   static bool attr = false;
   if(!attr) {
     cudaError_t e = cudaFuncSetAttribute(rnn_scan_bwd_kernel,
