@@ -1016,7 +1016,8 @@ __device__ void gru_bwd_row(const BKP& p, const mtkc_rnn_dir& D, int dir, int k,
 }
 
 __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int m, int P,
-                            unsigned& tepoch, float* sC, float* sE, float* sP, float* sQ) {
+                            unsigned& tepoch, float* sC, float* sE, float* sP, float* sQ,
+                            float* scratch) {
   const mtkc_rnn_scan_args& a = p.a;
   const int64_t b = a.b, T = a.T, A = a.a, S = a.S, KD = a.kd, A4 = A / 4, K4 = KD / 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1116,7 +1117,14 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
   // four positions' loads in flight
   const bool acc = ii > 0 || a.acc_uk;
   const int64_t cb = A4 * m / P, ce = A4 * (m + 1) / P;  // this member's columns
-  for(int64_t c4 = cb + threadIdx.x; c4 < ce; c4 += RT) {
+  // fewer column groups than threads: `sp` thread groups split the positions
+  // of each column (j = part, part + sp, ...), combined in part order below
+  const int64_t Cn = ce - cb;
+  const int sp = Cn >= RT ? 1 : (int)std::min<int64_t>(4, RT / std::max<int64_t>(Cn, 1));
+  const int part = sp > 1 ? (int)(threadIdx.x / Cn) : 0;
+  const int64_t cfirst = sp > 1 ? cb + threadIdx.x % Cn : cb + threadIdx.x;
+  const int64_t cstep = sp > 1 ? ce : RT;  // one column per thread when split
+  for(int64_t c4 = cfirst; part < sp && c4 < ce; c4 += cstep) {
     const int64_t c = 4 * c4;
     const float4 vv = ld4(a.attV + c);
     const float vc[4] = {vv.x, vv.y, vv.z, vv.w};
@@ -1125,11 +1133,11 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
       set4(gc, ld4(a.attLnG + c));
     float awq[4] = {0.f, 0.f, 0.f, 0.f}, av[4] = {0.f, 0.f, 0.f, 0.f};
     float ag[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
-    for(int64_t j0 = 0; j0 < S; j0 += 4) {
+    for(int64_t j0 = part; j0 < S; j0 += 4 * sp) {
       float4 tv[4], xv[4], gv[4];
 #pragma unroll
       for(int u = 0; u < 4; ++u) {
-        const int64_t j = j0 + u;
+        const int64_t j = j0 + u * sp;
         if(j < S) {
           tv[u] = ld4(a.attT + (tr * S + j) * A + c);
           xv[u] = ln ? ld4(a.attLnx + (tr * S + j) * A + c) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1138,7 +1146,7 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
       }
 #pragma unroll
       for(int u = 0; u < 4; ++u) {
-        const int64_t j = j0 + u;
+        const int64_t j = j0 + u * sp;
         if(j >= S)
           break;
         const float dej = sE[j];
@@ -1162,11 +1170,41 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
         st4(a.guk + (r * S + j) * A + c, gu);
       }
     }
+    if(sp > 1) {  // partial sums of this part -> scratch [sp][Cn][16]
+      float* dst = scratch + ((int64_t)part * Cn + (c4 - cb)) * 16;
+      st4(dst, awq);
+      st4(dst + 4, av);
+      st4(dst + 8, ag);
+      st4(dst + 12, ab);
+      continue;
+    }
     st4(a.dwq + tr * A + c, awq);
     st4(a.vpart + tr * A + c, av);
     if(ln) {
       st4(a.vpart + TB * A + tr * A + c, ag);
       st4(a.vpart + 2 * TB * A + tr * A + c, ab);
+    }
+  }
+  if(sp > 1) {
+    __syncthreads();
+    for(int64_t k = threadIdx.x; k < Cn; k += RT) {
+      float q[16];
+      for(int i = 0; i < 16; ++i)
+        q[i] = 0.f;
+      for(int pp = 0; pp < sp; ++pp) {  // fixed part order
+        const float* src = scratch + ((int64_t)pp * Cn + k) * 16;
+        for(int i = 0; i < 16; ++i)
+          q[i] += src[i];
+      }
+      const int64_t c = 4 * (cb + k);
+      const float awq[4] = {q[0], q[1], q[2], q[3]}, av[4] = {q[4], q[5], q[6], q[7]};
+      const float ag[4] = {q[8], q[9], q[10], q[11]}, ab[4] = {q[12], q[13], q[14], q[15]};
+      st4(a.dwq + tr * A + c, awq);
+      st4(a.vpart + tr * A + c, av);
+      if(ln) {
+        st4(a.vpart + TB * A + tr * A + c, ag);
+        st4(a.vpart + 2 * TB * A + tr * A + c, ab);
+      }
     }
   }
   __syncthreads();
@@ -1287,7 +1325,8 @@ __global__ void __launch_bounds__(RT, 1)
       if(att1) {
         mark(p.prof, npf, 3);
         for(int64_t u = gi; u < b * p.team; u += gs)
-          att_bwd_row(p, ii, t, u / p.team, (int)(u % p.team), p.team, tepoch, sC, sE, sP, sQ);
+          att_bwd_row(p, ii, t, u / p.team, (int)(u % p.team), p.team, tepoch, sC, sE, sP, sQ,
+                      (float*)sm.sA);
         mark(p.prof, npf, 5);
         grid_bar(ctr, gs, epoch);
         Prod Q;
