@@ -605,6 +605,13 @@ int mtkc_bahdanau_backward(const mtkc_bahdanau_args* a, void* stream);
 int mtkc_xent_forward(const float* logits, const int32_t* targets, const float* mask,
                       int64_t rows, int64_t vocab, float* lse, float* row_loss, float* loss,
                       float count, void* stream);
+/* Fused forward + backward (TF32 training path, vocab % 4 == 0, vocab <= 32768):
+ * the loss as mtkc_xent_forward and, in place over `logits`, the gradient
+ * (softmax - onehot) * m * scale / count for the loss seed `scale`. */
+int mtkc_xent_fused_supported(int64_t vocab);
+int mtkc_xent_fused(float* logits, const int32_t* targets, const float* mask, int64_t rows,
+                    int64_t vocab, float scale, float* row_loss, float* loss, float count,
+                    void* stream);
 int mtkc_xent_backward(float* glogits, const float* logits, const float* lse,
                        const int32_t* targets, const float* mask, const float* gloss,
                        int64_t rows, int64_t vocab, float count, int accumulate,

@@ -1803,10 +1803,19 @@ struct CeAux {
   Tensor mask, stats, rowLoss;
   bool hasMask = false;
   Real count = 0;
+  // fused forward+backward (crossEntropyFused): the gradient replaced the
+  // logits in the forward, for this loss seed
+  bool fused = false;
+  Real scale = 1;
 };
 }  // namespace
 
 NodeRef ExpressionGraph::crossEntropy(NodeRef logits, const IntMat& targets, const Tensor& mask) {
+  return crossEntropy(logits, targets, mask, false);
+}
+
+NodeRef ExpressionGraph::crossEntropy(NodeRef logits, const IntMat& targets, const Tensor& mask,
+                                      bool fusedBackward) {
   checkRef(logits);
   int64_t vocab = logits.shape.back();
   int64_t positions = logits.shape.size() / vocab;
@@ -1837,11 +1846,26 @@ NodeRef ExpressionGraph::crossEntropy(NodeRef logits, const IntMat& targets, con
   n.shape = Shape({1});
   n.inputs = {logits.index};
   n.aux = aux;
+  // Fused path (TF32 training, the logits' only consumer is this loss and the
+  // loss is the backward root): one pass writes the loss AND the gradient
+  // over the logits for the graph's current loss seed.
+  aux->fused = fusedBackward && Device::get().precision() == Precision::TF32 &&
+               mtkc_xent_fused_supported(vocab) && !inference_ &&
+               !nodes_[(size_t)resolve(logits.index)].isParam;
+  aux->scale = lossScale_;
   n.fwd = [aux, vocab, positions](ExpressionGraph& g, Node& n) {
     if(aux->count == Real(0))
       throw ContractError("cross entropy over a fully-masked batch");
     aux->stats = g.allocTensor(Shape({positions, 2}));
     aux->rowLoss = g.allocTensor(Shape({positions}));
+    if(aux->fused) {
+      Node& L = g.node(g.resolve(n.inputs[0]));
+      MTKC(mtkc_xent_fused(L.value.dev(), (const int32_t*)aux->tg->ptr + aux->tgOff,
+                           aux->hasMask ? aux->mask.devc() : nullptr, positions, vocab,
+                           (float)aux->scale, aux->rowLoss.dev(), n.value.dev(), aux->count,
+                           stream()));
+      return;
+    }
     // TF32 mode: the one-pass kernels (the FP32 path keeps the reference's order)
     const bool fast = Device::get().precision() == Precision::TF32;
     MTKC((fast ? mtkc_xent_forward_fast : mtkc_xent_forward)(g.valPtr(n.inputs[0]), (const int32_t*)aux->tg->ptr + aux->tgOff,
@@ -1850,6 +1874,15 @@ NodeRef ExpressionGraph::crossEntropy(NodeRef logits, const IntMat& targets, con
                            stream()));
   };
   n.bwd = [aux, vocab, positions](ExpressionGraph& g, Node& n) {
+    if(aux->fused) {  // the logits buffer already holds their gradient
+      Node& L = g.node(g.resolve(n.inputs[0]));
+      if(g.lossScale() != aux->scale || L.gradLive || !L.grad.empty())
+        throw ContractError("fused cross entropy: the loss seed changed or the logits have "
+                            "other consumers");
+      L.grad = L.value;
+      L.gradLive = true;
+      return;
+    }
     const float* go = g.gradSrc(n);
     auto d = g.gradDst(n.inputs[0]);
     const bool fast = Device::get().precision() == Precision::TF32;

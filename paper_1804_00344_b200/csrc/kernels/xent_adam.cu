@@ -260,6 +260,69 @@ __global__ void __launch_bounds__(256) xent_bwd_fast_kernel(float* g, const floa
   }
 }
 
+// Fused cross-entropy forward + backward (TF32 training path): one CTA of
+// 1024 threads per row keeps the whole row in registers (V <= 4096*NV), so
+// the logits are read from HBM once: row max, sum of exp (two-pass, the
+// reference's order of operations, graph.cpp:880-922), the row loss, and
+// the gradient d = (exp(x - max)/sum - onehot) * m * scale / count written
+// IN PLACE over the logits (their only consumer is this loss; `scale` is
+// the loss seed the backward would receive).
+constexpr int XF = 1024;
+template <int NV>
+__global__ void __launch_bounds__(XF, 1) xent_fused_kernel(float* logits, const int32_t* tg,
+                                                           const float* mask, int64_t V,
+                                                           float scale, float count,
+                                                           float* rowLoss) {
+  MTKC_PDL_ENTRY();
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  float4* x4 = reinterpret_cast<float4*>(logits + r * V);
+  const int64_t V4 = V / 4;
+  float4 v[NV];
+  float mx = -INFINITY;
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t j = threadIdx.x + (int64_t)k * XF;
+    v[k] = j < V4 ? __ldcs(x4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    mx = fmaxf(mx, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+  }
+  mx = block_max(mx, red);
+  float s = 0.f;
+#pragma unroll
+  for(int k = 0; k < NV; ++k)
+    if(threadIdx.x + (int64_t)k * XF < V4)
+      s += (__expf(v[k].x - mx) + __expf(v[k].y - mx)) + (__expf(v[k].z - mx) + __expf(v[k].w - mx));
+  s = block_sum(s, red);
+  const float m = mask ? mask[r] : 1.f;
+  const int32_t y = tg[r];
+  if(threadIdx.x == 0) {
+    // x[y] is read before any thread overwrites the row: block_sum ends in a barrier
+    rowLoss[r] = m != 0.f ? m * (mx + logf(s) - logits[r * V + y]) : 0.f;
+  }
+  __syncthreads();
+  const float gm = (scale / count) * m;
+  const float sc = m != 0.f ? gm / s : 0.f;
+#pragma unroll
+  for(int k = 0; k < NV; ++k) {
+    const int64_t j = threadIdx.x + (int64_t)k * XF;
+    if(j >= V4)
+      break;
+    float4 o;
+    o.x = sc * __expf(v[k].x - mx);
+    o.y = sc * __expf(v[k].y - mx);
+    o.z = sc * __expf(v[k].z - mx);
+    o.w = sc * __expf(v[k].w - mx);
+    const int64_t dd = (int64_t)y - 4 * j;
+    if(m != 0.f && dd >= 0 && dd < 4) {
+      if(dd == 0) o.x -= gm;
+      if(dd == 1) o.y -= gm;
+      if(dd == 2) o.z -= gm;
+      if(dd == 3) o.w -= gm;
+    }
+    __stcs(x4 + j, o);
+  }
+}
+
 // One element of the reference's Adam + EMA, with separately rounded ops
 // (kernels are compiled with -fmad=false) in the reference's order.
 __device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v, float& a,
@@ -377,6 +440,30 @@ int mtkc_xent_forward_fast(const float* logits, const int32_t* targets, const fl
   ::mtkc::launch(xent_fwd_fast_kernel, (unsigned)rows, XT, 0, S(stream), logits, targets, mask,
                  vocab, lse, row_loss);
   MTKC_POST_LAUNCH("xent_fwd_fast_kernel");
+  ::mtkc::launch(loss_sum_kernel, 1, 1024, 0, S(stream), row_loss, rows, count, loss);
+  MTKC_POST_LAUNCH("loss_sum_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_xent_fused_supported(int64_t vocab) { return vocab % 4 == 0 && vocab <= 4 * XF * 8; }
+
+int mtkc_xent_fused(float* logits, const int32_t* targets, const float* mask, int64_t rows,
+                    int64_t vocab, float scale, float* row_loss, float* loss, float count,
+                    void* stream) {
+  if(rows <= 0)
+    return MTKC_OK;
+  if(!mtkc_xent_fused_supported(vocab) || (uintptr_t)logits % 16)
+    return fail(MTKC_DIMENSION, "fused cross entropy needs vocab % 4 == 0, vocab <= 32768");
+  ProfScope prof(S(stream), "xent", 8.0 * rows * vocab);  // read logits, write dlogits
+  const int nv = (int)cdiv(vocab / 4, XF);
+#define XF_LAUNCH(NVV)                                                                       \
+  if(nv <= NVV) {                                                                            \
+    ::mtkc::launch(xent_fused_kernel<NVV>, (unsigned)rows, XF, 0, S(stream), logits, targets, \
+                   mask, vocab, scale, count, row_loss);                                     \
+  } else
+  XF_LAUNCH(1) XF_LAUNCH(2) XF_LAUNCH(4) XF_LAUNCH(8) {}
+#undef XF_LAUNCH
+  MTKC_POST_LAUNCH("xent_fused_kernel");
   ::mtkc::launch(loss_sum_kernel, 1, 1024, 0, S(stream), row_loss, rows, count, loss);
   MTKC_POST_LAUNCH("loss_sum_kernel");
   return MTKC_OK;
