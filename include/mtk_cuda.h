@@ -389,6 +389,21 @@ int mtkc_attention_tc_varlen(float* out, int64_t ldo, float* probs, const float*
                              const int32_t* koff, int64_t b, int64_t tq_max, int64_t tk_max,
                              int heads, int64_t dk, float scale, int causal, int* flags,
                              void* stream);
+/* Length-bucketed launch of the packed form: only the n_sent sentences
+ * sent_ids[0..n_sent) (device int32), all of length <= tile_len, with the
+ * tile size of tile_len -- short sentences do not pay for the longest one. */
+int mtkc_attention_tc_varlen_ids(float* out, int64_t ldo, float* probs, const float* q,
+                                 int64_t ldq, const float* k, const float* v, int64_t ldk,
+                                 const int32_t* qoff, const int32_t* koff,
+                                 const int32_t* sent_ids, int64_t n_sent, int64_t tile_len,
+                                 int64_t b, int64_t tq_max, int64_t tk_max, int heads, int64_t dk,
+                                 float scale, int causal, int* flags, void* stream);
+int mtkc_attention_tc_varlen_ids_backward(
+    const float* gout, int64_t ldo, const float* probs, const float* q, int64_t ldq,
+    const float* k, const float* v, int64_t ldk, float* gq, float* gk, float* gv,
+    const int32_t* qoff, const int32_t* koff, const int32_t* sent_ids, int64_t n_sent,
+    int64_t tile_len, int64_t b, int64_t tq_max, int64_t tk_max, int heads, int64_t dk,
+    float scale, int accumulate_q, int accumulate_k, int accumulate_v, void* stream);
 int mtkc_attention_tc_varlen_backward(const float* gout, int64_t ldo, const float* probs,
                                       const float* q, int64_t ldq, const float* k,
                                       const float* v, int64_t ldk, float* gq, float* gk,

@@ -1612,24 +1612,48 @@ NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef k, NodeRef v,
   n.aux = aux;
   const float scale = (float)(1.0 / std::sqrt((double)dk));  // layers.cpp:106
   std::shared_ptr<const RowPacking> QP = qp, KP = kp;
+  // sentences bucketed by tile size (16/32/48/64 rows): one launch per
+  // non-empty bucket, each with the smallest tile its sentences fit
+  struct Bucket {
+    int64_t tile, off, n;
+  };
+  std::vector<Bucket> buckets;
+  std::vector<int32_t> ids;
+  for(int64_t tile : {16, 32, 48, 64}) {
+    const int64_t off = (int64_t)ids.size();
+    for(int64_t i = 0; i < b; ++i) {
+      const int64_t L = std::max(qp->off[(size_t)i + 1] - qp->off[(size_t)i],
+                                 kp->off[(size_t)i + 1] - kp->off[(size_t)i]);
+      if(L <= tile && L > tile - 16)
+        ids.push_back((int32_t)i);
+    }
+    if((int64_t)ids.size() > off)
+      buckets.push_back(Bucket{tile, off, (int64_t)ids.size() - off});
+  }
+  int64_t idsOff = 0;
+  auto idsBuf = uploadIntsTo(*this, ids, &idsOff);
   n.fwd = [=](ExpressionGraph& g, Node& n) {
     aux->probs = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));
-    MTKC(mtkc_attention_tc_varlen(n.value.dev(), d, aux->probs.dev(), g.valPtr(n.inputs[0]), d,
-                                  g.valPtr(n.inputs[1]), g.valPtr(n.inputs[2]), d,
-                                  (const int32_t*)QP->dev->ptr + QP->devOff,
-                                  (const int32_t*)KP->dev->ptr + KP->devOff, b, tq, tk, heads, dk,
-                                  scale, causal ? 1 : 0, Device::get().flags(), stream()));
+    for(const Bucket& bk : buckets)
+      MTKC(mtkc_attention_tc_varlen_ids(
+          n.value.dev(), d, aux->probs.dev(), g.valPtr(n.inputs[0]), d, g.valPtr(n.inputs[1]),
+          g.valPtr(n.inputs[2]), d, (const int32_t*)QP->dev->ptr + QP->devOff,
+          (const int32_t*)KP->dev->ptr + KP->devOff,
+          (const int32_t*)idsBuf->ptr + idsOff + bk.off, bk.n, bk.tile, b, tq, tk, heads, dk,
+          scale, causal ? 1 : 0, Device::get().flags(), stream()));
   };
   n.bwd = [=](ExpressionGraph& g, Node& n) {
     const float* go = g.gradSrc(n);
     auto dq = g.gradDst(n.inputs[0]);
     auto dkk = g.gradDst(n.inputs[1]);
     auto dv = g.gradDst(n.inputs[2]);
-    MTKC(mtkc_attention_tc_varlen_backward(
-        go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d, g.valPtr(n.inputs[1]),
-        g.valPtr(n.inputs[2]), d, dq.ptr, dkk.ptr, dv.ptr,
-        (const int32_t*)QP->dev->ptr + QP->devOff, (const int32_t*)KP->dev->ptr + KP->devOff, b,
-        tq, tk, heads, dk, scale, dq.accumulate, dkk.accumulate, dv.accumulate, stream()));
+    for(const Bucket& bk : buckets)  // disjoint rows: every launch keeps the accumulate flags
+      MTKC(mtkc_attention_tc_varlen_ids_backward(
+          go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d, g.valPtr(n.inputs[1]),
+          g.valPtr(n.inputs[2]), d, dq.ptr, dkk.ptr, dv.ptr,
+          (const int32_t*)QP->dev->ptr + QP->devOff, (const int32_t*)KP->dev->ptr + KP->devOff,
+          (const int32_t*)idsBuf->ptr + idsOff + bk.off, bk.n, bk.tile, b, tq, tk, heads, dk,
+          scale, dq.accumulate, dkk.accumulate, dv.accumulate, stream()));
   };
   return addNode(std::move(n));
 }

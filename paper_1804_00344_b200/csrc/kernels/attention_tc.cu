@@ -90,6 +90,7 @@ struct TcAttP {
   // (the probability tensor keeps the padded [b, heads, tq, tk] layout)
   const int* qoff;
   const int* koff;
+  const int* sid;  // sentence of CTA row blockIdx.y (length-bucketed launches), or NULL
 };
 
 struct TcAttBP {
@@ -110,6 +111,7 @@ struct TcAttBP {
   float* colpart;  // optional [3][b][heads*64]: column sums of this CTA's dq/dk/dv
   const int* qoff;  // varlen, as in TcAttP
   const int* koff;
+  const int* sid;
 };
 
 // strides (floats): L4 = 4*odd mod 32 for row-fragment reads (g*L + t),
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_fwd_kernel(TcAttP p) {
   float* V = K + TT * L4;                       // [TT][L8]
   float* mk = V + TT * L8;                      // [TT] key usable (mask)
   float* xch = mk + TT;                         // [2][2][TT] row max / row sum per key half
-  const int h = blockIdx.x, bi = blockIdx.y;
+  const int h = blockIdx.x, bi = p.sid ? p.sid[blockIdx.y] : (int)blockIdx.y;
   int tq = p.tq, tk = p.tk;
   int64_t qb = (int64_t)bi * tq, kb = (int64_t)bi * tk;  // first query / key row
   if(p.qoff) {
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(TT * 4) attn_tc_bwd_kernel(TcAttBP p) {
   float* P = dO + TT * L4;                      // [TT][LP]
   float* Dp = P + TT * LP;                      // [2][TT] row sums of dP*P per key half
   float* csum = Dp + 2 * TT;                    // [3][NWB][64] per-row-block column sums
-  const int h = blockIdx.x, bi = blockIdx.y;
+  const int h = blockIdx.x, bi = p.sid ? p.sid[blockIdx.y] : (int)blockIdx.y;
   int tq = p.tq, tk = p.tk;
   int64_t qb = (int64_t)bi * tq, kb = (int64_t)bi * tk;
   if(p.qoff) {
@@ -541,9 +543,13 @@ int set_smem_attr(const void* fn, size_t bytes) {
       "cudaFuncSetAttribute(attention_tc)");
 }
 
-// varlen offsets of the current call (set by the _varlen entry points)
+// varlen offsets of the current call (set by the _varlen entry points);
+// with g_sid the launch covers g_nsent sentences whose longest sequence is
+// g_tile (the tile size), not all b sentences
 thread_local const int* g_qoff = nullptr;
 thread_local const int* g_koff = nullptr;
+thread_local const int* g_sid = nullptr;
+thread_local int64_t g_nsent = 0, g_tile = 0;
 
 }  // namespace
 
@@ -559,7 +565,8 @@ int mtkc_attention_tc(float* out, int64_t ldo, float* probs, const float* q, int
                       int causal, int* flags, void* stream) {
   if(b <= 0 || tq <= 0 || tk <= 0)
     return MTKC_OK;
-  int tt = tc_tile(tq, tk, dk, ldq, ldk, ldo, {out, q, k, v});
+  int tt = g_sid ? tc_tile(g_tile, g_tile, dk, ldq, ldk, ldo, {out, q, k, v})
+                 : tc_tile(tq, tk, dk, ldq, ldk, ldo, {out, q, k, v});
   if(!tt)
     return fail(MTKC_DIMENSION,
                 "tensor-core attention needs head dim 64, tq/tk <= 64, 16-byte aligned rows");
@@ -568,8 +575,8 @@ int mtkc_attention_tc(float* out, int64_t ldo, float* probs, const float* q, int
     prof.detail = "tcfwd_b" + std::to_string(b) + "_tq" + std::to_string(tq) + "_tk" +
                   std::to_string(tk);
   TcAttP p{out, ldo, probs, q, ldq, k, v, ldk, key_mask, (int)tq, (int)tk, heads, scale, causal,
-           flags, g_qoff, g_koff};
-  dim3 grid((unsigned)heads, (unsigned)b);
+           flags, g_qoff, g_koff, g_sid};
+  dim3 grid((unsigned)heads, (unsigned)(g_sid ? g_nsent : b));
 #define MTKC_TC_FWD(TTV)                                                          \
   if(tt == TTV) {                                                                 \
     size_t smem = fwd_smem<TTV>();                                                \
@@ -591,7 +598,8 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
                                float* colpart, void* stream) {
   if(b <= 0 || tq <= 0 || tk <= 0)
     return MTKC_OK;
-  int tt = tc_tile(tq, tk, dk, ldq, ldk, ldo, {gout, q, k, v, gq, gk, gv});
+  int tt = g_sid ? tc_tile(g_tile, g_tile, dk, ldq, ldk, ldo, {gout, q, k, v, gq, gk, gv})
+                 : tc_tile(tq, tk, dk, ldq, ldk, ldo, {gout, q, k, v, gq, gk, gv});
   if(!tt)
     return fail(MTKC_DIMENSION,
                 "tensor-core attention needs head dim 64, tq/tk <= 64, 16-byte aligned rows");
@@ -600,8 +608,8 @@ int mtkc_attention_tc_backward(const float* gout, int64_t ldo, const float* prob
     prof.detail = "tcbwd_b" + std::to_string(b) + "_tq" + std::to_string(tq) + "_tk" +
                   std::to_string(tk);
   TcAttBP p{gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, (int)tq, (int)tk, heads, scale,
-            accumulate_q, accumulate_k, accumulate_v, colpart, g_qoff, g_koff};
-  dim3 grid((unsigned)heads, (unsigned)b);
+            accumulate_q, accumulate_k, accumulate_v, colpart, g_qoff, g_koff, g_sid};
+  dim3 grid((unsigned)heads, (unsigned)(g_sid ? g_nsent : b));
 #define MTKC_TC_BWD(TTV)                                                          \
   if(tt == TTV) {                                                                 \
     size_t smem = bwd_smem<TTV>();                                                \
@@ -641,6 +649,43 @@ int mtkc_attention_tc_varlen_backward(const float* gout, int64_t ldo, const floa
                                       tq_max, tk_max, heads, dk, scale, accumulate_q,
                                       accumulate_k, accumulate_v, nullptr, stream);
   g_qoff = g_koff = nullptr;
+  return rc;
+}
+
+int mtkc_attention_tc_varlen_ids(float* out, int64_t ldo, float* probs, const float* q,
+                                 int64_t ldq, const float* k, const float* v, int64_t ldk,
+                                 const int32_t* qoff, const int32_t* koff,
+                                 const int32_t* sent_ids, int64_t n_sent, int64_t tile_len,
+                                 int64_t b, int64_t tq_max, int64_t tk_max, int heads, int64_t dk,
+                                 float scale, int causal, int* flags, void* stream) {
+  g_sid = sent_ids;
+  g_nsent = n_sent;
+  g_tile = tile_len;
+  int rc = n_sent > 0 ? mtkc_attention_tc_varlen(out, ldo, probs, q, ldq, k, v, ldk, qoff, koff,
+                                                 b, tq_max, tk_max, heads, dk, scale, causal,
+                                                 flags, stream)
+                      : MTKC_OK;
+  g_sid = nullptr;
+  g_nsent = g_tile = 0;
+  return rc;
+}
+
+int mtkc_attention_tc_varlen_ids_backward(
+    const float* gout, int64_t ldo, const float* probs, const float* q, int64_t ldq,
+    const float* k, const float* v, int64_t ldk, float* gq, float* gk, float* gv,
+    const int32_t* qoff, const int32_t* koff, const int32_t* sent_ids, int64_t n_sent,
+    int64_t tile_len, int64_t b, int64_t tq_max, int64_t tk_max, int heads, int64_t dk,
+    float scale, int accumulate_q, int accumulate_k, int accumulate_v, void* stream) {
+  g_sid = sent_ids;
+  g_nsent = n_sent;
+  g_tile = tile_len;
+  int rc = n_sent > 0 ? mtkc_attention_tc_varlen_backward(
+                            gout, ldo, probs, q, ldq, k, v, ldk, gq, gk, gv, qoff, koff, b,
+                            tq_max, tk_max, heads, dk, scale, accumulate_q, accumulate_k,
+                            accumulate_v, stream)
+                      : MTKC_OK;
+  g_sid = nullptr;
+  g_nsent = g_tile = 0;
   return rc;
 }
 
