@@ -527,6 +527,8 @@ typedef struct mtkc_rnn_scan_args {
   int64_t b, T, d;
   int ndir;              /* 1 (decoder) or 2 (bidirectional encoder) */
   float eps;
+  int lean_cache;        /* forward: store only what mtkc_rnn_scan_backward reads (the h-gate
+                            third of hu, no xw2); 0 keeps the per-step path's full caches */
   const float* maskT;    /* [T x b] padding blend mask of the last block, or NULL */
   mtkc_rnn_dir dir[2];
   /* Bahdanau attention between blocks 1 and 2 (decoder, ndir == 1) */

@@ -432,6 +432,9 @@ bool forwardPersistent(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X)
   if(!persistEnabled())
     return false;
   mtkc_rnn_scan_args a = scanArgs(g, n, X);
+  // the backward will be persistent too (same conditions): skip the caches
+  // only the per-step backward reads
+  a.lean_cache = !(X.att && X.A.kd > 2048) ? 1 : 0;
   const bool ok = mtkc_rnn_scan_supported(&a) != 0;
   Device& dev = Device::get();
   const size_t need = ok ? mtkc_rnn_scan_workspace(&a) : 0;

@@ -348,10 +348,12 @@ __device__ void gru_row(const KP& p, const mtkc_rnn_dir& D, int k, int64_t t, in
       continue;
     const int64_t j = 4 * g;
     float* huOut = B.hu + tr * d3 + j;
-    st4(huOut, hz[q]);
-    st4(huOut + d, hr[q]);
+    if(!p.a.lean_cache) {  // the persistent backward reads only the h-gate third
+      st4(huOut, hz[q]);
+      st4(huOut + d, hr[q]);
+    }
     st4(huOut + 2 * d, hh[q]);
-    if(partX) {
+    if(partX && !p.a.lean_cache) {
       float* xo = D.xw2 + tr * d3 + j;
       st4(xo, xz[q]);
       st4(xo + d, xr[q]);
