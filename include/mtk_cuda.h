@@ -568,6 +568,10 @@ int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream);
  * as K-split tcgen05 phases).  Weight / bias / LN gradients are NOT formed:
  * the caller sums them over all b*T rows from dG, dGx, dac, lnp, dwq, vpart
  * (and the key gradient from attWts and dctx) after the sweep. */
+/* keys gradient of the scan's attention: gkeys[r,s,:] (+)= sum_t attWts[t*b+r, s] *
+ * dctx[t*b+r, :]  (T x (256 + S) floats of shared memory per CTA) */
+int mtkc_rnn_key_grad(float* gkeys, const float* attW, const float* dctx, int64_t b, int64_t T,
+                      int64_t S, int64_t kd, int accumulate, void* stream);
 size_t mtkc_rnn_scan_bwd_workspace(const mtkc_rnn_scan_args* a);
 int mtkc_rnn_scan_backward(const mtkc_rnn_scan_args* a, void* stream);
 

@@ -781,7 +781,11 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
     const int slots[3] = {A.v, A.lnG, A.lnB};
     for(int j = 0; j < np; ++j)
       colsum(c, g.gradDst(n.inputs[(size_t)slots[j]]), D.vpart.devc() + j * TB * A.a, TB, A.a);
-    if(D.inter) {  // keys: d(keys)[r] (+)= sum_t w_t[r]^T dctx_t[r], one batched product
+    if(D.inter) {  // keys: d(keys)[r] (+)= sum_t w_t[r]^T dctx_t[r]
+      MTKC(mtkc_rnn_key_grad(D.gkeys.ptr, D.attW.devc(), D.dctx.devc(), b, T, A.S, A.kd,
+                             D.gkeys.accumulate, c.st));
+    }
+    if(false) {  // (batched-GEMM form of the same sum)
       mtkc_gemm_args q{};
       q.M = A.S;
       q.N = A.kd;

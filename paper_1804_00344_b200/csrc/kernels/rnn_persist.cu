@@ -1872,3 +1872,65 @@ int mtkc_rnn_scan_backward(const mtkc_rnn_scan_args* a, void* stream) {
 
 }  // extern "C"
 
+
+// ------------------------------------------------------------ key gradient
+// d(keys)[r, s, :] (+)= sum_t w[t, r, s] * dctx[t, r, :] (the context's key
+// gradient, bahdanau_dw_kernel's gk term summed over the decoder steps):
+// one CTA per (row r, 256-column chunk); the row's weights and the chunk of
+// every step's context gradient are staged in shared memory, sums in step
+// order.
+namespace {
+constexpr int KG_COLS = 256;
+__global__ void __launch_bounds__(256) rnn_key_grad_kernel(float* gkeys, const float* attW,
+                                                           const float* dctx, int64_t b,
+                                                           int64_t T, int64_t S, int64_t kd,
+                                                           int acc) {
+  MTKC_PDL_ENTRY();
+  extern __shared__ float ks[];  // [T][KG_COLS] dctx chunk, then [T][S] weights
+  const int64_t r = blockIdx.y, c0 = (int64_t)blockIdx.x * KG_COLS;
+  const int64_t nc = min((int64_t)KG_COLS, kd - c0);
+  float* sd = ks;
+  float* sw = ks + T * KG_COLS;
+  for(int64_t i = threadIdx.x; i < T * KG_COLS; i += blockDim.x) {
+    const int64_t t = i / KG_COLS, c = i % KG_COLS;
+    sd[i] = c < nc ? dctx[(t * b + r) * kd + c0 + c] : 0.f;
+  }
+  for(int64_t i = threadIdx.x; i < T * S; i += blockDim.x) {
+    const int64_t t = i / S, s = i % S;
+    sw[i] = attW[(t * b + r) * S + s];
+  }
+  __syncthreads();
+  const int64_t c = threadIdx.x;
+  if(c >= nc)
+    return;
+  for(int64_t s = 0; s < S; ++s) {
+    float v = 0.f;
+    for(int64_t t = 0; t < T; ++t)
+      v += sw[t * S + s] * sd[t * KG_COLS + c];
+    float* o = gkeys + (r * S + s) * kd + c0 + c;
+    *o = acc ? *o + v : v;
+  }
+}
+}  // namespace
+
+extern "C" int mtkc_rnn_key_grad(float* gkeys, const float* attW, const float* dctx, int64_t b,
+                                 int64_t T, int64_t nS, int64_t kd, int accumulate, void* stream) {
+  if(b <= 0 || T <= 0 || nS <= 0 || kd <= 0)
+    return MTKC_OK;
+  const size_t smem = (size_t)T * (KG_COLS + nS) * sizeof(float);
+  if(smem > 200 * 1024)
+    return fail(MTKC_DIMENSION, "rnn key gradient: T x (256 + S) floats exceed shared memory");
+  static size_t attr = 0;
+  if(smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(rnn_key_grad_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if(e != cudaSuccess)
+      return cuda_status(e, "rnn key gradient smem attribute");
+    attr = smem;
+  }
+  ProfScope prof(S(stream), "rnn_scan_bwd", 4.0 * (double)(b * nS * kd + T * b * kd));
+  ::mtkc::launch(rnn_key_grad_kernel, dim3((unsigned)cdiv(kd, KG_COLS), (unsigned)b), 256, smem,
+                 S(stream), gkeys, attW, dctx, b, T, nS, kd, accumulate);
+  MTKC_POST_LAUNCH("rnn_key_grad_kernel");
+  return MTKC_OK;
+}
