@@ -279,6 +279,16 @@ int mtkc_transpose(float* out, const float* src, const int64_t sd[4], const int 
                    int accumulate, void* stream);
 /* strided block copy: for o < outer: dst[o*dst_stride + dst_off .. +len] (+)=
  * src[o*src_stride + src_off .. +len]  (concat/slice and their backwards) */
+/* up to MTKC_COPY_MAX_JOBS strided 2-d copies in one launch:
+ * dst[r*ldd + c] (+)= src[r*lds + c] for r < rows, c < cols */
+#define MTKC_COPY_MAX_JOBS 32
+typedef struct mtkc_copy_job {
+  const float* src;
+  float* dst;
+  int64_t rows, cols, lds, ldd;
+  int accumulate;
+} mtkc_copy_job;
+int mtkc_copy_many(const mtkc_copy_job* jobs, int n, void* stream);
 int mtkc_copy_blocks(float* dst, int64_t dst_stride, int64_t dst_off, const float* src,
                      int64_t src_stride, int64_t src_off, int64_t outer, int64_t len,
                      int accumulate, void* stream);

@@ -1582,19 +1582,14 @@ std::shared_ptr<RowPacking> RowPacking::fromMask(const Tensor& mask) {
   return p;
 }
 
-NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef k, NodeRef v,
-                                         const std::shared_ptr<const RowPacking>& qp,
-                                         const std::shared_ptr<const RowPacking>& kp,
-                                         bool causal, int heads) {
-  checkRef(q);
-  checkRef(k);
-  checkRef(v);
-  if(!qp || !kp || qp->b != kp->b)
-    throw ContractError("attentionPacked: packings of different batches");
-  if(q.shape.rank() != 2 || k.shape.rank() != 2 || v.shape != k.shape ||
-     q.shape[0] != qp->n() || k.shape[0] != kp->n() || q.shape[1] != k.shape[1])
-    throw DimensionError("attentionPacked expects q [nq,d], k/v [nk,d]: " + q.shape.str() +
-                         " " + k.shape.str());
+namespace {
+// attentionPacked body: k/v columns [kCol, kCol+d) / [vCol, vCol+d) of rows
+// with stride ldk (kvShared: k and v are the same wide node)
+NodeRef attentionPackedImpl(ExpressionGraph& g, NodeRef q, NodeRef k, NodeRef v, int64_t kCol,
+                            int64_t vCol, int64_t ldk, bool kvShared,
+                            const std::shared_ptr<const RowPacking>& qp,
+                            const std::shared_ptr<const RowPacking>& kp, bool causal, int heads) {
+  using Node = ExpressionGraph::Node;
   const int64_t d = q.shape[1], b = qp->b, tq = qp->maxLen, tk = kp->maxLen;
   if(d % heads != 0)
     throw DimensionError("model dim not divisible by heads");
@@ -1603,11 +1598,11 @@ NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef k, NodeRef v,
     throw ContractError("attentionPacked: needs the TF32 tensor-core attention path");
   for(const RowPacking* rp : {qp.get(), kp.get()})
     if(!rp->dev)
-      rp->dev = uploadIntsTo(*this, rp->off, &rp->devOff);
+      rp->dev = uploadIntsTo(g, rp->off, &rp->devOff);
   Node n;
   n.op = "attentionPacked";
   n.shape = q.shape;
-  n.inputs = {q.index, k.index, v.index};
+  n.inputs = kvShared ? std::vector<int>{q.index, k.index} : std::vector<int>{q.index, k.index, v.index};
   auto aux = std::make_shared<AttAux>();
   n.aux = aux;
   const float scale = (float)(1.0 / std::sqrt((double)dk));  // layers.cpp:106
@@ -1631,14 +1626,15 @@ NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef k, NodeRef v,
       buckets.push_back(Bucket{tile, off, (int64_t)ids.size() - off});
   }
   int64_t idsOff = 0;
-  auto idsBuf = uploadIntsTo(*this, ids, &idsOff);
+  auto idsBuf = uploadIntsTo(g, ids, &idsOff);
+  const int vSlot = kvShared ? 1 : 2;
   n.fwd = [=](ExpressionGraph& g, Node& n) {
     aux->probs = g.allocTensor(Shape({b, (int64_t)heads, tq, tk}));
     for(const Bucket& bk : buckets)
       MTKC(mtkc_attention_tc_varlen_ids(
-          n.value.dev(), d, aux->probs.dev(), g.valPtr(n.inputs[0]), d, g.valPtr(n.inputs[1]),
-          g.valPtr(n.inputs[2]), d, (const int32_t*)QP->dev->ptr + QP->devOff,
-          (const int32_t*)KP->dev->ptr + KP->devOff,
+          n.value.dev(), d, aux->probs.dev(), g.valPtr(n.inputs[0]), d,
+          g.valPtr(n.inputs[1]) + kCol, g.valPtr(n.inputs[(size_t)vSlot]) + vCol, ldk,
+          (const int32_t*)QP->dev->ptr + QP->devOff, (const int32_t*)KP->dev->ptr + KP->devOff,
           (const int32_t*)idsBuf->ptr + idsOff + bk.off, bk.n, bk.tile, b, tq, tk, heads, dk,
           scale, causal ? 1 : 0, Device::get().flags(), stream()));
   };
@@ -1646,14 +1642,125 @@ NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef k, NodeRef v,
     const float* go = g.gradSrc(n);
     auto dq = g.gradDst(n.inputs[0]);
     auto dkk = g.gradDst(n.inputs[1]);
-    auto dv = g.gradDst(n.inputs[2]);
+    // shared wide node: this node's k / v columns are written by it alone
+    auto dv = kvShared ? dkk : g.gradDst(n.inputs[2]);
+    const int accK = kvShared ? 0 : dkk.accumulate, accV = kvShared ? 0 : dv.accumulate;
     for(const Bucket& bk : buckets)  // disjoint rows: every launch keeps the accumulate flags
       MTKC(mtkc_attention_tc_varlen_ids_backward(
-          go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d, g.valPtr(n.inputs[1]),
-          g.valPtr(n.inputs[2]), d, dq.ptr, dkk.ptr, dv.ptr,
+          go, d, aux->probs.devc(), g.valPtr(n.inputs[0]), d, g.valPtr(n.inputs[1]) + kCol,
+          g.valPtr(n.inputs[(size_t)vSlot]) + vCol, ldk, dq.ptr, dkk.ptr + kCol, dv.ptr + vCol,
           (const int32_t*)QP->dev->ptr + QP->devOff, (const int32_t*)KP->dev->ptr + KP->devOff,
           (const int32_t*)idsBuf->ptr + idsOff + bk.off, bk.n, bk.tile, b, tq, tk, heads, dk,
-          scale, dq.accumulate, dkk.accumulate, dv.accumulate, stream()));
+          scale, dq.accumulate, accK, accV, stream()));
+  };
+  return g.addNode(std::move(n));
+}
+}  // namespace
+
+NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef k, NodeRef v,
+                                         const std::shared_ptr<const RowPacking>& qp,
+                                         const std::shared_ptr<const RowPacking>& kp,
+                                         bool causal, int heads) {
+  checkRef(q);
+  checkRef(k);
+  checkRef(v);
+  if(!qp || !kp || qp->b != kp->b)
+    throw ContractError("attentionPacked: packings of different batches");
+  if(q.shape.rank() != 2 || k.shape.rank() != 2 || v.shape != k.shape ||
+     q.shape[0] != qp->n() || k.shape[0] != kp->n() || q.shape[1] != k.shape[1])
+    throw DimensionError("attentionPacked expects q [nq,d], k/v [nk,d]: " + q.shape.str() +
+                         " " + k.shape.str());
+  return attentionPackedImpl(*this, q, k, v, 0, 0, q.shape[1], false, qp, kp, causal, heads);
+}
+
+NodeRef ExpressionGraph::attentionPacked(NodeRef q, NodeRef kv, int64_t kCol, int64_t vCol,
+                                         const std::shared_ptr<const RowPacking>& qp,
+                                         const std::shared_ptr<const RowPacking>& kp,
+                                         bool causal, int heads) {
+  checkRef(q);
+  checkRef(kv);
+  if(!qp || !kp || qp->b != kp->b)
+    throw ContractError("attentionPacked: packings of different batches");
+  const int64_t d = q.shape.back();
+  if(q.shape.rank() != 2 || kv.shape.rank() != 2 || q.shape[0] != qp->n() ||
+     kv.shape[0] != kp->n() || kCol < 0 || vCol < 0 || kCol + d > kv.shape[1] ||
+     vCol + d > kv.shape[1])
+    throw DimensionError("attentionPacked: q " + q.shape.str() + " kv " + kv.shape.str());
+  return attentionPackedImpl(*this, q, kv, kv, kCol, vCol, kv.shape[1], true, qp, kp, causal,
+                             heads);
+}
+
+NodeRef ExpressionGraph::affineMulti(NodeRef x, const std::vector<NodeRef>& Ws,
+                                     const std::vector<NodeRef>& bs) {
+  checkRef(x);
+  if(Ws.empty() || Ws.size() != bs.size() || Ws.size() > MTKC_COPY_MAX_JOBS / 2)
+    throw ContractError("affineMulti: 1..16 weight/bias pairs");
+  const int64_t K = x.shape.back(), rows = x.shape.size() / K;
+  std::vector<int64_t> cols, offs;
+  int64_t N = 0;
+  for(size_t i = 0; i < Ws.size(); ++i) {
+    checkRef(Ws[i]);
+    checkRef(bs[i]);
+    if(Ws[i].shape.rank() != 2 || Ws[i].shape[0] != K || bs[i].shape.size() != Ws[i].shape[1])
+      throw DimensionError("affineMulti: W " + Ws[i].shape.str() + " b " + bs[i].shape.str());
+    offs.push_back(N);
+    cols.push_back(Ws[i].shape[1]);
+    N += Ws[i].shape[1];
+  }
+  std::vector<int64_t> dims = x.shape.dims();
+  dims.back() = N;
+  Node n;
+  n.op = "affineMulti";
+  n.shape = Shape(dims);
+  n.inputs = {x.index};
+  for(auto& w : Ws)
+    n.inputs.push_back(w.index);
+  for(auto& b : bs)
+    n.inputs.push_back(b.index);
+  struct MultiAux {
+    Tensor wcat, bcat;
+  };
+  auto aux = std::make_shared<MultiAux>();
+  n.aux = aux;
+  const int64_t P = (int64_t)Ws.size();
+  n.fwd = [=](ExpressionGraph& g, Node& n) {
+    aux->wcat = g.allocTensor(Shape({K, N}));
+    aux->bcat = g.allocTensor(Shape({N}));
+    std::vector<mtkc_copy_job> jobs;
+    for(int64_t i = 0; i < P; ++i) {  // [W_0|W_1|..] and [b_0|b_1|..]
+      jobs.push_back(mtkc_copy_job{g.valPtr(n.inputs[(size_t)(1 + i)]), aux->wcat.dev() + offs[(size_t)i],
+                                   K, cols[(size_t)i], cols[(size_t)i], N, 0});
+      jobs.push_back(mtkc_copy_job{g.valPtr(n.inputs[(size_t)(1 + P + i)]),
+                                   aux->bcat.dev() + offs[(size_t)i], 1, cols[(size_t)i],
+                                   cols[(size_t)i], N, 0});
+    }
+    MTKC(mtkc_copy_many(jobs.data(), (int)jobs.size(), stream()));
+    gemm(rows, N, K, g.valPtr(n.inputs[0]), K, false, aux->wcat.devc(), N, false, n.value.dev(),
+         N, 0.f, aux->bcat.devc());
+  };
+  n.bwd = [=](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    if(g.node(g.resolve(n.inputs[0])).needsGrad) {  // dx (+)= dY [W..]^T
+      auto dx = g.gradDst(n.inputs[0]);
+      gemm(rows, K, N, go, N, false, aux->wcat.devc(), N, true, dx.ptr, K,
+           dx.accumulate ? 1.f : 0.f);
+    }
+    // d[W..] = x^T dY with the bias gradients as its operand sums, then
+    // scattered to the parameters
+    Tensor dw = g.allocTensor(Shape({K, N}));
+    Tensor db = g.allocTensor(Shape({N}));
+    gemm(K, N, rows, g.valPtr(n.inputs[0]), K, true, go, N, false, dw.dev(), N, 0.f, nullptr,
+         MTKC_EPI_NONE, nullptr, 1, 0, 0, 0, db.dev(), MTKC_COLSUM_B, 0);
+    std::vector<mtkc_copy_job> jobs;
+    for(int64_t i = 0; i < P; ++i) {
+      auto gw = g.gradDst(n.inputs[(size_t)(1 + i)]);
+      auto gb = g.gradDst(n.inputs[(size_t)(1 + P + i)]);
+      jobs.push_back(mtkc_copy_job{dw.devc() + offs[(size_t)i], gw.ptr, K, cols[(size_t)i], N,
+                                   cols[(size_t)i], gw.accumulate});
+      jobs.push_back(mtkc_copy_job{db.devc() + offs[(size_t)i], gb.ptr, 1, cols[(size_t)i], N,
+                                   cols[(size_t)i], gb.accumulate});
+    }
+    MTKC(mtkc_copy_many(jobs.data(), (int)jobs.size(), stream()));
   };
   return addNode(std::move(n));
 }

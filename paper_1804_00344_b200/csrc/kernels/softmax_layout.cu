@@ -2,6 +2,8 @@
 // layout kernels: transposeInto / concatInto / sliceInto (tensor.cpp:480-541),
 // gatherRowsInto / scatterAddRows (:456-476) and the embedding lookup fused
 // with the positional encoding (graph.cpp:595-622 + layers.cpp:164-179).
+#include <algorithm>
+
 #include "common.cuh"
 
 using namespace mtkc;
@@ -108,6 +110,25 @@ __global__ void transpose_kernel(TrP p) {
     int64_t i0 = r / p.od[1];
     float v = p.src[i0 * p.ss[0] + i1 * p.ss[1] + i2 * p.ss[2] + i3 * p.ss[3]];
     p.out[i] = p.acc ? p.out[i] + v : v;
+  }
+}
+
+struct CopyJobs {
+  mtkc_copy_job j[MTKC_COPY_MAX_JOBS];
+  int n;
+};
+
+// several strided 2-d copies in one launch (blockIdx.y = job)
+__global__ void copy_many_kernel(const __grid_constant__ CopyJobs cj) {
+  MTKC_PDL_ENTRY();
+  const mtkc_copy_job& J = cj.j[blockIdx.y];
+  const int64_t n = J.rows * J.cols;
+  for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+      i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / J.cols, c = i - r * J.cols;
+    const float v = J.src[r * J.lds + c];
+    float* d = J.dst + r * J.ldd + c;
+    *d = J.accumulate ? *d + v : v;
   }
 }
 
@@ -334,6 +355,24 @@ int mtkc_transpose(float* out, const float* src, const int64_t sd[4], const int 
     return MTKC_OK;
   ::mtkc::launch(transpose_kernel, grid1d(p.n, 256), 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("transpose_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_copy_many(const mtkc_copy_job* jobs, int n, void* stream) {
+  if(n <= 0)
+    return MTKC_OK;
+  if(n > MTKC_COPY_MAX_JOBS)
+    return fail(MTKC_CONTRACT, "mtkc_copy_many: too many jobs");
+  CopyJobs cj{};
+  int64_t most = 0;
+  for(int i = 0; i < n; ++i) {
+    cj.j[i] = jobs[i];
+    most = std::max<int64_t>(most, jobs[i].rows * jobs[i].cols);
+  }
+  cj.n = n;
+  ::mtkc::launch(copy_many_kernel, dim3(grid1d(most, 256, 148 * 4), (unsigned)n), 256, 0,
+                 S(stream), cj);
+  MTKC_POST_LAUNCH("copy_many_kernel");
   return MTKC_OK;
 }
 
