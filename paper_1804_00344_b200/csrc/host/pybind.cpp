@@ -306,6 +306,15 @@ PYBIND11_MODULE(_mtk, m) {
       .def("arena_high_water", [](G& g) { return g.arena().highWaterBytes(); })
       .def("param_pool_size", [](G& g) { return g.pool().used(); });
 
+  // ---------------------------------------------------------- arena (tensor.h:43-61)
+  py::class_<Arena>(m, "Arena")
+      .def(py::init<size_t>(), py::arg("capacity_bytes"))
+      .def("alloc", [](Arena& a, int64_t elems) { a.alloc(elems); })
+      .def("reset", &Arena::reset)
+      .def("capacity", &Arena::capacity)
+      .def("outstanding_bytes", &Arena::outstandingBytes)
+      .def("high_water_bytes", &Arena::highWaterBytes);
+
   // ---------------------------------------------------------- data
   py::class_<Examples>(m, "Examples")
       .def(py::init([](py::list sources, py::list targets, py::list extra) {

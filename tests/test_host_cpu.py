@@ -116,3 +116,13 @@ def test_dp_sharding_restatement():
     assert S.shard(take=8, world=4, local_workers=2, rank=3) == [6, 7]
     assert S.shard(take=5, world=4, local_workers=2, rank=3) == []
     assert S.shard(take=5, world=4, local_workers=2, rank=2) == [4]
+
+
+def test_arena_enforces_capacity():
+    """Arena capacity check (tensor.cpp:42-44; test_tensor.cpp:209-212): the
+    request is refused with NumericError before any device memory is taken."""
+    from paper_1804_00344_b200 import mtk as M
+    a = M.Arena(64)
+    with pytest.raises(M.NumericError):
+        a.alloc(1000)
+    assert a.outstanding_bytes() == 0
