@@ -351,6 +351,11 @@ int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* 
 /* ======================================================================== */
 int mtkc_embed(float* out, const float* table, const int32_t* ids, int64_t n, int64_t e,
                int64_t vocab, float s, const float* pe, int64_t t, int* flags, void* stream);
+/* packed rows: out[n,:] = table[ids[n],:]*s + pe[pos[n],:] (pos = position of
+ * row n in its sentence; addPositionalEncoding over real tokens only) */
+int mtkc_embed_pos(float* out, const float* table, const int32_t* ids, const int32_t* pos,
+                   int64_t n, int64_t e, int64_t vocab, float s, const float* pe, int* flags,
+                   void* stream);
 
 /* ======================================================================== */
 /* scaled dot-product multi-head attention core (MultiHeadAttention::apply,  */

@@ -1404,6 +1404,47 @@ NodeRef ExpressionGraph::embed(NodeRef table, const IntMat& ids) {
   return addNode(std::move(n));
 }
 
+NodeRef ExpressionGraph::embedPositions(NodeRef table, const std::vector<int32_t>& ids,
+                                        const std::vector<int32_t>& pos, Real s,
+                                        const Tensor& pe) {
+  checkRef(table);
+  if(table.shape.rank() != 2 || ids.size() != pos.size() || pe.shape().rank() != 2 ||
+     pe.shape()[1] != table.shape[1])
+    throw DimensionError("embedPositions shapes");
+  const int64_t vocab = table.shape[0], e = table.shape[1], cnt = (int64_t)ids.size();
+  for(size_t i = 0; i < ids.size(); ++i) {
+    if(ids[i] < 0 || ids[i] >= vocab)
+      throw DataError("token id " + std::to_string(ids[i]) + " out of vocabulary of size " +
+                      std::to_string(vocab));
+    if(pos[i] < 0 || pos[i] >= pe.shape()[0])
+      throw ContractError("embedPositions: position out of the table");
+  }
+  Node n;
+  n.op = "embedPositions";
+  n.shape = Shape({cnt, e});
+  n.inputs = {table.index};
+  auto aux = std::make_shared<EmbedAux>();
+  aux->ids = uploadIntsTo(*this, ids, &aux->off);
+  int64_t posOff = 0;
+  auto posBuf = uploadIntsTo(*this, pos, &posOff);
+  if(!inference_)
+    aux->plan = makeScatterPlan(*this, ids);
+  aux->scale = s;
+  aux->pe = sharedConst(pe);
+  n.aux = aux;
+  n.fwd = [aux, posBuf, posOff, cnt, e, vocab](ExpressionGraph& g, Node& n) {
+    MTKC(mtkc_embed_pos(n.value.dev(), g.valPtr(n.inputs[0]), (const int32_t*)aux->ids->ptr + aux->off,
+                        (const int32_t*)posBuf->ptr + posOff, cnt, e, vocab, aux->scale,
+                        aux->pe->devc(), Device::get().flags(), stream()));
+  };
+  n.bwd = [aux, e, vocab](ExpressionGraph& g, Node& n) {
+    const float* go = g.gradSrc(n);
+    float* dst = accPtr(g, n.inputs[0], vocab * e);
+    scatterPlanAdd(g, aux->plan, dst, go, e, aux->scale);
+  };
+  return addNode(std::move(n));
+}
+
 NodeRef ExpressionGraph::scaleAddConst(NodeRef x, Real s, const Tensor& pe) {
   checkRef(x);
   if(x.shape.size() % pe.size() != 0)

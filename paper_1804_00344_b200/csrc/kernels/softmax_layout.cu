@@ -261,7 +261,7 @@ __global__ void embed_kernel(float* out, const float* table, const int32_t* ids,
 
 __global__ void embed4_kernel(float4* out, const float4* table, const int32_t* ids, int64_t n,
                               int64_t e4, int64_t vocab, float s, const float4* pe, int64_t t,
-                              int* flags) {
+                              int* flags, const int32_t* pos) {
   MTKC_PDL_ENTRY();
   int64_t total = n * e4;
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -282,7 +282,7 @@ __global__ void embed4_kernel(float4* out, const float4* table, const int32_t* i
       v.w = s * v.w;
     }
     if(pe) {
-      float4 q = pe[(r % t) * e4 + c];
+      float4 q = pe[(pos ? (int64_t)pos[r] : r % t) * e4 + c];
       v.x = v.x + q.x;
       v.y = v.y + q.y;
       v.z = v.z + q.z;
@@ -439,11 +439,26 @@ int mtkc_embed(float* out, const float* table, const int32_t* ids, int64_t n, in
              (!pe || (uintptr_t)pe % 16 == 0);
   if(vec)
     ::mtkc::launch(embed4_kernel, grid1d(n * e / 4, 256), 256, 0, S(stream), 
-        (float4*)out, (const float4*)table, ids, n, e / 4, vocab, s, (const float4*)pe, t, flags);
+        (float4*)out, (const float4*)table, ids, n, e / 4, vocab, s, (const float4*)pe, t, flags,
+        (const int32_t*)nullptr);
   else
     ::mtkc::launch(embed_kernel, grid1d(n * e, 256), 256, 0, S(stream), out, table, ids, n, e, vocab, s, pe,
                                                            t, flags);
   MTKC_POST_LAUNCH("embed_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_embed_pos(float* out, const float* table, const int32_t* ids, const int32_t* pos,
+                   int64_t n, int64_t e, int64_t vocab, float s, const float* pe, int* flags,
+                   void* stream) {
+  if(n * e <= 0)
+    return MTKC_OK;
+  if(e % 4 || (uintptr_t)out % 16 || (uintptr_t)table % 16 || !pe || (uintptr_t)pe % 16)
+    return fail(MTKC_DIMENSION, "mtkc_embed_pos: 16-byte aligned rows and a position table");
+  ::mtkc::launch(embed4_kernel, grid1d(n * e / 4, 256), 256, 0, S(stream), (float4*)out,
+                 (const float4*)table, ids, n, e / 4, vocab, s, (const float4*)pe, (int64_t)1,
+                 flags, pos);
+  MTKC_POST_LAUNCH("embed4_kernel");
   return MTKC_OK;
 }
 
