@@ -123,6 +123,22 @@ __global__ void copy_many_kernel(const __grid_constant__ CopyJobs cj) {
   MTKC_PDL_ENTRY();
   const mtkc_copy_job& J = cj.j[blockIdx.y];
   const int64_t n = J.rows * J.cols;
+  if(J.cols % 4 == 0 && J.lds % 4 == 0 && J.ldd % 4 == 0 &&
+     (((uintptr_t)J.src | (uintptr_t)J.dst) & 15) == 0) {  // float4 rows
+    const int64_t c4 = J.cols / 4, n4 = J.rows * c4;
+    for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+        i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = i / c4, c = (i - r * c4) * 4;
+      float4 v = *reinterpret_cast<const float4*>(J.src + r * J.lds + c);
+      float4* d = reinterpret_cast<float4*>(J.dst + r * J.ldd + c);
+      if(J.accumulate) {
+        const float4 o = *d;
+        v = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+      }
+      *d = v;
+    }
+    return;
+  }
   for(int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
       i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / J.cols, c = i - r * J.cols;
