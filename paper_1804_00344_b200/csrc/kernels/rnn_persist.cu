@@ -1499,6 +1499,8 @@ Plan make_plan(const mtkc_rnn_scan_args* a) {
   const int mT = (int)((b + 127) / 128);
   const int nTh = (int)(d3 / NTH);
   P.KCh = pick_kc((int)(d / 32), P.gs / std::max(1, nTh * mT));
+  if(const char* e = getenv("MTK_RNN_KCH"))  // tuning override
+    P.KCh = pick_kc((int)(d / 32), atoi(e));
   P.KCx = a->has_att ? pick_kc((int)(a->kd / 32), P.gs / std::max(1, nTh * mT)) : 1;
   P.NTq = a->has_att ? (a->a % 64 == 0 ? 64 : 32) : 32;
   P.KCq = a->has_att ? pick_kc((int)(d / 32), P.gs / std::max<int>(1, (int)(a->a / P.NTq) * mT))
@@ -1567,6 +1569,8 @@ BPlan make_bplan(const mtkc_rnn_scan_args* a) {
   P.NTb = d % 64 == 0 ? 64 : 32;
   P.NTc = a->has_att ? (a->kd % 64 == 0 ? 64 : 32) : 32;
   P.KCb = pick_kc((int)(d3 / 32), P.gs / std::max<int>(1, (int)(d / P.NTb) * mT));
+  if(const char* e = getenv("MTK_RNN_KCB"))  // tuning override
+    P.KCb = pick_kc((int)(d3 / 32), atoi(e));
   P.KCc = a->has_att ? pick_kc((int)(d3 / 32), P.gs / std::max<int>(1, (int)(a->kd / P.NTc) * mT)) : 1;
   P.KCq = a->has_att ? pick_kc((int)(a->a / 32), P.gs / std::max<int>(1, (int)(d / P.NTb) * mT)) : 1;
   size_t off = 0;
