@@ -88,6 +88,40 @@ def test_cli_train_matches_reference(cuda, tmp_path):
 
 
 @pytest.mark.gpu
+def test_cli_train_async_matches_reference(cuda, tmp_path):
+    """`train --async` with one worker (trainAsync, train.cpp:302-404) saves
+    the same model as the reference's asynchronous run."""
+    from oracle import refbind as R
+    from paper_1804_00344_b200 import config_text, mtk as M, synth
+    V = 60
+    src, tgt = synth.corpus(40, V)
+    tok = lambda ids: " ".join(f"w{int(i)}" for i in ids)
+    s_path = write(tmp_path / "s.txt", [tok(s) for s in src])
+    t_path = write(tmp_path / "t.txt", [tok(t) for t in tgt])
+    vocab = write(tmp_path / "vocab.txt", ["</s>", "<unk>"] + [f"w{i}" for i in range(2, V)])
+    cfg = write(tmp_path / "train.cfg", ["arch: transformer", "emb-dim: 32", "heads: 2",
+                                        "layers: 1", "dropout: 0", "tying: all",
+                                        "mini-batch-tokens: 330", "max-updates: 3",
+                                        "workers: 1", "seed: 9"])
+    model = str(tmp_path / "model.mtk")
+    env = dict(os.environ, MTK_PRECISION="fp32")
+    r = run("train", "--model", model, "--train-sets", s_path, t_path, "--vocabs", vocab, vocab,
+            "--config", cfg, "--async", env=env)
+    assert r.returncode == 0, r.stderr
+    ref_cfg = config_text(arch="transformer", vocab=V, emb=32, heads=2, layers=1, dropout=0.0,
+                          tying="all")
+    ref = R.RefModel(ref_cfg, 9)
+    ref.train(R.Examples(src, tgt), workers=1, budget=330, seed=9, epochs=1, max_updates=3,
+              async_=True)
+    g = M.ExpressionGraph(1)
+    M.Model(M.read_model_config(model)).register_params(g)
+    M.load_params(model, g)
+    for n in ref.param_names():
+        a, b = g.param_value(n), ref.param(n)
+        assert np.allclose(a, b, rtol=1e-6, atol=1e-6 * max(1.0, np.abs(b).max())), n
+
+
+@pytest.mark.gpu
 def test_cli_translate_and_score(cuda, tmp_path):
     """`translate` (beam search, n-best file in the reference's
     "id ||| text ||| F0=... ||| score" format) and `score` (forced decoding)
