@@ -1502,6 +1502,8 @@ Plan make_plan(const mtkc_rnn_scan_args* a) {
   if(const char* e = getenv("MTK_RNN_KCH"))  // tuning override
     P.KCh = pick_kc((int)(d / 32), atoi(e));
   P.KCx = a->has_att ? pick_kc((int)(a->kd / 32), P.gs / std::max(1, nTh * mT)) : 1;
+  if(const char* e = getenv("MTK_RNN_KCX"))  // tuning override
+    P.KCx = a->has_att ? pick_kc((int)(a->kd / 32), atoi(e)) : 1;
   P.NTq = a->has_att ? (a->a % 64 == 0 ? 64 : 32) : 32;
   P.KCq = a->has_att ? pick_kc((int)(d / 32), P.gs / std::max<int>(1, (int)(a->a / P.NTq) * mT))
                      : 1;
@@ -1572,6 +1574,8 @@ BPlan make_bplan(const mtkc_rnn_scan_args* a) {
   if(const char* e = getenv("MTK_RNN_KCB"))  // tuning override
     P.KCb = pick_kc((int)(d3 / 32), atoi(e));
   P.KCc = a->has_att ? pick_kc((int)(d3 / 32), P.gs / std::max<int>(1, (int)(a->kd / P.NTc) * mT)) : 1;
+  if(const char* e = getenv("MTK_RNN_KCC"))  // tuning override
+    P.KCc = a->has_att ? pick_kc((int)(d3 / 32), atoi(e)) : 1;
   P.KCq = a->has_att ? pick_kc((int)(a->a / 32), P.gs / std::max<int>(1, (int)(d / P.NTb) * mT)) : 1;
   size_t off = 0;
   auto take = [&](size_t floats) {
