@@ -343,6 +343,21 @@ int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* 
                                   float* dgain, float* dbias, int64_t rows, int64_t d,
                                   int accumulate_dx, int accumulate_params, float* workspace,
                                   size_t workspace_bytes, void* stream);
+/* Deferred parameter reduction: OR MTKC_LN_DEFER_PARAMS into              */
+/* accumulate_params and the backward only writes its per-block partials   */
+/* (mtkc_layernorm_stats_partial_blocks(rows) x 2 x d floats) into the      */
+/* workspace; a later mtkc_layernorm_param_reduce_many sums many layers'   */
+/* partials in one launch, bit-identical to the undeferred path.           */
+#define MTKC_LN_DEFER_PARAMS 2
+int64_t mtkc_layernorm_stats_partial_blocks(int64_t rows);
+typedef struct mtkc_ln_param_job {
+  float* dgain;
+  float* dbias;
+  const float* partials;
+  int64_t blocks, d;
+  int accumulate;
+} mtkc_ln_param_job;
+int mtkc_layernorm_param_reduce_many(const mtkc_ln_param_job* jobs, int n_jobs, void* stream);
 
 /* ======================================================================== */
 /* embedding (embed graph.cpp:595-622) fused with positional encoding       */

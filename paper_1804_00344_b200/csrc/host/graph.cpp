@@ -213,6 +213,14 @@ ExpressionGraph::GradDst ExpressionGraph::gradDst(int nodeIndex, bool supportsGa
   Node& n = nodes_[(size_t)r];
   if(n.isParam) {
     Param& p = paramOf(n);
+    if(!lnPending_.empty()) {  // a later writer must see the deferred sum first
+      const float* gp = p.grad.devc();
+      for(const auto& j : lnPending_)
+        if(gp == j.dgain || gp == j.dbias) {
+          flushLnParams();
+          break;
+        }
+    }
     int acc = p.gradLive ? 1 : 0;
     p.gradLive = true;
     return {p.grad.dev(), acc, nullptr, nullptr};
@@ -1337,6 +1345,17 @@ NodeRef ExpressionGraph::layerNorm(NodeRef x, NodeRef gain, NodeRef bias, Real e
     }
     Device& dev = Device::get();
     if(cache->fast && (((uintptr_t)go | (uintptr_t)dx.ptr) % 16) == 0) {
+      if(g.lnDeferActive()) {
+        const int64_t blocks = mtkc_layernorm_stats_partial_blocks(rows);
+        Tensor part = g.allocTensor(Shape({blocks, 2, d}));
+        MTKC(mtkc_layernorm_stats_backward(
+            go, g.valPtr(n.inputs[0]), g.valPtr(n.inputs[1]), cache->mean.devc(),
+            cache->invStd.devc(), dx.ptr, dg.ptr, db.ptr, rows, d, dx.accumulate,
+            dg.accumulate | MTKC_LN_DEFER_PARAMS, part.dev(), (size_t)part.size() * sizeof(float),
+            dev.stream()));
+        g.deferLnParams(dg.ptr, db.ptr, part.devc(), blocks, d, dg.accumulate);
+        return;
+      }
       float* w = dev.scratch(mtkc_layernorm_stats_workspace_bytes(rows, d));
       MTKC(mtkc_layernorm_stats_backward(go, g.valPtr(n.inputs[0]), g.valPtr(n.inputs[1]),
                                          cache->mean.devc(), cache->invStd.devc(), dx.ptr, dg.ptr,
@@ -2115,6 +2134,9 @@ void ExpressionGraph::backward(NodeRef loss, const std::function<void(int)>& aft
     auto d = gradDst(loss.index);
     MTKC(mtkc_fill(d.ptr, lossScale_, 1, stream()));
   }
+  static const bool noDefer = getenv("MTK_LN_NODEFER") != nullptr;
+  lnPending_.clear();  // a sweep that threw leaves nothing behind
+  lnDefer_ = !afterNode && !noDefer;
   for(int i = loss.index; i >= 0; --i) {
     Node& n = nodes_[(size_t)i];
     if(!(n.alias >= 0 || !n.bwd || !n.gradLive || !n.needsGrad))
@@ -2122,6 +2144,26 @@ void ExpressionGraph::backward(NodeRef loss, const std::function<void(int)>& aft
     if(afterNode)
       afterNode(i);
   }
+  flushLnParams();
+  lnDefer_ = false;
+}
+
+void ExpressionGraph::deferLnParams(float* dgain, float* dbias, const float* partials,
+                                    int64_t blocks, int64_t d, int accumulate) {
+  lnPending_.push_back({dgain, dbias, partials, blocks, d, accumulate});
+  if(lnPending_.size() >= 32)
+    flushLnParams();
+}
+
+void ExpressionGraph::flushLnParams() {
+  if(lnPending_.empty())
+    return;
+  std::vector<mtkc_ln_param_job> jobs;
+  jobs.reserve(lnPending_.size());
+  for(const auto& p : lnPending_)
+    jobs.push_back({p.dgain, p.dbias, p.partials, p.blocks, p.d, p.accumulate});
+  lnPending_.clear();
+  MTKC(mtkc_layernorm_param_reduce_many(jobs.data(), (int)jobs.size(), stream()));
 }
 
 std::vector<ExpressionGraph::GradBucket> ExpressionGraph::gradBuckets(int64_t targetElems) const {

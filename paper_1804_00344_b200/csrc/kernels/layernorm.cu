@@ -433,6 +433,64 @@ __global__ void __launch_bounds__(LN_WARPS * 32)
   }
 }
 
+// Several independent two-quantity reductions in one launch: blockIdx.y picks
+// the job, each job summed exactly as colred_final_kernel<2> would (same
+// lane split, same order), so the deferred result is bit-identical.
+struct ColredJob2 {
+  float* out0;
+  float* out1;
+  const float* part;
+  int64_t nblk, cols;
+  int acc;
+};
+constexpr int COLRED_MAX_JOBS = 32;
+struct ColredJobs2 {
+  ColredJob2 j[COLRED_MAX_JOBS];
+};
+
+__global__ void __launch_bounds__(256) colred_final_many_kernel(const __grid_constant__ ColredJobs2 jobs) {
+  MTKC_PDL_ENTRY();
+  const ColredJob2& jb = jobs.j[blockIdx.y];
+  __shared__ float red[8][2][32];
+  const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + cx;
+  if((int64_t)blockIdx.x * 32 >= jb.cols)
+    return;  // whole block past this job's columns (uniform)
+  float s[2] = {0.f, 0.f};
+  if(c < jb.cols) {
+    for(int64_t rb = ry; rb < jb.nblk; rb += 64) {
+      float v[8][2];
+#pragma unroll
+      for(int u = 0; u < 8; ++u)
+#pragma unroll
+        for(int q = 0; q < 2; ++q)
+          v[u][q] = rb + 8 * u < jb.nblk ? __ldcg(jb.part + ((rb + 8 * u) * 2 + q) * jb.cols + c)
+                                         : 0.f;
+#pragma unroll
+      for(int u = 0; u < 8; ++u)
+#pragma unroll
+        for(int q = 0; q < 2; ++q)
+          s[q] += v[u][q];
+    }
+  }
+#pragma unroll
+  for(int q = 0; q < 2; ++q)
+    red[ry][q][cx] = s[q];
+  __syncthreads();
+  if(ry == 0 && c < jb.cols) {
+    float t[2];
+#pragma unroll
+    for(int q = 0; q < 2; ++q) {
+      t[q] = 0.f;
+#pragma unroll
+      for(int k = 0; k < 8; ++k)
+        t[q] += red[k][q][cx];
+    }
+    jb.out0[c] = (jb.acc ? jb.out0[c] : 0.f) + t[0];
+    jb.out1[c] = (jb.acc ? jb.out1[c] : 0.f) + t[1];
+  }
+}
+
 template <template <int> class K, typename... Args>
 void launch_v(int64_t d, dim3 grid, cudaStream_t st, Args... args);
 
@@ -588,11 +646,39 @@ int mtkc_layernorm_stats_backward(const float* dy, const float* x, const float* 
   LN4_BWD(1) LN4_BWD(2) LN4_BWD(4) LN4_BWD(8) {}
 #undef LN4_BWD
   MTKC_POST_LAUNCH("ln_bwd4_kernel");
-  if(part) {
+  if(part && !(accumulate_params & MTKC_LN_DEFER_PARAMS)) {
     ::mtkc::launch(colred_final_kernel<2>, colred_final_grid(d), 256, 0, st, dgain, dbias, part, nblk, d,
                                                                   accumulate_params);
     MTKC_POST_LAUNCH("colred_final_kernel");
   }
+  return MTKC_OK;
+}
+
+int64_t mtkc_layernorm_stats_partial_blocks(int64_t rows) {
+  if(rows <= 0)
+    return 0;
+  const int64_t rpc = std::max<int64_t>(LN_WARPS, cdiv(cdiv(rows, 2 * 148), LN_WARPS) * LN_WARPS);
+  return cdiv(rows, rpc);
+}
+
+int mtkc_layernorm_param_reduce_many(const mtkc_ln_param_job* jobs, int n_jobs, void* stream) {
+  if(n_jobs <= 0)
+    return MTKC_OK;
+  if(n_jobs > COLRED_MAX_JOBS)
+    return fail(MTKC_CONTRACT, "mtkc_layernorm_param_reduce_many: at most 32 jobs per call");
+  ColredJobs2 js{};
+  int64_t maxCols = 0;
+  for(int i = 0; i < n_jobs; ++i) {
+    const mtkc_ln_param_job& j = jobs[i];
+    if(!j.dgain || !j.dbias || !j.partials || j.d <= 0 || j.blocks <= 0)
+      return fail(MTKC_CONTRACT, "mtkc_layernorm_param_reduce_many: empty job");
+    js.j[i] = ColredJob2{j.dgain, j.dbias, j.partials, j.blocks, j.d, j.accumulate ? 1 : 0};
+    maxCols = std::max(maxCols, j.d);
+  }
+  cudaStream_t st = S(stream);
+  ::mtkc::launch(colred_final_many_kernel, dim3(colred_final_grid(maxCols), (unsigned)n_jobs), 256,
+                 0, st, js);
+  MTKC_POST_LAUNCH("colred_final_many_kernel");
   return MTKC_OK;
 }
 

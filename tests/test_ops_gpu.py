@@ -84,6 +84,51 @@ def test_layernorm(rows, d):
     _close(g.param_grad("b"), gb, 2e-5)
 
 
+def test_layernorm_deferred_params_shared_and_many():
+    """backward() defers each layer norm's gain/bias column sums and reduces
+    them in one launch (32 jobs max) at the end of the sweep.  Two norms
+    sharing gain/bias force an early flush (the second writer must accumulate
+    onto the first's finished sum); 40 independent norms cross the 32-job
+    chunk boundary.  Every gradient still matches the reference."""
+    rng = np.random.default_rng(11)
+    rows, d, n = 50, 64, 40
+    g = M.ExpressionGraph(1)
+    xs = [rng.normal(size=(rows, d)).astype(np.float32) for _ in range(n + 2)]
+    Gs = [rng.normal(size=(rows, d)).astype(np.float32) for _ in range(n + 2)]
+    gains = [rng.normal(size=d).astype(np.float32) for _ in range(n + 1)]
+    biases = [rng.normal(size=d).astype(np.float32) for _ in range(n + 1)]
+    losses = []
+    gs = _param(g, "gs", gains[n])
+    bs = _param(g, "bs", biases[n])
+    for i in range(n + 2):
+        nx = _param(g, f"x{i}", xs[i])
+        if i < n:
+            o = g.layer_norm(nx, _param(g, f"g{i}", gains[i]), _param(g, f"b{i}", biases[i]))
+        else:  # two norms on one (gain, bias) pair
+            o = g.layer_norm(nx, gs, bs)
+        losses.append(_seeded(g, o, Gs[i]))
+    loss = losses[0]
+    for l in losses[1:]:
+        loss = g.add(loss, l)
+    g.forward()
+    g.zero_grads()
+    g.backward(loss)
+    sg = np.zeros(d, np.float32)
+    sb = np.zeros(d, np.float32)
+    for i in range(n + 2):
+        gi, bi = (gains[i], biases[i]) if i < n else (gains[n], biases[n])
+        _, gx, gg, gb = R.op_layernorm(xs[i], gi, bi, Gs[i])
+        _close(g.param_grad(f"x{i}"), gx, 2e-5)
+        if i < n:
+            _close(g.param_grad(f"g{i}"), gg, 2e-5)
+            _close(g.param_grad(f"b{i}"), gb, 2e-5)
+        else:
+            sg += gg
+            sb += gb
+    _close(g.param_grad("gs"), sg, 2e-5)
+    _close(g.param_grad("bs"), sb, 2e-5)
+
+
 def test_softmax_masked():
     rng = np.random.default_rng(2)
     x = (rng.normal(size=(4, 3, 17)) * 4).astype(np.float32)
