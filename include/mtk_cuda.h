@@ -181,6 +181,11 @@ int mtkc_gemm_last_path(void);
  * buckets are in flight (a persistent GEMM holding all 148 SMs would queue
  * the all-reduce kernels behind it); host-side state, not stream-ordered. */
 int mtkc_gemm_set_sm_limit(int sms);
+/* Tuning switch: 1 (default) lets the tensor-core GEMM run 256-row tiles on
+ * CTA pairs (cta_group::2), 0 keeps single-CTA 128-row tiles, 3 pairs only
+ * the products without fused operand sums (colsum); host-side state, read
+ * at each call (MTK_GEMM_NO_PAIR=1 sets 0 at load, MTK_GEMM_PAIR_NO_CS=1 3). */
+int mtkc_gemm_set_pair(int enable);
 
 /* ======================================================================== */
 /* elementwise / broadcast (tensor.cpp:111-237, graph.cpp:139-268)          */

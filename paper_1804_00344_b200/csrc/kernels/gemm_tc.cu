@@ -101,26 +101,52 @@ struct TcMaps {
   CUtensorMap a[3], b[3], c[3], g, r;  // r: addend (source of the beta term)
 };
 
-template <int BN>
+// staging buffers (32x32 fp32, 4 KB) per epilogue warp: two for the TMA
+// store double buffer; a ring of four in the LOADS instantiation, where each
+// buffer takes a TMA-loaded residual / C box, the result in place and the
+// store, three chunks ahead of the one being drained
+template <bool LOADS>
+constexpr int epi_bufs() {
+  return LOADS ? 4 : 2;
+}
+
+template <int BN, bool PAIR = false, bool LOADS = false>
 struct TcSmem {
   static constexpr uint32_t A_BYTES = BM * BK * 4;
-  static constexpr uint32_t B_BYTES = BN * BK * 4;
-  // pipeline depth: as many stages as fit next to the epilogue staging
-  // (227 KB): 6 x 32 KB for BN=128, 4 x 48 KB for BN=256.  fp32 operands
-  // make a k-block short in FLOPs, so depth is what covers L2/HBM latency.
-  static constexpr int ST = KA == 2 ? (BN == 256 ? 2 : 3)
-                                    : (EPI_WARPS == 8 ? (BN == 256 ? 3 : 5) : (BN == 256 ? 4 : 6));
+  // a CTA pair (cta_group::2) stages half of the tile's B columns per CTA
+  static constexpr uint32_t B_BYTES = (PAIR ? BN / 2 : BN) * BK * 4;
   // per epilogue warp (8): two 32x32 fp32 staging tiles (128B-swizzled, TMA store)
-  static constexpr size_t EPI_BYTES = EPI_WARPS * 2 * 32 * 32 * sizeof(float);
-  static constexpr size_t BYTES = 1024 + ST * (size_t)(A_BYTES + B_BYTES) + EPI_BYTES + 256;
+  static constexpr size_t EPI_BYTES = EPI_WARPS * epi_bufs<LOADS>() * 32 * 32 * sizeof(float);
+  // pipeline depth: as many stages as fit next to the epilogue staging
+  // (227 KB): 6 x 32 KB for BN=128, 4 x 48 KB for BN=256; a CTA pair's
+  // half-B stages give 6 x 32 KB (BN=256) / 8 x 24 KB (BN=128).  fp32
+  // operands make a k-block short in FLOPs, so depth is what covers latency.
+  static constexpr int ST_FIT = (int)((232448 - 1024 - EPI_BYTES - 512) / (A_BYTES + B_BYTES));
+  static constexpr int ST_LEGACY = KA == 2 ? (BN == 256 ? 2 : 3)
+                                 : (EPI_WARPS == 8 ? (BN == 256 ? 3 : 5) : (BN == 256 ? 4 : 6));
+  static constexpr int ST = PAIR ? (ST_FIT < 8 ? ST_FIT : 8)
+                                 : (ST_FIT < ST_LEGACY ? ST_FIT : ST_LEGACY);
+  static constexpr size_t BYTES = 1024 + ST * (size_t)(A_BYTES + B_BYTES) + EPI_BYTES + 512;
 };
 
 // LOADS: the epilogue reads beta*C and/or a ReLU gate (TMA-loaded boxes);
 // a separate instantiation so the common bias/ReLU epilogue stays lean.
-template <int BN, bool A_MN, bool B_MN, bool LOADS>
+// PAIR: a cluster of two CTAs on neighbouring SMs computes one 256 x BN tile
+// with tcgen05.mma.cta_group::2 issued by the even CTA.  Each CTA stages its
+// own 128 rows of A and half of the tile's B columns, so every SM receives
+// 2/3 of the operand bytes of a single-CTA 128 x BN tile (the L2 -> SM
+// traffic is what bounds these fp32-operand GEMMs); each CTA's TMEM holds
+// its 128 rows of the accumulator and its own epilogue drains them.
+template <int BN, bool A_MN, bool B_MN, bool LOADS, bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tf32_tc_kernel(const __grid_constant__ TcMaps maps, TcP p) {
-  using L = TcSmem<BN>;
+  using L = TcSmem<BN, PAIR, LOADS>;
+  constexpr int NB = epi_bufs<LOADS>();
+  constexpr int BNL = PAIR ? BN / 2 : BN;  // B columns staged by this CTA
+  constexpr int MT = PAIR ? 2 * BM : BM;    // output rows per tile
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int units = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   constexpr int ST = L::ST;
   constexpr uint32_t A_BYTES = L::A_BYTES, B_BYTES = L::B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
@@ -134,8 +160,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;   // [2] MMA -> epilogue
   uint64_t* tempty = tfull + 2;   // [2] epilogue -> MMA
-  uint64_t* ldbar = tempty + 2;   // [8] TMA loads of C / gate boxes, per epilogue warp
-  uint32_t* tmemSlot = (uint32_t*)(ldbar + 8);
+  uint64_t* ldbar = tempty + 2;   // [EPI_WARPS * NB] TMA loads of C / gate boxes
+  uint32_t* tmemSlot = (uint32_t*)(ldbar + EPI_WARPS * NB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -150,27 +176,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       prefetch_tmap(&maps.g);
     if(p.hasAddend && p.tmaStore)
       prefetch_tmap(&maps.r);
-    for(int w = 0; w < 8; ++w)
+    for(int w = 0; w < EPI_WARPS * NB; ++w)
       mbar_init(&ldbar[w], 1);
     for(int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 1);
+      // pair with operand sums: the odd CTA's operand-sum warp relays its
+      // stage's arrival to the even CTA (see the producer)
+      mbar_init(&full[s], (PAIR && p.csOp && rank == 0) ? 2 : 1);
       mbar_init(&empty[s], p.csOp ? 2 : 1);  // MMA commit (+ operand-sum warp)
     }
     for(int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS);  // one arrival per epilogue warp
+      mbar_init(&tempty[a], EPI_WARPS * (PAIR ? 2 : 1));  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if(warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmemSlot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if(PAIR) {  // both CTAs of the pair allocate together (same column base)
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmemSlot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmemSlot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if(PAIR)
+    cluster_sync_all();  // the peer's barriers are initialised before any remote signal
+  else
+    __syncthreads();
   tc_fence_after();
   // PDL: barrier init, TMEM allocation and descriptor prefetch above overlap
   // the previous kernel's tail; wait for it before any operand is read
@@ -188,7 +226,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     t -= tprob * tilesPerProb;
     split = t / tilesPerSplit;
     int rem = t - split * tilesPerSplit;
-    m0 = (rem % p.mt) * BM;
+    m0 = (rem % p.mt) * MT + (int)rank * BM;
     n0 = (rem / p.mt) * BN;
     kb0 = split * p.kbPerSplit;
     nkb = min(p.numKb, kb0 + p.kbPerSplit) - kb0;
@@ -197,14 +235,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if(warp == 0) {
     if(lane == 0) {
       int i = 0;  // global k-block counter (ring position)
-      for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x) {
+      for(int t = unit0; t < p.numTiles; t += units) {
         int m0, n0, kb0, nkb, split;
         tileCoords(t, m0, n0, kb0, nkb, split);
+        const int nB = n0 + (int)rank * BNL;  // this CTA's B columns
         for(int kb = 0; kb < nkb; ++kb, ++i) {
           int s = i % ST;
           if(i >= ST)
             mbar_wait(&empty[s], ((i / ST) - 1) & 1);
-          mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+          // pair: both CTAs' bytes complete on the even CTA's barrier -- or,
+          // when the odd CTA's operand-sum warp must see its own stage, on
+          // each CTA's own barrier, the odd one relayed by that warp
+          const bool relay = PAIR && p.csOp;
+          if(!PAIR || rank == 0 || relay)
+            mbar_expect_tx(&full[s], (A_BYTES + B_BYTES) * ((PAIR && !relay) ? 2u : 1u));
+          const uint32_t fb = PAIR ? mapa_shared(smem_u32(&full[s]), relay ? rank : 0u) : 0u;
+          auto ld2 = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if(PAIR)
+              tma_load_2d_cg2(dst, m, fb, c0, c1);
+            else
+              tma_load_2d(dst, m, &full[s], c0, c1);
+          };
+          auto ld3 = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2) {
+            if(PAIR)
+              tma_load_3d_cg2(dst, m, fb, c0, c1, c2);
+            else
+              tma_load_3d(dst, m, &full[s], c0, c1, c2);
+          };
           const int kbg = kb0 + kb;
           const int pk = p.kconcat ? kbg / p.nkbProb : tprob;  // problem of this k-block
           const int k0 = (p.kconcat ? kbg - pk * p.nkbProb : kbg) * BK;
@@ -214,42 +271,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t* b = sB + s * B_BYTES;
           if(A_MN) {
             if(p.a3d)
-              tma_load_3d(a, mapA, &full[s], 0, k0, m0 / 32);
+              ld3(a, mapA, 0, k0, m0 / 32);
             else
               for(int j = 0; j < BM / 32; ++j)
-                tma_load_2d(a + j * (BK * 128), mapA, &full[s], m0 + j * 32, k0);
+                ld2(a + j * (BK * 128), mapA, m0 + j * 32, k0);
           } else if(KA == 1) {
-            tma_load_2d(a, mapA, &full[s], k0, m0);
+            ld2(a, mapA, k0, m0);
           } else if(p.ak3d) {  // [KA][BM][32]
-            tma_load_3d(a, mapA, &full[s], 0, m0, k0 / 32);
+            ld3(a, mapA, 0, m0, k0 / 32);
           } else {
             for(int c = 0; c < KA; ++c)
-              tma_load_2d(a + c * (BM * 128), mapA, &full[s], k0 + c * 32, m0);
+              ld2(a + c * (BM * 128), mapA, k0 + c * 32, m0);
           }
           if(B_MN) {
             if(p.b3d)
-              tma_load_3d(b, mapB, &full[s], 0, k0, n0 / 32);
+              ld3(b, mapB, 0, k0, nB / 32);
             else
-              for(int j = 0; j < BN / 32; ++j)
-                tma_load_2d(b + j * (BK * 128), mapB, &full[s], n0 + j * 32, k0);
+              for(int j = 0; j < BNL / 32; ++j)
+                ld2(b + j * (BK * 128), mapB, nB + j * 32, k0);
           } else if(KA == 1) {
-            tma_load_2d(b, mapB, &full[s], k0, n0);
-          } else if(p.bk3d) {  // [KA][BN][32]
-            tma_load_3d(b, mapB, &full[s], 0, n0, k0 / 32);
+            ld2(b, mapB, k0, nB);
+          } else if(p.bk3d) {  // [KA][BNL][32]
+            ld3(b, mapB, 0, nB, k0 / 32);
           } else {
             for(int c = 0; c < KA; ++c)
-              tma_load_2d(b + c * (BN * 128), mapB, &full[s], k0 + c * 32, n0);
+              ld2(b + c * (BNL * 128), mapB, k0 + c * 32, nB);
           }
         }
       }
     }
   } else if(warp == 1) {
+    if(!PAIR || rank == 0) {  // the even CTA issues the pair's MMAs
     // instruction descriptor: D=f32, A=B=tf32, majors, N>>3, M>>4
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
                            ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+                           ((uint32_t)(MT >> 4) << 24);
     int i = 0, lt = 0;
-    for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x, ++lt) {
+    for(int t = unit0; t < p.numTiles; t += units, ++lt) {
       int m0, n0, kb0, nkb, split;
       tileCoords(t, m0, n0, kb0, nkb, split);
       const int acc = lt & 1;
@@ -277,18 +335,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                : umma_desc(aBase + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16,
                                            1024, 2);
             uint64_t bd = B_MN ? umma_desc(bBase + kk * 1024, BK * 128, 512, 1)
-                               : umma_desc(bBase + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16,
+                               : umma_desc(bBase + (kk >> 2) * (BNL * 128) + (kk & 3) * 32, 16,
                                            1024, 2);
-            if(!(p.dbg & 2))
-              mma_tf32(tacc, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            if(!(p.dbg & 2)) {
+              if(PAIR)
+                mma_tf32_cg2(tacc, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+              else
+                mma_tf32(tacc, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            }
           }
-          mma_commit(&empty[s]);
+          if(PAIR)
+            mma_commit_cg2(&empty[s], 3);  // frees the stage in both CTAs
+          else
+            mma_commit(&empty[s]);
         }
         __syncwarp();
       }
-      if(lane == 0)
-        mma_commit(&tfull[acc]);
+      if(lane == 0) {
+        if(PAIR)
+          mma_commit_cg2(&tfull[acc], 3);  // both CTAs' epilogues
+        else
+          mma_commit(&tfull[acc]);
+      }
       __syncwarp();
+    }
+    } else if(PAIR && p.csOp) {
+      // odd CTA with operand sums: its stages complete on its own barriers
+      // (the operand-sum warp reads them); this otherwise idle warp relays
+      // each arrival to the even CTA's MMA issuer
+      int i = 0;
+      for(int t = unit0; t < p.numTiles; t += units) {
+        int m0, n0, kb0, nkb, split;
+        tileCoords(t, m0, n0, kb0, nkb, split);
+        for(int kb = 0; kb < nkb; ++kb, ++i) {
+          const int s = i % ST;
+          mbar_wait(&full[s], (i / ST) & 1);
+          if(lane == 0)
+            mbar_arrive_cluster(mapa_shared(smem_u32(&full[s]), 0));
+          __syncwarp();
+        }
+      }
     }
   } else if(warp < CS_WARP) {
     // epilogue warps 2..9: TMEM lane quarter q = warp % 4 (the quarter a
@@ -297,20 +383,58 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int cBeg = h * (BN * 4 / EPI_WARPS), cEnd = cBeg + BN * 4 / EPI_WARPS;
     // two swizzled 32x32 staging tiles per warp (TMA-store mode); the
     // fallback path reuses the first one as a padded transpose buffer
-    float* stage0 = sEpi + ew * 2 * 1024;
+    float* stage0 = sEpi + ew * NB * 1024;
     int chunk = 0;  // chunks handed to the TMA engine by this warp
     uint32_t ldPhase = 0;  // TMA C / gate box loads completed by this warp
-    // LOADS with one extra source (beta*C / addend, or the ReLU gate): each
-    // lane prefetches its row's 32 values of the NEXT chunk into registers
-    // while the current chunk is processed (the load latency hides behind the
-    // TMEM read and the stores); both sources together use TMA boxes.
-    const bool pf = LOADS && !p.part && p.tmaStore && !(p.dbg & 4) &&
+    // beta*C / addend without a gate (the fused residual): a ring of NB
+    // staging buffers per warp; chunk j's box is TMA-loaded NB - 1 chunks
+    // ahead into buffer j % NB, the result overwrites it in place and is
+    // TMA-stored from there (the load latency hides behind NB - 1 chunks)
+    const bool ring = LOADS && NB > 2 && !p.part && p.tmaStore && !(p.dbg & 4) &&
+                      p.beta != 0.f && p.gate == nullptr;
+    constexpr int CPT = BN * 4 / EPI_WARPS / 32;  // chunks per tile and warp
+    int jr = 0;                                   // ring position (every chunk)
+    // box origin of this warp's rows in tile tt (cached: chunks arrive in order)
+    int rcT = -1, rcRow = 0, rcCol = 0, rcPr = 0;
+    auto ringTile = [&](int tt) {
+      if(tt == rcT)
+        return;
+      rcT = tt;
+      rcPr = p.kconcat ? 0 : tt / tilesPerProb;
+      const int r2 = (tt - rcPr * tilesPerProb) % tilesPerSplit;
+      const int mi = r2 % p.mt;
+      rcRow = mi * MT + (int)rank * BM + q * 32;
+      rcCol = ((r2 - mi) / p.mt) * BN + cBeg;
+    };
+    auto ringIssue = [&](int jj) {  // lane 0: the box of this warp's chunk jj
+      const int ti = jj / CPT, tt = unit0 + ti * units;
+      if(tt >= p.numTiles)
+        return;
+      uint64_t* bar = &ldbar[ew * NB + jj % NB];
+      ringTile(tt);
+      const int col = rcCol + 32 * (jj - ti * CPT);
+      if(rcRow >= p.M || col >= p.N) {  // nothing to load: complete the phase
+        mbar_arrive(bar);
+        return;
+      }
+      mbar_expect_tx(bar, 4096u);
+      tma_load_2d(stage0 + (jj % NB) * 1024, p.hasAddend ? &maps.r : &maps.c[rcPr], bar, col,
+                  rcRow);
+    };
+    if(ring && lane == 0)
+      for(int jj = 0; jj < NB - 1; ++jj)
+        ringIssue(jj);
+    // LOADS with one extra source otherwise (the ReLU gate, or beta*C when
+    // the ring is off): each lane prefetches its row's 32 values of the NEXT
+    // chunk into registers while the current chunk is processed; both sources
+    // together use TMA boxes.
+    const bool pf = LOADS && !ring && !p.part && p.tmaStore && !(p.dbg & 4) &&
                     ((p.beta != 0.f) != (p.gate != nullptr));
     float nx[32];
     auto loadChunk = [&](int tt, int cc) {
       const int pr = p.kconcat ? 0 : tt / tilesPerProb;
       const int r2 = (tt - pr * tilesPerProb) % tilesPerSplit;
-      const int64_t row = (int64_t)(r2 % p.mt) * BM + q * 32 + lane;
+      const int64_t row = (int64_t)(r2 % p.mt) * MT + rank * BM + q * 32 + lane;
       const int64_t col = (int64_t)(r2 / p.mt) * BN + cc;
       const float* src = p.gate ? p.gate : (p.hasAddend ? p.addend : p.CP[pr]);
       src += row * p.ldc + col;
@@ -329,31 +453,52 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           nx[i] = (row < p.M && col + i < p.N) ? src[i] : 0.f;
       }
     };
-    if(pf && (int)blockIdx.x < p.numTiles)
-      loadChunk(blockIdx.x, cBeg);
+    if(pf && unit0 < p.numTiles)
+      loadChunk(unit0, cBeg);
     int lt = 0;
-    for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x, ++lt) {
+    for(int t = unit0; t < p.numTiles; t += units, ++lt) {
       int m0, n0, kb0, nkb, split;
       tileCoords(t, m0, n0, kb0, nkb, split);
       const int acc = lt & 1;
       const int64_t rowBase = m0 + q * 32;
       // the epilogue's extra sources (residual / beta*C, ReLU gate) of this
-      // warp's rows into L2 while the tile's main loop still runs
-      if(LOADS && p.tmaStore && !p.part && lane == 0 && rowBase < p.M) {
-        const int pr = p.kconcat ? 0 : t / tilesPerProb;
-        const CUtensorMap* src0 = p.beta != 0.f ? (p.hasAddend ? &maps.r : &maps.c[pr]) : nullptr;
-        const CUtensorMap* src1 = p.gate ? &maps.g : nullptr;
-        for(int c0 = cBeg; c0 < cEnd && n0 + c0 < p.N; c0 += 32) {
-          if(src0)
-            tma_prefetch_2d(src0, n0 + c0, (int)rowBase);
-          if(src1)
-            tma_prefetch_2d(src1, n0 + c0, (int)rowBase);
+      // warp's rows into L2 while the tile's main loop still runs -- for the
+      // ring, one tile ahead (its loads run a few chunks into the next tile)
+      if(LOADS && p.tmaStore && !p.part && lane == 0) {
+        for(int tp = (ring && lt == 0) ? t : (ring ? t + units : t);
+            tp <= (ring ? t + units : t) && tp < p.numTiles; tp += units) {
+          int pm0, pn0, pkb0, pnkb, psplit;
+          tileCoords(tp, pm0, pn0, pkb0, pnkb, psplit);
+          const int prow = pm0 + q * 32;
+          if(prow >= p.M)
+            continue;
+          const int pr = p.kconcat ? 0 : tp / tilesPerProb;
+          const CUtensorMap* src0 =
+              p.beta != 0.f ? (p.hasAddend ? &maps.r : &maps.c[pr]) : nullptr;
+          const CUtensorMap* src1 = p.gate ? &maps.g : nullptr;
+          for(int c0 = cBeg; c0 < cEnd && pn0 + c0 < p.N; c0 += 32) {
+            if(src0)
+              tma_prefetch_2d(src0, pn0 + c0, prow);
+            if(src1)
+              tma_prefetch_2d(src1, pn0 + c0, prow);
+          }
         }
+        tprob = p.kconcat ? 0 : t / tilesPerProb;  // tileCoords above moved it
+      }
+      const float* biasT = p.biasP[tprob];
+      // this warp's bias columns, lane l holding column cBeg + 32 j + l of
+      // chunk j: loaded before the accumulator wait, so the latency hides
+      // behind the main loop (broadcast to the row-owning lanes by shuffles)
+      constexpr int NCH = BN * 4 / EPI_WARPS / 32;
+      float bw[NCH];
+#pragma unroll
+      for(int j = 0; j < NCH; ++j) {
+        const int64_t c = (int64_t)n0 + cBeg + 32 * j + lane;
+        bw[j] = (biasT && !p.part && c < p.N) ? __ldg(biasT + c) : 0.f;
       }
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const CUtensorMap* mapC = &maps.c[p.part ? 0 : tprob];
-      const float* biasT = p.biasP[tprob];
       float* CT = p.CP[tprob];
       const int zpart = split * nOut + tprob;  // partial plane of this tile
       // relu_mask_out words of this lane's row, stored once per tile (a full
@@ -370,7 +515,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for(int i = 0; i < 32; ++i)
             cur[i] = nx[i];
-          const int tn = c0 + 32 < cEnd ? t : t + (int)gridDim.x;
+          const int tn = c0 + 32 < cEnd ? t : t + units;
           if(tn < p.numTiles)
             loadChunk(tn, c0 + 32 < cEnd ? c0 + 32 : cBeg);
         }
@@ -381,19 +526,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
         if(c0 + 32 >= cEnd) {  // our share read: hand it back to the MMA warp
           tc_fence_before();
-          if(lane == 0)
-            mbar_arrive(&tempty[acc]);
+          if(lane == 0) {
+            if(PAIR)
+              mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            else
+              mbar_arrive(&tempty[acc]);
+          }
         }
-        if(n0 + c0 >= p.N || rowBase >= p.M || (p.dbg & 1))
+        if(ring) {  // this chunk's box, whether or not the chunk is stored
+          mbar_wait(&ldbar[ew * NB + jr % NB], (jr / NB) & 1);
+        }
+        if(n0 + c0 >= p.N || rowBase >= p.M || (p.dbg & 1)) {
+          if(ring) {  // keep the ring moving: the buffer of chunk jr - 1 is free
+            if(lane == 0) {
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              ringIssue(jr + NB - 1);
+            }
+            __syncwarp();
+            ++jr;
+          }
           continue;
+        }
         const int64_t col0 = n0 + c0;
         if(p.tmaStore) {
-          float* stage = stage0 + (chunk & 1) * 1024;
+          float* stage = ring ? stage0 + (jr % NB) * 1024 : stage0 + (chunk & 1) * 1024;
           // the TMA engine must have finished reading this buffer (chunk - 2)
           // before it is refilled: early when a C / gate box lands in it,
           // otherwise as late as possible (after the arithmetic)
           // boxes land in the staging buffer (LOADS without prefetch): wait early
-          const bool loads = LOADS && !pf;
+          const bool loads = LOADS && !pf && !ring;
           if(chunk >= 2 && loads) {
             if(lane == 0)
               asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -406,7 +567,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if(!p.part) {
             const bool needC = LOADS && p.beta != 0.f, needG = LOADS && p.gate != nullptr;
             float* grow = stage;  // gate box buffer
-            if((needC || needG) && !pf) {
+            if((needC || needG) && !pf && !ring) {
               // C and/or the ReLU gate arrive as swizzled 32x32 boxes by TMA
               // (coalesced, async) instead of per-lane strided row reads
               if(needC && needG) {
@@ -436,22 +597,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 v[i] = p.alpha * v[i];
             }
             if(biasT) {
-              if(col0 + 32 <= p.N && ((uintptr_t)(biasT + col0) & 15) == 0) {
-                const float4* b4p = reinterpret_cast<const float4*>(biasT + col0);
+              const int jc = (c0 - cBeg) >> 5;
+              float bl = bw[0];
 #pragma unroll
-                for(int j = 0; j < 8; ++j) {
-                  const float4 b4 = __ldg(b4p + j);
-                  v[4 * j] = v[4 * j] + b4.x;
-                  v[4 * j + 1] = v[4 * j + 1] + b4.y;
-                  v[4 * j + 2] = v[4 * j + 2] + b4.z;
-                  v[4 * j + 3] = v[4 * j + 3] + b4.w;
-                }
-              } else {
-                const float bl = col0 + lane < p.N ? biasT[col0 + lane] : 0.f;
+              for(int j = 1; j < NCH; ++j)
+                bl = j == jc ? bw[j] : bl;
 #pragma unroll
-                for(int i = 0; i < 32; ++i)
-                  v[i] = v[i] + __shfl_sync(0xffffffffu, bl, i);
-              }
+              for(int i = 0; i < 32; ++i)
+                v[i] = v[i] + __shfl_sync(0xffffffffu, bl, i);
             }
             if(p.epi == MTKC_EPI_RELU) {
 #pragma unroll
@@ -513,7 +666,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             __syncwarp();  // every lane has read its C / gate row before the overwrite
           }
-          if(chunk >= 2 && !loads) {
+          if(chunk >= 2 && !loads && !ring) {
             if(lane == 0)
               asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             __syncwarp();
@@ -537,6 +690,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                   ::"l"((uint64_t)mapC), "r"(smem_u32(stage)), "r"((int)col0), "r"((int)rowBase)
                   : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if(ring) {  // all but this store have read their buffers: refill one
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              ringIssue(jr + NB - 1);
+            }
+          }
+          if(ring) {
+            __syncwarp();
+            ++jr;
           }
           ++chunk;
           continue;
@@ -622,15 +783,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // same for every such k; lanes l, l^10, l^20, l^30 hold the same columns.
     constexpr int CH = (BN > BM ? BN : BM) / 32;
     const bool sumB = p.csOp == 2;
-    const int nch = sumB ? BN / 32 : BM / 32;
+    const int nch = sumB ? BNL / 32 : BM / 32;
     const uint32_t sBytes = sumB ? B_BYTES : A_BYTES;
     const uint8_t* sOp = (sumB ? sB : sA) + (lane >> 3) * 128 + (lane & 7) * 16;
     int i = 0;
-    for(int t = blockIdx.x; t < p.numTiles; t += gridDim.x) {
+    for(int t = unit0; t < p.numTiles; t += units) {
       int m0, n0, kb0, nkb, split;
       tileCoords(t, m0, n0, kb0, nkb, split);
       // the first csR tiles of the operand block take its k-blocks in turn
-      const int R = p.csR, ri = sumB ? m0 / BM : n0 / BN;
+      const int R = p.csR, ri = sumB ? (m0 - (int)rank * BM) / MT : n0 / BN;
       const bool on = (sumB ? B_MN : A_MN) && ri < R;
       float4 acc[CH];
 #pragma unroll
@@ -660,7 +821,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if(!on)
         continue;
-      const int64_t len = p.csLen, base0 = sumB ? n0 : m0;
+      const int64_t len = p.csLen, base0 = sumB ? n0 + (int)rank * BNL : m0;
       float* dst = p.csSlots > 1
                        ? p.csPart + ((int64_t)tprob * p.csSlots + split * R + ri) * len
                        : p.csOut[tprob];
@@ -684,11 +845,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if(PAIR)
+    cluster_sync_all();  // no CTA leaves while its peer may still signal it
+  else
+    __syncthreads();
   if(warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
+    if(PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS));
   }
 }
 
@@ -900,33 +1068,75 @@ int g_sms = 0;
 int g_sm_limit = 0;  // 0 = every SM; else the persistent grid's cap (SMs left to NCCL)
 inline int gemm_sms() { return g_sm_limit > 0 && g_sm_limit < g_sms ? g_sm_limit : g_sms; }
 
-template <int BN, bool A_MN, bool B_MN, bool LOADS>
+// CTA pairs resident at once (clusters of two; a TPC's two SMs), 0 = unknown
+int g_pair_units = 0;
+bool g_pair_enabled = getenv("MTK_GEMM_NO_PAIR") == nullptr;
+// pairs also for products with fused operand sums (the odd CTA relays its
+// stage arrivals to the even CTA); MTK_GEMM_PAIR_NO_CS=1 keeps them single
+bool g_pair_colsum = getenv("MTK_GEMM_PAIR_NO_CS") == nullptr;
+
+template <int BN, bool A_MN, bool B_MN, bool LOADS, bool PAIR>
 int launch_tc(const TcMaps& maps, const TcP& p, cudaStream_t st) {
-  constexpr size_t smem = TcSmem<BN>::BYTES;
-  auto kern = gemm_tf32_tc_kernel<BN, A_MN, B_MN, LOADS>;
-  static bool attr = false;
-  if(!attr) {
+  constexpr size_t smem = TcSmem<BN, PAIR>::BYTES;
+  auto kern = gemm_tf32_tc_kernel<BN, A_MN, B_MN, LOADS, PAIR>;
+  static int units = 0;  // persistent grid cap (pairs for PAIR)
+  if(!units) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if(e != cudaSuccess)
       return cuda_status(e, "gemm_tf32_tc smem attribute");
-    attr = true;
+    units = g_sms;
+    if(PAIR) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * (unsigned)(g_sms / 2));
+      cfg.blockDim = dim3(TC_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      e = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
+      if(e != cudaSuccess || nc <= 0) {
+        cudaGetLastError();
+        nc = g_sms / 2;
+      }
+      units = std::min(nc, g_sms / 2);
+      g_pair_units = units;
+    }
   }
-  int grid = std::min(p.numTiles, gemm_sms());
-  ::mtkc::launch(kern, grid, TC_THREADS, smem, st, maps, p);
+  const int cap = PAIR ? std::min(units, gemm_sms() / 2) : gemm_sms();
+  const int grid = std::min(p.numTiles, std::max(1, cap));
+  if(PAIR)
+    ::mtkc::launch_cluster(kern, dim3(2 * grid), TC_THREADS, smem, st, 2, maps, p);
+  else
+    ::mtkc::launch(kern, grid, TC_THREADS, smem, st, maps, p);
   MTKC_POST_LAUNCH("gemm_tf32_tc_kernel");
   return MTKC_OK;
 }
 
-template <int BN, bool LOADS>
+template <int BN, bool LOADS, bool PAIR>
 int dispatch_majors(bool aMN, bool bMN, const TcMaps& maps, const TcP& p, cudaStream_t st) {
   if(!aMN && !bMN)
-    return launch_tc<BN, false, false, LOADS>(maps, p, st);
+    return launch_tc<BN, false, false, LOADS, PAIR>(maps, p, st);
   if(!aMN && bMN)
-    return launch_tc<BN, false, true, LOADS>(maps, p, st);
+    return launch_tc<BN, false, true, LOADS, PAIR>(maps, p, st);
   if(aMN && !bMN)
-    return launch_tc<BN, true, false, LOADS>(maps, p, st);
-  return launch_tc<BN, true, true, LOADS>(maps, p, st);
+    return launch_tc<BN, true, false, LOADS, PAIR>(maps, p, st);
+  return launch_tc<BN, true, true, LOADS, PAIR>(maps, p, st);
+}
+
+template <bool PAIR>
+int dispatch_tc(int BN, bool loads, bool aMN, bool bMN, const TcMaps& maps, const TcP& p,
+                cudaStream_t st) {
+  if(loads)
+    return BN == 256 ? dispatch_majors<256, true, PAIR>(aMN, bMN, maps, p, st)
+                     : dispatch_majors<128, true, PAIR>(aMN, bMN, maps, p, st);
+  return BN == 256 ? dispatch_majors<256, false, PAIR>(aMN, bMN, maps, p, st)
+                   : dispatch_majors<128, false, PAIR>(aMN, bMN, maps, p, st);
 }
 
 }  // namespace
@@ -978,13 +1188,25 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
     if(g_sms <= 0)
       g_sms = 148;
   }
-  const int sms = gemm_sms();
   const int nOut = kconcat ? 1 : nprob;
-  const int64_t mt = cdiv(a.M, BM);
+  // CTA pairs (256-row tiles over two SMs; the fused operand sums are taken
+  // by each CTA over its own staged half).  Measured (tools/epi_var.py,
+  // gemm_bench.py MTK_BENCH_AB=1): pairs win
+  // once the single-CTA tiles fill more than one wave or the k loop is long
+  // (operand traffic dominates); a single short wave (M x 512 x 512) and the
+  // small-M weight-gradient products stay single-CTA
+  const int64_t tiles1 = cdiv(a.M, BM) * cdiv(a.N, a.N >= 256 ? 256 : 128) * nOut;
+  const bool pair = g_pair_enabled && a.M >= 1024 && (csOp == 0 || g_pair_colsum) &&
+                    (tiles1 > gemm_sms() || cdiv(a.K, BK) * (kconcat ? nprob : 1) >= 32);
+  // scheduling units: CTAs, or CTA pairs
+  const int sms = pair ? std::max(1, (g_pair_units ? std::min(g_pair_units, gemm_sms() / 2)
+                                                   : gemm_sms() / 2))
+                       : gemm_sms();
+  const int64_t mt = cdiv(a.M, pair ? 2 * BM : BM);
   // wide tiles halve the re-reads of A (the L2->SM operand traffic that
   // bounds fp32-storage GEMMs) -- worth a partly idle wave; narrow tiles only
   // when there are so few wide tiles that split-K would have to fill the GPU
-  int BN = (a.N >= 256 && mt * cdiv(a.N, 256) * nOut >= 32) ? 256 : 128;
+  int BN = (a.N >= 256 && mt * cdiv(a.N, 256) * nOut >= (pair ? 16 : 32)) ? 256 : 128;
   if(const char* e = getenv("MTK_GEMM_BN"))  // tuning override (tools/gemm_bench.py)
     BN = (atoi(e) == 256 && a.N >= 256) ? 256 : 128;
   const int64_t nt = cdiv(a.N, BN);
@@ -1041,14 +1263,15 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
       ok = make_map(&maps.a[q], b.A, a.K, a.M, a.lda, 32, BM, false);
     if(!ok)
       return false;
+    const uint32_t bnl = pair ? (uint32_t)BN / 2 : (uint32_t)BN;  // B columns per CTA
     if(bMN && b3d)
-      ok = make_map3(&maps.b[q], b.B, a.N, a.K, a.ldb, BK, (uint32_t)BN / 32);
+      ok = make_map3(&maps.b[q], b.B, a.N, a.K, a.ldb, BK, bnl / 32);
     else if(bMN)  // storage [K x N]
       ok = make_map(&maps.b[q], b.B, a.N, a.K, a.ldb, 32, BK, true);
     else if(bk3d)
-      ok = make_mapk3(&maps.b[q], b.B, a.K, a.N, a.ldb, (uint32_t)BN);
+      ok = make_mapk3(&maps.b[q], b.B, a.K, a.N, a.ldb, bnl);
     else     // storage [N x K]
-      ok = make_map(&maps.b[q], b.B, a.K, a.N, a.ldb, 32, (uint32_t)BN, false);
+      ok = make_map(&maps.b[q], b.B, a.K, a.N, a.ldb, 32, bnl, false);
     if(!ok)
       return false;
   }
@@ -1130,12 +1353,8 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   if(getenv("MTK_GEMM_NO_TMA_STORE"))
     p.tmaStore = 0;
   const bool loads = p.tmaStore && !p.part && (a.beta != 0.f || a.gate != nullptr);
-  if(loads)
-    *rc = BN == 256 ? dispatch_majors<256, true>(aMN, bMN, maps, p, st)
-                    : dispatch_majors<128, true>(aMN, bMN, maps, p, st);
-  else
-    *rc = BN == 256 ? dispatch_majors<256, false>(aMN, bMN, maps, p, st)
-                    : dispatch_majors<128, false>(aMN, bMN, maps, p, st);
+  *rc = pair ? dispatch_tc<true>(BN, loads, aMN, bMN, maps, p, st)
+             : dispatch_tc<false>(BN, loads, aMN, bMN, maps, p, st);
   if(*rc == MTKC_OK && splits > 1) {  // one launch for every output problem
     ReduceOut outs{};
     bool vec = a.N % 4 == 0 && a.ldc % 4 == 0 && (uintptr_t)a.workspace % 16 == 0;
@@ -1195,6 +1414,12 @@ bool tc_gemm(const mtkc_gemm_args& a, cudaStream_t st, int* rc, bool* csFused) {
 namespace mtkc {
 void gemm_set_sm_limit(int sms) { g_sm_limit = sms > 0 ? sms : 0; }
 }  // namespace mtkc
+
+extern "C" int mtkc_gemm_set_pair(int enable) {
+  mtkc::g_pair_enabled = enable != 0;
+  mtkc::g_pair_colsum = enable != 3;
+  return MTKC_OK;
+}
 
 extern "C" int mtkc_gemm_set_sm_limit(int sms) {
   mtkc::gemm_set_sm_limit(sms);

@@ -26,7 +26,13 @@ shapes = [  # (name, M, N, K, transA, transB)
     ("ffn1 fwd +bias+relu", R, 2048, 512, 0, 0, "relu"),
     ("ffn2 dX +gate", R, 2048, 512, 0, 1, "gate"),
     ("proj dW beta=1", 512, 512, R, 1, 0, "beta"),
+    ("proj fwd +b+resid", R, 512, 512, 0, 0, "addend"),
+    ("ffn2 fwd +b+resid", R, 512, 2048, 0, 0, "addend"),
+    ("ffn1 dW +colsum", 512, 2048, R, 1, 0, "colsum"),
 ]
+if os.environ.get("MTK_BENCH_ONLY"):
+    keep = os.environ["MTK_BENCH_ONLY"].split(",")
+    shapes = [s for s in shapes if any(k in s[0] for k in keep)]
 ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 stream = torch.cuda.current_stream().cuda_stream
 for name, M, N, K, ta, tb, *extra in shapes:
@@ -46,16 +52,39 @@ for name, M, N, K, ta, tb, *extra in shapes:
         args["gate"] = gate.data_ptr()
     if ep == "beta":
         args["beta"] = 1.0
-    for _ in range(3):
+    if ep == "addend":
+        addend = torch.randn(M, N, device="cuda")
+        args["bias"] = bias.data_ptr()
+        args["beta"] = 1.0
+        args["addend"] = addend.data_ptr()
+    if ep == "colsum":
+        cs = torch.zeros(N, device="cuda")
+        args["colsum"] = cs.data_ptr()
+        args["colsum_of"] = 2  # MTKC_COLSUM_B
+    def run():
         cabi.gemm(M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, **args)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        cabi.gemm(M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], C.data_ptr(), N, **args)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    tf = 2.0 * M * N * K / ms / 1e9
+
+    modes = [1, 0] if os.environ.get("MTK_BENCH_AB") else [None]
+    best = {}
+    for rnd in range(2 if modes[0] is not None else 1):
+        for mode in modes:
+            if mode is not None:
+                cabi.lib().mtkc_gemm_set_pair(mode)
+            for _ in range(3):
+                run()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                run()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            best[mode] = min(best.get(mode, 1e9), ms)
     ref = (A.t() if ta else A) @ (B.t() if tb else B)
     err = ((C - ref).abs().max() / ref.abs().max()).item() if not ep else float("nan")
-    print(f"{name:22s} M{M:6d} N{N:6d} K{K:6d}  {ms*1e3:9.1f} us  {tf:7.1f} TF/s  relerr {err:.1e}", flush=True)
+    line = f"{name:22s} M{M:6d} N{N:6d} K{K:6d}"
+    for mode, ms in best.items():
+        tf = 2.0 * M * N * K / ms / 1e9
+        tag = "" if mode is None else ("pair " if mode else "single ")
+        line += f"  {tag}{ms*1e3:8.1f} us {tf:6.1f} TF/s"
+    print(line + f"  relerr {err:.1e}", flush=True)
