@@ -1077,7 +1077,7 @@ bool g_pair_colsum = getenv("MTK_GEMM_PAIR_NO_CS") == nullptr;
 
 template <int BN, bool A_MN, bool B_MN, bool LOADS, bool PAIR>
 int launch_tc(const TcMaps& maps, const TcP& p, cudaStream_t st) {
-  constexpr size_t smem = TcSmem<BN, PAIR>::BYTES;
+  constexpr size_t smem = TcSmem<BN, PAIR, LOADS>::BYTES;
   auto kern = gemm_tf32_tc_kernel<BN, A_MN, B_MN, LOADS, PAIR>;
   static int units = 0;  // persistent grid cap (pairs for PAIR)
   if(!units) {

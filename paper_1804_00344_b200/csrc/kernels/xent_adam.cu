@@ -9,6 +9,7 @@
 // recomputes p = exp(x - max)/sum in the same order as the reference and
 // writes the logits gradient in one pass: 2*4*N*V bytes of HBM per step.
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 using namespace mtkc;
 
@@ -323,6 +324,88 @@ __global__ void __launch_bounds__(XF, 1) xent_fused_kernel(float* logits, const 
   }
 }
 
+// Persistent form of xent_fused_kernel: one CTA per SM walks rows
+// r, r + grid, ...; while row r is reduced and its gradient stored from
+// registers, row r + grid already streams into shared memory (one bulk
+// copy), so every SM keeps a row of reads in flight through the whole
+// kernel (the one-row-per-CTA form idles HBM during its reductions).
+// Same arithmetic, same order as xent_fused_kernel.
+template <int NV>
+__global__ void __launch_bounds__(XF, 1) xent_fused_persist_kernel(float* logits,
+                                                                   const int32_t* tg,
+                                                                   const float* mask, int64_t rows,
+                                                                   int64_t V, float scale,
+                                                                   float count, float* rowLoss) {
+  extern __shared__ __align__(16) float srow[];  // [V]
+  __shared__ float red[32];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t V4 = V / 4;
+  const uint32_t bytes = (uint32_t)(V * 4);
+  if(threadIdx.x == 0) {
+    mtkc::tc::mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  MTKC_PDL_ENTRY();
+  if(threadIdx.x == 0 && (int64_t)blockIdx.x < rows) {
+    mtkc::tc::mbar_expect_tx(&bar, bytes);
+    mtkc::tc::bulk_load_1d(srow, logits + (int64_t)blockIdx.x * V, bytes, &bar);
+  }
+  uint32_t phase = 0;
+  const float4* s4 = reinterpret_cast<const float4*>(srow);
+  for(int64_t r = blockIdx.x; r < rows; r += gridDim.x, phase ^= 1) {
+    mtkc::tc::mbar_wait(&bar, phase);
+    float4 v[NV];
+    float mx = -INFINITY;
+#pragma unroll
+    for(int k = 0; k < NV; ++k) {
+      const int64_t j = threadIdx.x + (int64_t)k * XF;
+      v[k] = j < V4 ? s4[j] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      mx = fmaxf(mx, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+    }
+    const int32_t y = tg[r];
+    const float xy = srow[y];
+    __syncthreads();  // the row buffer is free: stream in the next row
+    if(threadIdx.x == 0 && r + gridDim.x < rows) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mtkc::tc::mbar_expect_tx(&bar, bytes);
+      mtkc::tc::bulk_load_1d(srow, logits + (r + gridDim.x) * V, bytes, &bar);
+    }
+    mx = block_max(mx, red);
+    float s = 0.f;
+#pragma unroll
+    for(int k = 0; k < NV; ++k)
+      if(threadIdx.x + (int64_t)k * XF < V4)
+        s += (__expf(v[k].x - mx) + __expf(v[k].y - mx)) + (__expf(v[k].z - mx) + __expf(v[k].w - mx));
+    s = block_sum(s, red);
+    const float m = mask ? mask[r] : 1.f;
+    if(threadIdx.x == 0)
+      rowLoss[r] = m != 0.f ? m * (mx + logf(s) - xy) : 0.f;
+    const float gm = (scale / count) * m;
+    const float sc = m != 0.f ? gm / s : 0.f;
+    float4* x4 = reinterpret_cast<float4*>(logits + r * V);
+#pragma unroll
+    for(int k = 0; k < NV; ++k) {
+      const int64_t j = threadIdx.x + (int64_t)k * XF;
+      if(j >= V4)
+        break;
+      float4 o;
+      o.x = sc * __expf(v[k].x - mx);
+      o.y = sc * __expf(v[k].y - mx);
+      o.z = sc * __expf(v[k].z - mx);
+      o.w = sc * __expf(v[k].w - mx);
+      const int64_t dd = (int64_t)y - 4 * j;
+      if(m != 0.f && dd >= 0 && dd < 4) {
+        if(dd == 0) o.x -= gm;
+        if(dd == 1) o.y -= gm;
+        if(dd == 2) o.z -= gm;
+        if(dd == 3) o.w -= gm;
+      }
+      __stcs(x4 + j, o);
+    }
+  }
+}
+
 // One element of the reference's Adam + EMA, with separately rounded ops
 // (kernels are compiled with -fmad=false) in the reference's order.
 __device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v, float& a,
@@ -456,13 +539,35 @@ int mtkc_xent_fused(float* logits, const int32_t* targets, const float* mask, in
     return fail(MTKC_DIMENSION, "fused cross entropy needs vocab % 4 == 0, vocab <= 32768");
   ProfScope prof(S(stream), "xent", 8.0 * rows * vocab);  // read logits, write dlogits
   const int nv = (int)cdiv(vocab / 4, XF);
+  static const bool persist = getenv("MTK_XENT_ROWS") == nullptr;  // A/B switch
+  if(persist) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::min<int64_t>(rows, sms);
+    const size_t smem = (size_t)vocab * sizeof(float);
+#define XF_LAUNCH(NVV)                                                                        \
+  if(nv <= NVV) {                                                                             \
+    static bool attr = false;                                                                 \
+    if(!attr) {                                                                               \
+      cudaFuncSetAttribute(xent_fused_persist_kernel<NVV>,                                    \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32768);           \
+      attr = true;                                                                            \
+    }                                                                                         \
+    ::mtkc::launch(xent_fused_persist_kernel<NVV>, grid, XF, smem, S(stream), logits, targets, \
+                   mask, rows, vocab, scale, count, row_loss);                                \
+  } else
+    XF_LAUNCH(1) XF_LAUNCH(2) XF_LAUNCH(4) XF_LAUNCH(8) {}
+#undef XF_LAUNCH
+  } else {
 #define XF_LAUNCH(NVV)                                                                       \
   if(nv <= NVV) {                                                                            \
     ::mtkc::launch(xent_fused_kernel<NVV>, (unsigned)rows, XF, 0, S(stream), logits, targets, \
                    mask, vocab, scale, count, row_loss);                                     \
   } else
-  XF_LAUNCH(1) XF_LAUNCH(2) XF_LAUNCH(4) XF_LAUNCH(8) {}
+    XF_LAUNCH(1) XF_LAUNCH(2) XF_LAUNCH(4) XF_LAUNCH(8) {}
 #undef XF_LAUNCH
+  }
   MTKC_POST_LAUNCH("xent_fused_kernel");
   ::mtkc::launch(loss_sum_kernel, 1, 1024, 0, S(stream), row_loss, rows, count, loss);
   MTKC_POST_LAUNCH("loss_sum_kernel");
