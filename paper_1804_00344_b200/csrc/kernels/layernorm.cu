@@ -358,18 +358,26 @@ __global__ void __launch_bounds__(LN_WARPS * 32)
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   int it = 0;
-  if(r0 + w < r1)
+  // the row statistics travel one row ahead with the staged rows (a load at
+  // use would put an L2 round trip in front of every row)
+  float muN = 0.f, rsN = 0.f;
+  if(r0 + w < r1) {
     issue(r0 + w, 0);
+    muN = __ldg(mean + r0 + w);
+    rsN = __ldg(invStd + r0 + w);
+  }
   for(int64_t row = r0 + w; row < r1; row += LN_WARPS, ++it) {
     const int st = it % LNS;
+    const float mu = muN, rs = rsN;
     if(row + LN_WARPS < r1) {
       issue(row + LN_WARPS, (it + 1) % LNS);
+      muN = __ldg(mean + row + LN_WARPS);
+      rsN = __ldg(invStd + row + LN_WARPS);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     const float4* b = stg + st * 3 * NV * 32;
-    const float mu = mean[row], rs = invStd[row];
     float4 dy4[NV], xh[NV];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
