@@ -394,14 +394,30 @@ def run_b200(a):
         f = algorithmic_flops(a.config, b.src_mask().sum(axis=1), b.tgt_mask().sum(axis=1))
         for k in flops:
             flops[k] += f[k] / prof_steps
-    tensor_classes = {"gemm_tc", "gemm_fp32", "attention"}
+    tensor_classes = {"gemm_tc", "gemm_fp32", "attention", "rnn_scan", "rnn_scan_bwd"}
+    # the persistent scans report executed FLOPs over the padded b x T grid:
+    # scale them to real tokens (the 8(d) basis) by the batches' fill ratio
+    real = sum(float(b.src_mask().sum() + b.tgt_mask().sum()) for b in prof_batches)
+    padded = sum(float(b.src_mask().size + b.tgt_mask().size) for b in prof_batches)
+    fill = real / padded if padded else 1.0
+
+    scan_flops = sum(v["work"] for k, v in classes.items() if k.startswith("rnn_scan")) * fill
+
+    def class_flops(k):
+        if k.startswith("rnn_scan"):
+            return classes[k]["work"] * fill
+        if k == "attention":
+            return flops["attention"]
+        if scan_flops:  # RNN: the GEMMs do what the scans (incl. their attention) do not
+            return max(flops["total"] - scan_flops, 0.0)
+        return flops["gemm"]
     dom = max(classes, key=lambda k: classes[k]["ms_corr"]) if classes else None
     roof = None
     if dom:
         c = classes[dom]
         tensor = dom in tensor_classes or dom.startswith("gemm")
         if tensor:
-            alg = flops["attention"] if dom == "attention" else flops["gemm"]
+            alg = class_flops(dom)
         else:
             alg = c["work"]
         per_launch_work = alg / max(c["launches"], 1)
@@ -415,7 +431,10 @@ def run_b200(a):
                 "frac_tf32_peak": round(achieved / (peak / 2), 4) if tensor else None,
                 "traffic": traffic, "traffic_source": tsrc,
                 "algorithmic_per_launch": per_launch_work,
-                "algorithmic_basis": "SURVEY 8(d) FLOPs over real (unpadded) tokens of the profiled batches"
+                "algorithmic_basis": ("recurrent/attention products executed in the scan "
+                                      "(rnn_persist.cu scan_flops) x real/padded token fill "
+                                      f"{fill:.3f}" if dom.startswith("rnn_scan") else
+                                      "SURVEY 8(d) FLOPs over real (unpadded) tokens of the profiled batches")
                                      if tensor else "algorithmic bytes per call (DESIGN.md 5)",
                 "launches_per_step": c["launches"],
                 "ms_per_step": round(c["ms_corr"], 3), "ms_per_step_raw": round(c["ms"], 3),
@@ -429,7 +448,7 @@ def run_b200(a):
                  "share": round(v["ms_corr"] / (ms_max / a.steps), 4),
                  "launches_per_step": v["launches"]}
         if tensor and k != "gemm_fp32":
-            alg = flops["attention"] if k == "attention" else flops["gemm"]
+            alg = class_flops(k)
             entry["tflops"] = round(alg / (v["ms_corr"] / 1e3) / 1e12, 2)
             entry["frac_bf16_peak"] = round(alg / (v["ms_corr"] / 1e3) / 1e12 / tflops, 4)
         elif v["work"] > 0:

@@ -1620,6 +1620,26 @@ bool bwd_supported(const mtkc_rnn_scan_args* a) {
 }
 }  // namespace
 
+// Executed tensor-op FLOPs of one scan launch over the padded b x T grid
+// (the roofline basis of bench.py's rnn classes, scaled there to real
+// tokens): recurrent products h*U of every block and direction, plus with
+// attention ctx*W2 (kd x 3d), the query s1*W (d x a) and the score /
+// context contractions (S x a, S x kd per row and step).  The backward
+// computes the same products transposed (input gradients; the weight
+// gradients are hoisted GEMMs) and the attention backward's two
+// contractions again.
+static double scan_flops(const mtkc_rnn_scan_args* a, bool bwd) {
+  const double bt = (double)a->b * (double)a->T, d = (double)a->d;
+  double f = 0.0;
+  for(int q = 0; q < a->ndir; ++q)
+    f += 2.0 * bt * d * 3.0 * d * a->dir[q].nblocks;
+  if(a->has_att) {
+    const double S = (double)a->S, A = (double)a->a, kd = (double)a->kd;
+    f += 2.0 * bt * (kd * 3.0 * d + d * A) + 2.0 * bt * S * (A + kd) * (bwd ? 2.0 : 1.0);
+  }
+  return f;
+}
+
 extern "C" {
 
 int mtkc_rnn_scan_supported(const mtkc_rnn_scan_args* a) { return supported(a) ? 1 : 0; }
@@ -1639,7 +1659,7 @@ int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream) {
   cudaStream_t st = S(stream);
   uint8_t* ws = (uint8_t*)a->workspace;
   const int64_t b = a->b, T = a->T, d = a->d, d3 = 3 * d;
-  ProfScope prof(st, "rnn_scan", 0.0);
+  ProfScope prof(st, "rnn_scan", scan_flops(a, false));
 
   // K-major weight copies (weights are constant within the step)
   TJobs jobs{};
@@ -1769,7 +1789,7 @@ int mtkc_rnn_scan_backward(const mtkc_rnn_scan_args* a, void* stream) {
   cudaStream_t st = S(stream);
   uint8_t* ws = (uint8_t*)a->workspace;
   const int64_t b = a->b, T = a->T, d = a->d, d3 = 3 * d;
-  ProfScope prof(st, "rnn_scan_bwd", 0.0);
+  ProfScope prof(st, "rnn_scan_bwd", scan_flops(a, true));
   // [Uz|Ur|Uh] and [Wz|Wr|Wx] side by side (K-major B operands of the
   // input-gradient products)
   CJobs jobs{};
