@@ -478,12 +478,15 @@ __device__ void gru_row(const KP& p, const mtkc_rnn_dir& D, int k, int64_t t, in
 // position (one warp each, float4 lanes, the position's loads in flight
 // together), masked softmax, context (float4 columns, positions unrolled).
 constexpr int AQ = MAXA / 128;  // float4 groups per lane over the attention width
+constexpr int CU = 12;          // positions per batch of loads in the context sums
+constexpr int BU = 8;           // positions per batch of loads in the attention backward columns
 
 // Team member `m` of `P` (P CTAs per row, P = 1 without teams): scores of
 // the positions j = m, m+P, ... then (P > 1) a team barrier, then the
 // context columns of its 1/P share.
 __device__ void att_row(const KP& p, int64_t t, int64_t r, int m, int P, unsigned& tepoch,
-                        float* sW, float* sE, float* sP) {
+                        float* sW, float* sE, float* sP, int& np_) {
+  mark(p.prof, np_, 8);
   const mtkc_rnn_scan_args& a = p.a;
   const int64_t b = a.b, A = a.a, S = a.S, KD = a.kd, A4 = A / 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -497,6 +500,7 @@ __device__ void att_row(const KP& p, int64_t t, int64_t r, int m, int P, unsigne
       st4(a.wq + tr * A + 4 * c4, v);
   }
   __syncthreads();
+  mark(p.prof, np_, 9);
   const bool ln = a.attLnG != nullptr;
   const int nq = (int)((A4 + 31) / 32);  // groups per lane (<= AQ)
   for(int64_t j = m + (int64_t)warp * P; j < S; j += (int64_t)(RT / 32) * P) {
@@ -581,6 +585,7 @@ __device__ void att_row(const KP& p, int64_t t, int64_t r, int m, int P, unsigne
       sE[j] = __ldcg(p.teamBuf + r * S + j);
   }
   __syncthreads();
+  mark(p.prof, np_, 11);
   if(warp == 0) {  // masked softmax over positions (tensor.cpp:393-440)
     const float* mk = a.attMask ? a.attMask + r * S : nullptr;
     float mx = -INFINITY;
@@ -607,34 +612,29 @@ __device__ void att_row(const KP& p, int64_t t, int64_t r, int m, int P, unsigne
     }
   }
   __syncthreads();
+  mark(p.prof, np_, 12);
   // context: sum over positions in ascending order, 4 positions' loads in
   // flight; this member's share of the columns
   const float* keys = a.keys + r * S * KD;
   const int64_t K4 = KD / 4, kb = K4 * m / P, ke = K4 * (m + 1) / P;
+  // (CU positions' loads in flight per thread: the loop is L2-latency bound)
   for(int64_t k4 = kb + threadIdx.x; k4 < ke; k4 += RT) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    int64_t j = 0;
-    for(; j + 4 <= S; j += 4) {
-      float4 kv[4];
+    for(int64_t j = 0; j < S; j += CU) {
+      float4 kv[CU];
 #pragma unroll
-      for(int u = 0; u < 4; ++u)
-        kv[u] = ld4(keys + (j + u) * KD + 4 * k4);
+      for(int u = 0; u < CU; ++u)
+        kv[u] = j + u < S ? ld4(keys + (j + u) * KD + 4 * k4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for(int u = 0; u < 4; ++u) {
+      for(int u = 0; u < CU; ++u) {
+        if(j + u >= S)
+          break;
         const float w = sP[j + u];
         acc[0] += w * kv[u].x;
         acc[1] += w * kv[u].y;
         acc[2] += w * kv[u].z;
         acc[3] += w * kv[u].w;
       }
-    }
-    for(; j < S; ++j) {
-      const float4 kv = ld4(keys + j * KD + 4 * k4);
-      const float w = sP[j];
-      acc[0] += w * kv.x;
-      acc[1] += w * kv.y;
-      acc[2] += w * kv.z;
-      acc[3] += w * kv.w;
     }
     st4(a.ctx + tr * KD + 4 * k4, acc);
   }
@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(RT, 1)
         grid_bar(ctr, gs, epoch);
         mark(p.prof, npf, 3);
         for(int64_t u = gi; u < b * p.team; u += gs)  // team member u % team of row u / team
-          att_row(p, t, u / p.team, (int)(u % p.team), p.team, tepoch, sW, sE, sP);
+          att_row(p, t, u / p.team, (int)(u % p.team), p.team, tepoch, sW, sE, sP, npf);
         mark(p.prof, npf, 5);
         grid_bar(ctr, gs, epoch);
       }
@@ -1019,7 +1019,8 @@ __device__ void gru_bwd_row(const BKP& p, const mtkc_rnn_dir& D, int dir, int k,
 
 __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int m, int P,
                             unsigned& tepoch, float* sC, float* sE, float* sP, float* sQ,
-                            float* scratch) {
+                            float* scratch, int& np_) {
+  mark(p.prof, np_, 8);
   const mtkc_rnn_scan_args& a = p.a;
   const int64_t b = a.b, T = a.T, A = a.a, S = a.S, KD = a.kd, A4 = A / 4, K4 = KD / 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1035,24 +1036,28 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
       st4(a.dctx + tr * KD + 4 * k4, v);
   }
   __syncthreads();
+  mark(p.prof, np_, 9);
   // d(weights)_j = dctx . keys_j  (bahdanau_dw_kernel; the key gradient
   // sum_t w_tj dctx_t is one batched product after the sweep); positions
   // j = m, m+P, ... of this team member
   for(int64_t j = m + (int64_t)warp * P; j < S; j += (int64_t)(RT / 32) * P) {
     const float* keys = a.keys + (r * S + j) * KD;
     float acc = 0.f;
-    for(int64_t c4 = lane; c4 < K4; c4 += 128) {
-      float4 kv[4], cv[4];
+    // every key load of the lane issued before the sums (K4 <= MAXA / 4):
+    // same (chunk, u) summation order as a 4-wide loop over c4 = lane + 128 i
+    float4 kv[MAXA / 128];
 #pragma unroll
-      for(int u = 0; u < 4; ++u) {
-        const int64_t cc = c4 + 32 * u;
-        kv[u] = cc < K4 ? ld4(keys + 4 * cc) : make_float4(0.f, 0.f, 0.f, 0.f);
-        cv[u] = cc < K4 ? *reinterpret_cast<const float4*>(sC + 4 * cc)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    for(int q = 0; q < MAXA / 128; ++q) {
+      const int64_t cc = lane + 32 * q;
+      kv[q] = cc < K4 ? ld4(keys + 4 * cc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for(int q = 0; q < MAXA / 128; ++q) {
+      const int64_t cc = lane + 32 * q;
+      if(cc < K4) {
+        const float4 cv = *reinterpret_cast<const float4*>(sC + 4 * cc);
+        acc += cv.x * kv[q].x + cv.y * kv[q].y + cv.z * kv[q].z + cv.w * kv[q].w;
       }
-#pragma unroll
-      for(int u = 0; u < 4; ++u)
-        acc += cv[u].x * kv[u].x + cv[u].y * kv[u].y + cv[u].z * kv[u].z + cv[u].w * kv[u].w;
     }
     acc = warp_sum(acc);
     if(lane == 0) {
@@ -1067,6 +1072,7 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
       sE[j] = __ldcg(p.teamBuf + (r * S + j) * 2);
   }
   __syncthreads();
+  mark(p.prof, np_, 11);
   if(warp == 0) {  // softmax backward: de_j = w_j (dw_j - sum_l w_l dw_l)
     float s = 0.f;
     for(int64_t j = lane; j < S; j += 32)
@@ -1077,6 +1083,7 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
       sE[j] = a.attWts[tr * S + j] * (sE[j] - s);
   }
   __syncthreads();
+  mark(p.prof, np_, 12);
   const bool ln = a.attLnG != nullptr;
   if(ln) {  // LN backward row statistics per position (bahdanau_de_kernel)
     for(int64_t j = m + (int64_t)warp * P; j < S; j += (int64_t)(RT / 32) * P) {
@@ -1115,6 +1122,7 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
     }
     __syncthreads();
   }
+  mark(p.prof, np_, 13);
   // per column (bahdanau_cols_kernel): d(uk), d(wq), v / LN partials;
   // four positions' loads in flight
   const bool acc = ii > 0 || a.acc_uk;
@@ -1135,10 +1143,10 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
       set4(gc, ld4(a.attLnG + c));
     float awq[4] = {0.f, 0.f, 0.f, 0.f}, av[4] = {0.f, 0.f, 0.f, 0.f};
     float ag[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
-    for(int64_t j0 = part; j0 < S; j0 += 4 * sp) {
-      float4 tv[4], xv[4], gv[4];
+    for(int64_t j0 = part; j0 < S; j0 += BU * sp) {
+      float4 tv[BU], xv[BU], gv[BU];
 #pragma unroll
-      for(int u = 0; u < 4; ++u) {
+      for(int u = 0; u < BU; ++u) {
         const int64_t j = j0 + u * sp;
         if(j < S) {
           tv[u] = ld4(a.attT + (tr * S + j) * A + c);
@@ -1147,7 +1155,7 @@ __device__ void att_bwd_row(const BKP& p, int64_t ii, int64_t t, int64_t r, int 
         }
       }
 #pragma unroll
-      for(int u = 0; u < 4; ++u) {
+      for(int u = 0; u < BU; ++u) {
         const int64_t j = j0 + u * sp;
         if(j >= S)
           break;
@@ -1328,7 +1336,7 @@ __global__ void __launch_bounds__(RT, 1)
         mark(p.prof, npf, 3);
         for(int64_t u = gi; u < b * p.team; u += gs)
           att_bwd_row(p, ii, t, u / p.team, (int)(u % p.team), p.team, tepoch, sC, sE, sP, sQ,
-                      (float*)sm.sA);
+                      (float*)sm.sA, npf);
         mark(p.prof, npf, 5);
         grid_bar(ctr, gs, epoch);
         Prod Q;
@@ -1758,15 +1766,17 @@ int mtkc_rnn_scan_forward(const mtkc_rnn_scan_args* a, void* stream) {
     std::vector<unsigned long long> h(8192 * 2);
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), profBuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    double sum[8] = {0}, cnt[8] = {0};
+    double sum[16] = {0}, cnt[16] = {0};
     for(int i = 0; i + 1 < 8192 && h[2 * i + 3]; ++i) {
       int k = (int)h[2 * i];
       sum[k] += (double)(h[2 * i + 3] - h[2 * i + 1]);
       cnt[k] += 1;
     }
-    const char* nm[8] = {"prod-hU", "pw", "prod-q", "att", "prod-hU+ctxW", "barrier", "end", "200bars"};
+    const char* nm[16] = {"prod-hU", "pw", "prod-q", "att", "prod-hU+ctxW", "barrier", "end",
+                          "200bars", "att:wq", "att:scores", "-", "att:softmax", "att:context",
+                          "-", "-", "-"};
     fprintf(stderr, "[rnn prof] ndir %d b %lld T %lld:", a->ndir, (long long)b, (long long)T);
-    for(int k = 0; k < 8; ++k)
+    for(int k = 0; k < 16; ++k)
       if(cnt[k] > 0)
         fprintf(stderr, " %s %.0f x %.2f us", nm[k], cnt[k], sum[k] / cnt[k] / 1e3);
     fprintf(stderr, "\n");
@@ -1882,16 +1892,18 @@ int mtkc_rnn_scan_backward(const mtkc_rnn_scan_args* a, void* stream) {
     std::vector<unsigned long long> h(8192 * 2);
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), profBuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    double sum[8] = {0}, cnt[8] = {0};
+    double sum[16] = {0}, cnt[16] = {0};
     for(int i = 0; i + 1 < 8192 && h[2 * i + 3]; ++i) {
       int k = (int)h[2 * i];
       sum[k] += (double)(h[2 * i + 3] - h[2 * i + 1]);
       cnt[k] += 1;
     }
-    const char* nm[8] = {"prodB", "pwB", "prodQ", "attB", "prodB+ctx", "barrier", "end", "-"};
+    const char* nm[16] = {"prodB", "pwB", "prodQ", "attB", "prodB+ctx", "barrier", "end", "-",
+                          "attB:dctx", "attB:dw", "-", "attB:softmax", "attB:lnstats",
+                          "attB:cols", "-", "-"};
     fprintf(stderr, "[rnn prof bwd] ndir %d b %lld T %lld:", a->ndir, (long long)b, (long long)T);
-    for(int k = 0; k < 6; ++k)
-      if(cnt[k] > 0)
+    for(int k = 0; k < 16; ++k)
+      if(cnt[k] > 0 && k != 6)
         fprintf(stderr, " %s %.0f x %.2f us", nm[k], cnt[k], sum[k] / cnt[k] / 1e3);
     fprintf(stderr, "\n");
   }
