@@ -1196,7 +1196,12 @@ bool tc_gemm_group(const mtkc_gemm_args* probs, int nprob, int kconcat, cudaStre
   // (operand traffic dominates); a single short wave (M x 512 x 512) and the
   // small-M weight-gradient products stay single-CTA
   const int64_t tiles1 = cdiv(a.M, BM) * cdiv(a.N, a.N >= 256 ? 256 : 128) * nOut;
-  const bool pair = g_pair_enabled && a.M >= 1024 && (csOp == 0 || g_pair_colsum) &&
+  // (M = 512 with N >= 2048 -- the d x 4d weight gradients: pairs measured
+  // 35.3 -> 33.1 us at K = 6530; M x 512 stays single-CTA)
+  static const int64_t pairMinM =
+      getenv("MTK_GEMM_PAIR_MINM") ? atoll(getenv("MTK_GEMM_PAIR_MINM")) : 1024;
+  const bool pairM = a.M >= pairMinM || (a.M >= 512 && a.N >= 2048);
+  const bool pair = g_pair_enabled && pairM && (csOp == 0 || g_pair_colsum) &&
                     (tiles1 > gemm_sms() || cdiv(a.K, BK) * (kconcat ? nprob : 1) >= 32);
   // scheduling units: CTAs, or CTA pairs
   const int sms = pair ? std::max(1, (g_pair_units ? std::min(g_pair_units, gemm_sms() / 2)
