@@ -77,6 +77,12 @@ int mtkc_free(void* ptr);
 int mtkc_host_alloc_pinned(void** ptr, size_t bytes);
 int mtkc_host_free_pinned(void* ptr);
 int mtkc_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+/* Host -> device copy from page-locked memory (mtkc_host_alloc_pinned) as a
+ * kernel reading the mapped host buffer: stays inside the programmatic-
+ * dependent-launch chain of the stream (Device::upload's staging ring; the
+ * reference has no device, the seam is Tensor's host->device sync,
+ * tensor.h:14-98).  MTK_COPY_ENGINE=1: cudaMemcpyAsync. */
+int mtkc_upload_pinned(void* dst, const void* pinned_src, size_t bytes, void* stream);
 int mtkc_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
 int mtkc_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 int mtkc_memset(void* dst, int value, size_t bytes, void* stream);

@@ -96,15 +96,15 @@ void Device::upload(void* dst, const void* src, size_t bytes) {
   if(!bytes)
     return;
   size_t need = (bytes + 255) & ~(size_t)255;
-  if(need > pinnedBytes_ / 2) {  // oversized: plain (possibly blocking) copy
-    MTKC(mtkc_memcpy_h2d(dst, src, bytes, stream_));
-    return;
-  }
-  if(!pinned_) {
+  if(!pinned_) {  // (allocated before the size test: with no ring every copy was pageable)
     pinnedBytes_ = (size_t)64 << 20;
     void* p = nullptr;
     MTKC(mtkc_host_alloc_pinned(&p, pinnedBytes_));
     pinned_ = (char*)p;
+  }
+  if(need > pinnedBytes_ / 2) {  // oversized: plain (possibly blocking) copy
+    MTKC(mtkc_memcpy_h2d(dst, src, bytes, stream_));
+    return;
   }
   if(head_ + need > pinnedBytes_)
     head_ = 0;
@@ -121,7 +121,7 @@ void Device::upload(void* dst, const void* src, size_t bytes) {
     }
   }
   std::memcpy(pinned_ + b, src, bytes);
-  MTKC(mtkc_memcpy_h2d(dst, pinned_ + b, bytes, stream_));
+  MTKC(mtkc_upload_pinned(dst, pinned_ + b, bytes, stream_));
   void* ev = nullptr;
   if(!eventPool_.empty()) {
     ev = eventPool_.back();

@@ -41,9 +41,40 @@ void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_r
 
 static std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
 
+namespace {
+// dst[i] = src[i]; host (mapped pinned) sources are read into registers
+// before the programmatic-dependency wait, device sources after it
+constexpr int COPY_U = 4;
+template <typename T>
+__global__ void __launch_bounds__(256) copy_kernel(T* dst, const T* src, size_t n, int hostSrc) {
+  if(hostSrc) {
+    const size_t i0 = (size_t)blockIdx.x * 256 * COPY_U + threadIdx.x;
+    T v[COPY_U];
+#pragma unroll
+    for(int u = 0; u < COPY_U; ++u)
+      if(i0 + (size_t)u * 256 < n)
+        v[u] = src[i0 + (size_t)u * 256];
+    MTKC_PDL_ENTRY();
+#pragma unroll
+    for(int u = 0; u < COPY_U; ++u)
+      if(i0 + (size_t)u * 256 < n)
+        dst[i0 + (size_t)u * 256] = v[u];
+    return;
+  }
+  MTKC_PDL_ENTRY();
+  for(size_t i = (size_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (size_t)gridDim.x * 256)
+    dst[i] = src[i];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) fill_kernel(T* dst, size_t n, T v) {
+  MTKC_PDL_ENTRY();
+  for(size_t i = (size_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (size_t)gridDim.x * 256)
+    dst[i] = v;
+}
+
 // MTK_TRACE_BLOCK=<us>: report (with a host backtrace) every runtime call that
 // blocked the host longer than <us> microseconds -- finds hidden syncs.
-namespace {
 double trace_block_us() {
   static double us = [] {
     const char* e = std::getenv("MTK_TRACE_BLOCK");
@@ -238,17 +269,80 @@ int mtkc_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
                      "cudaMemcpyAsync(D2H)");
 }
 
+// Copies and fills as kernels: a copy-engine operation in the stream ends
+// the programmatic-dependent-launch chain (the DMA waits for the previous
+// kernel to drain, the next kernel cannot start before the DMA is done), a
+// few microseconds of idle device per copy; a kernel overlaps its neighbours
+// like every other launch.  MTK_COPY_ENGINE=1 restores cudaMemcpyAsync /
+// cudaMemsetAsync.
+static bool copy_engine() {
+  static const bool e = getenv("MTK_COPY_ENGINE") && getenv("MTK_COPY_ENGINE")[0] == '1';
+  return e;
+}
+
+static int copy_kernel_launch(void* dst, const void* src, size_t bytes, bool hostSrc, cudaStream_t st) {
+  const uintptr_t al = (uintptr_t)dst | (uintptr_t)src | (uintptr_t)bytes;
+  const int vec = (al & 15) == 0 ? 16 : ((al & 3) == 0 ? 4 : 1);
+  const size_t n = bytes / (size_t)vec;
+  // host sources: every element in registers before the wait (one pass)
+  const size_t perCta = 256 * (size_t)COPY_U;
+  const unsigned grid = (unsigned)std::min<size_t>((n + perCta - 1) / perCta,
+                                                   hostSrc ? 65535 : 148 * 8);
+  cudaError_t e;
+  if(vec == 16)
+    e = launch(copy_kernel<uint4>, dim3(grid), dim3(256), 0, st, (uint4*)dst, (const uint4*)src,
+               n, hostSrc ? 1 : 0);
+  else if(vec == 4)
+    e = launch(copy_kernel<uint32_t>, dim3(grid), dim3(256), 0, st, (uint32_t*)dst,
+               (const uint32_t*)src, n, hostSrc ? 1 : 0);
+  else
+    e = launch(copy_kernel<uint8_t>, dim3(grid), dim3(256), 0, st, (uint8_t*)dst,
+               (const uint8_t*)src, n, hostSrc ? 1 : 0);
+  count_launch();
+  return cuda_status(e, "copy_kernel");
+}
+
 int mtkc_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
   if(!bytes)
     return MTKC_OK;
-  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, S(stream)),
-                     "cudaMemcpyAsync(D2D)");
+  if(copy_engine())
+    return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, S(stream)),
+                       "cudaMemcpyAsync(D2D)");
+  return copy_kernel_launch(dst, src, bytes, false, S(stream));
+}
+
+int mtkc_upload_pinned(void* dst, const void* pinned_src, size_t bytes, void* stream) {
+  if(!bytes)
+    return MTKC_OK;
+  g_h2d.fetch_add(bytes, std::memory_order_relaxed);
+  if(copy_engine() || bytes > ((size_t)64 << 20))
+    return cuda_status(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, S(stream)),
+                       "cudaMemcpyAsync(H2D)");
+  return copy_kernel_launch(dst, pinned_src, bytes, true, S(stream));
 }
 
 int mtkc_memset(void* dst, int value, size_t bytes, void* stream) {
   if(!bytes)
     return MTKC_OK;
-  return cuda_status(cudaMemsetAsync(dst, value, bytes, S(stream)), "cudaMemsetAsync");
+  if(copy_engine())
+    return cuda_status(cudaMemsetAsync(dst, value, bytes, S(stream)), "cudaMemsetAsync");
+  const uint32_t b = (uint32_t)value & 0xffu;
+  const uint32_t w = b | (b << 8) | (b << 16) | (b << 24);
+  const uintptr_t al = (uintptr_t)dst | (uintptr_t)bytes;
+  const int vec = (al & 15) == 0 ? 16 : ((al & 3) == 0 ? 4 : 1);
+  const size_t n = bytes / (size_t)vec;
+  const unsigned grid = (unsigned)std::min<size_t>((n + 256 * 4 - 1) / (256 * 4), 148 * 8);
+  cudaError_t e;
+  if(vec == 16)
+    e = launch(fill_kernel<uint4>, dim3(grid), dim3(256), 0, S(stream), (uint4*)dst, n,
+               make_uint4(w, w, w, w));
+  else if(vec == 4)
+    e = launch(fill_kernel<uint32_t>, dim3(grid), dim3(256), 0, S(stream), (uint32_t*)dst, n, w);
+  else
+    e = launch(fill_kernel<uint8_t>, dim3(grid), dim3(256), 0, S(stream), (uint8_t*)dst, n,
+               (uint8_t)b);
+  count_launch();
+  return cuda_status(e, "fill_kernel");
 }
 
 int mtkc_stream_create(void** stream) {
