@@ -264,6 +264,25 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
 int mtkc_colsum_group(float* const* outs, const float* const* ins, const int* accumulate, int n,
                       int64_t rows, int64_t cols, float* workspace, size_t workspace_bytes,
                       void* stream);
+/* Up to MTKC_COLSUM_MAX_JOBS column sums over the same `rows` in one
+ * launch (the reference's per-parameter bias / layer-norm gain gradients,
+ * graph.cpp:771, 801 and tensor.cpp:545-599, as the RNN scans' hoisted
+ * sums): job z sums columns [0, cols) of in [rows x ld]; column c goes to
+ * out[c / seg][c % seg] (accumulated when acc[c / seg]), dropped when that
+ * out is NULL.  Sums are bit-identical to mtkc_colsum per job.  cols, ld,
+ * seg multiples of 4, in 16-byte aligned; workspace >= ceil(rows/64) *
+ * sum(cols) floats. */
+#define MTKC_COLSUM_MAX_JOBS 4
+#define MTKC_COLSUM_MAX_SEGS 6
+typedef struct {
+  const float* in;
+  int64_t ld, cols, seg;
+  int nseg;
+  float* out[MTKC_COLSUM_MAX_SEGS];
+  int acc[MTKC_COLSUM_MAX_SEGS];
+} mtkc_colsum_job;
+int mtkc_colsum_multi(const mtkc_colsum_job* jobs, int n, int64_t rows, float* workspace,
+                      size_t workspace_bytes, void* stream);
 /* flags |= MTKC_FLAG_NONFINITE if any in[i] is not finite (allFinite) */
 int mtkc_check_finite(const float* in, int64_t n, int* flags, void* stream);
 /* *dst |= *src on the device (stream-ordered): the step's device error bits

@@ -706,26 +706,42 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
       }
       gemm3(c, false, d, d, TB, As, d, true, dp, ld, false, C, d, beta);
     }
-    if(!inter) {  // biases (graph.cpp:771, 801): one grouped column sum
-      ExpressionGraph::GradDst gz = g.gradDst(n.inputs[(size_t)Bk.b[0]]),
-                               gr = g.gradDst(n.inputs[(size_t)Bk.b[1]]),
-                               gb = g.gradDst(n.inputs[(size_t)Bk.b[2]]);
-      float* outs[3] = {gz.ptr, gr.ptr, gb.ptr};
-      const float* ins[3] = {q.dpz.devc(), q.dpr.devc(), q.dac.devc()};
-      const int acc[3] = {gz.accumulate, gr.accumulate, gb.accumulate};
-      MTKC(mtkc_colsum_group(outs, ins, acc, 3, TB, d, c.cs, c.csBytes, c.st));
-    } else {  // sum over the [dpz|dpr|duh] rows, then bz, br slices; bh from dac
-      Tensor sums = g.allocTensor(Shape({3 * d}));
-      colsum(c, ExpressionGraph::GradDst{sums.dev(), 0, nullptr, nullptr}, dGk, TB, 3 * d);
-      for(int j = 0; j < 2; ++j) {
-        auto dst = g.gradDst(n.inputs[(size_t)Bk.b[j]]);
-        if(dst.accumulate)
-          MTKC(mtkc_axpy(dst.ptr, sums.devc() + j * d, 1.f, d, c.st));
-        else
-          MTKC(mtkc_memcpy_d2d(dst.ptr, sums.devc() + j * d, (size_t)d * sizeof(float), c.st));
-      }
-      colsum(c, g.gradDst(n.inputs[(size_t)Bk.b[2]]), q.dac.devc(), TB, d);
+    // biases (graph.cpp:771, 801) and the per-gate LN gains/biases: one
+    // launch of column sums straight into the gradient slots (bz, br from
+    // the dpz | dpr columns, bh from dac; LN from the lnp partials)
+    mtkc_colsum_job jobs[MTKC_COLSUM_MAX_JOBS];
+    int nj = 0;
+    auto job = [&](const float* in, int64_t ldIn, int64_t cols) -> mtkc_colsum_job& {
+      mtkc_colsum_job& J = jobs[nj++];
+      J = mtkc_colsum_job{};
+      J.in = in;
+      J.ld = ldIn;
+      J.cols = cols;
+      J.seg = d;
+      J.nseg = (int)(cols / d);
+      return J;
+    };
+    auto slot = [&](mtkc_colsum_job& J, int s, int paramSlot) {
+      auto dst = g.gradDst(n.inputs[(size_t)paramSlot]);
+      J.out[s] = dst.ptr;
+      J.acc[s] = dst.accumulate;
+    };
+    if(!inter) {
+      slot(job(q.dpz.devc(), d, d), 0, Bk.b[0]);
+      slot(job(q.dpr.devc(), d, d), 0, Bk.b[1]);
+    } else {
+      mtkc_colsum_job& J = job(dGk, 3 * d, 2 * d);  // dpz | dpr columns of [dpz|dpr|duh]
+      slot(J, 0, Bk.b[0]);
+      slot(J, 1, Bk.b[1]);
     }
+    slot(job(q.dac.devc(), d, d), 0, Bk.b[2]);
+    if(X.ln) {  // per-gate LN gain/bias partials [TB x 6d]
+      const int nln = Bk.in > 0 ? 6 : 4;
+      mtkc_colsum_job& J = job(q.lnp.devc(), 6 * d, (int64_t)nln * d);
+      for(int j = 0; j < nln; ++j)
+        slot(J, j, Bk.ln[j]);
+    }
+    MTKC(mtkc_colsum_multi(jobs, nj, TB, c.cs, c.csBytes, c.st));
     const float* dGxk = inter && !q.dGx.empty() ? q.dGx.devc() : nullptr;
     const float* dx[3] = {inter ? dGxk : q.dpz.devc(), inter ? dGxk + d : q.dpr.devc(),
                           inter ? dGxk + 2 * d : q.dax.devc()};
@@ -755,19 +771,6 @@ void backwardEnd(ExpressionGraph& g, ExpressionGraph::Node& n, ScanAux& X, Dir& 
         float* C1[1] = {dXt};
         const float b1[1] = {accX ? 1.f : 0.f};
         gemm3(c, true, TB, X.e, d, dx, ld, false, Bw, d, true, C1, X.e, b1);
-      }
-    }
-    if(X.ln) {  // per-gate LN gain/bias: one column sum over b*T rows, then slices
-      const int nln = Bk.in > 0 ? 6 : 4;
-      Tensor sums = g.allocTensor(Shape({6 * d}));
-      colsum(c, ExpressionGraph::GradDst{sums.dev(), 0, nullptr, nullptr}, q.lnp.devc(), TB,
-             6 * d);
-      for(int j = 0; j < nln; ++j) {
-        auto dst = g.gradDst(n.inputs[(size_t)Bk.ln[j]]);
-        if(dst.accumulate)
-          MTKC(mtkc_axpy(dst.ptr, sums.devc() + j * d, 1.f, d, c.st));
-        else
-          MTKC(mtkc_memcpy_d2d(dst.ptr, sums.devc() + j * d, (size_t)d * sizeof(float), c.st));
       }
     }
   }

@@ -181,6 +181,121 @@ __global__ void __launch_bounds__(256) colsum_onepass_kernel(ColsumGroup grp, fl
   }
 }
 
+// Several column sums over the same rows in one launch (the per-block bias
+// and layer-norm gradient sums of the RNN scans): job z sums columns
+// [0, cols) of a [rows x ld] matrix, stage 1 and the last-CTA slab finish
+// exactly as colsum_onepass_kernel (same row blocks, same fixed order: the
+// sums are bit-identical to one mtkc_colsum per job), and column c lands in
+// segment c / seg: out[s][c % seg] (= or +=), or nowhere when out[s] is NULL.
+struct ColsumMulti {
+  mtkc_colsum_job j[MTKC_COLSUM_MAX_JOBS];
+  int n;
+  int slab0[MTKC_COLSUM_MAX_JOBS + 1];  // first global slab of each job
+  int64_t part0[MTKC_COLSUM_MAX_JOBS];  // partial-row offset (floats) of each job
+};
+
+__global__ void __launch_bounds__(256) colsum_multi_kernel(const __grid_constant__ ColsumMulti m,
+                                                           float* part, int64_t rows) {
+  MTKC_PDL_ENTRY();
+  int z = 0;
+  while(z + 1 < m.n && (int)blockIdx.x >= m.slab0[z + 1])
+    ++z;
+  const mtkc_colsum_job& J = m.j[z];
+  const int64_t cols = J.cols, ld = J.ld;
+  part += m.part0[z];
+  const int slab = (int)blockIdx.x - m.slab0[z];
+  __shared__ float4 red[8][32];
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)slab * CR_COLS + lane * 4;
+  const int64_t r0 = (int64_t)blockIdx.y * CR_ROWS + w;
+  const int64_t nblk = gridDim.y;
+  float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if(c < cols) {
+    float4 xa[CR_RPW];
+#pragma unroll
+    for(int i = 0; i < CR_RPW; ++i) {
+      const int64_t r = r0 + 8 * i;
+      xa[i] = r < rows ? __ldg(reinterpret_cast<const float4*>(J.in + r * ld + c))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for(int i = 0; i < CR_RPW; ++i)
+      f4add(s0, xa[i]);
+  }
+  red[w][lane] = s0;
+  __syncthreads();
+  if(w == 0) {
+    if(c < cols) {
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for(int k = 0; k < 8; ++k)
+        f4add(t, red[k][lane]);
+      *reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * cols + c) = t;
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  if(threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&g_colsum_ticket[blockIdx.x], 1u);
+    last = prev == (unsigned)(nblk - 1);
+  }
+  __syncthreads();
+  if(!last)
+    return;
+  __threadfence();
+  float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+  if(c < cols)
+    for(int64_t rb = w; rb < nblk; rb += 64) {
+      float4 v[8];
+#pragma unroll
+      for(int u = 0; u < 8; ++u)
+        v[u] = rb + 8 * u < nblk
+                   ? __ldcg(reinterpret_cast<const float4*>(part + (rb + 8 * u) * cols + c))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for(int u = 0; u < 8; ++u)
+        f4add(t, v[u]);
+    }
+  red[w][lane] = t;
+  __syncthreads();
+  if(w == 0) {
+    if(c < cols) {
+      float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for(int k = 0; k < 8; ++k)
+        f4add(u, red[k][lane]);
+      const int sg = (int)(c / J.seg);  // seg % 4 == 0: the 4 columns share a segment
+      float* o = J.out[sg];
+      if(o) {
+        o += c - (int64_t)sg * J.seg;
+        const float uu[4] = {u.x, u.y, u.z, u.w};
+        for(int e = 0; e < 4; ++e)
+          o[e] = J.acc[sg] ? o[e] + uu[e] : uu[e];
+      }
+    }
+    if(lane == 0)
+      g_colsum_ticket[blockIdx.x] = 0u;
+  }
+}
+
+__global__ void colsum_multi_direct_kernel(const __grid_constant__ ColsumMulti m, int64_t rows) {
+  MTKC_PDL_ENTRY();
+  const mtkc_colsum_job& J = m.j[blockIdx.y];
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if(c >= J.cols)
+    return;
+  float s = 0.f;
+  for(int64_t r = 0; r < rows; ++r)
+    s += J.in[r * J.ld + c];
+  const int sg = (int)(c / J.seg);
+  float* o = J.out[sg];
+  if(o) {
+    o += c - (int64_t)sg * J.seg;
+    *o = J.acc[sg] ? *o + s : s;
+  }
+}
+
 __global__ void finite_kernel(const float* in, int64_t n, int* flags) {
   MTKC_PDL_ENTRY();
   bool bad = false;
@@ -266,6 +381,54 @@ int mtkc_colsum(float* out, const float* in, int64_t rows, int64_t cols, int acc
   ::mtkc::launch(colred_final_kernel<1>, colred_final_grid(cols), 256, 0, S(stream), 
       out, nullptr, workspace, nblk, cols, accumulate);
   MTKC_POST_LAUNCH("colred_final_kernel");
+  return MTKC_OK;
+}
+
+int mtkc_colsum_multi(const mtkc_colsum_job* jobs, int n, int64_t rows, float* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if(n <= 0 || rows <= 0)
+    return MTKC_OK;
+  if(n > MTKC_COLSUM_MAX_JOBS)
+    return fail(MTKC_CONTRACT, "mtkc_colsum_multi: too many jobs");
+  ColsumMulti m{};
+  m.n = n;
+  const int64_t nblk = cdiv(rows, CR_ROWS);
+  int64_t slabs = 0, partFloats = 0;
+  double bytes = 0;
+  bool ok = rows > 8 && nblk <= 65535 && workspace && (uintptr_t)workspace % 16 == 0;
+  for(int z = 0; z < n && ok; ++z) {
+    const mtkc_colsum_job& J = jobs[z];
+    ok = J.cols > 0 && J.cols % 4 == 0 && J.ld % 4 == 0 && J.ld >= J.cols && J.seg > 0 &&
+         J.seg % 4 == 0 && J.nseg >= (int)cdiv(J.cols, J.seg) && J.nseg <= MTKC_COLSUM_MAX_SEGS &&
+         (uintptr_t)J.in % 16 == 0;
+    m.j[z] = J;
+    m.slab0[z] = (int)slabs;
+    m.part0[z] = partFloats;
+    slabs += cdiv(J.cols, CR_COLS);
+    partFloats += nblk * J.cols;
+    bytes += 4.0 * rows * J.cols;
+  }
+  m.slab0[n] = (int)slabs;
+  ok = ok && slabs <= CS_MAX_SLABS && (size_t)partFloats * sizeof(float) <= workspace_bytes;
+  ProfScope prof(S(stream), "colsum", bytes);
+  if(!ok) {  // few rows / odd shapes: one thread per column, rows in order
+    int64_t maxc = 0;
+    for(int z = 0; z < n; ++z) {
+      m.j[z] = jobs[z];
+      if(jobs[z].seg <= 0 || jobs[z].nseg * jobs[z].seg < jobs[z].cols)
+        return fail(MTKC_CONTRACT, "mtkc_colsum_multi: segments do not cover the columns");
+      maxc = std::max(maxc, jobs[z].cols);
+    }
+    ::mtkc::launch(colsum_multi_direct_kernel, dim3((unsigned)cdiv(maxc, 128), (unsigned)n), 128,
+                   0, S(stream), m, rows);
+    MTKC_POST_LAUNCH("colsum_multi_direct_kernel");
+    return MTKC_OK;
+  }
+  if(prof_detail())
+    prof.detail = "multi" + std::to_string(n) + "_r" + std::to_string(rows);
+  ::mtkc::launch(colsum_multi_kernel, dim3((unsigned)slabs, (unsigned)nblk), 256, 0, S(stream), m,
+                 workspace, rows);
+  MTKC_POST_LAUNCH("colsum_multi_kernel");
   return MTKC_OK;
 }
 
