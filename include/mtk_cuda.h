@@ -79,9 +79,9 @@ int mtkc_host_free_pinned(void* ptr);
 int mtkc_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 /* Host -> device copy from page-locked memory (mtkc_host_alloc_pinned) as a
  * kernel reading the mapped host buffer: stays inside the programmatic-
- * dependent-launch chain of the stream (Device::upload's staging ring; the
- * reference has no device, the seam is Tensor's host->device sync,
- * tensor.h:14-98).  MTK_COPY_ENGINE=1: cudaMemcpyAsync. */
+ * dependent-launch chain of the stream (Device::upload's staging ring under
+ * MTK_UPLOAD_RING=1; the reference has no device, the seam is Tensor's
+ * host->device sync, tensor.h:14-98).  MTK_COPY_ENGINE=1: cudaMemcpyAsync. */
 int mtkc_upload_pinned(void* dst, const void* pinned_src, size_t bytes, void* stream);
 int mtkc_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
 int mtkc_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
