@@ -48,7 +48,7 @@ constexpr int RST = 6;         // smem ring stages
 constexpr int NTH = 96;        // n-tile of the gate products (3d is a multiple of 96)
 constexpr uint32_t A_STAGE = 128 * 32 * 4;  // 16 KB: 128 rows x 32 fp32
 constexpr uint32_t B_STAGE = NTH * 32 * 4;  // 12 KB
-constexpr int TMEM_COLS = 128;
+constexpr int TMEM_COLS = 256;  // two 128-column accumulators (units alternate)
 constexpr int MAXA = 2048;  // attention width cap (row-phase smem)
 constexpr int MAXS = 1024;  // source positions cap
 
@@ -188,8 +188,10 @@ __device__ void run_prods(const Prod* P, int np, int gi, int gs, const Smem& sm,
       int q, mt, nt, kc;
       decode(u, q, mt, nt, kc);
       const Prod& pr = P[q];
-      if(ucnt > 0)
-        mbar_wait(&sm.tempty[0], (ucnt - 1) & 1);
+      // accumulator ucnt & 1: wait until the epilogue drained its previous use
+      const int acc = (int)(ucnt & 1);
+      if(ucnt >= 2)
+        mbar_wait(&sm.tempty[acc], ((ucnt >> 1) - 1) & 1);
       tc_fence_after();
       // D=f32, A=B=tf32, both K-major, N>>3, M>>4
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(pr.NT >> 3) << 17) |
@@ -204,14 +206,14 @@ __device__ void run_prods(const Prod* P, int np, int gi, int gs, const Smem& sm,
           const uint32_t bBase = smem_u32(sm.sB + s * B_STAGE);
 #pragma unroll
           for(int kk = 0; kk < 4; ++kk)
-            mma_tf32(sm.tmem, umma_desc(aBase + kk * 32, 16, 1024, 2),
+            mma_tf32(sm.tmem + (uint32_t)acc * 128u, umma_desc(aBase + kk * 32, 16, 1024, 2),
                      umma_desc(bBase + kk * 32, 16, 1024, 2), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
           mma_commit(&sm.empty[s]);
         }
         __syncwarp();
       }
       if(lane == 0)
-        mma_commit(&sm.tfull[0]);
+        mma_commit(&sm.tfull[acc]);
       __syncwarp();
       ++ucnt;
     }
@@ -221,12 +223,13 @@ __device__ void run_prods(const Prod* P, int np, int gi, int gs, const Smem& sm,
       int q, mt, nt, kc;
       decode(u, q, mt, nt, kc);
       const Prod& pr = P[q];
-      mbar_wait(&sm.tfull[0], ucnt & 1);
+      const int acc = (int)(ucnt & 1);
+      mbar_wait(&sm.tfull[acc], (ucnt >> 1) & 1);
       tc_fence_after();
       const int64_t row = (int64_t)mt * 128 + qd * 32 + lane;
       for(int c0 = 0; c0 < pr.NT; c0 += 32) {
         float v[32];
-        tmem_ld32(sm.tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)c0, v);
+        tmem_ld32(sm.tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)acc * 128u + (uint32_t)c0, v);
         if(row < b) {
           float4* dst = reinterpret_cast<float4*>(pr.part + ((int64_t)kc * b + row) * pr.N +
                                                   (int64_t)nt * pr.NT + c0);
@@ -238,7 +241,7 @@ __device__ void run_prods(const Prod* P, int np, int gi, int gs, const Smem& sm,
       tc_fence_before();
       __syncwarp();
       if(lane == 0)
-        mbar_arrive(&sm.tempty[0]);
+        mbar_arrive(&sm.tempty[acc]);
       ++ucnt;
     }
   }
@@ -662,8 +665,8 @@ __global__ void __launch_bounds__(RT, 1)
   sm.full = bars;
   sm.empty = bars + RST;
   sm.tfull = bars + 2 * RST;
-  sm.tempty = bars + 2 * RST + 1;
-  uint32_t* tmemSlot = (uint32_t*)(bars + 2 * RST + 2);
+  sm.tempty = bars + 2 * RST + 2;
+  uint32_t* tmemSlot = (uint32_t*)(bars + 2 * RST + 4);
   const int warp = threadIdx.x >> 5;
   const mtkc_rnn_scan_args& a = p.a;
 
@@ -672,8 +675,10 @@ __global__ void __launch_bounds__(RT, 1)
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], 1);
     }
-    mbar_init(&sm.tfull[0], 1);
-    mbar_init(&sm.tempty[0], 4);
+    for(int i = 0; i < 2; ++i) {
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for(int q = 0; q < a.ndir; ++q) {
@@ -1235,8 +1240,8 @@ __global__ void __launch_bounds__(RT, 1)
   sm.full = bars;
   sm.empty = bars + RST;
   sm.tfull = bars + 2 * RST;
-  sm.tempty = bars + 2 * RST + 1;
-  uint32_t* tmemSlot = (uint32_t*)(bars + 2 * RST + 2);
+  sm.tempty = bars + 2 * RST + 2;
+  uint32_t* tmemSlot = (uint32_t*)(bars + 2 * RST + 4);
   float* sQ = (float*)(tmemSlot + 4);
   const int warp = threadIdx.x >> 5;
   const mtkc_rnn_scan_args& a = p.a;
@@ -1245,8 +1250,10 @@ __global__ void __launch_bounds__(RT, 1)
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], 1);
     }
-    mbar_init(&sm.tfull[0], 1);
-    mbar_init(&sm.tempty[0], 4);
+    for(int i = 0; i < 2; ++i) {
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for(int q = 0; q < a.ndir; ++q) {
