@@ -113,6 +113,54 @@ __global__ void transpose_kernel(TrP p) {
   }
 }
 
+// float4 form when the innermost output dim is contiguous in the source (a
+// permutation of row blocks, e.g. batch-major <-> time-major activations):
+// one index decomposition per 4 elements, 32-bit when the sizes allow
+template <typename I>
+__global__ void transpose4_kernel(TrP p) {
+  MTKC_PDL_ENTRY();
+  const I n4 = (I)(p.n / 4), d3 = (I)(p.od[3] / 4), d2 = (I)p.od[2], d1 = (I)p.od[1];
+  float4* out4 = reinterpret_cast<float4*>(p.out);
+  for(I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < n4; i += (I)gridDim.x * blockDim.x) {
+    I r = i;
+    const I c4 = r % d3;
+    r /= d3;
+    const I i2 = r % d2;
+    r /= d2;
+    const I i1 = r % d1;
+    const I i0 = r / d1;
+    const float4 v = *reinterpret_cast<const float4*>(
+        p.src + (int64_t)i0 * p.ss[0] + (int64_t)i1 * p.ss[1] + (int64_t)i2 * p.ss[2] +
+        4 * (int64_t)c4);
+    if(p.acc) {
+      const float4 o = out4[i];
+      out4[i] = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+    } else {
+      out4[i] = v;
+    }
+  }
+}
+
+template <typename I>
+__global__ void copy_blocks4_kernel(float* dst, int64_t dstStride, int64_t dstOff,
+                                    const float* src, int64_t srcStride, int64_t srcOff,
+                                    int64_t outer, int64_t len, int acc) {
+  MTKC_PDL_ENTRY();
+  const I l4 = (I)(len / 4), n4 = (I)(outer * (len / 4));
+  for(I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < n4; i += (I)gridDim.x * blockDim.x) {
+    const I o = i / l4, j = i - o * l4;
+    const float4 v =
+        *reinterpret_cast<const float4*>(src + (int64_t)o * srcStride + srcOff + 4 * (int64_t)j);
+    float4* d = reinterpret_cast<float4*>(dst + (int64_t)o * dstStride + dstOff + 4 * (int64_t)j);
+    if(acc) {
+      const float4 x = *d;
+      *d = make_float4(x.x + v.x, x.y + v.y, x.z + v.z, x.w + v.w);
+    } else {
+      *d = v;
+    }
+  }
+}
+
 struct CopyJobs {
   mtkc_copy_job j[MTKC_COPY_MAX_JOBS];
   int n;
@@ -369,6 +417,16 @@ int mtkc_transpose(float* out, const float* src, const int64_t sd[4], const int 
   p.acc = accumulate;
   if(p.n <= 0)
     return MTKC_OK;
+  const bool vec = p.ss[3] == 1 && p.od[3] % 4 == 0 && p.ss[0] % 4 == 0 && p.ss[1] % 4 == 0 &&
+                   p.ss[2] % 4 == 0 && (((uintptr_t)out | (uintptr_t)src) & 15) == 0;
+  if(vec) {
+    if(p.n / 4 < ((int64_t)1 << 31))
+      ::mtkc::launch(transpose4_kernel<uint32_t>, grid1d(p.n / 4, 256), 256, 0, S(stream), p);
+    else
+      ::mtkc::launch(transpose4_kernel<int64_t>, grid1d(p.n / 4, 256), 256, 0, S(stream), p);
+    MTKC_POST_LAUNCH("transpose4_kernel");
+    return MTKC_OK;
+  }
   ::mtkc::launch(transpose_kernel, grid1d(p.n, 256), 256, 0, S(stream), p);
   MTKC_POST_LAUNCH("transpose_kernel");
   return MTKC_OK;
@@ -397,6 +455,18 @@ int mtkc_copy_blocks(float* dst, int64_t dst_stride, int64_t dst_off, const floa
                      int accumulate, void* stream) {
   if(outer * len <= 0)
     return MTKC_OK;
+  if(len % 4 == 0 && dst_stride % 4 == 0 && dst_off % 4 == 0 && src_stride % 4 == 0 &&
+     src_off % 4 == 0 && (((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const int64_t n4 = outer * (len / 4);
+    if(n4 < ((int64_t)1 << 31))
+      ::mtkc::launch(copy_blocks4_kernel<uint32_t>, grid1d(n4, 256), 256, 0, S(stream), dst,
+                     dst_stride, dst_off, src, src_stride, src_off, outer, len, accumulate);
+    else
+      ::mtkc::launch(copy_blocks4_kernel<int64_t>, grid1d(n4, 256), 256, 0, S(stream), dst,
+                     dst_stride, dst_off, src, src_stride, src_off, outer, len, accumulate);
+    MTKC_POST_LAUNCH("copy_blocks4_kernel");
+    return MTKC_OK;
+  }
   ::mtkc::launch(copy_blocks_kernel, grid1d(outer * len, 256), 256, 0, S(stream), 
       dst, dst_stride, dst_off, src, src_stride, src_off, outer, len, accumulate);
   MTKC_POST_LAUNCH("copy_blocks_kernel");

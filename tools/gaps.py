@@ -39,7 +39,7 @@ ev = []
 for e in prof.events():
     if "CUDA" not in str(getattr(e, "device_type", "")):
         continue
-    ev.append((e.time_range.start, e.time_range.end, e.name[:70]))
+    ev.append((e.time_range.start, e.time_range.end, e.name[:160]))
 ev.sort()
 ev = [x for x in ev if "sleep" not in x[2]]
 t0, t1 = ev[0][0], max(x[1] for x in ev)
@@ -60,3 +60,16 @@ print(f"{name}: wall {wall/1e3:.3f} ms/update, busy {busy/steps/1e3:.3f} ms, idl
 for k, (c, us) in sorted(gaps.items(), key=lambda kv: -kv[1][1])[:25]:
     print(f"{us/steps:9.1f} us/update {c/steps:6.1f}x  {k[0]} -> {k[1]}")
 print("non-kernel activities:", {k: v for k, v in kinds.items() if "emcpy" in k or "emset" in k})
+# exclusive device time per activity name (each instant to the activity that finishes it)
+per = collections.defaultdict(lambda: [0, 0.0])
+pe = None
+for s_, e_, n in ev:
+    ex = e_ - (s_ if pe is None else max(s_, pe))
+    pe = e_ if pe is None else max(pe, e_)
+    k = n.replace("(anonymous namespace)::", "").replace("mtkc::", "")
+    k = k.split("(")[0].split("<")[0][:60]
+    per[k][0] += 1
+    per[k][1] += max(ex, 0.0)
+print("exclusive time per activity (us/update, launches/update):")
+for k, (c, us) in sorted(per.items(), key=lambda kv: -kv[1][1])[:30]:
+    print(f"{us/steps:9.1f} {c/steps:6.1f}x  {k}")
