@@ -184,9 +184,10 @@ def peaks():
 def traffic_per_call(config, cls, calls_per_step):
     """dram__bytes_read.sum + dram__bytes_write.sum of the class per C-ABI call,
     from the committed ncu capture of one update (tools/traffic.py)."""
-    path = os.path.join(ROOT, "profiles", f"r02b_traffic_{config}.json")
-    if not os.path.exists(path):
-        path = os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")
+    for tag in ("r02c", "r02b", "r01"):
+        path = os.path.join(ROOT, "profiles", f"{tag}_traffic_{config}.json")
+        if os.path.exists(path):
+            break
     try:
         with open(path) as f:
             j = json.load(f)["classes"][cls]
